@@ -1,0 +1,737 @@
+// capi.cpp -- the C ABI (include/ihom_b200.h) over the device hierarchy,
+// homogenizer, design pipeline and the optimisation loop
+// (src/runner.cpp:51-136). Exceptions map to status codes at this boundary.
+#include "../../include/ihom_b200.h"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "density.hpp"
+#include "hierarchy.hpp"
+#include "objective.hpp"
+
+using namespace ihomgpu;
+
+namespace {
+
+thread_local std::string g_err;
+const void* g_bound = nullptr;  // context whose constant tables are resident
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return IHOM_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return IHOM_E_INVALID;
+  } catch (const NumericError& e) {
+    g_err = e.what();
+    return IHOM_E_NUMERIC;
+  } catch (const EvalError& e) {
+    g_err = e.what();
+    return IHOM_E_EVAL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return IHOM_E_CUDA;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return IHOM_E_STATE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return IHOM_E_INTERNAL;
+  }
+}
+
+// Library stream for the context-free design-pipeline entry points.
+cudaStream_t lib_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  static thread_local int dev = -1;
+  int cur = 0;
+  IHOM_CUDA(cudaGetDevice(&cur));
+  if (!s || dev != cur) {
+    IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    dev = cur;
+  }
+  return s;
+}
+
+struct Scratch {  // reduction workspace for context-free calls
+  DevBuf<double> red;
+  DevBuf<int> flag;
+  Workspace ws;
+  Scratch() : red(21 * kReducePartials + 128), flag(1) {
+    ws.partials = red.p;
+    ws.scalar = red.p + 21 * kReducePartials;
+    ws.scalar2 = ws.scalar + 1;
+    ws.scalars = ws.scalar + 8;
+    ws.flag = flag.p;
+  }
+};
+
+Scratch& scratch() {
+  static thread_local std::unique_ptr<Scratch> s;
+  if (!s) s = std::make_unique<Scratch>();
+  return *s;
+}
+
+long long count(const int n[3]) {
+  for (int k = 0; k < 3; ++k)
+    if (n[k] < 1) throw std::invalid_argument("grid resolution must be positive");
+  return (long long)n[0] * n[1] * n[2];
+}
+
+// Stages a host or device input array into device memory.
+struct DevIn {
+  DevBuf<double> own;
+  const double* p = nullptr;
+  DevIn(const double* src, size_t n, int where, cudaStream_t s) {
+    if (where == IHOM_DEVICE) {
+      p = src;
+    } else {
+      own.alloc(n);
+      IHOM_CUDA(cudaMemcpyAsync(own.p, src, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      p = own.p;
+    }
+  }
+};
+
+// Device output: either the caller's device pointer or a staging buffer copied back on finish().
+struct DevOut {
+  DevBuf<double> own;
+  double* p = nullptr;
+  double* dst;
+  size_t n;
+  int where;
+  DevOut(double* d, size_t count, int w) : dst(d), n(count), where(w) {
+    if (w == IHOM_DEVICE) p = d;
+    else {
+      own.alloc(count);
+      p = own.p;
+    }
+  }
+  void finish(cudaStream_t s) {
+    if (where != IHOM_DEVICE) IHOM_CUDA(cudaMemcpyAsync(dst, own.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  }
+};
+
+}  // namespace
+
+struct ihom_ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  int precision = IHOM_MIXED;
+  int n[3] = {0, 0, 0};
+  std::unique_ptr<Homogenizer<float>> hf;
+  std::unique_ptr<Homogenizer<double>> hd;
+  DevBuf<double> stage;  // 3*nv nodal staging
+
+  template <class F>
+  void with(F&& f) {
+    IHOM_CUDA(cudaSetDevice(device));
+    if (g_bound != this) {
+      if (hf) hf->hierarchy().bind_tables();
+      else hd->hierarchy().bind_tables();
+      g_bound = this;
+    }
+    if (hf) f(*hf);
+    else f(*hd);
+  }
+  long long nv() const { return (long long)n[0] * n[1] * n[2]; }
+};
+
+extern "C" {
+
+const char* ihom_last_error(void) { return g_err.c_str(); }
+const char* ihom_version(void) { return "ihom-b200 0.1 (sm_100a)"; }
+
+ihom_ctx* ihom_create(const ihom_desc* d, const ihom_solver_opts* o) {
+  ihom_ctx* ctx = nullptr;
+  const int rc = guarded([&] {
+    if (!d) throw std::invalid_argument("null descriptor");
+    auto c = std::make_unique<ihom_ctx>();
+    c->device = d->device;
+    IHOM_CUDA(cudaSetDevice(c->device));
+    IHOM_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    c->precision = d->precision;
+    for (int k = 0; k < 3; ++k) c->n[k] = d->n[k];
+    Material m{d->youngs, d->poisson};
+    validate_material(m);
+    SolverOptions so;
+    if (o) {
+      so.tol = o->tol;
+      so.max_cycles = o->max_cycles;
+      so.pre_sweeps = o->pre_sweeps;
+      so.post_sweeps = o->post_sweeps;
+      so.mode = o->mode;
+    }
+    if (d->precision == IHOM_ALL_DOUBLE) c->hd = std::make_unique<Homogenizer<double>>(d->n, m, d->penal, so, c->s);
+    else if (d->precision == IHOM_MIXED) c->hf = std::make_unique<Homogenizer<float>>(d->n, m, d->penal, so, c->s);
+    else throw std::invalid_argument("precision must be IHOM_MIXED or IHOM_ALL_DOUBLE");
+    c->stage.alloc(size_t(3 * c->nv()));
+    g_bound = c.get();
+    ctx = c.release();
+  });
+  return rc == IHOM_OK ? ctx : nullptr;
+}
+
+void ihom_destroy(ihom_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->s);
+  if (g_bound == ctx) g_bound = nullptr;
+  cudaStream_t s = ctx->s;
+  delete ctx;
+  cudaStreamDestroy(s);
+}
+
+int ihom_set_solver(ihom_ctx* ctx, const ihom_solver_opts* o) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      SolverOptions& so = h.options();
+      so.tol = o->tol;
+      so.max_cycles = o->max_cycles;
+      so.pre_sweeps = o->pre_sweeps;
+      so.post_sweeps = o->post_sweeps;
+      so.mode = o->mode;
+    });
+  });
+}
+
+int ihom_set_density(ihom_ctx* ctx, const double* rho, int where) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      DevIn in(rho, size_t(ctx->nv()), where, ctx->s);
+      h.set_density(in.p);
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+    });
+  });
+}
+
+int ihom_solve_cell_problems(ihom_ctx* ctx, ihom_cell_stats* st) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      const CellSolveStats s = h.solve_cell_problems();
+      if (st) {
+        st->total_cycles = s.total_cycles;
+        st->worst_residual = s.worst_residual;
+        st->worst_load = s.worst_load;
+        st->converged = s.converged ? 1 : 0;
+      }
+    });
+  });
+}
+
+int ihom_effective_tensor(ihom_ctx* ctx, double C[36]) {
+  return guarded([&] { ctx->with([&](auto& h) { h.effective_tensor(C); }); });
+}
+
+int ihom_tensor_sensitivity(ihom_ctx* ctx, const double seed[36], double* out, int where) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      DevOut o(out, size_t(ctx->nv()), where);
+      h.tensor_sensitivity(seed, o.p);
+      o.finish(ctx->s);
+    });
+  });
+}
+
+int ihom_get_displacement(ihom_ctx* ctx, int load, double* u, int where) {
+  return guarded([&] {
+    if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
+    ctx->with([&](auto& h) {
+      DevOut o(u, size_t(3 * ctx->nv()), where);
+      launch_aos_soa(h.displacement(load), o.p, ctx->nv(), false, ctx->s);
+      o.finish(ctx->s);
+    });
+  });
+}
+
+int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u, int where) {
+  return guarded([&] {
+    if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
+    ctx->with([&](auto& h) {
+      DevIn in(u, size_t(3 * ctx->nv()), where, ctx->s);
+      launch_aos_soa(in.p, h.displacement(load), ctx->nv(), true, ctx->s);
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+    });
+  });
+}
+
+int ihom_num_levels(ihom_ctx* ctx) {
+  int n = 0;
+  if (guarded([&] { ctx->with([&](auto& h) { n = h.hierarchy().num_levels(); }); }) != IHOM_OK) return -1;
+  return n;
+}
+
+int ihom_level_dims(ihom_ctx* ctx, int l, int n[3]) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      if (l < 0 || l >= h.hierarchy().num_levels()) throw std::invalid_argument("level out of range");
+      for (int k = 0; k < 3; ++k) n[k] = h.hierarchy().geo(l).n[k];
+    });
+  });
+}
+
+int ihom_level_field(ihom_ctx* ctx, int l, int which, int write, double* buf) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      auto& H = h.hierarchy();
+      if (l < 0 || l >= H.num_levels()) throw std::invalid_argument("level out of range");
+      double* f = which == 0 ? H.level_u(l) : which == 1 ? H.level_f(l) : H.level_r(l);
+      const long long nv = H.geo(l).nv;
+      if (write) {
+        DevIn in(buf, size_t(3 * nv), IHOM_HOST, ctx->s);
+        launch_aos_soa(in.p, f, nv, true, ctx->s);
+        IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+      } else {
+        DevOut o(buf, size_t(3 * nv), IHOM_HOST);
+        launch_aos_soa(f, o.p, nv, false, ctx->s);
+        o.finish(ctx->s);
+      }
+    });
+  });
+}
+
+int ihom_apply(ihom_ctx* ctx, int l, const double* x, double* y) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      auto& H = h.hierarchy();
+      if (l < 0 || l >= H.num_levels()) throw std::invalid_argument("level out of range");
+      const long long nv = H.geo(l).nv;
+      DevIn in(x, size_t(3 * nv), IHOM_HOST, ctx->s);
+      DevBuf<double> xs(static_cast<size_t>(3 * nv)), ys(static_cast<size_t>(3 * nv));
+      launch_aos_soa(in.p, xs.p, nv, true, ctx->s);
+      H.apply(l, xs.p, ys.p);
+      DevOut o(y, size_t(3 * nv), IHOM_HOST);
+      launch_aos_soa(ys.p, o.p, nv, false, ctx->s);
+      o.finish(ctx->s);
+    });
+  });
+}
+
+int ihom_relax(ihom_ctx* ctx, int l, int sweeps) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      h.hierarchy().relax(l, sweeps);
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+    });
+  });
+}
+
+int ihom_compute_residual(ihom_ctx* ctx, int l) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      h.hierarchy().compute_residual(l);
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+    });
+  });
+}
+
+int ihom_coarsest_solve(ihom_ctx* ctx) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      h.hierarchy().coarsest_solve();
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+    });
+  });
+}
+
+int ihom_v_cycle(ihom_ctx* ctx, double* rel) {
+  return guarded([&] { ctx->with([&](auto& h) { *rel = h.hierarchy().v_cycle(h.options()); }); });
+}
+
+int ihom_solve(ihom_ctx* ctx, const double* f, double* u, ihom_solve_stats* st) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      auto& H = h.hierarchy();
+      const long long nv = H.geo(0).nv;
+      DevIn fin(f, size_t(3 * nv), IHOM_HOST, ctx->s);
+      launch_aos_soa(fin.p, H.level_f(0), nv, true, ctx->s);
+      DevIn uin(u, size_t(3 * nv), IHOM_HOST, ctx->s);
+      DevBuf<double> us(static_cast<size_t>(3 * nv));
+      launch_aos_soa(uin.p, us.p, nv, true, ctx->s);
+      const SolveStats s = H.solve_bound(us.p, h.options());
+      DevOut o(u, size_t(3 * nv), IHOM_HOST);
+      launch_aos_soa(us.p, o.p, nv, false, ctx->s);
+      o.finish(ctx->s);
+      if (st) {
+        st->cycles = s.cycles;
+        st->rel_residual = s.rel_residual;
+        st->converged = s.converged ? 1 : 0;
+      }
+    });
+  });
+}
+
+int ihom_get_stencil(ihom_ctx* ctx, int l, double* out) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      using T = typename std::remove_reference_t<decltype(h.hierarchy())>::value_type;
+      auto& H = h.hierarchy();
+      if (l < 1 || l >= H.num_levels()) throw std::invalid_argument("level has no assembled stencil");
+      const long long nv = H.geo(l).nv;
+      std::vector<T> st(size_t(243 * nv));
+      IHOM_CUDA(cudaMemcpyAsync(st.data(), H.stencil(l), sizeof(T) * st.size(), cudaMemcpyDeviceToHost, ctx->s));
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+      for (long long v = 0; v < nv; ++v)
+        for (int k = 0; k < 243; ++k) out[v * 243 + k] = double(st[size_t(k * nv + v)]);
+    });
+  });
+}
+
+int ihom_get_coeff(ihom_ctx* ctx, double* out) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      using T = typename std::remove_reference_t<decltype(h.hierarchy())>::value_type;
+      std::vector<T> c(size_t(ctx->nv()));
+      IHOM_CUDA(cudaMemcpyAsync(c.data(), h.hierarchy().coeff(), sizeof(T) * c.size(), cudaMemcpyDeviceToHost, ctx->s));
+      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+      for (size_t i = 0; i < c.size(); ++i) out[i] = double(c[i]);
+    });
+  });
+}
+
+int ihom_macro_force(ihom_ctx* ctx, int load, double* f) {
+  return guarded([&] {
+    if (load < 0 || load > 5) throw std::invalid_argument("macro strain index must be in [0, 6)");
+    ctx->with([&](auto& h) {
+      auto& H = h.hierarchy();
+      const long long nv = H.geo(0).nv;
+      DevBuf<double> fs(static_cast<size_t>(3 * nv));
+      launch_macro_force(H.geo(0), H.coeff(), load, fs.p, ctx->s);
+      DevOut o(f, size_t(3 * nv), IHOM_HOST);
+      launch_aos_soa(fs.p, o.p, nv, false, ctx->s);
+      o.finish(ctx->s);
+    });
+  });
+}
+
+double ihom_op_scale(ihom_ctx* ctx) {
+  double v = 0.0;
+  guarded([&] { ctx->with([&](auto& h) { v = h.hierarchy().op_scale(); }); });
+  return v;
+}
+
+long long ihom_kernel_launches(ihom_ctx* ctx) {
+  long long v = 0;
+  guarded([&] { ctx->with([&](auto& h) { v = h.hierarchy().launches(); }); });
+  return v;
+}
+
+int ihom_grid_locs(const int n[3], long long* locs, long long* nbr27) {
+  return guarded([&] {
+    const long long m = count(n);
+    if (m >= (1LL << 31)) throw std::invalid_argument("grid too large");
+    const GridGeo g = make_geo(n[0], n[1], n[2]);
+    cudaStream_t s = lib_stream();
+    DevBuf<long long> d(static_cast<size_t>(m)), d27(nbr27 ? size_t(27 * m) : 0);
+    launch_grid_locs(g, d.p, nbr27 ? d27.p : nullptr, s);
+    IHOM_CUDA(cudaMemcpyAsync(locs, d.p, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+    if (nbr27) IHOM_CUDA(cudaMemcpyAsync(nbr27, d27.p, sizeof(long long) * 27 * m, cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ------------------------------------------------------------------ design pipeline
+int ihom_radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, int where) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevIn in(f, size_t(m), where, s);
+    DevOut o(out, size_t(m), where);
+    radial_filter(n, in.p, radius, kernel, o.p, s);
+    o.finish(s);
+  });
+}
+
+int ihom_density_expr_eval(const int n[3], double radius, int kernel, double exponent, const double* design,
+                           double* phys, double* pre_out, int where) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevIn in(design, size_t(m), where, s);
+    DevOut pre(pre_out, size_t(m), pre_out ? where : IHOM_HOST);
+    if (!pre_out) pre.dst = nullptr;
+    radial_filter(n, in.p, radius >= 1.0 ? radius : 0.0, kernel, pre.p, s);  // src/density.cpp:65-72
+    DevOut o(phys, size_t(m), where);
+    pow_field(pre.p, exponent, m, o.p, s);
+    o.finish(s);
+    if (pre_out) pre.finish(s);
+  });
+}
+
+int ihom_density_expr_backward(const int n[3], double radius, int kernel, double exponent, const double* pre,
+                               const double* g_phys, double* g_design, int where) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevIn p(pre, size_t(m), where, s);
+    DevIn g(g_phys, size_t(m), where, s);
+    DevBuf<double> tmp(static_cast<size_t>(m));
+    pow_backward(p.p, g.p, exponent, m, tmp.p, s);  // src/density.cpp:74-83
+    DevOut o(g_design, size_t(m), where);
+    radial_filter(n, tmp.p, radius >= 1.0 ? radius : 0.0, kernel, o.p, s);
+    o.finish(s);
+  });
+}
+
+int ihom_symmetrize(const int n[3], double* field, int sym, int where) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevOut o(field, size_t(m), where);
+    if (where != IHOM_DEVICE) IHOM_CUDA(cudaMemcpyAsync(o.p, field, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    DevBuf<double> tmp(static_cast<size_t>(m));
+    symmetrize(n, o.p, sym, tmp.p, s);
+    o.finish(s);
+  });
+}
+
+int ihom_field_mean(const double* f, long long m, double* mean, int where) {
+  return guarded([&] {
+    if (m <= 0) {
+      *mean = 0.0;
+      return;
+    }
+    cudaStream_t s = lib_stream();
+    DevIn in(f, size_t(m), where, s);
+    Scratch& sc = scratch();
+    field_sum(in.p, m, sc.ws.partials, sc.ws.scalar, s);
+    double sum = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&sum, sc.ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    *mean = sum / double(m);
+  });
+}
+
+int ihom_oc_update(long long m, const double* rho, const double* sens, const ihom_oc_config* cfg, double* out,
+                   double* lambda, int* ok, int where) {
+  return guarded([&] {
+    if (m <= 0) throw std::invalid_argument("empty density field");
+    cudaStream_t s = lib_stream();
+    DevIn r(rho, size_t(m), where, s);
+    DevIn g(sens, size_t(m), where, s);
+    DevOut o(out, size_t(m), where);
+    OCConfig c;
+    if (cfg) {
+      c.min_density = cfg->min_density;
+      c.step_limit = cfg->step_limit;
+      c.damp = cfg->damp;
+      c.volume = cfg->volume;
+      c.bisect_tol = cfg->bisect_tol;
+    }
+    const OCResult res = oc_update(m, r.p, g.p, c, o.p, scratch().ws, s);
+    o.finish(s);
+    if (lambda) *lambda = res.lambda;
+    if (ok) *ok = res.bisection_ok ? 1 : 0;
+  });
+}
+
+int ihom_sensitivity_filter(const int n[3], const double* sens, const double* rho, double radius, double* out,
+                            int where) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevIn g(sens, size_t(m), where, s);
+    DevIn r(rho, size_t(m), where, s);
+    DevOut o(out, size_t(m), where);
+    sensitivity_filter(n, g.p, r.p, radius, o.p, s);
+    o.finish(s);
+  });
+}
+
+int ihom_init_trig(const int n[3], int basis_n, uint64_t seed, double volume, double sigmoid_k, double* rho,
+                   int* fallback) {
+  return guarded([&] {
+    const long long m = count(n);
+    cudaStream_t s = lib_stream();
+    DevBuf<double> d(static_cast<size_t>(m)), y(static_cast<size_t>(m));
+    const bool fb = init_trig(n, basis_n, seed, volume, sigmoid_k, d.p, y.p, scratch().ws, s);
+    IHOM_CUDA(cudaMemcpyAsync(rho, d.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    if (fallback) *fallback = fb ? 1 : 0;
+  });
+}
+
+int ihom_objective(int obj, double beta, double eta, double tau, double gamma, int iter, const double C[36],
+                   double* value, double grad[36]) {
+  return guarded([&] {
+    Expr e = obj == IHOM_OBJ_BULK    ? bulk_objective()
+             : obj == IHOM_OBJ_SHEAR ? shear_objective()
+             : obj == IHOM_OBJ_NPR_RELAXED ? npr_relaxed(beta, iter)
+             : obj == IHOM_OBJ_NPR_LOG     ? npr_log(eta, tau, gamma)
+                                           : throw std::invalid_argument("unknown objective");
+    *value = e.eval(C);
+    if (grad) e.backward(1.0, C, grad);
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ optimisation loop
+namespace {
+
+Expr make_objective(const ihom_run_config& c, int iter) {  // src/runner.cpp:13-21
+  switch (c.obj) {
+    case IHOM_OBJ_BULK: return bulk_objective();
+    case IHOM_OBJ_SHEAR: return shear_objective();
+    case IHOM_OBJ_NPR_RELAXED: return npr_relaxed(c.beta, iter);
+    case IHOM_OBJ_NPR_LOG: return npr_log(c.eta, c.tau, c.gamma);
+    default: throw std::invalid_argument("unknown objective");
+  }
+}
+
+struct ConvergeChecker {  // inc/oc.hpp:35-61
+  double threshold = 5e-4;
+  int required = 3, hits = 0;
+  double prev = 0.0;
+  bool has_prev = false;
+  bool update(double f) {
+    if (has_prev) {
+      const double rel = std::abs(f - prev) / std::max(std::abs(prev), 1e-12);
+      hits = rel < threshold ? hits + 1 : 0;
+    }
+    prev = f;
+    has_prev = true;
+    return hits >= required;
+  }
+};
+
+template <typename T>
+void run_impl(const ihom_run_config& cfg, const double* init_rho, ihom_iter_record* records, int capacity, int* nrec,
+              double* rho_out, int* flags, ihom_observer obs, void* user) {
+  IHOM_CUDA(cudaSetDevice(cfg.device));
+  if (cfg.reso < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
+  if (!(cfg.vol > 0.0 && cfg.vol <= 1.0)) throw std::invalid_argument("volume fraction out of range");
+  const int n[3] = {cfg.reso, cfg.reso, cfg.reso};
+  const long long m = (long long)cfg.reso * cfg.reso * cfg.reso;
+  cudaStream_t s;
+  IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{s};
+  SolverOptions so;
+  so.tol = cfg.tol;
+  so.max_cycles = cfg.max_cycles;
+  so.mode = cfg.solver_mode;
+  // homogenizer penal = 1: the SIMP power lives in DensityExpr (src/runner.cpp:59-62)
+  Homogenizer<T> hom(n, Material{cfg.youngs, cfg.poisson}, 1.0, so, s);
+  g_bound = nullptr;  // tables now belong to this run
+  Workspace& ws = hom.hierarchy().workspace();
+  DevBuf<double> rho(static_cast<size_t>(m)), next(static_cast<size_t>(m)), pre(static_cast<size_t>(m)), phys(static_cast<size_t>(m)), grad(static_cast<size_t>(m)), tmp(static_cast<size_t>(m)),
+      gd(static_cast<size_t>(m));
+  *flags = 0;
+  if (cfg.init == 0) {  // init_constant (src/density.cpp:261-265)
+    std::vector<double> c(size_t(m), cfg.vol);
+    IHOM_CUDA(cudaMemcpyAsync(rho.p, c.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  } else if (cfg.init == 1) {
+    if (init_trig(n, cfg.basis_n, cfg.seed, cfg.vol, 15.0, rho.p, tmp.p, ws, s)) *flags |= 4;
+  } else {
+    if (!init_rho) throw std::invalid_argument("init from file requires init_rho");
+    IHOM_CUDA(cudaMemcpyAsync(rho.p, init_rho, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    clamp_field(rho.p, m, kRhoMin, 1.0, s);  // src/runner.cpp:38-42
+  }
+  if (cfg.sym != IHOM_SYM_NONE) {
+    symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+    clamp_field(rho.p, m, kRhoMin, 1.0, s);
+  }
+  const bool dfilt = cfg.filter_placement == 0 && cfg.filter_radius >= 1.0;
+  OCConfig oc;
+  oc.volume = cfg.vol;
+  oc.step_limit = cfg.step;
+  oc.damp = cfg.damp;
+  ConvergeChecker conv;
+  std::vector<double> h_prev, h_next;
+  *nrec = 0;
+  auto mean_of = [&](const double* f) {
+    field_sum(f, m, ws.partials, ws.scalar, s);
+    double sum = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    return sum / double(m);
+  };
+  for (int iter = 0; iter < cfg.max_iter; ++iter) {
+    const auto t0 = std::chrono::steady_clock::now();
+    // DensityExpr::eval (src/density.cpp:65-72)
+    radial_filter(n, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s);
+    pow_field(pre.p, cfg.penal, m, phys.p, s);
+    hom.set_density(phys.p);
+    const CellSolveStats st = hom.solve_cell_problems();
+    ihom_iter_record rec{};
+    hom.effective_tensor(rec.C);
+    const Expr objective = make_objective(cfg, iter);
+    const double fval = objective.eval(rec.C);
+    rec.iter = iter;
+    rec.objective = fval;
+    rec.volume = mean_of(rho.p);
+    rec.cycles = st.total_cycles;
+    rec.residual = st.worst_residual;
+    rec.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (*nrec < capacity) records[(*nrec)++] = rec;
+    if (!st.converged) {
+      *flags |= 1;
+      break;
+    }
+    if (conv.update(fval)) {
+      *flags |= 2;
+      break;
+    }
+    if (iter + 1 == cfg.max_iter) break;
+    double seed[36];
+    objective.backward(1.0, rec.C, seed);
+    hom.tensor_sensitivity(seed, grad.p);
+    pow_backward(pre.p, grad.p, cfg.penal, m, tmp.p, s);  // DensityExpr::backward
+    radial_filter(n, tmp.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, gd.p, s);
+    if (cfg.filter_placement == 1 && cfg.filter_radius >= 1.0) {
+      sensitivity_filter(n, gd.p, rho.p, cfg.filter_radius, tmp.p, s);
+      IHOM_CUDA(cudaMemcpyAsync(gd.p, tmp.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    }
+    if (cfg.sym != IHOM_SYM_NONE) symmetrize(n, gd.p, cfg.sym, tmp.p, s);
+    const OCResult res = oc_update(m, rho.p, gd.p, oc, next.p, ws, s);
+    if (!res.bisection_ok) *flags |= 8;
+    std::swap(rho.p, next.p);  // prev now in next.p
+    if (cfg.sym != IHOM_SYM_NONE) {
+      symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+      clamp_field(rho.p, m, kRhoMin, 1.0, s);
+    }
+    if (*nrec > 0) {
+      records[*nrec - 1].lambda = res.lambda;
+      records[*nrec - 1].oc_trials = res.trials;
+    }
+    if (obs) {
+      h_prev.resize(static_cast<size_t>(m));
+      h_next.resize(static_cast<size_t>(m));
+      IHOM_CUDA(cudaMemcpyAsync(h_prev.data(), next.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+      IHOM_CUDA(cudaMemcpyAsync(h_next.data(), rho.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+      IHOM_CUDA(cudaStreamSynchronize(s));
+      if (!obs(iter, h_prev.data(), h_next.data(), &records[*nrec - 1], user)) break;
+    }
+  }
+  if (rho_out) IHOM_CUDA(cudaMemcpyAsync(rho_out, rho.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ihom_run_optimization(const ihom_run_config* cfg, const double* init_rho, ihom_iter_record* records, int capacity,
+                          int* nrec, double* rho_out, int* flags, ihom_observer obs, void* user) {
+  return guarded([&] {
+    if (!cfg) throw std::invalid_argument("null config");
+    if (cfg->precision == IHOM_ALL_DOUBLE)
+      run_impl<double>(*cfg, init_rho, records, capacity, nrec, rho_out, flags, obs, user);
+    else
+      run_impl<float>(*cfg, init_rho, records, capacity, nrec, rho_out, flags, obs, user);
+  });
+}
+
+}  // extern "C"

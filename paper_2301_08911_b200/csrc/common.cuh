@@ -1,0 +1,177 @@
+// common.cuh -- shared device/host definitions for the B200 homogenization path.
+//
+// Layout contract (bit-exact with the reference, inc/grid.hpp:73-78):
+//   * vertex storage is colour-major: 8 parity classes, each a dense
+//     [hz][hy][hx] block of halved coordinates, x fastest;
+//   * nodal fields are SoA f64: comp c of vertex loc at p[c*nv + loc];
+//   * element fields are x-fastest, eidx = x + n0*(y + n1*z);
+//   * coarse stencils are SoA [27*9][nv] in T (f32 mixed / f64 all-double),
+//     entry (n, r, c) of vertex loc at st[(9*n + 3*r + c)*nv + loc]
+//     (n = 27-neighbour index x-fastest, inc/fem.hpp:30-35).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace ihomgpu {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
+#define IHOM_CUDA(call)                                                                         \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      throw ::ihomgpu::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " at " + \
+                                 __FILE__ + ":" + std::to_string(__LINE__));                   \
+  } while (0)
+
+#define IHOM_LAUNCH_CHECK() IHOM_CUDA(cudaGetLastError())
+
+// Geometry of one periodic grid level (inc/grid.hpp:18-56), passed by value.
+struct GridGeo {
+  int n[3];
+  int cd[8][3];        // colour block dims (n_k - o_k + 1) / 2
+  long long base[8];   // colour block base
+  long long size[8];   // colour block size
+  long long nv;        // vertex count == element count
+};
+
+inline GridGeo make_geo(int nx, int ny, int nz) {
+  GridGeo g{};
+  g.n[0] = nx;
+  g.n[1] = ny;
+  g.n[2] = nz;
+  long long b = 0;
+  for (int id = 0; id < 8; ++id) {
+    const int o[3] = {id & 1, (id >> 1) & 1, (id >> 2) & 1};
+    for (int k = 0; k < 3; ++k) g.cd[id][k] = (g.n[k] - o[k] + 1) / 2;
+    g.base[id] = b;
+    g.size[id] = (long long)g.cd[id][0] * g.cd[id][1] * g.cd[id][2];
+    b += g.size[id];
+  }
+  g.nv = b;
+  return g;
+}
+
+__host__ __device__ inline int color_of(int x, int y, int z) { return (x & 1) | ((y & 1) << 1) | ((z & 1) << 2); }
+
+// color_block_location for canonical coordinates (inc/grid.hpp:73-78).
+__host__ __device__ inline unsigned vloc(const GridGeo& g, int x, int y, int z) {
+  const int id = color_of(x, y, z);
+  return (unsigned)(g.base[id] + (x >> 1) + ((long long)(y >> 1) + (long long)(z >> 1) * g.cd[id][1]) * g.cd[id][0]);
+}
+
+// Coordinates of the i-th vertex of colour block `color` (inverse of vloc within a block).
+__host__ __device__ inline void block_coords(const GridGeo& g, int color, unsigned i, int& x, int& y, int& z) {
+  const unsigned d0 = (unsigned)g.cd[color][0], d1 = (unsigned)g.cd[color][1];
+  const unsigned hx = i % d0;
+  const unsigned t = i / d0;
+  const unsigned hy = t % d1, hz = t / d1;
+  x = 2 * (int)hx + (color & 1);
+  y = 2 * (int)hy + ((color >> 1) & 1);
+  z = 2 * (int)hz + ((color >> 2) & 1);
+}
+
+// Colour of location loc (inc/grid.hpp:81-92 colour search).
+__host__ __device__ inline int color_at(const GridGeo& g, long long loc) {
+  int id = 7;
+  while (id > 0 && loc < g.base[id]) --id;
+  return id;
+}
+
+__host__ __device__ inline unsigned eidx(const GridGeo& g, int x, int y, int z) {
+  return (unsigned)(x + (long long)g.n[0] * (y + (long long)g.n[1] * z));
+}
+
+// gather_neighborhood (src/fem.cpp:37-68): 27 neighbour locations (x fastest,
+// 13 = self) and the 8 incident element indices (v - 1 + bits(ke)).
+struct Nbhd {
+  unsigned v[27];
+  unsigned e[8];
+};
+
+__device__ __forceinline__ void gather27(const GridGeo& g, int x, int y, int z, Nbhd& nb) {
+  int par[3][3], half[3][3], ec[3][2];
+  const int c[3] = {x, y, z};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int n = g.n[k], v = c[k];
+    const int vm = (v == 0) ? n - 1 : v - 1;
+    const int vp = (v + 1 == n) ? 0 : v + 1;
+    par[k][0] = vm & 1;
+    par[k][1] = v & 1;
+    par[k][2] = vp & 1;
+    half[k][0] = vm >> 1;
+    half[k][1] = v >> 1;
+    half[k][2] = vp >> 1;
+    ec[k][0] = vm;
+    ec[k][1] = v;
+  }
+#pragma unroll
+  for (int t2 = 0; t2 < 3; ++t2)
+#pragma unroll
+    for (int t1 = 0; t1 < 3; ++t1)
+#pragma unroll
+      for (int t0 = 0; t0 < 3; ++t0) {
+        const int id = par[0][t0] | (par[1][t1] << 1) | (par[2][t2] << 2);
+        nb.v[t0 + 3 * t1 + 9 * t2] =
+            (unsigned)(g.base[id] + half[0][t0] + (long long)(half[1][t1] + half[2][t2] * g.cd[id][1]) * g.cd[id][0]);
+      }
+#pragma unroll
+  for (int ke = 0; ke < 8; ++ke)
+    nb.e[ke] = (unsigned)(ec[0][ke & 1] + g.n[0] * (ec[1][(ke >> 1) & 1] + g.n[1] * ec[2][(ke >> 2) & 1]));
+}
+
+// 27-neighbour index of pair (ke, j): offset de + dj - 1 (src/fem.cpp:18-21).
+__host__ __device__ constexpr int pair_ngb(int ke, int j) {
+  return ((ke & 1) + (j & 1)) + 3 * (((ke >> 1) & 1) + ((j >> 1) & 1)) + 9 * (((ke >> 2) & 1) + ((j >> 2) & 1));
+}
+
+// Partial-pivoting 3x3 solve, src/fem.cpp:72-94.
+__device__ __forceinline__ void solve3(const double m[9], const double rhs[3], double out[3]) {
+  double a[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) a[i] = m[i];
+  double b[3] = {rhs[0], rhs[1], rhs[2]};
+  int piv[3] = {0, 1, 2};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    int best = c;
+#pragma unroll
+    for (int r = c + 1; r < 3; ++r)
+      if (fabs(a[3 * piv[r] + c]) > fabs(a[3 * piv[best] + c])) best = r;
+    const int tmp = piv[c];
+    piv[c] = piv[best];
+    piv[best] = tmp;
+    const double d = a[3 * piv[c] + c];
+#pragma unroll
+    for (int r = c + 1; r < 3; ++r) {
+      const double fac = a[3 * piv[r] + c] / d;
+#pragma unroll
+      for (int cc = c; cc < 3; ++cc) a[3 * piv[r] + cc] -= fac * a[3 * piv[c] + cc];
+      b[piv[r]] -= fac * b[piv[c]];
+    }
+  }
+#pragma unroll
+  for (int c = 2; c >= 0; --c) {
+    double s = b[piv[c]];
+#pragma unroll
+    for (int cc = c + 1; cc < 3; ++cc) s -= a[3 * piv[c] + cc] * out[cc];
+    out[c] = s / a[3 * piv[c] + c];
+  }
+}
+
+inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace ihomgpu

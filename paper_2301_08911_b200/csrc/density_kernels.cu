@@ -1,0 +1,538 @@
+// density_kernels.cu -- design-side kernels of the iteration:
+//   radial_filter / DensityExpr eval+backward  (src/density.cpp:23-83)
+//   symmetrize                                 (src/density.cpp:100-150)
+//   OC trial / bisection reductions            (src/oc.cpp:14-77)
+//   sensitivity_filter                         (src/oc.cpp:79-111)
+//   clamp_bounds, field_mean                   (src/runner.cpp:47-49, src/density.cpp:11-14)
+// Element fields are f64, x-fastest.
+#include "density.hpp"
+#include "kernels.hpp"
+
+#include <cmath>
+#include <vector>
+
+namespace ihomgpu {
+
+constexpr int kMaxTaps = 343;  // radius < 4
+__constant__ int c_tap_d[kMaxTaps][3];
+__constant__ double c_tap_w[kMaxTaps];
+constexpr int kMaxOps = 48;
+__constant__ int c_sym_perm[kMaxOps][3];
+__constant__ int c_sym_flip[kMaxOps][3];
+
+// kernel_taps (src/density.cpp:23-45): kernel 0 = linear, 1 = spline4; normalised.
+// sensitivity_filter taps (src/oc.cpp:85-96): linear cone, NOT normalised (wsum returned).
+static std::vector<Tap> make_taps(double radius, int kernel, bool normalise, double* wsum) {
+  std::vector<Tap> taps;
+  const int r = int(std::floor(radius));
+  for (int dz = -r; dz <= r; ++dz)
+    for (int dy = -r; dy <= r; ++dy)
+      for (int dx = -r; dx <= r; ++dx) {
+        const double dist = std::sqrt(double(dx * dx + dy * dy + dz * dz));
+        double w;
+        if (normalise) {
+          if (dist > radius) continue;
+          if (kernel == 0) {
+            w = radius - dist;
+          } else {
+            const double q = 1.0 - (dist / radius) * (dist / radius);
+            w = q * q;
+          }
+        } else {
+          w = radius - dist;
+        }
+        if (w > 0.0) taps.push_back({{dx, dy, dz}, w});
+      }
+  double total = 0.0;
+  for (const auto& t : taps) total += t.w;
+  if (normalise)
+    for (auto& t : taps) t.w /= total;
+  if (wsum) *wsum = total;
+  if ((int)taps.size() > kMaxTaps) throw std::invalid_argument("filter radius too large (max 3.99)");
+  return taps;
+}
+
+static void upload_taps(const std::vector<Tap>& taps, cudaStream_t s) {
+  static int d[kMaxTaps][3];
+  static double w[kMaxTaps];
+  for (size_t i = 0; i < taps.size(); ++i) {
+    for (int k = 0; k < 3; ++k) d[i][k] = taps[i].d[k];
+    w[i] = taps[i].w;
+  }
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_tap_d, d, sizeof(int) * 3 * taps.size(), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_tap_w, w, sizeof(double) * taps.size(), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+}
+
+__device__ __forceinline__ int wrapd(int c, int n) {
+  c %= n;
+  return c < 0 ? c + n : c;
+}
+
+// mode 0: out = conv(f); mode 1: out = conv(rho*f) / (max(rho,rmin)*wsum)  (sensitivity filter)
+__global__ void filter_kernel(int nx, int ny, int nz, int ntaps, const double* __restrict__ f,
+                              const double* __restrict__ rho, double wsum, int mode, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long m = (long long)nx * ny * nz;
+  if (i >= m) return;
+  const int x = int(i % nx);
+  const long long r = i / nx;
+  const int y = int(r % ny), z = int(r / ny);
+  double s = 0.0;
+  for (int t = 0; t < ntaps; ++t) {
+    const long long k = wrapd(x + c_tap_d[t][0], nx) +
+                        (long long)nx * (wrapd(y + c_tap_d[t][1], ny) + (long long)ny * wrapd(z + c_tap_d[t][2], nz));
+    s += mode == 0 ? c_tap_w[t] * f[k] : c_tap_w[t] * rho[k] * f[k];
+  }
+  out[i] = mode == 0 ? s : s / (fmax(rho[i], kRhoMin) * wsum);
+}
+
+void radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, cudaStream_t s) {
+  const long long m = (long long)n[0] * n[1] * n[2];
+  if (radius < 1.0) {
+    IHOM_CUDA(cudaMemcpyAsync(out, f, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  const auto taps = make_taps(radius, kernel, true, nullptr);
+  upload_taps(taps, s);
+  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), f, nullptr, 1.0, 0, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+void sensitivity_filter(const int n[3], const double* sens, const double* rho, double radius, double* out,
+                        cudaStream_t s) {
+  const long long m = (long long)n[0] * n[1] * n[2];
+  if (radius < 1.0) {
+    IHOM_CUDA(cudaMemcpyAsync(out, sens, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  double wsum = 0.0;
+  const auto taps = make_taps(radius, 0, false, &wsum);
+  upload_taps(taps, s);
+  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), sens, rho, wsum, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+// out = x^p  /  out = g * p * x^(p-1)
+__global__ void pow_kernel(const double* __restrict__ x, const double* __restrict__ g, double p, long long m,
+                           double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  out[i] = g ? g[i] * p * pow(x[i], p - 1.0) : pow(x[i], p);
+}
+
+void pow_field(const double* x, double p, long long m, double* out, cudaStream_t s) {
+  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, nullptr, p, m, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+void pow_backward(const double* x, const double* g, double p, long long m, double* out, cudaStream_t s) {
+  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, g, p, m, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- symmetrize
+static int symmetry_group(int sym, int perm[kMaxOps][3], int flip[kMaxOps][3]) {
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  int k = 0;
+  auto push = [&](const int* p, int m) {
+    for (int a = 0; a < 3; ++a) {
+      perm[k][a] = p[a];
+      flip[k][a] = (m >> a) & 1;
+    }
+    ++k;
+  };
+  auto sign = [](const int* p) {
+    int s = 1;
+    for (int i = 0; i < 3; ++i)
+      for (int j = i + 1; j < 3; ++j)
+        if (p[i] > p[j]) s = -s;
+    return s;
+  };
+  switch (sym) {  // src/density.cpp:100-127
+    case 1:
+      for (int m = 0; m < 8; ++m) push(perms[0], m);
+      break;
+    case 2:
+      for (const auto& p : perms)
+        for (int m = 0; m < 8; ++m) push(p, m);
+      break;
+    case 3:
+      for (const auto& p : perms)
+        for (int m = 0; m < 8; ++m) {
+          const int nflip = (m & 1) + ((m >> 1) & 1) + ((m >> 2) & 1);
+          if (sign(p) * ((nflip % 2) ? -1 : 1) == 1) push(p, m);
+        }
+      break;
+    default:
+      throw std::invalid_argument("unknown symmetry");
+  }
+  return k;
+}
+
+__global__ void symmetrize_kernel(int nx, int ny, int nz, int nops, const double* __restrict__ in,
+                                  double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long m = (long long)nx * ny * nz;
+  if (i >= m) return;
+  const int n[3] = {nx, ny, nz};
+  int e[3];
+  e[0] = int(i % nx);
+  const long long r = i / nx;
+  e[1] = int(r % ny);
+  e[2] = int(r / ny);
+  double s = 0.0;
+  for (int o = 0; o < nops; ++o) {
+    int q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      q[k] = e[c_sym_perm[o][k]];
+      if (c_sym_flip[o][k]) q[k] = n[k] - 1 - q[k];
+    }
+    s += in[q[0] + (long long)nx * (q[1] + (long long)ny * q[2])];
+  }
+  out[i] = s * (1.0 / double(nops));
+}
+
+void symmetrize(const int n[3], double* field, int sym, double* scratch, cudaStream_t s) {
+  if (sym == 0) return;
+  if (sym != 1 && (n[0] != n[1] || n[1] != n[2]))
+    throw std::invalid_argument("reflect6/rotate3 symmetry requires a cubic grid");
+  static int perm[kMaxOps][3], flip[kMaxOps][3];
+  const int nops = symmetry_group(sym, perm, flip);
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+  const long long m = (long long)n[0] * n[1] * n[2];
+  IHOM_CUDA(cudaMemcpyAsync(scratch, field, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+  symmetrize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], nops, scratch, field);
+  IHOM_LAUNCH_CHECK();
+  IHOM_CUDA(cudaStreamSynchronize(s));  // constant staging buffers are static
+}
+
+__global__ void clamp_kernel(double* f, long long m, double lo, double hi) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) f[i] = fmin(fmax(f[i], lo), hi);
+}
+
+void clamp_field(double* f, long long m, double lo, double hi, cudaStream_t s) {
+  clamp_kernel<<<ceil_div(m, 256), 256, 0, s>>>(f, m, lo, hi);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- reductions for OC
+constexpr int kDT = 256;
+
+__device__ __forceinline__ double block_reduce_d(double v, double* sh, bool is_max) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_down_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, w) : v + w;
+  }
+  if ((t & 31) == 0) sh[t >> 5] = v;
+  __syncthreads();
+  double r = is_max ? -INFINITY : 0.0;
+  if (t < 32) {
+    r = (t < (int)(blockDim.x >> 5)) ? sh[t] : r;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_down_sync(0xffffffffu, r, o);
+      r = is_max ? fmax(r, w) : r + w;
+    }
+  }
+  __syncthreads();
+  return r;
+}
+
+static int dgrid(long long n) {
+  long long g = (n + kDT * 8 - 1) / (kDT * 8);
+  if (g < 1) g = 1;
+  if (g > kReducePartials) g = kReducePartials;
+  return int(g);
+}
+
+__global__ void finalize_d(const double* partials, int nparts, bool is_max, double* out) {
+  __shared__ double sh[32];
+  double s = is_max ? -INFINITY : 0.0;
+  for (int i = threadIdx.x; i < nparts; i += kDT) s = is_max ? fmax(s, partials[i]) : s + partials[i];
+  const double r = block_reduce_d(s, sh, is_max);
+  if (threadIdx.x == 0) *out = r;
+}
+
+__global__ void sum_kernel(const double* __restrict__ f, long long m, double* partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) s += f[i];
+  const double r = block_reduce_d(s, sh, false);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+void field_sum(const double* f, long long m, double* partials, double* out, cudaStream_t s) {
+  const int g = dgrid(m);
+  sum_kernel<<<g, kDT, 0, s>>>(f, m, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_d<<<1, kDT, 0, s>>>(partials, g, false, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+// max(1e-30, -g) over the field plus a non-finite flag (src/oc.cpp:29-38)
+__global__ void oc_scale_kernel(const double* __restrict__ g, long long m, double* partials, int* bad) {
+  __shared__ double sh[32];
+  double s = 1e-30;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    const double v = g[i];
+    if (!isfinite(v)) atomicExch(bad, 1);
+    s = fmax(s, fmax(1e-30, -v));
+  }
+  const double r = block_reduce_d(s, sh, true);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+struct OCParams {
+  double damp, step, lo, hi;
+};
+
+__device__ __forceinline__ double oc_value(double rho, double g, double inv_scale, double lambda, OCParams p) {
+  const double b0 = fmax(1e-30, -g) * inv_scale;  // (src/oc.cpp:39-41)
+  const double ratio = b0 / lambda;
+  double x = rho * (p.damp == 0.5 ? sqrt(ratio) : pow(ratio, p.damp));  // src/oc.cpp:18
+  x = fmin(fmax(x, rho - p.step), rho + p.step);
+  return fmin(fmax(x, p.lo), p.hi);
+}
+
+// trial: partial sums of the trial field; write != 0 also stores it.
+__global__ void oc_trial_kernel(const double* __restrict__ rho, const double* __restrict__ g, long long m,
+                                const double* scale, double lambda, OCParams p, double* partials, double* out) {
+  __shared__ double sh[32];
+  const double inv_scale = 1.0 / *scale;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    const double v = oc_value(rho[i], g[i], inv_scale, lambda, p);
+    if (out) out[i] = v;
+    s += v;
+  }
+  const double r = block_reduce_d(s, sh, false);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+// oc_update (src/oc.cpp:27-77): host-driven geometric bisection; each trial is one
+// fused pass (b0 normalisation, pow, step clamp, box clamp, block sums) with a
+// single 8-byte read-back.
+OCResult oc_update(long long m, const double* rho, const double* g, const OCConfig& cfg, double* out, Workspace& ws,
+                   cudaStream_t s) {
+  const int grid = dgrid(m);
+  IHOM_CUDA(cudaMemsetAsync(ws.flag, 0, sizeof(int), s));
+  oc_scale_kernel<<<grid, kDT, 0, s>>>(g, m, ws.partials, ws.flag);
+  IHOM_LAUNCH_CHECK();
+  finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, true, ws.scalar);
+  IHOM_LAUNCH_CHECK();
+  int bad = 0;
+  double scale = 0.0;
+  IHOM_CUDA(cudaMemcpyAsync(&bad, ws.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  if (bad) throw std::invalid_argument("non-finite sensitivity");
+  // keep the scale on device in ws.scalar (read by every trial)
+  const OCParams p{cfg.damp, cfg.step_limit, cfg.min_density, 1.0};
+  auto trial = [&](double lambda, bool write) {
+    oc_trial_kernel<<<grid, kDT, 0, s>>>(rho, g, m, ws.scalar, lambda, p, ws.partials, write ? out : nullptr);
+    IHOM_LAUNCH_CHECK();
+    finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);
+    IHOM_LAUNCH_CHECK();
+    double sum = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    return sum / double(m);
+  };
+  OCResult res;
+  const double lo0 = 1e-12, hi0 = 1e12;
+  const double mean_lo = trial(lo0, false);
+  if (cfg.volume >= mean_lo) {
+    trial(lo0, true);
+    res.lambda = lo0 * scale;
+    res.bisection_ok = std::abs(mean_lo - cfg.volume) <= cfg.bisect_tol;
+    return res;
+  }
+  const double mean_hi = trial(hi0, false);
+  if (cfg.volume <= mean_hi) {
+    trial(hi0, true);
+    res.lambda = hi0 * scale;
+    res.bisection_ok = std::abs(mean_hi - cfg.volume) <= cfg.bisect_tol;
+    return res;
+  }
+  double lo = lo0, hi = hi0, lambda = lo0, mean = 0.0;
+  for (int it = 0; it < 60; ++it) {
+    lambda = std::sqrt(lo * hi);
+    mean = trial(lambda, false);
+    res.trials = it + 1;
+    if (std::abs(mean - cfg.volume) <= cfg.bisect_tol) {
+      trial(lambda, true);
+      res.lambda = lambda * scale;
+      return res;
+    }
+    (mean > cfg.volume ? lo : hi) = lambda;
+  }
+  trial(lambda, true);
+  res.lambda = lambda * scale;
+  res.bisection_ok = std::abs(mean - cfg.volume) <= cfg.bisect_tol;
+  return res;
+}
+
+}  // namespace ihomgpu
+
+namespace ihomgpu {
+
+// ---------------------------------------------------------------- trig init
+// init_trig (src/density.cpp:169-259): the random weights and rotation are
+// drawn on the host with the reference's counter-based splitmix64 stream;
+// the Q_n basis evaluation and the sigmoid-offset bisection run on device.
+constexpr int kMaxTrigW = 48 + 48 * 49 / 2;
+__constant__ double c_trig_w[kMaxTrigW];
+__constant__ double c_trig_rot[9];
+
+__global__ void trig_eval_kernel(int nx, int ny, int nz, int basis_n, double* __restrict__ y) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long m = (long long)nx * ny * nz;
+  if (i >= m) return;
+  const int n[3] = {nx, ny, nz};
+  int e[3];
+  e[0] = int(i % nx);
+  const long long r = i / nx;
+  e[1] = int(r % ny);
+  e[2] = int(r / ny);
+  double xb[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    xb[a] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xb[a] += c_trig_rot[a * 3 + k] * ((e[k] + 0.5) / double(n[k]) - 0.5);
+  }
+  double t[48];
+  const int nt = 6 * basis_n;
+  for (int ax = 0, j = 0; ax < 3; ++ax)
+    for (int k = 1; k <= basis_n; ++k) {
+      t[j++] = cos(2.0 * M_PI * k * xb[ax]);
+      t[j++] = sin(2.0 * M_PI * k * xb[ax]);
+    }
+  double s = 0.0;
+  int j = 0;
+  for (int a = 0; a < nt; ++a) s += c_trig_w[j++] * t[a];
+  for (int a = 0; a < nt; ++a)
+    for (int b = a; b < nt; ++b) s += c_trig_w[j++] * t[a] * t[b];
+  y[i] = s;
+}
+
+__global__ void minmax_kernel(const double* __restrict__ y, long long m, double* partials) {
+  __shared__ double sh[32];
+  double lo = INFINITY, hi = -INFINITY;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    lo = fmin(lo, y[i]);
+    hi = fmax(hi, y[i]);
+  }
+  const double rhi = block_reduce_d(hi, sh, true);
+  const double rlo = -block_reduce_d(-lo, sh, true);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = rhi;
+    partials[kReducePartials + blockIdx.x] = rlo;
+  }
+}
+
+__global__ void project_kernel(const double* __restrict__ y, long long m, double vhat, double k, double mu,
+                               double* __restrict__ rho, double* partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    const double v = kRhoMin + vhat / (1.0 + exp(-k * (y[i] - mu)));
+    rho[i] = v;
+    s += v;
+  }
+  const double r = block_reduce_d(s, sh, false);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+static std::uint64_t splitmix64(std::uint64_t x) {  // src/density.cpp:154-159
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d449bd133111ebULL;
+  return x ^ (x >> 31);
+}
+static double uniform_pm1(std::uint64_t seed, std::uint64_t counter) {  // :162-165
+  const std::uint64_t h = splitmix64(splitmix64(seed) ^ (counter * 0xd1b54a32d192ed03ULL + 1));
+  return double(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+bool init_trig(const int n[3], int basis_n, std::uint64_t seed, double volume, double sigmoid_k, double* rho,
+               double* scratch, Workspace& ws, cudaStream_t s) {
+  if (basis_n < 1 || basis_n > 8) throw std::invalid_argument("trig basis order must be in [1, 8]");
+  if (!(volume > kRhoMin && volume <= 1.0)) throw std::invalid_argument("volume fraction out of range");
+  const long long m = (long long)n[0] * n[1] * n[2];
+  const int nt = 6 * basis_n;
+  const int nq = nt + nt * (nt + 1) / 2;
+  std::vector<double> w(static_cast<size_t>(nq));
+  for (int j = 0; j < nq; ++j) w[size_t(j)] = uniform_pm1(seed, std::uint64_t(j));
+  double q[4], qn = 0.0;
+  for (int j = 0; j < 4; ++j) {
+    q[j] = uniform_pm1(seed, std::uint64_t(nq + j));
+    qn += q[j] * q[j];
+  }
+  if (qn < 1e-12) {
+    q[0] = 1.0;
+    q[1] = q[2] = q[3] = 0.0;
+    qn = 1.0;
+  }
+  qn = std::sqrt(qn);
+  for (double& c : q) c /= qn;
+  const double qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+  const double rot[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                         2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                         2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_w, w.data(), sizeof(double) * nq, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_rot, rot, sizeof(rot), 0, cudaMemcpyHostToDevice, s));
+  double* y = scratch;
+  trig_eval_kernel<<<ceil_div(m, 128), 128, 0, s>>>(n[0], n[1], n[2], basis_n, y);
+  IHOM_LAUNCH_CHECK();
+  const int grid = dgrid(m);
+  minmax_kernel<<<grid, kDT, 0, s>>>(y, m, ws.partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, true, ws.scalar);
+  // min = -max(-x): reuse finalize on the second half
+  std::vector<double> mins(static_cast<size_t>(grid));
+  double yhi = 0.0;
+  IHOM_CUDA(cudaMemcpyAsync(&yhi, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaMemcpyAsync(mins.data(), ws.partials + kReducePartials, sizeof(double) * grid, cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  double ylo = mins[0];
+  for (double v : mins) ylo = std::min(ylo, v);
+  const double vhat = std::min(1.5 * volume, 1.0 - kRhoMin);
+  const double k = sigmoid_k;
+  auto project = [&](double mu) {
+    project_kernel<<<grid, kDT, 0, s>>>(y, m, vhat, k, mu, rho, ws.partials);
+    IHOM_LAUNCH_CHECK();
+    finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);
+    double sum = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    return sum / double(m);
+  };
+  auto constant = [&]() {
+    std::vector<double> c(size_t(m), volume);
+    IHOM_CUDA(cudaMemcpyAsync(rho, c.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  };
+  double lo = ylo - 45.0 / k, hi = yhi + 45.0 / k;
+  if (!(project(lo) >= volume && project(hi) <= volume)) {
+    constant();
+    return true;
+  }
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double mean = project(mid);
+    if (std::abs(mean - volume) <= 1e-4) return false;
+    (mean > volume ? lo : hi) = mid;
+  }
+  if (std::abs(project(0.5 * (lo + hi)) - volume) <= 1e-4) return false;
+  constant();
+  return true;
+}
+
+}  // namespace ihomgpu

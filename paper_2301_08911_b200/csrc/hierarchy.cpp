@@ -1,0 +1,488 @@
+// hierarchy.cpp -- host orchestration of the device multigrid hierarchy and
+// the homogenizer (src/multigrid.cpp:245-501, src/homogenization.cpp:16-144).
+#include "hierarchy.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <type_traits>
+
+namespace ihomgpu {
+
+namespace {
+
+constexpr int kRedDoubles = 21 * kReducePartials + 128;
+
+// Dense assembly of a level operator in the reference dof order 3*loc + c
+// (src/multigrid.cpp:335-366).
+std::vector<double> assemble_dense_l0(const GridGeo& g, const std::vector<double>& coeff, const K0Matrix& k0) {
+  const long long nv = g.nv, N = 3 * nv;
+  std::vector<double> a(size_t(N * N), 0.0);
+  for (long long ei = 0; ei < nv; ++ei) {
+    const int ex = int(ei % g.n[0]);
+    const long long r = ei / g.n[0];
+    const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
+    long long locs[8];
+    for (int j = 0; j < 8; ++j)
+      locs[j] = vloc(g, (ex + (j & 1)) % g.n[0], (ey + ((j >> 1) & 1)) % g.n[1], (ez + ((j >> 2) & 1)) % g.n[2]);
+    const double q = coeff[size_t(ei)];
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j)
+        for (int rr = 0; rr < 3; ++rr)
+          for (int c = 0; c < 3; ++c)
+            a[size_t((3 * locs[i] + rr) * N + 3 * locs[j] + c)] += q * k0.k[3 * i + rr][3 * j + c];
+  }
+  return a;
+}
+
+template <typename T>
+std::vector<double> assemble_dense_stencil(const GridGeo& g, const std::vector<T>& st) {
+  const long long nv = g.nv, N = 3 * nv;
+  std::vector<double> a(size_t(N * N), 0.0);
+  for (long long loc = 0; loc < nv; ++loc) {
+    const int color = color_at(g, loc);
+    int x, y, z;
+    block_coords(g, color, (unsigned)(loc - g.base[color]), x, y, z);
+    for (int n = 0; n < 27; ++n) {
+      const int tx = n % 3 - 1, ty = (n / 3) % 3 - 1, tz = n / 9 - 1;
+      const long long wl = vloc(g, (x + tx + g.n[0]) % g.n[0], (y + ty + g.n[1]) % g.n[1], (z + tz + g.n[2]) % g.n[2]);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+          a[size_t((3 * loc + r) * N + 3 * wl + c)] += double(st[size_t((9 * n + 3 * r + c) * nv + loc)]);
+    }
+  }
+  return a;
+}
+
+// Cholesky of the shifted SPD matrix (stands in for Eigen::LDLT,
+// src/multigrid.cpp:380-382) and its explicit inverse.
+std::vector<double> spd_inverse(std::vector<double> a, int N) {
+  for (int j = 0; j < N; ++j) {
+    double d = a[size_t(j) * N + j];
+    for (int k = 0; k < j; ++k) d -= a[size_t(j) * N + k] * a[size_t(j) * N + k];
+    if (!(d > 0.0)) throw NumericError("coarsest-level factorization failed");
+    const double l = std::sqrt(d);
+    a[size_t(j) * N + j] = l;
+    for (int i = j + 1; i < N; ++i) {
+      double s = a[size_t(i) * N + j];
+      for (int k = 0; k < j; ++k) s -= a[size_t(i) * N + k] * a[size_t(j) * N + k];
+      a[size_t(i) * N + j] = s / l;
+    }
+  }
+  std::vector<double> inv(size_t(N) * N, 0.0), col(static_cast<size_t>(N));
+  for (int c = 0; c < N; ++c) {
+    for (int i = 0; i < N; ++i) col[size_t(i)] = (i == c) ? 1.0 : 0.0;
+    for (int i = 0; i < N; ++i) {
+      double s = col[size_t(i)];
+      for (int k = 0; k < i; ++k) s -= a[size_t(i) * N + k] * col[size_t(k)];
+      col[size_t(i)] = s / a[size_t(i) * N + i];
+    }
+    for (int i = N - 1; i >= 0; --i) {
+      double s = col[size_t(i)];
+      for (int k = i + 1; k < N; ++k) s -= a[size_t(k) * N + i] * col[size_t(k)];
+      col[size_t(i)] = s / a[size_t(i) * N + i];
+    }
+    for (int i = 0; i < N; ++i) inv[size_t(i) * N + c] = col[size_t(i)];
+  }
+  return inv;
+}
+
+bool can_coarsen(const GridGeo& g) {  // inc/grid.hpp:47-51
+  for (int k = 0; k < 3; ++k)
+    if (g.n[k] % 2 != 0 || g.n[k] / 2 < 4) return false;
+  return true;
+}
+
+}  // namespace
+
+// ============================================================== Hierarchy
+template <typename T>
+Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s)
+    : mat_(mat), penal_(penal), s_(s) {
+  for (int k = 0; k < 3; ++k)
+    if (n[k] < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
+  if ((long long)n[0] * n[1] * n[2] >= (1LL << 31)) throw std::invalid_argument("grid too large for 32-bit vertex indexing");
+  k0_ = element_stiffness(mat);
+  bind_tables();
+  GridGeo g = make_geo(n[0], n[1], n[2]);
+  levels_.emplace_back();
+  levels_.back().g = g;
+  while (can_coarsen(g)) {
+    g = make_geo(g.n[0] / 2, g.n[1] / 2, g.n[2] / 2);
+    levels_.emplace_back();
+    levels_.back().g = g;
+  }
+  if (levels_.back().g.nv > 343) throw std::invalid_argument("coarsest level larger than 7^3 is not supported");
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    Level& L = levels_[l];
+    const size_t n3 = size_t(3 * L.g.nv);
+    L.u.alloc(n3);
+    L.f.alloc(n3);
+    L.r.alloc(n3);
+    IHOM_CUDA(cudaMemsetAsync(L.u.p, 0, sizeof(double) * n3, s_));
+    IHOM_CUDA(cudaMemsetAsync(L.f.p, 0, sizeof(double) * n3, s_));
+    IHOM_CUDA(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n3, s_));
+    if (l > 0) L.st.alloc(size_t(243 * L.g.nv));
+  }
+  coeff_.alloc(size_t(levels_[0].g.nv));
+  ndof_c_ = int(3 * levels_.back().g.nv);
+  cwork_.alloc(size_t(3 * ndof_c_));
+  red_.alloc(kRedDoubles);
+  err_.alloc(1);
+  IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
+  ws_.partials = red_.p;
+  ws_.scalar = red_.p + 21 * kReducePartials;
+  ws_.scalar2 = ws_.scalar + 1;
+  ws_.scalars = ws_.scalar + 8;
+  ws_.flag = err_.p;
+  IHOM_CUDA(cudaMallocHost(&h_pinned_, 64 * sizeof(double)));
+}
+
+template <typename T>
+void Hierarchy<T>::bind_tables() {
+  const StiffnessTables tab(k0_);
+  upload_fem_tables(tab, k0_, s_);
+  upload_galerkin_tables(ElementGalerkin(k0_), s_);
+}
+
+template <typename T>
+void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-279
+  const GridGeo& g0 = levels_[0].g;
+  launch_coeff<T>(rho, coeff_.p, g0.nv, penal_, s_);
+  if (levels_.size() > 1) {
+    launch_galerkin_from_elements<T>(g0, levels_[1].g, coeff_.p, levels_[1].st.p, s_);
+    for (size_t l = 2; l < levels_.size(); ++l)
+      launch_galerkin_from_stencil<T>(levels_[l - 1].g, levels_[l].g, levels_[l - 1].st.p, levels_[l].st.p, s_);
+  }
+  factor_coarsest();
+  density_set_ = true;
+}
+
+template <typename T>
+void Hierarchy<T>::factor_coarsest() {  // src/multigrid.cpp:368-383
+  const int lc = num_levels() - 1;
+  const GridGeo& g = levels_[size_t(lc)].g;
+  std::vector<double> a;
+  if (lc == 0) {
+    std::vector<T> c(size_t(g.nv));
+    IHOM_CUDA(cudaMemcpyAsync(c.data(), coeff_.p, sizeof(T) * c.size(), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    std::vector<double> cd(c.begin(), c.end());
+    a = assemble_dense_l0(g, cd, k0_);
+  } else {
+    std::vector<T> st(size_t(243 * g.nv));
+    IHOM_CUDA(cudaMemcpyAsync(st.data(), levels_[size_t(lc)].st.p, sizeof(T) * st.size(), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    a = assemble_dense_stencil<T>(g, st);
+  }
+  const int N = ndof_c_;
+  double dsum = 0.0;
+  for (int i = 0; i < N; ++i) dsum += a[size_t(i) * N + i];
+  op_scale_ = dsum / double(N);  // mean diagonal (src/multigrid.cpp:373)
+  std::vector<double> shifted = a;
+  const long long nv = g.nv;
+  for (long long i = 0; i < nv; ++i)
+    for (long long j = 0; j < nv; ++j)
+      for (int c = 0; c < 3; ++c) shifted[size_t((3 * i + c) * N + 3 * j + c)] += op_scale_ / double(nv);
+  const std::vector<double> inv = spd_inverse(shifted, N);
+  A_.alloc(a.size());
+  Ainv_.alloc(inv.size());
+  IHOM_CUDA(cudaMemcpyAsync(A_.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice, s_));
+  IHOM_CUDA(cudaMemcpyAsync(Ainv_.p, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, s_));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+}
+
+template <typename T>
+double Hierarchy<T>::negligible_load(long long ndof) const {  // src/multigrid.cpp:388-390
+  return 1e-12 * op_scale_ * std::sqrt(double(ndof));
+}
+
+template <typename T>
+void Hierarchy<T>::check_error(const char* where) {
+  int e = 0;
+  IHOM_CUDA(cudaMemcpyAsync(&e, err_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+  if (e) {
+    IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
+    if (e == 1) throw NumericError(std::string("non-invertible coarse stencil diagonal (") + where + ")");
+    throw NumericError(std::string("coarsest operator is singular beyond translations (") + where + ")");
+  }
+}
+
+template <typename T>
+void Hierarchy<T>::remove_translations(double* f, int l) {  // src/multigrid.cpp:81-86
+  const long long nv = levels_[size_t(l)].g.nv;
+  launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
+  launch_sub_means<double>(f, nv, ws_.scalars, s_);
+  launches_ += 3;
+}
+
+template <typename T>
+double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:88-94
+  launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_);
+  launches_ += 2;
+  IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+  return std::sqrt(h_pinned_[0]);
+}
+
+template <typename T>
+void Hierarchy<T>::apply(int l, const double* x, double* y) {  // src/multigrid.cpp:392-398
+  const Level& L = levels_[size_t(l)];
+  if (l == 0) launch_l0_apply<T, double, double>(L.g, coeff_.p, x, nullptr, y, s_);
+  else launch_stencil_apply<T, double>(L.g, L.st.p, x, nullptr, y, s_);
+  ++launches_;
+}
+
+template <typename T>
+void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
+  Level& L = levels_[size_t(l)];
+  double* u = level_u(l);
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int c = 0; c < 8; ++c) {
+      if (L.g.size[c] == 0) continue;
+      if (l == 0) launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_);
+      else launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_);
+      ++launches_;
+    }
+}
+
+template <typename T>
+void Hierarchy<T>::compute_residual(int l) {  // src/multigrid.cpp:410-424
+  Level& L = levels_[size_t(l)];
+  if (l == 0) launch_l0_apply<T, double, double>(L.g, coeff_.p, level_u(0), L.f.p, L.r.p, s_);
+  else launch_stencil_apply<T, double>(L.g, L.st.p, L.u.p, L.f.p, L.r.p, s_);
+  ++launches_;
+}
+
+template <typename T>
+void Hierarchy<T>::coarsest_solve() {  // src/multigrid.cpp:426-451
+  const int lc = num_levels() - 1;
+  Level& L = levels_[size_t(lc)];
+  launch_coarsest_solve<double>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.f.p, level_u(lc), negligible_load(ndof_c_),
+                                cwork_.p, err_.p, s_);
+  ++launches_;
+}
+
+template <typename T>
+double Hierarchy<T>::v_cycle(const SolverOptions& opts) {  // src/multigrid.cpp:453-472
+  if (!density_set_) throw StateError("set_density before v_cycle");
+  if (opts.mode == kMixedDefect && std::is_same_v<T, float>) return v_cycle_defect(opts);
+  const int lmax = num_levels() - 1;
+  for (int l = 0; l < lmax; ++l) {
+    if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].u.p, 0, sizeof(double) * 3 * levels_[size_t(l)].g.nv, s_));
+    relax(l, opts.pre_sweeps);
+    compute_residual(l);
+    launch_restrict<double>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].r.p,
+                            levels_[size_t(l + 1)].f.p, s_);
+    ++launches_;
+  }
+  if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].u.p, 0, sizeof(double) * 3 * levels_[size_t(lmax)].g.nv, s_));
+  coarsest_solve();
+  for (int l = lmax - 1; l >= 0; --l) {
+    launch_prolong_add<double>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].u.p, level_u(l), s_);
+    ++launches_;
+    relax(l, opts.post_sweeps);
+  }
+  compute_residual(0);
+  const long long n0 = 3 * levels_[0].g.nv;
+  // ||f_0|| is constant inside solve() unless the coarsest solve (lmax == 0) re-projects f_0
+  const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(levels_[0].f.p, n0);
+  const double rn = norm(levels_[0].r.p, n0);
+  check_error("v_cycle");
+  return fn > 0.0 ? rn / fn : 0.0;
+}
+
+// ---- mixed-precision defect-correction cycle (kMixedDefect) ----
+template <typename T>
+void Hierarchy<T>::ensure_inner() {
+  if (inner_ready_) return;
+  for (auto& L : levels_) {
+    const size_t n3 = size_t(3 * L.g.nv);
+    L.eu.alloc(n3);
+    L.ef.alloc(n3);
+    L.er.alloc(n3);
+  }
+  inner_ready_ = true;
+}
+
+template <typename T>
+void Hierarchy<T>::relax_f32(int l, int sweeps) {
+  Level& L = levels_[size_t(l)];
+  if constexpr (std::is_same_v<T, float>) {
+    for (int sw = 0; sw < sweeps; ++sw)
+      for (int c = 0; c < 8; ++c) {
+        if (L.g.size[c] == 0) continue;
+        if (l == 0) launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_);
+        else launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_);
+        ++launches_;
+      }
+  }
+}
+
+template <typename T>
+void Hierarchy<T>::residual_f32(int l) {
+  Level& L = levels_[size_t(l)];
+  if constexpr (std::is_same_v<T, float>) {
+    if (l == 0) launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_);
+    else launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_);
+    ++launches_;
+  }
+}
+
+template <typename T>
+void Hierarchy<T>::coarsest_f32() {
+  const int lc = num_levels() - 1;
+  Level& L = levels_[size_t(lc)];
+  launch_coarsest_solve<float>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.ef.p, L.eu.p, 0.0, cwork_.p, err_.p, s_);
+  ++launches_;
+}
+
+template <typename T>
+double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
+  ensure_inner();
+  const int lmax = num_levels() - 1;
+  Level& L0 = levels_[0];
+  const long long n0 = 3 * L0.g.nv;
+  // inner right-hand side: the current outer residual. Inside solve() it is
+  // current (computed before the loop and at the end of every cycle).
+  if (!u0_bound_) compute_residual(0);
+  launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+  IHOM_CUDA(cudaMemsetAsync(L0.eu.p, 0, sizeof(float) * n0, s_));
+  launches_ += 1;
+  for (int l = 0; l < lmax; ++l) {
+    if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
+    relax_f32(l, opts.pre_sweeps);
+    residual_f32(l);
+    launch_restrict<float>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].er.p,
+                           levels_[size_t(l + 1)].ef.p, s_);
+    ++launches_;
+  }
+  if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(lmax)].g.nv, s_));
+  coarsest_f32();
+  for (int l = lmax - 1; l >= 0; --l) {
+    launch_prolong_add<float>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].eu.p,
+                              levels_[size_t(l)].eu.p, s_);
+    ++launches_;
+    relax_f32(l, opts.post_sweeps);
+  }
+  launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
+  ++launches_;
+  compute_residual(0);
+  const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(L0.f.p, n0);
+  const double rn = norm(L0.r.p, n0);
+  check_error("v_cycle");
+  return fn > 0.0 ? rn / fn : 0.0;
+}
+
+template <typename T>
+SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts) {  // src/multigrid.cpp:474-501
+  if (!density_set_) throw StateError("set_density before solve");
+  u0_bound_ = u;
+  Level& L0 = levels_[0];
+  const long long n0 = 3 * L0.g.nv;
+  SolveStats st;
+  try {
+    remove_translations(L0.f.p, 0);
+    fnorm0_ = norm(L0.f.p, n0);
+    if (fnorm0_ <= negligible_load(n0)) {
+      IHOM_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n0, s_));
+      st.converged = true;
+      u0_bound_ = nullptr;
+      return st;
+    }
+    compute_residual(0);
+    st.rel_residual = norm(L0.r.p, n0) / fnorm0_;
+    while (st.rel_residual > opts.tol && st.cycles < opts.max_cycles) {
+      st.rel_residual = v_cycle(opts);
+      ++st.cycles;
+    }
+    st.converged = st.rel_residual <= opts.tol;
+    remove_translations(u, 0);
+  } catch (...) {
+    u0_bound_ = nullptr;
+    throw;
+  }
+  u0_bound_ = nullptr;
+  return st;
+}
+
+// ============================================================== Homogenizer
+template <typename T>
+Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts,
+                            cudaStream_t s)
+    : hier_(n, mat, penal, s), opts_(opts), penal_(penal) {
+  const long long nv = hier_.geo(0).nv;
+  rho_.alloc(size_t(nv));
+  for (auto& u : u_) {
+    u.alloc(size_t(3 * nv));
+    IHOM_CUDA(cudaMemsetAsync(u.p, 0, sizeof(double) * 3 * nv, s));
+  }
+  seed_.alloc(36);
+  IHOM_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void Homogenizer<T>::set_density(const double* rho) {  // src/homogenization.cpp:16-21
+  IHOM_CUDA(cudaMemcpyAsync(rho_.p, rho, sizeof(double) * rho_.n, cudaMemcpyDeviceToDevice, hier_.stream()));
+  hier_.set_density(rho_.p);
+  density_set_ = true;
+}
+
+template <typename T>
+CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cpp:23-40
+  if (!density_set_) throw StateError("set_density before solve_cell_problems");
+  CellSolveStats out;
+  const GridGeo& g = hier_.geo(0);
+  for (int i = 0; i < 6; ++i) {
+    launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream());
+    const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_);
+    out.total_cycles += s.cycles;
+    if (s.rel_residual >= out.worst_residual) {
+      out.worst_residual = s.rel_residual;
+      out.worst_load = i;
+    }
+    if (!s.converged) out.converged = false;
+  }
+  return out;
+}
+
+template <typename T>
+void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp:58-111
+  const double* u[6];
+  for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
+  Workspace& ws = hier_.workspace();
+  const Material& m = hier_.material();
+  launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
+                                  ws.partials, ws.scalars + 16, hier_.stream());
+  double c21[21];
+  IHOM_CUDA(cudaMemcpyAsync(c21, ws.scalars + 16, sizeof(c21), cudaMemcpyDeviceToHost, hier_.stream()));
+  IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
+  const double M = double(hier_.geo(0).nv);
+  int q = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j, ++q) {
+      C[i * 6 + j] = c21[q] / M;
+      C[j * 6 + i] = C[i * 6 + j];
+    }
+}
+
+template <typename T>
+void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  // src/homogenization.cpp:113-144
+  double s[36];
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) s[i * 6 + j] = 0.5 * (seed[i * 6 + j] + seed[j * 6 + i]);
+  IHOM_CUDA(cudaMemcpyAsync(seed_.p, s, sizeof(s), cudaMemcpyHostToDevice, hier_.stream()));
+  const double* u[6];
+  for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
+  const Material& m = hier_.material();
+  launch_tensor_sensitivity<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
+                                    seed_.p, out, hier_.stream());
+  IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
+}
+
+template class Hierarchy<float>;
+template class Hierarchy<double>;
+template class Homogenizer<float>;
+template class Homogenizer<double>;
+
+}  // namespace ihomgpu

@@ -1,0 +1,192 @@
+// hierarchy.hpp -- device-resident geometric multigrid hierarchy and the
+// homogenizer that drives the six periodic cell problems.
+//
+// Mirrors ihom::Hierarchy<T> (inc/multigrid.hpp:53-93) and
+// ihom::Homogenizer<T> (inc/homogenization.hpp:26-51): same method names,
+// same semantics, T = coefficient/stencil storage (float: mixed, double:
+// all-double). Nodal data are f64 SoA in device memory.
+//
+// Two solver modes:
+//   kVCycle    -- the reference's stationary V-cycle iteration, step for step
+//                 (src/multigrid.cpp:453-501), f64 nodal data throughout;
+//   kMixedDefect (mixed precision only) -- the same V-cycle in defect-correction
+//                 form: the outer residual r = f - K u and the update u += e
+//                 are f64, the inner V-cycle on K e = r runs on f32 nodal data
+//                 (identical to the reference's cycle in exact arithmetic;
+//                 see DESIGN.md "solver modes").
+#pragma once
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "density.hpp"
+#include "kernels.hpp"
+#include "tables.hpp"
+
+namespace ihomgpu {
+
+enum SolverMode { kVCycle = 0, kMixedDefect = 1 };
+
+struct SolverOptions {  // inc/multigrid.hpp:22-27
+  double tol = 1e-2;
+  int max_cycles = 50;
+  int pre_sweeps = 1;
+  int post_sweeps = 1;
+  int mode = kVCycle;
+};
+
+struct SolveStats {  // inc/multigrid.hpp:29-33
+  int cycles = 0;
+  double rel_residual = 0.0;
+  bool converged = false;
+};
+
+struct CellSolveStats {  // inc/homogenization.hpp:13-18
+  int total_cycles = 0;
+  double worst_residual = 0.0;
+  int worst_load = -1;
+  bool converged = true;
+};
+
+// RAII device buffer.
+template <typename X>
+struct DevBuf {
+  X* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) IHOM_CUDA(cudaMalloc(&p, sizeof(X) * count));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p;
+    n = o.n;
+    o.p = nullptr;
+    o.n = 0;
+    return *this;
+  }
+};
+
+template <typename T>
+class Hierarchy {
+ public:
+  using value_type = T;
+  Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s);
+  ~Hierarchy() {
+    if (h_pinned_) cudaFreeHost(h_pinned_);
+  }
+  Hierarchy(const Hierarchy&) = delete;
+  Hierarchy& operator=(const Hierarchy&) = delete;
+
+  void set_density(const double* rho_phys_dev);
+  void bind_tables();  // re-upload this hierarchy's constant tables (shared per process)
+  int num_levels() const { return int(levels_.size()); }
+  const GridGeo& geo(int l) const { return levels_[size_t(l)].g; }
+
+  // Reference operations on the f64 level fields.
+  void apply(int l, const double* x, double* y);  // y = K_l x
+  void relax(int l, int sweeps);
+  void compute_residual(int l);
+  void coarsest_solve();
+  double v_cycle(const SolverOptions& opts);
+  // Solve K u = f with l0.f already holding the load; u is the warm start /
+  // result buffer (bound as level-0 u for the duration of the call).
+  SolveStats solve_bound(double* u, const SolverOptions& opts);
+
+  double* level_u(int l) { return l == 0 && u0_bound_ ? u0_bound_ : levels_[size_t(l)].u.p; }
+  double* level_f(int l) { return levels_[size_t(l)].f.p; }
+  double* level_r(int l) { return levels_[size_t(l)].r.p; }
+  const T* stencil(int l) const { return levels_[size_t(l)].st.p; }
+  const T* coeff() const { return coeff_.p; }
+  double op_scale() const { return op_scale_; }
+  double negligible_load(long long ndof) const;
+
+  // Deterministic device reductions used by the solver.
+  void remove_translations(double* f, int l);
+  double norm(const double* x, long long n);
+
+  cudaStream_t stream() const { return s_; }
+  Workspace& workspace() { return ws_; }
+  const K0Matrix& k0() const { return k0_; }
+  const Material& material() const { return mat_; }
+  long long launches() const { return launches_; }
+
+ private:
+  struct Level {
+    GridGeo g;
+    DevBuf<double> u, f, r;
+    DevBuf<T> st;                 // coarse stencil, SoA [243][nv]
+    DevBuf<float> eu, ef, er;     // f32 inner-cycle fields (kMixedDefect)
+  };
+  void factor_coarsest();
+  void check_error(const char* where);
+  void ensure_inner();
+  double v_cycle_defect(const SolverOptions& opts);
+  void relax_f32(int l, int sweeps);
+  void residual_f32(int l);
+  void coarsest_f32();
+
+  Material mat_;
+  double penal_;
+  K0Matrix k0_;
+  cudaStream_t s_;
+  std::vector<Level> levels_;
+  DevBuf<T> coeff_;
+  DevBuf<double> Ainv_, A_, cwork_;
+  int ndof_c_ = 0;
+  double op_scale_ = 0.0;
+  bool density_set_ = false;
+  bool inner_ready_ = false;
+  double* u0_bound_ = nullptr;
+  double fnorm0_ = 0.0;
+  DevBuf<double> red_;   // partials + scalars
+  DevBuf<int> err_;
+  Workspace ws_;
+  double* h_pinned_ = nullptr;  // small pinned read-back buffer
+  long long launches_ = 0;
+};
+
+template <typename T>
+class Homogenizer {
+ public:
+  Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts, cudaStream_t s);
+
+  void set_density(const double* rho_phys_dev);
+  CellSolveStats solve_cell_problems();
+  void effective_tensor(double C[36]);
+  void tensor_sensitivity(const double seed[36], double* out_dev);
+
+  double* displacement(int i) { return u_[size_t(i)].p; }
+  Hierarchy<T>& hierarchy() { return hier_; }
+  SolverOptions& options() { return opts_; }
+  const double* density() const { return rho_.p; }
+  long long nv() const { return hier_.geo(0).nv; }
+
+ private:
+  Hierarchy<T> hier_;
+  SolverOptions opts_;
+  double penal_;
+  DevBuf<double> rho_;
+  std::array<DevBuf<double>, 6> u_;
+  DevBuf<double> seed_;
+  bool density_set_ = false;
+};
+
+}  // namespace ihomgpu

@@ -1,0 +1,89 @@
+// kernels.hpp -- host-callable launchers for every device kernel of the hot
+// path. All launchers are asynchronous on the given stream; templates are
+// instantiated explicitly in the .cu files for the supported type sets.
+//
+// Type parameters: TC = element-coefficient / stencil storage (float in mixed
+// mode, double in all-double mode); TN = nodal storage; TA = arithmetic type
+// of the merged stencil.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tables.hpp"
+
+namespace ihomgpu {
+
+// ---- constant tables (one upload per material; cheap, idempotent) ----
+void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t s);
+void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s);
+
+// ---- level 0, matrix-free (src/fem.cpp:98-156, src/multigrid.cpp:263-279) ----
+template <typename TC>
+void launch_coeff(const double* rho, TC* coeff, long long m, double penal, cudaStream_t s);
+
+// y = K u (f == nullptr) or y = f - K u, over all vertices.
+template <typename TC, typename TN, typename TA>
+void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s);
+
+// One colour pass of the 8-colour Gauss-Seidel (src/fem.cpp:122-137).
+template <typename TC, typename TN, typename TA>
+void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s);
+
+template <typename TC>
+void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s);
+
+// ---- transfer (src/multigrid.cpp:12-79) ----
+template <typename TN>
+void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s);
+template <typename TN>
+void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s);
+
+// ---- coarse levels (src/multigrid.cpp:186-239, 281-333) ----
+template <typename TS, typename TN>
+void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s);
+template <typename TS, typename TN>
+void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
+                             cudaStream_t s);
+template <typename TC>
+void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s);
+template <typename TS>
+void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s);
+
+// Coarsest level: x = Ainv f with <=3 refinement steps against A, translation
+// projection in/out, singularity flag (src/multigrid.cpp:426-451). Single block.
+template <typename TN>
+void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, TN* f, TN* u,
+                           double negligible, double* work, int* err, cudaStream_t s);
+
+// ---- reductions (deterministic: fixed partition per size, fixed fold order) ----
+// sums of the three SoA components: out[3]
+template <typename TN>
+void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s);
+// out[0] = dot(a, b) over n entries
+template <typename TN>
+void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s);
+// x[c*nv + i] -= sums[c] / nv
+template <typename TN>
+void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s);
+// u += e (f64 += TN)
+template <typename TN>
+void launch_axpy_update(double* u, const TN* e, long long n, cudaStream_t s);
+// y = (TO) x
+template <typename TI, typename TO>
+void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s);
+constexpr int kReducePartials = 1184;  // 8 * 148: capacity of the partials buffer (per component)
+void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s);
+void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s);
+
+// ---- homogenization (src/homogenization.cpp:58-144) ----
+// partial sums (21 per block) of q_e * d_i^T K0 d_j; finalized into C[21].
+template <typename TN>
+void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap_f32,
+                             double lambda, double mu, double* partials, double* c21, cudaStream_t s);
+template <typename TN>
+void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal,
+                               bool snap_f32, double lambda, double mu, const double* sym_seed36, double* out,
+                               cudaStream_t s);
+
+}  // namespace ihomgpu

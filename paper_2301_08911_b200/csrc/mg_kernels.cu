@@ -1,0 +1,408 @@
+// mg_kernels.cu -- multigrid transfer, coarse stencil kernels, Galerkin
+// assembly and the coarsest dense solve (src/multigrid.cpp:12-79, 102-239,
+// 281-333, 426-451).
+#include "kernels.hpp"
+
+namespace ihomgpu {
+
+// ---------------------------------------------------------------- transfer
+// transfer_weight_1d, src/multigrid.cpp:12-15
+__host__ __device__ constexpr double tw1(int c) { return (c < 0 ? -c : c) >= 2 ? 0.0 : (2.0 - (c < 0 ? -c : c)) / 2.0; }
+
+__device__ __forceinline__ int wrapi(int c, int n) {
+  c %= n;
+  return c < 0 ? c + n : c;
+}
+
+// f_c = I^T r_f over the 27 fine vertices around 2*vc (src/multigrid.cpp:19-41).
+template <typename TN>
+__global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf, TN* __restrict__ fc) {
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= gc.nv) return;
+  const int color = color_at(gc, loc);
+  int x, y, z;
+  block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
+  double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const double w = tw1(dx) * tw1(dy) * tw1(dz);
+        const unsigned fl = vloc(gf, wrapi(2 * x + dx, gf.n[0]), wrapi(2 * y + dy, gf.n[1]), wrapi(2 * z + dz, gf.n[2]));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += w * double(rf[c * gf.nv + fl]);
+      }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) fc[c * gc.nv + loc] = TN(acc[c]);
+}
+
+template <typename TN>
+void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s) {
+  restrict_kernel<TN><<<ceil_div(gc.nv, 128), 128, 0, s>>>(gf, gc, rf, fc);
+  IHOM_LAUNCH_CHECK();
+}
+
+// u_f += I u_c (src/multigrid.cpp:43-79).
+template <typename TN>
+__global__ void prolong_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc, TN* __restrict__ uf) {
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= gf.nv) return;
+  const int color = color_at(gf, loc);
+  int v[3];
+  block_coords(gf, color, (unsigned)(loc - gf.base[color]), v[0], v[1], v[2]);
+  int base[3], cnt[3];
+  double w1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if ((v[k] & 1) == 0) {
+      base[k] = v[k] / 2;
+      cnt[k] = 1;
+      w1[k] = 1.0;
+    } else {
+      base[k] = (v[k] - 1) / 2;
+      cnt[k] = 2;
+      w1[k] = 0.5;
+    }
+  }
+  const double w = w1[0] * w1[1] * w1[2];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < cnt[0]; ++a)
+    for (int b = 0; b < cnt[1]; ++b)
+      for (int c = 0; c < cnt[2]; ++c) {
+        const unsigned cl = vloc(gc, wrapi(base[0] + a, gc.n[0]), wrapi(base[1] + b, gc.n[1]), wrapi(base[2] + c, gc.n[2]));
+#pragma unroll
+        for (int d = 0; d < 3; ++d) acc[d] += w * double(uc[d * gc.nv + cl]);
+      }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) uf[d * gf.nv + loc] = TN(double(uf[d * gf.nv + loc]) + acc[d]);
+}
+
+template <typename TN>
+void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s) {
+  prolong_kernel<TN><<<ceil_div(gf.nv, 128), 128, 0, s>>>(gc, gf, uc, uf);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- stencil apply / GS
+// y = K x (f == nullptr) or y = f - K x; stencil SoA [243][nv] (src/multigrid.cpp:186-205, 412-424).
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st,
+                                                            const TN* __restrict__ x, const TN* __restrict__ f,
+                                                            TN* __restrict__ y) {
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= g.nv) return;
+  const int color = color_at(g, loc);
+  int vx, vy, vz;
+  block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
+  Nbhd nb;
+  gather27(g, vx, vy, vz, nb);
+  const long long nv = g.nv;
+  double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll 3
+  for (int n = 0; n < 27; ++n) {
+    const double a = double(x[nb.v[n]]), b = double(x[nv + nb.v[n]]), c = double(x[2 * nv + nb.v[n]]);
+    const TS* row = st + (size_t)(9 * n) * nv + loc;
+    acc[0] += double(row[0]) * a + double(row[nv]) * b + double(row[2 * nv]) * c;
+    acc[1] += double(row[3 * nv]) * a + double(row[4 * nv]) * b + double(row[5 * nv]) * c;
+    acc[2] += double(row[6 * nv]) * a + double(row[7 * nv]) * b + double(row[8 * nv]) * c;
+  }
+  if (f) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(double(f[c * nv + loc]) - acc[c]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(acc[c]);
+  }
+}
+
+template <typename TS, typename TN>
+void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s) {
+  stencil_apply_kernel<TS, TN><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, x, f, y);
+  IHOM_LAUNCH_CHECK();
+}
+
+// Colour pass of the coarse GS with the determinant check (src/multigrid.cpp:207-239).
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st,
+                                                         const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
+                                                         int color, int* err) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.size[color]) return;
+  int vx, vy, vz;
+  block_coords(g, color, (unsigned)i, vx, vy, vz);
+  Nbhd nb;
+  gather27(g, vx, vy, vz, nb);
+  const long long nv = g.nv;
+  const long long loc = g.base[color] + i;
+  double m[3] = {0.0, 0.0, 0.0}, S[9];
+#pragma unroll 3
+  for (int n = 0; n < 27; ++n) {
+    const TS* row = st + (size_t)(9 * n) * nv + loc;
+    if (n == 13) {
+#pragma unroll
+      for (int e = 0; e < 9; ++e) S[e] = double(row[e * nv]);
+      continue;
+    }
+    const double a = double(ur[nb.v[n]]), b = double(ur[nv + nb.v[n]]), c = double(ur[2 * nv + nb.v[n]]);
+    m[0] += double(row[0]) * a + double(row[nv]) * b + double(row[2 * nv]) * c;
+    m[1] += double(row[3 * nv]) * a + double(row[4 * nv]) * b + double(row[5 * nv]) * c;
+    m[2] += double(row[6 * nv]) * a + double(row[7 * nv]) * b + double(row[8 * nv]) * c;
+  }
+  const double rhs[3] = {double(f[loc]) - m[0], double(f[nv + loc]) - m[1], double(f[2 * nv + loc]) - m[2]};
+  const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
+                     S[2] * (S[3] * S[7] - S[4] * S[6]);
+  if (det == 0.0 || !isfinite(det)) {
+    atomicExch(err, 1);
+    return;
+  }
+  double out[3];
+  solve3(S, rhs, out);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) uw[c * nv + loc] = TN(out[c]);
+}
+
+template <typename TS, typename TN>
+void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
+                             cudaStream_t s) {
+  stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- Galerkin assembly
+// Level-1 table: for every output neighbour n a list of (oidx, W[9]) terms,
+// flattened; c_eg_start[n] .. c_eg_start[n+1].
+constexpr int kMaxEgTerms = 512;
+__constant__ int c_eg_start[28];
+__constant__ int c_eg_oidx[kMaxEgTerms];
+__constant__ double c_eg_w[kMaxEgTerms][9];
+
+void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
+  int start[28];
+  static int oidx[kMaxEgTerms];
+  static double w[kMaxEgTerms][9];
+  int k = 0;
+  for (int n = 0; n < 27; ++n) {
+    start[n] = k;
+    for (const auto& t : eg.by_n[size_t(n)]) {
+      if (k >= kMaxEgTerms) throw std::logic_error("element Galerkin table overflow");
+      oidx[k] = t.oidx;
+      for (int e = 0; e < 9; ++e) w[k][e] = t.w[e];
+      ++k;
+    }
+  }
+  start[27] = k;
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_start, start, sizeof(start), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_oidx, oidx, sizeof(int) * k, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_w, w, sizeof(double) * 9 * k, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));  // host staging buffers are static
+}
+
+// assemble_stencil_from_elements (src/multigrid.cpp:281-305): one thread per
+// coarse vertex; the 64 fine-element coefficients are staged per thread in
+// shared memory ([64][blockDim] to keep banks conflict-free).
+constexpr int kGalThreads = 64;
+template <typename TC>
+__global__ void __launch_bounds__(kGalThreads) gal_elem_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
+                                                               TC* __restrict__ st) {
+  __shared__ double qs[64][kGalThreads];
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = loc < gc.nv;
+  const int t = threadIdx.x;
+  int x = 0, y = 0, z = 0;
+  if (active) {
+    const int color = color_at(gc, loc);
+    block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
+    for (int oz = -2; oz <= 1; ++oz)
+      for (int oy = -2; oy <= 1; ++oy)
+        for (int ox = -2; ox <= 1; ++ox) {
+          const int oidx = (ox + 2) + 4 * ((oy + 2) + 4 * (oz + 2));
+          const unsigned e = eidx(gf, wrapi(2 * x + ox, gf.n[0]), wrapi(2 * y + oy, gf.n[1]), wrapi(2 * z + oz, gf.n[2]));
+          qs[oidx][t] = double(coeff[e]);
+        }
+  }
+  if (!active) return;
+  const long long nvc = gc.nv;
+  for (int n = 0; n < 27; ++n) {
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = c_eg_start[n]; k < c_eg_start[n + 1]; ++k) {
+      const double q = qs[c_eg_oidx[k]][t];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) acc[e] += q * c_eg_w[k][e];
+    }
+#pragma unroll
+    for (int e = 0; e < 9; ++e) st[(size_t)(9 * n + e) * nvc + loc] = TC(acc[e]);
+  }
+}
+
+template <typename TC>
+void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s) {
+  gal_elem_kernel<TC><<<ceil_div(gc.nv, kGalThreads), kGalThreads, 0, s>>>(gf, gc, coeff, st);
+  IHOM_LAUNCH_CHECK();
+}
+
+// assemble_stencil_from_stencil (src/multigrid.cpp:307-333). The 2197 (s,t)
+// terms factor per axis: weight w(s) w(s+t-2 delta) with per-axis pairs
+// enumerated on the fly (no table); order of summation follows the
+// reference (s outer, t inner, x fastest).
+template <typename TS>
+__global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
+                                                          TS* __restrict__ stc) {
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= gc.nv) return;
+  const int color = color_at(gc, loc);
+  int x, y, z;
+  block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
+  unsigned fl[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
+    fl[s] = vloc(gf, wrapi(2 * x + sx, gf.n[0]), wrapi(2 * y + sy, gf.n[1]), wrapi(2 * z + sz, gf.n[2]));
+  }
+  const long long nvf = gf.nv, nvc = gc.nv;
+  for (int n = 0; n < 27; ++n) {
+    const int dx = n % 3 - 1, dy = (n / 3) % 3 - 1, dz = n / 9 - 1;
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+    for (int s = 0; s < 27; ++s) {
+      const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
+      const double ws = tw1(sx) * tw1(sy) * tw1(sz);
+#pragma unroll 1
+      for (int t = 0; t < 27; ++t) {
+        const int tx = t % 3 - 1, ty = (t / 3) % 3 - 1, tz = t / 9 - 1;
+        const double wt = tw1(sx + tx - 2 * dx) * tw1(sy + ty - 2 * dy) * tw1(sz + tz - 2 * dz);
+        const double w = ws * wt;
+        if (w == 0.0) continue;
+        const TS* b = stf + (size_t)(9 * t) * nvf + fl[s];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) acc[e] += w * double(b[(size_t)e * nvf]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 9; ++e) stc[(size_t)(9 * n + e) * nvc + loc] = TS(acc[e]);
+  }
+}
+
+template <typename TS>
+void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s) {
+  gal_stencil_kernel<TS><<<ceil_div(gc.nv, 128), 128, 0, s>>>(gf, gc, stf, stc);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- coarsest solve
+// One block. Vectors are SoA in the caller's nodal type; the dense matrices are
+// in the dof order 3*loc + c of the reference (src/multigrid.cpp:335-366).
+constexpr int kCoarseThreads = 512;
+
+__device__ double block_sum_1(double v, double* red) {
+  const int t = threadIdx.x;
+  red[t] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (t < s) red[t] += red[t + s];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// x is in dof order; returns sqrt(sum((A x - f)^2)) with f in dof order.
+__device__ double dense_resid(int N, const double* A, const double* x, const double* f, double* r, double* red) {
+  double part = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < N; ++j) s += A[(size_t)i * N + j] * x[j];
+    r[i] = f[i] - s;
+    part += r[i] * r[i];
+  }
+  __syncthreads();
+  return sqrt(block_sum_1(part, red));
+}
+
+template <typename TN>
+__global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long long nv, const double* __restrict__ Ainv,
+                                                                  const double* __restrict__ A, TN* f, TN* u,
+                                                                  double negligible, double* work, int* err) {
+  __shared__ double red[kCoarseThreads];
+  double* fv = work;           // [N] f in dof order
+  double* x = work + N;        // [N]
+  double* r = work + 2 * N;    // [N]
+  // remove_translations(f) (src/multigrid.cpp:81-86, 427)
+  for (int c = 0; c < 3; ++c) {
+    double part = 0.0;
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) part += double(f[c * nv + i]);
+    const double mean = block_sum_1(part, red) / double(nv);
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) {
+      const TN v = TN(double(f[c * nv + i]) - mean);
+      f[c * nv + i] = v;
+      fv[3 * i + c] = double(v);
+    }
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) part += fv[i] * fv[i];
+  const double fn = sqrt(block_sum_1(part, red));
+  if (fn <= negligible) {  // src/multigrid.cpp:430-433
+    for (int i = threadIdx.x; i < N; i += blockDim.x) u[(i % 3) * nv + i / 3] = TN(0);
+    return;
+  }
+  // x = Ainv f
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < N; ++j) s += Ainv[(size_t)i * N + j] * fv[j];
+    x[i] = s;
+  }
+  __syncthreads();
+  if (fn > 0.0) {  // refinement against the unshifted matrix (src/multigrid.cpp:435-447)
+    double rel = dense_resid(N, A, x, fv, r, red) / fn;
+    for (int it = 0; it < 3 && rel > 1e-9; ++it) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < N; ++j) s += Ainv[(size_t)i * N + j] * r[j];
+        x[i] += s;
+      }
+      __syncthreads();
+      rel = dense_resid(N, A, x, fv, r, red) / fn;
+    }
+    if (!(rel < 1e-3)) {
+      if (threadIdx.x == 0) atomicExch(err, 2);
+      return;
+    }
+  }
+  // u = x; remove_translations(u) (src/multigrid.cpp:449-450)
+  for (int c = 0; c < 3; ++c) {
+    double p2 = 0.0;
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) p2 += x[3 * i + c];
+    const double mean = block_sum_1(p2, red) / double(nv);
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) u[c * nv + i] = TN(x[3 * i + c] - mean);
+  }
+}
+
+template <typename TN>
+void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, TN* f, TN* u,
+                           double negligible, double* work, int* err, cudaStream_t s) {
+  coarsest_kernel<TN><<<1, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, f, u, negligible, work, err);
+  IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- instantiations
+template void launch_restrict<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
+template void launch_restrict<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
+template void launch_prolong_add<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
+template void launch_prolong_add<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
+template void launch_stencil_apply<float, double>(const GridGeo&, const float*, const double*, const double*, double*, cudaStream_t);
+template void launch_stencil_apply<double, double>(const GridGeo&, const double*, const double*, const double*, double*, cudaStream_t);
+template void launch_stencil_apply<float, float>(const GridGeo&, const float*, const float*, const float*, float*, cudaStream_t);
+template void launch_stencil_gs_color<float, double>(const GridGeo&, const float*, const double*, double*, int, int*, cudaStream_t);
+template void launch_stencil_gs_color<double, double>(const GridGeo&, const double*, const double*, double*, int, int*, cudaStream_t);
+template void launch_stencil_gs_color<float, float>(const GridGeo&, const float*, const float*, float*, int, int*, cudaStream_t);
+template void launch_galerkin_from_elements<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
+template void launch_galerkin_from_elements<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
+template void launch_galerkin_from_stencil<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
+template void launch_galerkin_from_stencil<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
+template void launch_coarsest_solve<double>(int, long long, const double*, const double*, double*, double*, double, double*, int*, cudaStream_t);
+template void launch_coarsest_solve<float>(int, long long, const double*, const double*, float*, float*, double, double*, int*, cudaStream_t);
+
+}  // namespace ihomgpu

@@ -1,0 +1,191 @@
+// reduce_kernels.cu -- deterministic reductions and small vector kernels.
+//
+// The reference's block_sum (inc/parallel.hpp:38-56) is worker-count
+// independent; here the partition is a function of the problem size only
+// (fixed grid of <= kReducePartials blocks, grid-stride, fixed tree fold), so
+// results are bitwise reproducible run to run on the same device model.
+#include "kernels.hpp"
+
+namespace ihomgpu {
+
+constexpr int kRT = 256;
+
+inline int reduce_grid(long long n) {
+  long long g = (n + kRT * 8 - 1) / (kRT * 8);
+  if (g < 1) g = 1;
+  if (g > kReducePartials) g = kReducePartials;
+  return int(g);
+}
+
+__device__ __forceinline__ double block_reduce(double v, double* sh) {
+  const int t = threadIdx.x;
+  // warp level, fixed shuffle order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((t & 31) == 0) sh[t >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (t < 32) {
+    r = (t < (int)(blockDim.x >> 5)) ? sh[t] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+template <typename TN>
+__global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x, long long nv, double* partials) {
+  __shared__ double sh[32];
+  double s[3] = {0.0, 0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < nv; i += (long long)gridDim.x * kRT) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s[c] += double(x[c * nv + i]);
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double r = block_reduce(s[c], sh);
+    if (threadIdx.x == 0) partials[c * kReducePartials + blockIdx.x] = r;
+  }
+}
+
+__global__ void __launch_bounds__(kRT) finalize_kernel(const double* partials, int nparts, int ncomp, double* out) {
+  __shared__ double sh[32];
+  for (int c = 0; c < ncomp; ++c) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kRT) s += partials[c * kReducePartials + i];
+    const double r = block_reduce(s, sh);
+    if (threadIdx.x == 0) out[c] = r;
+  }
+}
+
+template <typename TN>
+void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s) {
+  const int g = reduce_grid(nv);
+  comp_sums_kernel<TN><<<g, kRT, 0, s>>>(x, nv, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 3, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+template <typename TN>
+__global__ void __launch_bounds__(kRT) dot_kernel(const TN* __restrict__ a, const TN* __restrict__ b, long long n,
+                                                  double* partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT)
+    s += double(a[i]) * double(b[i]);
+  const double r = block_reduce(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+template <typename TN>
+void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s) {
+  const int g = reduce_grid(n);
+  dot_kernel<TN><<<g, kRT, 0, s>>>(a, b, n, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+template <typename TN>
+__global__ void sub_means_kernel(TN* x, long long nv, const double* sums) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double inv = 1.0 / double(nv);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) x[c * nv + i] = TN(double(x[c * nv + i]) - sums[c] * inv);
+}
+
+template <typename TN>
+void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s) {
+  sub_means_kernel<TN><<<ceil_div(nv, 256), 256, 0, s>>>(x, nv, sums);
+  IHOM_LAUNCH_CHECK();
+}
+
+template <typename TN>
+__global__ void axpy_kernel(double* u, const TN* __restrict__ e, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) u[i] += double(e[i]);
+}
+
+template <typename TN>
+void launch_axpy_update(double* u, const TN* e, long long n, cudaStream_t s) {
+  axpy_kernel<TN><<<ceil_div(n, 256), 256, 0, s>>>(u, e, n);
+  IHOM_LAUNCH_CHECK();
+}
+
+template <typename TI, typename TO>
+__global__ void convert_kernel(const TI* __restrict__ x, TO* __restrict__ y, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = TO(x[i]);
+}
+
+template <typename TI, typename TO>
+void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s) {
+  convert_kernel<TI, TO><<<ceil_div(n, 256), 256, 0, s>>>(x, y, n);
+  IHOM_LAUNCH_CHECK();
+}
+
+template void launch_comp_sums<double>(const double*, long long, double*, double*, cudaStream_t);
+template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t);
+template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t);
+template void launch_dot<float>(const float*, const float*, long long, double*, double*, cudaStream_t);
+template void launch_sub_means<double>(double*, long long, const double*, cudaStream_t);
+template void launch_sub_means<float>(float*, long long, const double*, cudaStream_t);
+template void launch_axpy_update<float>(double*, const float*, long long, cudaStream_t);
+template void launch_axpy_update<double>(double*, const double*, long long, cudaStream_t);
+template void launch_convert<double, float>(const double*, float*, long long, cudaStream_t);
+template void launch_convert<float, double>(const float*, double*, long long, cudaStream_t);
+
+}  // namespace ihomgpu
+
+namespace ihomgpu {
+
+// AoS [nv][3] <-> SoA [3][nv] transposes for the boundary (nodal fields cross
+// the C ABI in the reference's AoS layout).
+__global__ void aos_soa_kernel(const double* __restrict__ in, double* __restrict__ out, long long nv, int to_soa) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (to_soa) out[c * nv + i] = in[3 * i + c];
+    else out[3 * i + c] = in[c * nv + i];
+  }
+}
+
+void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s) {
+  aos_soa_kernel<<<ceil_div(nv, 256), 256, 0, s>>>(in, out, nv, to_soa ? 1 : 0);
+  IHOM_LAUNCH_CHECK();
+}
+
+}  // namespace ihomgpu
+
+namespace ihomgpu {
+
+// Colour-block location of every vertex, enumerated x-fastest (bit-exact
+// check of inc/grid.hpp:73-78 and of the device neighbour arithmetic:
+// out27 (optional) receives the 27 neighbour locations of every location).
+__global__ void grid_locs_kernel(GridGeo g, long long* __restrict__ out, long long* __restrict__ out27) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.nv) return;
+  const int x = int(i % g.n[0]);
+  const long long r = i / g.n[0];
+  const int y = int(r % g.n[1]), z = int(r / g.n[1]);
+  out[i] = vloc(g, x, y, z);
+  if (out27) {
+    const int color = color_at(g, i);
+    int vx, vy, vz;
+    block_coords(g, color, (unsigned)(i - g.base[color]), vx, vy, vz);
+    Nbhd nb;
+    gather27(g, vx, vy, vz, nb);
+    for (int n = 0; n < 27; ++n) out27[27 * i + n] = nb.v[n];
+  }
+}
+
+void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s) {
+  grid_locs_kernel<<<ceil_div(g.nv, 256), 256, 0, s>>>(g, out, out27);
+  IHOM_LAUNCH_CHECK();
+}
+
+}  // namespace ihomgpu

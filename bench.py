@@ -1,0 +1,282 @@
+#!/usr/bin/env python
+"""Benchmark: seconds per optimisation iteration (BASELINE.json metric).
+
+One "step" = one full optimisation iteration of the reference loop
+(src/runner.cpp:83-131): filter+pow -> Galerkin rebuild -> 6 periodic
+unit-strain multigrid solves -> C^H -> objective -> sensitivities -> filter
+adjoint -> symmetrize -> OC bisection -> symmetrize+clamp.
+
+Default workload (N=1): BASELINE configs[3], the paper's headline size --
+negative Poisson's ratio (npr-relaxed, beta 0.8) at 512^3, vol 0.2, reference
+defaults otherwise (E=1e6, nu=0.3, p=3, spline4 r=2, reflect6, trig init seed 0,
+tol 1e-2, 50 cycles, mixed precision). Synthetic data = the reference's own
+seeded trig initialisation (no datasets needed).
+
+  value  : device-resident design (torch CUDA buffers), CUDA events on the
+           library stream around each step, max over ranks.
+  e2e    : the same step through the public API with pinned HOST buffers:
+           H2D of the design and D2H of the updated design inside the timed region.
+  The two legs are interleaved step by step so they sample the same phase of
+  the optimisation.
+
+--impl reference: the reference algorithm's CPU implementation on the host
+cores (the oracle port, oracle/; the reference itself only partly compiles here,
+see DESIGN.md), each step a bounded sample (one 64^3 iteration after 3 warm-up
+iterations, scaled by element count to the workload).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_512_NPR_S = 27.86  # PAPER.md:1308 (RTX 3090), BASELINE.md section 1
+SAMPLE_RESO = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--reso", type=int, default=512)
+    ap.add_argument("--obj", default="npr-relaxed")
+    ap.add_argument("--vol", type=float, default=0.2)
+    ap.add_argument("--mode", default="mixed_defect", choices=["vcycle", "mixed_defect"])
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "double"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(family):
+    """dram bytes per launch of `family` from the committed ncu summary (profiles/), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(family)
+    except Exception:
+        return None
+
+
+def cpu_oracle_iterations(args, threads, warm, timed):
+    """Per-iteration wall seconds of the oracle (CPU port) at SAMPLE_RESO for iterations warm..warm+timed-1."""
+    import oracle
+    oracle.set_threads(threads)
+    recs, _, _ = oracle.run(reso=SAMPLE_RESO, vol=args.vol, obj=args.obj, mixed=args.precision == "mixed",
+                            max_iter=warm + timed)
+    return [r["ms"] / 1e3 for r in recs[warm:warm + timed]]
+
+
+def scale_factor(args):
+    return (args.reso / SAMPLE_RESO) ** 3
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    secs = cpu_oracle_iterations(args, threads, args.warmup, args.steps)
+    v = statistics.mean(secs) * scale_factor(args)
+    sample = (f"oracle port (C++/OpenMP restatement of the reference loop): iterations {args.warmup}.."
+              f"{args.warmup + args.steps - 1} of {args.obj} {SAMPLE_RESO}^3 (mean {statistics.mean(secs):.3f} s), "
+              f"scaled x{scale_factor(args):.0f} by element count to {args.reso}^3")
+    line = {"impl": "reference", "metric": f"sec/opt-iteration at {args.reso}^3", "value": round(v, 3),
+            "unit": "s/iteration", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 coeff/stencil + f64 nodal (reference mixed)", "data": "synthetic (reference trig init)",
+            "config": workload(args),
+            "cpu_baseline": {"value": round(v, 3), "unit": "s/iteration", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": "s/iteration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload(args):
+    return {"workload": f"{args.obj} {args.reso}^3 vol {args.vol} (BASELINE configs[3] paper headline size)"
+            if args.reso == 512 else f"{args.obj} {args.reso}^3 vol {args.vol}",
+            "reso": args.reso, "obj": args.obj, "vol": args.vol, "precision": args.precision,
+            "solver_mode": args.mode, "filter": "spline4 r=2", "symmetry": "reflect6", "init": "trig seed 0",
+            "tol": 1e-2, "max_cycles": 50,
+            "l2": "inputs larger than L2 (each 512^3 f64 field is 1 GiB vs 126 MB L2)",
+            "parallelism": "replicas" if args.gpus > 1 else "single GPU"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2301_08911_b200 as ih
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = ih.RunConfig(reso=args.reso, vol=args.vol, obj=args.obj, max_iter=10 ** 6, precision=args.precision,
+                       solver_mode=args.mode, device=local)
+    opt = ih.Optimizer(cfg)
+    m = args.reso ** 3
+    dev_rho = torch.empty(m, dtype=torch.float64, device="cuda")
+    host_rho = torch.empty(m, dtype=torch.float64).pin_memory()
+    host_np = host_rho.numpy()
+    ext = torch.cuda.ExternalStream(opt.stream())
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        st, _ = opt.step(rho_out=dev_rho)
+        if st != 0:
+            raise RuntimeError(f"optimisation stopped during warm-up: {ih.Optimizer.STATUS[st]}")
+    clocks = ClockSampler(local)
+    clocks.start()
+    ih.profile_enable(True)
+    l0 = ih.launch_count()
+    dev_ms, e2e_ms, recs = [], [], []
+    for k in range(args.steps):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(ext)
+        st, rec = opt.step(rho_in=dev_rho, rho_out=dev_rho)
+        b.record(ext)
+        barrier()
+        dev_ms.append(a.elapsed_time(b))
+        recs.append(rec)
+        if not args.no_e2e:
+            host_np[:] = dev_rho.cpu().numpy()  # current design -> pinned host (outside the timed region)
+            barrier()
+            a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a2.record(ext)
+            st2, rec2 = opt.step(rho_in=host_np, rho_out=host_np)
+            b2.record(ext)
+            barrier()
+            e2e_ms.append(a2.elapsed_time(b2))
+            dev_rho.copy_(torch.from_numpy(host_np).to("cuda"))
+    launches = ih.launch_count() - l0
+    prof = ih.profile_totals()
+    ih.profile_enable(False)
+    clk = clocks.stop()
+
+    t_dev = statistics.mean(dev_ms) / 1e3
+    t_e2e = statistics.mean(e2e_ms) / 1e3 if e2e_ms else None
+    if world > 1:
+        t = torch.tensor([t_dev, t_e2e or 0.0], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_dev, t_e2e = float(t[0]), (float(t[1]) if e2e_ms else None)
+    if rank != 0:
+        return
+    # dominant kernel family by device time over the timed region
+    fam, ent = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    peak, peak_kind = measured_peak()
+    achieved = ent["bytes"] / (ent["ms"] * 1e-3) / 1e9 if ent["ms"] > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": fam, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                "bytes_per_launch": ent["bytes"] / max(1, ent["launches"]),
+                "avg_launch_ms": ent["ms"] / max(1, ent["launches"]),
+                "traffic": ncu_traffic(fam)}
+    total_ms = sum(e["ms"] for e in prof.values())
+    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"], "share": round(v["ms"] / total_ms, 4),
+                   "GB/s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] else None}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+    line = {"metric": f"sec/opt-iteration at {args.reso}^3", "value": round(t_dev, 4), "unit": "s/iteration",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_dev * 1e3, 2),
+            "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": round(t_dev / PAPER_512_NPR_S, 4) if args.reso == 512 and args.obj == "npr-relaxed" else None,
+            "dtype": "f32 coeff/stencil + f64 nodal (mixed); inner correction cycle f32" if args.mode == "mixed_defect"
+            else "f32 coeff/stencil + f64 nodal (mixed)",
+            "data": "synthetic (reference seeded trig init, no dataset)", "config": workload(args),
+            "roofline": roofline, "gpu_launches": launches, "clocks": clk,
+            "cycles_per_iteration": [r["cycles"] for r in recs],
+            "objective": [r["objective"] for r in recs], "kernels": kernels}
+    if t_e2e is not None:
+        line["e2e"] = {"value": round(t_e2e, 4), "unit": "s/iteration", "h2d_bytes_per_step": 8 * m,
+                       "d2h_bytes_per_step": 8 * m}
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        secs = cpu_oracle_iterations(args, threads, 3, 1)
+        line["cpu_baseline"] = {"value": round(secs[0] * scale_factor(args), 2), "unit": "s/iteration",
+                                "cores": threads, "kind": "port",
+                                "sample": f"oracle port, iteration 3 (after 3 warm-up iterations) of {args.obj} "
+                                          f"{SAMPLE_RESO}^3 ({secs[0]:.2f} s) scaled x{scale_factor(args):.0f} by "
+                                          f"element count to {args.reso}^3"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -181,6 +181,26 @@ int ihom_run_optimization(const ihom_run_config* cfg, const double* init_rho /* 
                           ihom_iter_record* records, int capacity, int* nrec, double* rho_out /* host */,
                           int* flags, ihom_observer obs, void* user);
 
+/* Stepping interface to the same loop: one optimisation iteration per call.
+   rho_in (optional) replaces the current design before the iteration; rho_out (optional)
+   receives the updated design; both live in `where` memory. status: 0 = design updated,
+   1 = solver failed, 2 = converged, 3 = last iteration (no update in cases 1-3). */
+typedef struct ihom_opt ihom_opt;
+ihom_opt* ihom_opt_create(const ihom_run_config* cfg, const double* init_rho /* host, may be null */);
+void ihom_opt_destroy(ihom_opt* opt);
+int ihom_opt_step(ihom_opt* opt, const double* rho_in, double* rho_out, int where, ihom_iter_record* rec,
+                  int* status);
+int ihom_opt_design(ihom_opt* opt, double* out, int where);
+int ihom_opt_flags(ihom_opt* opt);
+long long ihom_opt_launches(ihom_opt* opt);
+void* ihom_opt_stream(ihom_opt* opt); /* the cudaStream_t every kernel of this optimiser runs on */
+
+/* Per-kernel-family device time (CUDA events on the launching stream) and algorithmic bytes. */
+int ihom_profile_enable(int on); /* enabling resets the totals */
+int ihom_profile_count(void);
+long long ihom_launch_count(void); /* kernels launched by this library since load */
+int ihom_profile_get(int index, char* family, int cap, long long* launches, double* ms, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

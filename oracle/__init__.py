@@ -362,7 +362,7 @@ def run(reso=32, vol=0.2, obj="bulk", max_iter=5, mixed=True, tol=1e-2, max_cycl
     out = []
     for r in recs[: nrec.value]:
         out.append(dict(iter=r.iter, objective=r.objective, volume=r.volume, cycles=r.cycles,
-                        residual=r.residual, C=np.array(r.C[:]).reshape(6, 6)))
+                        residual=r.residual, ms=r.ms, C=np.array(r.C[:]).reshape(6, 6)))
     fl = flags.value
     return out, rho, dict(solver_failed=bool(fl & 1), converged=bool(fl & 2),
                           init_fallback=bool(fl & 4), oc_warning=bool(fl & 8))

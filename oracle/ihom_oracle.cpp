@@ -20,6 +20,7 @@
 // colour-block order of inc/grid.hpp:73-78, element fields x-fastest.
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -1793,6 +1794,7 @@ int orc_run(const OrcRunConfig* cfg, OrcIterRecord* records, int* nrec, double* 
           next(static_cast<size_t>(m));
       *nrec = 0;
       for (int iter = 0; iter < cfg->max_iter; ++iter) {
+        const auto t0 = std::chrono::steady_clock::now();
         // DensityExpr::eval, src/density.cpp:65-72
         if (dfilt) radial_filter(reso, rho.data(), cfg->filter_radius, cfg->kernel, pre.data());
         else pre = rho;
@@ -1809,7 +1811,7 @@ int orc_run(const OrcRunConfig* cfg, OrcIterRecord* records, int* nrec, double* 
         rec.volume = field_mean(rho.data(), m);
         rec.cycles = st.total_cycles;
         rec.residual = st.worst_residual;
-        rec.ms = 0.0;
+        rec.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         ++*nrec;
         if (!st.converged) {
           *flags |= 1;
@@ -1839,6 +1841,8 @@ int orc_run(const OrcRunConfig* cfg, OrcIterRecord* records, int* nrec, double* 
           symmetrize(rho.data(), reso, cfg->sym);
           clamp_bounds(rho);
         }
+        // full-iteration wall time (the reference's rec.ms stops after the objective, src/runner.cpp:98)
+        rec.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       }
       std::memcpy(rho_out, rho.data(), sizeof(double) * size_t(m));
     };

@@ -621,3 +621,110 @@ def hs_shear_bound(youngs, poisson, f):  # src/runner.cpp:175-179
     g = youngs / (2.0 * (1.0 + poisson))
     q = (1.0 - f) * 6.0 * (k + 2.0 * g) / (5.0 * (3.0 * k + 4.0 * g))
     return f * g / (1.0 + q)
+
+
+# ---------------------------------------------------------------- stepping optimiser + profiler
+class Optimizer:
+    """One optimisation iteration per step() (the loop body of src/runner.cpp:83-131)."""
+
+    STATUS = {0: "updated", 1: "solver_failed", 2: "converged", 3: "last_iteration"}
+
+    def __init__(self, cfg: RunConfig, init_rho=None):
+        L = lib()
+        L.ihom_opt_create.restype = C.c_void_p
+        L.ihom_opt_create.argtypes = [C.POINTER(_RunConfig), _dp]
+        L.ihom_opt_destroy.argtypes = [C.c_void_p]
+        L.ihom_opt_step.argtypes = [C.c_void_p, _dp, _dp, C.c_int, C.POINTER(_IterRecord), C.POINTER(C.c_int)]
+        L.ihom_opt_design.argtypes = [C.c_void_p, _dp, C.c_int]
+        L.ihom_opt_flags.argtypes = [C.c_void_p]
+        L.ihom_opt_launches.argtypes = [C.c_void_p]
+        L.ihom_opt_launches.restype = C.c_longlong
+        L.ihom_opt_stream.argtypes = [C.c_void_p]
+        L.ihom_opt_stream.restype = C.c_void_p
+        self.cfg = cfg
+        self.m = cfg.reso ** 3
+        self._c = cfg._c()
+        init = None if init_rho is None else np.ascontiguousarray(init_rho, dtype=np.float64).ravel()
+        self._p = L.ihom_opt_create(C.byref(self._c), init.ctypes.data_as(_dp) if init is not None else None)
+        if not self._p:
+            _raise_last()
+
+    def close(self):
+        if getattr(self, "_p", None):
+            lib().ihom_opt_destroy(C.c_void_p(self._p))
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, rho_in=None, rho_out=None):
+        """Returns (status, record). rho_in/rho_out: numpy (host) or torch CUDA float64 tensors."""
+        where = IHOM_HOST
+        pin = pout = None
+        keep = []
+        for buf in (rho_in, rho_out):
+            if buf is not None and _is_torch_cuda(buf):
+                where = IHOM_DEVICE
+        if rho_in is not None:
+            if where == IHOM_DEVICE:
+                pin = C.cast(C.c_void_p(rho_in.data_ptr()), _dp)
+            else:
+                a = rho_in if isinstance(rho_in, np.ndarray) and rho_in.flags.c_contiguous else \
+                    np.ascontiguousarray(rho_in, dtype=np.float64)
+                keep.append(a)
+                pin = a.ctypes.data_as(_dp)
+        if rho_out is not None:
+            if where == IHOM_DEVICE:
+                pout = C.cast(C.c_void_p(rho_out.data_ptr()), _dp)
+            else:
+                if not (isinstance(rho_out, np.ndarray) and rho_out.dtype == np.float64 and rho_out.flags.c_contiguous):
+                    raise ValueError("rho_out must be a contiguous float64 numpy array")
+                pout = rho_out.ctypes.data_as(_dp)
+        rec = _IterRecord()
+        st = C.c_int()
+        _check(lib().ihom_opt_step(C.c_void_p(self._p), pin, pout, where, C.byref(rec), C.byref(st)))
+        return st.value, _rec_dict(rec)
+
+    def design(self):
+        out = np.zeros(self.m)
+        _check(lib().ihom_opt_design(C.c_void_p(self._p), out.ctypes.data_as(_dp), IHOM_HOST))
+        return out
+
+    def flags(self):
+        fl = lib().ihom_opt_flags(C.c_void_p(self._p))
+        return dict(solver_failed=bool(fl & 1), converged=bool(fl & 2), init_fallback=bool(fl & 4),
+                    oc_warning=bool(fl & 8))
+
+    def kernel_launches(self) -> int:
+        return lib().ihom_opt_launches(C.c_void_p(self._p))
+
+    def stream(self) -> int:
+        return lib().ihom_opt_stream(C.c_void_p(self._p)) or 0
+
+
+def profile_enable(on: bool = True):
+    _check(lib().ihom_profile_enable(1 if on else 0))
+
+
+def launch_count() -> int:
+    """Kernels launched by libihom_b200.so since it was loaded."""
+    L = lib()
+    L.ihom_launch_count.restype = C.c_longlong
+    return L.ihom_launch_count()
+
+
+def profile_totals() -> dict:
+    """{family: {"launches", "ms", "bytes"}} of device time per kernel family since profile_enable(True)."""
+    L = lib()
+    L.ihom_profile_get.argtypes = [C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_longlong), _dp, _dp]
+    n = L.ihom_profile_count()
+    out = {}
+    for i in range(n):
+        buf = C.create_string_buffer(64)
+        cnt, ms, by = C.c_longlong(), C.c_double(), C.c_double()
+        _check(L.ihom_profile_get(i, buf, 64, C.byref(cnt), C.byref(ms), C.byref(by)))
+        out[buf.value.decode()] = dict(launches=cnt.value, ms=ms.value, bytes=by.value)
+    return out

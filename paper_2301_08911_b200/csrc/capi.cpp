@@ -4,6 +4,8 @@
 #include "../../include/ihom_b200.h"
 
 #include <chrono>
+#include <cstdio>
+#include <iterator>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -14,6 +16,7 @@
 #include "density.hpp"
 #include "hierarchy.hpp"
 #include "objective.hpp"
+#include "profiler.hpp"
 
 using namespace ihomgpu;
 
@@ -604,69 +607,112 @@ struct ConvergeChecker {  // inc/oc.hpp:35-61
   }
 };
 
+struct OptBase {
+  virtual ~OptBase() = default;
+  // status: 0 updated, 1 solver failed, 2 converged (no update), 3 last iteration (no update)
+  virtual int step(ihom_iter_record* rec) = 0;
+  virtual double* design() = 0;
+  virtual double* prev_design() = 0;
+  virtual long long count() const = 0;
+  virtual long long launches() = 0;
+  virtual cudaStream_t stream() const = 0;
+  virtual void bind() = 0;
+  int flags = 0;
+  int iter = 0;
+  bool done = false;
+};
+
+// One optimisation iteration per step(), exactly the loop body of
+// src/runner.cpp:83-131 (the loop itself is ihom_run_optimization or the
+// caller driving ihom_opt_step).
 template <typename T>
-void run_impl(const ihom_run_config& cfg, const double* init_rho, ihom_iter_record* records, int capacity, int* nrec,
-              double* rho_out, int* flags, ihom_observer obs, void* user) {
-  IHOM_CUDA(cudaSetDevice(cfg.device));
-  if (cfg.reso < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
-  if (!(cfg.vol > 0.0 && cfg.vol <= 1.0)) throw std::invalid_argument("volume fraction out of range");
-  const int n[3] = {cfg.reso, cfg.reso, cfg.reso};
-  const long long m = (long long)cfg.reso * cfg.reso * cfg.reso;
-  cudaStream_t s;
-  IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{s};
-  SolverOptions so;
-  so.tol = cfg.tol;
-  so.max_cycles = cfg.max_cycles;
-  so.mode = cfg.solver_mode;
-  // homogenizer penal = 1: the SIMP power lives in DensityExpr (src/runner.cpp:59-62)
-  Homogenizer<T> hom(n, Material{cfg.youngs, cfg.poisson}, 1.0, so, s);
-  g_bound = nullptr;  // tables now belong to this run
-  Workspace& ws = hom.hierarchy().workspace();
-  DevBuf<double> rho(static_cast<size_t>(m)), next(static_cast<size_t>(m)), pre(static_cast<size_t>(m)), phys(static_cast<size_t>(m)), grad(static_cast<size_t>(m)), tmp(static_cast<size_t>(m)),
-      gd(static_cast<size_t>(m));
-  *flags = 0;
-  if (cfg.init == 0) {  // init_constant (src/density.cpp:261-265)
-    std::vector<double> c(size_t(m), cfg.vol);
-    IHOM_CUDA(cudaMemcpyAsync(rho.p, c.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
-  } else if (cfg.init == 1) {
-    if (init_trig(n, cfg.basis_n, cfg.seed, cfg.vol, 15.0, rho.p, tmp.p, ws, s)) *flags |= 4;
-  } else {
-    if (!init_rho) throw std::invalid_argument("init from file requires init_rho");
-    IHOM_CUDA(cudaMemcpyAsync(rho.p, init_rho, sizeof(double) * m, cudaMemcpyHostToDevice, s));
-    clamp_field(rho.p, m, kRhoMin, 1.0, s);  // src/runner.cpp:38-42
-  }
-  if (cfg.sym != IHOM_SYM_NONE) {
-    symmetrize(n, rho.p, cfg.sym, tmp.p, s);
-    clamp_field(rho.p, m, kRhoMin, 1.0, s);
-  }
-  const bool dfilt = cfg.filter_placement == 0 && cfg.filter_radius >= 1.0;
+struct Optimizer : OptBase {
+  ihom_run_config cfg;
+  int n[3];
+  long long m;
+  cudaStream_t s = nullptr;
+  std::unique_ptr<Homogenizer<T>> hom;
+  DevBuf<double> rho, next, pre, phys, grad, tmp, gd;
+  bool dfilt = false;
   OCConfig oc;
-  oc.volume = cfg.vol;
-  oc.step_limit = cfg.step;
-  oc.damp = cfg.damp;
   ConvergeChecker conv;
-  std::vector<double> h_prev, h_next;
-  *nrec = 0;
-  auto mean_of = [&](const double* f) {
+
+  Optimizer(const ihom_run_config& c, const double* init_rho) : cfg(c) {
+    IHOM_CUDA(cudaSetDevice(cfg.device));
+    if (cfg.reso < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
+    if (!(cfg.vol > 0.0 && cfg.vol <= 1.0)) throw std::invalid_argument("volume fraction out of range");
+    n[0] = n[1] = n[2] = cfg.reso;
+    m = (long long)cfg.reso * cfg.reso * cfg.reso;
+    IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SolverOptions so;
+    so.tol = cfg.tol;
+    so.max_cycles = cfg.max_cycles;
+    so.mode = cfg.solver_mode;
+    // homogenizer penal = 1: the SIMP power lives in DensityExpr (src/runner.cpp:59-62)
+    hom = std::make_unique<Homogenizer<T>>(n, Material{cfg.youngs, cfg.poisson}, 1.0, so, s);
+    g_bound = this;
+    for (DevBuf<double>* b : {&rho, &next, &pre, &phys, &grad, &tmp, &gd}) b->alloc(size_t(m));
+    Workspace& ws = hom->hierarchy().workspace();
+    if (cfg.init == 0) {  // init_constant (src/density.cpp:261-265)
+      std::vector<double> v(size_t(m), cfg.vol);
+      IHOM_CUDA(cudaMemcpyAsync(rho.p, v.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+      IHOM_CUDA(cudaStreamSynchronize(s));
+    } else if (cfg.init == 1) {
+      if (init_trig(n, cfg.basis_n, cfg.seed, cfg.vol, 15.0, rho.p, tmp.p, ws, s)) flags |= 4;
+    } else {
+      if (!init_rho) throw std::invalid_argument("init from file requires init_rho");
+      IHOM_CUDA(cudaMemcpyAsync(rho.p, init_rho, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+      clamp_field(rho.p, m, kRhoMin, 1.0, s);  // src/runner.cpp:38-42
+    }
+    if (cfg.sym != IHOM_SYM_NONE) {  // src/runner.cpp:66-69
+      symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+      clamp_field(rho.p, m, kRhoMin, 1.0, s);
+    }
+    IHOM_CUDA(cudaMemcpyAsync(next.p, rho.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    dfilt = cfg.filter_placement == 0 && cfg.filter_radius >= 1.0;
+    oc.volume = cfg.vol;
+    oc.step_limit = cfg.step;
+    oc.damp = cfg.damp;
+  }
+  ~Optimizer() override {
+    hom.reset();
+    if (g_bound == this) g_bound = nullptr;
+    if (s) cudaStreamDestroy(s);
+  }
+  void bind() override {
+    IHOM_CUDA(cudaSetDevice(cfg.device));
+    if (g_bound != this) {
+      hom->hierarchy().bind_tables();
+      g_bound = this;
+    }
+  }
+  double* design() override { return rho.p; }
+  double* prev_design() override { return next.p; }
+  long long count() const override { return m; }
+  long long launches() override { return hom->hierarchy().launches(); }
+  cudaStream_t stream() const override { return s; }
+
+  double mean_of(const double* f) {
+    Workspace& ws = hom->hierarchy().workspace();
     field_sum(f, m, ws.partials, ws.scalar, s);
     double sum = 0.0;
     IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
     IHOM_CUDA(cudaStreamSynchronize(s));
     return sum / double(m);
-  };
-  for (int iter = 0; iter < cfg.max_iter; ++iter) {
+  }
+
+  int step(ihom_iter_record* out) override {
+    if (done) throw StateError("optimisation already finished");
     const auto t0 = std::chrono::steady_clock::now();
+    Workspace& ws = hom->hierarchy().workspace();
     // DensityExpr::eval (src/density.cpp:65-72)
     radial_filter(n, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s);
     pow_field(pre.p, cfg.penal, m, phys.p, s);
-    hom.set_density(phys.p);
-    const CellSolveStats st = hom.solve_cell_problems();
+    hom->set_density(phys.p);
+    const CellSolveStats st = hom->solve_cell_problems();
     ihom_iter_record rec{};
-    hom.effective_tensor(rec.C);
+    hom->effective_tensor(rec.C);
     const Expr objective = make_objective(cfg, iter);
     const double fval = objective.eval(rec.C);
     rec.iter = iter;
@@ -675,49 +721,45 @@ void run_impl(const ihom_run_config& cfg, const double* init_rho, ihom_iter_reco
     rec.cycles = st.total_cycles;
     rec.residual = st.worst_residual;
     rec.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    if (*nrec < capacity) records[(*nrec)++] = rec;
-    if (!st.converged) {
-      *flags |= 1;
-      break;
+    int status = 0;
+    if (!st.converged) {  // src/runner.cpp:105-113
+      flags |= 1;
+      status = 1;
+    } else if (conv.update(fval)) {
+      flags |= 2;
+      status = 2;
+    } else if (iter + 1 == cfg.max_iter) {
+      status = 3;
     }
-    if (conv.update(fval)) {
-      *flags |= 2;
-      break;
-    }
-    if (iter + 1 == cfg.max_iter) break;
-    double seed[36];
-    objective.backward(1.0, rec.C, seed);
-    hom.tensor_sensitivity(seed, grad.p);
-    pow_backward(pre.p, grad.p, cfg.penal, m, tmp.p, s);  // DensityExpr::backward
-    radial_filter(n, tmp.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, gd.p, s);
-    if (cfg.filter_placement == 1 && cfg.filter_radius >= 1.0) {
-      sensitivity_filter(n, gd.p, rho.p, cfg.filter_radius, tmp.p, s);
-      IHOM_CUDA(cudaMemcpyAsync(gd.p, tmp.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-    }
-    if (cfg.sym != IHOM_SYM_NONE) symmetrize(n, gd.p, cfg.sym, tmp.p, s);
-    const OCResult res = oc_update(m, rho.p, gd.p, oc, next.p, ws, s);
-    if (!res.bisection_ok) *flags |= 8;
-    std::swap(rho.p, next.p);  // prev now in next.p
-    if (cfg.sym != IHOM_SYM_NONE) {
-      symmetrize(n, rho.p, cfg.sym, tmp.p, s);
-      clamp_field(rho.p, m, kRhoMin, 1.0, s);
-    }
-    if (*nrec > 0) {
-      records[*nrec - 1].lambda = res.lambda;
-      records[*nrec - 1].oc_trials = res.trials;
-    }
-    if (obs) {
-      h_prev.resize(static_cast<size_t>(m));
-      h_next.resize(static_cast<size_t>(m));
-      IHOM_CUDA(cudaMemcpyAsync(h_prev.data(), next.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
-      IHOM_CUDA(cudaMemcpyAsync(h_next.data(), rho.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (status == 0) {
+      double seed[36];
+      objective.backward(1.0, rec.C, seed);
+      hom->tensor_sensitivity(seed, grad.p);
+      pow_backward(pre.p, grad.p, cfg.penal, m, tmp.p, s);  // DensityExpr::backward
+      radial_filter(n, tmp.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, gd.p, s);
+      if (cfg.filter_placement == 1 && cfg.filter_radius >= 1.0) {
+        sensitivity_filter(n, gd.p, rho.p, cfg.filter_radius, tmp.p, s);
+        IHOM_CUDA(cudaMemcpyAsync(gd.p, tmp.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+      }
+      if (cfg.sym != IHOM_SYM_NONE) symmetrize(n, gd.p, cfg.sym, tmp.p, s);
+      const OCResult res = oc_update(m, rho.p, gd.p, oc, next.p, ws, s);
+      if (!res.bisection_ok) flags |= 8;
+      std::swap(rho.p, next.p);  // previous design now in next.p
+      if (cfg.sym != IHOM_SYM_NONE) {
+        symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+        clamp_field(rho.p, m, kRhoMin, 1.0, s);
+      }
+      rec.lambda = res.lambda;
+      rec.oc_trials = res.trials;
       IHOM_CUDA(cudaStreamSynchronize(s));
-      if (!obs(iter, h_prev.data(), h_next.data(), &records[*nrec - 1], user)) break;
+    } else {
+      done = true;
     }
+    ++iter;
+    if (out) *out = rec;
+    return status;
   }
-  if (rho_out) IHOM_CUDA(cudaMemcpyAsync(rho_out, rho.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
-  IHOM_CUDA(cudaStreamSynchronize(s));
-}
+};
 
 }  // namespace
 
@@ -727,11 +769,109 @@ int ihom_run_optimization(const ihom_run_config* cfg, const double* init_rho, ih
                           int* nrec, double* rho_out, int* flags, ihom_observer obs, void* user) {
   return guarded([&] {
     if (!cfg) throw std::invalid_argument("null config");
-    if (cfg->precision == IHOM_ALL_DOUBLE)
-      run_impl<double>(*cfg, init_rho, records, capacity, nrec, rho_out, flags, obs, user);
-    else
-      run_impl<float>(*cfg, init_rho, records, capacity, nrec, rho_out, flags, obs, user);
+    std::unique_ptr<OptBase> o;
+    if (cfg->precision == IHOM_ALL_DOUBLE) o = std::make_unique<Optimizer<double>>(*cfg, init_rho);
+    else o = std::make_unique<Optimizer<float>>(*cfg, init_rho);
+    *nrec = 0;
+    std::vector<double> h_prev, h_next;
+    const long long m = o->count();
+    for (int it = 0; it < cfg->max_iter; ++it) {  // src/runner.cpp:83-132
+      ihom_iter_record rec{};
+      const int status = o->step(&rec);
+      if (*nrec < capacity) records[(*nrec)++] = rec;
+      if (status != 0) break;
+      if (obs) {
+        h_prev.resize(size_t(m));
+        h_next.resize(size_t(m));
+        IHOM_CUDA(cudaMemcpyAsync(h_prev.data(), o->prev_design(), sizeof(double) * m, cudaMemcpyDeviceToHost, o->stream()));
+        IHOM_CUDA(cudaMemcpyAsync(h_next.data(), o->design(), sizeof(double) * m, cudaMemcpyDeviceToHost, o->stream()));
+        IHOM_CUDA(cudaStreamSynchronize(o->stream()));
+        if (!obs(it, h_prev.data(), h_next.data(), &rec, user)) break;
+      }
+    }
+    if (rho_out) {
+      IHOM_CUDA(cudaMemcpyAsync(rho_out, o->design(), sizeof(double) * m, cudaMemcpyDeviceToHost, o->stream()));
+      IHOM_CUDA(cudaStreamSynchronize(o->stream()));
+    }
+    *flags = o->flags;
   });
+}
+
+struct ihom_opt {
+  std::unique_ptr<OptBase> o;
+};
+
+ihom_opt* ihom_opt_create(const ihom_run_config* cfg, const double* init_rho) {
+  ihom_opt* out = nullptr;
+  const int rc = guarded([&] {
+    if (!cfg) throw std::invalid_argument("null config");
+    auto h = std::make_unique<ihom_opt>();
+    if (cfg->precision == IHOM_ALL_DOUBLE) h->o = std::make_unique<Optimizer<double>>(*cfg, init_rho);
+    else h->o = std::make_unique<Optimizer<float>>(*cfg, init_rho);
+    out = h.release();
+  });
+  return rc == IHOM_OK ? out : nullptr;
+}
+
+void ihom_opt_destroy(ihom_opt* h) { delete h; }
+
+int ihom_opt_step(ihom_opt* h, const double* rho_in, double* rho_out, int where, ihom_iter_record* rec, int* status) {
+  return guarded([&] {
+    OptBase& o = *h->o;
+    o.bind();
+    const long long m = o.count();
+    const cudaMemcpyKind kin = where == IHOM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (rho_in) IHOM_CUDA(cudaMemcpyAsync(o.design(), rho_in, sizeof(double) * m, kin, o.stream()));
+    const int st = o.step(rec);
+    if (status) *status = st;
+    if (rho_out) {
+      const cudaMemcpyKind kout = where == IHOM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      IHOM_CUDA(cudaMemcpyAsync(rho_out, o.design(), sizeof(double) * m, kout, o.stream()));
+    }
+    IHOM_CUDA(cudaStreamSynchronize(o.stream()));
+  });
+}
+
+int ihom_opt_design(ihom_opt* h, double* out, int where) {
+  return guarded([&] {
+    OptBase& o = *h->o;
+    const cudaMemcpyKind k = where == IHOM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    IHOM_CUDA(cudaMemcpyAsync(out, o.design(), sizeof(double) * o.count(), k, o.stream()));
+    IHOM_CUDA(cudaStreamSynchronize(o.stream()));
+  });
+}
+
+int ihom_opt_flags(ihom_opt* h) { return h->o->flags; }
+long long ihom_opt_launches(ihom_opt* h) { return h->o->launches(); }
+void* ihom_opt_stream(ihom_opt* h) { return (void*)h->o->stream(); }
+
+int ihom_profile_enable(int on) {
+  return guarded([&] {
+    Profiler::get().enable(on != 0);
+    if (on) Profiler::get().reset();
+  });
+}
+
+int ihom_profile_get(int index, char* family, int cap, long long* launches, double* ms, double* bytes) {
+  int rc = guarded([&] {
+    const auto& t = Profiler::get().totals();
+    if (index < 0 || index >= (int)t.size()) throw std::invalid_argument("profile index out of range");
+    auto it = t.begin();
+    std::advance(it, index);
+    std::snprintf(family, size_t(cap), "%s", it->first.c_str());
+    *launches = it->second.launches;
+    *ms = it->second.ms;
+    *bytes = it->second.bytes;
+  });
+  return rc;
+}
+
+long long ihom_launch_count(void) { return launch_counter(); }
+
+int ihom_profile_count(void) {
+  int n = 0;
+  guarded([&] { n = (int)Profiler::get().totals().size(); });
+  return n;
 }
 
 }  // extern "C"

@@ -36,7 +36,17 @@ struct StateError : std::logic_error {
                                  __FILE__ + ":" + std::to_string(__LINE__));                   \
   } while (0)
 
-#define IHOM_LAUNCH_CHECK() IHOM_CUDA(cudaGetLastError())
+// Every kernel launch is followed by IHOM_LAUNCH_CHECK(); it also counts launches
+// (reported to the bench as gpu_launches).
+inline long long& launch_counter() {
+  static long long c = 0;
+  return c;
+}
+#define IHOM_LAUNCH_CHECK()           \
+  do {                                \
+    ++::ihomgpu::launch_counter();    \
+    IHOM_CUDA(cudaGetLastError());    \
+  } while (0)
 
 // Geometry of one periodic grid level (inc/grid.hpp:18-56), passed by value.
 struct GridGeo {

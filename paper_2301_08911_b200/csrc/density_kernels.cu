@@ -7,6 +7,7 @@
 // Element fields are f64, x-fastest.
 #include "density.hpp"
 #include "kernels.hpp"
+#include "profiler.hpp"
 
 #include <cmath>
 #include <vector>
@@ -95,6 +96,7 @@ void radial_filter(const int n[3], const double* f, double radius, int kernel, d
   }
   const auto taps = make_taps(radius, kernel, true, nullptr);
   upload_taps(taps, s);
+  ProfScope p(s, "filter", double(m) * 16.0);
   filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), f, nullptr, 1.0, 0, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -109,6 +111,7 @@ void sensitivity_filter(const int n[3], const double* sens, const double* rho, d
   double wsum = 0.0;
   const auto taps = make_taps(radius, 0, false, &wsum);
   upload_taps(taps, s);
+  ProfScope p(s, "filter", double(m) * 24.0);
   filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), sens, rho, wsum, 1, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -122,11 +125,13 @@ __global__ void pow_kernel(const double* __restrict__ x, const double* __restric
 }
 
 void pow_field(const double* x, double p, long long m, double* out, cudaStream_t s) {
+  ProfScope ps(s, "pow", double(m) * 16.0);
   pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, nullptr, p, m, out);
   IHOM_LAUNCH_CHECK();
 }
 
 void pow_backward(const double* x, const double* g, double p, long long m, double* out, cudaStream_t s) {
+  ProfScope ps(s, "pow", double(m) * 24.0);
   pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, g, p, m, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -204,7 +209,10 @@ void symmetrize(const int n[3], double* field, int sym, double* scratch, cudaStr
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
   const long long m = (long long)n[0] * n[1] * n[2];
   IHOM_CUDA(cudaMemcpyAsync(scratch, field, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-  symmetrize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], nops, scratch, field);
+  {
+    ProfScope p(s, "symmetrize", double(m) * 16.0);
+    symmetrize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], nops, scratch, field);
+  }
   IHOM_LAUNCH_CHECK();
   IHOM_CUDA(cudaStreamSynchronize(s));  // constant staging buffers are static
 }
@@ -215,6 +223,7 @@ __global__ void clamp_kernel(double* f, long long m, double lo, double hi) {
 }
 
 void clamp_field(double* f, long long m, double lo, double hi, cudaStream_t s) {
+  ProfScope p(s, "vector", double(m) * 16.0);
   clamp_kernel<<<ceil_div(m, 256), 256, 0, s>>>(f, m, lo, hi);
   IHOM_LAUNCH_CHECK();
 }
@@ -269,6 +278,7 @@ __global__ void sum_kernel(const double* __restrict__ f, long long m, double* pa
 
 void field_sum(const double* f, long long m, double* partials, double* out, cudaStream_t s) {
   const int g = dgrid(m);
+  ProfScope p(s, "reduce", double(m) * 8.0);
   sum_kernel<<<g, kDT, 0, s>>>(f, m, partials);
   IHOM_LAUNCH_CHECK();
   finalize_d<<<1, kDT, 0, s>>>(partials, g, false, out);
@@ -335,6 +345,7 @@ OCResult oc_update(long long m, const double* rho, const double* g, const OCConf
   // keep the scale on device in ws.scalar (read by every trial)
   const OCParams p{cfg.damp, cfg.step_limit, cfg.min_density, 1.0};
   auto trial = [&](double lambda, bool write) {
+    ProfScope pt(s, "oc_trial", double(m) * (write ? 24.0 : 16.0));
     oc_trial_kernel<<<grid, kDT, 0, s>>>(rho, g, m, ws.scalar, lambda, p, ws.partials, write ? out : nullptr);
     IHOM_LAUNCH_CHECK();
     finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);

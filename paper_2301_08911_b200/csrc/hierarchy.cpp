@@ -2,6 +2,8 @@
 // the homogenizer (src/multigrid.cpp:245-501, src/homogenization.cpp:16-144).
 #include "hierarchy.hpp"
 
+#include "profiler.hpp"
+
 #include <cmath>
 #include <cstring>
 #include <type_traits>
@@ -86,6 +88,21 @@ std::vector<double> spd_inverse(std::vector<double> a, int N) {
   return inv;
 }
 
+// Algorithmic bytes, sN = nodal bytes, sC = coefficient/stencil bytes.
+double gs_l0_bytes(const GridGeo& g, int c, double sN, double sC) {
+  // other colours' u (7/8 of 3 comps) + all element coefficients + f_c read + u_c write
+  return double(g.nv) * (7.0 / 8.0 * 3.0 * sN + sC) + double(g.size[c]) * 6.0 * sN;
+}
+double gs_coarse_bytes(const GridGeo& g, int c, double sN, double sC) {
+  return double(g.size[c]) * (243.0 * sC + 6.0 * sN) + double(g.nv - g.size[c]) * 3.0 * sN;
+}
+double resid_l0_bytes(const GridGeo& g, double sN, double sC, bool with_f) {
+  return double(g.nv) * ((with_f ? 9.0 : 6.0) * sN + sC);
+}
+double resid_coarse_bytes(const GridGeo& g, double sN, double sC, bool with_f) {
+  return double(g.nv) * (243.0 * sC + (with_f ? 9.0 : 6.0) * sN);
+}
+
 bool can_coarsen(const GridGeo& g) {  // inc/grid.hpp:47-51
   for (int k = 0; k < 3; ++k)
     if (g.n[k] % 2 != 0 || g.n[k] / 2 < 4) return false;
@@ -147,11 +164,21 @@ void Hierarchy<T>::bind_tables() {
 template <typename T>
 void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-279
   const GridGeo& g0 = levels_[0].g;
-  launch_coeff<T>(rho, coeff_.p, g0.nv, penal_, s_);
+  {
+    ProfScope p(s_, "coeff", double(g0.nv) * (8.0 + sizeof(T)));
+    launch_coeff<T>(rho, coeff_.p, g0.nv, penal_, s_);
+  }
+  launches_ += 1;
   if (levels_.size() > 1) {
-    launch_galerkin_from_elements<T>(g0, levels_[1].g, coeff_.p, levels_[1].st.p, s_);
-    for (size_t l = 2; l < levels_.size(); ++l)
+    {
+      ProfScope p(s_, "galerkin_l1", double(g0.nv) * sizeof(T) + double(levels_[1].g.nv) * 243.0 * sizeof(T));
+      launch_galerkin_from_elements<T>(g0, levels_[1].g, coeff_.p, levels_[1].st.p, s_);
+    }
+    for (size_t l = 2; l < levels_.size(); ++l) {
+      ProfScope p(s_, "galerkin_coarse", double(levels_[l - 1].g.nv + levels_[l].g.nv) * 243.0 * sizeof(T));
       launch_galerkin_from_stencil<T>(levels_[l - 1].g, levels_[l].g, levels_[l - 1].st.p, levels_[l].st.p, s_);
+    }
+    launches_ += (long long)levels_.size() - 1;
   }
   factor_coarsest();
   density_set_ = true;
@@ -211,14 +238,23 @@ void Hierarchy<T>::check_error(const char* where) {
 template <typename T>
 void Hierarchy<T>::remove_translations(double* f, int l) {  // src/multigrid.cpp:81-86
   const long long nv = levels_[size_t(l)].g.nv;
-  launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
-  launch_sub_means<double>(f, nv, ws_.scalars, s_);
+  {
+    ProfScope p(s_, "reduce", double(nv) * 24.0);
+    launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
+  }
+  {
+    ProfScope p(s_, "vector", double(nv) * 48.0);
+    launch_sub_means<double>(f, nv, ws_.scalars, s_);
+  }
   launches_ += 3;
 }
 
 template <typename T>
 double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:88-94
-  launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_);
+  {
+    ProfScope p(s_, "reduce", double(n) * 8.0);
+    launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_);
+  }
   launches_ += 2;
   IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
@@ -228,8 +264,13 @@ double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:
 template <typename T>
 void Hierarchy<T>::apply(int l, const double* x, double* y) {  // src/multigrid.cpp:392-398
   const Level& L = levels_[size_t(l)];
-  if (l == 0) launch_l0_apply<T, double, double>(L.g, coeff_.p, x, nullptr, y, s_);
-  else launch_stencil_apply<T, double>(L.g, L.st.p, x, nullptr, y, s_);
+  if (l == 0) {
+    ProfScope p(s_, "l0_apply", resid_l0_bytes(L.g, 8, sizeof(T), false));
+    launch_l0_apply<T, double, double>(L.g, coeff_.p, x, nullptr, y, s_);
+  } else {
+    ProfScope p(s_, "coarse_apply", resid_coarse_bytes(L.g, 8, sizeof(T), false));
+    launch_stencil_apply<T, double>(L.g, L.st.p, x, nullptr, y, s_);
+  }
   ++launches_;
 }
 
@@ -240,8 +281,13 @@ void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
-      if (l == 0) launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_);
-      else launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_);
+      if (l == 0) {
+        ProfScope p(s_, "l0_gs_f64", gs_l0_bytes(L.g, c, 8, sizeof(T)));
+        launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_);
+      } else {
+        ProfScope p(s_, l == 1 ? "l1_gs_f64" : "coarse_gs_f64", gs_coarse_bytes(L.g, c, 8, sizeof(T)));
+        launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_);
+      }
       ++launches_;
     }
 }
@@ -249,8 +295,13 @@ void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
 template <typename T>
 void Hierarchy<T>::compute_residual(int l) {  // src/multigrid.cpp:410-424
   Level& L = levels_[size_t(l)];
-  if (l == 0) launch_l0_apply<T, double, double>(L.g, coeff_.p, level_u(0), L.f.p, L.r.p, s_);
-  else launch_stencil_apply<T, double>(L.g, L.st.p, L.u.p, L.f.p, L.r.p, s_);
+  if (l == 0) {
+    ProfScope p(s_, "l0_residual_f64", resid_l0_bytes(L.g, 8, sizeof(T), true));
+    launch_l0_apply<T, double, double>(L.g, coeff_.p, level_u(0), L.f.p, L.r.p, s_);
+  } else {
+    ProfScope p(s_, l == 1 ? "l1_residual_f64" : "coarse_residual_f64", resid_coarse_bytes(L.g, 8, sizeof(T), true));
+    launch_stencil_apply<T, double>(L.g, L.st.p, L.u.p, L.f.p, L.r.p, s_);
+  }
   ++launches_;
 }
 
@@ -258,6 +309,7 @@ template <typename T>
 void Hierarchy<T>::coarsest_solve() {  // src/multigrid.cpp:426-451
   const int lc = num_levels() - 1;
   Level& L = levels_[size_t(lc)];
+  ProfScope p(s_, "coarsest", 0.0);
   launch_coarsest_solve<double>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.f.p, level_u(lc), negligible_load(ndof_c_),
                                 cwork_.p, err_.p, s_);
   ++launches_;
@@ -272,14 +324,21 @@ double Hierarchy<T>::v_cycle(const SolverOptions& opts) {  // src/multigrid.cpp:
     if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].u.p, 0, sizeof(double) * 3 * levels_[size_t(l)].g.nv, s_));
     relax(l, opts.pre_sweeps);
     compute_residual(l);
-    launch_restrict<double>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].r.p,
-                            levels_[size_t(l + 1)].f.p, s_);
+    {
+      ProfScope p(s_, "restrict", double(levels_[size_t(l)].g.nv) * 27.0);
+      launch_restrict<double>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].r.p,
+                              levels_[size_t(l + 1)].f.p, s_);
+    }
     ++launches_;
   }
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].u.p, 0, sizeof(double) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_solve();
   for (int l = lmax - 1; l >= 0; --l) {
-    launch_prolong_add<double>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].u.p, level_u(l), s_);
+    {
+      ProfScope p(s_, "prolong", double(levels_[size_t(l)].g.nv) * 51.0);
+      launch_prolong_add<double>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].u.p,
+                                 level_u(l), s_);
+    }
     ++launches_;
     relax(l, opts.post_sweeps);
   }
@@ -312,8 +371,13 @@ void Hierarchy<T>::relax_f32(int l, int sweeps) {
     for (int sw = 0; sw < sweeps; ++sw)
       for (int c = 0; c < 8; ++c) {
         if (L.g.size[c] == 0) continue;
-        if (l == 0) launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_);
-        else launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_);
+        if (l == 0) {
+          ProfScope p(s_, "l0_gs_f32", gs_l0_bytes(L.g, c, 4, 4));
+          launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_);
+        } else {
+          ProfScope p(s_, l == 1 ? "l1_gs_f32" : "coarse_gs_f32", gs_coarse_bytes(L.g, c, 4, 4));
+          launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_);
+        }
         ++launches_;
       }
   }
@@ -323,8 +387,13 @@ template <typename T>
 void Hierarchy<T>::residual_f32(int l) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
-    if (l == 0) launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_);
-    else launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_);
+    if (l == 0) {
+      ProfScope p(s_, "l0_residual_f32", resid_l0_bytes(L.g, 4, 4, true));
+      launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_);
+    } else {
+      ProfScope p(s_, l == 1 ? "l1_residual_f32" : "coarse_residual_f32", resid_coarse_bytes(L.g, 4, 4, true));
+      launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_);
+    }
     ++launches_;
   }
 }
@@ -333,6 +402,7 @@ template <typename T>
 void Hierarchy<T>::coarsest_f32() {
   const int lc = num_levels() - 1;
   Level& L = levels_[size_t(lc)];
+  ProfScope p(s_, "coarsest", 0.0);
   launch_coarsest_solve<float>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.ef.p, L.eu.p, 0.0, cwork_.p, err_.p, s_);
   ++launches_;
 }
@@ -346,26 +416,38 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
   // inner right-hand side: the current outer residual. Inside solve() it is
   // current (computed before the loop and at the end of every cycle).
   if (!u0_bound_) compute_residual(0);
-  launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+  {
+    ProfScope p(s_, "vector", double(n0) * 12.0);
+    launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+  }
   IHOM_CUDA(cudaMemsetAsync(L0.eu.p, 0, sizeof(float) * n0, s_));
   launches_ += 1;
   for (int l = 0; l < lmax; ++l) {
     if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
     relax_f32(l, opts.pre_sweeps);
     residual_f32(l);
-    launch_restrict<float>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].er.p,
-                           levels_[size_t(l + 1)].ef.p, s_);
+    {
+      ProfScope p(s_, "restrict", double(levels_[size_t(l)].g.nv) * 13.5);
+      launch_restrict<float>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].er.p,
+                             levels_[size_t(l + 1)].ef.p, s_);
+    }
     ++launches_;
   }
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_f32();
   for (int l = lmax - 1; l >= 0; --l) {
-    launch_prolong_add<float>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].eu.p,
-                              levels_[size_t(l)].eu.p, s_);
+    {
+      ProfScope p(s_, "prolong", double(levels_[size_t(l)].g.nv) * 25.5);
+      launch_prolong_add<float>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].eu.p,
+                                levels_[size_t(l)].eu.p, s_);
+    }
     ++launches_;
     relax_f32(l, opts.post_sweeps);
   }
-  launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
+  {
+    ProfScope p(s_, "vector", double(n0) * 20.0);
+    launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
+  }
   ++launches_;
   compute_residual(0);
   const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(L0.f.p, n0);
@@ -434,7 +516,10 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   CellSolveStats out;
   const GridGeo& g = hier_.geo(0);
   for (int i = 0; i < 6; ++i) {
-    launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream());
+    {
+      ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
+      launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream());
+    }
     const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_);
     out.total_cycles += s.cycles;
     if (s.rel_residual >= out.worst_residual) {
@@ -452,8 +537,11 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
   for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
   Workspace& ws = hier_.workspace();
   const Material& m = hier_.material();
-  launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
-                                  ws.partials, ws.scalars + 16, hier_.stream());
+  {
+    ProfScope p(hier_.stream(), "tensor", double(hier_.geo(0).nv) * 152.0);
+    launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
+                                    ws.partials, ws.scalars + 16, hier_.stream());
+  }
   double c21[21];
   IHOM_CUDA(cudaMemcpyAsync(c21, ws.scalars + 16, sizeof(c21), cudaMemcpyDeviceToHost, hier_.stream()));
   IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
@@ -475,8 +563,11 @@ void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  /
   const double* u[6];
   for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
   const Material& m = hier_.material();
-  launch_tensor_sensitivity<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
-                                    seed_.p, out, hier_.stream());
+  {
+    ProfScope p(hier_.stream(), "sensitivity", double(hier_.geo(0).nv) * 160.0);
+    launch_tensor_sensitivity<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
+                                      seed_.p, out, hier_.stream());
+  }
   IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
 }
 

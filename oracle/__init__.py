@@ -151,7 +151,7 @@ def fem_tables(E=1.0, nu=0.3):
 
 
 def _n3(n):
-    return (n, n, n) if np.isscalar(n) else tuple(n)
+    return (int(n),) * 3 if np.isscalar(n) else tuple(int(v) for v in n)
 
 
 def fem(n, which, coeff, u=None, f=None, E=1e6, nu=0.3, mixed=False, load=0):

@@ -199,6 +199,9 @@ void* ihom_opt_stream(ihom_opt* opt); /* the cudaStream_t every kernel of this o
 int ihom_profile_enable(int on); /* enabling resets the totals */
 int ihom_profile_count(void);
 long long ihom_launch_count(void); /* kernels launched by this library since load */
+/* Runs one kernel family `reps` times on the context's current data (isolated timing / ncu target):
+   l0_gs_f64|f32, l0_residual_f64|f32, l1_gs_*, l1_residual_*, vcycle_f64|f32, set_density, tensor, sensitivity. */
+int ihom_bench_op(ihom_ctx* ctx, const char* op, int reps);
 int ihom_profile_get(int index, char* family, int cap, long long* launches, double* ms, double* bytes);
 
 #ifdef __cplusplus

@@ -297,6 +297,10 @@ class Hierarchy:
     def kernel_launches(self) -> int:
         return lib().ihom_kernel_launches(self._ctx())
 
+    def bench_op(self, op: str, reps: int = 1):
+        """Runs one kernel family reps times (see ihom_bench_op); time it with profile_enable/profile_totals."""
+        _check(lib().ihom_bench_op(self._ctx(), op.encode(), int(reps)))
+
 
 class Homogenizer:
     """Device twin of ihom::Homogenizer<T> (inc/homogenization.hpp:26-51).

@@ -380,11 +380,11 @@ int ihom_get_stencil(ihom_ctx* ctx, int l, double* out) {
       auto& H = h.hierarchy();
       if (l < 1 || l >= H.num_levels()) throw std::invalid_argument("level has no assembled stencil");
       const long long nv = H.geo(l).nv;
-      std::vector<T> st(size_t(243 * nv));
+      std::vector<T> st(stencil_alloc(nv));
       IHOM_CUDA(cudaMemcpyAsync(st.data(), H.stencil(l), sizeof(T) * st.size(), cudaMemcpyDeviceToHost, ctx->s));
       IHOM_CUDA(cudaStreamSynchronize(ctx->s));
       for (long long v = 0; v < nv; ++v)
-        for (int k = 0; k < 243; ++k) out[v * 243 + k] = double(st[size_t(k * nv + v)]);
+        for (int k = 0; k < 243; ++k) out[v * 243 + k] = double(st[st_index(k, (unsigned)v)]);
     });
   });
 }
@@ -867,6 +867,29 @@ int ihom_profile_get(int index, char* family, int cap, long long* launches, doub
 }
 
 long long ihom_launch_count(void) { return launch_counter(); }
+
+int ihom_bench_op(ihom_ctx* ctx, const char* op, int reps) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      const std::string o(op);
+      if (o == "tensor" || o == "sensitivity") {
+        for (int r = 0; r < reps; ++r) {
+          if (o == "tensor") {
+            double C[36];
+            h.effective_tensor(C);
+          } else {
+            double seed[36] = {};
+            for (int i = 0; i < 6; ++i) seed[i * 6 + i] = 1.0;
+            DevBuf<double> out(static_cast<size_t>(ctx->nv()));
+            h.tensor_sensitivity(seed, out.p);
+          }
+        }
+      } else {
+        h.hierarchy().bench_op(o, reps);
+      }
+    });
+  });
+}
 
 int ihom_profile_count(void) {
   int n = 0;

@@ -5,8 +5,9 @@
 //     [hz][hy][hx] block of halved coordinates, x fastest;
 //   * nodal fields are SoA f64: comp c of vertex loc at p[c*nv + loc];
 //   * element fields are x-fastest, eidx = x + n0*(y + n1*z);
-//   * coarse stencils are SoA [27*9][nv] in T (f32 mixed / f64 all-double),
-//     entry (n, r, c) of vertex loc at st[(9*n + 3*r + c)*nv + loc]
+//   * coarse stencils are blocked SoA [nv/32][243][32] in T (f32 mixed / f64
+//     all-double): entry k = 9*n + 3*r + c of vertex loc at st_index(k, loc),
+//     so a warp's 243 coefficient streams form one contiguous block
 //     (n = 27-neighbour index x-fastest, inc/fem.hpp:30-35).
 #pragma once
 
@@ -148,39 +149,56 @@ __host__ __device__ constexpr int pair_ngb(int ke, int j) {
   return ((ke & 1) + (j & 1)) + 3 * (((ke >> 1) & 1) + ((j >> 1) & 1)) + 9 * (((ke >> 2) & 1) + ((j >> 2) & 1));
 }
 
-// Partial-pivoting 3x3 solve, src/fem.cpp:72-94.
-__device__ __forceinline__ void solve3(const double m[9], const double rhs[3], double out[3]) {
-  double a[9];
+// Partial-pivoting 3x3 solve, src/fem.cpp:72-94: same elimination order and
+// pivot choice (first strictly larger |a| wins), written with register row
+// swaps instead of an index array so nothing spills to local memory.
+__device__ __forceinline__ void swap_rows(double* a, double* b, double& ra, double& rb, bool doit) {
 #pragma unroll
-  for (int i = 0; i < 9; ++i) a[i] = m[i];
-  double b[3] = {rhs[0], rhs[1], rhs[2]};
-  int piv[3] = {0, 1, 2};
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    int best = c;
-#pragma unroll
-    for (int r = c + 1; r < 3; ++r)
-      if (fabs(a[3 * piv[r] + c]) > fabs(a[3 * piv[best] + c])) best = r;
-    const int tmp = piv[c];
-    piv[c] = piv[best];
-    piv[best] = tmp;
-    const double d = a[3 * piv[c] + c];
-#pragma unroll
-    for (int r = c + 1; r < 3; ++r) {
-      const double fac = a[3 * piv[r] + c] / d;
-#pragma unroll
-      for (int cc = c; cc < 3; ++cc) a[3 * piv[r] + cc] -= fac * a[3 * piv[c] + cc];
-      b[piv[r]] -= fac * b[piv[c]];
-    }
+  for (int k = 0; k < 3; ++k) {
+    const double t = a[k];
+    a[k] = doit ? b[k] : a[k];
+    b[k] = doit ? t : b[k];
   }
-#pragma unroll
-  for (int c = 2; c >= 0; --c) {
-    double s = b[piv[c]];
-#pragma unroll
-    for (int cc = c + 1; cc < 3; ++cc) s -= a[3 * piv[c] + cc] * out[cc];
-    out[c] = s / a[3 * piv[c] + c];
-  }
+  const double t = ra;
+  ra = doit ? rb : ra;
+  rb = doit ? t : rb;
 }
+
+__device__ __forceinline__ void solve3(const double m[9], const double rhs[3], double out[3]) {
+  double r0[3] = {m[0], m[1], m[2]}, r1[3] = {m[3], m[4], m[5]}, r2[3] = {m[6], m[7], m[8]};
+  double b0 = rhs[0], b1 = rhs[1], b2 = rhs[2];
+  {  // column 0: pivot row = first strictly largest |a_r0| (swap(piv[0], piv[best]))
+    const bool s1 = fabs(r1[0]) > fabs(r0[0]);
+    const bool s2 = fabs(r2[0]) > (s1 ? fabs(r1[0]) : fabs(r0[0]));
+    swap_rows(r0, r2, b0, b2, s2);
+    swap_rows(r0, r1, b0, b1, s1 && !s2);
+  }
+  {
+    const double f1 = r1[0] / r0[0];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r1[k] -= f1 * r0[k];
+    b1 -= f1 * b0;
+    const double f2 = r2[0] / r0[0];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r2[k] -= f2 * r0[k];
+    b2 -= f2 * b0;
+  }
+  swap_rows(r1, r2, b1, b2, fabs(r2[1]) > fabs(r1[1]));
+  {
+    const double f2 = r2[1] / r1[1];
+#pragma unroll
+    for (int k = 1; k < 3; ++k) r2[k] -= f2 * r1[k];
+    b2 -= f2 * b1;
+  }
+  out[2] = b2 / r2[2];
+  out[1] = (b1 - r1[2] * out[2]) / r1[1];
+  out[0] = (b0 - r0[1] * out[1] - r0[2] * out[2]) / r0[0];
+}
+
+__host__ __device__ __forceinline__ size_t st_index(int k, unsigned loc) {
+  return ((size_t)(loc >> 5) * 243 + (size_t)k) * 32 + (loc & 31u);
+}
+inline size_t stencil_alloc(long long nv) { return (size_t)((nv + 31) / 32) * 32 * 243; }
 
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 

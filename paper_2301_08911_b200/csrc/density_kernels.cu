@@ -199,15 +199,107 @@ __global__ void symmetrize_kernel(int nx, int ny, int nz, int nops, const double
   out[i] = s * (1.0 / double(nops));
 }
 
+// reflect3 / first half of reflect6: average over the 8 axis flips. One thread
+// per element of the octant [0, ceil(n/2))^3 reads the 8 mirror images once and
+// writes the average to all of them (the result is flip-invariant).
+__global__ void flip_avg_kernel(int nx, int ny, int nz, const double* __restrict__ in, double* __restrict__ out) {
+  const int hx = (nx + 1) / 2, hy = (ny + 1) / 2, hz = (nz + 1) / 2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)hx * hy * hz) return;
+  const int x = int(i % hx);
+  const long long r = i / hx;
+  const int y = int(r % hy), z = int(r / hy);
+  const int xs[2] = {x, nx - 1 - x}, ys[2] = {y, ny - 1 - y}, zs[2] = {z, nz - 1 - z};
+  double sum = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m)  // reference op order within one permutation: m = fx | fy<<1 | fz<<2
+    sum += in[xs[m & 1] + (long long)nx * (ys[(m >> 1) & 1] + (long long)ny * zs[(m >> 2) & 1])];
+  const double v = sum * 0.125;
+#pragma unroll
+  for (int m = 0; m < 8; ++m)
+    out[xs[m & 1] + (long long)nx * (ys[(m >> 1) & 1] + (long long)ny * zs[(m >> 2) & 1])] = v;
+}
+
+// Second half of reflect6: average over the 6 axis permutations on a cubic grid,
+// tiled 8^3. A CTA owns an orbit representative tile B (bx <= by <= bz), stages
+// the 6 permuted source tiles in shared memory (coalesced 64-byte rows), averages,
+// and writes the (permutation-invariant) result to all 6 image tiles.
+constexpr int kPT = 8;
+__global__ void __launch_bounds__(512) perm_avg_kernel(int n, const double* __restrict__ in, double* __restrict__ out) {
+  __shared__ double tile[6][kPT * kPT * kPT];
+  __shared__ double avg[kPT * kPT * kPT];
+  const int nt = n / kPT;
+  // decode the representative tile from blockIdx.x over all (bx,by,bz) with bx<=by<=bz
+  int b[3];
+  {
+    int k = blockIdx.x, bz = 0;
+    while (k >= (bz + 1) * (bz + 2) / 2) {
+      k -= (bz + 1) * (bz + 2) / 2;
+      ++bz;
+    }
+    int by = 0;
+    while (k >= by + 1) {
+      k -= by + 1;
+      ++by;
+    }
+    b[0] = k;
+    b[1] = by;
+    b[2] = bz;
+  }
+  if (b[2] >= nt) return;
+  const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  const int t = threadIdx.x;
+  const int l[3] = {t % kPT, (t / kPT) % kPT, t / (kPT * kPT)};
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {  // source tile p(B), element l (x fastest): coalesced rows
+    const int sb[3] = {b[perm[p][0]], b[perm[p][1]], b[perm[p][2]]};
+    tile[p][t] = in[(sb[0] * kPT + l[0]) + (long long)n * ((sb[1] * kPT + l[1]) + (long long)n * (sb[2] * kPT + l[2]))];
+  }
+  __syncthreads();
+  double sum = 0.0;
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {  // image of e = (B, l) under p lies in tile p(B) at local (l[p0], l[p1], l[p2])
+    const int a = l[perm[p][0]], bb = l[perm[p][1]], c = l[perm[p][2]];
+    sum += tile[p][a + kPT * (bb + kPT * c)];
+  }
+  avg[t] = sum * (1.0 / 6.0);
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {  // out at p(e) = avg(e): thread writes image-tile element (a,b,c) = t
+    const int sb[3] = {b[perm[p][0]], b[perm[p][1]], b[perm[p][2]]};
+    int e[3];
+    e[perm[p][0]] = l[0];
+    e[perm[p][1]] = l[1];
+    e[perm[p][2]] = l[2];
+    out[(sb[0] * kPT + l[0]) + (long long)n * ((sb[1] * kPT + l[1]) + (long long)n * (sb[2] * kPT + l[2]))] =
+        avg[e[0] + kPT * (e[1] + kPT * e[2])];
+  }
+}
+
 void symmetrize(const int n[3], double* field, int sym, double* scratch, cudaStream_t s) {
   if (sym == 0) return;
   if (sym != 1 && (n[0] != n[1] || n[1] != n[2]))
     throw std::invalid_argument("reflect6/rotate3 symmetry requires a cubic grid");
+  const long long m = (long long)n[0] * n[1] * n[2];
+  if (sym == 1 || (sym == 2 && n[0] % kPT == 0)) {  // factored fast path (src/density.cpp:100-150 group)
+    const long long oct = (long long)((n[0] + 1) / 2) * ((n[1] + 1) / 2) * ((n[2] + 1) / 2);
+    ProfScope p(s, "symmetrize", double(m) * 16.0 * (sym == 2 ? 2.0 : 1.0));
+    flip_avg_kernel<<<ceil_div(oct, 256), 256, 0, s>>>(n[0], n[1], n[2], field, sym == 2 ? scratch : scratch);
+    IHOM_LAUNCH_CHECK();
+    if (sym == 1) {
+      IHOM_CUDA(cudaMemcpyAsync(field, scratch, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    } else {
+      const int nt = n[0] / kPT;
+      const int reps = nt * (nt + 1) * (nt + 2) / 6;
+      perm_avg_kernel<<<reps, kPT * kPT * kPT, 0, s>>>(n[0], scratch, field);
+      IHOM_LAUNCH_CHECK();
+    }
+    return;
+  }
   static int perm[kMaxOps][3], flip[kMaxOps][3];
   const int nops = symmetry_group(sym, perm, flip);
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
-  const long long m = (long long)n[0] * n[1] * n[2];
   IHOM_CUDA(cudaMemcpyAsync(scratch, field, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
   {
     ProfScope p(s, "symmetrize", double(m) * 16.0);

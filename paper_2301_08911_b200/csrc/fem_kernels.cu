@@ -9,18 +9,45 @@
 // with TA = double this avoids the per-coefficient f32->f64 conversion
 // (F2F, ~16/clk/SM on B200, measured) the reference's float merge would need.
 #include "kernels.hpp"
+#include "ku_gen.cuh"
 
 namespace ihomgpu {
 
 __constant__ double c_blk_d[8][8][9];
 __constant__ float c_blk_f[8][8][9];
 __constant__ double c_fmacro[8][6][3];
+// kappa classes of the factored stencil (ku_gen.cuh): kappa_k = lam' alpha_k + mu' beta_k
+__constant__ double c_kap_d[kKappaClasses];
+__constant__ float c_kap_f[kKappaClasses];
 
 void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t s) {
-  (void)k;
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_blk_d, t.blk, sizeof(t.blk), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_blk_f, t.blk_f, sizeof(t.blk_f), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_fmacro, t.fmacro, sizeof(t.fmacro), 0, cudaMemcpyHostToDevice, s));
+  // lam' and mu' recovered from K0 itself: K0[0][0] = 8 lam' + 32 mu', K0[0][1] = 3 lam' + 3 mu'
+  // (the 14-value structure, tests/test_material.cpp:50-68); verified against every kappa class below.
+  const double a = k.k[0][0], b = k.k[0][1];
+  const double mu = (a - 8.0 * b / 3.0) / 24.0, lam = b / 3.0 - mu;
+  static double kd[kKappaClasses];
+  static float kf[kKappaClasses];
+  for (int c = 0; c < kKappaClasses; ++c) {
+    kd[c] = lam * kKappaAlpha[c] + mu * kKappaBeta[c];
+    kf[c] = float(kd[c]);
+  }
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_d, kd, sizeof(kd), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_f, kf, sizeof(kf), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename TA>
+__device__ __forceinline__ const TA* kappa();
+template <>
+__device__ __forceinline__ const double* kappa<double>() {
+  return c_kap_d;
+}
+template <>
+__device__ __forceinline__ const float* kappa<float>() {
+  return c_kap_f;
 }
 
 template <typename TA>
@@ -107,10 +134,9 @@ __global__ void __launch_bounds__(128) l0_apply_kernel(GridGeo g, const TC* __re
   TA q[8];
   load_q(coeff, nb, q);
   const long long nv = g.nv;
-  const TN *ux = u, *uy = u + nv, *uz = u + 2 * nv;
-  TA acc[3] = {TA(0), TA(0), TA(0)};
-  accum_offdiag<TA, TN>(q, nb, ux, uy, uz, acc);
-  accum_block<TA, TN, 13>(q, nb, ux, uy, uz, acc);
+  auto U = [&](int n, int c) { return TA(__ldg(u + c * nv + nb.v[n])); };
+  TA acc[3];
+  ku_vertex<TA>(q, kappa<TA>(), U, acc);  // factored K0 (ku_gen.cuh), inc/fem.hpp:86-105 semantics
   if (f) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(TA(f[c * nv + loc]) - acc[c]);
@@ -140,11 +166,9 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
   TA q[8];
   load_q(coeff, nb, q);
   const long long nv = g.nv;
-  const TN *ux = ur, *uy = ur + nv, *uz = ur + 2 * nv;
-  TA m[3] = {TA(0), TA(0), TA(0)};
-  accum_offdiag<TA, TN>(q, nb, ux, uy, uz, m);
-  TA sblk[9];
-  merged_block<TA, 13>(q, sblk);
+  auto U = [&](int n, int c) { return TA(__ldg(ur + c * nv + nb.v[n])); };
+  TA m[3], sblk[9];
+  ku_vertex_split<TA>(q, kappa<TA>(), U, m, sblk);  // S (n = 13) and M u (n != 13), inc/fem.hpp:109-133
   const long long loc = g.base[color] + i;
   double S[9], rhs[3], out[3];
 #pragma unroll

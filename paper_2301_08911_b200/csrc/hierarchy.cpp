@@ -49,7 +49,7 @@ std::vector<double> assemble_dense_stencil(const GridGeo& g, const std::vector<T
       const long long wl = vloc(g, (x + tx + g.n[0]) % g.n[0], (y + ty + g.n[1]) % g.n[1], (z + tz + g.n[2]) % g.n[2]);
       for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c)
-          a[size_t((3 * loc + r) * N + 3 * wl + c)] += double(st[size_t((9 * n + 3 * r + c) * nv + loc)]);
+          a[size_t((3 * loc + r) * N + 3 * wl + c)] += double(st[st_index(9 * n + 3 * r + c, (unsigned)loc)]);
     }
   }
   return a;
@@ -138,7 +138,7 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
     IHOM_CUDA(cudaMemsetAsync(L.u.p, 0, sizeof(double) * n3, s_));
     IHOM_CUDA(cudaMemsetAsync(L.f.p, 0, sizeof(double) * n3, s_));
     IHOM_CUDA(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n3, s_));
-    if (l > 0) L.st.alloc(size_t(243 * L.g.nv));
+    if (l > 0) L.st.alloc(stencil_alloc(L.g.nv));
   }
   coeff_.alloc(size_t(levels_[0].g.nv));
   ndof_c_ = int(3 * levels_.back().g.nv);
@@ -196,7 +196,7 @@ void Hierarchy<T>::factor_coarsest() {  // src/multigrid.cpp:368-383
     std::vector<double> cd(c.begin(), c.end());
     a = assemble_dense_l0(g, cd, k0_);
   } else {
-    std::vector<T> st(size_t(243 * g.nv));
+    std::vector<T> st(stencil_alloc(g.nv));
     IHOM_CUDA(cudaMemcpyAsync(st.data(), levels_[size_t(lc)].st.p, sizeof(T) * st.size(), cudaMemcpyDeviceToHost, s_));
     IHOM_CUDA(cudaStreamSynchronize(s_));
     a = assemble_dense_stencil<T>(g, st);
@@ -486,6 +486,45 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts) {  //
   }
   u0_bound_ = nullptr;
   return st;
+}
+
+template <typename T>
+void Hierarchy<T>::bench_op(const std::string& op, int reps) {
+  if (!density_set_) throw StateError("set_density before bench_op");
+  const bool f32 = op.find("_f32") != std::string::npos;
+  if (f32 && !std::is_same_v<T, float>) throw std::invalid_argument("f32 inner kernels exist in mixed precision only");
+  if (f32) ensure_inner();
+  const int lmax = num_levels() - 1;
+  for (int r = 0; r < reps; ++r) {
+    if (op == "l0_gs_f64") relax(0, 1);
+    else if (op == "l0_gs_f32") relax_f32(0, 1);
+    else if (op == "l0_residual_f64") compute_residual(0);
+    else if (op == "l0_residual_f32") residual_f32(0);
+    else if (op == "l1_gs_f64" && lmax >= 1) relax(1, 1);
+    else if (op == "l1_gs_f32" && lmax >= 1) relax_f32(1, 1);
+    else if (op == "l1_residual_f64" && lmax >= 1) compute_residual(1);
+    else if (op == "l1_residual_f32" && lmax >= 1) residual_f32(1);
+    else if (op == "vcycle_f64" || op == "vcycle_f32") {
+      SolverOptions o;
+      o.mode = f32 ? kMixedDefect : kVCycle;
+      v_cycle(o);
+    } else if (op == "set_density") {
+      // Galerkin rebuild from the current coefficients (coeff kernel skipped)
+      if (levels_.size() > 1) {
+        {
+          ProfScope p(s_, "galerkin_l1", double(levels_[0].g.nv) * sizeof(T) + double(levels_[1].g.nv) * 243.0 * sizeof(T));
+          launch_galerkin_from_elements<T>(levels_[0].g, levels_[1].g, coeff_.p, levels_[1].st.p, s_);
+        }
+        for (size_t l = 2; l < levels_.size(); ++l) {
+          ProfScope p(s_, "galerkin_coarse", double(levels_[l - 1].g.nv + levels_[l].g.nv) * 243.0 * sizeof(T));
+          launch_galerkin_from_stencil<T>(levels_[l - 1].g, levels_[l].g, levels_[l - 1].st.p, levels_[l].st.p, s_);
+        }
+      }
+    } else {
+      throw std::invalid_argument("unknown bench op: " + op);
+    }
+  }
+  IHOM_CUDA(cudaStreamSynchronize(s_));
 }
 
 // ============================================================== Homogenizer

@@ -18,6 +18,7 @@
 
 #include <array>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -122,6 +123,8 @@ class Hierarchy {
   void remove_translations(double* f, int l);
   double norm(const double* x, long long n);
 
+  // Runs one kernel family `reps` times on the current level data (benchmark / ncu target).
+  void bench_op(const std::string& op, int reps);
   cudaStream_t stream() const { return s_; }
   Workspace& workspace() { return ws_; }
   const K0Matrix& k0() const { return k0_; }

@@ -19,27 +19,29 @@ constexpr int kGradPerLoad = 36;   // 3 comps x 3 directions x 4 points
 
 __device__ __forceinline__ int wrapp(int c, int n) { return c >= n ? c - n : c; }
 
-// Computes the 21 upper-triangle energies for element (ex,ey,ez).
-// gs: per-thread smem slice, stride kHT.
-template <typename TN>
+// Computes the 21 upper-triangle energies for element (ex,ey,ez) in arithmetic
+// type TE (f64 all-double; f32 in mixed mode, where u is read through the
+// reference's f32 snapshot anyway). gs: per-thread smem slice, stride kHT.
+template <typename TN, typename TE>
 __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const TN* const* u, bool snap,
-                                 double lam, double mu, double* gs, double E[21]) {
-  const double p1 = 0.5 + 0.5 / 1.7320508075688772;  // gp[1]; N_a(g) = (a == g) ? p1 : p0
-  const double p0 = 0.5 - 0.5 / 1.7320508075688772;
+                                 TE lam, TE mu, TE* gs, TE E[21]) {
+  const TE p1 = TE(0.5 + 0.5 / 1.7320508075688772);  // gp[1]; N_a(g) = (a == g) ? p1 : p0
+  const TE p0 = TE(0.5 - 0.5 / 1.7320508075688772);
   unsigned loc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     loc[j] = vloc(g, wrapp(ex + (j & 1), g.n[0]), wrapp(ey + ((j >> 1) & 1), g.n[1]), wrapp(ez + ((j >> 2) & 1), g.n[2]));
   const long long nv = g.nv;
+#pragma unroll
   for (int i = 0; i < 6; ++i) {
     const TN* ui = u[i];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double U[8];
+      TE U[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const double v = double(ui[c * nv + loc[j]]);
-        U[j] = snap ? double(float(v)) : v;
+        U[j] = snap ? TE(float(v)) : TE(v);
       }
       // direction k: differences across k at the 4 corners of the other two axes (a,b),
       // then bilinear interpolation to the 4 Gauss points (ga, gb).
@@ -47,7 +49,7 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
       for (int k = 0; k < 3; ++k) {
         const int ka = (k + 1) % 3, kb = (k + 2) % 3;
         const int sk = 1 << k, sa = 1 << ka, sb = 1 << kb;
-        double D[2][2];
+        TE D[2][2];
 #pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -59,7 +61,7 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
         for (int ga = 0; ga < 2; ++ga)
 #pragma unroll
           for (int gb = 0; gb < 2; ++gb) {
-            double s = 0.0;
+            TE s = TE(0);
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -70,7 +72,7 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
     }
   }
 #pragma unroll
-  for (int q = 0; q < 21; ++q) E[q] = 0.0;
+  for (int q = 0; q < 21; ++q) E[q] = TE(0);
   // grad(i, c, k, gx,gy,gz): the two "other" axes of k are (k+1)%3, (k+2)%3.
   auto G = [&](int i, int c, int k, const int gp[3]) {
     const int ga = gp[(k + 1) % 3], gb = gp[(k + 2) % 3];
@@ -78,23 +80,23 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
   };
   for (int gq = 0; gq < 8; ++gq) {
     const int gp[3] = {gq & 1, (gq >> 1) & 1, (gq >> 2) & 1};
-    double ed[6][6], sg[6][6];
+    TE ed[6][6], sg[6][6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
-      double e[6];
+      TE e[6];
       e[0] = -G(i, 0, 0, gp);
       e[1] = -G(i, 1, 1, gp);
       e[2] = -G(i, 2, 2, gp);
       e[3] = -(G(i, 0, 1, gp) + G(i, 1, 0, gp));
       e[4] = -(G(i, 1, 2, gp) + G(i, 2, 1, gp));
       e[5] = -(G(i, 0, 2, gp) + G(i, 2, 0, gp));
-      e[i] += 1.0;  // strain of chi^i (engineering order 11,22,33,12,23,13)
-      const double tr = e[0] + e[1] + e[2];
+      e[i] += TE(1);  // strain of chi^i (engineering order 11,22,33,12,23,13)
+      const TE tr = e[0] + e[1] + e[2];
 #pragma unroll
       for (int v = 0; v < 6; ++v) ed[i][v] = e[v];
-      sg[i][0] = lam * tr + 2.0 * mu * e[0];
-      sg[i][1] = lam * tr + 2.0 * mu * e[1];
-      sg[i][2] = lam * tr + 2.0 * mu * e[2];
+      sg[i][0] = lam * tr + TE(2) * mu * e[0];
+      sg[i][1] = lam * tr + TE(2) * mu * e[1];
+      sg[i][2] = lam * tr + TE(2) * mu * e[2];
       sg[i][3] = mu * e[3];
       sg[i][4] = mu * e[4];
       sg[i][5] = mu * e[5];
@@ -104,10 +106,10 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int j = i; j < 6; ++j, ++q) {
-        double s = 0.0;
+        TE s = TE(0);
 #pragma unroll
         for (int v = 0; v < 6; ++v) s += ed[i][v] * sg[j][v];
-        E[q] += 0.125 * s;
+        E[q] += TE(0.125) * s;
       }
   }
 }
@@ -132,10 +134,11 @@ struct U6 {
   const void* p[6];
 };
 
-template <typename TN>
+template <typename TN, typename TE>
 __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                      bool snap, double lam, double mu, double* partials) {
-  extern __shared__ double gsm[];
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  TE* gsm = reinterpret_cast<TE*>(gsm_raw);
   __shared__ double sh[32];
   const TN* u[6];
 #pragma unroll
@@ -147,13 +150,13 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
     const int ex = int(e % g.n[0]);
     const long long r = e / g.n[0];
     const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
-    double E[21];
-    element_energies<TN>(g, ex, ey, ez, u, snap, lam, mu, gsm + threadIdx.x, E);
+    TE E[21];
+    element_energies<TN, TE>(g, ex, ey, ez, u, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
     const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
-    for (int k = 0; k < 21; ++k) acc[k] += q * E[k];
+    for (int k = 0; k < 21; ++k) acc[k] += q * double(E[k]);
   }
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < 21; ++k) {
     const double r = block_reduce_h(acc[k], sh);
     if (threadIdx.x == 0) partials[k * kReducePartials + blockIdx.x] = r;
@@ -170,32 +173,38 @@ __global__ void tensor_finalize(const double* partials, int nparts, double* out)
   }
 }
 
-static size_t grad_smem() { return sizeof(double) * 6 * kGradPerLoad * kHT; }
+static size_t grad_smem(bool f32) { return (f32 ? sizeof(float) : sizeof(double)) * 6 * kGradPerLoad * kHT; }
 
-template <typename TN>
-static void set_smem(const void* fn) {
-  IHOM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem()));
+static void set_smem(const void* fn, bool f32) {
+  IHOM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem(f32)));
 }
 
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
                              double lam, double mu, double* partials, double* c21, cudaStream_t s) {
-  set_smem<TN>((const void*)tensor_kernel<TN>);
   long long blocks = (g.nv + kHT - 1) / kHT;
   if (blocks > kReducePartials) blocks = kReducePartials;
   U6 uu;
   for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
-  tensor_kernel<TN><<<(unsigned)blocks, kHT, grad_smem(), s>>>(g, uu, rho, penal, snap, lam, mu, partials);
+  if (snap) {
+    set_smem((const void*)tensor_kernel<TN, float>, true);
+    tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials);
+  } else {
+    set_smem((const void*)tensor_kernel<TN, double>, false);
+    tensor_kernel<TN, double><<<(unsigned)blocks, kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                               partials);
+  }
   IHOM_LAUNCH_CHECK();
   tensor_finalize<<<1, 256, 0, s>>>(partials, (int)blocks, c21);
   IHOM_LAUNCH_CHECK();
 }
 
-template <typename TN>
+template <typename TN, typename TE>
 __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                    bool snap, double lam, double mu, const double* __restrict__ seed,
                                                    double* __restrict__ out) {
-  extern __shared__ double gsm[];
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  TE* gsm = reinterpret_cast<TE*>(gsm_raw);
   const TN* u[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) u[i] = static_cast<const TN*>(uu.p[i]);
@@ -204,24 +213,31 @@ __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const doubl
   const int ex = int(e % g.n[0]);
   const long long r = e / g.n[0];
   const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
-  double E[21];
-  element_energies<TN>(g, ex, ey, ez, u, snap, lam, mu, gsm + threadIdx.x, E);
+  TE E[21];
+  element_energies<TN, TE>(g, ex, ey, ez, u, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
   double acc = 0.0;  // sum_ij s_ij E_ij with s symmetric (src/homogenization.cpp:120,138-140)
   int q = 0;
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
-    for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * E[q];
+    for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * double(E[q]);
   out[e] = penal * pow(rho[e], penal - 1.0) * acc / double(g.nv);  // :141
 }
 
 template <typename TN>
 void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
                                double lam, double mu, const double* sym_seed36, double* out, cudaStream_t s) {
-  set_smem<TN>((const void*)sens_kernel<TN>);
   U6 uu;
   for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
-  sens_kernel<TN><<<ceil_div(g.nv, kHT), kHT, grad_smem(), s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36, out);
+  if (snap) {
+    set_smem((const void*)sens_kernel<TN, float>, true);
+    sens_kernel<TN, float><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                             sym_seed36, out);
+  } else {
+    set_smem((const void*)sens_kernel<TN, double>, false);
+    sens_kernel<TN, double><<<ceil_div(g.nv, kHT), kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                               sym_seed36, out);
+  }
   IHOM_LAUNCH_CHECK();
 }
 

@@ -100,13 +100,14 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   gather27(g, vx, vy, vz, nb);
   const long long nv = g.nv;
   double acc[3] = {0.0, 0.0, 0.0};
+  const TS* row = st + st_index(0, (unsigned)loc);
 #pragma unroll 3
   for (int n = 0; n < 27; ++n) {
     const double a = double(x[nb.v[n]]), b = double(x[nv + nb.v[n]]), c = double(x[2 * nv + nb.v[n]]);
-    const TS* row = st + (size_t)(9 * n) * nv + loc;
-    acc[0] += double(row[0]) * a + double(row[nv]) * b + double(row[2 * nv]) * c;
-    acc[1] += double(row[3 * nv]) * a + double(row[4 * nv]) * b + double(row[5 * nv]) * c;
-    acc[2] += double(row[6 * nv]) * a + double(row[7 * nv]) * b + double(row[8 * nv]) * c;
+    const TS* bl = row + 32 * 9 * n;
+    acc[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
+    acc[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
+    acc[2] += double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
   }
   if (f) {
 #pragma unroll
@@ -137,18 +138,19 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
   const long long nv = g.nv;
   const long long loc = g.base[color] + i;
   double m[3] = {0.0, 0.0, 0.0}, S[9];
+  const TS* row0 = st + st_index(0, (unsigned)loc);
 #pragma unroll 3
   for (int n = 0; n < 27; ++n) {
-    const TS* row = st + (size_t)(9 * n) * nv + loc;
+    const TS* bl = row0 + 32 * 9 * n;
     if (n == 13) {
 #pragma unroll
-      for (int e = 0; e < 9; ++e) S[e] = double(row[e * nv]);
+      for (int e = 0; e < 9; ++e) S[e] = double(bl[32 * e]);
       continue;
     }
     const double a = double(ur[nb.v[n]]), b = double(ur[nv + nb.v[n]]), c = double(ur[2 * nv + nb.v[n]]);
-    m[0] += double(row[0]) * a + double(row[nv]) * b + double(row[2 * nv]) * c;
-    m[1] += double(row[3 * nv]) * a + double(row[4 * nv]) * b + double(row[5 * nv]) * c;
-    m[2] += double(row[6 * nv]) * a + double(row[7 * nv]) * b + double(row[8 * nv]) * c;
+    m[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
+    m[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
+    m[2] += double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
   }
   const double rhs[3] = {double(f[loc]) - m[0], double(f[nv + loc]) - m[1], double(f[2 * nv + loc]) - m[2]};
   const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
@@ -223,7 +225,6 @@ __global__ void __launch_bounds__(kGalThreads) gal_elem_kernel(GridGeo gf, GridG
         }
   }
   if (!active) return;
-  const long long nvc = gc.nv;
   for (int n = 0; n < 27; ++n) {
     double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = c_eg_start[n]; k < c_eg_start[n + 1]; ++k) {
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kGalThreads) gal_elem_kernel(GridGeo gf, GridG
       for (int e = 0; e < 9; ++e) acc[e] += q * c_eg_w[k][e];
     }
 #pragma unroll
-    for (int e = 0; e < 9; ++e) st[(size_t)(9 * n + e) * nvc + loc] = TC(acc[e]);
+    for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, (unsigned)loc)] = TC(acc[e]);
   }
 }
 
@@ -242,51 +243,70 @@ void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const T
   IHOM_LAUNCH_CHECK();
 }
 
-// assemble_stencil_from_stencil (src/multigrid.cpp:307-333). The 2197 (s,t)
-// terms factor per axis: weight w(s) w(s+t-2 delta) with per-axis pairs
-// enumerated on the fly (no table); order of summation follows the
-// reference (s outer, t inner, x fastest).
+// assemble_stencil_from_stencil (src/multigrid.cpp:307-333):
+//   [K_vc]_{vc+delta} = sum_{s,t} w(s) w(s+t-2 delta) [K_{2vc+s}]_t
+// One thread per (coarse vertex, output neighbour delta): blockIdx.y = delta, so
+// every warp walks the same (s, t, w) term list from constant memory
+// (2197 terms, grouped by delta in the reference's s-outer/t-inner order) and
+// accumulates 9 f64 entries.
+constexpr int kMaxSgTerms = 2197;
+__constant__ int c_sg_start[28];
+__constant__ unsigned short c_sg_st[kMaxSgTerms];  // s | t << 5
+__constant__ float c_sg_w[kMaxSgTerms];            // products of 1, 1/2, 1/4, 1/8: exact in f32
+
+static void upload_stencil_galerkin(cudaStream_t s) {
+  static bool done = false;
+  if (done) return;
+  static int start[28];
+  static unsigned short st[kMaxSgTerms];
+  static float w[kMaxSgTerms];
+  const StencilGalerkin sg;
+  int k = 0;
+  for (int n = 0; n < 27; ++n) {
+    start[n] = k;
+    for (const auto& t : sg.by_n[size_t(n)]) {
+      st[k] = (unsigned short)(t.s | (t.t << 5));
+      w[k] = float(t.w);
+      ++k;
+    }
+  }
+  start[27] = k;
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sg_start, start, sizeof(start), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sg_st, st, sizeof(unsigned short) * k, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sg_w, w, sizeof(float) * k, 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  done = true;
+}
+
 template <typename TS>
 __global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
                                                           TS* __restrict__ stc) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.y;
   if (loc >= gc.nv) return;
   const int color = color_at(gc, loc);
   int x, y, z;
   block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
-  unsigned fl[27];
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int k1 = c_sg_start[n + 1];
+  for (int k = c_sg_start[n]; k < k1; ++k) {
+    const int st = c_sg_st[k];
+    const int s = st & 31, t = st >> 5;
+    const unsigned fl = vloc(gf, wrapi(2 * x + s % 3 - 1, gf.n[0]), wrapi(2 * y + (s / 3) % 3 - 1, gf.n[1]),
+                             wrapi(2 * z + s / 9 - 1, gf.n[2]));
+    const double w = double(c_sg_w[k]);
+    const TS* b = stf + st_index(9 * t, fl);
 #pragma unroll
-  for (int s = 0; s < 27; ++s) {
-    const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
-    fl[s] = vloc(gf, wrapi(2 * x + sx, gf.n[0]), wrapi(2 * y + sy, gf.n[1]), wrapi(2 * z + sz, gf.n[2]));
+    for (int e = 0; e < 9; ++e) acc[e] += w * double(__ldg(b + 32 * e));
   }
-  const long long nvf = gf.nv, nvc = gc.nv;
-  for (int n = 0; n < 27; ++n) {
-    const int dx = n % 3 - 1, dy = (n / 3) % 3 - 1, dz = n / 9 - 1;
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 1
-    for (int s = 0; s < 27; ++s) {
-      const int sx = s % 3 - 1, sy = (s / 3) % 3 - 1, sz = s / 9 - 1;
-      const double ws = tw1(sx) * tw1(sy) * tw1(sz);
-#pragma unroll 1
-      for (int t = 0; t < 27; ++t) {
-        const int tx = t % 3 - 1, ty = (t / 3) % 3 - 1, tz = t / 9 - 1;
-        const double wt = tw1(sx + tx - 2 * dx) * tw1(sy + ty - 2 * dy) * tw1(sz + tz - 2 * dz);
-        const double w = ws * wt;
-        if (w == 0.0) continue;
-        const TS* b = stf + (size_t)(9 * t) * nvf + fl[s];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) acc[e] += w * double(b[(size_t)e * nvf]);
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < 9; ++e) stc[(size_t)(9 * n + e) * nvc + loc] = TS(acc[e]);
-  }
+  for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, (unsigned)loc)] = TS(acc[e]);
 }
 
 template <typename TS>
 void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s) {
-  gal_stencil_kernel<TS><<<ceil_div(gc.nv, 128), 128, 0, s>>>(gf, gc, stf, stc);
+  upload_stencil_galerkin(s);
+  gal_stencil_kernel<TS><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, stf, stc);
   IHOM_LAUNCH_CHECK();
 }
 

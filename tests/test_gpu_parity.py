@@ -248,10 +248,15 @@ def test_radial_filter(ih, orc, kernel, radius):
 
 
 @pytest.mark.parametrize("sym", ["reflect3", "reflect6", "rotate3"])
-def test_symmetrize(ih, orc, sym):
-    n = 8
-    f = mt_uniform(512, 41, 0, 1)
-    assert rel(ih.symmetrize(n, f, sym), orc.symmetrize(n, f, sym)) < 1e-15
+@pytest.mark.parametrize("n", [8, 16, 24, 12, (7, 9, 11)])
+def test_symmetrize(ih, orc, sym, n):
+    n3 = (n,) * 3 if np.isscalar(n) else n
+    if sym != "reflect3" and len(set(n3)) > 1:
+        with pytest.raises(ValueError):
+            ih.symmetrize(n3, np.zeros(int(np.prod(n3))), sym)
+        return
+    f = mt_uniform(int(np.prod(n3)), 41, 0, 1)
+    assert rel(ih.symmetrize(n3, f, sym), orc.symmetrize(n3, f, sym)) < 1e-15
 
 
 def test_oc_update_matches_oracle(ih, orc):

@@ -3,7 +3,9 @@
 // Layout contract (bit-exact with the reference, inc/grid.hpp:73-78):
 //   * vertex storage is colour-major: 8 parity classes, each a dense
 //     [hz][hy][hx] block of halved coordinates, x fastest;
-//   * nodal fields are SoA f64: comp c of vertex loc at p[c*nv + loc];
+//   * nodal fields are AoS (the reference's NodalField, inc/fem.hpp:15-26):
+//     comp c of vertex loc at p[3*loc + c] -- one address per neighbour, the
+//     three components at immediate offsets;
 //   * element fields are x-fastest, eidx = x + n0*(y + n1*z);
 //   * coarse stencils are blocked SoA [nv/32][243][32] in T (f32 mixed / f64
 //     all-double): entry k = 9*n + 3*r + c of vertex loc at st_index(k, loc),

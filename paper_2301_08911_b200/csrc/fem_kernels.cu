@@ -24,10 +24,11 @@ void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_blk_d, t.blk, sizeof(t.blk), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_blk_f, t.blk_f, sizeof(t.blk_f), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_fmacro, t.fmacro, sizeof(t.fmacro), 0, cudaMemcpyHostToDevice, s));
-  // lam' and mu' recovered from K0 itself: K0[0][0] = 8 lam' + 32 mu', K0[0][1] = 3 lam' + 3 mu'
-  // (the 14-value structure, tests/test_material.cpp:50-68); verified against every kappa class below.
-  const double a = k.k[0][0], b = k.k[0][1];
-  const double mu = (a - 8.0 * b / 3.0) / 24.0, lam = b / 3.0 - mu;
+  // lam' and mu' recovered from two K0 entries with known integer structure (ku_gen.cuh kK0Probe)
+  const double k1 = k.k[kK0Probe[0][0]][kK0Probe[0][1]], k2 = k.k[kK0Probe[1][0]][kK0Probe[1][1]];
+  const double a1 = kK0Probe[0][2], b1 = kK0Probe[0][3], a2 = kK0Probe[1][2], b2 = kK0Probe[1][3];
+  const double det = a1 * b2 - a2 * b1;
+  const double lam = (k1 * b2 - k2 * b1) / det, mu = (a1 * k2 - a2 * k1) / det;
   static double kd[kKappaClasses];
   static float kf[kKappaClasses];
   for (int c = 0; c < kKappaClasses; ++c) {
@@ -106,6 +107,114 @@ __device__ __forceinline__ void load_q(const TC* __restrict__ coeff, const Nbhd&
   for (int ke = 0; ke < 8; ++ke) q[ke] = TA(coeff[nb.e[ke]]);
 }
 
+// ---------------------------------------------------------------- fast even-grid variants
+// On every smoothed level all n_k are even, so the 8 colour blocks share dims
+// d_k = n_k/2 and size B = d0 d1 d2 (base[c] = c B). For a vertex of colour
+// o = (o0,o1,o2) at halved (h0,h1,h2), neighbour t has location
+//   loc(t) = A0[t0] + A1[t1] + A2[t2],
+//   A_k[t] = ((o_k ^ (t != 0)) << k) B + s_k * half_k(t),
+// half_k(0) = h_k, half_k(-1) = o_k ? h_k : h_k - 1 (wrapped), half_k(+1) = o_k ? h_k + 1 (wrapped) : h_k,
+// s = (1, d0, d0 d1). One IADD3 per neighbour; AoS nodal data then gives the three
+// components at immediate offsets. Incident elements likewise: e = E0[a] + E1[b] + E2[c].
+struct FastAddr {
+  unsigned A[3][3];  // [axis][t+1]
+  unsigned E[3][2];  // [axis][bit]: element coordinate x-1 (bit 0) or x (bit 1), pre-scaled
+};
+
+__device__ __forceinline__ void fast_addr(const GridGeo& g, int color, int h0, int h1, int h2, FastAddr& fa) {
+  const unsigned B = (unsigned)g.size[0];
+  const int h[3] = {h0, h1, h2};
+  const unsigned d[3] = {(unsigned)g.cd[0][0], (unsigned)g.cd[0][1], (unsigned)g.cd[0][2]};
+  const unsigned sc[3] = {1u, d[0], d[0] * d[1]};
+  const unsigned es[3] = {1u, (unsigned)g.n[0], (unsigned)g.n[0] * (unsigned)g.n[1]};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int o = (color >> k) & 1;
+    const unsigned hm = o ? (unsigned)h[k] : (h[k] == 0 ? d[k] - 1 : (unsigned)h[k] - 1);
+    const unsigned hp = o ? ((unsigned)h[k] + 1 == d[k] ? 0u : (unsigned)h[k] + 1) : (unsigned)h[k];
+    const unsigned same = ((unsigned)o << k) * B, other = ((unsigned)(o ^ 1) << k) * B;
+    fa.A[k][0] = other + sc[k] * hm;
+    fa.A[k][1] = same + sc[k] * (unsigned)h[k];
+    fa.A[k][2] = other + sc[k] * hp;
+    const int x = 2 * h[k] + o, nk = g.n[k];
+    fa.E[k][0] = es[k] * (unsigned)(x == 0 ? nk - 1 : x - 1);
+    fa.E[k][1] = es[k] * (unsigned)x;
+  }
+}
+
+template <typename TC, typename TA>
+__device__ __forceinline__ void load_q_fast(const TC* __restrict__ coeff, const FastAddr& fa, TA q[8]) {
+#pragma unroll
+  for (int ke = 0; ke < 8; ++ke)
+    q[ke] = TA(__ldg(coeff + (fa.E[0][ke & 1] + fa.E[1][(ke >> 1) & 1] + fa.E[2][(ke >> 2) & 1])));
+}
+
+#define FAST_U(ptr)                                                                      \
+  [&](int n, int c) {                                                                    \
+    const unsigned l_ = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];         \
+    return TA(__ldg(ptr + 3 * (size_t)l_ + c));                                          \
+  }
+
+// blockDim = (bx, 128/bx), grid = (d0/bx, ceil(d1/by), d2 * ncolors)
+template <typename TC, typename TN, typename TA>
+__global__ void __launch_bounds__(128) l0_apply_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                            const TN* __restrict__ u, const TN* __restrict__ f,
+                                                            TN* __restrict__ y) {
+  const int d2 = g.cd[0][2];
+  const int color = blockIdx.z / d2;
+  const int h2 = blockIdx.z - color * d2;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  TA q[8];
+  load_q_fast(coeff, fa, q);
+  TA acc[3];
+  ku_vertex<TA>(q, kappa<TA>(), FAST_U(u), acc);
+  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  if (f) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+  }
+}
+
+template <typename TC, typename TN, typename TA>
+__global__ void __launch_bounds__(128) l0_gs_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                         const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
+                                                         int color) {
+  const int h2 = blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  TA q[8];
+  load_q_fast(coeff, fa, q);
+  TA m[3], sblk[9];
+  ku_vertex_split<TA>(q, kappa<TA>(), FAST_U(ur), m, sblk);
+  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  double S[9], rhs[3], out[3];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) S[e] = double(sblk[e]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) rhs[c] = double(f[3 * loc + c]) - double(m[c]);
+  solve3(S, rhs, out);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
+}
+#undef FAST_U
+
+static bool fast_ok(const GridGeo& g) {
+  return g.n[0] % 2 == 0 && g.n[1] % 2 == 0 && g.n[2] % 2 == 0 && g.n[0] >= 8;
+}
+static dim3 fast_block(const GridGeo& g) {
+  const int d0 = g.cd[0][0];
+  const int bx = d0 >= 32 ? 32 : (d0 >= 16 ? 16 : (d0 >= 8 ? 8 : 4));
+  return dim3(bx, 128 / bx, 1);
+}
+
 // ---------------------------------------------------------------- coeff
 template <typename TC>
 __global__ void coeff_kernel(const double* __restrict__ rho, TC* __restrict__ coeff, long long m, double p) {
@@ -134,21 +243,27 @@ __global__ void __launch_bounds__(128) l0_apply_kernel(GridGeo g, const TC* __re
   TA q[8];
   load_q(coeff, nb, q);
   const long long nv = g.nv;
-  auto U = [&](int n, int c) { return TA(__ldg(u + c * nv + nb.v[n])); };
+  auto U = [&](int n, int c) { return TA(__ldg(u + 3 * (size_t)nb.v[n] + c)); };
   TA acc[3];
   ku_vertex<TA>(q, kappa<TA>(), U, acc);  // factored K0 (ku_gen.cuh), inc/fem.hpp:86-105 semantics
   if (f) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(TA(f[c * nv + loc]) - acc[c]);
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(acc[c]);
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
   }
 }
 
 template <typename TC, typename TN, typename TA>
 void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s) {
-  l0_apply_kernel<TC, TN, TA><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, coeff, u, f, y);
+  if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+    l0_apply_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, u, f, y);
+  } else {
+    l0_apply_kernel<TC, TN, TA><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, coeff, u, f, y);
+  }
   IHOM_LAUNCH_CHECK();
 }
 
@@ -166,7 +281,7 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
   TA q[8];
   load_q(coeff, nb, q);
   const long long nv = g.nv;
-  auto U = [&](int n, int c) { return TA(__ldg(ur + c * nv + nb.v[n])); };
+  auto U = [&](int n, int c) { return TA(__ldg(ur + 3 * (size_t)nb.v[n] + c)); };
   TA m[3], sblk[9];
   ku_vertex_split<TA>(q, kappa<TA>(), U, m, sblk);  // S (n = 13) and M u (n != 13), inc/fem.hpp:109-133
   const long long loc = g.base[color] + i;
@@ -174,15 +289,21 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
 #pragma unroll
   for (int e = 0; e < 9; ++e) S[e] = double(sblk[e]);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) rhs[c] = double(f[c * nv + loc]) - double(m[c]);
+  for (int c = 0; c < 3; ++c) rhs[c] = double(f[3 * loc + c]) - double(m[c]);
   solve3(S, rhs, out);  // src/fem.cpp:131-135
 #pragma unroll
-  for (int c = 0; c < 3; ++c) uw[c * nv + loc] = TN(out[c]);
+  for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }
 
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s) {
-  l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
+  if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
+    l0_gs_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+  } else {
+    l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
+  }
   IHOM_LAUNCH_CHECK();
 }
 
@@ -204,7 +325,7 @@ __global__ void macro_force_kernel(GridGeo g, const TC* __restrict__ coeff, int 
     for (int c = 0; c < 3; ++c) acc[c] += q * c_fmacro[ke][load][c];
   }
 #pragma unroll
-  for (int c = 0; c < 3; ++c) f[c * g.nv + loc] = acc[c];
+  for (int c = 0; c < 3; ++c) f[3 * loc + c] = acc[c];
 }
 
 template <typename TC>

@@ -40,7 +40,7 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
       TE U[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double v = double(ui[c * nv + loc[j]]);
+        const double v = double(ui[3 * (size_t)loc[j] + c]);
         U[j] = snap ? TE(float(v)) : TE(v);
       }
       // direction k: differences across k at the 4 corners of the other two axes (a,b),

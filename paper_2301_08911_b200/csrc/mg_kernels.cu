@@ -32,10 +32,10 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
         const double w = tw1(dx) * tw1(dy) * tw1(dz);
         const unsigned fl = vloc(gf, wrapi(2 * x + dx, gf.n[0]), wrapi(2 * y + dy, gf.n[1]), wrapi(2 * z + dz, gf.n[2]));
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] += w * double(rf[c * gf.nv + fl]);
+        for (int c = 0; c < 3; ++c) acc[c] += w * double(rf[3 * (size_t)fl + c]);
       }
 #pragma unroll
-  for (int c = 0; c < 3; ++c) fc[c * gc.nv + loc] = TN(acc[c]);
+  for (int c = 0; c < 3; ++c) fc[3 * loc + c] = TN(acc[c]);
 }
 
 template <typename TN>
@@ -73,10 +73,10 @@ __global__ void prolong_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc
       for (int c = 0; c < cnt[2]; ++c) {
         const unsigned cl = vloc(gc, wrapi(base[0] + a, gc.n[0]), wrapi(base[1] + b, gc.n[1]), wrapi(base[2] + c, gc.n[2]));
 #pragma unroll
-        for (int d = 0; d < 3; ++d) acc[d] += w * double(uc[d * gc.nv + cl]);
+        for (int d = 0; d < 3; ++d) acc[d] += w * double(uc[3 * (size_t)cl + d]);
       }
 #pragma unroll
-  for (int d = 0; d < 3; ++d) uf[d * gf.nv + loc] = TN(double(uf[d * gf.nv + loc]) + acc[d]);
+  for (int d = 0; d < 3; ++d) uf[3 * loc + d] = TN(double(uf[3 * loc + d]) + acc[d]);
 }
 
 template <typename TN>
@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   const TS* row = st + st_index(0, (unsigned)loc);
 #pragma unroll 3
   for (int n = 0; n < 27; ++n) {
-    const double a = double(x[nb.v[n]]), b = double(x[nv + nb.v[n]]), c = double(x[2 * nv + nb.v[n]]);
+    const TN* xn = x + 3 * (size_t)nb.v[n];
+    const double a = double(xn[0]), b = double(xn[1]), c = double(xn[2]);
     const TS* bl = row + 32 * 9 * n;
     acc[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
     acc[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
@@ -111,10 +112,10 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   }
   if (f) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(double(f[c * nv + loc]) - acc[c]);
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(double(f[3 * loc + c]) - acc[c]);
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[c * nv + loc] = TN(acc[c]);
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
   }
 }
 
@@ -147,12 +148,13 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
       for (int e = 0; e < 9; ++e) S[e] = double(bl[32 * e]);
       continue;
     }
-    const double a = double(ur[nb.v[n]]), b = double(ur[nv + nb.v[n]]), c = double(ur[2 * nv + nb.v[n]]);
+    const TN* un = ur + 3 * (size_t)nb.v[n];
+    const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
     m[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
     m[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
     m[2] += double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
   }
-  const double rhs[3] = {double(f[loc]) - m[0], double(f[nv + loc]) - m[1], double(f[2 * nv + loc]) - m[2]};
+  const double rhs[3] = {double(f[3 * loc]) - m[0], double(f[3 * loc + 1]) - m[1], double(f[3 * loc + 2]) - m[2]};
   const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
                      S[2] * (S[3] * S[7] - S[4] * S[6]);
   if (det == 0.0 || !isfinite(det)) {
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
   double out[3];
   solve3(S, rhs, out);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) uw[c * nv + loc] = TN(out[c]);
+  for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }
 
 template <typename TS, typename TN>
@@ -352,11 +354,11 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
   // remove_translations(f) (src/multigrid.cpp:81-86, 427)
   for (int c = 0; c < 3; ++c) {
     double part = 0.0;
-    for (long long i = threadIdx.x; i < nv; i += blockDim.x) part += double(f[c * nv + i]);
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) part += double(f[3 * i + c]);
     const double mean = block_sum_1(part, red) / double(nv);
     for (long long i = threadIdx.x; i < nv; i += blockDim.x) {
-      const TN v = TN(double(f[c * nv + i]) - mean);
-      f[c * nv + i] = v;
+      const TN v = TN(double(f[3 * i + c]) - mean);
+      f[3 * i + c] = v;
       fv[3 * i + c] = double(v);
     }
   }
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
   for (int i = threadIdx.x; i < N; i += blockDim.x) part += fv[i] * fv[i];
   const double fn = sqrt(block_sum_1(part, red));
   if (fn <= negligible) {  // src/multigrid.cpp:430-433
-    for (int i = threadIdx.x; i < N; i += blockDim.x) u[(i % 3) * nv + i / 3] = TN(0);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) u[i] = TN(0);
     return;
   }
   // x = Ainv f
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
     double p2 = 0.0;
     for (long long i = threadIdx.x; i < nv; i += blockDim.x) p2 += x[3 * i + c];
     const double mean = block_sum_1(p2, red) / double(nv);
-    for (long long i = threadIdx.x; i < nv; i += blockDim.x) u[c * nv + i] = TN(x[3 * i + c] - mean);
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) u[3 * i + c] = TN(x[3 * i + c] - mean);
   }
 }
 

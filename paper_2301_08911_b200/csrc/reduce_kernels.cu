@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x
   double s[3] = {0.0, 0.0, 0.0};
   for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < nv; i += (long long)gridDim.x * kRT) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) s[c] += double(x[c * nv + i]);
+    for (int c = 0; c < 3; ++c) s[c] += double(x[3 * i + c]);
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -94,7 +94,7 @@ __global__ void sub_means_kernel(TN* x, long long nv, const double* sums) {
   if (i >= nv) return;
   const double inv = 1.0 / double(nv);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) x[c * nv + i] = TN(double(x[c * nv + i]) - sums[c] * inv);
+  for (int c = 0; c < 3; ++c) x[3 * i + c] = TN(double(x[3 * i + c]) - sums[c] * inv);
 }
 
 template <typename TN>
@@ -155,8 +155,9 @@ __global__ void aos_soa_kernel(const double* __restrict__ in, double* __restrict
 }
 
 void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s) {
-  aos_soa_kernel<<<ceil_div(nv, 256), 256, 0, s>>>(in, out, nv, to_soa ? 1 : 0);
-  IHOM_LAUNCH_CHECK();
+  // device nodal storage is AoS like the boundary: a plain copy
+  (void)to_soa;
+  if (in != out) IHOM_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * 3 * nv, cudaMemcpyDeviceToDevice, s));
 }
 
 }  // namespace ihomgpu

@@ -51,9 +51,9 @@ def make_hom(ih, n, precision, penal=3.0, tol=1e-2, max_cycles=50, mode="vcycle"
 
 
 @pytest.mark.parametrize("precision,tol", [("double", 1e-12), ("mixed", 2e-6)])
-@pytest.mark.parametrize("n", [8, 16])
+@pytest.mark.parametrize("n", [8, 16, (10, 8, 12), (5, 7, 9), 64])
 def test_level0_apply_residual(ih, orc, precision, tol, n):
-    nv = n ** 3
+    nv = int(np.prod(n)) if not np.isscalar(n) else n ** 3
     rho = mt_uniform(nv, 1, 1e-3, 1.0)
     hom = make_hom(ih, n, precision, penal=3.0)
     hom.set_density(rho)
@@ -73,8 +73,9 @@ def test_level0_apply_residual(ih, orc, precision, tol, n):
 
 
 @pytest.mark.parametrize("precision,tol", [("double", 1e-11), ("mixed", 2e-6)])
-def test_level0_gauss_seidel_sweep(ih, orc, precision, tol):
-    n, nv = 8, 512
+@pytest.mark.parametrize("n", [8, (10, 8, 12), 32])
+def test_level0_gauss_seidel_sweep(ih, orc, precision, tol, n):
+    nv = int(np.prod(n)) if not np.isscalar(n) else n ** 3
     rho = mt_uniform(nv, 3, 1e-3, 1.0)
     hom = make_hom(ih, n, precision)
     hom.set_density(rho)
@@ -208,8 +209,9 @@ def test_laminate_harmonic_mean(ih):
 def test_tensor_and_sensitivity_vs_oracle(ih, orc, precision, tol):
     n = 8
     rho = mt_uniform(512, 1008, 1e-3, 1.0)
-    hom = make_hom(ih, n, precision, tol=1e-10, max_cycles=200)
-    oh = orc.Homogenizer(n, E=E, nu=NU, penal=3.0, mixed=precision == "mixed", tol=1e-10, max_cycles=200)
+    stol = 1e-10 if precision == "double" else 1e-6  # f32 stencils bound the mixed-mode residual
+    hom = make_hom(ih, n, precision, tol=stol, max_cycles=200)
+    oh = orc.Homogenizer(n, E=E, nu=NU, penal=3.0, mixed=precision == "mixed", tol=stol, max_cycles=200)
     hom.set_density(rho)
     oh.set_density(rho)
     s1, s2 = hom.solve_cell_problems(), oh.solve_cell_problems()

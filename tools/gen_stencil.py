@@ -117,6 +117,18 @@ def main():
     for key, (f, al, be) in terms.items():
         used[key] = build(f)
     nclass = len(classes)
+    # self-check: rebuild every merged block from (form, sign, class) and compare with the direct merge
+    lam_t, mu_t = 0.37, 1.91
+    q = np.random.default_rng(0).uniform(0.1, 1.0, 8)
+    K = lam_t * A + mu_t * B
+    for (n, r, c), (f, al, be) in terms.items():
+        direct = sum(q[ke] * K[3 * (7 - ke) + r, 3 * j + c] for ke in range(8) for j in range(8) if ngb(ke, j) == n)
+        k, cs = cls_of[(n, r, c)]
+        kap = lam_t * classes[k][0] + mu_t * classes[k][1]
+        assert abs(cs * kap * np.dot(f, q) - direct) < 1e-12 * max(1.0, abs(direct)), (n, r, c)
+    # probes to recover lam', mu' from K0 on the device side: K0[i][j] = a lam' + b mu'
+    probes = [(0, 0, int(A[0, 0]), int(B[0, 0])), (0, 1, int(A[0, 1]), int(B[0, 1]))]
+    assert probes[0][2] * probes[1][3] - probes[0][3] * probes[1][2] != 0
     out = []
     out.append("// ku_gen.cuh -- GENERATED by tools/gen_stencil.py; do not edit.")
     out.append("// Level-0 vertex stencil in factored form (see the generator's docstring).")
@@ -127,6 +139,8 @@ def main():
     out.append("// kappa_k = lam' * alpha_k + mu' * beta_k")
     out.append("constexpr int kKappaAlpha[kKappaClasses] = {" + ", ".join(str(c[0]) for c in classes) + "};")
     out.append("constexpr int kKappaBeta[kKappaClasses] = {" + ", ".join(str(c[1]) for c in classes) + "};")
+    out.append("// K0[i][j] = a lam' + b mu' for these two entries (recovers lam', mu' from K0)")
+    out.append("constexpr int kK0Probe[2][4] = {" + ", ".join("{%d, %d, %d, %d}" % p for p in probes) + "};")
     for split in (False, True):
         fname = "ku_vertex_split" if split else "ku_vertex"
         out.append("")

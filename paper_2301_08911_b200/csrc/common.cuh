@@ -202,6 +202,49 @@ __host__ __device__ __forceinline__ size_t st_index(int k, unsigned loc) {
 }
 inline size_t stencil_alloc(long long nv) { return (size_t)((nv + 31) / 32) * 32 * 243; }
 
+// On every smoothed level all n_k are even, so the 8 colour blocks share dims
+// d_k = n_k/2 and size B = d0 d1 d2 (base[c] = c B). For a vertex of colour
+// o = (o0,o1,o2) at halved (h0,h1,h2), neighbour t has location
+//   loc(t) = A0[t0] + A1[t1] + A2[t2],
+//   A_k[t] = ((o_k ^ (t != 0)) << k) B + s_k * half_k(t),
+// half_k(0) = h_k, half_k(-1) = o_k ? h_k : h_k - 1 (wrapped), half_k(+1) = o_k ? h_k + 1 (wrapped) : h_k,
+// s = (1, d0, d0 d1). One IADD3 per neighbour; AoS nodal data then gives the three
+// components at immediate offsets. Incident elements likewise: e = E0[a] + E1[b] + E2[c].
+struct FastAddr {
+  unsigned A[3][3];  // [axis][t+1]
+  unsigned E[3][2];  // [axis][bit]: element coordinate x-1 (bit 0) or x (bit 1), pre-scaled
+};
+
+__device__ __forceinline__ void fast_addr(const GridGeo& g, int color, int h0, int h1, int h2, FastAddr& fa) {
+  const unsigned B = (unsigned)g.size[0];
+  const int h[3] = {h0, h1, h2};
+  const unsigned d[3] = {(unsigned)g.cd[0][0], (unsigned)g.cd[0][1], (unsigned)g.cd[0][2]};
+  const unsigned sc[3] = {1u, d[0], d[0] * d[1]};
+  const unsigned es[3] = {1u, (unsigned)g.n[0], (unsigned)g.n[0] * (unsigned)g.n[1]};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int o = (color >> k) & 1;
+    const unsigned hm = o ? (unsigned)h[k] : (h[k] == 0 ? d[k] - 1 : (unsigned)h[k] - 1);
+    const unsigned hp = o ? ((unsigned)h[k] + 1 == d[k] ? 0u : (unsigned)h[k] + 1) : (unsigned)h[k];
+    const unsigned same = ((unsigned)o << k) * B, other = ((unsigned)(o ^ 1) << k) * B;
+    fa.A[k][0] = other + sc[k] * hm;
+    fa.A[k][1] = same + sc[k] * (unsigned)h[k];
+    fa.A[k][2] = other + sc[k] * hp;
+    const int x = 2 * h[k] + o, nk = g.n[k];
+    fa.E[k][0] = es[k] * (unsigned)(x == 0 ? nk - 1 : x - 1);
+    fa.E[k][1] = es[k] * (unsigned)x;
+  }
+}
+
+inline bool fast_ok(const GridGeo& g) {
+  return g.n[0] % 2 == 0 && g.n[1] % 2 == 0 && g.n[2] % 2 == 0 && g.n[0] >= 8;
+}
+inline dim3 fast_block(const GridGeo& g) {
+  const int d0 = g.cd[0][0];
+  const int bx = d0 >= 32 ? 32 : (d0 >= 16 ? 16 : (d0 >= 8 ? 8 : 4));
+  return dim3(bx, 128 / bx, 1);
+}
+
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 }  // namespace ihomgpu

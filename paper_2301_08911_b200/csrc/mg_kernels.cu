@@ -38,8 +38,97 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
   for (int c = 0; c < 3; ++c) fc[3 * loc + c] = TN(acc[c]);
 }
 
+// Fast even-grid transfers. Restriction: coarse vertex vc is the fine colour-0
+// vertex with halved coordinates vc, so its 27 fine neighbours are FastAddr of
+// (fine grid, colour 0, h = vc). Prolongation: per axis 1 (even) or 2 (odd)
+// coarse parents; colour-specialised so the loop bounds are compile-time.
+template <typename TN>
+__global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf,
+                                                            TN* __restrict__ fc) {
+  const int d2 = gc.cd[0][2];
+  const int color = blockIdx.z / d2;
+  const int h2 = blockIdx.z - color * d2;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+  const int cx = 2 * h0 + (color & 1), cy = 2 * h1 + ((color >> 1) & 1), cz = 2 * h2 + ((color >> 2) & 1);
+  FastAddr fa;
+  fast_addr(gf, 0, cx, cy, cz, fa);
+  double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int n = 0; n < 27; ++n) {
+    const int dx = n % 3 - 1, dy = (n / 3) % 3 - 1, dz = n / 9 - 1;
+    const double w = tw1(dx) * tw1(dy) * tw1(dz);
+    const TN* r = rf + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] += w * double(__ldg(r + c));
+  }
+  const size_t loc = (size_t)color * gc.size[0] + h0 + (size_t)gc.cd[0][0] * (h1 + (size_t)gc.cd[0][1] * h2);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) fc[3 * loc + c] = TN(acc[c]);
+}
+
+template <typename TN, int O0, int O1, int O2>
+__device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1, int h2, const TN* __restrict__ uc,
+                                               double acc[3]) {
+  const int o[3] = {O0, O1, O2};
+  const int h[3] = {h0, h1, h2};
+  const unsigned Bc = (unsigned)gc.size[0];
+  const unsigned sc[3] = {1u, (unsigned)gc.cd[0][0], (unsigned)gc.cd[0][0] * (unsigned)gc.cd[0][1]};
+  unsigned P[3][2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {  // coarse coordinate c -> ((c & 1) << k) Bc + sc_k (c >> 1)
+    const int c0 = h[k];
+    const int c1 = (h[k] + 1 == gc.n[k]) ? 0 : h[k] + 1;
+    P[k][0] = (((unsigned)c0 & 1u) << k) * Bc + sc[k] * (unsigned)(c0 >> 1);
+    P[k][1] = (((unsigned)c1 & 1u) << k) * Bc + sc[k] * (unsigned)(c1 >> 1);
+  }
+  const double w = (O0 ? 0.5 : 1.0) * (O1 ? 0.5 : 1.0) * (O2 ? 0.5 : 1.0);
+#pragma unroll
+  for (int a = 0; a < 1 + O0; ++a)
+#pragma unroll
+    for (int b = 0; b < 1 + O1; ++b)
+#pragma unroll
+      for (int c = 0; c < 1 + O2; ++c) {
+        const TN* u = uc + 3 * (size_t)(P[0][a] + P[1][b] + P[2][c]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) acc[d] += w * double(__ldg(u + d));
+      }
+  (void)o;
+}
+
+template <typename TN>
+__global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc,
+                                                           TN* __restrict__ uf) {
+  const int d2 = gf.cd[0][2];
+  const int color = blockIdx.z / d2;
+  const int h2 = blockIdx.z - color * d2;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
+  double acc[3] = {0.0, 0.0, 0.0};
+  switch (color) {  // uniform per block
+    case 0: prolong_vertex<TN, 0, 0, 0>(gc, h0, h1, h2, uc, acc); break;
+    case 1: prolong_vertex<TN, 1, 0, 0>(gc, h0, h1, h2, uc, acc); break;
+    case 2: prolong_vertex<TN, 0, 1, 0>(gc, h0, h1, h2, uc, acc); break;
+    case 3: prolong_vertex<TN, 1, 1, 0>(gc, h0, h1, h2, uc, acc); break;
+    case 4: prolong_vertex<TN, 0, 0, 1>(gc, h0, h1, h2, uc, acc); break;
+    case 5: prolong_vertex<TN, 1, 0, 1>(gc, h0, h1, h2, uc, acc); break;
+    case 6: prolong_vertex<TN, 0, 1, 1>(gc, h0, h1, h2, uc, acc); break;
+    default: prolong_vertex<TN, 1, 1, 1>(gc, h0, h1, h2, uc, acc); break;
+  }
+  const size_t loc = (size_t)color * gf.size[0] + h0 + (size_t)gf.cd[0][0] * (h1 + (size_t)gf.cd[0][1] * h2);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) uf[3 * loc + d] = TN(double(uf[3 * loc + d]) + acc[d]);
+}
+
 template <typename TN>
 void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s) {
+  if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
+    const dim3 b = fast_block(gc);
+    const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 8 * gc.cd[0][2]);
+    restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, fc);
+    IHOM_LAUNCH_CHECK();
+    return;
+  }
   restrict_kernel<TN><<<ceil_div(gc.nv, 128), 128, 0, s>>>(gf, gc, rf, fc);
   IHOM_LAUNCH_CHECK();
 }
@@ -81,6 +170,13 @@ __global__ void prolong_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc
 
 template <typename TN>
 void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s) {
+  if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
+    const dim3 b = fast_block(gf);
+    const dim3 gr(ceil_div(gf.cd[0][0], b.x), ceil_div(gf.cd[0][1], b.y), 8 * gf.cd[0][2]);
+    prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, uf);
+    IHOM_LAUNCH_CHECK();
+    return;
+  }
   prolong_kernel<TN><<<ceil_div(gf.nv, 128), 128, 0, s>>>(gc, gf, uc, uf);
   IHOM_LAUNCH_CHECK();
 }
@@ -119,9 +215,87 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   }
 }
 
+// Fast even-grid variants (FastAddr, common.cuh): one IADD3 per neighbour
+// location, AoS components at immediate offsets, blocked stencil rows.
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st,
+                                                                 const TN* __restrict__ x, const TN* __restrict__ f,
+                                                                 TN* __restrict__ y) {
+  const int d2 = g.cd[0][2];
+  const int color = blockIdx.z / d2;
+  const int h2 = blockIdx.z - color * d2;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  const TS* row = st + st_index(0, loc);
+  double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int n = 0; n < 27; ++n) {
+    const TN* xn = x + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+    const double a = double(__ldg(xn)), b = double(__ldg(xn + 1)), c = double(__ldg(xn + 2));
+    const TS* bl = row + 32 * 9 * n;
+    acc[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
+    acc[1] += double(__ldg(bl + 96)) * a + double(__ldg(bl + 128)) * b + double(__ldg(bl + 160)) * c;
+    acc[2] += double(__ldg(bl + 192)) * a + double(__ldg(bl + 224)) * b + double(__ldg(bl + 256)) * c;
+  }
+  if (f) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[3 * (size_t)loc + c] = TN(double(f[3 * (size_t)loc + c]) - acc[c]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[3 * (size_t)loc + c] = TN(acc[c]);
+  }
+}
+
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st,
+                                                              const TN* __restrict__ f, const TN* __restrict__ ur,
+                                                              TN* uw, int color, int* err) {
+  const int h2 = blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  const TS* row = st + st_index(0, loc);
+  double m[3] = {0.0, 0.0, 0.0}, S[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) S[e] = double(__ldg(row + 32 * (9 * 13 + e)));
+#pragma unroll
+  for (int n = 0; n < 27; ++n) {
+    if (n == 13) continue;
+    const TN* un = ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+    const double a = double(__ldg(un)), b = double(__ldg(un + 1)), c = double(__ldg(un + 2));
+    const TS* bl = row + 32 * 9 * n;
+    m[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
+    m[1] += double(__ldg(bl + 96)) * a + double(__ldg(bl + 128)) * b + double(__ldg(bl + 160)) * c;
+    m[2] += double(__ldg(bl + 192)) * a + double(__ldg(bl + 224)) * b + double(__ldg(bl + 256)) * c;
+  }
+  const double rhs[3] = {double(f[3 * (size_t)loc]) - m[0], double(f[3 * (size_t)loc + 1]) - m[1],
+                         double(f[3 * (size_t)loc + 2]) - m[2]};
+  const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
+                     S[2] * (S[3] * S[7] - S[4] * S[6]);
+  if (det == 0.0 || !isfinite(det)) {
+    atomicExch(err, 1);
+    return;
+  }
+  double out[3];
+  solve3(S, rhs, out);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) uw[3 * (size_t)loc + c] = TN(out[c]);
+}
+
 template <typename TS, typename TN>
 void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s) {
-  stencil_apply_kernel<TS, TN><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, x, f, y);
+  if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+    stencil_apply_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, x, f, y);
+  } else {
+    stencil_apply_kernel<TS, TN><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, x, f, y);
+  }
   IHOM_LAUNCH_CHECK();
 }
 
@@ -170,7 +344,13 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
                              cudaStream_t s) {
-  stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+  if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
+    stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, u, color, err);
+  } else {
+    stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+  }
   IHOM_LAUNCH_CHECK();
 }
 
@@ -204,44 +384,41 @@ void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
 }
 
 // assemble_stencil_from_elements (src/multigrid.cpp:281-305): one thread per
-// coarse vertex; the 64 fine-element coefficients are staged per thread in
-// shared memory ([64][blockDim] to keep banks conflict-free).
-constexpr int kGalThreads = 64;
+// (coarse vertex, output neighbour n), blockIdx.y = n, so a warp walks the same
+// constant-memory term list (oidx, W[9]) and accumulates 9 f64 entries from the
+// f32/f64 coefficients of the fine elements it names (L1-resident reuse).
 template <typename TC>
-__global__ void __launch_bounds__(kGalThreads) gal_elem_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
-                                                               TC* __restrict__ st) {
-  __shared__ double qs[64][kGalThreads];
+__global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
+                                                       TC* __restrict__ st) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = loc < gc.nv;
-  const int t = threadIdx.x;
-  int x = 0, y = 0, z = 0;
-  if (active) {
-    const int color = color_at(gc, loc);
-    block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
-    for (int oz = -2; oz <= 1; ++oz)
-      for (int oy = -2; oy <= 1; ++oy)
-        for (int ox = -2; ox <= 1; ++ox) {
-          const int oidx = (ox + 2) + 4 * ((oy + 2) + 4 * (oz + 2));
-          const unsigned e = eidx(gf, wrapi(2 * x + ox, gf.n[0]), wrapi(2 * y + oy, gf.n[1]), wrapi(2 * z + oz, gf.n[2]));
-          qs[oidx][t] = double(coeff[e]);
-        }
-  }
-  if (!active) return;
-  for (int n = 0; n < 27; ++n) {
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int k = c_eg_start[n]; k < c_eg_start[n + 1]; ++k) {
-      const double q = qs[c_eg_oidx[k]][t];
+  const int n = blockIdx.y;
+  if (loc >= gc.nv) return;
+  const int color = color_at(gc, loc);
+  int x, y, z;
+  block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
+  // wrapped fine coordinates 2*vc + o for o in {-2..1} per axis
+  int ex[4], ey[4], ez[4];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) acc[e] += q * c_eg_w[k][e];
-    }
-#pragma unroll
-    for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, (unsigned)loc)] = TC(acc[e]);
+  for (int o = 0; o < 4; ++o) {
+    ex[o] = wrapi(2 * x + o - 2, gf.n[0]);
+    ey[o] = gf.n[0] * wrapi(2 * y + o - 2, gf.n[1]);
+    ez[o] = gf.n[0] * gf.n[1] * wrapi(2 * z + o - 2, gf.n[2]);
   }
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int k1 = c_eg_start[n + 1];
+  for (int k = c_eg_start[n]; k < k1; ++k) {
+    const int oi = c_eg_oidx[k];
+    const double q = double(__ldg(coeff + (ex[oi & 3] + ey[(oi >> 2) & 3] + ez[oi >> 4])));
+#pragma unroll
+    for (int e = 0; e < 9; ++e) acc[e] += q * c_eg_w[k][e];
+  }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, (unsigned)loc)] = TC(acc[e]);
 }
 
 template <typename TC>
 void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s) {
-  gal_elem_kernel<TC><<<ceil_div(gc.nv, kGalThreads), kGalThreads, 0, s>>>(gf, gc, coeff, st);
+  gal_elem_kernel<TC><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, coeff, st);
   IHOM_LAUNCH_CHECK();
 }
 

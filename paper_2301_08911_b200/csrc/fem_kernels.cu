@@ -126,9 +126,9 @@ template <typename TC, typename TN, typename TA>
 __global__ void __launch_bounds__(128) l0_apply_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
                                                             const TN* __restrict__ u, const TN* __restrict__ f,
                                                             TN* __restrict__ y) {
-  const int d2 = g.cd[0][2];
-  const int color = blockIdx.z / d2;
-  const int h2 = blockIdx.z - color * d2;
+  // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
   FastAddr fa;
@@ -144,6 +144,49 @@ __global__ void __launch_bounds__(128) l0_apply_fast_kernel(GridGeo g, const TC*
   } else {
 #pragma unroll
     for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+  }
+}
+
+// Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
+// f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
+// plus deterministic per-block partial sums of |r|^2 (the convergence norm).
+// Replaces residual + dot + convert (136 -> 64 B/vertex).
+template <typename TC>
+__global__ void __launch_bounds__(128) l0_residual_norm_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                    const double* __restrict__ u,
+                                                                    const double* __restrict__ f,
+                                                                    float* __restrict__ r32, double* partials) {
+  __shared__ double red[4];
+  // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  double ss = 0.0;
+  if (h0 < g.cd[0][0] && h1 < g.cd[0][1]) {
+    using TA = double;
+    FastAddr fa;
+    fast_addr(g, color, h0, h1, h2, fa);
+    TA q[8];
+    load_q_fast(coeff, fa, q);
+    TA acc[3];
+    ku_vertex<TA>(q, kappa<TA>(), FAST_U(u), acc);
+    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double r = f[3 * loc + c] - acc[c];
+      r32[3 * loc + c] = float(r);
+      ss += r * r;
+    }
+  }
+  // block reduction in a fixed order (warp shuffles, then 4 warps)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((t & 31) == 0) red[t >> 5] = ss;
+  __syncthreads();
+  if (t == 0) {
+    const size_t bid = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    partials[bid] = (red[0] + red[1]) + (red[2] + red[3]);
   }
 }
 
@@ -287,6 +330,17 @@ __global__ void macro_force_kernel(GridGeo g, const TC* __restrict__ coeff, int 
 }
 
 template <typename TC>
+long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
+                                  double* partials, cudaStream_t s) {
+  if (!fast_ok(g)) throw std::invalid_argument("fused residual needs an even level-0 grid");
+  const dim3 b = fast_block(g);
+  const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+  l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  IHOM_LAUNCH_CHECK();
+  return (long long)gr.x * gr.y * gr.z;
+}
+
+template <typename TC>
 void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s) {
   macro_force_kernel<TC><<<ceil_div(g.nv, 256), 256, 0, s>>>(g, coeff, load, f);
   IHOM_LAUNCH_CHECK();
@@ -297,6 +351,8 @@ template void launch_coeff<float>(const double*, float*, long long, double, cuda
 template void launch_coeff<double>(const double*, double*, long long, double, cudaStream_t);
 template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t);
 template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t);
+template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, const double*, const double*, float*,
+                                                  double*, cudaStream_t);
 
 #define INST_L0(TC, TN, TA)                                                                                    \
   template void launch_l0_apply<TC, TN, TA>(const GridGeo&, const TC*, const TN*, const TN*, TN*, cudaStream_t); \

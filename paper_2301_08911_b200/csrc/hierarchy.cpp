@@ -408,17 +408,45 @@ void Hierarchy<T>::coarsest_f32() {
 }
 
 template <typename T>
+double Hierarchy<T>::defect_residual() {
+  Level& L0 = levels_[0];
+  if constexpr (std::is_same_v<T, float>) {
+    if (!npart_.p) npart_.alloc(size_t(L0.g.nv / 32 + 1024));
+    long long nb;
+    {
+      ProfScope p(s_, "l0_residual_f64", double(L0.g.nv) * (48.0 + sizeof(T) + 12.0));
+      nb = launch_l0_residual_norm<float>(L0.g, coeff_.p, level_u(0), L0.f.p, L0.ef.p, npart_.p, s_);
+    }
+    {
+      ProfScope p(s_, "reduce", double(nb) * 8.0);
+      launch_sum(npart_.p, nb, ws_.partials, ws_.scalars + 4, s_);
+    }
+    launches_ += 3;
+    IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    return std::sqrt(h_pinned_[0]);
+  } else {
+    throw StateError("defect residual exists in mixed precision only");
+  }
+}
+
+template <typename T>
 double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
   ensure_inner();
   const int lmax = num_levels() - 1;
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
-  // inner right-hand side: the current outer residual. Inside solve() it is
-  // current (computed before the loop and at the end of every cycle).
-  if (!u0_bound_) compute_residual(0);
-  {
-    ProfScope p(s_, "vector", double(n0) * 12.0);
-    launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+  // inner right-hand side ef0 = float(f - K u): inside solve() it is left current
+  // by the fused residual at the end of the previous cycle (or before the loop).
+  const bool fast = fast_ok(L0.g);
+  if (!u0_bound_ || !fast) {
+    if (fast) {
+      defect_residual();
+    } else {
+      compute_residual(0);
+      ProfScope p(s_, "vector", double(n0) * 12.0);
+      launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+    }
   }
   IHOM_CUDA(cudaMemsetAsync(L0.eu.p, 0, sizeof(float) * n0, s_));
   launches_ += 1;
@@ -449,9 +477,14 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
     launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
   }
   ++launches_;
-  compute_residual(0);
+  double rn;
+  if (fast) {
+    rn = defect_residual();  // also leaves ef0 ready for the next cycle
+  } else {
+    compute_residual(0);
+    rn = norm(L0.r.p, n0);
+  }
   const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(L0.f.p, n0);
-  const double rn = norm(L0.r.p, n0);
   check_error("v_cycle");
   return fn > 0.0 ? rn / fn : 0.0;
 }
@@ -472,8 +505,17 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts) {  //
       u0_bound_ = nullptr;
       return st;
     }
-    compute_residual(0);
-    st.rel_residual = norm(L0.r.p, n0) / fnorm0_;
+    if (opts.mode == kMixedDefect && std::is_same_v<T, float> && fast_ok(L0.g)) {
+      ensure_inner();
+      st.rel_residual = defect_residual() / fnorm0_;  // ef0 now holds the inner right-hand side
+    } else {
+      compute_residual(0);
+      st.rel_residual = norm(L0.r.p, n0) / fnorm0_;
+      if (opts.mode == kMixedDefect && std::is_same_v<T, float>) {
+        ensure_inner();
+        launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+      }
+    }
     while (st.rel_residual > opts.tol && st.cycles < opts.max_cycles) {
       st.rel_residual = v_cycle(opts);
       ++st.cycles;

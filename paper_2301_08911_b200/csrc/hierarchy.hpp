@@ -145,6 +145,7 @@ class Hierarchy {
   void relax_f32(int l, int sweeps);
   void residual_f32(int l);
   void coarsest_f32();
+  double defect_residual();  // ef0 = float(f0 - K u0), returns ||f0 - K u0||
 
   Material mat_;
   double penal_;
@@ -161,6 +162,7 @@ class Hierarchy {
   double fnorm0_ = 0.0;
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;
+  DevBuf<double> npart_;  // per-block |r|^2 partials of the fused defect residual
   Workspace ws_;
   double* h_pinned_ = nullptr;  // small pinned read-back buffer
   long long launches_ = 0;

@@ -30,6 +30,11 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s);
 
+// Fused defect residual: r32 = float(f - K u) (f64 arithmetic), per-block |r|^2 partials; returns #partials.
+template <typename TC>
+long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
+                                  double* partials, cudaStream_t s);
+
 template <typename TC>
 void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s);
 
@@ -73,6 +78,7 @@ void launch_axpy_update(double* u, const TN* e, long long n, cudaStream_t s);
 template <typename TI, typename TO>
 void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s);
 constexpr int kReducePartials = 1184;  // 8 * 148: capacity of the partials buffer (per component)
+void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s);
 void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s);
 void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s);
 

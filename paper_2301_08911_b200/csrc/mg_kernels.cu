@@ -45,9 +45,8 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
 template <typename TN>
 __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf,
                                                             TN* __restrict__ fc) {
-  const int d2 = gc.cd[0][2];
-  const int color = blockIdx.z / d2;
-  const int h2 = blockIdx.z - color * d2;
+  const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
   const int cx = 2 * h0 + (color & 1), cy = 2 * h1 + ((color >> 1) & 1), cz = 2 * h2 + ((color >> 2) & 1);
@@ -99,9 +98,8 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
 template <typename TN>
 __global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc,
                                                            TN* __restrict__ uf) {
-  const int d2 = gf.cd[0][2];
-  const int color = blockIdx.z / d2;
-  const int h2 = blockIdx.z - color * d2;
+  const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
   double acc[3] = {0.0, 0.0, 0.0};
@@ -221,9 +219,9 @@ template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st,
                                                                  const TN* __restrict__ x, const TN* __restrict__ f,
                                                                  TN* __restrict__ y) {
-  const int d2 = g.cd[0][2];
-  const int color = blockIdx.z / d2;
-  const int h2 = blockIdx.z - color * d2;
+  // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
   FastAddr fa;

@@ -127,6 +127,22 @@ void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s) {
   IHOM_LAUNCH_CHECK();
 }
 
+__global__ void __launch_bounds__(kRT) sum_kernel_r(const double* __restrict__ a, long long n, double* partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT) s += a[i];
+  const double r = block_reduce(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s) {
+  const int g = reduce_grid(n);
+  sum_kernel_r<<<g, kRT, 0, s>>>(a, n, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
 template void launch_comp_sums<double>(const double*, long long, double*, double*, cudaStream_t);
 template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t);
 template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t);

@@ -154,21 +154,23 @@ __host__ __device__ constexpr int pair_ngb(int ke, int j) {
 // Partial-pivoting 3x3 solve, src/fem.cpp:72-94: same elimination order and
 // pivot choice (first strictly larger |a| wins), written with register row
 // swaps instead of an index array so nothing spills to local memory.
-__device__ __forceinline__ void swap_rows(double* a, double* b, double& ra, double& rb, bool doit) {
+template <typename R>
+__device__ __forceinline__ void swap_rows(R* a, R* b, R& ra, R& rb, bool doit) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double t = a[k];
+    const R t = a[k];
     a[k] = doit ? b[k] : a[k];
     b[k] = doit ? t : b[k];
   }
-  const double t = ra;
+  const R t = ra;
   ra = doit ? rb : ra;
   rb = doit ? t : rb;
 }
 
-__device__ __forceinline__ void solve3(const double m[9], const double rhs[3], double out[3]) {
-  double r0[3] = {m[0], m[1], m[2]}, r1[3] = {m[3], m[4], m[5]}, r2[3] = {m[6], m[7], m[8]};
-  double b0 = rhs[0], b1 = rhs[1], b2 = rhs[2];
+template <typename R>
+__device__ __forceinline__ void solve3(const R m[9], const R rhs[3], R out[3]) {
+  R r0[3] = {m[0], m[1], m[2]}, r1[3] = {m[3], m[4], m[5]}, r2[3] = {m[6], m[7], m[8]};
+  R b0 = rhs[0], b1 = rhs[1], b2 = rhs[2];
   {  // column 0: pivot row = first strictly largest |a_r0| (swap(piv[0], piv[best]))
     const bool s1 = fabs(r1[0]) > fabs(r0[0]);
     const bool s2 = fabs(r2[0]) > (s1 ? fabs(r1[0]) : fabs(r0[0]));
@@ -176,18 +178,18 @@ __device__ __forceinline__ void solve3(const double m[9], const double rhs[3], d
     swap_rows(r0, r1, b0, b1, s1 && !s2);
   }
   {
-    const double f1 = r1[0] / r0[0];
+    const R f1 = r1[0] / r0[0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) r1[k] -= f1 * r0[k];
     b1 -= f1 * b0;
-    const double f2 = r2[0] / r0[0];
+    const R f2 = r2[0] / r0[0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) r2[k] -= f2 * r0[k];
     b2 -= f2 * b0;
   }
   swap_rows(r1, r2, b1, b2, fabs(r2[1]) > fabs(r1[1]));
   {
-    const double f2 = r2[1] / r1[1];
+    const R f2 = r2[1] / r1[1];
 #pragma unroll
     for (int k = 1; k < 3; ++k) r2[k] -= f2 * r1[k];
     b2 -= f2 * b1;

@@ -147,6 +147,116 @@ __global__ void __launch_bounds__(128) l0_apply_fast_kernel(GridGeo g, const TC*
   }
 }
 
+// ---------------------------------------------------------------- shared-memory tiled variants
+// A block owns a TX x TY x TZ tile (halved coordinates) of one colour c. The
+// neighbours of its vertices live in the 8 colour blocks c ^ m; along axis k the
+// needed halved range is the tile itself (bit k of m clear) or the tile plus one
+// (bit set), starting at h0 - 1 for even parity and h0 for odd. Every region is
+// staged in a padded (TX+1)(TY+1)(TZ+1) smem slot with bulk coalesced loads; a
+// neighbour t then sits at  slot(m(t)) + ((lz + [t2=1]) EY + ly + [t1=1]) EX + lx + [t0=1]
+// -- a compile-time offset from one per-thread base (no per-neighbour global
+// address math, no dependent global-load chains).
+constexpr int kTX = 32, kTY = 4, kTZ = 1;
+constexpr int kEX = kTX + 1, kEY = kTY + 1, kEZ = kTZ + 1;
+constexpr int kSlot = kEX * kEY * kEZ;  // vertices per padded region
+
+template <typename TN>
+__device__ __forceinline__ void stage_tile(const GridGeo& g, int color, int h0x, int h0y, int h0z,
+                                           const TN* __restrict__ u, TN* sm, bool skip_self) {
+  const unsigned B = (unsigned)g.size[0];
+  const int d0 = g.cd[0][0], d1 = g.cd[0][1], d2 = g.cd[0][2];
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  const int nthr = blockDim.x * blockDim.y;
+  for (int m = 0; m < 8; ++m) {
+    if (skip_self && m == 0) continue;
+    const int b0 = m & 1, b1 = (m >> 1) & 1, b2 = (m >> 2) & 1;
+    const int ex = kTX + b0, ey = kTY + b1, ez = kTZ + b2;
+    // start of the needed halved range per axis
+    const int sx = b0 ? h0x - ((color & 1) ? 0 : 1) : h0x;
+    const int sy = b1 ? h0y - (((color >> 1) & 1) ? 0 : 1) : h0y;
+    const int sz = b2 ? h0z - (((color >> 2) & 1) ? 0 : 1) : h0z;
+    const unsigned cb = (unsigned)(color ^ m) * B;
+    TN* dst = sm + 3 * m * kSlot;
+    const int cnt = ex * ey * ez * 3;
+    for (int i = tid; i < cnt; i += nthr) {
+      const int comp = i % 3, v = i / 3;
+      const int lx = v % ex, ly = (v / ex) % ey, lz = v / (ex * ey);
+      int gx = sx + lx, gy = sy + ly, gz = sz + lz;
+      gx = gx < 0 ? gx + d0 : (gx >= d0 ? gx - d0 : gx);
+      gy = gy < 0 ? gy + d1 : (gy >= d1 ? gy - d1 : gy);
+      gz = gz < 0 ? gz + d2 : (gz >= d2 ? gz - d2 : gz);
+      const unsigned loc = cb + (unsigned)gx + (unsigned)d0 * ((unsigned)gy + (unsigned)d1 * (unsigned)gz);
+      dst[3 * ((lz * kEY + ly) * kEX + lx) + comp] = __ldg(u + 3 * (size_t)loc + comp);
+    }
+  }
+}
+
+// neighbour n (27-index) of the thread's vertex, component c, from the staged tile
+#define TILE_U(sm)                                                                                      \
+  [&](int n, int c) {                                                                                   \
+    const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9 - 1;                                    \
+    const int m = (t0 != 0) | ((t1 != 0) << 1) | ((t2 != 0) << 2);                                      \
+    const int off = m * kSlot + (((t2 == 1) * kEY + (t1 == 1)) * kEX + (t0 == 1));                      \
+    return TA(sm[3 * (base + off) + c]);                                                                \
+  }
+
+// blockDim (kTX, kTY), grid (d0/kTX, d1/kTY, d2/kTZ * ncol): GS (ncol = 1, colour arg) or all colours.
+template <typename TC, typename TN, typename TA, bool GS>
+__global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                            const TN* __restrict__ u, const TN* __restrict__ f,
+                                                            TN* y, int color) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TN* sm = reinterpret_cast<TN*>(smraw);
+  int h2;
+  if (GS) {
+    h2 = blockIdx.z * kTZ;
+  } else {
+    color = blockIdx.z & 7;
+    h2 = (blockIdx.z >> 3) * kTZ;
+  }
+  const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
+  stage_tile<TN>(g, color, h0x, h0y, h2, u, sm, GS);
+  __syncthreads();
+  const int lx = threadIdx.x, ly = threadIdx.y, lz = 0;
+  const int base = (lz * kEY + ly) * kEX + lx;
+  FastAddr fa;
+  fast_addr(g, color, h0x + lx, h0y + ly, h2 + lz, fa);
+  TA q[8];
+  load_q_fast(coeff, fa, q);
+  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  if (GS) {
+    TA m[3], sblk[9];
+    ku_vertex_split<TA>(q, kappa<TA>(), TILE_U(sm), m, sblk);
+    TN S[9], rhs[3], out[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) S[e] = TN(sblk[e]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = TN(f[3 * loc + c]) - TN(m[c]);
+    solve3<TN>(S, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[3 * loc + c] = out[c];
+  } else {
+    TA acc[3];
+    ku_vertex<TA>(q, kappa<TA>(), TILE_U(sm), acc);
+    if (f) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+    }
+  }
+}
+
+static bool tile_ok(const GridGeo& g) {
+  return fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
+}
+
+template <typename TN>
+static size_t tile_smem() {
+  return sizeof(TN) * 3 * 8 * kSlot;
+}
+
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
 // plus deterministic per-block partial sums of |r|^2 (the convergence norm).
@@ -204,12 +314,14 @@ __global__ void __launch_bounds__(128) l0_gs_fast_kernel(GridGeo g, const TC* __
   TA m[3], sblk[9];
   ku_vertex_split<TA>(q, kappa<TA>(), FAST_U(ur), m, sblk);
   const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
-  double S[9], rhs[3], out[3];
+  // solve in the nodal type: f64 for f64 nodal data (reference), f32 in the f32 inner cycle
+  using TS = TN;
+  TS S[9], rhs[3], out[3];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = double(sblk[e]);
+  for (int e = 0; e < 9; ++e) S[e] = TS(sblk[e]);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) rhs[c] = double(f[3 * loc + c]) - double(m[c]);
-  solve3(S, rhs, out);
+  for (int c = 0; c < 3; ++c) rhs[c] = TS(f[3 * loc + c]) - TS(m[c]);
+  solve3<TS>(S, rhs, out);
 #pragma unroll
   for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }
@@ -258,7 +370,13 @@ __global__ void __launch_bounds__(128) l0_apply_kernel(GridGeo g, const TC* __re
 
 template <typename TC, typename TN, typename TA>
 void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s) {
-  if (fast_ok(g)) {
+  if (tile_ok(g)) {
+    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
+    const size_t sm = tile_smem<TN>();
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    l0_tile_kernel<TC, TN, TA, false><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, y, 0);
+  } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
     l0_apply_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, u, f, y);
@@ -298,7 +416,13 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
 
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s) {
-  if (fast_ok(g)) {
+  if (tile_ok(g)) {
+    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, g.cd[0][2] / kTZ);
+    const size_t sm = tile_smem<TN>();
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    l0_tile_kernel<TC, TN, TA, true><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, u, color);
+  } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
     l0_gs_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);

@@ -382,19 +382,56 @@ void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
 }
 
 // assemble_stencil_from_elements (src/multigrid.cpp:281-305): one thread per
-// (coarse vertex, output neighbour n), blockIdx.y = n, so a warp walks the same
-// constant-memory term list (oidx, W[9]) and accumulates 9 f64 entries from the
-// f32/f64 coefficients of the fine elements it names (L1-resident reuse).
+// (coarse vertex, output neighbour n). blockIdx.z = n + 27 (colour + 8 h2): the 27
+// neighbours and then the 8 colours of one coarse plane run back to back, so the
+// 64 fine coefficients of a region are fetched once and reused from L1/L2. The
+// term list of n (<= 64 x (oidx, W[9])) is staged in shared memory (broadcast reads).
+constexpr int kMaxEgPerN = 64;
 template <typename TC>
 __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
                                                        TC* __restrict__ st) {
+  __shared__ double w_s[kMaxEgPerN][9];
+  __shared__ int o_s[kMaxEgPerN];
+  const int n = blockIdx.z % 27;
+  const int rest = blockIdx.z / 27;
+  const int color = rest & 7, h2 = rest >> 3;
+  const int k0 = c_eg_start[n], nt = c_eg_start[n + 1] - k0;
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  for (int i = t; i < nt * 9; i += blockDim.x * blockDim.y) w_s[i / 9][i % 9] = c_eg_w[k0 + i / 9][i % 9];
+  for (int i = t; i < nt; i += blockDim.x * blockDim.y) o_s[i] = c_eg_oidx[k0 + i];
+  __syncthreads();
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+  const int x = 2 * h0 + (color & 1), y = 2 * h1 + ((color >> 1) & 1), z = 2 * h2 + ((color >> 2) & 1);
+  int ex[4], ey[4], ez[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {  // wrapped fine coordinates 2*vc + o - 2
+    ex[o] = wrapi(2 * x + o - 2, gf.n[0]);
+    ey[o] = gf.n[0] * wrapi(2 * y + o - 2, gf.n[1]);
+    ez[o] = gf.n[0] * gf.n[1] * wrapi(2 * z + o - 2, gf.n[2]);
+  }
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < nt; ++k) {
+    const int oi = o_s[k];
+    const double q = double(__ldg(coeff + (ex[oi & 3] + ey[(oi >> 2) & 3] + ez[oi >> 4])));
+#pragma unroll
+    for (int e = 0; e < 9; ++e) acc[e] += q * w_s[k][e];
+  }
+  const unsigned loc = (unsigned)(color * gc.size[0] + h0 + (long long)gc.cd[0][0] * (h1 + (long long)gc.cd[0][1] * h2));
+#pragma unroll
+  for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, loc)] = TC(acc[e]);
+}
+
+// generic (odd coarse grids): one thread per (coarse vertex, n), term list from constant memory
+template <typename TC>
+__global__ void __launch_bounds__(128) gal_elem_generic_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
+                                                               TC* __restrict__ st) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int n = blockIdx.y;
   if (loc >= gc.nv) return;
   const int color = color_at(gc, loc);
   int x, y, z;
   block_coords(gc, color, (unsigned)(loc - gc.base[color]), x, y, z);
-  // wrapped fine coordinates 2*vc + o for o in {-2..1} per axis
   int ex[4], ey[4], ez[4];
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
@@ -403,8 +440,7 @@ __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, c
     ez[o] = gf.n[0] * gf.n[1] * wrapi(2 * z + o - 2, gf.n[2]);
   }
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int k1 = c_eg_start[n + 1];
-  for (int k = c_eg_start[n]; k < k1; ++k) {
+  for (int k = c_eg_start[n]; k < c_eg_start[n + 1]; ++k) {
     const int oi = c_eg_oidx[k];
     const double q = double(__ldg(coeff + (ex[oi & 3] + ey[(oi >> 2) & 3] + ez[oi >> 4])));
 #pragma unroll
@@ -416,7 +452,13 @@ __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, c
 
 template <typename TC>
 void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s) {
-  gal_elem_kernel<TC><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, coeff, st);
+  if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
+    const dim3 b = fast_block(gc);
+    const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
+    gal_elem_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, st);
+  } else {
+    gal_elem_generic_kernel<TC><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, coeff, st);
+  }
   IHOM_LAUNCH_CHECK();
 }
 

@@ -11,6 +11,9 @@
 #include "kernels.hpp"
 #include "ku_gen.cuh"
 
+#include <cstdlib>
+#include <string>
+
 namespace ihomgpu {
 
 __constant__ double c_blk_d[8][8][9];
@@ -160,35 +163,59 @@ constexpr int kTX = 32, kTY = 4, kTZ = 1;
 constexpr int kEX = kTX + 1, kEY = kTY + 1, kEZ = kTZ + 1;
 constexpr int kSlot = kEX * kEY * kEZ;  // vertices per padded region
 
+template <typename TN, int M>
+__device__ __forceinline__ void stage_region(const GridGeo& g, int color, int h0x, int h0y, int h0z,
+                                             const TN* __restrict__ u, TN* sm) {
+  constexpr int b0 = M & 1, b1 = (M >> 1) & 1, b2 = (M >> 2) & 1;
+  constexpr int ex = kTX + b0, ey = kTY + b1, ez = kTZ + b2;
+  constexpr int rowlen = 3 * ex;  // contiguous AoS values of one row
+  const unsigned B = (unsigned)g.size[0];
+  const int d0 = g.cd[0][0], d1 = g.cd[0][1], d2 = g.cd[0][2];
+  const int sx = b0 ? h0x - ((color & 1) ? 0 : 1) : h0x;
+  const int sy = b1 ? h0y - (((color >> 1) & 1) ? 0 : 1) : h0y;
+  const int sz = b2 ? h0z - (((color >> 2) & 1) ? 0 : 1) : h0z;
+  const unsigned cb = (unsigned)(color ^ M) * B;
+  TN* dst = sm + 3 * M * kSlot;
+  const bool xwrap = sx < 0 || sx + ex > d0;
+  // warp threadIdx.y copies rows r = threadIdx.y, +kTY, ...; lanes stride the row
+#pragma unroll
+  for (int r0 = 0; r0 < ey * ez; r0 += kTY) {
+    const int r = r0 + threadIdx.y;
+    if (r < ey * ez) {
+      const int ly = r % ey, lz = r / ey;
+      int gy = sy + ly, gz = sz + lz;
+      gy = gy < 0 ? gy + d1 : (gy >= d1 ? gy - d1 : gy);
+      gz = gz < 0 ? gz + d2 : (gz >= d2 ? gz - d2 : gz);
+      const unsigned rowloc = cb + (unsigned)d0 * ((unsigned)gy + (unsigned)d1 * (unsigned)gz);
+      TN* drow = dst + 3 * ((lz * kEY + ly) * kEX);
+      if (!xwrap) {
+        const TN* grow = u + 3 * (size_t)(rowloc + (unsigned)sx);
+#pragma unroll
+        for (int e = threadIdx.x; e < rowlen; e += kTX) drow[e] = __ldg(grow + e);
+      } else {
+#pragma unroll
+        for (int e = threadIdx.x; e < rowlen; e += kTX) {
+          const int lx = e / 3, comp = e - 3 * (e / 3);
+          int gx = sx + lx;
+          gx = gx < 0 ? gx + d0 : (gx >= d0 ? gx - d0 : gx);
+          drow[e] = __ldg(u + 3 * (size_t)(rowloc + (unsigned)gx) + comp);
+        }
+      }
+    }
+  }
+}
+
 template <typename TN>
 __device__ __forceinline__ void stage_tile(const GridGeo& g, int color, int h0x, int h0y, int h0z,
                                            const TN* __restrict__ u, TN* sm, bool skip_self) {
-  const unsigned B = (unsigned)g.size[0];
-  const int d0 = g.cd[0][0], d1 = g.cd[0][1], d2 = g.cd[0][2];
-  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
-  const int nthr = blockDim.x * blockDim.y;
-  for (int m = 0; m < 8; ++m) {
-    if (skip_self && m == 0) continue;
-    const int b0 = m & 1, b1 = (m >> 1) & 1, b2 = (m >> 2) & 1;
-    const int ex = kTX + b0, ey = kTY + b1, ez = kTZ + b2;
-    // start of the needed halved range per axis
-    const int sx = b0 ? h0x - ((color & 1) ? 0 : 1) : h0x;
-    const int sy = b1 ? h0y - (((color >> 1) & 1) ? 0 : 1) : h0y;
-    const int sz = b2 ? h0z - (((color >> 2) & 1) ? 0 : 1) : h0z;
-    const unsigned cb = (unsigned)(color ^ m) * B;
-    TN* dst = sm + 3 * m * kSlot;
-    const int cnt = ex * ey * ez * 3;
-    for (int i = tid; i < cnt; i += nthr) {
-      const int comp = i % 3, v = i / 3;
-      const int lx = v % ex, ly = (v / ex) % ey, lz = v / (ex * ey);
-      int gx = sx + lx, gy = sy + ly, gz = sz + lz;
-      gx = gx < 0 ? gx + d0 : (gx >= d0 ? gx - d0 : gx);
-      gy = gy < 0 ? gy + d1 : (gy >= d1 ? gy - d1 : gy);
-      gz = gz < 0 ? gz + d2 : (gz >= d2 ? gz - d2 : gz);
-      const unsigned loc = cb + (unsigned)gx + (unsigned)d0 * ((unsigned)gy + (unsigned)d1 * (unsigned)gz);
-      dst[3 * ((lz * kEY + ly) * kEX + lx) + comp] = __ldg(u + 3 * (size_t)loc + comp);
-    }
-  }
+  if (!skip_self) stage_region<TN, 0>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 1>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 2>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 3>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 4>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 5>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 6>(g, color, h0x, h0y, h0z, u, sm);
+  stage_region<TN, 7>(g, color, h0x, h0y, h0z, u, sm);
 }
 
 // neighbour n (27-index) of the thread's vertex, component c, from the staged tile
@@ -248,13 +275,63 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* 
   }
 }
 
+// Variant selection (IHOM_L0_KERNEL=tile|fast; default tile) so both can be measured on one box.
+static bool tile_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("IHOM_L0_KERNEL");
+    return (e && std::string(e) == "fast") ? 0 : 1;
+  }();
+  return v != 0;
+}
 static bool tile_ok(const GridGeo& g) {
-  return fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
+  return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
 }
 
 template <typename TN>
 static size_t tile_smem() {
   return sizeof(TN) * 3 * 8 * kSlot;
+}
+
+// Tiled defect residual: ef0 = float(f - K u) with f64 arithmetic + |r|^2 block partials.
+template <typename TC>
+__global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                   const double* __restrict__ u,
+                                                                   const double* __restrict__ f,
+                                                                   float* __restrict__ r32, double* partials) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* sm = reinterpret_cast<double*>(smraw);
+  __shared__ double red[4];
+  using TA = double;
+  const int color = blockIdx.z & 7;
+  const int h2 = (blockIdx.z >> 3) * kTZ;
+  const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
+  stage_tile<double>(g, color, h0x, h0y, h2, u, sm, false);
+  __syncthreads();
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int base = ly * kEX + lx;
+  FastAddr fa;
+  fast_addr(g, color, h0x + lx, h0y + ly, h2, fa);
+  TA q[8];
+  load_q_fast(coeff, fa, q);
+  TA acc[3];
+  ku_vertex<TA>(q, kappa<TA>(), TILE_U(sm), acc);
+  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  double ss = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double r = f[3 * loc + c] - acc[c];
+    r32[3 * loc + c] = float(r);
+    ss += r * r;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((t & 31) == 0) red[t >> 5] = ss;
+  __syncthreads();
+  if (t == 0) {
+    const size_t bid = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    partials[bid] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
 }
 
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
@@ -457,6 +534,15 @@ template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
                                   double* partials, cudaStream_t s) {
   if (!fast_ok(g)) throw std::invalid_argument("fused residual needs an even level-0 grid");
+  if (tile_ok(g)) {
+    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
+    const size_t sm = tile_smem<double>();
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_defect_kernel<TC>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    l0_tile_defect_kernel<TC><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, r32, partials);
+    IHOM_LAUNCH_CHECK();
+    return (long long)gr.x * gr.y * gr.z;
+  }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
   l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);

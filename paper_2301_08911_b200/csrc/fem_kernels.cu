@@ -11,6 +11,8 @@
 #include "kernels.hpp"
 #include "ku_gen.cuh"
 
+#include <cuda_pipeline.h>
+
 #include <cstdlib>
 #include <string>
 
@@ -191,14 +193,14 @@ __device__ __forceinline__ void stage_region(const GridGeo& g, int color, int h0
       if (!xwrap) {
         const TN* grow = u + 3 * (size_t)(rowloc + (unsigned)sx);
 #pragma unroll
-        for (int e = threadIdx.x; e < rowlen; e += kTX) drow[e] = __ldg(grow + e);
+        for (int e = threadIdx.x; e < rowlen; e += kTX) __pipeline_memcpy_async(drow + e, grow + e, sizeof(TN));
       } else {
 #pragma unroll
         for (int e = threadIdx.x; e < rowlen; e += kTX) {
           const int lx = e / 3, comp = e - 3 * (e / 3);
           int gx = sx + lx;
           gx = gx < 0 ? gx + d0 : (gx >= d0 ? gx - d0 : gx);
-          drow[e] = __ldg(u + 3 * (size_t)(rowloc + (unsigned)gx) + comp);
+          __pipeline_memcpy_async(drow + e, u + 3 * (size_t)(rowloc + (unsigned)gx) + comp, sizeof(TN));
         }
       }
     }
@@ -242,15 +244,17 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* 
     h2 = (blockIdx.z >> 3) * kTZ;
   }
   const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
-  stage_tile<TN>(g, color, h0x, h0y, h2, u, sm, GS);
-  __syncthreads();
+  stage_tile<TN>(g, color, h0x, h0y, h2, u, sm, GS);  // cp.async (LDGSTS): all copies in flight at once
+  __pipeline_commit();
   const int lx = threadIdx.x, ly = threadIdx.y, lz = 0;
   const int base = (lz * kEY + ly) * kEX + lx;
   FastAddr fa;
   fast_addr(g, color, h0x + lx, h0y + ly, h2 + lz, fa);
   TA q[8];
-  load_q_fast(coeff, fa, q);
+  load_q_fast(coeff, fa, q);  // overlaps the staging copies
   const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  __pipeline_wait_prior(0);
+  __syncthreads();
   if (GS) {
     TA m[3], sblk[9];
     ku_vertex_split<TA>(q, kappa<TA>(), TILE_U(sm), m, sblk);
@@ -306,13 +310,15 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, con
   const int h2 = (blockIdx.z >> 3) * kTZ;
   const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
   stage_tile<double>(g, color, h0x, h0y, h2, u, sm, false);
-  __syncthreads();
+  __pipeline_commit();
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int base = ly * kEX + lx;
   FastAddr fa;
   fast_addr(g, color, h0x + lx, h0y + ly, h2, fa);
   TA q[8];
   load_q_fast(coeff, fa, q);
+  __pipeline_wait_prior(0);
+  __syncthreads();
   TA acc[3];
   ku_vertex<TA>(q, kappa<TA>(), TILE_U(sm), acc);
   const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];

@@ -522,10 +522,49 @@ __global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc
   for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, (unsigned)loc)] = TS(acc[e]);
 }
 
+// Even coarse grid: colour-fastest blocks (blockIdx.z = n + 27 (colour + 8 h2)); the
+// 27 fine-neighbour locations of 2 vc (fine colour 0, halved vc) are computed once
+// per thread with FastAddr and kept in shared memory.
+template <typename TS>
+__global__ void __launch_bounds__(128) gal_stencil_fast_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
+                                                               TS* __restrict__ stc) {
+  __shared__ unsigned fls[27][128];
+  const int n = blockIdx.z % 27;
+  const int rest = blockIdx.z / 27;
+  const int color = rest & 7, h2 = rest >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+  const int x = 2 * h0 + (color & 1), y = 2 * h1 + ((color >> 1) & 1), z = 2 * h2 + ((color >> 2) & 1);
+  FastAddr fa;
+  fast_addr(gf, 0, x, y, z, fa);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) fls[s][tid] = fa.A[0][s % 3] + fa.A[1][(s / 3) % 3] + fa.A[2][s / 9];
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int k1 = c_sg_start[n + 1];
+  for (int k = c_sg_start[n]; k < k1; ++k) {
+    const int st = c_sg_st[k];
+    const unsigned fl = fls[st & 31][tid];
+    const double w = double(c_sg_w[k]);
+    const TS* b = stf + st_index(9 * (st >> 5), fl);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) acc[e] += w * double(__ldg(b + 32 * e));
+  }
+  const unsigned loc = (unsigned)(color * gc.size[0] + h0 + (long long)gc.cd[0][0] * (h1 + (long long)gc.cd[0][1] * h2));
+#pragma unroll
+  for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, loc)] = TS(acc[e]);
+}
+
 template <typename TS>
 void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s) {
   upload_stencil_galerkin(s);
-  gal_stencil_kernel<TS><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, stf, stc);
+  if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0 && fast_ok(gf)) {
+    const dim3 b = fast_block(gc);
+    const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
+    gal_stencil_fast_kernel<TS><<<gr, b, 0, s>>>(gf, gc, stf, stc);
+  } else {
+    gal_stencil_kernel<TS><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, stf, stc);
+  }
   IHOM_LAUNCH_CHECK();
 }
 

@@ -127,8 +127,8 @@ __device__ __forceinline__ void load_q_fast(const TC* __restrict__ coeff, const 
   }
 
 // blockDim = (bx, 128/bx), grid = (d0/bx, ceil(d1/by), d2 * ncolors)
-template <typename TC, typename TN, typename TA>
-__global__ void __launch_bounds__(128) l0_apply_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+template <typename TC, typename TN, typename TA, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) l0_apply_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
                                                             const TN* __restrict__ u, const TN* __restrict__ f,
                                                             TN* __restrict__ y) {
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
@@ -279,14 +279,23 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* 
   }
 }
 
-// Variant selection (IHOM_L0_KERNEL=tile|fast; default tile) so both can be measured on one box.
+// Variant selection (IHOM_L0_KERNEL=tile|fast; default fast: measured faster on B200, see profiles/).
 static bool tile_enabled() {
   static const int v = [] {
     const char* e = std::getenv("IHOM_L0_KERNEL");
-    return (e && std::string(e) == "fast") ? 0 : 1;
+    return (e && std::string(e) == "tile") ? 1 : 0;
   }();
   return v != 0;
 }
+// Occupancy variant (IHOM_L0_MINB=0|1): 1 caps registers for more resident warps.
+static int minb_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("IHOM_L0_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 static bool tile_ok(const GridGeo& g) {
   return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
 }
@@ -344,8 +353,8 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, con
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
 // plus deterministic per-block partial sums of |r|^2 (the convergence norm).
 // Replaces residual + dot + convert (136 -> 64 B/vertex).
-template <typename TC>
-__global__ void __launch_bounds__(128) l0_residual_norm_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+template <typename TC, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) l0_residual_norm_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
                                                                     const double* __restrict__ u,
                                                                     const double* __restrict__ f,
                                                                     float* __restrict__ r32, double* partials) {
@@ -383,8 +392,8 @@ __global__ void __launch_bounds__(128) l0_residual_norm_fast_kernel(GridGeo g, c
   }
 }
 
-template <typename TC, typename TN, typename TA>
-__global__ void __launch_bounds__(128) l0_gs_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
+template <typename TC, typename TN, typename TA, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) l0_gs_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
                                                          const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
                                                          int color) {
   const int h2 = blockIdx.z;
@@ -462,7 +471,10 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    l0_apply_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, u, f, y);
+    if (minb_variant() == 1)
+      l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 5><<<gr, b, 0, s>>>(g, coeff, u, f, y);
+    else
+      l0_apply_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, u, f, y);
   } else {
     l0_apply_kernel<TC, TN, TA><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, coeff, u, f, y);
   }
@@ -508,7 +520,10 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    l0_gs_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+    if (minb_variant() == 1)
+      l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 5><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+    else
+      l0_gs_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
   } else {
     l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
   }
@@ -551,7 +566,10 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-  l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  if (minb_variant() == 1)
+    l0_residual_norm_fast_kernel<TC, 5><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  else
+    l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }

@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--reso", type=int, default=512)
     ap.add_argument("--obj", default="npr-relaxed")
     ap.add_argument("--vol", type=float, default=0.2)
-    ap.add_argument("--mode", default="mixed_defect", choices=["vcycle", "mixed_defect"])
+    ap.add_argument("--mode", default="mixed_defect", choices=["vcycle", "mixed_defect", "pcg"])
     ap.add_argument("--precision", default="mixed", choices=["mixed", "double"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -43,7 +43,7 @@ enum {
 };
 enum { IHOM_HOST = 0, IHOM_DEVICE = 1 };
 enum { IHOM_MIXED = 0, IHOM_ALL_DOUBLE = 1 };          /* inc/config.hpp Precision */
-enum { IHOM_SOLVER_VCYCLE = 0, IHOM_SOLVER_MIXED_DEFECT = 1 };
+enum { IHOM_SOLVER_VCYCLE = 0, IHOM_SOLVER_MIXED_DEFECT = 1, IHOM_SOLVER_PCG = 2 };
 enum { IHOM_SYM_NONE = 0, IHOM_SYM_REFLECT3 = 1, IHOM_SYM_REFLECT6 = 2, IHOM_SYM_ROTATE3 = 3 };
 enum { IHOM_KERNEL_LINEAR = 0, IHOM_KERNEL_SPLINE4 = 1 };
 enum { IHOM_OBJ_BULK = 0, IHOM_OBJ_SHEAR = 1, IHOM_OBJ_NPR_RELAXED = 2, IHOM_OBJ_NPR_LOG = 3 };

@@ -34,7 +34,7 @@ kNumLoadCases = 6
 
 IHOM_HOST, IHOM_DEVICE = 0, 1
 PRECISION = {"mixed": 0, "double": 1, "all_double": 1}
-SOLVER_MODE = {"vcycle": 0, "mixed_defect": 1}
+SOLVER_MODE = {"vcycle": 0, "mixed_defect": 1, "pcg": 2}
 SYMMETRY = {"none": 0, "reflect3": 1, "reflect6": 2, "rotate3": 3}
 KERNEL = {"linear": 0, "spline4": 1}
 OBJECTIVE = {"bulk": 0, "shear": 1, "npr-relaxed": 2, "npr_relaxed": 2, "npr-log": 3, "npr_log": 3}

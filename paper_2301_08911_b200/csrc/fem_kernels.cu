@@ -287,15 +287,6 @@ static bool tile_enabled() {
   }();
   return v != 0;
 }
-// Occupancy variant (IHOM_L0_MINB=0|1): 1 caps registers for more resident warps.
-static int minb_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("IHOM_L0_MINB");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 static bool tile_ok(const GridGeo& g) {
   return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
 }
@@ -471,10 +462,9 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    if (minb_variant() == 1)
-      l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 5><<<gr, b, 0, s>>>(g, coeff, u, f, y);
-    else
-      l0_apply_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, u, f, y);
+    // f32 kernels capped at 64 registers (8 blocks/SM: more warps in flight, measured faster);
+    // f64 kernels uncapped (a cap spills and was measured slower).
+    l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, u, f, y);
   } else {
     l0_apply_kernel<TC, TN, TA><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, coeff, u, f, y);
   }
@@ -520,10 +510,7 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    if (minb_variant() == 1)
-      l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 5><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
-    else
-      l0_gs_fast_kernel<TC, TN, TA><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+    l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
   } else {
     l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
   }
@@ -566,10 +553,7 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-  if (minb_variant() == 1)
-    l0_residual_norm_fast_kernel<TC, 5><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
-  else
-    l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }

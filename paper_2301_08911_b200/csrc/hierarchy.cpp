@@ -365,11 +365,12 @@ void Hierarchy<T>::ensure_inner() {
 }
 
 template <typename T>
-void Hierarchy<T>::relax_f32(int l, int sweeps) {
+void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
     for (int sw = 0; sw < sweeps; ++sw)
-      for (int c = 0; c < 8; ++c) {
+      for (int ci = 0; ci < 8; ++ci) {
+        const int c = reverse ? 7 - ci : ci;
         if (L.g.size[c] == 0) continue;
         if (l == 0) {
           ProfScope p(s_, "l0_gs_f32", gs_l0_bytes(L.g, c, 4, 4));
@@ -430,24 +431,14 @@ double Hierarchy<T>::defect_residual() {
   }
 }
 
+// One V-cycle on K e = ef0 starting from e = 0, entirely on the f32 inner fields.
+// symmetric: post-smoothing walks the colours 7..0 (adjoint of the pre-smoother),
+// which makes the cycle an SPD preconditioner for PCG.
 template <typename T>
-double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
-  ensure_inner();
+void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
   const int lmax = num_levels() - 1;
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
-  // inner right-hand side ef0 = float(f - K u): inside solve() it is left current
-  // by the fused residual at the end of the previous cycle (or before the loop).
-  const bool fast = fast_ok(L0.g);
-  if (!u0_bound_ || !fast) {
-    if (fast) {
-      defect_residual();
-    } else {
-      compute_residual(0);
-      ProfScope p(s_, "vector", double(n0) * 12.0);
-      launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
-    }
-  }
   IHOM_CUDA(cudaMemsetAsync(L0.eu.p, 0, sizeof(float) * n0, s_));
   launches_ += 1;
   for (int l = 0; l < lmax; ++l) {
@@ -470,8 +461,103 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
                                 levels_[size_t(l)].eu.p, s_);
     }
     ++launches_;
-    relax_f32(l, opts.post_sweeps);
+    relax_f32(l, opts.post_sweeps, symmetric);
   }
+}
+
+template <typename T>
+SolveStats Hierarchy<T>::solve_pcg(double* u, const SolverOptions& opts) {
+  SolveStats st;
+  if constexpr (!std::is_same_v<T, float>) {
+    throw std::invalid_argument("MG-PCG mode needs mixed precision (f32 inner preconditioner)");
+  } else {
+    Level& L0 = levels_[0];
+    const long long nv = L0.g.nv, n0 = 3 * nv;
+    ensure_inner();
+    if (!pcg_p_.p) {
+      pcg_p_.alloc(size_t(n0));
+      pcg_q_.alloc(size_t(n0));
+      pcg_s_.alloc(8);
+    }
+    double* sc = pcg_s_.p;  // [0] rz [1] pq [2] alpha [3] beta [4] rr [5] rz_new
+    auto readback = [&](const double* d) {
+      IHOM_CUDA(cudaMemcpyAsync(h_pinned_, d, sizeof(double), cudaMemcpyDeviceToHost, s_));
+      IHOM_CUDA(cudaStreamSynchronize(s_));
+      return h_pinned_[0];
+    };
+    auto precondition = [&]() {  // eu0 = M^-1 ef0, rz_new = (r, eu0)
+      inner_vcycle(opts, true);
+      ProfScope p(s_, "reduce", double(n0) * 12.0);
+      launch_dot_df(L0.r.p, L0.eu.p, n0, ws_.partials, sc + 5, s_);
+      launches_ += 2;
+    };
+    compute_residual(0);  // r = f - K u (f64)
+    double rn = norm(L0.r.p, n0);
+    st.rel_residual = rn / fnorm0_;
+    if (st.rel_residual <= opts.tol) {
+      st.converged = true;
+      return st;
+    }
+    {
+      ProfScope p(s_, "vector", double(n0) * 12.0);
+      launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+    }
+    precondition();
+    launch_pcg_p(pcg_p_.p, L0.eu.p, sc + 3, n0, true, s_);
+    IHOM_CUDA(cudaMemcpyAsync(sc, sc + 5, sizeof(double), cudaMemcpyDeviceToDevice, s_));
+    launches_ += 1;
+    while (st.cycles < opts.max_cycles) {
+      {
+        ProfScope p(s_, "l0_apply_f64", double(nv) * (48.0 + sizeof(T)));
+        launch_l0_apply<T, double, double>(L0.g, coeff_.p, pcg_p_.p, nullptr, pcg_q_.p, s_);  // q = K p
+      }
+      {
+        ProfScope p(s_, "reduce", double(n0) * 16.0);
+        launch_dot<double>(pcg_p_.p, pcg_q_.p, n0, ws_.partials, sc + 1, s_);
+      }
+      launch_ratio(sc, sc + 1, sc + 2, s_);  // alpha = rz / pq
+      {
+        ProfScope p(s_, "vector", double(n0) * 60.0);
+        launch_pcg_ur(u, L0.r.p, pcg_p_.p, pcg_q_.p, sc + 2, L0.ef.p, n0, ws_.partials, sc + 4, s_);
+      }
+      launches_ += 6;
+      ++st.cycles;
+      st.rel_residual = std::sqrt(readback(sc + 4)) / fnorm0_;
+      check_error("pcg");
+      if (st.rel_residual <= opts.tol) break;
+      precondition();
+      launch_ratio(sc + 5, sc, sc + 3, s_);  // beta = rz_new / rz
+      IHOM_CUDA(cudaMemcpyAsync(sc, sc + 5, sizeof(double), cudaMemcpyDeviceToDevice, s_));
+      {
+        ProfScope p(s_, "vector", double(n0) * 20.0);
+        launch_pcg_p(pcg_p_.p, L0.eu.p, sc + 3, n0, false, s_);
+      }
+      launches_ += 2;
+    }
+    st.converged = st.rel_residual <= opts.tol;
+  }
+  return st;
+}
+
+template <typename T>
+double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
+  ensure_inner();
+  const int lmax = num_levels() - 1;
+  Level& L0 = levels_[0];
+  const long long n0 = 3 * L0.g.nv;
+  // inner right-hand side ef0 = float(f - K u): inside solve() it is left current
+  // by the fused residual at the end of the previous cycle (or before the loop).
+  const bool fast = fast_ok(L0.g);
+  if (!u0_bound_ || !fast) {
+    if (fast) {
+      defect_residual();
+    } else {
+      compute_residual(0);
+      ProfScope p(s_, "vector", double(n0) * 12.0);
+      launch_convert<double, float>(L0.r.p, L0.ef.p, n0, s_);
+    }
+  }
+  inner_vcycle(opts, false);
   {
     ProfScope p(s_, "vector", double(n0) * 20.0);
     launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
@@ -502,6 +588,12 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts) {  //
     if (fnorm0_ <= negligible_load(n0)) {
       IHOM_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n0, s_));
       st.converged = true;
+      u0_bound_ = nullptr;
+      return st;
+    }
+    if (opts.mode == kPCG) {
+      st = solve_pcg(u, opts);
+      remove_translations(u, 0);
       u0_bound_ = nullptr;
       return st;
     }

@@ -9,6 +9,9 @@
 // Two solver modes:
 //   kVCycle    -- the reference's stationary V-cycle iteration, step for step
 //                 (src/multigrid.cpp:453-501), f64 nodal data throughout;
+//   kPCG (mixed precision) -- conjugate gradients on K u = f in f64, preconditioned
+//                 by one symmetric inner V-cycle (f32; post-smoothing in reverse
+//                 colour order so the preconditioner is SPD), same stopping rule;
 //   kMixedDefect (mixed precision only) -- the same V-cycle in defect-correction
 //                 form: the outer residual r = f - K u and the update u += e
 //                 are f64, the inner V-cycle on K e = r runs on f32 nodal data
@@ -28,7 +31,7 @@
 
 namespace ihomgpu {
 
-enum SolverMode { kVCycle = 0, kMixedDefect = 1 };
+enum SolverMode { kVCycle = 0, kMixedDefect = 1, kPCG = 2 };
 
 struct SolverOptions {  // inc/multigrid.hpp:22-27
   double tol = 1e-2;
@@ -142,7 +145,9 @@ class Hierarchy {
   void check_error(const char* where);
   void ensure_inner();
   double v_cycle_defect(const SolverOptions& opts);
-  void relax_f32(int l, int sweeps);
+  void relax_f32(int l, int sweeps, bool reverse = false);
+  void inner_vcycle(const SolverOptions& opts, bool symmetric);  // eu0 ~= K^-1 ef0 from zero
+  SolveStats solve_pcg(double* u, const SolverOptions& opts);
   void residual_f32(int l);
   void coarsest_f32();
   double defect_residual();  // ef0 = float(f0 - K u0), returns ||f0 - K u0||
@@ -163,6 +168,7 @@ class Hierarchy {
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;
   DevBuf<double> npart_;  // per-block |r|^2 partials of the fused defect residual
+  DevBuf<double> pcg_p_, pcg_q_, pcg_s_;  // PCG direction, K p, device scalars
   Workspace ws_;
   double* h_pinned_ = nullptr;  // small pinned read-back buffer
   long long launches_ = 0;

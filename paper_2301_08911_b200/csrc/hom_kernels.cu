@@ -179,189 +179,20 @@ static void set_smem(const void* fn, bool f32) {
   IHOM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem(f32)));
 }
 
-// ---------------------------------------------------------------- 6-threads-per-element variant
-// Block = kEL elements x 6 load lanes. Lane i builds, for its element, the
-// d-strain of load i (e_i - eps(u^i)) at the 8 Gauss points as the 7 invariants
-// (tr, exx, eyy, ezz, gxy, gyz, gxz) in shared memory; then the 21 (i<=j) pairs are
-// split over the 6 lanes: E_ij = 1/8 sum_g [lam tr_i tr_j + 2 mu sum eii_i eii_j + mu sum g_i g_j].
-constexpr int kEL = 32;
-constexpr int kE6 = 6 * kEL;
-constexpr int kElemStride = 6 * 8 * 7 + 1;  // odd stride: conflict-free lanes
-
-template <typename TN, typename TE>
-__device__ __forceinline__ void strain_invariants(const GridGeo& g, long long e, int li, const TN* const* u, bool snap,
-                                                  TE* dst /* [8][7] */) {
-  const TE p1 = TE(0.5 + 0.5 / 1.7320508075688772), p0 = TE(0.5 - 0.5 / 1.7320508075688772);
-  const int ex = int(e % g.n[0]);
-  const long long r = e / g.n[0];
-  const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
-  unsigned loc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    loc[j] = vloc(g, wrapp(ex + (j & 1), g.n[0]), wrapp(ey + ((j >> 1) & 1), g.n[1]), wrapp(ez + ((j >> 2) & 1), g.n[2]));
-  const TN* ui = u[0];
-#pragma unroll
-  for (int i = 1; i < 6; ++i)
-    if (li == i) ui = u[i];
-  TE G[3][3][2][2];  // d u_c / d x_k at the Gauss points of the two other axes
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    TE U[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double v = double(__ldg(ui + 3 * (size_t)loc[j] + c));
-      U[j] = snap ? TE(float(v)) : TE(v);
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int sk = 1 << k, sa = 1 << ((k + 1) % 3), sb = 1 << ((k + 2) % 3);
-      TE D[2][2];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) D[a][b] = U[a * sa + b * sb + sk] - U[a * sa + b * sb];
-#pragma unroll
-      for (int ga = 0; ga < 2; ++ga) {
-        const TE w0a = ga == 0 ? p1 : p0, w1a = ga == 0 ? p0 : p1;
-        const TE A0 = w0a * D[0][0] + w1a * D[1][0], A1 = w0a * D[0][1] + w1a * D[1][1];
-#pragma unroll
-        for (int gb = 0; gb < 2; ++gb) {
-          const TE w0b = gb == 0 ? p1 : p0, w1b = gb == 0 ? p0 : p1;
-          G[c][k][ga][gb] = w0b * A0 + w1b * A1;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int gq = 0; gq < 8; ++gq) {
-    const int gp[3] = {gq & 1, (gq >> 1) & 1, (gq >> 2) & 1};
-    auto Gv = [&](int c, int k) { return G[c][k][gp[(k + 1) % 3]][gp[(k + 2) % 3]]; };
-    TE e6[6];
-    e6[0] = -Gv(0, 0);
-    e6[1] = -Gv(1, 1);
-    e6[2] = -Gv(2, 2);
-    e6[3] = -(Gv(0, 1) + Gv(1, 0));
-    e6[4] = -(Gv(1, 2) + Gv(2, 1));
-    e6[5] = -(Gv(0, 2) + Gv(2, 0));
-#pragma unroll
-    for (int v = 0; v < 6; ++v)
-      if (v == li) e6[v] += TE(1);  // strain of chi^li (engineering order 11,22,33,12,23,13)
-    dst[gq * 7 + 0] = e6[0] + e6[1] + e6[2];
-#pragma unroll
-    for (int v = 0; v < 6; ++v) dst[gq * 7 + 1 + v] = e6[v];
-  }
-}
-
-__constant__ unsigned char c_pair_i[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
-__constant__ unsigned char c_pair_j[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
-
-template <typename TE>
-__device__ __forceinline__ TE pair_energy(const TE* si, const TE* sj, TE lam, TE mu) {
-  TE atr = TE(0), an = TE(0), as = TE(0);
-#pragma unroll
-  for (int gq = 0; gq < 8; ++gq) {
-    atr += si[gq * 7] * sj[gq * 7];
-    an += si[gq * 7 + 1] * sj[gq * 7 + 1] + si[gq * 7 + 2] * sj[gq * 7 + 2] + si[gq * 7 + 3] * sj[gq * 7 + 3];
-    as += si[gq * 7 + 4] * sj[gq * 7 + 4] + si[gq * 7 + 5] * sj[gq * 7 + 5] + si[gq * 7 + 6] * sj[gq * 7 + 6];
-  }
-  return TE(0.125) * (lam * atr + TE(2) * mu * an + mu * as);
-}
-
-template <typename TN, typename TE>
-__global__ void __launch_bounds__(kE6) tensor6_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
-                                                      bool snap, double lam, double mu, double* partials) {
-  extern __shared__ __align__(16) unsigned char sraw[];
-  double* red = reinterpret_cast<double*>(sraw);           // [kE6][4]
-  TE* S = reinterpret_cast<TE*>(red + kE6 * 4);             // [kEL][kElemStride]
-  const TN* u[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) u[i] = static_cast<const TN*>(uu.p[i]);
-  const int t = threadIdx.x, el = t / 6, li = t % 6;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (long long e0 = (long long)blockIdx.x * kEL; e0 < g.nv; e0 += (long long)gridDim.x * kEL) {
-    const long long e = e0 + el;
-    __syncthreads();
-    if (e < g.nv) strain_invariants<TN, TE>(g, e, li, u, snap, S + el * kElemStride + li * 56);
-    __syncthreads();
-    if (e < g.nv) {
-      const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
-      const TE* base = S + el * kElemStride;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int p = li + 6 * k;
-        if (p < 21)
-          acc[k] += q * double(pair_energy<TE>(base + c_pair_i[p] * 56, base + c_pair_j[p] * 56, TE(lam), TE(mu)));
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) red[t * 4 + k] = acc[k];
-  __syncthreads();
-  if (t < 21) {  // pair p lives in lane p % 6, slot p / 6; sum the kEL elements in fixed order
-    const int lane = t % 6, slot = t / 6;
-    double sum = 0.0;
-    for (int el2 = 0; el2 < kEL; ++el2) sum += red[(el2 * 6 + lane) * 4 + slot];
-    partials[t * kReducePartials + blockIdx.x] = sum;
-  }
-}
-
-template <typename TN, typename TE>
-__global__ void __launch_bounds__(kE6) sens6_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
-                                                    bool snap, double lam, double mu, const double* __restrict__ seed,
-                                                    double* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char sraw[];
-  double* red = reinterpret_cast<double*>(sraw);  // [kE6]
-  TE* S = reinterpret_cast<TE*>(red + kE6 * 4);
-  const TN* u[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) u[i] = static_cast<const TN*>(uu.p[i]);
-  const int t = threadIdx.x, el = t / 6, li = t % 6;
-  const long long e = (long long)blockIdx.x * kEL + el;
-  if (e < g.nv) strain_invariants<TN, TE>(g, e, li, u, snap, S + el * kElemStride + li * 56);
-  __syncthreads();
-  double part = 0.0;
-  if (e < g.nv) {
-    const TE* base = S + el * kElemStride;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int p = li + 6 * k;
-      if (p < 21) {
-        const int i = c_pair_i[p], j = c_pair_j[p];
-        part += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] *
-                double(pair_energy<TE>(base + i * 56, base + j * 56, TE(lam), TE(mu)));
-      }
-    }
-  }
-  red[t] = part;
-  __syncthreads();
-  if (li == 0 && e < g.nv) {  // fixed order over the element's 6 lanes (src/homogenization.cpp:138-141)
-    double acc = 0.0;
-    for (int l = 0; l < 6; ++l) acc += red[el * 6 + l];
-    out[e] = penal * pow(rho[e], penal - 1.0) * acc / double(g.nv);
-  }
-}
-
-template <typename TE>
-static size_t smem6() {
-  return sizeof(double) * kE6 * 4 + sizeof(TE) * kEL * kElemStride;
-}
-
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
                              double lam, double mu, double* partials, double* c21, cudaStream_t s) {
-  long long blocks = (g.nv + kEL - 1) / kEL;
+  long long blocks = (g.nv + kHT - 1) / kHT;
   if (blocks > kReducePartials) blocks = kReducePartials;
   U6 uu;
   for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
   if (snap) {
-    const size_t sm = smem6<float>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)tensor6_kernel<TN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    tensor6_kernel<TN, float><<<(unsigned)blocks, kE6, sm, s>>>(g, uu, rho, penal, snap, lam, mu, partials);
+    set_smem((const void*)tensor_kernel<TN, float>, true);
+    tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials);
   } else {
-    const size_t sm = smem6<double>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)tensor6_kernel<TN, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    tensor6_kernel<TN, double><<<(unsigned)blocks, kE6, sm, s>>>(g, uu, rho, penal, snap, lam, mu, partials);
+    set_smem((const void*)tensor_kernel<TN, double>, false);
+    tensor_kernel<TN, double><<<(unsigned)blocks, kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                               partials);
   }
   IHOM_LAUNCH_CHECK();
   tensor_finalize<<<1, 256, 0, s>>>(partials, (int)blocks, c21);
@@ -398,15 +229,14 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
                                double lam, double mu, const double* sym_seed36, double* out, cudaStream_t s) {
   U6 uu;
   for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
-  const unsigned blocks = ceil_div(g.nv, kEL);
   if (snap) {
-    const size_t sm = smem6<float>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)sens6_kernel<TN, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    sens6_kernel<TN, float><<<blocks, kE6, sm, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36, out);
+    set_smem((const void*)sens_kernel<TN, float>, true);
+    sens_kernel<TN, float><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                             sym_seed36, out);
   } else {
-    const size_t sm = smem6<double>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)sens6_kernel<TN, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    sens6_kernel<TN, double><<<blocks, kE6, sm, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36, out);
+    set_smem((const void*)sens_kernel<TN, double>, false);
+    sens_kernel<TN, double><<<ceil_div(g.nv, kHT), kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                               sym_seed36, out);
   }
   IHOM_LAUNCH_CHECK();
 }

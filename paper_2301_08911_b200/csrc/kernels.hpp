@@ -79,6 +79,12 @@ template <typename TI, typename TO>
 void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s);
 constexpr int kReducePartials = 1184;  // 8 * 148: capacity of the partials buffer (per component)
 void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s);
+// MG-PCG helpers
+void launch_dot_df(const double* a, const float* b, long long n, double* partials, double* out, cudaStream_t s);
+void launch_pcg_p(double* p, const float* z, const double* beta, long long n, bool first, cudaStream_t s);
+void launch_pcg_ur(double* u, double* r, const double* p, const double* q, const double* alpha, float* r32,
+                   long long n, double* partials, double* out, cudaStream_t s);
+void launch_ratio(const double* num, const double* den, double* out, cudaStream_t s);
 void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s);
 void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s);
 

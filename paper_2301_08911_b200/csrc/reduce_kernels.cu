@@ -143,6 +143,73 @@ void launch_sum(const double* a, long long n, double* partials, double* out, cud
   IHOM_LAUNCH_CHECK();
 }
 
+// ---- MG-PCG vector kernels (f64 outer vectors, f32 preconditioned residual) ----
+__global__ void __launch_bounds__(kRT) dot_df_kernel(const double* __restrict__ a, const float* __restrict__ b,
+                                                     long long n, double* partials) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT)
+    s += a[i] * double(b[i]);
+  const double r = block_reduce(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+void launch_dot_df(const double* a, const float* b, long long n, double* partials, double* out, cudaStream_t s) {
+  const int g = reduce_grid(n);
+  dot_df_kernel<<<g, kRT, 0, s>>>(a, b, n, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+// p = z + beta p  (beta read from device memory: no host round trip)
+__global__ void pcg_p_kernel(double* __restrict__ p, const float* __restrict__ z, const double* __restrict__ beta,
+                             long long n, int first) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  p[i] = first ? double(z[i]) : double(z[i]) + beta[0] * p[i];
+}
+
+void launch_pcg_p(double* p, const float* z, const double* beta, long long n, bool first, cudaStream_t s) {
+  pcg_p_kernel<<<ceil_div(n, 256), 256, 0, s>>>(p, z, beta, n, first ? 1 : 0);
+  IHOM_LAUNCH_CHECK();
+}
+
+// u += alpha p; r -= alpha q; r32 = float(r); partials of r^2 (fixed grid, fixed fold)
+__global__ void __launch_bounds__(kRT) pcg_ur_kernel(double* __restrict__ u, double* __restrict__ r,
+                                                     const double* __restrict__ p, const double* __restrict__ q,
+                                                     const double* __restrict__ alpha, float* __restrict__ r32,
+                                                     long long n, double* partials) {
+  __shared__ double sh[32];
+  const double a = alpha[0];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT) {
+    u[i] += a * p[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    r32[i] = float(ri);
+    s += ri * ri;
+  }
+  const double rr = block_reduce(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = rr;
+}
+
+void launch_pcg_ur(double* u, double* r, const double* p, const double* q, const double* alpha, float* r32,
+                   long long n, double* partials, double* out, cudaStream_t s) {
+  const int g = reduce_grid(n);
+  pcg_ur_kernel<<<g, kRT, 0, s>>>(u, r, p, q, alpha, r32, n, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
+// scalar = num / den on device (alpha, beta)
+__global__ void ratio_kernel(const double* num, const double* den, double* out) { out[0] = num[0] / den[0]; }
+void launch_ratio(const double* num, const double* den, double* out, cudaStream_t s) {
+  ratio_kernel<<<1, 1, 0, s>>>(num, den, out);
+  IHOM_LAUNCH_CHECK();
+}
+
 template void launch_comp_sums<double>(const double*, long long, double*, double*, cudaStream_t);
 template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t);
 template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t);

@@ -298,3 +298,32 @@ def test_32cubed_bulk_5_iterations_matches_oracle(ih, orc, mode):
         assert abs(r["objective"] - ro["objective"]) <= 1e-4 * abs(ro["objective"])
         assert np.abs(r["C"] - ro["C"]).max() <= 1e-4 * np.abs(ro["C"]).max()
     assert np.abs(rep.density - rho_o).max() <= 1e-3
+
+
+@pytest.mark.parametrize("mode", ["pcg", "mixed_defect"])
+def test_fast_modes_tight_tolerance_match_oracle(ih, orc, mode):
+    """Solver-independent comparison (SURVEY 8d config 1 'also at tight tol'): with both
+    sides converged tightly the per-iteration C^H must agree whatever the solver."""
+    tol = 1e-6
+    cfg = ih.RunConfig(reso=16, vol=0.3, obj="shear", max_iter=3, precision="mixed", solver_mode=mode, tol=tol,
+                       max_cycles=200)
+    rep = ih.run_optimization(cfg)
+    recs, rho_o, _ = orc.run(reso=16, vol=0.3, obj="shear", max_iter=3, mixed=True, tol=tol, max_cycles=200)
+    assert len(rep.records) == len(recs) == 3
+    for r, ro in zip(rep.records, recs):
+        assert np.abs(r["C"] - ro["C"]).max() <= 1e-5 * np.abs(ro["C"]).max()
+    assert np.abs(rep.density - rho_o).max() <= 1e-4
+
+
+def test_pcg_converges_in_fewer_cycles_than_vcycle(ih):
+    n = 32
+    rho, _ = ih.init_trig(n, 2, 0, 0.2)
+    phys = ih.radial_filter(n, rho, 2.0, "spline4") ** 3
+    cyc = {}
+    for mode in ("vcycle", "pcg"):
+        hom = make_hom(ih, n, "mixed", penal=1.0, tol=1e-6, max_cycles=200, mode=mode)
+        hom.set_density(phys)
+        st = hom.solve_cell_problems()
+        assert st["converged"]
+        cyc[mode] = st["total_cycles"]
+    assert cyc["pcg"] <= cyc["vcycle"]

@@ -285,9 +285,107 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
   for (int c = 0; c < 3; ++c) uw[3 * (size_t)loc + c] = TN(out[c]);
 }
 
+// Small levels (latency-bound: a few thousand vertices, long per-thread load
+// chains): one warp per vertex, lane n < 27 handles neighbour n, partial sums
+// reduced with a fixed-order xor shuffle (deterministic).
+__device__ __forceinline__ unsigned nbr_loc(const GridGeo& g, int x, int y, int z, int n) {
+  const int tx = n % 3 - 1, ty = (n / 3) % 3 - 1, tz = n / 9 - 1;
+  int a = x + tx, b = y + ty, c = z + tz;
+  a = a < 0 ? a + g.n[0] : (a >= g.n[0] ? a - g.n[0] : a);
+  b = b < 0 ? b + g.n[1] : (b >= g.n[1] ? b - g.n[1] : b);
+  c = c < 0 ? c + g.n[2] : (c >= g.n[2] ? c - g.n[2] : c);
+  return vloc(g, a, b, c);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st,
+                                                                 const TN* __restrict__ x, const TN* __restrict__ f,
+                                                                 TN* __restrict__ y) {
+  const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (loc >= g.nv) return;
+  const int color = color_at(g, loc);
+  int vx, vy, vz;
+  block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (lane < 27) {
+    const TN* xn = x + 3 * (size_t)nbr_loc(g, vx, vy, vz, lane);
+    const double a = double(xn[0]), b = double(xn[1]), c = double(xn[2]);
+    const TS* bl = st + st_index(9 * lane, (unsigned)loc);
+    a0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
+    a1 = double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
+    a2 = double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  if (lane == 0) {
+    if (f) {
+      y[3 * loc] = TN(double(f[3 * loc]) - a0);
+      y[3 * loc + 1] = TN(double(f[3 * loc + 1]) - a1);
+      y[3 * loc + 2] = TN(double(f[3 * loc + 2]) - a2);
+    } else {
+      y[3 * loc] = TN(a0);
+      y[3 * loc + 1] = TN(a1);
+      y[3 * loc + 2] = TN(a2);
+    }
+  }
+}
+
+template <typename TS, typename TN>
+__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st,
+                                                              const TN* __restrict__ f, const TN* __restrict__ ur,
+                                                              TN* uw, int color, int* err) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= g.size[color]) return;
+  int vx, vy, vz;
+  block_coords(g, color, (unsigned)i, vx, vy, vz);
+  const long long loc = g.base[color] + i;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  if (lane < 27 && lane != 13) {
+    const TN* un = ur + 3 * (size_t)nbr_loc(g, vx, vy, vz, lane);
+    const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
+    const TS* bl = st + st_index(9 * lane, (unsigned)loc);
+    m0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
+    m1 = double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
+    m2 = double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
+  }
+  m0 = warp_sum(m0);
+  m1 = warp_sum(m1);
+  m2 = warp_sum(m2);
+  if (lane == 0) {
+    const TS* row = st + st_index(9 * 13, (unsigned)loc);
+    double S[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) S[e] = double(row[32 * e]);
+    const double rhs[3] = {double(f[3 * loc]) - m0, double(f[3 * loc + 1]) - m1, double(f[3 * loc + 2]) - m2};
+    const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
+                       S[2] * (S[3] * S[7] - S[4] * S[6]);
+    if (det == 0.0 || !isfinite(det)) {
+      atomicExch(err, 1);
+      return;
+    }
+    double out[3];
+    solve3(S, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
+  }
+}
+
+constexpr long long kWarpVertexMax = 32768;  // levels up to 64^3 use warp-per-vertex
+
 template <typename TS, typename TN>
 void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s) {
-  if (fast_ok(g)) {
+  if (g.nv <= 8 * kWarpVertexMax) {
+    stencil_apply_warp_kernel<TS, TN><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, x, f, y);
+  } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
     stencil_apply_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, x, f, y);
@@ -342,7 +440,9 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
                              cudaStream_t s) {
-  if (fast_ok(g)) {
+  if (g.size[color] <= kWarpVertexMax) {
+    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+  } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
     stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, u, color, err);

@@ -195,6 +195,13 @@ int ihom_opt_flags(ihom_opt* opt);
 long long ihom_opt_launches(ihom_opt* opt);
 void* ihom_opt_stream(ihom_opt* opt); /* the cudaStream_t every kernel of this optimiser runs on */
 
+/* Multi-GPU (one process per GPU): load case i is solved by rank owner6[i] (NULL: i % nranks)
+   and broadcast to every rank over NCCL; C^H, sensitivities and the design update then run
+   identically on all ranks. uid128 = ncclUniqueId bytes from ihom_nccl_unique_id on rank 0. */
+int ihom_nccl_unique_id(void* out128);
+int ihom_opt_set_comm(ihom_opt* opt, const void* uid128, int rank, int nranks, const int* owner6);
+int ihom_set_comm(ihom_ctx* ctx, const void* uid128, int rank, int nranks, const int* owner6);
+
 /* Per-kernel-family device time (CUDA events on the launching stream) and algorithmic bytes. */
 int ihom_profile_enable(int on); /* enabling resets the totals */
 int ihom_profile_count(void);

@@ -384,6 +384,13 @@ class Homogenizer:
     def hierarchy(self) -> Hierarchy:
         return Hierarchy(self)
 
+    def set_comm(self, uid: bytes, rank: int, nranks: int, owners=None):
+        """Split solve_cell_problems over nranks GPUs (load i on owners[i]; see distributed.py)."""
+        L = lib()
+        L.ihom_set_comm.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        own = (C.c_int * 6)(*owners) if owners is not None else None
+        _check(L.ihom_set_comm(self._ctx(), uid, int(rank), int(nranks), own))
+
 
 def _raise_last():
     msg = lib().ihom_last_error().decode()
@@ -704,6 +711,13 @@ class Optimizer:
 
     def kernel_launches(self) -> int:
         return lib().ihom_opt_launches(C.c_void_p(self._p))
+
+    def set_comm(self, uid: bytes, rank: int, nranks: int, owners=None):
+        """Split the 6 cell problems over nranks GPUs (see distributed.py)."""
+        L = lib()
+        L.ihom_opt_set_comm.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        own = (C.c_int * 6)(*owners) if owners is not None else None
+        _check(L.ihom_opt_set_comm(C.c_void_p(self._p), uid, int(rank), int(nranks), own))
 
     def stream(self) -> int:
         return lib().ihom_opt_stream(C.c_void_p(self._p)) or 0

@@ -127,6 +127,7 @@ struct DevOut {
 }  // namespace
 
 struct ihom_ctx {
+  std::unique_ptr<Comm> comm;
   int device = 0;
   cudaStream_t s = nullptr;
   int precision = IHOM_MIXED;
@@ -203,6 +204,22 @@ int ihom_set_solver(ihom_ctx* ctx, const ihom_solver_opts* o) {
       so.pre_sweeps = o->pre_sweeps;
       so.post_sweeps = o->post_sweeps;
       so.mode = o->mode;
+    });
+  });
+}
+
+int ihom_set_comm(ihom_ctx* ctx, const void* uid128, int rank, int nranks, const int* owner6) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      if (nranks <= 1) {
+        h.set_comm(nullptr, nullptr);
+        ctx->comm.reset();
+        return;
+      }
+      NcclUid id;
+      std::memcpy(id.internal, uid128, sizeof(id.internal));
+      ctx->comm = std::make_unique<Comm>(id, rank, nranks, ctx->device);
+      h.set_comm(ctx->comm.get(), owner6);
     });
   });
 }
@@ -617,6 +634,8 @@ struct OptBase {
   virtual long long launches() = 0;
   virtual cudaStream_t stream() const = 0;
   virtual void bind() = 0;
+  virtual void set_comm(Comm* c, const int* owner) = 0;
+  std::unique_ptr<Comm> comm;
   int flags = 0;
   int iter = 0;
   bool done = false;
@@ -692,6 +711,7 @@ struct Optimizer : OptBase {
   long long count() const override { return m; }
   long long launches() override { return hom->hierarchy().launches(); }
   cudaStream_t stream() const override { return s; }
+  void set_comm(Comm* c, const int* owner) override { hom->set_comm(c, owner); }
 
   double mean_of(const double* f) {
     Workspace& ws = hom->hierarchy().workspace();
@@ -838,6 +858,31 @@ int ihom_opt_design(ihom_opt* h, double* out, int where) {
     const cudaMemcpyKind k = where == IHOM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     IHOM_CUDA(cudaMemcpyAsync(out, o.design(), sizeof(double) * o.count(), k, o.stream()));
     IHOM_CUDA(cudaStreamSynchronize(o.stream()));
+  });
+}
+
+int ihom_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    const NcclUid id = Comm::unique_id();
+    std::memcpy(out128, id.internal, sizeof(id.internal));
+  });
+}
+
+int ihom_opt_set_comm(ihom_opt* h, const void* uid128, int rank, int nranks, const int* owner6) {
+  return guarded([&] {
+    OptBase& o = *h->o;
+    o.bind();
+    if (nranks <= 1) {
+      o.set_comm(nullptr, nullptr);
+      o.comm.reset();
+      return;
+    }
+    NcclUid id;
+    std::memcpy(id.internal, uid128, sizeof(id.internal));
+    int dev = 0;
+    IHOM_CUDA(cudaGetDevice(&dev));
+    o.comm = std::make_unique<Comm>(id, rank, nranks, dev);
+    o.set_comm(o.comm.get(), owner6);
   });
 }
 

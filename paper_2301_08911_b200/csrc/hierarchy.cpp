@@ -686,20 +686,43 @@ void Homogenizer<T>::set_density(const double* rho) {  // src/homogenization.cpp
 template <typename T>
 CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cpp:23-40
   if (!density_set_) throw StateError("set_density before solve_cell_problems");
-  CellSolveStats out;
   const GridGeo& g = hier_.geo(0);
+  const bool multi = comm_ && comm_->size() > 1;
+  double per[18] = {};  // per load: cycles, rel_residual, converged
   for (int i = 0; i < 6; ++i) {
+    if (multi && owner_[i] != comm_->rank()) continue;
     {
       ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
       launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream());
     }
     const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_);
-    out.total_cycles += s.cycles;
-    if (s.rel_residual >= out.worst_residual) {
-      out.worst_residual = s.rel_residual;
+    per[3 * i] = s.cycles;
+    per[3 * i + 1] = s.rel_residual;
+    per[3 * i + 2] = s.converged ? 1.0 : 0.0;
+  }
+  if (multi) {
+    // every solved field from its owner to all ranks (NVLink), then one allreduce of the stats
+    cudaStream_t s = hier_.stream();
+    {
+      ProfScope p(s, "nccl_broadcast", double(6 * 3 * g.nv * 8));
+      comm_->group_start();
+      for (int i = 0; i < 6; ++i) comm_->broadcast(u_[size_t(i)].p, size_t(3 * g.nv), owner_[i], s);
+      comm_->group_end();
+    }
+    if (!stats_.p) stats_.alloc(18);
+    IHOM_CUDA(cudaMemcpyAsync(stats_.p, per, sizeof(per), cudaMemcpyHostToDevice, s));
+    comm_->allreduce_sum(stats_.p, 18, s);
+    IHOM_CUDA(cudaMemcpyAsync(per, stats_.p, sizeof(per), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  }
+  CellSolveStats out;  // combined in load order, exactly as the reference loop does
+  for (int i = 0; i < 6; ++i) {
+    out.total_cycles += int(per[3 * i]);
+    if (per[3 * i + 1] >= out.worst_residual) {
+      out.worst_residual = per[3 * i + 1];
       out.worst_load = i;
     }
-    if (!s.converged) out.converged = false;
+    if (per[3 * i + 2] == 0.0) out.converged = false;
   }
   return out;
 }

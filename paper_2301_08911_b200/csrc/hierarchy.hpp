@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "common.cuh"
 #include "density.hpp"
 #include "kernels.hpp"
@@ -185,6 +186,11 @@ class Homogenizer {
   void tensor_sensitivity(const double seed[36], double* out_dev);
 
   double* displacement(int i) { return u_[size_t(i)].p; }
+  // Multi-GPU: load case i is solved by rank owner[i], then broadcast to all ranks.
+  void set_comm(Comm* c, const int owner[6]) {
+    comm_ = c;
+    for (int i = 0; i < 6; ++i) owner_[i] = owner ? owner[i] : (c ? i % c->size() : 0);
+  }
   Hierarchy<T>& hierarchy() { return hier_; }
   SolverOptions& options() { return opts_; }
   const double* density() const { return rho_.p; }
@@ -197,7 +203,10 @@ class Homogenizer {
   DevBuf<double> rho_;
   std::array<DevBuf<double>, 6> u_;
   DevBuf<double> seed_;
+  DevBuf<double> stats_;  // per-load (cycles, rel, converged) for the multi-GPU combine
   bool density_set_ = false;
+  Comm* comm_ = nullptr;
+  int owner_[6] = {0, 0, 0, 0, 0, 0};
 };
 
 }  // namespace ihomgpu

@@ -1,0 +1,59 @@
+"""Multi-GPU plumbing for the hot path (one process per GPU).
+
+Round-1 scheme: the six periodic cell problems of an iteration are
+independent solves, so rank r solves the load cases ``load_owners(n)`` assigns
+it; the library then broadcasts every solved displacement field from its owner
+over NCCL (NVLink) and every rank evaluates C^H, the sensitivities and the OC
+update identically. The result is bitwise equal to the 1-GPU run.
+
+``torch.distributed`` only carries the 128-byte NCCL unique id from rank 0 to
+the others (plumbing); the collectives themselves run inside libihom_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+NUM_LOADS = 6
+
+
+def load_owners(nranks: int) -> list:
+    """Rank that solves load case i (i % nranks; ranks >= 6 get none)."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    return [i % nranks for i in range(NUM_LOADS)]
+
+
+def combine_cell_stats(per_load) -> dict:
+    """CellSolveStats from per-load (cycles, rel_residual, converged), in load order
+    exactly as src/homogenization.cpp:29-38 accumulates them."""
+    out = dict(total_cycles=0, worst_residual=0.0, worst_load=-1, converged=True)
+    for i, (cyc, rel, conv) in enumerate(per_load):
+        out["total_cycles"] += int(cyc)
+        if rel >= out["worst_residual"]:
+            out["worst_residual"] = float(rel)
+            out["worst_load"] = i
+        if not conv:
+            out["converged"] = False
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    from . import _check, lib
+    buf = (C.c_char * 128)()
+    _check(lib().ihom_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def share_unique_id(rank: int) -> bytes:
+    """Rank 0 creates the NCCL id; torch.distributed (any backend) broadcasts it."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().astype(np.uint8).tobytes())

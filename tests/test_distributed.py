@@ -1,0 +1,97 @@
+"""Multi-process host logic of the multi-GPU scheme (gloo, world size 2, CPU).
+
+Each rank solves only the load cases distributed.load_owners() assigns it
+(the oracle stands in for the GPU solver), the solved displacement fields are
+broadcast from their owners, and every rank then evaluates C^H and the
+sensitivity: both must equal the single-process result bitwise, and the
+combined solver statistics must equal the single-process ones.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+E, NU = 1e6, 0.3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, rho, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_2301_08911_b200 import distributed as dd
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    owners = dd.load_owners(world)
+    h = oracle.Homogenizer(n, E=E, nu=NU, penal=3.0, mixed=True, tol=1e-6, max_cycles=100)
+    h.set_density(rho)
+    coeff = np.power(np.asarray(rho, np.float64).astype(np.float32).astype(np.float64), 3.0)
+    per = np.zeros((6, 3))
+    for i in range(6):
+        if owners[i] != rank:
+            continue
+        f = oracle.fem(n, "macro", coeff, E=E, nu=NU, mixed=True, load=i)
+        u, st = h.solve(f, np.zeros_like(f))
+        h.set_displacement(i, u)
+        per[i] = (st["cycles"], st["rel_residual"], float(st["converged"]))
+    for i in range(6):  # owner -> everyone
+        t = torch.from_numpy(h.displacement(i).ravel().copy())
+        dist.broadcast(t, owners[i])
+        h.set_displacement(i, t.numpy())
+    tp = torch.from_numpy(per.ravel().copy())
+    dist.all_reduce(tp)
+    stats = dd.combine_cell_stats(tp.numpy().reshape(6, 3))
+    c = h.effective_tensor()
+    g = h.tensor_sensitivity(np.eye(6))
+    q.put((rank, c, g, stats))
+    dist.destroy_process_group()
+
+
+def test_load_split_matches_single_process():
+    import oracle
+    from paper_2301_08911_b200 import distributed as dd
+    n = 8
+    rho = np.random.default_rng(9).uniform(0.1, 1.0, n ** 3)
+    # single process reference: the oracle's own solve_cell_problems
+    h = oracle.Homogenizer(n, E=E, nu=NU, penal=3.0, mixed=True, tol=1e-6, max_cycles=100)
+    h.set_density(rho)
+    st1 = h.solve_cell_problems()
+    c1, g1 = h.effective_tensor(), h.tensor_sensitivity(np.eye(6))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, rho, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, c, g, stats in res:
+        assert np.array_equal(c, c1), rank
+        assert np.array_equal(g, g1), rank
+        assert stats["total_cycles"] == st1["total_cycles"]
+        assert stats["worst_load"] == st1["worst_load"]
+        assert stats["worst_residual"] == st1["worst_residual"]
+        assert stats["converged"] == st1["converged"]
+
+
+def test_load_owners():
+    from paper_2301_08911_b200 import distributed as dd
+    assert dd.load_owners(1) == [0] * 6
+    assert dd.load_owners(2) == [0, 1, 0, 1, 0, 1]
+    assert dd.load_owners(4) == [0, 1, 2, 3, 0, 1]
+    assert dd.load_owners(8) == [0, 1, 2, 3, 4, 5]
+    with pytest.raises(ValueError):
+        dd.load_owners(0)

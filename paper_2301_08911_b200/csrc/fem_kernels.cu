@@ -14,6 +14,7 @@
 #include <cuda_pipeline.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <string>
 
 namespace ihomgpu {
@@ -287,6 +288,15 @@ static bool tile_enabled() {
   }();
   return v != 0;
 }
+// Two-vertex GS variant (IHOM_L0_GS2=0 disables; default on).
+static bool gs2_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("IHOM_L0_GS2");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 static bool tile_ok(const GridGeo& g) {
   return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
 }
@@ -337,6 +347,53 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, con
   if (t == 0) {
     const size_t bid = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
     partials[bid] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
+}
+
+// Two same-colour vertices per thread, stacked in halved z (h2, h2+1): the upper
+// neighbour plane of the first (t2 = +1) is the lower plane of the second
+// (t2 = -1), so those 9 neighbours are loaded once into registers and reused.
+template <typename TC, typename TN, int MINB>
+__global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                const TN* __restrict__ f, const TN* __restrict__ ur,
+                                                                TN* uw, int color) {
+  using TA = TN;
+  const int h2 = 2 * blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa, fb;
+  fast_addr(g, color, h0, h1, h2, fa);
+  fast_addr(g, color, h0, h1, h2 + 1, fb);
+  TA shared_pl[9][3];  // plane t2 = +1 of vertex a == plane t2 = -1 of vertex b
+#pragma unroll
+  for (int n = 0; n < 9; ++n) {
+    const TN* p = ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) shared_pl[n][c] = TA(__ldg(p + c));
+  }
+  auto Ua = [&](int n, int c) {
+    if (n >= 18) return shared_pl[n - 18][c];
+    return TA(__ldg(ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c));
+  };
+  auto Ub = [&](int n, int c) {
+    if (n < 9) return shared_pl[n][c];
+    return TA(__ldg(ur + 3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c));
+  };
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const FastAddr& fx = v == 0 ? fa : fb;
+    TA q[8];
+    load_q_fast(coeff, fx, q);
+    TA m[3], sblk[9];
+    if (v == 0) ku_vertex_split<TA>(q, kappa<TA>(), Ua, m, sblk);
+    else ku_vertex_split<TA>(q, kappa<TA>(), Ub, m, sblk);
+    const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
+    TN rhs[3], out[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = TN(f[3 * loc + c]) - m[c];
+    solve3<TN>(sblk, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
   }
 }
 
@@ -510,7 +567,15 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+    bool done = false;
+    if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
+      if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
+        const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
+        l0_gs_fast2_kernel<TC, TN, 5><<<gr2, b, 0, s>>>(g, coeff, f, u, u, color);
+        done = true;
+      }
+    }
+    if (!done) l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
   } else {
     l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
   }
@@ -553,7 +618,13 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-  l0_residual_norm_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  static const int minb = [] {
+    const char* e = std::getenv("IHOM_RES_MINB");
+    return e ? std::atoi(e) : 3;
+  }();
+  if (minb >= 4) l0_residual_norm_fast_kernel<TC, 4><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  else if (minb == 3) l0_residual_norm_fast_kernel<TC, 3><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  else l0_residual_norm_fast_kernel<TC, 1><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }

@@ -267,7 +267,7 @@ int ihom_get_displacement(ihom_ctx* ctx, int load, double* u, int where) {
     if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
     ctx->with([&](auto& h) {
       DevOut o(u, size_t(3 * ctx->nv()), where);
-      launch_aos_soa(h.displacement(load), o.p, ctx->nv(), false, ctx->s);
+      copy_nodal(h.displacement(load), o.p, ctx->nv(), ctx->s);
       o.finish(ctx->s);
     });
   });
@@ -278,7 +278,7 @@ int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u, int where) {
     if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
     ctx->with([&](auto& h) {
       DevIn in(u, size_t(3 * ctx->nv()), where, ctx->s);
-      launch_aos_soa(in.p, h.displacement(load), ctx->nv(), true, ctx->s);
+      copy_nodal(in.p, h.displacement(load), ctx->nv(), ctx->s);
       IHOM_CUDA(cudaStreamSynchronize(ctx->s));
     });
   });
@@ -308,11 +308,11 @@ int ihom_level_field(ihom_ctx* ctx, int l, int which, int write, double* buf) {
       const long long nv = H.geo(l).nv;
       if (write) {
         DevIn in(buf, size_t(3 * nv), IHOM_HOST, ctx->s);
-        launch_aos_soa(in.p, f, nv, true, ctx->s);
+        copy_nodal(in.p, f, nv, ctx->s);
         IHOM_CUDA(cudaStreamSynchronize(ctx->s));
       } else {
         DevOut o(buf, size_t(3 * nv), IHOM_HOST);
-        launch_aos_soa(f, o.p, nv, false, ctx->s);
+        copy_nodal(f, o.p, nv, ctx->s);
         o.finish(ctx->s);
       }
     });
@@ -327,10 +327,10 @@ int ihom_apply(ihom_ctx* ctx, int l, const double* x, double* y) {
       const long long nv = H.geo(l).nv;
       DevIn in(x, size_t(3 * nv), IHOM_HOST, ctx->s);
       DevBuf<double> xs(static_cast<size_t>(3 * nv)), ys(static_cast<size_t>(3 * nv));
-      launch_aos_soa(in.p, xs.p, nv, true, ctx->s);
+      copy_nodal(in.p, xs.p, nv, ctx->s);
       H.apply(l, xs.p, ys.p);
       DevOut o(y, size_t(3 * nv), IHOM_HOST);
-      launch_aos_soa(ys.p, o.p, nv, false, ctx->s);
+      copy_nodal(ys.p, o.p, nv, ctx->s);
       o.finish(ctx->s);
     });
   });
@@ -373,13 +373,13 @@ int ihom_solve(ihom_ctx* ctx, const double* f, double* u, ihom_solve_stats* st) 
       auto& H = h.hierarchy();
       const long long nv = H.geo(0).nv;
       DevIn fin(f, size_t(3 * nv), IHOM_HOST, ctx->s);
-      launch_aos_soa(fin.p, H.level_f(0), nv, true, ctx->s);
+      copy_nodal(fin.p, H.level_f(0), nv, ctx->s);
       DevIn uin(u, size_t(3 * nv), IHOM_HOST, ctx->s);
       DevBuf<double> us(static_cast<size_t>(3 * nv));
-      launch_aos_soa(uin.p, us.p, nv, true, ctx->s);
+      copy_nodal(uin.p, us.p, nv, ctx->s);
       const SolveStats s = H.solve_bound(us.p, h.options());
       DevOut o(u, size_t(3 * nv), IHOM_HOST);
-      launch_aos_soa(us.p, o.p, nv, false, ctx->s);
+      copy_nodal(us.p, o.p, nv, ctx->s);
       o.finish(ctx->s);
       if (st) {
         st->cycles = s.cycles;
@@ -427,7 +427,7 @@ int ihom_macro_force(ihom_ctx* ctx, int load, double* f) {
       DevBuf<double> fs(static_cast<size_t>(3 * nv));
       launch_macro_force(H.geo(0), H.coeff(), load, fs.p, ctx->s);
       DevOut o(f, size_t(3 * nv), IHOM_HOST);
-      launch_aos_soa(fs.p, o.p, nv, false, ctx->s);
+      copy_nodal(fs.p, o.p, nv, ctx->s);
       o.finish(ctx->s);
     });
   });

@@ -495,7 +495,6 @@ __global__ void __launch_bounds__(128) l0_apply_kernel(GridGeo g, const TC* __re
   gather27(g, x, yy, z, nb);
   TA q[8];
   load_q(coeff, nb, q);
-  const long long nv = g.nv;
   auto U = [&](int n, int c) { return TA(__ldg(u + 3 * (size_t)nb.v[n] + c)); };
   TA acc[3];
   ku_vertex<TA>(q, kappa<TA>(), U, acc);  // factored K0 (ku_gen.cuh), inc/fem.hpp:86-105 semantics
@@ -541,7 +540,6 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
   gather27(g, x, yy, z, nb);
   TA q[8];
   load_q(coeff, nb, q);
-  const long long nv = g.nv;
   auto U = [&](int n, int c) { return TA(__ldg(ur + 3 * (size_t)nb.v[n] + c)); };
   TA m[3], sblk[9];
   ku_vertex_split<TA>(q, kappa<TA>(), U, m, sblk);  // S (n = 13) and M u (n != 13), inc/fem.hpp:109-133

@@ -4,7 +4,7 @@
 // Mirrors ihom::Hierarchy<T> (inc/multigrid.hpp:53-93) and
 // ihom::Homogenizer<T> (inc/homogenization.hpp:26-51): same method names,
 // same semantics, T = coefficient/stencil storage (float: mixed, double:
-// all-double). Nodal data are f64 SoA in device memory.
+// all-double). Nodal data are f64 AoS [loc][3] in device memory.
 //
 // Two solver modes:
 //   kVCycle    -- the reference's stationary V-cycle iteration, step for step
@@ -139,7 +139,7 @@ class Hierarchy {
   struct Level {
     GridGeo g;
     DevBuf<double> u, f, r;
-    DevBuf<T> st;                 // coarse stencil, SoA [243][nv]
+    DevBuf<T> st;                 // coarse stencil, blocked [nv/32][243][32] (st_index)
     DevBuf<float> eu, ef, er;     // f32 inner-cycle fields (kMixedDefect)
   };
   void factor_coarsest();

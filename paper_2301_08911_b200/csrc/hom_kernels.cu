@@ -31,7 +31,6 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     loc[j] = vloc(g, wrapp(ex + (j & 1), g.n[0]), wrapp(ey + ((j >> 1) & 1), g.n[1]), wrapp(ez + ((j >> 2) & 1), g.n[2]));
-  const long long nv = g.nv;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const TN* ui = u[i];

@@ -62,7 +62,7 @@ void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const dou
                            double negligible, double* work, int* err, cudaStream_t s);
 
 // ---- reductions (deterministic: fixed partition per size, fixed fold order) ----
-// sums of the three SoA components: out[3]
+// sums of the three AoS components: out[3]
 template <typename TN>
 void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s);
 // out[0] = dot(a, b) over n entries
@@ -86,7 +86,7 @@ void launch_pcg_ur(double* u, double* r, const double* p, const double* q, const
                    long long n, double* partials, double* out, cudaStream_t s);
 void launch_ratio(const double* num, const double* den, double* out, cudaStream_t s);
 void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s);
-void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s);
+void copy_nodal(const double* in, double* out, long long nv, cudaStream_t s);
 
 // ---- homogenization (src/homogenization.cpp:58-144) ----
 // partial sums (21 per block) of q_e * d_i^T K0 d_j; finalized into C[21].

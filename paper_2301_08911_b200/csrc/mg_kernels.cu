@@ -180,7 +180,7 @@ void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* 
 }
 
 // ---------------------------------------------------------------- stencil apply / GS
-// y = K x (f == nullptr) or y = f - K x; stencil SoA [243][nv] (src/multigrid.cpp:186-205, 412-424).
+// y = K x (f == nullptr) or y = f - K x; blocked stencil rows st_index(k, loc) (src/multigrid.cpp:186-205, 412-424).
 template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st,
                                                             const TN* __restrict__ x, const TN* __restrict__ f,
@@ -192,7 +192,6 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
   Nbhd nb;
   gather27(g, vx, vy, vz, nb);
-  const long long nv = g.nv;
   double acc[3] = {0.0, 0.0, 0.0};
   const TS* row = st + st_index(0, (unsigned)loc);
 #pragma unroll 3
@@ -406,7 +405,6 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
   block_coords(g, color, (unsigned)i, vx, vy, vz);
   Nbhd nb;
   gather27(g, vx, vy, vz, nb);
-  const long long nv = g.nv;
   const long long loc = g.base[color] + i;
   double m[3] = {0.0, 0.0, 0.0}, S[9];
   const TS* row0 = st + st_index(0, (unsigned)loc);
@@ -669,7 +667,7 @@ void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS
 }
 
 // ---------------------------------------------------------------- coarsest solve
-// One block. Vectors are SoA in the caller's nodal type; the dense matrices are
+// One block. Vectors are AoS [loc][3] in the caller's nodal type; the dense matrices are
 // in the dof order 3*loc + c of the reference (src/multigrid.cpp:335-366).
 constexpr int kCoarseThreads = 512;
 

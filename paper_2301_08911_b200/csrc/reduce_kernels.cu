@@ -225,21 +225,9 @@ template void launch_convert<float, double>(const float*, double*, long long, cu
 
 namespace ihomgpu {
 
-// AoS [nv][3] <-> SoA [3][nv] transposes for the boundary (nodal fields cross
-// the C ABI in the reference's AoS layout).
-__global__ void aos_soa_kernel(const double* __restrict__ in, double* __restrict__ out, long long nv, int to_soa) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nv) return;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    if (to_soa) out[c * nv + i] = in[3 * i + c];
-    else out[3 * i + c] = in[c * nv + i];
-  }
-}
-
-void launch_aos_soa(const double* in, double* out, long long nv, bool to_soa, cudaStream_t s) {
-  // device nodal storage is AoS like the boundary: a plain copy
-  (void)to_soa;
+// Nodal fields cross the C ABI in the reference's AoS layout, which is also
+// the device layout: a plain device copy.
+void copy_nodal(const double* in, double* out, long long nv, cudaStream_t s) {
   if (in != out) IHOM_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * 3 * nv, cudaMemcpyDeviceToDevice, s));
 }
 

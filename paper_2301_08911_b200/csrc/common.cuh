@@ -215,7 +215,31 @@ inline size_t stencil_alloc(long long nv) { return (size_t)((nv + 31) / 32) * 32
 struct FastAddr {
   unsigned A[3][3];  // [axis][t+1]
   unsigned E[3][2];  // [axis][bit]: element coordinate x-1 (bit 0) or x (bit 1), pre-scaled
+  bool zlo, zhi;     // the t2 = -1 / +1 neighbour plane (and, for zlo, the z-1 element plane) wraps
 };
+
+// z-slab neighbours of one array. A slab's grid is periodic in x
+// and y; in z, reads that wrap through its lower / upper face go to the same
+// array of the slab below / above, at the wrapped index (every slab has the
+// same local layout, so the wrapped plane of the local layout IS the
+// neighbour's boundary plane). The peer array is another slab's buffer on the
+// same device or peer memory mapped over NVLink. A periodic single-slab grid
+// links every array to itself, which is exactly the old wrap.
+template <typename X>
+struct ZLink {
+  const X* lo = nullptr;
+  const X* hi = nullptr;
+};
+template <typename X>
+inline ZLink<X> resolve(ZLink<X> l, const X* self) {
+  if (!l.lo) l.lo = self;
+  if (!l.hi) l.hi = self;
+  return l;
+}
+template <typename X>
+inline bool is_self(const ZLink<X>& l, const X* self) {
+  return (!l.lo || l.lo == self) && (!l.hi || l.hi == self);
+}
 
 __device__ __forceinline__ void fast_addr(const GridGeo& g, int color, int h0, int h1, int h2, FastAddr& fa) {
   const unsigned B = (unsigned)g.size[0];
@@ -236,6 +260,15 @@ __device__ __forceinline__ void fast_addr(const GridGeo& g, int color, int h0, i
     fa.E[k][0] = es[k] * (unsigned)(x == 0 ? nk - 1 : x - 1);
     fa.E[k][1] = es[k] * (unsigned)x;
   }
+  const int o2 = (color >> 2) & 1;
+  fa.zlo = o2 == 0 && h2 == 0;
+  fa.zhi = o2 == 1 && (unsigned)h2 + 1 == d[2];
+}
+
+// Base pointer of neighbour plane t2 (0, 1, 2 = z-1, z, z+1) under a z link.
+template <typename X>
+__device__ __forceinline__ const X* zbase(const FastAddr& fa, const X* self, const ZLink<X>& zl, int t2) {
+  return t2 == 0 ? (fa.zlo ? zl.lo : self) : (t2 == 2 ? (fa.zhi ? zl.hi : self) : self);
 }
 
 inline bool fast_ok(const GridGeo& g) {

@@ -1,0 +1,105 @@
+// fabric.hpp -- how the z-slabs of one grid reach each other.
+//
+// A z-slab decomposition puts slab r (global z planes [r t, (r+1) t)) on rank
+// r. Kernels read across a slab face directly from the neighbour's buffer (a
+// ZLink, common.cuh): peer memory mapped over NVLink between processes, or
+// another slab's buffer on the same device when all slabs live in one process
+// (the single-GPU test configuration). Synchronisation and reductions are
+// stream-ordered device operations, so no rank ever blocks its host on a peer
+// except while collectively exchanging buffer addresses at allocation time.
+//
+//   exchange(local)  collective: every rank's pointer of the same logical
+//                    buffer, mapped into this rank (called in the same order
+//                    on every rank -- SPMD allocation order);
+//   barrier(s)       work enqueued on s after the barrier sees every rank's
+//                    work enqueued before its barrier;
+//   allreduce(x, n)  n doubles, sum or max, folded in rank order -- the
+//                    result is bitwise identical on every rank, so every rank
+//                    takes the same convergence / bisection decisions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+namespace ihomgpu {
+
+constexpr int kMaxRanks = 8;
+constexpr int kMailbox = 64;  // doubles per allreduce slot
+
+struct PeerTable {  // a buffer on every rank, by rank (kernel argument)
+  const void* p[kMaxRanks];
+};
+
+class Fabric {
+ public:
+  explicit Fabric(int nranks);
+  virtual ~Fabric() = default;
+  int size() const { return n_; }
+  virtual std::vector<void*> exchange(int rank, void* local) = 0;
+  virtual void barrier(int rank, cudaStream_t s) = 0;
+  void allreduce(int rank, double* x, int n, bool is_max, cudaStream_t s);
+  // per-rank mailboxes (2 slots of kMailbox doubles, alternating per allreduce)
+  void init_mailboxes(int rank);
+
+ protected:
+  int n_;
+  struct RankState {
+    double* mailbox = nullptr;  // own, device
+    PeerTable boxes{};          // every rank's mailbox
+    int parity = 0;
+  };
+  std::vector<RankState> rs_;
+};
+
+// All slabs in this process on one device, one host thread per slab.
+class LocalFabric : public Fabric {
+ public:
+  LocalFabric(int nranks, int device);
+  ~LocalFabric() override;
+  std::vector<void*> exchange(int rank, void* local) override;
+  void barrier(int rank, cudaStream_t s) override;
+
+ private:
+  void host_barrier();
+  int device_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  long long generation_ = 0;
+  std::vector<void*> slots_;
+  std::vector<cudaEvent_t> ev_;
+};
+
+// One slab per process; buffers exchanged as CUDA IPC handles through a
+// host allgather supplied by the caller (torch.distributed, MPI, ...).
+// Barriers are device-side flags in peer memory (release/acquire, system scope).
+using HostAllgather = void (*)(const void* send, void* recv, std::size_t bytes, void* user);
+
+class IpcFabric : public Fabric {
+ public:
+  IpcFabric(int rank, int nranks, int device, HostAllgather ag, void* user);
+  ~IpcFabric() override;
+  std::vector<void*> exchange(int rank, void* local) override;
+  void barrier(int rank, cudaStream_t s) override;
+
+ private:
+  int rank_, device_;
+  HostAllgather ag_;
+  void* user_;
+  unsigned long long* flag_ = nullptr;  // own arrival counter (device)
+  PeerTable flags_{};
+  unsigned long long epoch_ = 0;
+  std::map<std::pair<int, std::uintptr_t>, void*> opened_;  // (rank, remote base) -> mapped base
+};
+
+// Kernels (fabric.cu)
+void launch_signal_wait(unsigned long long* own, PeerTable flags, int nranks, unsigned long long epoch, cudaStream_t s);
+void launch_mailbox_fold(PeerTable boxes, int nranks, int n, bool is_max, double* out, cudaStream_t s);
+
+}  // namespace ihomgpu

@@ -120,18 +120,33 @@ __device__ __forceinline__ void load_q_fast(const TC* __restrict__ coeff, const 
   for (int ke = 0; ke < 8; ++ke)
     q[ke] = TA(__ldg(coeff + (fa.E[0][ke & 1] + fa.E[1][(ke >> 1) & 1] + fa.E[2][(ke >> 2) & 1])));
 }
+// z-slab form: the z-1 element plane of a vertex on the lower face is the
+// top element plane of the slab below.
+template <typename TC, typename TA>
+__device__ __forceinline__ void load_q_fast(const TC* __restrict__ coeff, const ZLink<TC>& cl, const FastAddr& fa,
+                                            TA q[8]) {
+  const TC* lo = fa.zlo ? cl.lo : coeff;
+#pragma unroll
+  for (int ke = 0; ke < 8; ++ke)
+    q[ke] = TA(__ldg(((ke >> 2) & 1 ? coeff : lo) + (fa.E[0][ke & 1] + fa.E[1][(ke >> 1) & 1] + fa.E[2][(ke >> 2) & 1])));
+}
 
-#define FAST_U(ptr)                                                                      \
-  [&](int n, int c) {                                                                    \
-    const unsigned l_ = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];         \
-    return TA(__ldg(ptr + 3 * (size_t)l_ + c));                                          \
+// neighbour n (27-index), component c of nodal array ptr with z link zl
+#define FAST_U(ptr, zl)                                                                                   \
+  [&, zb0_ = zbase(fa, ptr, zl, 0), zb2_ = zbase(fa, ptr, zl, 2)](int n, int c) {                      \
+    const unsigned l_ = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];                          \
+    return TA(__ldg((n < 9 ? zb0_ : (n < 18 ? ptr : zb2_)) + 3 * (size_t)l_ + c));                       \
   }
 
 // blockDim = (bx, 128/bx), grid = (d0/bx, ceil(d1/by), d2 * ncolors)
-template <typename TC, typename TN, typename TA, int MINB = 1>
+template <typename TC, typename TN, typename TA, int MINB = 1, bool ZL = false>
 __global__ void __launch_bounds__(128, MINB) l0_apply_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                            const TN* __restrict__ u, const TN* __restrict__ f,
-                                                            TN* __restrict__ y) {
+                                                            ZLink<TC> cl, const TN* __restrict__ u, ZLink<TN> ul,
+                                                            const TN* __restrict__ f, TN* __restrict__ y) {
+  if constexpr (!ZL) {  // single periodic domain: every wrap reads the array itself
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
   const int h2 = blockIdx.z >> 3;
@@ -140,9 +155,9 @@ __global__ void __launch_bounds__(128, MINB) l0_apply_fast_kernel(GridGeo g, con
   FastAddr fa;
   fast_addr(g, color, h0, h1, h2, fa);
   TA q[8];
-  load_q_fast(coeff, fa, q);
+  load_q_fast(coeff, cl, fa, q);
   TA acc[3];
-  ku_vertex<TA>(q, kappa<TA>(), FAST_U(u), acc);
+  ku_vertex<TA>(q, kappa<TA>(), FAST_U(u, ul), acc);
   const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   if (f) {
 #pragma unroll
@@ -353,10 +368,15 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, con
 // Two same-colour vertices per thread, stacked in halved z (h2, h2+1): the upper
 // neighbour plane of the first (t2 = +1) is the lower plane of the second
 // (t2 = -1), so those 9 neighbours are loaded once into registers and reused.
-template <typename TC, typename TN, int MINB>
+template <typename TC, typename TN, int MINB, bool ZL = false>
 __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                                TN* uw, int color) {
+                                                                ZLink<TC> cl, const TN* __restrict__ f,
+                                                                const TN* __restrict__ ur, ZLink<TN> ul, TN* uw,
+                                                                int color) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {ur, ur};
+  }
   using TA = TN;
   const int h2 = 2 * blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
@@ -365,25 +385,28 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
   fast_addr(g, color, h0, h1, h2, fa);
   fast_addr(g, color, h0, h1, h2 + 1, fb);
   TA shared_pl[9][3];  // plane t2 = +1 of vertex a == plane t2 = -1 of vertex b
+  const TN* pa2 = zbase(fa, ur, ul, 2);  // == zbase(fb, ur, ul, 0) (a's upper plane is b's lower)
 #pragma unroll
   for (int n = 0; n < 9; ++n) {
-    const TN* p = ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
+    const TN* p = pa2 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) shared_pl[n][c] = TA(__ldg(p + c));
   }
+  const TN* pa0 = zbase(fa, ur, ul, 0);
+  const TN* pb2 = zbase(fb, ur, ul, 2);
   auto Ua = [&](int n, int c) {
     if (n >= 18) return shared_pl[n - 18][c];
-    return TA(__ldg(ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c));
+    return TA(__ldg((n < 9 ? pa0 : ur) + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c));
   };
   auto Ub = [&](int n, int c) {
     if (n < 9) return shared_pl[n][c];
-    return TA(__ldg(ur + 3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c));
+    return TA(__ldg((n < 18 ? ur : pb2) + 3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c));
   };
 #pragma unroll
   for (int v = 0; v < 2; ++v) {
     const FastAddr& fx = v == 0 ? fa : fb;
     TA q[8];
-    load_q_fast(coeff, fx, q);
+    load_q_fast(coeff, cl, fx, q);
     TA m[3], sblk[9];
     if (v == 0) ku_vertex_split<TA>(q, kappa<TA>(), Ua, m, sblk);
     else ku_vertex_split<TA>(q, kappa<TA>(), Ub, m, sblk);
@@ -401,11 +424,15 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
 // plus deterministic per-block partial sums of |r|^2 (the convergence norm).
 // Replaces residual + dot + convert (136 -> 64 B/vertex).
-template <typename TC, int MINB = 1>
+template <typename TC, int MINB = 1, bool ZL = false>
 __global__ void __launch_bounds__(128, MINB) l0_residual_norm_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                    const double* __restrict__ u,
-                                                                    const double* __restrict__ f,
+                                                                    ZLink<TC> cl, const double* __restrict__ u,
+                                                                    ZLink<double> ul, const double* __restrict__ f,
                                                                     float* __restrict__ r32, double* partials) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
   __shared__ double red[4];
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
@@ -417,9 +444,9 @@ __global__ void __launch_bounds__(128, MINB) l0_residual_norm_fast_kernel(GridGe
     FastAddr fa;
     fast_addr(g, color, h0, h1, h2, fa);
     TA q[8];
-    load_q_fast(coeff, fa, q);
+    load_q_fast(coeff, cl, fa, q);
     TA acc[3];
-    ku_vertex<TA>(q, kappa<TA>(), FAST_U(u), acc);
+    ku_vertex<TA>(q, kappa<TA>(), FAST_U(u, ul), acc);
     const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -440,19 +467,23 @@ __global__ void __launch_bounds__(128, MINB) l0_residual_norm_fast_kernel(GridGe
   }
 }
 
-template <typename TC, typename TN, typename TA, int MINB = 1>
+template <typename TC, typename TN, typename TA, int MINB = 1, bool ZL = false>
 __global__ void __launch_bounds__(128, MINB) l0_gs_fast_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                         const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
-                                                         int color) {
+                                                         ZLink<TC> cl, const TN* __restrict__ f,
+                                                         const TN* __restrict__ ur, ZLink<TN> ul, TN* uw, int color) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {ur, ur};
+  }
   const int h2 = blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
   FastAddr fa;
   fast_addr(g, color, h0, h1, h2, fa);
   TA q[8];
-  load_q_fast(coeff, fa, q);
+  load_q_fast(coeff, cl, fa, q);
   TA m[3], sblk[9];
-  ku_vertex_split<TA>(q, kappa<TA>(), FAST_U(ur), m, sblk);
+  ku_vertex_split<TA>(q, kappa<TA>(), FAST_U(ur, ul), m, sblk);
   const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   // solve in the nodal type: f64 for f64 nodal data (reference), f32 in the f32 inner cycle
   using TS = TN;
@@ -508,8 +539,13 @@ __global__ void __launch_bounds__(128) l0_apply_kernel(GridGeo g, const TC* __re
 }
 
 template <typename TC, typename TN, typename TA>
-void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s) {
-  if (tile_ok(g)) {
+void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s,
+                     ZLink<TC> cl, ZLink<TN> ul) {
+  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
+  if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
+  cl = resolve(cl, coeff);
+  ul = resolve(ul, u);
+  if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
     const size_t sm = tile_smem<TN>();
     IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, false>,
@@ -520,7 +556,8 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
     // f32 kernels capped at 64 registers (8 blocks/SM: more warps in flight, measured faster);
     // f64 kernels uncapped (a cap spills and was measured slower).
-    l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, u, f, y);
+    if (linked) l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1, true><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
+    else l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
   } else {
     l0_apply_kernel<TC, TN, TA><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, coeff, u, f, y);
   }
@@ -555,8 +592,13 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
 }
 
 template <typename TC, typename TN, typename TA>
-void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s) {
-  if (tile_ok(g)) {
+void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
+                        ZLink<TC> cl, ZLink<TN> ul) {
+  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
+  if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
+  cl = resolve(cl, coeff);
+  ul = resolve(ul, u);
+  if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, g.cd[0][2] / kTZ);
     const size_t sm = tile_smem<TN>();
     IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, true>,
@@ -569,11 +611,15 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
     if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
       if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
-        l0_gs_fast2_kernel<TC, TN, 5><<<gr2, b, 0, s>>>(g, coeff, f, u, u, color);
+        if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else l0_gs_fast2_kernel<TC, TN, 5><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         done = true;
       }
     }
-    if (!done) l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, f, u, u, color);
+    if (!done && linked)
+      l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1, true><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+    else if (!done)
+      l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
   } else {
     l0_gs_kernel<TC, TN, TA><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, coeff, f, u, u, color);
   }
@@ -603,9 +649,12 @@ __global__ void macro_force_kernel(GridGeo g, const TC* __restrict__ coeff, int 
 
 template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
-                                  double* partials, cudaStream_t s) {
+                                  double* partials, cudaStream_t s, ZLink<TC> cl, ZLink<double> ul) {
   if (!fast_ok(g)) throw std::invalid_argument("fused residual needs an even level-0 grid");
-  if (tile_ok(g)) {
+  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
+  cl = resolve(cl, coeff);
+  ul = resolve(ul, u);
+  if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
     const size_t sm = tile_smem<double>();
     IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_defect_kernel<TC>,
@@ -620,30 +669,62 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
     const char* e = std::getenv("IHOM_RES_MINB");
     return e ? std::atoi(e) : 3;
   }();
-  if (minb >= 4) l0_residual_norm_fast_kernel<TC, 4><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
-  else if (minb == 3) l0_residual_norm_fast_kernel<TC, 3><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
-  else l0_residual_norm_fast_kernel<TC, 1><<<gr, b, 0, s>>>(g, coeff, u, f, r32, partials);
+  if (linked) l0_residual_norm_fast_kernel<TC, 3, true><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
+  else if (minb >= 4) l0_residual_norm_fast_kernel<TC, 4><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
+  else if (minb == 3) l0_residual_norm_fast_kernel<TC, 3><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
+  else l0_residual_norm_fast_kernel<TC, 1><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }
 
+// even-grid form (FastAddr element offsets; z-slab aware)
 template <typename TC>
-void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s) {
-  macro_force_kernel<TC><<<ceil_div(g.nv, 256), 256, 0, s>>>(g, coeff, load, f);
+__global__ void __launch_bounds__(128) macro_force_fast_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                               int load, double* __restrict__ f) {
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  double q[8];
+  load_q_fast(coeff, cl, fa, q);
+  double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int ke = 0; ke < 8; ++ke)  // src/fem.cpp:145-150
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] += q[ke] * c_fmacro[ke][load][c];
+  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) f[3 * loc + c] = acc[c];
+}
+
+template <typename TC>
+void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s, ZLink<TC> cl) {
+  if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+    macro_force_fast_kernel<TC><<<gr, b, 0, s>>>(g, coeff, resolve(cl, coeff), load, f);
+  } else {
+    if (!is_self(cl, coeff)) throw std::invalid_argument("z-slab level needs an even grid");
+    macro_force_kernel<TC><<<ceil_div(g.nv, 256), 256, 0, s>>>(g, coeff, load, f);
+  }
   IHOM_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- instantiations
 template void launch_coeff<float>(const double*, float*, long long, double, cudaStream_t);
 template void launch_coeff<double>(const double*, double*, long long, double, cudaStream_t);
-template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t);
-template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t);
+template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t, ZLink<float>);
+template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t, ZLink<double>);
 template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, const double*, const double*, float*,
-                                                  double*, cudaStream_t);
+                                                  double*, cudaStream_t, ZLink<float>, ZLink<double>);
 
 #define INST_L0(TC, TN, TA)                                                                                    \
-  template void launch_l0_apply<TC, TN, TA>(const GridGeo&, const TC*, const TN*, const TN*, TN*, cudaStream_t); \
-  template void launch_l0_gs_color<TC, TN, TA>(const GridGeo&, const TC*, const TN*, TN*, int, cudaStream_t);
+  template void launch_l0_apply<TC, TN, TA>(const GridGeo&, const TC*, const TN*, const TN*, TN*, cudaStream_t, \
+                                            ZLink<TC>, ZLink<TN>);                                            \
+  template void launch_l0_gs_color<TC, TN, TA>(const GridGeo&, const TC*, const TN*, TN*, int, cudaStream_t,      \
+                                               ZLink<TC>, ZLink<TN>);
 INST_L0(float, double, double)   // mixed, f64 nodal (parity)
 INST_L0(double, double, double)  // all-double
 INST_L0(float, float, float)     // mixed inner correction cycle

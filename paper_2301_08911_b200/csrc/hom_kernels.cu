@@ -22,24 +22,28 @@ __device__ __forceinline__ int wrapp(int c, int n) { return c >= n ? c - n : c; 
 // Computes the 21 upper-triangle energies for element (ex,ey,ez) in arithmetic
 // type TE (f64 all-double; f32 in mixed mode, where u is read through the
 // reference's f32 snapshot anyway). gs: per-thread smem slice, stride kHT.
+// z-slab: the upper vertex plane of the top element layer belongs to the slab
+// above (uhi).
 template <typename TN, typename TE>
-__device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const TN* const* u, bool snap,
-                                 TE lam, TE mu, TE* gs, TE E[21]) {
+__device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const TN* const* u, const TN* const* uhi,
+                                 bool snap, TE lam, TE mu, TE* gs, TE E[21]) {
   const TE p1 = TE(0.5 + 0.5 / 1.7320508075688772);  // gp[1]; N_a(g) = (a == g) ? p1 : p0
   const TE p0 = TE(0.5 - 0.5 / 1.7320508075688772);
   unsigned loc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     loc[j] = vloc(g, wrapp(ex + (j & 1), g.n[0]), wrapp(ey + ((j >> 1) & 1), g.n[1]), wrapp(ez + ((j >> 2) & 1), g.n[2]));
+  const bool top = ez + 1 == g.n[2];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const TN* ui = u[i];
+    const TN* uz = top ? uhi[i] : u[i];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       TE U[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double v = double(ui[3 * (size_t)loc[j] + c]);
+        const double v = double(((j >> 2) & 1 ? uz : ui)[3 * (size_t)loc[j] + c]);
         U[j] = snap ? TE(float(v)) : TE(v);
       }
       // direction k: differences across k at the 4 corners of the other two axes (a,b),
@@ -131,6 +135,7 @@ __device__ __forceinline__ double block_reduce_h(double v, double* sh) {
 
 struct U6 {
   const void* p[6];
+  const void* hi[6];  // z-slab: the same fields of the slab above (== p for one periodic domain)
 };
 
 template <typename TN, typename TE>
@@ -140,8 +145,12 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
   TE* gsm = reinterpret_cast<TE*>(gsm_raw);
   __shared__ double sh[32];
   const TN* u[6];
+  const TN* uh[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) u[i] = static_cast<const TN*>(uu.p[i]);
+  for (int i = 0; i < 6; ++i) {
+    u[i] = static_cast<const TN*>(uu.p[i]);
+    uh[i] = static_cast<const TN*>(uu.hi[i]);
+  }
   double acc[21];
 #pragma unroll
   for (int q = 0; q < 21; ++q) acc[q] = 0.0;
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
     const long long r = e / g.n[0];
     const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
     TE E[21];
-    element_energies<TN, TE>(g, ex, ey, ez, u, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
+    element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
     const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
     for (int k = 0; k < 21; ++k) acc[k] += q * double(E[k]);
@@ -180,11 +189,15 @@ static void set_smem(const void* fn, bool f32) {
 
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
-                             double lam, double mu, double* partials, double* c21, cudaStream_t s) {
+                             double lam, double mu, double* partials, double* c21, cudaStream_t s,
+                             const TN* const* uhi) {
   long long blocks = (g.nv + kHT - 1) / kHT;
   if (blocks > kReducePartials) blocks = kReducePartials;
   U6 uu;
-  for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
+  for (int i = 0; i < 6; ++i) {
+    uu.p[i] = u[i];
+    uu.hi[i] = uhi ? uhi[i] : u[i];
+  }
   if (snap) {
     set_smem((const void*)tensor_kernel<TN, float>, true);
     tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials);
@@ -201,48 +214,58 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
 template <typename TN, typename TE>
 __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                    bool snap, double lam, double mu, const double* __restrict__ seed,
-                                                   double* __restrict__ out) {
+                                                   double inv_m, double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   TE* gsm = reinterpret_cast<TE*>(gsm_raw);
   const TN* u[6];
+  const TN* uh[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) u[i] = static_cast<const TN*>(uu.p[i]);
+  for (int i = 0; i < 6; ++i) {
+    u[i] = static_cast<const TN*>(uu.p[i]);
+    uh[i] = static_cast<const TN*>(uu.hi[i]);
+  }
   const long long e = (long long)blockIdx.x * kHT + threadIdx.x;
   if (e >= g.nv) return;
   const int ex = int(e % g.n[0]);
   const long long r = e / g.n[0];
   const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
   TE E[21];
-  element_energies<TN, TE>(g, ex, ey, ez, u, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
+  element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
   double acc = 0.0;  // sum_ij s_ij E_ij with s symmetric (src/homogenization.cpp:120,138-140)
   int q = 0;
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * double(E[q]);
-  out[e] = penal * pow(rho[e], penal - 1.0) * acc / double(g.nv);  // :141
+  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;  // :141 (1/M over the whole grid)
 }
 
 template <typename TN>
 void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
-                               double lam, double mu, const double* sym_seed36, double* out, cudaStream_t s) {
+                               double lam, double mu, const double* sym_seed36, double* out, cudaStream_t s,
+                               const TN* const* uhi, long long m_total) {
   U6 uu;
-  for (int i = 0; i < 6; ++i) uu.p[i] = u[i];
+  for (int i = 0; i < 6; ++i) {
+    uu.p[i] = u[i];
+    uu.hi[i] = uhi ? uhi[i] : u[i];
+  }
+  const double inv_m = 1.0 / double(m_total > 0 ? m_total : g.nv);
   if (snap) {
     set_smem((const void*)sens_kernel<TN, float>, true);
     sens_kernel<TN, float><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                             sym_seed36, out);
+                                                                             sym_seed36, inv_m, out);
   } else {
     set_smem((const void*)sens_kernel<TN, double>, false);
     sens_kernel<TN, double><<<ceil_div(g.nv, kHT), kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                               sym_seed36, out);
+                                                                               sym_seed36, inv_m, out);
   }
   IHOM_LAUNCH_CHECK();
 }
 
 template void launch_effective_tensor<double>(const GridGeo&, const double* const[6], const double*, double, bool,
-                                              double, double, double*, double*, cudaStream_t);
+                                              double, double, double*, double*, cudaStream_t, const double* const*);
 template void launch_tensor_sensitivity<double>(const GridGeo&, const double* const[6], const double*, double, bool,
-                                                double, double, const double*, double*, cudaStream_t);
+                                                double, double, const double*, double*, cudaStream_t,
+                                                const double* const*, long long);
 
 }  // namespace ihomgpu

@@ -24,36 +24,48 @@ void launch_coeff(const double* rho, TC* coeff, long long m, double penal, cudaS
 
 // y = K u (f == nullptr) or y = f - K u, over all vertices.
 template <typename TC, typename TN, typename TA>
-void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s);
+void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f, TN* y, cudaStream_t s,
+                     ZLink<TC> cl = {}, ZLink<TN> ul = {});
 
 // One colour pass of the 8-colour Gauss-Seidel (src/fem.cpp:122-137).
 template <typename TC, typename TN, typename TA>
-void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s);
+void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
+                        ZLink<TC> cl = {}, ZLink<TN> ul = {});
 
 // Fused defect residual: r32 = float(f - K u) (f64 arithmetic), per-block |r|^2 partials; returns #partials.
 template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
-                                  double* partials, cudaStream_t s);
+                                  double* partials, cudaStream_t s, ZLink<TC> cl = {}, ZLink<double> ul = {});
 
 template <typename TC>
-void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s);
+void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s, ZLink<TC> cl = {});
 
 // ---- transfer (src/multigrid.cpp:12-79) ----
+// z-slab arguments: rl / cl link the source array to the slabs
+// below / above; gout + zoff redirect the coarse output of a restriction (or
+// Galerkin product) into the replicated global coarse level at this slab's
+// first halved plane zoff; a prolongation from the replicated level reads it
+// at coarse plane offset zoff. Defaults = one periodic domain.
 template <typename TN>
-void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s);
+void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s, ZLink<TN> rl = {},
+                     const GridGeo* gout = nullptr, int zoff = 0);
 template <typename TN>
-void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s);
+void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s,
+                        ZLink<TN> cl = {}, int zoff = 0);
 
 // ---- coarse levels (src/multigrid.cpp:186-239, 281-333) ----
 template <typename TS, typename TN>
-void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s);
+void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
+                          ZLink<TN> xl = {});
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
-                             cudaStream_t s);
+                             cudaStream_t s, ZLink<TN> ul = {});
 template <typename TC>
-void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s);
+void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s,
+                                   ZLink<TC> cl = {}, const GridGeo* gout = nullptr, int zoff = 0);
 template <typename TS>
-void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s);
+void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s,
+                                  ZLink<TS> sl = {}, const GridGeo* gout = nullptr, int zoff = 0);
 
 // Coarsest level: x = Ainv f with <=3 refinement steps against A, translation
 // projection in/out, singularity flag (src/multigrid.cpp:426-451). Single block.
@@ -92,10 +104,12 @@ void copy_nodal(const double* in, double* out, long long nv, cudaStream_t s);
 // partial sums (21 per block) of q_e * d_i^T K0 d_j; finalized into C[21].
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap_f32,
-                             double lambda, double mu, double* partials, double* c21, cudaStream_t s);
+                             double lambda, double mu, double* partials, double* c21, cudaStream_t s,
+                             const TN* const* uhi = nullptr);
+// z-slab: uhi = the six fields of the slab above; m_total = elements of the whole grid (the 1/M factor)
 template <typename TN>
 void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal,
                                bool snap_f32, double lambda, double mu, const double* sym_seed36, double* out,
-                               cudaStream_t s);
+                               cudaStream_t s, const TN* const* uhi = nullptr, long long m_total = 0);
 
 }  // namespace ihomgpu

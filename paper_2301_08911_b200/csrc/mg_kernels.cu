@@ -3,6 +3,8 @@
 // 281-333, 426-451).
 #include "kernels.hpp"
 
+#include <mutex>
+
 namespace ihomgpu {
 
 // ---------------------------------------------------------------- transfer
@@ -42,8 +44,13 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
 // vertex with halved coordinates vc, so its 27 fine neighbours are FastAddr of
 // (fine grid, colour 0, h = vc). Prolongation: per axis 1 (even) or 2 (odd)
 // coarse parents; colour-specialised so the loop bounds are compile-time.
+// z-slab forms: rf's lower face links to the slab below (rl); the coarse
+// output is either this slab's coarse level (gout == gc, zoff 0) or the
+// replicated global coarse level (gout global, zoff = this slab's first coarse
+// plane in halved coordinates) -- only the slab's own planes are written.
 template <typename TN>
 __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf,
+                                                            ZLink<TN> rl, GridGeo gout, int zoff,
                                                             TN* __restrict__ fc) {
   const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
   const int h2 = blockIdx.z >> 3;
@@ -52,25 +59,31 @@ __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo 
   const int cx = 2 * h0 + (color & 1), cy = 2 * h1 + ((color >> 1) & 1), cz = 2 * h2 + ((color >> 2) & 1);
   FastAddr fa;
   fast_addr(gf, 0, cx, cy, cz, fa);
+  const TN* rb = zbase(fa, rf, rl, 0);  // fine colour 0: only the z-1 plane can wrap
   double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
     const int dx = n % 3 - 1, dy = (n / 3) % 3 - 1, dz = n / 9 - 1;
     const double w = tw1(dx) * tw1(dy) * tw1(dz);
-    const TN* r = rf + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+    const TN* r = (n < 9 ? rb : rf) + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[c] += w * double(__ldg(r + c));
   }
-  const size_t loc = (size_t)color * gc.size[0] + h0 + (size_t)gc.cd[0][0] * (h1 + (size_t)gc.cd[0][1] * h2);
+  const size_t loc =
+      (size_t)color * gout.size[0] + h0 + (size_t)gout.cd[0][0] * (h1 + (size_t)gout.cd[0][1] * (h2 + zoff));
 #pragma unroll
   for (int c = 0; c < 3; ++c) fc[3 * loc + c] = TN(acc[c]);
 }
 
+// Coarse parents of a fine vertex at halved (h0, h1, h2): coarse coordinates
+// h_k and h_k + 1 (wrapped). z-slab: the coarse level is this slab's (zoff 0;
+// the wrapped z parent is the first plane of the slab above, cl.hi) or the
+// replicated global level (zoff = the slab's first coarse plane).
 template <typename TN, int O0, int O1, int O2>
 __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1, int h2, const TN* __restrict__ uc,
-                                               double acc[3]) {
+                                               const ZLink<TN>& cl, int zoff, double acc[3]) {
   const int o[3] = {O0, O1, O2};
-  const int h[3] = {h0, h1, h2};
+  const int h[3] = {h0, h1, h2 + zoff};
   const unsigned Bc = (unsigned)gc.size[0];
   const unsigned sc[3] = {1u, (unsigned)gc.cd[0][0], (unsigned)gc.cd[0][0] * (unsigned)gc.cd[0][1]};
   unsigned P[3][2];
@@ -82,13 +95,14 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
     P[k][1] = (((unsigned)c1 & 1u) << k) * Bc + sc[k] * (unsigned)(c1 >> 1);
   }
   const double w = (O0 ? 0.5 : 1.0) * (O1 ? 0.5 : 1.0) * (O2 ? 0.5 : 1.0);
+  const TN* ub[2] = {uc, h[2] + 1 == gc.n[2] ? cl.hi : uc};
 #pragma unroll
   for (int a = 0; a < 1 + O0; ++a)
 #pragma unroll
     for (int b = 0; b < 1 + O1; ++b)
 #pragma unroll
       for (int c = 0; c < 1 + O2; ++c) {
-        const TN* u = uc + 3 * (size_t)(P[0][a] + P[1][b] + P[2][c]);
+        const TN* u = ub[c] + 3 * (size_t)(P[0][a] + P[1][b] + P[2][c]);
 #pragma unroll
         for (int d = 0; d < 3; ++d) acc[d] += w * double(__ldg(u + d));
       }
@@ -97,21 +111,21 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
 
 template <typename TN>
 __global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc,
-                                                           TN* __restrict__ uf) {
+                                                           ZLink<TN> cl, int zoff, TN* __restrict__ uf) {
   const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
   const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
   double acc[3] = {0.0, 0.0, 0.0};
   switch (color) {  // uniform per block
-    case 0: prolong_vertex<TN, 0, 0, 0>(gc, h0, h1, h2, uc, acc); break;
-    case 1: prolong_vertex<TN, 1, 0, 0>(gc, h0, h1, h2, uc, acc); break;
-    case 2: prolong_vertex<TN, 0, 1, 0>(gc, h0, h1, h2, uc, acc); break;
-    case 3: prolong_vertex<TN, 1, 1, 0>(gc, h0, h1, h2, uc, acc); break;
-    case 4: prolong_vertex<TN, 0, 0, 1>(gc, h0, h1, h2, uc, acc); break;
-    case 5: prolong_vertex<TN, 1, 0, 1>(gc, h0, h1, h2, uc, acc); break;
-    case 6: prolong_vertex<TN, 0, 1, 1>(gc, h0, h1, h2, uc, acc); break;
-    default: prolong_vertex<TN, 1, 1, 1>(gc, h0, h1, h2, uc, acc); break;
+    case 0: prolong_vertex<TN, 0, 0, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 1: prolong_vertex<TN, 1, 0, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 2: prolong_vertex<TN, 0, 1, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 3: prolong_vertex<TN, 1, 1, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 4: prolong_vertex<TN, 0, 0, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 5: prolong_vertex<TN, 1, 0, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 6: prolong_vertex<TN, 0, 1, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    default: prolong_vertex<TN, 1, 1, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
   }
   const size_t loc = (size_t)color * gf.size[0] + h0 + (size_t)gf.cd[0][0] * (h1 + (size_t)gf.cd[0][1] * h2);
 #pragma unroll
@@ -119,14 +133,17 @@ __global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo g
 }
 
 template <typename TN>
-void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s) {
+void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc, cudaStream_t s, ZLink<TN> rl,
+                     const GridGeo* gout, int zoff) {
+  const bool slab = !is_self(rl, rf) || gout;
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 8 * gc.cd[0][2]);
-    restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, fc);
+    restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc, gout ? zoff : 0, fc);
     IHOM_LAUNCH_CHECK();
     return;
   }
+  if (slab) throw std::invalid_argument("z-slab restriction needs even fine and coarse grids");
   restrict_kernel<TN><<<ceil_div(gc.nv, 128), 128, 0, s>>>(gf, gc, rf, fc);
   IHOM_LAUNCH_CHECK();
 }
@@ -167,14 +184,17 @@ __global__ void prolong_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc
 }
 
 template <typename TN>
-void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s) {
+void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s, ZLink<TN> cl,
+                        int zoff) {
+  const bool slab = !is_self(cl, uc) || zoff != 0;
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gf);
     const dim3 gr(ceil_div(gf.cd[0][0], b.x), ceil_div(gf.cd[0][1], b.y), 8 * gf.cd[0][2]);
-    prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, uf);
+    prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
     IHOM_LAUNCH_CHECK();
     return;
   }
+  if (slab) throw std::invalid_argument("z-slab prolongation needs even fine and coarse grids");
   prolong_kernel<TN><<<ceil_div(gf.nv, 128), 128, 0, s>>>(gc, gf, uc, uf);
   IHOM_LAUNCH_CHECK();
 }
@@ -214,10 +234,11 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
 
 // Fast even-grid variants (FastAddr, common.cuh): one IADD3 per neighbour
 // location, AoS components at immediate offsets, blocked stencil rows.
-template <typename TS, typename TN>
+template <typename TS, typename TN, bool ZL = false>
 __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st,
-                                                                 const TN* __restrict__ x, const TN* __restrict__ f,
-                                                                 TN* __restrict__ y) {
+                                                                 const TN* __restrict__ x, ZLink<TN> xl,
+                                                                 const TN* __restrict__ f, TN* __restrict__ y) {
+  if constexpr (!ZL) xl = {x, x};
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
   const int h2 = blockIdx.z >> 3;
@@ -228,9 +249,10 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   const TS* row = st + st_index(0, loc);
   double acc[3] = {0.0, 0.0, 0.0};
+  const TN* xb[3] = {zbase(fa, x, xl, 0), x, zbase(fa, x, xl, 2)};
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
-    const TN* xn = x + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+    const TN* xn = xb[n / 9] + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
     const double a = double(__ldg(xn)), b = double(__ldg(xn + 1)), c = double(__ldg(xn + 2));
     const TS* bl = row + 32 * 9 * n;
     acc[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
@@ -246,10 +268,11 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   }
 }
 
-template <typename TS, typename TN>
+template <typename TS, typename TN, bool ZL = false>
 __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st,
                                                               const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              TN* uw, int color, int* err) {
+                                                              ZLink<TN> ul, TN* uw, int color, int* err) {
+  if constexpr (!ZL) ul = {ur, ur};
   const int h2 = blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
@@ -260,10 +283,11 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
   double m[3] = {0.0, 0.0, 0.0}, S[9];
 #pragma unroll
   for (int e = 0; e < 9; ++e) S[e] = double(__ldg(row + 32 * (9 * 13 + e)));
+  const TN* ub[3] = {zbase(fa, ur, ul, 0), ur, zbase(fa, ur, ul, 2)};
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
     if (n == 13) continue;
-    const TN* un = ur + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+    const TN* un = ub[n / 9] + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
     const double a = double(__ldg(un)), b = double(__ldg(un + 1)), c = double(__ldg(un + 2));
     const TS* bl = row + 32 * 9 * n;
     m[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
@@ -296,6 +320,15 @@ __device__ __forceinline__ unsigned nbr_loc(const GridGeo& g, int x, int y, int 
   return vloc(g, a, b, c);
 }
 
+// neighbour n of (x, y, z) in nodal array p; z wraps through the slab links
+template <typename TN>
+__device__ __forceinline__ const TN* nbr_ptr(const GridGeo& g, const TN* p, const ZLink<TN>& zl, int x, int y, int z,
+                                             int n) {
+  const int c = z + n / 9 - 1;
+  const TN* b = c < 0 ? zl.lo : (c >= g.n[2] ? zl.hi : p);
+  return b + 3 * (size_t)nbr_loc(g, x, y, z, n);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -304,8 +337,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st,
-                                                                 const TN* __restrict__ x, const TN* __restrict__ f,
-                                                                 TN* __restrict__ y) {
+                                                                 const TN* __restrict__ x, ZLink<TN> xl,
+                                                                 const TN* __restrict__ f, TN* __restrict__ y) {
   const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (loc >= g.nv) return;
@@ -314,7 +347,7 @@ __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, cons
   block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (lane < 27) {
-    const TN* xn = x + 3 * (size_t)nbr_loc(g, vx, vy, vz, lane);
+    const TN* xn = nbr_ptr(g, x, xl, vx, vy, vz, lane);
     const double a = double(xn[0]), b = double(xn[1]), c = double(xn[2]);
     const TS* bl = st + st_index(9 * lane, (unsigned)loc);
     a0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
@@ -340,7 +373,7 @@ __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, cons
 template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st,
                                                               const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              TN* uw, int color, int* err) {
+                                                              ZLink<TN> ul, TN* uw, int color, int* err) {
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= g.size[color]) return;
@@ -349,7 +382,7 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
   const long long loc = g.base[color] + i;
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
   if (lane < 27 && lane != 13) {
-    const TN* un = ur + 3 * (size_t)nbr_loc(g, vx, vy, vz, lane);
+    const TN* un = nbr_ptr(g, ur, ul, vx, vy, vz, lane);
     const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
     const TS* bl = st + st_index(9 * lane, (unsigned)loc);
     m0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
@@ -381,14 +414,19 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
 constexpr long long kWarpVertexMax = 32768;  // levels up to 64^3 use warp-per-vertex
 
 template <typename TS, typename TN>
-void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s) {
+void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
+                          ZLink<TN> xl) {
+  const bool linked = !is_self(xl, x);
+  xl = resolve(xl, x);
   if (g.nv <= 8 * kWarpVertexMax) {
-    stencil_apply_warp_kernel<TS, TN><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, x, f, y);
+    stencil_apply_warp_kernel<TS, TN><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, x, xl, f, y);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    stencil_apply_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, x, f, y);
+    if (linked) stencil_apply_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, x, xl, f, y);
+    else stencil_apply_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, x, xl, f, y);
   } else {
+    if (linked) throw std::invalid_argument("z-slab level needs an even grid");
     stencil_apply_kernel<TS, TN><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, x, f, y);
   }
   IHOM_LAUNCH_CHECK();
@@ -437,14 +475,18 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
 
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
-                             cudaStream_t s) {
+                             cudaStream_t s, ZLink<TN> ul) {
+  const bool linked = !is_self(ul, u);
+  ul = resolve(ul, u);
   if (g.size[color] <= kWarpVertexMax) {
-    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, ul, u, color, err);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, u, color, err);
+    if (linked) stencil_gs_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err);
+    else stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err);
   } else {
+    if (linked) throw std::invalid_argument("z-slab level needs an even grid");
     stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err);
   }
   IHOM_LAUNCH_CHECK();
@@ -485,9 +527,11 @@ void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
 // 64 fine coefficients of a region are fetched once and reused from L1/L2. The
 // term list of n (<= 64 x (oidx, W[9])) is staged in shared memory (broadcast reads).
 constexpr int kMaxEgPerN = 64;
+// z-slab form: fine element planes below the slab (2 z - 2, 2 z - 1 < 0) come
+// from the slab below (cl.lo); the output goes to gout at halved plane h2 + zoff.
 template <typename TC>
 __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
-                                                       TC* __restrict__ st) {
+                                                       ZLink<TC> cl, GridGeo gout, int zoff, TC* __restrict__ st) {
   __shared__ double w_s[kMaxEgPerN][9];
   __shared__ int o_s[kMaxEgPerN];
   const int n = blockIdx.z % 27;
@@ -508,14 +552,17 @@ __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, c
     ey[o] = gf.n[0] * wrapi(2 * y + o - 2, gf.n[1]);
     ez[o] = gf.n[0] * gf.n[1] * wrapi(2 * z + o - 2, gf.n[2]);
   }
+  const TC* zb[2] = {2 * z - 2 < 0 ? cl.lo : coeff, 2 * z - 1 < 0 ? cl.lo : coeff};  // planes o = 0, 1
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int k = 0; k < nt; ++k) {
     const int oi = o_s[k];
-    const double q = double(__ldg(coeff + (ex[oi & 3] + ey[(oi >> 2) & 3] + ez[oi >> 4])));
+    const int oz = oi >> 4;
+    const double q = double(__ldg((oz < 2 ? zb[oz] : coeff) + (ex[oi & 3] + ey[(oi >> 2) & 3] + ez[oz])));
 #pragma unroll
     for (int e = 0; e < 9; ++e) acc[e] += q * w_s[k][e];
   }
-  const unsigned loc = (unsigned)(color * gc.size[0] + h0 + (long long)gc.cd[0][0] * (h1 + (long long)gc.cd[0][1] * h2));
+  const unsigned loc =
+      (unsigned)(color * gout.size[0] + h0 + (long long)gout.cd[0][0] * (h1 + (long long)gout.cd[0][1] * (h2 + zoff)));
 #pragma unroll
   for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, loc)] = TC(acc[e]);
 }
@@ -549,12 +596,14 @@ __global__ void __launch_bounds__(128) gal_elem_generic_kernel(GridGeo gf, GridG
 }
 
 template <typename TC>
-void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s) {
+void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s,
+                                   ZLink<TC> cl, const GridGeo* gout, int zoff) {
   if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
-    gal_elem_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, st);
+    gal_elem_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, resolve(cl, coeff), gout ? *gout : gc, gout ? zoff : 0, st);
   } else {
+    if (!is_self(cl, coeff) || gout) throw std::invalid_argument("z-slab Galerkin needs an even coarse grid");
     gal_elem_generic_kernel<TC><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, coeff, st);
   }
   IHOM_LAUNCH_CHECK();
@@ -572,7 +621,9 @@ __constant__ unsigned short c_sg_st[kMaxSgTerms];  // s | t << 5
 __constant__ float c_sg_w[kMaxSgTerms];            // products of 1, 1/2, 1/4, 1/8: exact in f32
 
 static void upload_stencil_galerkin(cudaStream_t s) {
+  static std::mutex mu;
   static bool done = false;
+  std::lock_guard<std::mutex> lock(mu);  // z-slab threads share the process's constant tables
   if (done) return;
   static int start[28];
   static unsigned short st[kMaxSgTerms];
@@ -625,6 +676,7 @@ __global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc
 // per thread with FastAddr and kept in shared memory.
 template <typename TS>
 __global__ void __launch_bounds__(128) gal_stencil_fast_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
+                                                               ZLink<TS> sl, GridGeo gout, int zoff,
                                                                TS* __restrict__ stc) {
   __shared__ unsigned fls[27][128];
   const int n = blockIdx.z % 27;
@@ -638,29 +690,34 @@ __global__ void __launch_bounds__(128) gal_stencil_fast_kernel(GridGeo gf, GridG
   fast_addr(gf, 0, x, y, z, fa);
 #pragma unroll
   for (int s = 0; s < 27; ++s) fls[s][tid] = fa.A[0][s % 3] + fa.A[1][(s / 3) % 3] + fa.A[2][s / 9];
+  const TS* lo = zbase(fa, stf, sl, 0);  // fine rows of the z-1 plane (fine colour 0: only that one wraps)
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int k1 = c_sg_start[n + 1];
   for (int k = c_sg_start[n]; k < k1; ++k) {
     const int st = c_sg_st[k];
-    const unsigned fl = fls[st & 31][tid];
+    const int sv = st & 31;
+    const unsigned fl = fls[sv][tid];
     const double w = double(c_sg_w[k]);
-    const TS* b = stf + st_index(9 * (st >> 5), fl);
+    const TS* b = (sv < 9 ? lo : stf) + st_index(9 * (st >> 5), fl);
 #pragma unroll
     for (int e = 0; e < 9; ++e) acc[e] += w * double(__ldg(b + 32 * e));
   }
-  const unsigned loc = (unsigned)(color * gc.size[0] + h0 + (long long)gc.cd[0][0] * (h1 + (long long)gc.cd[0][1] * h2));
+  const unsigned loc =
+      (unsigned)(color * gout.size[0] + h0 + (long long)gout.cd[0][0] * (h1 + (long long)gout.cd[0][1] * (h2 + zoff)));
 #pragma unroll
   for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, loc)] = TS(acc[e]);
 }
 
 template <typename TS>
-void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s) {
+void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS* stf, TS* stc, cudaStream_t s,
+                                  ZLink<TS> sl, const GridGeo* gout, int zoff) {
   upload_stencil_galerkin(s);
   if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0 && fast_ok(gf)) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
-    gal_stencil_fast_kernel<TS><<<gr, b, 0, s>>>(gf, gc, stf, stc);
+    gal_stencil_fast_kernel<TS><<<gr, b, 0, s>>>(gf, gc, stf, resolve(sl, stf), gout ? *gout : gc, gout ? zoff : 0, stc);
   } else {
+    if (!is_self(sl, stf) || gout) throw std::invalid_argument("z-slab Galerkin needs even grids");
     gal_stencil_kernel<TS><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, stf, stc);
   }
   IHOM_LAUNCH_CHECK();
@@ -764,20 +821,31 @@ void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const dou
 }
 
 // ---------------------------------------------------------------- instantiations
-template void launch_restrict<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
-template void launch_restrict<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
-template void launch_prolong_add<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
-template void launch_prolong_add<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
-template void launch_stencil_apply<float, double>(const GridGeo&, const float*, const double*, const double*, double*, cudaStream_t);
-template void launch_stencil_apply<double, double>(const GridGeo&, const double*, const double*, const double*, double*, cudaStream_t);
-template void launch_stencil_apply<float, float>(const GridGeo&, const float*, const float*, const float*, float*, cudaStream_t);
-template void launch_stencil_gs_color<float, double>(const GridGeo&, const float*, const double*, double*, int, int*, cudaStream_t);
-template void launch_stencil_gs_color<double, double>(const GridGeo&, const double*, const double*, double*, int, int*, cudaStream_t);
-template void launch_stencil_gs_color<float, float>(const GridGeo&, const float*, const float*, float*, int, int*, cudaStream_t);
-template void launch_galerkin_from_elements<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
-template void launch_galerkin_from_elements<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
-template void launch_galerkin_from_stencil<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t);
-template void launch_galerkin_from_stencil<double>(const GridGeo&, const GridGeo&, const double*, double*, cudaStream_t);
+#define INST_T(TN)                                                                                              \
+  template void launch_restrict<TN>(const GridGeo&, const GridGeo&, const TN*, TN*, cudaStream_t, ZLink<TN>,   \
+                                    const GridGeo*, int);                                                       \
+  template void launch_prolong_add<TN>(const GridGeo&, const GridGeo&, const TN*, TN*, cudaStream_t, ZLink<TN>, \
+                                       int);
+INST_T(double)
+INST_T(float)
+#undef INST_T
+#define INST_S(TS, TN)                                                                                       \
+  template void launch_stencil_apply<TS, TN>(const GridGeo&, const TS*, const TN*, const TN*, TN*, cudaStream_t, \
+                                             ZLink<TN>);                                                      \
+  template void launch_stencil_gs_color<TS, TN>(const GridGeo&, const TS*, const TN*, TN*, int, int*,         \
+                                                cudaStream_t, ZLink<TN>);
+INST_S(float, double)
+INST_S(double, double)
+INST_S(float, float)
+#undef INST_S
+template void launch_galerkin_from_elements<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t,
+                                                   ZLink<float>, const GridGeo*, int);
+template void launch_galerkin_from_elements<double>(const GridGeo&, const GridGeo&, const double*, double*,
+                                                    cudaStream_t, ZLink<double>, const GridGeo*, int);
+template void launch_galerkin_from_stencil<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t,
+                                                  ZLink<float>, const GridGeo*, int);
+template void launch_galerkin_from_stencil<double>(const GridGeo&, const GridGeo&, const double*, double*,
+                                                   cudaStream_t, ZLink<double>, const GridGeo*, int);
 template void launch_coarsest_solve<double>(int, long long, const double*, const double*, double*, double*, double, double*, int*, cudaStream_t);
 template void launch_coarsest_solve<float>(int, long long, const double*, const double*, float*, float*, double, double*, int*, cudaStream_t);
 

@@ -26,6 +26,7 @@
 #ifndef IHOM_B200_H_
 #define IHOM_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -94,6 +95,26 @@ int ihom_effective_tensor(ihom_ctx* ctx, double C[36]);                         
 int ihom_tensor_sensitivity(ihom_ctx* ctx, const double seed[36], double* out, int where); /* tensor_sensitivity */
 int ihom_get_displacement(ihom_ctx* ctx, int load, double* u_aos, int where);     /* displacement(i) */
 int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u_aos, int where);
+
+/* ---- z-slab decomposition ----
+ * A grid of n[2] z planes is split into nranks slabs of t = n[2] / nranks
+ * planes (t a multiple of 4); slab r holds planes [r t, (r+1) t) of every
+ * element / vertex field (x-fastest elements; nodal fields in the slab's own
+ * colour-block order). Slabs read across their faces directly from the
+ * neighbours' memory: a LOCAL fabric keeps all slabs of a grid in this process
+ * on one device (one host thread per slab); an IPC fabric maps one slab per
+ * process over NVLink, exchanging CUDA IPC handles through the caller's
+ * host allgather (e.g. torch.distributed). Every ihom_*_slab context call is
+ * collective over the slabs of its fabric. The reference has no distributed
+ * mode; this replaces nothing and keeps every per-slab result equal to the
+ * single-domain one up to the order of the cross-slab sums. */
+typedef struct ihom_fabric ihom_fabric;
+typedef void (*ihom_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
+ihom_fabric* ihom_fabric_local(int nranks, int device);
+ihom_fabric* ihom_fabric_ipc(int rank, int nranks, int device, ihom_allgather_fn allgather, void* user);
+void ihom_fabric_destroy(ihom_fabric* f);
+ihom_ctx* ihom_create_slab(const ihom_desc* desc, const ihom_solver_opts* opts, ihom_fabric* f, int rank);
+int ihom_slab_info(ihom_ctx* ctx, int* z0, int* planes, int* nranks);
 
 /* ---- Hierarchy (inc/multigrid.hpp:53-93), via hierarchy() ---- */
 int ihom_num_levels(ihom_ctx* ctx);

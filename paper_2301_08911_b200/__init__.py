@@ -302,25 +302,113 @@ class Hierarchy:
         _check(lib().ihom_bench_op(self._ctx(), op.encode(), int(reps)))
 
 
+_ALLGATHER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class Fabric:
+    """How the z-slabs of one grid reach each other (include/ihom_b200.h).
+
+    Fabric.local(P): all P slabs in this process on one device, one host thread
+    per slab (every slab call is collective: drive the slabs from P threads, see
+    run_slabs). Fabric.ipc(rank, P, allgather): one slab per process; CUDA IPC
+    handles travel through ``allgather(bytes) -> list[bytes]`` (e.g. built on
+    torch.distributed), peers are read over NVLink.
+    """
+
+    def __init__(self, ptr, nranks, keep=None):
+        if not ptr:
+            _raise_last()
+        self._p, self.nranks, self._keep = ptr, int(nranks), keep
+
+    @staticmethod
+    def local(nranks: int, device: int = 0) -> "Fabric":
+        L = lib()
+        L.ihom_fabric_local.restype = C.c_void_p
+        L.ihom_fabric_local.argtypes = [C.c_int, C.c_int]
+        return Fabric(L.ihom_fabric_local(int(nranks), int(device)), nranks)
+
+    @staticmethod
+    def ipc(rank: int, nranks: int, allgather: Callable, device: int = 0) -> "Fabric":
+        def _cb(send, recv, nbytes, user):
+            parts = allgather(C.string_at(send, nbytes))
+            blob = b"".join(parts)
+            C.memmove(recv, blob, len(blob))
+        cb = _ALLGATHER_FN(_cb)
+        L = lib()
+        L.ihom_fabric_ipc.restype = C.c_void_p
+        L.ihom_fabric_ipc.argtypes = [C.c_int, C.c_int, C.c_int, _ALLGATHER_FN, C.c_void_p]
+        return Fabric(L.ihom_fabric_ipc(int(rank), int(nranks), int(device), cb, None), nranks, keep=cb)
+
+    def close(self):
+        if getattr(self, "_p", None):
+            L = lib()
+            L.ihom_fabric_destroy.argtypes = [C.c_void_p]
+            L.ihom_fabric_destroy(C.c_void_p(self._p))
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_slabs(nranks: int, fn: Callable[[int], object]) -> list:
+    """Runs fn(rank) for every slab of a local fabric in its own thread; returns the results by rank
+    (re-raises the first exception). ctypes releases the GIL inside library calls."""
+    import threading
+    out, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
 class Homogenizer:
     """Device twin of ihom::Homogenizer<T> (inc/homogenization.hpp:26-51).
 
     precision 'mixed' = Homogenizer<float> (f32 coefficients/stencils, f64 nodal);
-    'double' = Homogenizer<double>.
+    'double' = Homogenizer<double>. With ``fabric`` the context holds z-slab
+    ``rank`` of the grid (planes [z0, z0 + planes)); densities and sensitivities
+    are then that slab's elements and every call is collective over the slabs.
     """
 
     def __init__(self, reso, mat: BaseMaterial = None, penal: float = 3.0, opts: SolverOptions = None,
-                 precision: str = "mixed", device: int = 0):
+                 precision: str = "mixed", device: int = 0, fabric: Optional[Fabric] = None, rank: int = 0):
         mat = mat or BaseMaterial()
         opts = opts or SolverOptions()
         self.n = _n3(reso)
-        self.nv = int(np.prod(self.n))
         self.mat, self.penal, self.precision, self._opts = mat, penal, precision, opts
         d = _Desc((C.c_int * 3)(*self.n), mat.youngs, mat.poisson, penal, PRECISION[precision], device)
         o = opts._c()
-        self._p = lib().ihom_create(C.byref(d), C.byref(o))
+        if fabric is None:
+            self._p = lib().ihom_create(C.byref(d), C.byref(o))
+        else:
+            L = lib()
+            L.ihom_create_slab.restype = C.c_void_p
+            L.ihom_create_slab.argtypes = [C.POINTER(_Desc), C.POINTER(_SolverOpts), C.c_void_p, C.c_int]
+            self._p = L.ihom_create_slab(C.byref(d), C.byref(o), C.c_void_p(fabric._p), int(rank))
         if not self._p:
             _raise_last()
+        self.fabric = fabric
+        z0, t, P = C.c_int(), C.c_int(), C.c_int()
+        L = lib()
+        L.ihom_slab_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        _check(L.ihom_slab_info(self._ctx(), C.byref(z0), C.byref(t), C.byref(P)))
+        self.z0, self.planes, self.nranks = z0.value, t.value, P.value
+        self.nv = self.n[0] * self.n[1] * self.planes  # vertices / elements held by this context
 
     def _ctx(self):
         if not self._p:

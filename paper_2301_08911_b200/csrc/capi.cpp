@@ -23,7 +23,9 @@ using namespace ihomgpu;
 namespace {
 
 thread_local std::string g_err;
-const void* g_bound = nullptr;  // context whose constant tables are resident
+// context whose constant tables this thread bound last (z-slab threads each bind
+// their own context; the tables are per material, identical across slabs)
+thread_local const void* g_bound = nullptr;
 
 template <class F>
 int guarded(F&& f) {
@@ -126,6 +128,10 @@ struct DevOut {
 
 }  // namespace
 
+struct ihom_fabric {
+  std::unique_ptr<Fabric> f;
+};
+
 struct ihom_ctx {
   std::unique_ptr<Comm> comm;
   int device = 0;
@@ -147,7 +153,8 @@ struct ihom_ctx {
     if (hf) f(*hf);
     else f(*hd);
   }
-  long long nv() const { return (long long)n[0] * n[1] * n[2]; }
+  // vertices stored by this context (its z-slab's share of the grid)
+  long long nv() const { return hf ? hf->nv() : hd->nv(); }
 };
 
 extern "C" {
@@ -155,7 +162,7 @@ extern "C" {
 const char* ihom_last_error(void) { return g_err.c_str(); }
 const char* ihom_version(void) { return "ihom-b200 0.1 (sm_100a)"; }
 
-ihom_ctx* ihom_create(const ihom_desc* d, const ihom_solver_opts* o) {
+static ihom_ctx* create_ctx(const ihom_desc* d, const ihom_solver_opts* o, Slab slab) {
   ihom_ctx* ctx = nullptr;
   const int rc = guarded([&] {
     if (!d) throw std::invalid_argument("null descriptor");
@@ -175,14 +182,60 @@ ihom_ctx* ihom_create(const ihom_desc* d, const ihom_solver_opts* o) {
       so.post_sweeps = o->post_sweeps;
       so.mode = o->mode;
     }
-    if (d->precision == IHOM_ALL_DOUBLE) c->hd = std::make_unique<Homogenizer<double>>(d->n, m, d->penal, so, c->s);
-    else if (d->precision == IHOM_MIXED) c->hf = std::make_unique<Homogenizer<float>>(d->n, m, d->penal, so, c->s);
+    if (d->precision == IHOM_ALL_DOUBLE)
+      c->hd = std::make_unique<Homogenizer<double>>(d->n, m, d->penal, so, c->s, slab);
+    else if (d->precision == IHOM_MIXED)
+      c->hf = std::make_unique<Homogenizer<float>>(d->n, m, d->penal, so, c->s, slab);
     else throw std::invalid_argument("precision must be IHOM_MIXED or IHOM_ALL_DOUBLE");
     c->stage.alloc(size_t(3 * c->nv()));
     g_bound = c.get();
     ctx = c.release();
   });
   return rc == IHOM_OK ? ctx : nullptr;
+}
+
+ihom_ctx* ihom_create(const ihom_desc* d, const ihom_solver_opts* o) { return create_ctx(d, o, Slab{}); }
+
+ihom_ctx* ihom_create_slab(const ihom_desc* d, const ihom_solver_opts* o, ihom_fabric* f, int rank) {
+  if (!f) {
+    g_err = "null fabric";
+    return nullptr;
+  }
+  return create_ctx(d, o, Slab{f->f.get(), rank, f->f->size()});
+}
+
+ihom_fabric* ihom_fabric_local(int nranks, int device) {
+  ihom_fabric* out = nullptr;
+  guarded([&] {
+    auto f = std::make_unique<ihom_fabric>();
+    f->f = std::make_unique<LocalFabric>(nranks, device);
+    out = f.release();
+  });
+  return out;
+}
+
+ihom_fabric* ihom_fabric_ipc(int rank, int nranks, int device, ihom_allgather_fn ag, void* user) {
+  ihom_fabric* out = nullptr;
+  guarded([&] {
+    auto f = std::make_unique<ihom_fabric>();
+    f->f = std::make_unique<IpcFabric>(rank, nranks, device, reinterpret_cast<HostAllgather>(ag), user);
+    out = f.release();
+  });
+  return out;
+}
+
+void ihom_fabric_destroy(ihom_fabric* f) { delete f; }
+
+int ihom_slab_info(ihom_ctx* ctx, int* z0, int* planes, int* nranks) {
+  return guarded([&] {
+    ctx->with([&](auto& h) {
+      const Slab& sl = h.hierarchy().slab();
+      const int t = h.hierarchy().geo(0).n[2];
+      if (z0) *z0 = sl.rank * t;
+      if (planes) *planes = t;
+      if (nranks) *nranks = sl.nranks;
+    });
+  });
 }
 
 void ihom_destroy(ihom_ctx* ctx) {

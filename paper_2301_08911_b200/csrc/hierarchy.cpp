@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 namespace ihomgpu {
@@ -113,22 +114,44 @@ bool can_coarsen(const GridGeo& g) {  // inc/grid.hpp:47-51
 
 // ============================================================== Hierarchy
 template <typename T>
-Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s)
-    : mat_(mat), penal_(penal), s_(s) {
+Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab)
+    : mat_(mat), penal_(penal), s_(s), slab_(slab) {
   for (int k = 0; k < 3; ++k)
     if (n[k] < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
   if ((long long)n[0] * n[1] * n[2] >= (1LL << 31)) throw std::invalid_argument("grid too large for 32-bit vertex indexing");
+  int t = n[2];
+  if (slab_.on()) {  // z-slab constraints
+    if (slab_.rank < 0 || slab_.rank >= slab_.nranks || slab_.nranks != slab_.fab->size())
+      throw std::invalid_argument("bad z-slab rank / count");
+    if (n[2] % slab_.nranks != 0) throw std::invalid_argument("z planes must divide evenly among the slabs");
+    t = n[2] / slab_.nranks;
+    if (t % 4 != 0) throw std::invalid_argument("each z-slab needs a multiple of 4 planes");
+    if (n[0] % 2 != 0 || n[1] % 2 != 0 || n[0] < 8) throw std::invalid_argument("z-slabs need even x/y dims, x >= 8");
+  }
   k0_ = element_stiffness(mat);
   bind_tables();
   GridGeo g = make_geo(n[0], n[1], n[2]);
-  levels_.emplace_back();
-  levels_.back().g = g;
+  std::vector<GridGeo> global{g};
   while (can_coarsen(g)) {
     g = make_geo(g.n[0] / 2, g.n[1] / 2, g.n[2] / 2);
-    levels_.emplace_back();
-    levels_.back().g = g;
+    global.push_back(g);
   }
-  if (levels_.back().g.nv > 343) throw std::invalid_argument("coarsest level larger than 7^3 is not supported");
+  if (global.back().nv > 343) throw std::invalid_argument("coarsest level larger than 7^3 is not supported");
+  bool sharding = slab_.on();
+  for (size_t l = 0; l < global.size(); ++l) {
+    levels_.emplace_back();
+    Level& L = levels_.back();
+    const GridGeo& G = global[l];
+    L.nv_global = G.nv;
+    // level l is split into slabs while every slab keeps >= 4 planes (a multiple of 4,
+    // so the restriction into the next level stays on even colour blocks) and the
+    // even-grid kernels apply; below, every slab holds the whole (small) level.
+    sharding = sharding && (t % (4 << l) == 0) && G.n[0] % 2 == 0 && G.n[1] % 2 == 0 && G.n[0] >= 8;
+    L.sharded = sharding;
+    L.g = sharding ? make_geo(G.n[0], G.n[1], t >> l) : G;
+    if (slab_.on() && !sharding && rep0_ > int(l)) rep0_ = int(l);
+  }
+  if (slab_.on() && !levels_[0].sharded) throw std::invalid_argument("level 0 cannot be split into these slabs");
   for (size_t l = 0; l < levels_.size(); ++l) {
     Level& L = levels_[l];
     const size_t n3 = size_t(3 * L.g.nv);
@@ -152,10 +175,111 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
   ws_.scalars = ws_.scalar + 8;
   ws_.flag = err_.p;
   IHOM_CUDA(cudaMallocHost(&h_pinned_, 64 * sizeof(double)));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+  if (slab_.on()) {  // collective, same order on every slab
+    coeff_l_ = link(coeff_.p);
+    for (size_t l = 0; l < levels_.size(); ++l) {
+      Level& L = levels_[l];
+      if (L.sharded) {
+        L.ul = link(L.u.p);
+        L.rl = link(L.r.p);
+        if (l > 0) L.stl = link(L.st.p);
+      } else if (int(l) == rep0_) {
+        L.fpeer = peer_table(slab_.fab->exchange(slab_.rank, L.f.p));
+        L.stpeer = peer_table(slab_.fab->exchange(slab_.rank, L.st.p));
+      }
+    }
+  }
+}
+
+template <typename T>
+GridGeo Hierarchy<T>::transition_geo() const {
+  const GridGeo& f = levels_[size_t(rep0_ - 1)].g;
+  return make_geo(f.n[0] / 2, f.n[1] / 2, f.n[2] / 2);
+}
+
+template <typename T>
+int Hierarchy<T>::transition_zoff_h() const {
+  return slab_.rank * (levels_[size_t(rep0_ - 1)].g.n[2] / 4);
+}
+
+template <typename T>
+void Hierarchy<T>::sync() {
+  if (slab_.on()) slab_.fab->barrier(slab_.rank, s_);
+}
+
+template <typename T>
+void Hierarchy<T>::allreduce(double* dev, int n, bool is_max) {
+  if (slab_.on()) slab_.fab->allreduce(slab_.rank, dev, n, is_max, s_);
+}
+
+template <typename T>
+template <typename X>
+void Hierarchy<T>::gather_owned(int l, X* dst, PeerTable peers, int per_vertex) {
+  sync();  // every owner's planes written
+  {
+    ProfScope p(s_, "slab_gather", double(levels_[size_t(l)].g.nv) * per_vertex * sizeof(X));
+    launch_gather_owned<X>(levels_[size_t(l)].g, peers, levels_[size_t(l - 1)].g.n[2] / 2, slab_.rank, per_vertex,
+                           dst, s_);
+  }
+  ++launches_;
+  sync();  // nobody rewrites its planes while others still read them
+}
+
+template <typename T>
+void Hierarchy<T>::restrict_to(int l, const double* r, double* f) {
+  Level& F = levels_[size_t(l)];
+  Level& C = levels_[size_t(l + 1)];
+  const ZLink<double> rl = F.rl;
+  if (F.sharded) sync();
+  {
+    ProfScope p(s_, "restrict", double(F.g.nv) * 27.0);
+    if (!slab_.on() || C.sharded) {
+      launch_restrict<double>(F.g, C.g, r, f, s_, F.sharded ? rl : ZLink<double>{});
+    } else {
+      const GridGeo gc = transition_geo();
+      launch_restrict<double>(F.g, gc, r, f, s_, rl, &C.g, transition_zoff_h());
+    }
+  }
+  ++launches_;
+  if (slab_.on() && !C.sharded && F.sharded) gather_owned<double>(l + 1, f, C.fpeer, 3);
+}
+
+template <typename T>
+void Hierarchy<T>::restrict_to_f32(int l) {
+  Level& F = levels_[size_t(l)];
+  Level& C = levels_[size_t(l + 1)];
+  if (F.sharded) sync();
+  {
+    ProfScope p(s_, "restrict", double(F.g.nv) * 13.5);
+    if (!slab_.on() || C.sharded) {
+      launch_restrict<float>(F.g, C.g, F.er.p, C.ef.p, s_, F.sharded ? F.erl : ZLink<float>{});
+    } else {
+      const GridGeo gc = transition_geo();
+      launch_restrict<float>(F.g, gc, F.er.p, C.ef.p, s_, F.erl, &C.g, transition_zoff_h());
+    }
+  }
+  ++launches_;
+  if (slab_.on() && !C.sharded && F.sharded) gather_owned<float>(l + 1, C.ef.p, C.efpeer, 3);
+}
+
+template <typename T>
+void Hierarchy<T>::prolong_from(int l, const double* uc, double* u, ZLink<double> cl) {
+  Level& F = levels_[size_t(l)];
+  Level& C = levels_[size_t(l + 1)];
+  if (F.sharded) sync();
+  {
+    ProfScope p(s_, "prolong", double(F.g.nv) * 51.0);
+    if (!slab_.on() || C.sharded) launch_prolong_add<double>(C.g, F.g, uc, u, s_, C.sharded ? cl : ZLink<double>{});
+    else launch_prolong_add<double>(C.g, F.g, uc, u, s_, {}, slab_.rank * (F.g.n[2] / 2));
+  }
+  ++launches_;
 }
 
 template <typename T>
 void Hierarchy<T>::bind_tables() {
+  static std::mutex mu;  // z-slab threads of one process share the constant tables
+  std::lock_guard<std::mutex> lock(mu);
   const StiffnessTables tab(k0_);
   upload_fem_tables(tab, k0_, s_);
   upload_galerkin_tables(ElementGalerkin(k0_), s_);
@@ -169,16 +293,23 @@ void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-27
     launch_coeff<T>(rho, coeff_.p, g0.nv, penal_, s_);
   }
   launches_ += 1;
-  if (levels_.size() > 1) {
-    {
-      ProfScope p(s_, "galerkin_l1", double(g0.nv) * sizeof(T) + double(levels_[1].g.nv) * 243.0 * sizeof(T));
-      launch_galerkin_from_elements<T>(g0, levels_[1].g, coeff_.p, levels_[1].st.p, s_);
+  for (size_t l = 1; l < levels_.size(); ++l) {
+    Level& F = levels_[l - 1];
+    Level& C = levels_[l];
+    const bool transition = slab_.on() && F.sharded && !C.sharded;
+    const GridGeo gc = transition ? transition_geo() : C.g;
+    const GridGeo* gout = transition ? &C.g : nullptr;
+    const int zoff = transition ? transition_zoff_h() : 0;
+    if (F.sharded) sync();
+    if (l == 1) {
+      ProfScope p(s_, "galerkin_l1", double(g0.nv) * sizeof(T) + double(gc.nv) * 243.0 * sizeof(T));
+      launch_galerkin_from_elements<T>(g0, gc, coeff_.p, C.st.p, s_, F.sharded ? coeff_l_ : ZLink<T>{}, gout, zoff);
+    } else {
+      ProfScope p(s_, "galerkin_coarse", double(F.g.nv + gc.nv) * 243.0 * sizeof(T));
+      launch_galerkin_from_stencil<T>(F.g, gc, F.st.p, C.st.p, s_, F.sharded ? F.stl : ZLink<T>{}, gout, zoff);
     }
-    for (size_t l = 2; l < levels_.size(); ++l) {
-      ProfScope p(s_, "galerkin_coarse", double(levels_[l - 1].g.nv + levels_[l].g.nv) * 243.0 * sizeof(T));
-      launch_galerkin_from_stencil<T>(levels_[l - 1].g, levels_[l].g, levels_[l - 1].st.p, levels_[l].st.p, s_);
-    }
-    launches_ += (long long)levels_.size() - 1;
+    ++launches_;
+    if (transition) gather_owned<T>(int(l), C.st.p, C.stpeer, 243);
   }
   factor_coarsest();
   density_set_ = true;
@@ -226,8 +357,16 @@ double Hierarchy<T>::negligible_load(long long ndof) const {  // src/multigrid.c
 template <typename T>
 void Hierarchy<T>::check_error(const char* where) {
   int e = 0;
-  IHOM_CUDA(cudaMemcpyAsync(&e, err_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
-  IHOM_CUDA(cudaStreamSynchronize(s_));
+  if (slab_.on()) {  // collective: every slab throws together (or none does)
+    launch_int_to_double(err_.p, ws_.scalars + 60, s_);
+    allreduce(ws_.scalars + 60, 1, true);
+    IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 60, sizeof(double), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    e = int(h_pinned_[0]);
+  } else {
+    IHOM_CUDA(cudaMemcpyAsync(&e, err_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+  }
   if (e) {
     IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
     if (e == 1) throw NumericError(std::string("non-invertible coarse stencil diagonal (") + where + ")");
@@ -237,14 +376,16 @@ void Hierarchy<T>::check_error(const char* where) {
 
 template <typename T>
 void Hierarchy<T>::remove_translations(double* f, int l) {  // src/multigrid.cpp:81-86
-  const long long nv = levels_[size_t(l)].g.nv;
+  const Level& L = levels_[size_t(l)];
+  const long long nv = L.g.nv;
   {
     ProfScope p(s_, "reduce", double(nv) * 24.0);
     launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
   }
+  if (L.sharded) allreduce(ws_.scalars, 3);  // component sums over the whole grid
   {
     ProfScope p(s_, "vector", double(nv) * 48.0);
-    launch_sub_means<double>(f, nv, ws_.scalars, s_);
+    launch_sub_means<double>(f, nv, ws_.scalars, s_, L.nv_global);
   }
   launches_ += 3;
 }
@@ -256,6 +397,7 @@ double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:
     launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_);
   }
   launches_ += 2;
+  allreduce(ws_.scalars + 4, 1);  // level-0 fields only: split over the slabs
   IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
   return std::sqrt(h_pinned_[0]);
@@ -264,6 +406,7 @@ double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:
 template <typename T>
 void Hierarchy<T>::apply(int l, const double* x, double* y) {  // src/multigrid.cpp:392-398
   const Level& L = levels_[size_t(l)];
+  if (L.sharded) throw std::invalid_argument("apply() on a z-slab level: use the solver operations");
   if (l == 0) {
     ProfScope p(s_, "l0_apply", resid_l0_bytes(L.g, 8, sizeof(T), false));
     launch_l0_apply<T, double, double>(L.g, coeff_.p, x, nullptr, y, s_);
@@ -278,15 +421,17 @@ template <typename T>
 void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
   Level& L = levels_[size_t(l)];
   double* u = level_u(l);
+  const ZLink<double> ul = L.sharded ? ulink(l) : ZLink<double>{};
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
+      if (L.sharded) sync();  // colour c-1 of the neighbouring slabs is final
       if (l == 0) {
         ProfScope p(s_, "l0_gs_f64", gs_l0_bytes(L.g, c, 8, sizeof(T)));
-        launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_);
+        launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_, L.sharded ? coeff_l_ : ZLink<T>{}, ul);
       } else {
         ProfScope p(s_, l == 1 ? "l1_gs_f64" : "coarse_gs_f64", gs_coarse_bytes(L.g, c, 8, sizeof(T)));
-        launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_);
+        launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_, ul);
       }
       ++launches_;
     }
@@ -295,12 +440,15 @@ void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
 template <typename T>
 void Hierarchy<T>::compute_residual(int l) {  // src/multigrid.cpp:410-424
   Level& L = levels_[size_t(l)];
+  if (L.sharded) sync();
+  const ZLink<double> ul = L.sharded ? ulink(l) : ZLink<double>{};
   if (l == 0) {
     ProfScope p(s_, "l0_residual_f64", resid_l0_bytes(L.g, 8, sizeof(T), true));
-    launch_l0_apply<T, double, double>(L.g, coeff_.p, level_u(0), L.f.p, L.r.p, s_);
+    launch_l0_apply<T, double, double>(L.g, coeff_.p, level_u(0), L.f.p, L.r.p, s_, L.sharded ? coeff_l_ : ZLink<T>{},
+                                       ul);
   } else {
     ProfScope p(s_, l == 1 ? "l1_residual_f64" : "coarse_residual_f64", resid_coarse_bytes(L.g, 8, sizeof(T), true));
-    launch_stencil_apply<T, double>(L.g, L.st.p, L.u.p, L.f.p, L.r.p, s_);
+    launch_stencil_apply<T, double>(L.g, L.st.p, L.u.p, L.f.p, L.r.p, s_, ul);
   }
   ++launches_;
 }
@@ -324,22 +472,12 @@ double Hierarchy<T>::v_cycle(const SolverOptions& opts) {  // src/multigrid.cpp:
     if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].u.p, 0, sizeof(double) * 3 * levels_[size_t(l)].g.nv, s_));
     relax(l, opts.pre_sweeps);
     compute_residual(l);
-    {
-      ProfScope p(s_, "restrict", double(levels_[size_t(l)].g.nv) * 27.0);
-      launch_restrict<double>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].r.p,
-                              levels_[size_t(l + 1)].f.p, s_);
-    }
-    ++launches_;
+    restrict_to(l, levels_[size_t(l)].r.p, levels_[size_t(l + 1)].f.p);
   }
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].u.p, 0, sizeof(double) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_solve();
   for (int l = lmax - 1; l >= 0; --l) {
-    {
-      ProfScope p(s_, "prolong", double(levels_[size_t(l)].g.nv) * 51.0);
-      launch_prolong_add<double>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].u.p,
-                                 level_u(l), s_);
-    }
-    ++launches_;
+    prolong_from(l, levels_[size_t(l + 1)].u.p, level_u(l), levels_[size_t(l + 1)].ul);
     relax(l, opts.post_sweeps);
   }
   compute_residual(0);
@@ -361,6 +499,18 @@ void Hierarchy<T>::ensure_inner() {
     L.ef.alloc(n3);
     L.er.alloc(n3);
   }
+  IHOM_CUDA(cudaDeviceSynchronize());
+  if (slab_.on()) {  // collective, same order on every slab
+    for (size_t l = 0; l < levels_.size(); ++l) {
+      Level& L = levels_[l];
+      if (L.sharded) {
+        L.eul = link(L.eu.p);
+        L.erl = link(L.er.p);
+      } else if (int(l) == rep0_) {
+        L.efpeer = peer_table(slab_.fab->exchange(slab_.rank, L.ef.p));
+      }
+    }
+  }
   inner_ready_ = true;
 }
 
@@ -372,12 +522,14 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse) {
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;
         if (L.g.size[c] == 0) continue;
+        if (L.sharded) sync();
         if (l == 0) {
           ProfScope p(s_, "l0_gs_f32", gs_l0_bytes(L.g, c, 4, 4));
-          launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_);
+          launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_,
+                                                  L.sharded ? coeff_l_ : ZLink<float>{}, L.eul);
         } else {
           ProfScope p(s_, l == 1 ? "l1_gs_f32" : "coarse_gs_f32", gs_coarse_bytes(L.g, c, 4, 4));
-          launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_);
+          launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_, L.eul);
         }
         ++launches_;
       }
@@ -388,12 +540,14 @@ template <typename T>
 void Hierarchy<T>::residual_f32(int l) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
+    if (L.sharded) sync();
     if (l == 0) {
       ProfScope p(s_, "l0_residual_f32", resid_l0_bytes(L.g, 4, 4, true));
-      launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_);
+      launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_,
+                                           L.sharded ? coeff_l_ : ZLink<float>{}, L.eul);
     } else {
       ProfScope p(s_, l == 1 ? "l1_residual_f32" : "coarse_residual_f32", resid_coarse_bytes(L.g, 4, 4, true));
-      launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_);
+      launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_, L.eul);
     }
     ++launches_;
   }
@@ -414,14 +568,17 @@ double Hierarchy<T>::defect_residual() {
   if constexpr (std::is_same_v<T, float>) {
     if (!npart_.p) npart_.alloc(size_t(L0.g.nv / 32 + 1024));
     long long nb;
+    if (L0.sharded) sync();
     {
       ProfScope p(s_, "l0_residual_f64", double(L0.g.nv) * (48.0 + sizeof(T) + 12.0));
-      nb = launch_l0_residual_norm<float>(L0.g, coeff_.p, level_u(0), L0.f.p, L0.ef.p, npart_.p, s_);
+      nb = launch_l0_residual_norm<float>(L0.g, coeff_.p, level_u(0), L0.f.p, L0.ef.p, npart_.p, s_,
+                                          L0.sharded ? coeff_l_ : ZLink<float>{}, L0.sharded ? ulink(0) : ZLink<double>{});
     }
     {
       ProfScope p(s_, "reduce", double(nb) * 8.0);
       launch_sum(npart_.p, nb, ws_.partials, ws_.scalars + 4, s_);
     }
+    allreduce(ws_.scalars + 4, 1);
     launches_ += 3;
     IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
     IHOM_CUDA(cudaStreamSynchronize(s_));
@@ -445,20 +602,20 @@ void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
     if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
     relax_f32(l, opts.pre_sweeps);
     residual_f32(l);
-    {
-      ProfScope p(s_, "restrict", double(levels_[size_t(l)].g.nv) * 13.5);
-      launch_restrict<float>(levels_[size_t(l)].g, levels_[size_t(l + 1)].g, levels_[size_t(l)].er.p,
-                             levels_[size_t(l + 1)].ef.p, s_);
-    }
-    ++launches_;
+    restrict_to_f32(l);
   }
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_f32();
   for (int l = lmax - 1; l >= 0; --l) {
+    Level& F = levels_[size_t(l)];
+    Level& C = levels_[size_t(l + 1)];
+    if (F.sharded) sync();
     {
-      ProfScope p(s_, "prolong", double(levels_[size_t(l)].g.nv) * 25.5);
-      launch_prolong_add<float>(levels_[size_t(l + 1)].g, levels_[size_t(l)].g, levels_[size_t(l + 1)].eu.p,
-                                levels_[size_t(l)].eu.p, s_);
+      ProfScope p(s_, "prolong", double(F.g.nv) * 25.5);
+      if (!slab_.on() || C.sharded)
+        launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, C.sharded ? C.eul : ZLink<float>{});
+      else
+        launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, {}, slab_.rank * (F.g.n[2] / 2));
     }
     ++launches_;
     relax_f32(l, opts.post_sweeps, symmetric);
@@ -468,6 +625,7 @@ void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
 template <typename T>
 SolveStats Hierarchy<T>::solve_pcg(double* u, const SolverOptions& opts) {
   SolveStats st;
+  if (slab_.on()) throw std::invalid_argument("MG-PCG mode is not available on z-slabs (use vcycle or mixed_defect)");
   if constexpr (!std::is_same_v<T, float>) {
     throw std::invalid_argument("MG-PCG mode needs mixed precision (f32 inner preconditioner)");
   } else {
@@ -576,9 +734,11 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
 }
 
 template <typename T>
-SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts) {  // src/multigrid.cpp:474-501
+SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts, ZLink<double> ul) {  // src/multigrid.cpp:474-501
   if (!density_set_) throw StateError("set_density before solve");
+  if (slab_.on() && is_self(ul, u)) throw std::invalid_argument("z-slab solve needs the links of the bound field");
   u0_bound_ = u;
+  u0l_ = resolve(ul, u);
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
   SolveStats st;
@@ -664,8 +824,8 @@ void Hierarchy<T>::bench_op(const std::string& op, int reps) {
 // ============================================================== Homogenizer
 template <typename T>
 Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts,
-                            cudaStream_t s)
-    : hier_(n, mat, penal, s), opts_(opts), penal_(penal) {
+                            cudaStream_t s, Slab slab)
+    : hier_(n, mat, penal, s, slab), opts_(opts), penal_(penal) {
   const long long nv = hier_.geo(0).nv;
   rho_.alloc(size_t(nv));
   for (auto& u : u_) {
@@ -674,6 +834,7 @@ Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, c
   }
   seed_.alloc(36);
   IHOM_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < 6; ++i) ul_[size_t(i)] = hier_.link(u_[size_t(i)].p);  // collective on z-slabs
 }
 
 template <typename T>
@@ -688,14 +849,18 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   if (!density_set_) throw StateError("set_density before solve_cell_problems");
   const GridGeo& g = hier_.geo(0);
   const bool multi = comm_ && comm_->size() > 1;
+  const bool slabs = hier_.slab().on();
+  if (multi && slabs) throw std::invalid_argument("load-case split and z-slabs are exclusive");
   double per[18] = {};  // per load: cycles, rel_residual, converged
   for (int i = 0; i < 6; ++i) {
     if (multi && owner_[i] != comm_->rank()) continue;
+    hier_.sync();  // coefficients of the neighbouring slabs are current
     {
       ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
-      launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream());
+      launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream(),
+                            slabs ? hier_.coeff_link() : ZLink<T>{});
     }
-    const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_);
+    const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_, ul_[size_t(i)]);
     per[3 * i] = s.cycles;
     per[3 * i + 1] = s.rel_residual;
     per[3 * i + 2] = s.converged ? 1.0 : 0.0;
@@ -730,18 +895,24 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
 template <typename T>
 void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp:58-111
   const double* u[6];
-  for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
+  const double* uhi[6];
+  for (int i = 0; i < 6; ++i) {
+    u[i] = u_[size_t(i)].p;
+    uhi[i] = ul_[size_t(i)].hi ? ul_[size_t(i)].hi : u[i];
+  }
   Workspace& ws = hier_.workspace();
   const Material& m = hier_.material();
+  hier_.sync();  // the six fields of the slab above are final
   {
     ProfScope p(hier_.stream(), "tensor", double(hier_.geo(0).nv) * 152.0);
     launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
-                                    ws.partials, ws.scalars + 16, hier_.stream());
+                                    ws.partials, ws.scalars + 16, hier_.stream(), uhi);
   }
+  hier_.allreduce(ws.scalars + 16, 21);  // element sums over all slabs
   double c21[21];
   IHOM_CUDA(cudaMemcpyAsync(c21, ws.scalars + 16, sizeof(c21), cudaMemcpyDeviceToHost, hier_.stream()));
   IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
-  const double M = double(hier_.geo(0).nv);
+  const double M = double(hier_.global_nv(0));
   int q = 0;
   for (int i = 0; i < 6; ++i)
     for (int j = i; j < 6; ++j, ++q) {
@@ -757,12 +928,17 @@ void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  /
     for (int j = 0; j < 6; ++j) s[i * 6 + j] = 0.5 * (seed[i * 6 + j] + seed[j * 6 + i]);
   IHOM_CUDA(cudaMemcpyAsync(seed_.p, s, sizeof(s), cudaMemcpyHostToDevice, hier_.stream()));
   const double* u[6];
-  for (int i = 0; i < 6; ++i) u[i] = u_[size_t(i)].p;
+  const double* uhi[6];
+  for (int i = 0; i < 6; ++i) {
+    u[i] = u_[size_t(i)].p;
+    uhi[i] = ul_[size_t(i)].hi ? ul_[size_t(i)].hi : u[i];
+  }
   const Material& m = hier_.material();
+  hier_.sync();
   {
     ProfScope p(hier_.stream(), "sensitivity", double(hier_.geo(0).nv) * 160.0);
     launch_tensor_sensitivity<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
-                                      seed_.p, out, hier_.stream());
+                                      seed_.p, out, hier_.stream(), uhi, hier_.global_nv(0));
   }
   IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
 }

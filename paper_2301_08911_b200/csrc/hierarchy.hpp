@@ -27,6 +27,7 @@
 #include "comm.hpp"
 #include "common.cuh"
 #include "density.hpp"
+#include "fabric.hpp"
 #include "kernels.hpp"
 #include "tables.hpp"
 
@@ -89,13 +90,44 @@ struct DevBuf {
   }
 };
 
+// z-slab placement: this hierarchy holds global z planes
+// [rank t, (rank+1) t), t = n2 / nranks, of a grid whose other slabs are
+// reached through the fabric. nranks == 1: one periodic domain (no fabric).
+struct Slab {
+  Fabric* fab = nullptr;
+  int rank = 0;
+  int nranks = 1;
+  bool on() const { return fab != nullptr && nranks > 1; }
+};
+
+template <typename X>
+ZLink<X> neighbours(const std::vector<void*>& all, int rank) {
+  const int n = int(all.size());
+  return {static_cast<const X*>(all[size_t((rank + n - 1) % n)]), static_cast<const X*>(all[size_t((rank + 1) % n)])};
+}
+inline PeerTable peer_table(const std::vector<void*>& all) {
+  PeerTable t{};
+  for (size_t r = 0; r < all.size(); ++r) t.p[r] = all[r];
+  return t;
+}
+
 template <typename T>
 class Hierarchy {
  public:
   using value_type = T;
-  Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s);
+  // n = dims of the WHOLE grid; with a slab only planes [rank t, (rank+1) t) are stored
+  Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab = {});
   ~Hierarchy() {
+    quiesce();
     if (h_pinned_) cudaFreeHost(h_pinned_);
+  }
+  // z-slab teardown is collective: no slab frees buffers its neighbours may still read
+  void quiesce() noexcept {
+    try {
+      sync();
+      cudaStreamSynchronize(s_);
+    } catch (...) {
+    }
   }
   Hierarchy(const Hierarchy&) = delete;
   Hierarchy& operator=(const Hierarchy&) = delete;
@@ -112,10 +144,12 @@ class Hierarchy {
   void coarsest_solve();
   double v_cycle(const SolverOptions& opts);
   // Solve K u = f with l0.f already holding the load; u is the warm start /
-  // result buffer (bound as level-0 u for the duration of the call).
-  SolveStats solve_bound(double* u, const SolverOptions& opts);
+  // result buffer (bound as level-0 u for the duration of the call; ul = its
+  // z-slab links).
+  SolveStats solve_bound(double* u, const SolverOptions& opts, ZLink<double> ul = {});
 
   double* level_u(int l) { return l == 0 && u0_bound_ ? u0_bound_ : levels_[size_t(l)].u.p; }
+  ZLink<double> ulink(int l) const { return l == 0 && u0_bound_ ? u0l_ : levels_[size_t(l)].ul; }
   double* level_f(int l) { return levels_[size_t(l)].f.p; }
   double* level_r(int l) { return levels_[size_t(l)].r.p; }
   const T* stencil(int l) const { return levels_[size_t(l)].st.p; }
@@ -123,9 +157,22 @@ class Hierarchy {
   double op_scale() const { return op_scale_; }
   double negligible_load(long long ndof) const;
 
-  // Deterministic device reductions used by the solver.
+  // Deterministic device reductions used by the solver (over all slabs).
   void remove_translations(double* f, int l);
   double norm(const double* x, long long n);
+
+  // z-slab plumbing
+  const Slab& slab() const { return slab_; }
+  bool sharded(int l) const { return levels_[size_t(l)].sharded; }
+  long long global_nv(int l) const { return levels_[size_t(l)].nv_global; }
+  void sync();                                     // fabric barrier (no-op on one domain)
+  void allreduce(double* dev, int n, bool is_max = false);  // over slabs, rank-order fold
+  template <typename X>
+  ZLink<X> link(X* p) {                            // collective: this buffer on the slabs below / above
+    if (!slab_.on()) return {p, p};
+    return neighbours<X>(slab_.fab->exchange(slab_.rank, p), slab_.rank);
+  }
+  const ZLink<T>& coeff_link() const { return coeff_l_; }
 
   // Runs one kernel family `reps` times on the current level data (benchmark / ncu target).
   void bench_op(const std::string& op, int reps);
@@ -137,11 +184,27 @@ class Hierarchy {
 
  private:
   struct Level {
-    GridGeo g;
+    GridGeo g;                    // sharded: this slab's planes; replicated: the whole level
+    bool sharded = false;
+    long long nv_global = 0;
     DevBuf<double> u, f, r;
     DevBuf<T> st;                 // coarse stencil, blocked [nv/32][243][32] (st_index)
     DevBuf<float> eu, ef, er;     // f32 inner-cycle fields (kMixedDefect)
+    ZLink<double> ul, rl;         // z-slab links (sharded levels)
+    ZLink<float> eul, erl;
+    ZLink<T> stl;
+    PeerTable fpeer{}, efpeer{}, stpeer{};  // first replicated level: every slab's copy
   };
+  // the first replicated level L (slab mode): its planes owned by this slab
+  // are produced from the sharded level above, then gathered from the owners
+  int first_replicated() const { return rep0_; }
+  GridGeo transition_geo() const;  // this slab's share of level rep0_ (kernel iteration space)
+  int transition_zoff_h() const;   // its first halved plane in the replicated level
+  template <typename X>
+  void gather_owned(int l, X* dst, PeerTable peers, int per_vertex);
+  void restrict_to(int l, const double* r, double* f);   // level l -> l+1 (f64 fields)
+  void restrict_to_f32(int l);
+  void prolong_from(int l, const double* uc, double* u, ZLink<double> cl);
   void factor_coarsest();
   void check_error(const char* where);
   void ensure_inner();
@@ -157,6 +220,10 @@ class Hierarchy {
   double penal_;
   K0Matrix k0_;
   cudaStream_t s_;
+  Slab slab_;
+  int rep0_ = 1 << 30;      // first replicated level (slab mode)
+  ZLink<T> coeff_l_{};
+  ZLink<double> u0l_{};     // links of the bound level-0 u
   std::vector<Level> levels_;
   DevBuf<T> coeff_;
   DevBuf<double> Ainv_, A_, cwork_;
@@ -178,7 +245,11 @@ class Hierarchy {
 template <typename T>
 class Homogenizer {
  public:
-  Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts, cudaStream_t s);
+  Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts, cudaStream_t s,
+              Slab slab = {});
+  ~Homogenizer() { hier_.quiesce(); }
+  Homogenizer(const Homogenizer&) = delete;
+  Homogenizer& operator=(const Homogenizer&) = delete;
 
   void set_density(const double* rho_phys_dev);
   CellSolveStats solve_cell_problems();
@@ -202,6 +273,7 @@ class Homogenizer {
   double penal_;
   DevBuf<double> rho_;
   std::array<DevBuf<double>, 6> u_;
+  std::array<ZLink<double>, 6> ul_{};  // z-slab links of the six fields
   DevBuf<double> seed_;
   DevBuf<double> stats_;  // per-load (cycles, rel, converged) for the multi-GPU combine
   bool density_set_ = false;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "fabric.hpp"
 #include "tables.hpp"
 
 namespace ihomgpu {
@@ -80,9 +81,14 @@ void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, 
 // out[0] = dot(a, b) over n entries
 template <typename TN>
 void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s);
-// x[c*nv + i] -= sums[c] / nv
+// x[3 i + c] -= sums[c] / count (count = vertices of the whole grid; default nv)
 template <typename TN>
-void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s);
+void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count = 0);
+void launch_int_to_double(const int* in, double* out, cudaStream_t s);
+// z-slab: copy the planes of the replicated level g owned by the other slabs (planes per slab)
+template <typename X>
+void launch_gather_owned(const GridGeo& g, PeerTable peers, int planes, int me, int per_vertex, X* dst,
+                         cudaStream_t s);
 // u += e (f64 += TN)
 template <typename TN>
 void launch_axpy_update(double* u, const TN* e, long long n, cudaStream_t s);

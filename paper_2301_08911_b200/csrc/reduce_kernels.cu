@@ -89,17 +89,17 @@ void launch_dot(const TN* a, const TN* b, long long n, double* partials, double*
 }
 
 template <typename TN>
-__global__ void sub_means_kernel(TN* x, long long nv, const double* sums) {
+__global__ void sub_means_kernel(TN* x, long long nv, const double* sums, long long count) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nv) return;
-  const double inv = 1.0 / double(nv);
+  const double inv = 1.0 / double(count);
 #pragma unroll
   for (int c = 0; c < 3; ++c) x[3 * i + c] = TN(double(x[3 * i + c]) - sums[c] * inv);
 }
 
 template <typename TN>
-void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s) {
-  sub_means_kernel<TN><<<ceil_div(nv, 256), 256, 0, s>>>(x, nv, sums);
+void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count) {
+  sub_means_kernel<TN><<<ceil_div(nv, 256), 256, 0, s>>>(x, nv, sums, count > 0 ? count : nv);
   IHOM_LAUNCH_CHECK();
 }
 
@@ -214,8 +214,8 @@ template void launch_comp_sums<double>(const double*, long long, double*, double
 template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t);
 template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t);
 template void launch_dot<float>(const float*, const float*, long long, double*, double*, cudaStream_t);
-template void launch_sub_means<double>(double*, long long, const double*, cudaStream_t);
-template void launch_sub_means<float>(float*, long long, const double*, cudaStream_t);
+template void launch_sub_means<double>(double*, long long, const double*, cudaStream_t, long long);
+template void launch_sub_means<float>(float*, long long, const double*, cudaStream_t, long long);
 template void launch_axpy_update<float>(double*, const float*, long long, cudaStream_t);
 template void launch_axpy_update<double>(double*, const double*, long long, cudaStream_t);
 template void launch_convert<double, float>(const double*, float*, long long, cudaStream_t);
@@ -257,6 +257,43 @@ __global__ void grid_locs_kernel(GridGeo g, long long* __restrict__ out, long lo
 
 void launch_grid_locs(const GridGeo& g, long long* out, long long* out27, cudaStream_t s) {
   grid_locs_kernel<<<ceil_div(g.nv, 256), 256, 0, s>>>(g, out, out27);
+  IHOM_LAUNCH_CHECK();
+}
+
+// First replicated level of a z-slab hierarchy: every slab wrote the planes
+// z in [owner * planes, (owner+1) * planes) of its own copy; fetch the others'
+// planes from their owners (peer memory). per_vertex: 3 (AoS nodal) or 243
+// (blocked stencil rows).
+template <typename X>
+__global__ void gather_owned_kernel(GridGeo g, PeerTable peers, int planes, int me, int per_vertex, X* dst) {
+  const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= g.nv) return;
+  const int color = color_at(g, loc);
+  int x, y, z;
+  block_coords(g, color, (unsigned)(loc - g.base[color]), x, y, z);
+  const int owner = z / planes;
+  if (owner == me) return;
+  const X* src = static_cast<const X*>(peers.p[owner]);
+  if (per_vertex == 3) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dst[3 * loc + c] = src[3 * loc + c];
+  } else {
+    for (int k = 0; k < 243; ++k) dst[st_index(k, (unsigned)loc)] = src[st_index(k, (unsigned)loc)];
+  }
+}
+
+template <typename X>
+void launch_gather_owned(const GridGeo& g, PeerTable peers, int planes, int me, int per_vertex, X* dst,
+                         cudaStream_t s) {
+  gather_owned_kernel<X><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, peers, planes, me, per_vertex, dst);
+  IHOM_LAUNCH_CHECK();
+}
+template void launch_gather_owned<double>(const GridGeo&, PeerTable, int, int, int, double*, cudaStream_t);
+template void launch_gather_owned<float>(const GridGeo&, PeerTable, int, int, int, float*, cudaStream_t);
+
+__global__ void int_to_double_kernel(const int* in, double* out) { *out = double(*in); }
+void launch_int_to_double(const int* in, double* out, cudaStream_t s) {
+  int_to_double_kernel<<<1, 1, 0, s>>>(in, out);
   IHOM_LAUNCH_CHECK();
 }
 

@@ -1,0 +1,91 @@
+"""z-slab decomposition on one device.
+
+P slabs of one grid live in this process (Fabric.local), one host thread per
+slab; every cross-slab read goes through the same peer-pointer links the
+multi-GPU (IPC / NVLink) fabric uses. The per-vertex arithmetic of a slab is
+exactly the single-domain arithmetic, so the solve takes the same number of
+cycles and C^H / sensitivities agree with the one-domain run up to the order
+of the cross-slab sums.
+"""
+import numpy as np
+import pytest
+
+import paper_2301_08911_b200 as ih
+
+pytestmark = pytest.mark.gpu
+
+
+def _design(n, seed=0):
+    rho, _ = ih.init_trig(n, 2, seed, 0.3)
+    return ih.radial_filter(n, rho, 2.0, "spline4") ** 3
+
+
+def _seed():
+    s = np.zeros((6, 6))
+    s[:3, :3] = 1.0 / 9.0
+    s[3, 3] = s[4, 4] = s[5, 5] = 0.25
+    return s
+
+
+def _single(n, phys, precision, mode, tol):
+    hom = ih.Homogenizer(n, penal=1.0, precision=precision, opts=ih.SolverOptions(tol=tol, mode=mode))
+    hom.set_density(phys)
+    st = hom.solve_cell_problems()
+    C = hom.effective_tensor()
+    sens = hom.tensor_sensitivity(_seed())
+    hom.close()
+    return st, C, sens
+
+
+def _slabs(P, n, phys, precision, mode, tol):
+    fab = ih.Fabric.local(P)
+
+    def body(r):
+        hom = ih.Homogenizer(n, penal=1.0, precision=precision, opts=ih.SolverOptions(tol=tol, mode=mode),
+                             fabric=fab, rank=r)
+        m = n * n * hom.planes
+        hom.set_density(np.ascontiguousarray(phys[hom.z0 * n * n: hom.z0 * n * n + m]))
+        st = hom.solve_cell_problems()
+        C = hom.effective_tensor()
+        sens = hom.tensor_sensitivity(_seed())
+        hom.close()
+        return st, C, sens
+
+    out = ih.run_slabs(P, body)
+    fab.close()
+    return out
+
+
+@pytest.mark.parametrize("P,n,precision,mode", [
+    (2, 32, "double", "vcycle"),
+    (4, 32, "mixed", "vcycle"),
+    (4, 32, "mixed", "mixed_defect"),
+    (2, 64, "mixed", "mixed_defect"),
+    (8, 32, "mixed", "mixed_defect"),
+])
+def test_slabs_match_single_domain(P, n, precision, mode):
+    phys = _design(n)
+    st1, C1, s1 = _single(n, phys, precision, mode, 1e-2)
+    res = _slabs(P, n, phys, precision, mode, 1e-2)
+    for st, C, _ in res:
+        assert st["total_cycles"] == st1["total_cycles"]
+        assert st["converged"]
+        np.testing.assert_array_equal(C, res[0][1])  # every slab holds the same tensor (rank-order sums)
+        assert np.max(np.abs(C - C1)) <= 1e-9 * np.max(np.abs(C1))
+    sens = np.concatenate([r[2] for r in res])
+    assert np.max(np.abs(sens - s1)) <= 1e-9 * np.max(np.abs(s1))
+
+
+def test_slabs_tight_tolerance():
+    n, P = 32, 4
+    phys = _design(n, seed=3)
+    _, C1, _ = _single(n, phys, "double", "vcycle", 1e-9)
+    res = _slabs(P, n, phys, "double", "vcycle", 1e-9)
+    assert np.max(np.abs(res[0][1] - C1)) <= 1e-11 * np.max(np.abs(C1))
+
+
+def test_slab_geometry_rules():
+    fab = ih.Fabric.local(3)
+    with pytest.raises((ValueError, RuntimeError)):
+        ih.run_slabs(3, lambda r: ih.Homogenizer(32, fabric=fab, rank=r))  # 32 planes do not split in 3
+    fab.close()

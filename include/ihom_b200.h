@@ -208,6 +208,9 @@ int ihom_run_optimization(const ihom_run_config* cfg, const double* init_rho /* 
    1 = solver failed, 2 = converged, 3 = last iteration (no update in cases 1-3). */
 typedef struct ihom_opt ihom_opt;
 ihom_opt* ihom_opt_create(const ihom_run_config* cfg, const double* init_rho /* host, may be null */);
+/* z-slab `rank` of the run over fabric f: designs in / out are that slab's
+ * elements (global planes [rank t, (rank+1) t)); every call is collective. */
+ihom_opt* ihom_opt_create_slab(const ihom_run_config* cfg, const double* init_rho, ihom_fabric* f, int rank);
 void ihom_opt_destroy(ihom_opt* opt);
 int ihom_opt_step(ihom_opt* opt, const double* rho_in, double* rho_out, int where, ihom_iter_record* rec,
                   int* status);

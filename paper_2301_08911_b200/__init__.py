@@ -724,11 +724,16 @@ def hs_shear_bound(youngs, poisson, f):  # src/runner.cpp:175-179
 
 # ---------------------------------------------------------------- stepping optimiser + profiler
 class Optimizer:
-    """One optimisation iteration per step() (the loop body of src/runner.cpp:83-131)."""
+    """One optimisation iteration per step() (the loop body of src/runner.cpp:83-131).
+
+    With ``fabric`` this is z-slab ``rank`` of the run: designs in and out are the
+    slab's elements (x-fastest, planes [z0, z0 + planes)) and every call is
+    collective over the slabs (drive them from one thread each, see run_slabs).
+    """
 
     STATUS = {0: "updated", 1: "solver_failed", 2: "converged", 3: "last_iteration"}
 
-    def __init__(self, cfg: RunConfig, init_rho=None):
+    def __init__(self, cfg: RunConfig, init_rho=None, fabric: Optional[Fabric] = None, rank: int = 0):
         L = lib()
         L.ihom_opt_create.restype = C.c_void_p
         L.ihom_opt_create.argtypes = [C.POINTER(_RunConfig), _dp]
@@ -741,10 +746,20 @@ class Optimizer:
         L.ihom_opt_stream.argtypes = [C.c_void_p]
         L.ihom_opt_stream.restype = C.c_void_p
         self.cfg = cfg
-        self.m = cfg.reso ** 3
+        self.fabric = fabric
+        P = fabric.nranks if fabric is not None else 1
+        self.planes = cfg.reso // P
+        self.z0 = rank * self.planes
+        self.m = cfg.reso * cfg.reso * self.planes
         self._c = cfg._c()
         init = None if init_rho is None else np.ascontiguousarray(init_rho, dtype=np.float64).ravel()
-        self._p = L.ihom_opt_create(C.byref(self._c), init.ctypes.data_as(_dp) if init is not None else None)
+        iptr = init.ctypes.data_as(_dp) if init is not None else None
+        if fabric is None:
+            self._p = L.ihom_opt_create(C.byref(self._c), iptr)
+        else:
+            L.ihom_opt_create_slab.restype = C.c_void_p
+            L.ihom_opt_create_slab.argtypes = [C.POINTER(_RunConfig), _dp, C.c_void_p, C.c_int]
+            self._p = L.ihom_opt_create_slab(C.byref(self._c), iptr, C.c_void_p(fabric._p), int(rank))
         if not self._p:
             _raise_last()
 

@@ -8,6 +8,7 @@
 #include <iterator>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <type_traits>
@@ -701,7 +702,12 @@ template <typename T>
 struct Optimizer : OptBase {
   ihom_run_config cfg;
   int n[3];
-  long long m;
+  int nl[3];            // this slab's dims (n0, n1, t); == n on one domain
+  long long m;          // elements held here
+  long long m_total;    // elements of the whole grid
+  Slab slab;
+  std::map<const double*, ZLink<double>> zlinks;  // z-slab: design buffers on the slabs below / above
+  std::map<const double*, PeerTable> peers;       //         and on every slab
   cudaStream_t s = nullptr;
   std::unique_ptr<Homogenizer<T>> hom;
   DevBuf<double> rho, next, pre, phys, grad, tmp, gd;
@@ -709,35 +715,46 @@ struct Optimizer : OptBase {
   OCConfig oc;
   ConvergeChecker conv;
 
-  Optimizer(const ihom_run_config& c, const double* init_rho) : cfg(c) {
+  Optimizer(const ihom_run_config& c, const double* init_rho, Slab sl = {}) : cfg(c), slab(sl) {
     IHOM_CUDA(cudaSetDevice(cfg.device));
     if (cfg.reso < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
     if (!(cfg.vol > 0.0 && cfg.vol <= 1.0)) throw std::invalid_argument("volume fraction out of range");
     n[0] = n[1] = n[2] = cfg.reso;
-    m = (long long)cfg.reso * cfg.reso * cfg.reso;
+    m_total = (long long)cfg.reso * cfg.reso * cfg.reso;
+    nl[0] = n[0];
+    nl[1] = n[1];
+    nl[2] = slab.on() ? n[2] / slab.nranks : n[2];
+    m = (long long)nl[0] * nl[1] * nl[2];
     IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     SolverOptions so;
     so.tol = cfg.tol;
     so.max_cycles = cfg.max_cycles;
     so.mode = cfg.solver_mode;
     // homogenizer penal = 1: the SIMP power lives in DensityExpr (src/runner.cpp:59-62)
-    hom = std::make_unique<Homogenizer<T>>(n, Material{cfg.youngs, cfg.poisson}, 1.0, so, s);
+    hom = std::make_unique<Homogenizer<T>>(n, Material{cfg.youngs, cfg.poisson}, 1.0, so, s, slab);
     g_bound = this;
     for (DevBuf<double>* b : {&rho, &next, &pre, &phys, &grad, &tmp, &gd}) b->alloc(size_t(m));
+    IHOM_CUDA(cudaDeviceSynchronize());
+    if (slab.on())  // collective, same order on every slab
+      for (DevBuf<double>* b : {&rho, &next, &pre, &phys, &grad, &tmp, &gd}) {
+        const std::vector<void*> all = slab.fab->exchange(slab.rank, b->p);
+        zlinks[b->p] = neighbours<double>(all, slab.rank);
+        peers[b->p] = peer_table(all);
+      }
     Workspace& ws = hom->hierarchy().workspace();
     if (cfg.init == 0) {  // init_constant (src/density.cpp:261-265)
       std::vector<double> v(size_t(m), cfg.vol);
       IHOM_CUDA(cudaMemcpyAsync(rho.p, v.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
       IHOM_CUDA(cudaStreamSynchronize(s));
     } else if (cfg.init == 1) {
-      if (init_trig(n, cfg.basis_n, cfg.seed, cfg.vol, 15.0, rho.p, tmp.p, ws, s)) flags |= 4;
+      if (init_trig(n, cfg.basis_n, cfg.seed, cfg.vol, 15.0, rho.p, tmp.p, ws, s, slab)) flags |= 4;
     } else {
       if (!init_rho) throw std::invalid_argument("init from file requires init_rho");
       IHOM_CUDA(cudaMemcpyAsync(rho.p, init_rho, sizeof(double) * m, cudaMemcpyHostToDevice, s));
       clamp_field(rho.p, m, kRhoMin, 1.0, s);  // src/runner.cpp:38-42
     }
     if (cfg.sym != IHOM_SYM_NONE) {  // src/runner.cpp:66-69
-      symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+      sym(rho.p, tmp.p);
       clamp_field(rho.p, m, kRhoMin, 1.0, s);
     }
     IHOM_CUDA(cudaMemcpyAsync(next.p, rho.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
@@ -768,11 +785,19 @@ struct Optimizer : OptBase {
 
   double mean_of(const double* f) {
     Workspace& ws = hom->hierarchy().workspace();
-    field_sum(f, m, ws.partials, ws.scalar, s);
+    field_sum(f, m, ws.partials, ws.scalar, s, slab);
     double sum = 0.0;
     IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
     IHOM_CUDA(cudaStreamSynchronize(s));
-    return sum / double(m);
+    return sum / double(m_total);
+  }
+  ZLink<double> zl(const double* p) const {
+    auto it = zlinks.find(p);
+    return it == zlinks.end() ? ZLink<double>{} : it->second;
+  }
+  void sym(double* field, double* scratch) {
+    if (slab.on()) symmetrize_slab(n, slab, field, peers.at(field), scratch, peers.at(scratch), cfg.sym, s);
+    else symmetrize(n, field, cfg.sym, scratch, s);
   }
 
   int step(ihom_iter_record* out) override {
@@ -780,7 +805,8 @@ struct Optimizer : OptBase {
     const auto t0 = std::chrono::steady_clock::now();
     Workspace& ws = hom->hierarchy().workspace();
     // DensityExpr::eval (src/density.cpp:65-72)
-    radial_filter(n, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s);
+    slab.sync(s);  // neighbours' designs are current
+    radial_filter(nl, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s, zl(rho.p));
     pow_field(pre.p, cfg.penal, m, phys.p, s);
     hom->set_density(phys.p);
     const CellSolveStats st = hom->solve_cell_problems();
@@ -809,17 +835,20 @@ struct Optimizer : OptBase {
       objective.backward(1.0, rec.C, seed);
       hom->tensor_sensitivity(seed, grad.p);
       pow_backward(pre.p, grad.p, cfg.penal, m, tmp.p, s);  // DensityExpr::backward
-      radial_filter(n, tmp.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, gd.p, s);
+      slab.sync(s);
+      radial_filter(nl, tmp.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, gd.p, s, zl(tmp.p));
       if (cfg.filter_placement == 1 && cfg.filter_radius >= 1.0) {
-        sensitivity_filter(n, gd.p, rho.p, cfg.filter_radius, tmp.p, s);
+        slab.sync(s);
+        sensitivity_filter(nl, gd.p, rho.p, cfg.filter_radius, tmp.p, s, zl(gd.p), zl(rho.p));
+        slab.sync(s);
         IHOM_CUDA(cudaMemcpyAsync(gd.p, tmp.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
       }
-      if (cfg.sym != IHOM_SYM_NONE) symmetrize(n, gd.p, cfg.sym, tmp.p, s);
-      const OCResult res = oc_update(m, rho.p, gd.p, oc, next.p, ws, s);
+      if (cfg.sym != IHOM_SYM_NONE) sym(gd.p, tmp.p);
+      const OCResult res = oc_update(m, rho.p, gd.p, oc, next.p, ws, s, slab, m_total);
       if (!res.bisection_ok) flags |= 8;
       std::swap(rho.p, next.p);  // previous design now in next.p
       if (cfg.sym != IHOM_SYM_NONE) {
-        symmetrize(n, rho.p, cfg.sym, tmp.p, s);
+        sym(rho.p, tmp.p);
         clamp_field(rho.p, m, kRhoMin, 1.0, s);
       }
       rec.lambda = res.lambda;
@@ -873,6 +902,20 @@ int ihom_run_optimization(const ihom_run_config* cfg, const double* init_rho, ih
 struct ihom_opt {
   std::unique_ptr<OptBase> o;
 };
+
+ihom_opt* ihom_opt_create_slab(const ihom_run_config* cfg, const double* init_rho, ihom_fabric* f, int rank) {
+  ihom_opt* out = nullptr;
+  guarded([&] {
+    if (!cfg) throw std::invalid_argument("null config");
+    if (!f) throw std::invalid_argument("null fabric");
+    const Slab sl{f->f.get(), rank, f->f->size()};
+    auto h = std::make_unique<ihom_opt>();
+    if (cfg->precision == IHOM_ALL_DOUBLE) h->o = std::make_unique<Optimizer<double>>(*cfg, init_rho, sl);
+    else h->o = std::make_unique<Optimizer<float>>(*cfg, init_rho, sl);
+    out = h.release();
+  });
+  return out;
+}
 
 ihom_opt* ihom_opt_create(const ihom_run_config* cfg, const double* init_rho) {
   ihom_opt* out = nullptr;

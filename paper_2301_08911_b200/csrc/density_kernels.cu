@@ -10,6 +10,7 @@
 #include "profiler.hpp"
 
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 namespace ihomgpu {
@@ -71,8 +72,10 @@ __device__ __forceinline__ int wrapd(int c, int n) {
 }
 
 // mode 0: out = conv(f); mode 1: out = conv(rho*f) / (max(rho,rmin)*wsum)  (sensitivity filter)
+// z-slab: taps below / above the slab read the neighbours' planes (fl, rl).
 __global__ void filter_kernel(int nx, int ny, int nz, int ntaps, const double* __restrict__ f,
-                              const double* __restrict__ rho, double wsum, int mode, double* __restrict__ out) {
+                              const double* __restrict__ rho, double wsum, int mode, double* __restrict__ out,
+                              ZLink<double> fl, ZLink<double> rl) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long m = (long long)nx * ny * nz;
   if (i >= m) return;
@@ -81,9 +84,16 @@ __global__ void filter_kernel(int nx, int ny, int nz, int ntaps, const double* _
   const int y = int(r % ny), z = int(r / ny);
   double s = 0.0;
   for (int t = 0; t < ntaps; ++t) {
+    const int zz = z + c_tap_d[t][2];
     const long long k = wrapd(x + c_tap_d[t][0], nx) +
-                        (long long)nx * (wrapd(y + c_tap_d[t][1], ny) + (long long)ny * wrapd(z + c_tap_d[t][2], nz));
-    s += mode == 0 ? c_tap_w[t] * f[k] : c_tap_w[t] * rho[k] * f[k];
+                        (long long)nx * (wrapd(y + c_tap_d[t][1], ny) + (long long)ny * wrapd(zz, nz));
+    const double* fb = zz < 0 ? fl.lo : (zz >= nz ? fl.hi : f);
+    if (mode == 0) {
+      s += c_tap_w[t] * fb[k];
+    } else {
+      const double* rb = zz < 0 ? rl.lo : (zz >= nz ? rl.hi : rho);
+      s += c_tap_w[t] * rb[k] * fb[k];
+    }
   }
   out[i] = mode == 0 ? s : s / (fmax(rho[i], kRhoMin) * wsum);
 }
@@ -94,15 +104,17 @@ __global__ void filter_kernel(int nx, int ny, int nz, int ntaps, const double* _
 __constant__ double c_cube_w[7 * 7 * 7];
 template <int R>
 __global__ void __launch_bounds__(256) filter_cube_kernel(int nx, int ny, int nz, const double* __restrict__ f,
-                                                          double* __restrict__ out) {
+                                                          ZLink<double> fl, double* __restrict__ out) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, z = blockIdx.z;
   if (x >= nx) return;
   int X[2 * R + 1], Y[2 * R + 1], Z[2 * R + 1];
+  const double* zb[2 * R + 1];  // z-slab: planes beyond the slab come from its neighbours
 #pragma unroll
   for (int d = -R; d <= R; ++d) {
     X[d + R] = wrapd(x + d, nx);
     Y[d + R] = nx * wrapd(y + d, ny);
     Z[d + R] = nx * ny * wrapd(z + d, nz);
+    zb[d + R] = z + d < 0 ? fl.lo : (z + d >= nz ? fl.hi : f);
   }
   double s = 0.0;
 #pragma unroll
@@ -112,45 +124,54 @@ __global__ void __launch_bounds__(256) filter_cube_kernel(int nx, int ny, int nz
 #pragma unroll
       for (int dx = 0; dx <= 2 * R; ++dx) {
         const double w = c_cube_w[(dz * (2 * R + 1) + dy) * (2 * R + 1) + dx];
-        if (w != 0.0) s += w * __ldg(f + (size_t)(X[dx] + Y[dy] + Z[dz]));  // kernel_taps order: z, y, x
+        if (w != 0.0) s += w * __ldg(zb[dz] + (size_t)(X[dx] + Y[dy] + Z[dz]));  // kernel_taps order: z, y, x
       }
   out[x + (size_t)nx * (y + (size_t)ny * z)] = s;
 }
 
+static std::mutex g_const_mu;  // host staging of the constant-memory tap tables (z-slab threads)
+
 static bool filter_cube(const int n[3], const std::vector<Tap>& taps, double radius, const double* f, double* out,
-                        cudaStream_t s) {
+                        cudaStream_t s, ZLink<double> fl) {
   const int R = int(std::floor(radius));
   if (R < 1 || R > 3 || n[0] < 2 * R + 1 || n[1] < 2 * R + 1 || n[2] < 2 * R + 1) return false;
+  std::lock_guard<std::mutex> lock(g_const_mu);
   static double cube[7 * 7 * 7];
   const int W = 2 * R + 1;
   for (int i = 0; i < W * W * W; ++i) cube[i] = 0.0;
   for (const auto& t : taps) cube[((t.d[2] + R) * W + (t.d[1] + R)) * W + (t.d[0] + R)] = t.w;
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_cube_w, cube, sizeof(double) * W * W * W, 0, cudaMemcpyHostToDevice, s));
   const dim3 b(256), g(ceil_div(n[0], 256), n[1], n[2]);
-  if (R == 1) filter_cube_kernel<1><<<g, b, 0, s>>>(n[0], n[1], n[2], f, out);
-  else if (R == 2) filter_cube_kernel<2><<<g, b, 0, s>>>(n[0], n[1], n[2], f, out);
-  else filter_cube_kernel<3><<<g, b, 0, s>>>(n[0], n[1], n[2], f, out);
+  fl = resolve(fl, f);
+  if (R == 1) filter_cube_kernel<1><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
+  else if (R == 2) filter_cube_kernel<2><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
+  else filter_cube_kernel<3><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
   IHOM_LAUNCH_CHECK();
   IHOM_CUDA(cudaStreamSynchronize(s));  // cube staging buffer is static
   return true;
 }
 
-void radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, cudaStream_t s) {
+void radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, cudaStream_t s,
+                   ZLink<double> fl) {
   const long long m = (long long)n[0] * n[1] * n[2];
   if (radius < 1.0) {
     IHOM_CUDA(cudaMemcpyAsync(out, f, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     return;
   }
   const auto taps = make_taps(radius, kernel, true, nullptr);
+  if (!is_self(fl, f) && int(std::floor(radius)) > n[2]) throw std::invalid_argument("filter radius exceeds the z-slab");
   ProfScope p(s, "filter", double(m) * 16.0);
-  if (filter_cube(n, taps, radius, f, out, s)) return;
+  if (filter_cube(n, taps, radius, f, out, s, fl)) return;
+  std::lock_guard<std::mutex> lock(g_const_mu);
   upload_taps(taps, s);
-  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), f, nullptr, 1.0, 0, out);
+  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), f, nullptr, 1.0, 0, out,
+                                                 resolve(fl, f), ZLink<double>{f, f});
   IHOM_LAUNCH_CHECK();
+  IHOM_CUDA(cudaStreamSynchronize(s));
 }
 
 void sensitivity_filter(const int n[3], const double* sens, const double* rho, double radius, double* out,
-                        cudaStream_t s) {
+                        cudaStream_t s, ZLink<double> sl, ZLink<double> rl) {
   const long long m = (long long)n[0] * n[1] * n[2];
   if (radius < 1.0) {
     IHOM_CUDA(cudaMemcpyAsync(out, sens, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
@@ -158,10 +179,14 @@ void sensitivity_filter(const int n[3], const double* sens, const double* rho, d
   }
   double wsum = 0.0;
   const auto taps = make_taps(radius, 0, false, &wsum);
+  if (!is_self(sl, sens) && int(std::floor(radius)) > n[2]) throw std::invalid_argument("filter radius exceeds the z-slab");
+  std::lock_guard<std::mutex> lock(g_const_mu);
   upload_taps(taps, s);
   ProfScope p(s, "filter", double(m) * 24.0);
-  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), sens, rho, wsum, 1, out);
+  filter_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], (int)taps.size(), sens, rho, wsum, 1, out,
+                                                 resolve(sl, sens), resolve(rl, rho));
   IHOM_LAUNCH_CHECK();
+  IHOM_CUDA(cudaStreamSynchronize(s));
 }
 
 // out = x^p  /  out = g * p * x^(p-1)
@@ -344,6 +369,7 @@ void symmetrize(const int n[3], double* field, int sym, double* scratch, cudaStr
     }
     return;
   }
+  std::lock_guard<std::mutex> lock(g_const_mu);
   static int perm[kMaxOps][3], flip[kMaxOps][3];
   const int nops = symmetry_group(sym, perm, flip);
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
@@ -355,6 +381,111 @@ void symmetrize(const int n[3], double* field, int sym, double* scratch, cudaStr
   }
   IHOM_LAUNCH_CHECK();
   IHOM_CUDA(cudaStreamSynchronize(s));  // constant staging buffers are static
+}
+
+// ---- z-slab symmetrize: gather form over every slab's copy (peer memory).
+// Element e of this slab = global (x, y, z0 + zl); a global element (a, b, c)
+// lives on slab c / t at local plane c % t.
+__device__ __forceinline__ double slab_at(const PeerTable& in, int n0, int n1, int t, int a, int b, int c) {
+  const int owner = c / t;
+  return static_cast<const double*>(in.p[owner])[a + (long long)n0 * (b + (long long)n1 * (c - owner * t))];
+}
+
+// 8 axis flips, summed from the octant representative in flip_avg_kernel's
+// order -- bitwise the single-domain result.
+__global__ void flip_gather_kernel(int n0, int n1, int n2, int t, int z0, PeerTable in, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n0 * n1 * t) return;
+  const int x = int(i % n0);
+  const long long r = i / n0;
+  const int y = int(r % n1), z = z0 + int(r / n1);
+  const int rx = min(x, n0 - 1 - x), ry = min(y, n1 - 1 - y), rz = min(z, n2 - 1 - z);
+  const int xs[2] = {rx, n0 - 1 - rx}, ys[2] = {ry, n1 - 1 - ry}, zs[2] = {rz, n2 - 1 - rz};
+  double sum = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) sum += slab_at(in, n0, n1, t, xs[m & 1], ys[(m >> 1) & 1], zs[(m >> 2) & 1]);
+  out[i] = sum * 0.125;
+}
+
+// 6 axis permutations (cubic grid), summed from the sorted-coordinate
+// representative of the orbit: every orbit member gets the same bits.
+__global__ void perm_gather_kernel(int n, int t, int z0, PeerTable in, double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * n * t) return;
+  int e[3];
+  e[0] = int(i % n);
+  const long long r = i / n;
+  e[1] = int(r % n);
+  e[2] = z0 + int(r / n);
+  int a = e[0], b = e[1], c = e[2], tmp;  // sort ascending
+  if (a > b) { tmp = a; a = b; b = tmp; }
+  if (b > c) { tmp = b; b = c; c = tmp; }
+  if (a > b) { tmp = a; a = b; b = tmp; }
+  const int rep[3] = {a, b, c};
+  const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  double sum = 0.0;
+#pragma unroll
+  for (int p = 0; p < 6; ++p) sum += slab_at(in, n, n, t, rep[perm[p][0]], rep[perm[p][1]], rep[perm[p][2]]);
+  out[i] = sum * (1.0 / 6.0);
+}
+
+// generic group (rotate3, odd sizes): symmetrize_kernel's op order
+__global__ void sym_gather_kernel(int n0, int n1, int n2, int t, int z0, int nops, PeerTable in,
+                                  double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n0 * n1 * t) return;
+  const int n[3] = {n0, n1, n2};
+  int e[3];
+  e[0] = int(i % n0);
+  const long long r = i / n0;
+  e[1] = int(r % n1);
+  e[2] = z0 + int(r / n1);
+  double sum = 0.0;
+  for (int o = 0; o < nops; ++o) {
+    int q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      q[k] = e[c_sym_perm[o][k]];
+      if (c_sym_flip[o][k]) q[k] = n[k] - 1 - q[k];
+    }
+    sum += slab_at(in, n0, n1, t, q[0], q[1], q[2]);
+  }
+  out[i] = sum * (1.0 / double(nops));
+}
+
+void symmetrize_slab(const int n[3], const Slab& slab, double* field, PeerTable fpeers, double* scratch,
+                     PeerTable speers, int sym, cudaStream_t s) {
+  if (sym == 0) return;
+  if (sym != 1 && (n[0] != n[1] || n[1] != n[2]))
+    throw std::invalid_argument("reflect6/rotate3 symmetry requires a cubic grid");
+  const int t = n[2] / slab.nranks, z0 = slab.rank * t;
+  const long long m = (long long)n[0] * n[1] * t;
+  ProfScope p(s, "symmetrize", double(m) * 16.0 * (sym == 2 ? 2.0 : 1.0));
+  slab.sync(s);  // every slab's field is current
+  if (sym == 1 || sym == 2) {
+    flip_gather_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], t, z0, fpeers, scratch);
+    IHOM_LAUNCH_CHECK();
+    if (sym == 1) {
+      slab.sync(s);  // nobody overwrites its field while others still gather from it
+      IHOM_CUDA(cudaMemcpyAsync(field, scratch, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    } else {
+      slab.sync(s);
+      perm_gather_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], t, z0, speers, field);
+      IHOM_LAUNCH_CHECK();
+    }
+  } else {
+    std::lock_guard<std::mutex> lock(g_const_mu);
+    static int perm[kMaxOps][3], flip[kMaxOps][3];
+    const int nops = symmetry_group(sym, perm, flip);
+    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+    sym_gather_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], t, z0, nops, fpeers, scratch);
+    IHOM_LAUNCH_CHECK();
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    slab.sync(s);
+    IHOM_CUDA(cudaMemcpyAsync(field, scratch, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+  }
+  slab.sync(s);  // the symmetrized field is final on every slab
 }
 
 __global__ void clamp_kernel(double* f, long long m, double lo, double hi) {
@@ -416,13 +547,14 @@ __global__ void sum_kernel(const double* __restrict__ f, long long m, double* pa
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
-void field_sum(const double* f, long long m, double* partials, double* out, cudaStream_t s) {
+void field_sum(const double* f, long long m, double* partials, double* out, cudaStream_t s, const Slab& slab) {
   const int g = dgrid(m);
   ProfScope p(s, "reduce", double(m) * 8.0);
   sum_kernel<<<g, kDT, 0, s>>>(f, m, partials);
   IHOM_LAUNCH_CHECK();
   finalize_d<<<1, kDT, 0, s>>>(partials, g, false, out);
   IHOM_LAUNCH_CHECK();
+  slab.allreduce(out, 1, false, s);
 }
 
 // max(1e-30, -g) over the field plus a non-finite flag (src/oc.cpp:29-38)
@@ -469,8 +601,9 @@ __global__ void oc_trial_kernel(const double* __restrict__ rho, const double* __
 // fused pass (b0 normalisation, pow, step clamp, box clamp, block sums) with a
 // single 8-byte read-back.
 OCResult oc_update(long long m, const double* rho, const double* g, const OCConfig& cfg, double* out, Workspace& ws,
-                   cudaStream_t s) {
+                   cudaStream_t s, const Slab& slab, long long m_total) {
   const int grid = dgrid(m);
+  const double count = double(m_total > 0 ? m_total : m);
   IHOM_CUDA(cudaMemsetAsync(ws.flag, 0, sizeof(int), s));
   oc_scale_kernel<<<grid, kDT, 0, s>>>(g, m, ws.partials, ws.flag);
   IHOM_LAUNCH_CHECK();
@@ -478,9 +611,21 @@ OCResult oc_update(long long m, const double* rho, const double* g, const OCConf
   IHOM_LAUNCH_CHECK();
   int bad = 0;
   double scale = 0.0;
-  IHOM_CUDA(cudaMemcpyAsync(&bad, ws.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
-  IHOM_CUDA(cudaStreamSynchronize(s));
+  if (slab.on()) {  // max scale and the non-finite flag over all slabs
+    launch_int_to_double(ws.flag, ws.scalars + 62, s);
+    IHOM_CUDA(cudaMemcpyAsync(ws.scalars + 63, ws.scalar, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    slab.allreduce(ws.scalars + 62, 2, true, s);
+    IHOM_CUDA(cudaMemcpyAsync(ws.scalar, ws.scalars + 63, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double fl = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&fl, ws.scalars + 62, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    bad = fl != 0.0;
+  } else {
+    IHOM_CUDA(cudaMemcpyAsync(&bad, ws.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  }
   if (bad) throw std::invalid_argument("non-finite sensitivity");
   // keep the scale on device in ws.scalar (read by every trial)
   const OCParams p{cfg.damp, cfg.step_limit, cfg.min_density, 1.0};
@@ -490,10 +635,11 @@ OCResult oc_update(long long m, const double* rho, const double* g, const OCConf
     IHOM_LAUNCH_CHECK();
     finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);
     IHOM_LAUNCH_CHECK();
+    slab.allreduce(ws.scalar2, 1, false, s);
     double sum = 0.0;
     IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar2, sizeof(double), cudaMemcpyDeviceToHost, s));
     IHOM_CUDA(cudaStreamSynchronize(s));
-    return sum / double(m);
+    return sum / count;
   };
   OCResult res;
   const double lo0 = 1e-12, hi0 = 1e12;
@@ -541,16 +687,17 @@ constexpr int kMaxTrigW = 48 + 48 * 49 / 2;
 __constant__ double c_trig_w[kMaxTrigW];
 __constant__ double c_trig_rot[9];
 
-__global__ void trig_eval_kernel(int nx, int ny, int nz, int basis_n, double* __restrict__ y) {
+// z-slab: elements [0, nx ny t) of the slab starting at global plane z0
+__global__ void trig_eval_kernel(int nx, int ny, int nz, int planes, int z0, int basis_n, double* __restrict__ y) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long m = (long long)nx * ny * nz;
+  const long long m = (long long)nx * ny * planes;
   if (i >= m) return;
   const int n[3] = {nx, ny, nz};
   int e[3];
   e[0] = int(i % nx);
   const long long r = i / nx;
   e[1] = int(r % ny);
-  e[2] = int(r / ny);
+  e[2] = z0 + int(r / ny);
   double xb[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -613,10 +760,12 @@ static double uniform_pm1(std::uint64_t seed, std::uint64_t counter) {  // :162-
 }
 
 bool init_trig(const int n[3], int basis_n, std::uint64_t seed, double volume, double sigmoid_k, double* rho,
-               double* scratch, Workspace& ws, cudaStream_t s) {
+               double* scratch, Workspace& ws, cudaStream_t s, const Slab& slab) {
   if (basis_n < 1 || basis_n > 8) throw std::invalid_argument("trig basis order must be in [1, 8]");
   if (!(volume > kRhoMin && volume <= 1.0)) throw std::invalid_argument("volume fraction out of range");
-  const long long m = (long long)n[0] * n[1] * n[2];
+  const int t = n[2] / slab.nranks, z0 = slab.rank * t;
+  const long long m = (long long)n[0] * n[1] * t;
+  const double count = double((long long)n[0] * n[1] * n[2]);
   const int nt = 6 * basis_n;
   const int nq = nt + nt * (nt + 1) / 2;
   std::vector<double> w(static_cast<size_t>(nq));
@@ -637,11 +786,15 @@ bool init_trig(const int n[3], int basis_n, std::uint64_t seed, double volume, d
   const double rot[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
                          2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
                          2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
-  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_w, w.data(), sizeof(double) * nq, 0, cudaMemcpyHostToDevice, s));
-  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_rot, rot, sizeof(rot), 0, cudaMemcpyHostToDevice, s));
+  {
+    std::lock_guard<std::mutex> lock(g_const_mu);
+    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_w, w.data(), sizeof(double) * nq, 0, cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_trig_rot, rot, sizeof(rot), 0, cudaMemcpyHostToDevice, s));
+    trig_eval_kernel<<<ceil_div(m, 128), 128, 0, s>>>(n[0], n[1], n[2], t, z0, basis_n, scratch);
+    IHOM_LAUNCH_CHECK();
+    IHOM_CUDA(cudaStreamSynchronize(s));
+  }
   double* y = scratch;
-  trig_eval_kernel<<<ceil_div(m, 128), 128, 0, s>>>(n[0], n[1], n[2], basis_n, y);
-  IHOM_LAUNCH_CHECK();
   const int grid = dgrid(m);
   minmax_kernel<<<grid, kDT, 0, s>>>(y, m, ws.partials);
   IHOM_LAUNCH_CHECK();
@@ -654,16 +807,27 @@ bool init_trig(const int n[3], int basis_n, std::uint64_t seed, double volume, d
   IHOM_CUDA(cudaStreamSynchronize(s));
   double ylo = mins[0];
   for (double v : mins) ylo = std::min(ylo, v);
+  if (slab.on()) {  // global extremes: max over slabs of (yhi, -ylo)
+    const double ext[2] = {yhi, -ylo};
+    IHOM_CUDA(cudaMemcpyAsync(ws.scalars + 60, ext, sizeof(ext), cudaMemcpyHostToDevice, s));
+    slab.allreduce(ws.scalars + 60, 2, true, s);
+    double g2[2];
+    IHOM_CUDA(cudaMemcpyAsync(g2, ws.scalars + 60, sizeof(g2), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    yhi = g2[0];
+    ylo = -g2[1];
+  }
   const double vhat = std::min(1.5 * volume, 1.0 - kRhoMin);
   const double k = sigmoid_k;
   auto project = [&](double mu) {
     project_kernel<<<grid, kDT, 0, s>>>(y, m, vhat, k, mu, rho, ws.partials);
     IHOM_LAUNCH_CHECK();
     finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);
+    slab.allreduce(ws.scalar2, 1, false, s);
     double sum = 0.0;
     IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar2, sizeof(double), cudaMemcpyDeviceToHost, s));
     IHOM_CUDA(cudaStreamSynchronize(s));
-    return sum / double(m);
+    return sum / count;
   };
   auto constant = [&]() {
     std::vector<double> c(size_t(m), volume);

@@ -98,6 +98,22 @@ class IpcFabric : public Fabric {
   std::map<std::pair<int, std::uintptr_t>, void*> opened_;  // (rank, remote base) -> mapped base
 };
 
+// z-slab placement: this rank holds global z planes [rank t, (rank+1) t),
+// t = n2 / nranks, of a grid whose other slabs are reached through the
+// fabric. nranks == 1: one periodic domain (no fabric).
+struct Slab {
+  Fabric* fab = nullptr;
+  int rank = 0;
+  int nranks = 1;
+  bool on() const { return fab != nullptr && nranks > 1; }
+  void sync(cudaStream_t s) const {
+    if (on()) fab->barrier(rank, s);
+  }
+  void allreduce(double* x, int n, bool is_max, cudaStream_t s) const {
+    if (on()) fab->allreduce(rank, x, n, is_max, s);
+  }
+};
+
 // Kernels (fabric.cu)
 void launch_signal_wait(unsigned long long* own, PeerTable flags, int nranks, unsigned long long epoch, cudaStream_t s);
 void launch_mailbox_fold(PeerTable boxes, int nranks, int n, bool is_max, double* out, cudaStream_t s);

@@ -234,7 +234,7 @@ void Hierarchy<T>::restrict_to(int l, const double* r, double* f) {
   if (F.sharded) sync();
   {
     ProfScope p(s_, "restrict", double(F.g.nv) * 27.0);
-    if (!slab_.on() || C.sharded) {
+    if (!(F.sharded && !C.sharded)) {
       launch_restrict<double>(F.g, C.g, r, f, s_, F.sharded ? rl : ZLink<double>{});
     } else {
       const GridGeo gc = transition_geo();
@@ -252,7 +252,7 @@ void Hierarchy<T>::restrict_to_f32(int l) {
   if (F.sharded) sync();
   {
     ProfScope p(s_, "restrict", double(F.g.nv) * 13.5);
-    if (!slab_.on() || C.sharded) {
+    if (!(F.sharded && !C.sharded)) {
       launch_restrict<float>(F.g, C.g, F.er.p, C.ef.p, s_, F.sharded ? F.erl : ZLink<float>{});
     } else {
       const GridGeo gc = transition_geo();
@@ -270,7 +270,7 @@ void Hierarchy<T>::prolong_from(int l, const double* uc, double* u, ZLink<double
   if (F.sharded) sync();
   {
     ProfScope p(s_, "prolong", double(F.g.nv) * 51.0);
-    if (!slab_.on() || C.sharded) launch_prolong_add<double>(C.g, F.g, uc, u, s_, C.sharded ? cl : ZLink<double>{});
+    if (!(F.sharded && !C.sharded)) launch_prolong_add<double>(C.g, F.g, uc, u, s_, C.sharded ? cl : ZLink<double>{});
     else launch_prolong_add<double>(C.g, F.g, uc, u, s_, {}, slab_.rank * (F.g.n[2] / 2));
   }
   ++launches_;
@@ -612,7 +612,7 @@ void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
     if (F.sharded) sync();
     {
       ProfScope p(s_, "prolong", double(F.g.nv) * 25.5);
-      if (!slab_.on() || C.sharded)
+      if (!(F.sharded && !C.sharded))
         launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, C.sharded ? C.eul : ZLink<float>{});
       else
         launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, {}, slab_.rank * (F.g.n[2] / 2));

@@ -90,16 +90,6 @@ struct DevBuf {
   }
 };
 
-// z-slab placement: this hierarchy holds global z planes
-// [rank t, (rank+1) t), t = n2 / nranks, of a grid whose other slabs are
-// reached through the fabric. nranks == 1: one periodic domain (no fabric).
-struct Slab {
-  Fabric* fab = nullptr;
-  int rank = 0;
-  int nranks = 1;
-  bool on() const { return fab != nullptr && nranks > 1; }
-};
-
 template <typename X>
 ZLink<X> neighbours(const std::vector<void*>& all, int rank) {
   const int n = int(all.size());

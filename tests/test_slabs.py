@@ -89,3 +89,51 @@ def test_slab_geometry_rules():
     with pytest.raises((ValueError, RuntimeError)):
         ih.run_slabs(3, lambda r: ih.Homogenizer(32, fabric=fab, rank=r))  # 32 planes do not split in 3
     fab.close()
+
+
+def _run_single(cfg, iters):
+    opt = ih.Optimizer(cfg)
+    recs = []
+    for _ in range(iters):
+        st, rec = opt.step()
+        recs.append(rec)
+    d = opt.design()
+    opt.close()
+    return recs, d
+
+
+def _run_slabs(cfg, iters, P):
+    fab = ih.Fabric.local(P)
+
+    def body(r):
+        opt = ih.Optimizer(cfg, fabric=fab, rank=r)
+        recs = []
+        for _ in range(iters):
+            st, rec = opt.step()
+            recs.append(rec)
+        d = opt.design()
+        opt.close()
+        return recs, d
+
+    out = ih.run_slabs(P, body)
+    fab.close()
+    return out
+
+
+@pytest.mark.parametrize("P,obj,sym,precision,mode", [
+    (2, "bulk", "reflect6", "mixed", "mixed_defect"),
+    (4, "npr-relaxed", "reflect6", "mixed", "mixed_defect"),
+    (4, "shear", "reflect3", "double", "vcycle"),
+    (2, "bulk", "rotate3", "mixed", "vcycle"),
+])
+def test_slab_optimizer_matches_single_domain(P, obj, sym, precision, mode):
+    cfg = ih.RunConfig(reso=32, vol=0.3, obj=obj, sym=sym, max_iter=10, precision=precision, solver_mode=mode)
+    recs1, d1 = _run_single(cfg, 3)
+    res = _run_slabs(cfg, 3, P)
+    for recs, _ in res:
+        for a, b in zip(recs, recs1):
+            assert a["cycles"] == b["cycles"]
+            assert abs(a["objective"] - b["objective"]) <= 1e-9 * abs(b["objective"])
+            assert abs(a["volume"] - b["volume"]) <= 1e-12
+    d = np.concatenate([r[1] for r in res])
+    assert np.max(np.abs(d - d1)) <= 1e-9

@@ -51,6 +51,12 @@ def parse():
     ap.add_argument("--vol", type=float, default=0.2)
     ap.add_argument("--mode", default="mixed_defect", choices=["vcycle", "mixed_defect", "pcg"])
     ap.add_argument("--precision", default="mixed", choices=["mixed", "double"])
+    ap.add_argument("--multi", default="slab", choices=["slab", "loads"],
+                    help="N>1: z-slab decomposition over CUDA-IPC peer memory (default) or the 6 load cases "
+                         "split over ranks with NCCL broadcasts of the solved fields")
+    ap.add_argument("--same-device", action="store_true",
+                    help="testing only: every rank on cuda:0 (gloo plumbing) -- checks the multi-process slab "
+                         "path on a 1-GPU box; the timing is meaningless (ranks time-slice one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true",
@@ -166,8 +172,11 @@ def workload(args):
             "solver_mode": args.mode, "filter": "spline4 r=2", "symmetry": "reflect6", "init": "trig seed 0",
             "tol": 1e-2, "max_cycles": 50,
             "l2": "inputs larger than L2 (each 512^3 f64 field is 1 GiB vs 126 MB L2)",
-            "parallelism": (f"{args.gpus} GPUs: the 6 cell problems split across ranks, NCCL broadcast of the "
-                            "solved fields; C^H/sensitivity/OC replicated (z-slab decomposition: next round)")
+            "parallelism": (f"z-slab x{args.gpus}: {args.reso // args.gpus} z planes per GPU, halo reads and "
+                            "rank-order reductions over CUDA-IPC peer memory (NVLink), no host round trips"
+                            if args.multi == "slab" else
+                            f"{args.gpus} GPUs: the 6 cell problems split across ranks, NCCL broadcast of the "
+                            "solved fields; C^H/sensitivity/OC replicated")
             if args.gpus > 1 else "single GPU"}
 
 
@@ -178,17 +187,29 @@ def run_ours(args):
     import paper_2301_08911_b200 as ih
 
     rank, world, local = dist_info()
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = ih.RunConfig(reso=args.reso, vol=args.vol, obj=args.obj, max_iter=10 ** 6, precision=args.precision,
                        solver_mode=args.mode, device=local)
-    opt = ih.Optimizer(cfg)
-    if world > 1:
+    fab = None
+    m = args.reso ** 3
+    if world > 1 and args.multi == "slab":
+        from paper_2301_08911_b200 import distributed as dd
+        fab = dd.ipc_fabric(rank, world, device=local)
+        opt = ih.Optimizer(cfg, fabric=fab, rank=rank)
+        m = opt.m  # this rank's slab of the design
+    else:
+        opt = ih.Optimizer(cfg)
+    if world > 1 and args.multi == "loads":
         from paper_2301_08911_b200 import distributed as dd
         opt.set_comm(dd.share_unique_id(rank), rank, world, dd.load_owners(world))
-    m = args.reso ** 3
     dev_rho = torch.empty(m, dtype=torch.float64, device="cuda")
     host_rho = torch.empty(m, dtype=torch.float64).pin_memory()
     host_np = host_rho.numpy()
@@ -237,7 +258,7 @@ def run_ours(args):
     t_dev = statistics.mean(dev_ms) / 1e3
     t_e2e = statistics.mean(e2e_ms) / 1e3 if e2e_ms else None
     if world > 1:
-        t = torch.tensor([t_dev, t_e2e or 0.0], device="cuda", dtype=torch.float64)
+        t = torch.tensor([t_dev, t_e2e or 0.0], device="cpu" if args.same_device else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_dev, t_e2e = float(t[0]), (float(t[1]) if e2e_ms else None)
     if rank != 0:
@@ -268,8 +289,9 @@ def run_ours(args):
             "cycles_per_iteration": [r["cycles"] for r in recs],
             "objective": [r["objective"] for r in recs], "kernels": kernels}
     if t_e2e is not None:
-        line["e2e"] = {"value": round(t_e2e, 4), "unit": "s/iteration", "h2d_bytes_per_step": 8 * m,
-                       "d2h_bytes_per_step": 8 * m}
+        moved = 8 * (args.reso ** 3 if fab is not None else m)  # whole job: every rank moves its slab
+        line["e2e"] = {"value": round(t_e2e, 4), "unit": "s/iteration", "h2d_bytes_per_step": moved,
+                       "d2h_bytes_per_step": moved}
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         secs = cpu_oracle_iterations(args, threads, 3, 1)

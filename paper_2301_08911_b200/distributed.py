@@ -57,3 +57,33 @@ def share_unique_id(rank: int) -> bytes:
         t = t.cuda()
     dist.broadcast(t, 0)
     return bytes(t.cpu().numpy().astype(np.uint8).tobytes())
+
+
+# ---------------------------------------------------------------- z-slab fabric over processes
+def slab_planes(n: int, nranks: int, rank: int):
+    """(z0, planes) of z-slab ``rank`` of an n^3 grid (include/ihom_b200.h: t = n / nranks, a multiple
+    of 4 so every smoothed level keeps an even slab thickness)."""
+    if nranks < 1 or not 0 <= rank < nranks:
+        raise ValueError("bad rank / slab count")
+    t = n // nranks
+    if n % nranks or t % 4:
+        raise ValueError(f"{n} planes do not split into {nranks} slabs of a multiple of 4 planes")
+    return rank * t, t
+
+
+def torch_allgather(group=None):
+    """bytes -> [bytes of every rank] over torch.distributed (any backend): the host allgather an
+    IPC fabric exchanges its CUDA IPC handles with (plumbing only; no data-path traffic)."""
+    import torch.distributed as dist
+
+    def ag(blob: bytes):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, blob, group=group)
+        return out
+    return ag
+
+
+def ipc_fabric(rank: int, nranks: int, device: int = 0):
+    """One z-slab per process: peer buffers are mapped with CUDA IPC (NVLink between GPUs)."""
+    from . import Fabric
+    return Fabric.ipc(rank, nranks, torch_allgather(), device=device)

@@ -73,7 +73,10 @@ def test_slabs_match_single_domain(P, n, precision, mode):
         np.testing.assert_array_equal(C, res[0][1])  # every slab holds the same tensor (rank-order sums)
         assert np.max(np.abs(C - C1)) <= 1e-9 * np.max(np.abs(C1))
     sens = np.concatenate([r[2] for r in res])
-    assert np.max(np.abs(sens - s1)) <= 1e-9 * np.max(np.abs(s1))
+    # mixed: sensitivities read the f32 snapshot of u (src/homogenization.cpp:84-85); u differs from the
+    # one-domain u by the order of the cross-slab sums, which can flip an f32 rounding of an element's u
+    tol = 1e-9 if precision == "double" else 1e-6
+    assert np.max(np.abs(sens - s1)) <= tol * np.max(np.abs(s1))
 
 
 def test_slabs_tight_tolerance():

@@ -122,8 +122,10 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(family):
-    """dram bytes per launch of `family` from the committed ncu summary (profiles/), else None."""
+def ncu_traffic(family, reso):
+    """dram bytes per launch of `family` from the committed ncu summary (profiles/, captured at 512^3), else None."""
+    if reso != 512:
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(family)
@@ -273,7 +275,7 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                 "bytes_per_launch": ent["bytes"] / max(1, ent["launches"]),
                 "avg_launch_ms": ent["ms"] / max(1, ent["launches"]),
-                "traffic": ncu_traffic(fam)}
+                "traffic": ncu_traffic(fam, args.reso)}
     total_ms = sum(e["ms"] for e in prof.values()) or 1.0
     kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"], "share": round(v["ms"] / total_ms, 4),
                    "GB/s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] else None}

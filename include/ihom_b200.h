@@ -234,6 +234,11 @@ long long ihom_launch_count(void); /* kernels launched by this library since loa
    l0_gs_f64|f32, l0_residual_f64|f32, l1_gs_*, l1_residual_*, vcycle_f64|f32, set_density, tensor, sensitivity. */
 int ihom_bench_op(ihom_ctx* ctx, const char* op, int reps);
 int ihom_profile_get(int index, char* family, int cap, long long* launches, double* ms, double* bytes);
+/* Kernel-variant knobs (A/B switches; default = environment IHOM_<name>, else built-in):
+   L0_PAIR (paired FFMA2 level-0 f32 kernels, 1), PAIR_MINB (3|4), L0_GS2 (1), RES_MINB (3),
+   L0_KERNEL (0 fast | 1 smem-tiled). Every variant computes bit-identical results. */
+int ihom_set_knob(const char* name, int value);
+int ihom_get_knob(const char* name, int dflt);
 
 #ifdef __cplusplus
 }

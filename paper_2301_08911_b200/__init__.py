@@ -826,6 +826,15 @@ class Optimizer:
         return lib().ihom_opt_stream(C.c_void_p(self._p)) or 0
 
 
+def set_knob(name: str, value: int):
+    """Kernel-variant switch (include/ihom_b200.h ihom_set_knob); variants are bit-identical."""
+    _check(lib().ihom_set_knob(name.encode(), int(value)))
+
+
+def get_knob(name: str, default: int = 0) -> int:
+    return int(lib().ihom_get_knob(name.encode(), int(default)))
+
+
 def profile_enable(on: bool = True):
     _check(lib().ihom_profile_enable(1 if on else 0))
 

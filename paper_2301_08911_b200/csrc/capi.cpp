@@ -986,6 +986,14 @@ int ihom_opt_flags(ihom_opt* h) { return h->o->flags; }
 long long ihom_opt_launches(ihom_opt* h) { return h->o->launches(); }
 void* ihom_opt_stream(ihom_opt* h) { return (void*)h->o->stream(); }
 
+int ihom_set_knob(const char* name, int value) {
+  return guarded([&] {
+    if (!name) throw std::invalid_argument("knob name");
+    set_knob(name, value);
+  });
+}
+int ihom_get_knob(const char* name, int dflt) { return name ? knob(name, dflt) : dflt; }
+
 int ihom_profile_enable(int on) {
   return guarded([&] {
     Profiler::get().enable(on != 0);

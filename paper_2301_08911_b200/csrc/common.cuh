@@ -51,6 +51,13 @@ inline long long& launch_counter() {
     IHOM_CUDA(cudaGetLastError());    \
   } while (0)
 
+// Kernel-variant knobs (measurement / A-B switches, never numerics-changing unless
+// documented): the value is the environment variable IHOM_<NAME> when set, else
+// the default; ihom_set_knob() overrides it at run time (tests flip variants
+// in-process to prove bit-identity). Defined in knobs.cpp.
+int knob(const char* name, int dflt);
+void set_knob(const char* name, int value);
+
 // Geometry of one periodic grid level (inc/grid.hpp:18-56), passed by value.
 struct GridGeo {
   int n[3];

@@ -474,14 +474,19 @@ void symmetrize_slab(const int n[3], const Slab& slab, double* field, PeerTable 
       IHOM_LAUNCH_CHECK();
     }
   } else {
-    std::lock_guard<std::mutex> lock(g_const_mu);
-    static int perm[kMaxOps][3], flip[kMaxOps][3];
-    const int nops = symmetry_group(sym, perm, flip);
-    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
-    IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
-    sym_gather_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], t, z0, nops, fpeers, scratch);
-    IHOM_LAUNCH_CHECK();
-    IHOM_CUDA(cudaStreamSynchronize(s));
+    {
+      // the operator tables live in process-wide __constant__ memory shared by every slab thread of a
+      // local fabric: upload + gather under the lock, and release it BEFORE the slab barrier (a thread
+      // waiting at the barrier while holding it would stall the others on the lock: deadlock)
+      std::lock_guard<std::mutex> lock(g_const_mu);
+      static int perm[kMaxOps][3], flip[kMaxOps][3];
+      const int nops = symmetry_group(sym, perm, flip);
+      IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_perm, perm, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+      IHOM_CUDA(cudaMemcpyToSymbolAsync(c_sym_flip, flip, sizeof(int) * 3 * nops, 0, cudaMemcpyHostToDevice, s));
+      sym_gather_kernel<<<ceil_div(m, 256), 256, 0, s>>>(n[0], n[1], n[2], t, z0, nops, fpeers, scratch);
+      IHOM_LAUNCH_CHECK();
+      IHOM_CUDA(cudaStreamSynchronize(s));
+    }
     slab.sync(s);
     IHOM_CUDA(cudaMemcpyAsync(field, scratch, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
   }

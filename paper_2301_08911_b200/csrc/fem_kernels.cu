@@ -295,22 +295,10 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* 
   }
 }
 
-// Variant selection (IHOM_L0_KERNEL=tile|fast; default fast: measured faster on B200, see profiles/).
-static bool tile_enabled() {
-  static const int v = [] {
-    const char* e = std::getenv("IHOM_L0_KERNEL");
-    return (e && std::string(e) == "tile") ? 1 : 0;
-  }();
-  return v != 0;
-}
+// Variant selection (IHOM_L0_KERNEL=tile|0; default fast: measured faster on B200, see profiles/).
+static bool tile_enabled() { return knob("L0_KERNEL", 0) != 0; }
 // Two-vertex GS variant (IHOM_L0_GS2=0 disables; default on).
-static bool gs2_enabled() {
-  static const int v = [] {
-    const char* e = std::getenv("IHOM_L0_GS2");
-    return e ? std::atoi(e) : 1;
-  }();
-  return v != 0;
-}
+static bool gs2_enabled() { return knob("L0_GS2", 1) != 0; }
 
 static bool tile_ok(const GridGeo& g) {
   return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
@@ -419,6 +407,154 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
   }
 }
+
+// ---------------------------------------------------------------- paired f32 kernels (FFMA2)
+// One thread, two same-colour vertices stacked in halved z (h2, h2+1) -- the
+// fast2 pairing -- with the stencil evaluated ONCE in float2 lane-pair
+// arithmetic (vec2.cuh): lane x = the lower vertex, lane y = the upper one.
+// sm_100 issues FFMA2/FADD2/FMUL2 at the scalar instruction rate, so the
+// floating-point instruction count per vertex halves; every lane rounds like
+// the scalar kernel, so results are bit-identical to l0_gs_fast2_kernel /
+// l0_apply_fast_kernel<float, float, float>.
+struct PairPlanes {
+#if IHOM_PAIR_SHARE
+  float shared_pl[9][3];  // plane t2 = +1 of the lower vertex == plane t2 = -1 of the upper
+#endif
+  const float* pa0;  // lower vertex, plane t2 = -1
+  const float* pa2;  // lower vertex, plane t2 = +1 (== upper vertex, plane t2 = -1)
+  const float* pb2;  // upper vertex, plane t2 = +1
+};
+
+__device__ __forceinline__ void load_pair_planes(const FastAddr& fa, const FastAddr& fb, const float* __restrict__ u,
+                                                 const ZLink<float>& ul, PairPlanes& pp) {
+  const float* pa2 = zbase(fa, u, ul, 2);
+  pp.pa2 = pa2;
+#if IHOM_PAIR_SHARE
+#pragma unroll
+  for (int n = 0; n < 9; ++n) {
+    const float* p = pa2 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pp.shared_pl[n][c] = __ldg(p + c);
+  }
+#endif
+  pp.pa0 = zbase(fa, u, ul, 0);
+  pp.pb2 = zbase(fb, u, ul, 2);
+}
+
+#ifndef IHOM_PAIR_SHARE
+#define IHOM_PAIR_SHARE 0
+#endif
+#if IHOM_PAIR_SHARE
+#define PAIR_U(u)                                                                                                  \
+  [&](int n, int c) -> float2 {                                                                                    \
+    const float a_ = n >= 18 ? pp.shared_pl[n - 18][c]                                                             \
+                             : __ldg((n < 9 ? pp.pa0 : u) +                                                        \
+                                     3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c);    \
+    const float b_ = n < 9 ? pp.shared_pl[n][c]                                                                    \
+                           : __ldg((n < 18 ? u : pp.pb2) +                                                         \
+                                   3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c);      \
+    return make_float2(a_, b_);                                                                                    \
+  }
+#else
+// both lanes loaded straight into their register pair (the shared plane is re-read through L1 instead of
+// being held in 27 registers and copied into the other lane position)
+#define PAIR_U(u)                                                                                                  \
+  [&](int n, int c) -> float2 {                                                                                    \
+    const float a_ = __ldg((n < 9 ? pp.pa0 : (n < 18 ? u : pp.pa2)) +                                              \
+                           3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c);              \
+    const float b_ = __ldg((n < 9 ? pp.pa2 : (n < 18 ? u : pp.pb2)) +                                              \
+                           3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c);              \
+    return make_float2(a_, b_);                                                                                    \
+  }
+#endif
+
+template <typename TC>
+__device__ __forceinline__ void load_q_pair(const TC* __restrict__ coeff, const ZLink<TC>& cl, const FastAddr& fa,
+                                            const FastAddr& fb, float2 q[8]) {
+  float qa[8], qb[8];
+  load_q_fast(coeff, cl, fa, qa);
+  load_q_fast(coeff, cl, fb, qb);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) q[k] = make_float2(qa[k], qb[k]);
+}
+
+// GS colour pass; grid = (d0/bx, ceil(d1/by), d2/2)
+template <typename TC, int MINB, bool ZL = false>
+__global__ void __launch_bounds__(128, MINB) l0_gs_pair_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                               const float* __restrict__ f,
+                                                               const float* __restrict__ ur, ZLink<float> ul,
+                                                               float* uw, int color) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {ur, ur};
+  }
+  const int h2 = 2 * blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa, fb;
+  fast_addr(g, color, h0, h1, h2, fa);
+  fast_addr(g, color, h0, h1, h2 + 1, fb);
+  PairPlanes pp;
+  load_pair_planes(fa, fb, ur, ul, pp);
+  float2 q[8];
+  load_q_pair(coeff, cl, fa, fb, q);
+  float2 m[3], S[9];
+  ku_vertex_split<float2>(q, kappa<float>(), PAIR_U(ur), m, S);
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const FastAddr& fx = v == 0 ? fa : fb;
+    const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
+    float sblk[9], rhs[3], out[3];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) sblk[e] = v == 0 ? S[e].x : S[e].y;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - (v == 0 ? m[c].x : m[c].y);
+    solve3<float>(sblk, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
+  }
+}
+
+// y = K u, or y = f - K u (f != null); grid = (d0/bx, ceil(d1/by), 8 * d2/2), colour fastest
+template <typename TC, int MINB, bool ZL = false>
+__global__ void __launch_bounds__(128, MINB) l0_apply_pair_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                  ZLink<TC> cl, const float* __restrict__ u,
+                                                                  ZLink<float> ul, const float* __restrict__ f,
+                                                                  float* __restrict__ y) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
+  const int color = blockIdx.z & 7;
+  const int h2 = 2 * (blockIdx.z >> 3);
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  FastAddr fa, fb;
+  fast_addr(g, color, h0, h1, h2, fa);
+  fast_addr(g, color, h0, h1, h2 + 1, fb);
+  PairPlanes pp;
+  load_pair_planes(fa, fb, u, ul, pp);
+  float2 q[8];
+  load_q_pair(coeff, cl, fa, fb, q);
+  float2 acc[3];
+  ku_vertex<float2>(q, kappa<float>(), PAIR_U(u), acc);
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const FastAddr& fx = v == 0 ? fa : fb;
+    const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float a = v == 0 ? acc[c].x : acc[c].y;
+      y[3 * loc + c] = f ? f[3 * loc + c] - a : a;
+    }
+  }
+}
+
+// register budget of the paired kernels: 3 blocks/SM (168 regs, default) or 4 (128 regs): IHOM_PAIR_MINB
+static int pair_minb() { return knob("PAIR_MINB", 3); }
+
+// Paired variants on by default (IHOM_L0_PAIR=0 falls back to the scalar fast kernels).
+static bool pair_enabled() { return knob("L0_PAIR", 1) != 0; }
 
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
@@ -554,6 +690,16 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+    if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
+      if (g.cd[0][2] % 2 == 0 && pair_enabled()) {
+        const dim3 gr2(gr.x, gr.y, 8 * (g.cd[0][2] / 2));
+        if (linked) l0_apply_pair_kernel<TC, 3, true><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
+        else if (pair_minb() >= 4) l0_apply_pair_kernel<TC, 4><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
+        else l0_apply_pair_kernel<TC, 3><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
+        IHOM_LAUNCH_CHECK();
+        return;
+      }
+    }
     // f32 kernels capped at 64 registers (8 blocks/SM: more warps in flight, measured faster);
     // f64 kernels uncapped (a cap spills and was measured slower).
     if (linked) l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1, true><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
@@ -609,7 +755,13 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
     bool done = false;
     if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
-      if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
+      if (g.cd[0][2] % 2 == 0 && pair_enabled()) {
+        const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
+        if (linked) l0_gs_pair_kernel<TC, 3, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else if (pair_minb() >= 4) l0_gs_pair_kernel<TC, 4><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else l0_gs_pair_kernel<TC, 3><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        done = true;
+      } else if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
         if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else l0_gs_fast2_kernel<TC, TN, 5><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
@@ -665,10 +817,7 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-  static const int minb = [] {
-    const char* e = std::getenv("IHOM_RES_MINB");
-    return e ? std::atoi(e) : 3;
-  }();
+  const int minb = knob("RES_MINB", 3);
   if (linked) l0_residual_norm_fast_kernel<TC, 3, true><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
   else if (minb >= 4) l0_residual_norm_fast_kernel<TC, 4><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);
   else if (minb == 3) l0_residual_norm_fast_kernel<TC, 3><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, r32, partials);

@@ -794,6 +794,10 @@ void Hierarchy<T>::bench_op(const std::string& op, int reps) {
     else if (op == "l0_gs_f32") relax_f32(0, 1);
     else if (op == "l0_residual_f64") compute_residual(0);
     else if (op == "l0_residual_f32") residual_f32(0);
+    else if (op == "l0_defect_f64") {  // fused f64 defect residual + f32 rhs + norm (mixed_defect outer step)
+      ensure_inner();
+      defect_residual();
+    }
     else if (op == "l1_gs_f64" && lmax >= 1) relax(1, 1);
     else if (op == "l1_gs_f32" && lmax >= 1) relax_f32(1, 1);
     else if (op == "l1_residual_f64" && lmax >= 1) compute_residual(1);

@@ -107,9 +107,9 @@ def main():
         nlo, slo = build(flo)
         nhi, shi = build(fhi)
         name = f"F{len(code_forms)}"
-        a = nlo if slo > 0 else f"(-{nlo})"
+        a = nlo if slo > 0 else f"vneg({nlo})"
         op = "+" if shi > 0 else "-"
-        code_forms.append(f"  const TA {name} = {a} {op} {nhi};")
+        code_forms.append(f"  const TA {name} = {'vadd' if op == '+' else 'vsub'}({a}, {nhi});")
         forms[f] = name
         return name, 1
 
@@ -133,7 +133,10 @@ def main():
     out.append("// ku_gen.cuh -- GENERATED by tools/gen_stencil.py; do not edit.")
     out.append("// Level-0 vertex stencil in factored form (see the generator's docstring).")
     out.append(f"// {len(code_forms)} form adds, 243 F*u FMAs, {nclass} kappa classes.")
+    out.append("// TA is a scalar (float / double) or a lane pair (float2: sm_100 FFMA2/FADD2/FMUL2, two")
+    out.append("// vertices per thread); vadd/vsub/vneg/vfma/vmul/vbc/vzero are in vec2.cuh.")
     out.append("#pragma once")
+    out.append('#include "vec2.cuh"')
     out.append("namespace ihomgpu {")
     out.append(f"constexpr int kKappaClasses = {nclass};")
     out.append("// kappa_k = lam' * alpha_k + mu' * beta_k")
@@ -144,11 +147,11 @@ def main():
     for split in (False, True):
         fname = "ku_vertex_split" if split else "ku_vertex"
         out.append("")
-        out.append("// U(n, c): neighbour n (27-index, x fastest), component c, as TA.")
+        out.append("// U(n, c): neighbour n (27-index, x fastest), component c, as TA; kap: scalar kappa classes.")
         if split:
             out.append("// Off-diagonal part M (n != 13) into y; self block S (n == 13) into S[9].")
-        out.append("template <typename TA, typename LoadU>")
-        sig = f"__device__ __forceinline__ void {fname}(const TA q[8], const TA* __restrict__ kap, LoadU U, TA y[3]"
+        out.append("template <typename TA, typename TK, typename LoadU>")
+        sig = f"__device__ __forceinline__ void {fname}(const TA q[8], const TK* __restrict__ kap, LoadU U, TA y[3]"
         sig += ", TA S[9])" if split else ")"
         out.append(sig + " {")
         emitted = set()
@@ -158,15 +161,15 @@ def main():
             if not name.startswith("F") or name in emitted:
                 return
             line = code_forms[int(name[1:])]
-            for tok in line.split("=", 1)[1].replace("(", " ").replace(")", " ").replace("-", " ").replace(
-                    "+", " ").replace(";", " ").split():
+            for tok in line.split("=", 1)[1].replace("(", " ").replace(")", " ").replace(",", " ").replace(
+                    ";", " ").split():
                 if tok.startswith("F"):
                     emit_form(tok)
             out.append(line)
             emitted.add(name)
         for r in range(3):
             for k in range(nclass):
-                out.append(f"  TA a{r}_{k} = TA(0);")
+                out.append(f"  TA a{r}_{k} = vzero<TA>();")
         for n in range(27):
             if split and n == 13:
                 continue
@@ -181,13 +184,13 @@ def main():
                     name, fs = used[(n, r, c)]
                     k, cs = cls_of[(n, r, c)]
                     sgn = fs * cs
-                    src = name if sgn > 0 else f"(-{name})"
-                    out.append(f"    a{r}_{k} = fma({src}, u{c}, a{r}_{k});")
+                    src = name if sgn > 0 else f"vneg({name})"
+                    out.append(f"    a{r}_{k} = vfma({src}, u{c}, a{r}_{k});")
             out.append("  }")
         for r in range(3):
-            expr = f"kap[0] * a{r}_0"
+            expr = f"vmul(vbc<TA>(kap[0]), a{r}_0)"
             for k in range(1, nclass):
-                expr = f"fma(kap[{k}], a{r}_{k}, {expr})"
+                expr = f"vfma(vbc<TA>(kap[{k}]), a{r}_{k}, {expr})"
             out.append(f"  y[{r}] = {expr};")
         if split:
             for r in range(3):
@@ -198,7 +201,7 @@ def main():
                     name, fs = used[(13, r, c)]
                     k, cs = cls_of[(13, r, c)]
                     sgn = fs * cs
-                    out.append(f"  S[{3 * r + c}] = {'' if sgn > 0 else '-'}kap[{k}] * {name};")
+                    out.append(f"  S[{3 * r + c}] = vmul(vbc<TA>({'' if sgn > 0 else '-'}kap[{k}]), {name});")
         out.append("}")
     out.append("}  // namespace ihomgpu")
     path = os.path.join(ROOT, "paper_2301_08911_b200", "csrc", "ku_gen.cuh")

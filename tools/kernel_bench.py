@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2301_08911_b200 as ih  # noqa: E402
 
-ALL = "l0_gs_f32,l0_gs_f64,l0_residual_f64,l0_residual_f32,l1_gs_f32,l1_residual_f32,vcycle_f32,set_density,tensor,sensitivity"
+ALL = "l0_gs_f32,l0_gs_f64,l0_residual_f64,l0_defect_f64,l0_residual_f32,l1_gs_f32,l1_residual_f32,vcycle_f32,set_density,tensor,sensitivity"
 
 
 def main():

@@ -18,6 +18,27 @@ __global__ void k_ffma(float* out, float a, float b) {
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
 }
+// all-register FFMA (per-thread multiplier/addend) and the sm_100 paired FFMA2 (2 lanes of f32 per instruction)
+__global__ void k_ffma_reg(float* out, const float* in) {
+  const float a = in[threadIdx.x], b = in[threadIdx.x + 1];
+  float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0+4, x5=x0+5, x6=x0+6, x7=x0+7;
+  for (int i = 0; i < N_ITER; ++i) {
+    x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+    x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+__global__ void k_ffma2(float* out, const float* in) {
+  const float2 a = make_float2(in[threadIdx.x], in[threadIdx.x + 2]), b = make_float2(in[threadIdx.x + 1], in[threadIdx.x + 3]);
+  float2 x0 = make_float2(threadIdx.x, 1), x1 = make_float2(2, 3), x2 = make_float2(4, 5), x3 = make_float2(6, 7);
+  float2 x4 = make_float2(8, threadIdx.x), x5 = make_float2(9, 1), x6 = make_float2(10, 2), x7 = make_float2(11, 3);
+  for (int i = 0; i < N_ITER; ++i) {
+    x0 = __ffma2_rn(x0, a, b); x1 = __ffma2_rn(x1, a, b); x2 = __ffma2_rn(x2, a, b); x3 = __ffma2_rn(x3, a, b);
+    x4 = __ffma2_rn(x4, a, b); x5 = __ffma2_rn(x5, a, b); x6 = __ffma2_rn(x6, a, b); x7 = __ffma2_rn(x7, a, b);
+  }
+  const float2 s = __fadd2_rn(__fadd2_rn(__fadd2_rn(x0, x1), __fadd2_rn(x2, x3)), __fadd2_rn(__fadd2_rn(x4, x5), __fadd2_rn(x6, x7)));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s.x + s.y;
+}
 // f32 -> f64 conversions feeding DFMA (the mixed-precision stencil apply pattern)
 __global__ void k_f2d(double* out, float a) {
   float f0 = threadIdx.x * 1e-3f, f1 = f0 + 1, f2 = f0 + 2, f3 = f0 + 3, f4=f0+4,f5=f0+5,f6=f0+6,f7=f0+7;
@@ -53,6 +74,9 @@ int main() {
   };
   run("DFMA", [&] { k_dfma<<<blocks, threads>>>(d, 0.999, 1e-3); }, 8);
   run("FFMA", [&] { k_ffma<<<blocks, threads>>>(f, 0.999f, 1e-3f); }, 8);
+  float* in; cudaMalloc(&in, 4096 * 4); cudaMemset(in, 0, 4096 * 4);
+  run("FFMA all-register", [&] { k_ffma_reg<<<blocks, threads>>>(f, in); }, 8);
+  run("FFMA2 all-register (f32 lanes)", [&] { k_ffma2<<<blocks, threads>>>(f, in); }, 16);
   run("F2F.F64.F32 (+8 FADD +8 DADD)", [&] { k_f2d<<<blocks, threads>>>(d, 1e-3f); }, 8);
   run("F2F.F32.F64 (+8 DADD +8 FADD)", [&] { k_d2f<<<blocks, threads>>>(f, 1e-3); }, 8);
   printf("SMs %d\n", p.multiProcessorCount);

@@ -553,8 +553,8 @@ __global__ void __launch_bounds__(128, MINB) l0_apply_pair_kernel(GridGeo g, con
 // register budget of the paired kernels: 3 blocks/SM (168 regs, default) or 4 (128 regs): IHOM_PAIR_MINB
 static int pair_minb() { return knob("PAIR_MINB", 3); }
 
-// Paired variants on by default (IHOM_L0_PAIR=0 falls back to the scalar fast kernels).
-static bool pair_enabled() { return knob("L0_PAIR", 1) != 0; }
+// Paired variants: IHOM_L0_PAIR=1 (off by default: measured slower at 512^3, 0.84 vs 0.67 ms per GS pass -- 168 registers leave 12 warps per SM and the kernel is latency-bound; profiles/kernel_variants_r01.md).
+static bool pair_enabled() { return knob("L0_PAIR", 0) != 0; }
 
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,

@@ -333,6 +333,7 @@ int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u, int where) {
     ctx->with([&](auto& h) {
       DevIn in(u, size_t(3 * ctx->nv()), where, ctx->s);
       copy_nodal(in.p, h.displacement(load), ctx->nv(), ctx->s);
+      h.displacements_changed();
       IHOM_CUDA(cudaStreamSynchronize(ctx->s));
     });
   });

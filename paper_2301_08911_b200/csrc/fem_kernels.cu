@@ -681,7 +681,9 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
   if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
   cl = resolve(cl, coeff);
   ul = resolve(ul, u);
-  if (!linked && tile_ok(g)) {
+  if (sweep_ok(g)) {
+    launch_l0_apply_sweep<TC, TN, TA>(g, coeff, cl, u, ul, f, y, s);
+  } else if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
     const size_t sm = tile_smem<TN>();
     IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, false>,
@@ -806,6 +808,9 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
   cl = resolve(cl, coeff);
   ul = resolve(ul, u);
+  if constexpr (std::is_same_v<TC, float>) {
+    if (sweep_ok(g)) return launch_l0_defect_sweep(g, coeff, cl, u, ul, f, r32, partials, s);
+  }
   if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
     const size_t sm = tile_smem<double>();
@@ -880,3 +885,5 @@ INST_L0(float, float, float)     // mixed inner correction cycle
 #undef INST_L0
 
 }  // namespace ihomgpu
+
+#include "sweep_kernels.cuh"  // z-plane sweep variants (same TU: shares the kappa constants)

@@ -855,6 +855,7 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   const bool multi = comm_ && comm_->size() > 1;
   const bool slabs = hier_.slab().on();
   if (multi && slabs) throw std::invalid_argument("load-case split and z-slabs are exclusive");
+  ecache_valid_ = false;
   double per[18] = {};  // per load: cycles, rel_residual, converged
   for (int i = 0; i < 6; ++i) {
     if (multi && owner_[i] != comm_->rank()) continue;
@@ -907,11 +908,19 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
   Workspace& ws = hier_.workspace();
   const Material& m = hier_.material();
   hier_.sync();  // the six fields of the slab above are final
-  {
-    ProfScope p(hier_.stream(), "tensor", double(hier_.geo(0).nv) * 152.0);
-    launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
-                                    ws.partials, ws.scalars + 16, hier_.stream(), uhi);
+  const long long nv = hier_.geo(0).nv;
+  const size_t esz = std::is_same_v<T, float> ? sizeof(float) : sizeof(double);
+  void* ec = nullptr;
+  if (knob("ENERGY_CACHE", 1)) {
+    if (!ecache_.p) ecache_.alloc(size_t(21 * nv) * esz);
+    ec = ecache_.p;
   }
+  {
+    ProfScope p(hier_.stream(), "tensor", double(nv) * (152.0 + (ec ? 21.0 * double(esz) : 0.0)));
+    launch_effective_tensor<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
+                                    ws.partials, ws.scalars + 16, hier_.stream(), uhi, ec);
+  }
+  ecache_valid_ = ec != nullptr;
   hier_.allreduce(ws.scalars + 16, 21);  // element sums over all slabs
   double c21[21];
   IHOM_CUDA(cudaMemcpyAsync(c21, ws.scalars + 16, sizeof(c21), cudaMemcpyDeviceToHost, hier_.stream()));
@@ -939,7 +948,12 @@ void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  /
   }
   const Material& m = hier_.material();
   hier_.sync();
-  {
+  if (ecache_valid_) {  // energies of the current displacements from effective_tensor()
+    const long long nv = hier_.geo(0).nv;
+    const bool f32 = std::is_same_v<T, float>;
+    ProfScope p(hier_.stream(), "sensitivity", double(nv) * (21.0 * (f32 ? 4.0 : 8.0) + 16.0));
+    launch_sensitivity_cached(nv, ecache_.p, f32, rho_.p, penal_, seed_.p, out, hier_.stream(), hier_.global_nv(0));
+  } else {
     ProfScope p(hier_.stream(), "sensitivity", double(hier_.geo(0).nv) * 160.0);
     launch_tensor_sensitivity<double>(hier_.geo(0), u, rho_.p, penal_, std::is_same_v<T, float>, m.lambda(), m.mu(),
                                       seed_.p, out, hier_.stream(), uhi, hier_.global_nv(0));

@@ -247,6 +247,8 @@ class Homogenizer {
   void tensor_sensitivity(const double seed[36], double* out_dev);
 
   double* displacement(int i) { return u_[size_t(i)].p; }
+  // callers that write displacement(i) directly must drop the cached element energies
+  void displacements_changed() { ecache_valid_ = false; }
   // Multi-GPU: load case i is solved by rank owner[i], then broadcast to all ranks.
   void set_comm(Comm* c, const int owner[6]) {
     comm_ = c;
@@ -267,6 +269,9 @@ class Homogenizer {
   DevBuf<double> seed_;
   DevBuf<double> stats_;  // per-load (cycles, rel, converged) for the multi-GPU combine
   bool density_set_ = false;
+  // per-element energies of the last effective_tensor() (knob ENERGY_CACHE, default on): [21][nv]
+  DevBuf<unsigned char> ecache_;
+  bool ecache_valid_ = false;
   Comm* comm_ = nullptr;
   int owner_[6] = {0, 0, 0, 0, 0, 0};
 };

@@ -140,7 +140,8 @@ struct U6 {
 
 template <typename TN, typename TE>
 __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
-                                                     bool snap, double lam, double mu, double* partials) {
+                                                     bool snap, double lam, double mu, double* partials,
+                                                     TE* __restrict__ ecache) {
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   TE* gsm = reinterpret_cast<TE*>(gsm_raw);
   __shared__ double sh[32];
@@ -160,6 +161,10 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
     const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
     TE E[21];
     element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
+    if (ecache) {  // [21][nv]: the sensitivity pass reuses these instead of recomputing them
+#pragma unroll
+      for (int k = 0; k < 21; ++k) ecache[k * g.nv + e] = E[k];
+    }
     const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
     for (int k = 0; k < 21; ++k) acc[k] += q * double(E[k]);
@@ -190,7 +195,7 @@ static void set_smem(const void* fn, bool f32) {
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
                              double lam, double mu, double* partials, double* c21, cudaStream_t s,
-                             const TN* const* uhi) {
+                             const TN* const* uhi, void* ecache) {
   long long blocks = (g.nv + kHT - 1) / kHT;
   if (blocks > kReducePartials) blocks = kReducePartials;
   U6 uu;
@@ -200,11 +205,12 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
   }
   if (snap) {
     set_smem((const void*)tensor_kernel<TN, float>, true);
-    tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials);
+    tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials,
+                                                                             static_cast<float*>(ecache));
   } else {
     set_smem((const void*)tensor_kernel<TN, double>, false);
     tensor_kernel<TN, double><<<(unsigned)blocks, kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                               partials);
+                                                                               partials, static_cast<double*>(ecache));
   }
   IHOM_LAUNCH_CHECK();
   tensor_finalize<<<1, 256, 0, s>>>(partials, (int)blocks, c21);
@@ -240,6 +246,33 @@ __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const doubl
   out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;  // :141 (1/M over the whole grid)
 }
 
+// Sensitivity from the energies the tensor pass cached: identical arithmetic on identical E values.
+template <typename TE>
+__global__ void sens_cached_kernel(long long nv, const TE* __restrict__ ecache, const double* __restrict__ rho,
+                                   double penal, const double* __restrict__ seed, double inv_m, double* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nv) return;
+  double acc = 0.0;
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * double(ecache[q * nv + e]);
+  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;
+}
+
+void launch_sensitivity_cached(long long nv, const void* ecache, bool f32, const double* rho, double penal,
+                               const double* sym_seed36, double* out, cudaStream_t s, long long m_total) {
+  const double inv_m = 1.0 / double(m_total > 0 ? m_total : nv);
+  if (f32)
+    sens_cached_kernel<float><<<ceil_div(nv, 256), 256, 0, s>>>(nv, static_cast<const float*>(ecache), rho, penal,
+                                                                 sym_seed36, inv_m, out);
+  else
+    sens_cached_kernel<double><<<ceil_div(nv, 256), 256, 0, s>>>(nv, static_cast<const double*>(ecache), rho, penal,
+                                                                  sym_seed36, inv_m, out);
+  IHOM_LAUNCH_CHECK();
+}
+
 template <typename TN>
 void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap,
                                double lam, double mu, const double* sym_seed36, double* out, cudaStream_t s,
@@ -263,7 +296,8 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
 }
 
 template void launch_effective_tensor<double>(const GridGeo&, const double* const[6], const double*, double, bool,
-                                              double, double, double*, double*, cudaStream_t, const double* const*);
+                                              double, double, double*, double*, cudaStream_t, const double* const*,
+                                              void*);
 template void launch_tensor_sensitivity<double>(const GridGeo&, const double* const[6], const double*, double, bool,
                                                 double, double, const double*, double*, cudaStream_t,
                                                 const double* const*, long long);

@@ -33,6 +33,13 @@ template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
                         ZLink<TC> cl = {}, ZLink<TN> ul = {});
 
+// z-plane sweep variants (sweep_kernels.cuh): shared-memory plane ring, bit-identical outputs
+bool sweep_ok(const GridGeo& g);
+template <typename TC, typename TN, typename TA>
+void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul, const TN* f,
+                           TN* y, cudaStream_t s);
+long long launch_l0_defect_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
+                                 ZLink<double> ul, const double* f, float* r32, double* partials, cudaStream_t s);
 // Fused defect residual: r32 = float(f - K u) (f64 arithmetic), per-block |r|^2 partials; returns #partials.
 template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
@@ -111,7 +118,11 @@ void copy_nodal(const double* in, double* out, long long nv, cudaStream_t s);
 template <typename TN>
 void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const double* rho, double penal, bool snap_f32,
                              double lambda, double mu, double* partials, double* c21, cudaStream_t s,
-                             const TN* const* uhi = nullptr);
+                             const TN* const* uhi = nullptr, void* ecache = nullptr);
+// ecache: optional [21][nv] per-element energies written by the tensor pass (TE = f32 when snap_f32, else f64);
+// the sensitivity then reads them instead of recomputing (bit-identical).
+void launch_sensitivity_cached(long long nv, const void* ecache, bool f32, const double* rho, double penal,
+                               const double* sym_seed36, double* out, cudaStream_t s, long long m_total);
 // z-slab: uhi = the six fields of the slab above; m_total = elements of the whole grid (the 1/M factor)
 template <typename TN>
 void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const double* rho, double penal,

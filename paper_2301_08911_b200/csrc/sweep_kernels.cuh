@@ -1,0 +1,212 @@
+// sweep_kernels.cu -- level-0 K.u / residual as a z-plane sweep through shared memory.
+//
+// Same per-vertex arithmetic as l0_apply_fast_kernel / l0_residual_norm_fast_kernel
+// (the generated factored stencil ku_vertex, identical operand order), so every
+// output value is bit-identical; what changes is how the 27 neighbours arrive.
+//
+// The fast kernels read each neighbour straight from HBM/L2 in the colour-block
+// AoS layout: three component loads per neighbour at a 12/24-byte lane stride,
+// i.e. every L1 sector of a neighbour run is looked up three times, plus a
+// 64-bit address per neighbour. ncu (profiles/ncu_r01_l0_stalls.md): the f64
+// residual sits at 69% L1 throughput with only 36% issue active -- it is bound
+// by L1 wavefronts, not DFMA.
+//
+// Here a CTA owns a TX x TY column of vertices (actual coordinates, all 8
+// colours) over TZ planes and marches up z. A 4-slot ring of shared-memory
+// planes holds the (TX+2) x (TY+2) window of u (AoS, like global) for planes
+// z-1, z, z+1 while plane z+2 streams in with cp.async; a 3-slot ring holds the
+// (TX+1) x (TY+1) element windows of rho^p. Every neighbour is then an LDS at a
+// compile-time offset from one of three plane bases (AoS strides of 12 / 24
+// bytes are bank-conflict free for 32 consecutive lanes), and the only global
+// address arithmetic is the colour-block location of each window vertex,
+// computed once per plane. Periodic wrap and z-slab links are resolved while
+// loading a plane (the source pointer of plane -1 / t is the slab below /
+// above), so the compute loop has no boundary cases at all.
+//
+// Included by fem_kernels.cu (shares its __constant__ kappa tables; no -rdc).
+#pragma once
+#include <cuda_pipeline.h>
+
+namespace ihomgpu {
+
+constexpr int kSwTX = 32, kSwTY = 8;                  // vertices per plane per CTA (one per thread)
+constexpr int kSwWX = kSwTX + 2, kSwWY = kSwTY + 2;   // u window
+constexpr int kSwEX = kSwTX + 1, kSwEY = kSwTY + 1;   // element window
+constexpr int kSwUSlot = kSwWX * kSwWY * 3;           // TN values per u plane slot
+constexpr int kSwESlot = kSwEX * kSwEY;               // TC values per element plane slot
+
+enum SweepOut { kSwApply = 0, kSwResidual = 1, kSwDefect = 2 };
+
+template <typename TN, typename TC>
+constexpr size_t sweep_smem() {
+  return sizeof(TN) * 4 * kSwUSlot + sizeof(TC) * 3 * kSwESlot;
+}
+
+__device__ __forceinline__ int wrapc(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }
+
+// async copy of u plane zl (local index, -1 .. t) of the window into slot buffer dst
+template <typename TN>
+__device__ __forceinline__ void sweep_load_u(const GridGeo& g, const TN* __restrict__ u, const ZLink<TN>& ul, int X0,
+                                             int Y0, int zl, TN* dst) {
+  const int t = g.n[2];
+  const TN* src = zl < 0 ? ul.lo : (zl >= t ? ul.hi : u);
+  const int z = zl < 0 ? zl + t : (zl >= t ? zl - t : zl);
+  const int tid = threadIdx.y * kSwTX + threadIdx.x;
+  for (int v = tid; v < kSwWX * kSwWY; v += kSwTX * kSwTY) {
+    const int i = v % kSwWX, j = v / kSwWX;
+    const int x = wrapc(X0 - 1 + i, g.n[0]), y = wrapc(Y0 - 1 + j, g.n[1]);
+    const size_t loc = vloc(g, x, y, z);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) __pipeline_memcpy_async(dst + 3 * v + c, src + 3 * loc + c, sizeof(TN));
+  }
+}
+
+// async copy of element plane ezl (local, -1 .. t-1) of the window
+template <typename TC>
+__device__ __forceinline__ void sweep_load_e(const GridGeo& g, const TC* __restrict__ coeff, const ZLink<TC>& cl,
+                                             int X0, int Y0, int ezl, TC* dst) {
+  const int t = g.n[2];
+  const TC* src = ezl < 0 ? cl.lo : coeff;
+  const int ez = ezl < 0 ? ezl + t : ezl;
+  const int tid = threadIdx.y * kSwTX + threadIdx.x;
+  for (int v = tid; v < kSwEX * kSwEY; v += kSwTX * kSwTY) {
+    const int i = v % kSwEX, j = v / kSwEX;
+    const int x = wrapc(X0 - 1 + i, g.n[0]), y = wrapc(Y0 - 1 + j, g.n[1]);
+    const size_t e = (size_t)x + (size_t)g.n[0] * ((size_t)y + (size_t)g.n[1] * ez);
+    __pipeline_memcpy_async(dst + v, src + e, sizeof(TC));
+  }
+}
+
+// grid = (n0 / TX, n1 / TY, t / TZ); block = (TX, TY)
+template <typename TC, typename TN, typename TA, int OUT, int MINB>
+__global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
+    l0_sweep_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl, const TN* __restrict__ u, ZLink<TN> ul,
+                    const TN* __restrict__ f, TN* __restrict__ y, float* __restrict__ r32, double* partials, int TZ) {
+  extern __shared__ __align__(16) unsigned char sw_raw[];
+  TN* us = reinterpret_cast<TN*>(sw_raw);
+  TC* es = reinterpret_cast<TC*>(sw_raw + sizeof(TN) * 4 * kSwUSlot);
+  __shared__ double red[kSwTX * kSwTY / 32];
+  const int X0 = blockIdx.x * kSwTX, Y0 = blockIdx.y * kSwTY, Z0 = blockIdx.z * TZ;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int xg = X0 + tx, yg = Y0 + ty;
+  // prologue: u planes Z0-1, Z0, Z0+1 -> slots 3, 0, 1 (slot of plane z = (z - Z0) & 3); elements Z0-1, Z0
+  sweep_load_u(g, u, ul, X0, Y0, Z0 - 1, us + 3 * kSwUSlot);
+  sweep_load_u(g, u, ul, X0, Y0, Z0, us);
+  sweep_load_u(g, u, ul, X0, Y0, Z0 + 1, us + kSwUSlot);
+  sweep_load_e(g, coeff, cl, X0, Y0, Z0 - 1, es + 2 * kSwESlot);  // element slot of plane ez = (ez - Z0) mod 3
+  sweep_load_e(g, coeff, cl, X0, Y0, Z0, es);
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  double ss = 0.0;
+  const int ubase = 3 * ((ty + 1) * kSwWX + tx + 1);
+  for (int k = 0; k < TZ; ++k) {
+    const int z = Z0 + k;
+    if (k + 2 <= TZ) {  // plane z+2 (needed by the vertex plane z+1) and element plane z+1
+      sweep_load_u(g, u, ul, X0, Y0, z + 2, us + ((k + 2) & 3) * kSwUSlot);
+      if (k + 1 < TZ) sweep_load_e(g, coeff, cl, X0, Y0, z + 1, es + ((k + 1) % 3) * kSwESlot);
+    }
+    __pipeline_commit();
+    const TN* p0 = us + ((k + 3) & 3) * kSwUSlot + ubase;  // plane z-1
+    const TN* p1 = us + (k & 3) * kSwUSlot + ubase;        // plane z
+    const TN* p2 = us + ((k + 1) & 3) * kSwUSlot + ubase;  // plane z+1
+    const TC* e0 = es + ((k + 2) % 3) * kSwESlot + ty * kSwEX + tx;  // element plane z-1, element (x-1, y-1)
+    const TC* e1 = es + (k % 3) * kSwESlot + ty * kSwEX + tx;        // element plane z
+    TA q[8];
+#pragma unroll
+    for (int ke = 0; ke < 8; ++ke) {
+      const TC* eb = (ke >> 2) & 1 ? e1 : e0;
+      q[ke] = TA(eb[((ke >> 1) & 1) * kSwEX + (ke & 1)]);
+    }
+    auto U = [&](int n, int c) -> TA {
+      const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
+      const TN* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
+      return TA(p[3 * (t1 * kSwWX + t0) + c]);
+    };
+    TA acc[3];
+    ku_vertex<TA>(q, kappa<TA>(), U, acc);
+    const size_t loc = vloc(g, xg, yg, z);
+    if constexpr (OUT == kSwDefect) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double r = double(f[3 * loc + c]) - double(acc[c]);
+        r32[3 * loc + c] = float(r);
+        ss += r * r;
+      }
+    } else if constexpr (OUT == kSwResidual) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+    }
+    __pipeline_wait_prior(0);
+    __syncthreads();
+  }
+  if constexpr (OUT == kSwDefect) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+    const int t = ty * kSwTX + tx;
+    if ((t & 31) == 0) red[t >> 5] = ss;
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kSwTX * kSwTY / 32; ++w) s += red[w];
+      partials[blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z)] = s;
+    }
+  }
+}
+
+bool sweep_ok(const GridGeo& g) {
+  return knob("L0_SWEEP", 1) != 0 && g.n[0] % kSwTX == 0 && g.n[1] % kSwTY == 0 && g.n[2] % 2 == 0 && g.n[2] >= 4 &&
+         g.n[0] % 2 == 0 && g.n[1] % 2 == 0;
+}
+
+static int sweep_tz(const GridGeo& g) {
+  // planes per CTA: enough CTAs for ~4 waves at 2 CTAs/SM, at least 8 planes (halo amortised)
+  const long long cols = (long long)(g.n[0] / kSwTX) * (g.n[1] / kSwTY);
+  int tz = g.n[2];
+  while (tz % 2 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;
+  return tz;
+}
+
+template <typename TC, typename TN, typename TA, int OUT>
+static long long launch_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul, const TN* f,
+                              TN* y, float* r32, double* partials, cudaStream_t s) {
+  const int tz = sweep_tz(g);
+  const dim3 gr(g.n[0] / kSwTX, g.n[1] / kSwTY, g.n[2] / tz);
+  constexpr size_t sm = sweep_smem<TN, TC>();
+  constexpr int minb = sizeof(TA) == 8 ? 2 : 3;
+  const void* fn = (const void*)l0_sweep_kernel<TC, TN, TA, OUT, minb>;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    IHOM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  l0_sweep_kernel<TC, TN, TA, OUT, minb><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials, tz);
+  IHOM_LAUNCH_CHECK();
+  return (long long)gr.x * gr.y * gr.z;
+}
+
+template <typename TC, typename TN, typename TA>
+void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul, const TN* f,
+                           TN* y, cudaStream_t s) {
+  if (f) launch_sweep<TC, TN, TA, kSwResidual>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
+  else launch_sweep<TC, TN, TA, kSwApply>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
+}
+
+long long launch_l0_defect_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
+                                 ZLink<double> ul, const double* f, float* r32, double* partials, cudaStream_t s) {
+  return launch_sweep<float, double, double, kSwDefect>(g, coeff, cl, u, ul, f, nullptr, r32, partials, s);
+}
+
+template void launch_l0_apply_sweep<float, double, double>(const GridGeo&, const float*, ZLink<float>, const double*,
+                                                           ZLink<double>, const double*, double*, cudaStream_t);
+template void launch_l0_apply_sweep<double, double, double>(const GridGeo&, const double*, ZLink<double>,
+                                                            const double*, ZLink<double>, const double*, double*,
+                                                            cudaStream_t);
+template void launch_l0_apply_sweep<float, float, float>(const GridGeo&, const float*, ZLink<float>, const float*,
+                                                         ZLink<float>, const float*, float*, cudaStream_t);
+
+}  // namespace ihomgpu

@@ -11,7 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _solve(ih, n, knobs, fabric_p=0):
+def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)
@@ -24,7 +24,7 @@ def _solve(ih, n, knobs, fabric_p=0):
             fab = ih.Fabric.local(fabric_p)
 
             def body(r):
-                hom = ih.Homogenizer(n, penal=1.0, precision="mixed", opts=ih.SolverOptions(tol=1e-4, mode="mixed_defect"),
+                hom = ih.Homogenizer(n, penal=1.0, precision=precision, opts=ih.SolverOptions(tol=1e-4, mode=mode),
                                      fabric=fab, rank=r)
                 m = n * n * hom.planes
                 hom.set_density(np.ascontiguousarray(phys[hom.z0 * n * n: hom.z0 * n * n + m]))
@@ -35,15 +35,16 @@ def _solve(ih, n, knobs, fabric_p=0):
             res = ih.run_slabs(fabric_p, body)
             fab.close()
             return res[0][0], res[0][1], [np.concatenate([r[2][i] for r in res]) for i in range(6)]
-        hom = ih.Homogenizer(n, penal=1.0, precision="mixed", opts=ih.SolverOptions(tol=1e-4, mode="mixed_defect"))
+        hom = ih.Homogenizer(n, penal=1.0, precision=precision, opts=ih.SolverOptions(tol=1e-4, mode=mode))
         hom.set_density(phys)
         st = hom.solve_cell_problems()
         out = (st["total_cycles"], hom.effective_tensor(), [hom.displacement(i) for i in range(6)])
         hom.close()
         return out
     finally:
-        ih.set_knob("L0_PAIR", 1)
+        ih.set_knob("L0_PAIR", 0)
         ih.set_knob("PAIR_MINB", 3)
+        ih.set_knob("L0_SWEEP", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -63,4 +64,57 @@ def test_paired_level0_kernels_bit_identical_on_slabs(ih):
     assert pair[0] == base[0]
     np.testing.assert_array_equal(pair[1], base[1])
     for a, b in zip(pair[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["mixed", "double"])
+def test_energy_cache_bit_identical_and_invalidated(ih, precision):
+    n = 16
+    rho = np.random.default_rng(11).uniform(0.05, 1.0, n ** 3) ** 3
+    seed = np.arange(36.0).reshape(6, 6) / 36.0
+
+    def run(cache):
+        ih.set_knob("ENERGY_CACHE", cache)
+        try:
+            hom = ih.Homogenizer(n, penal=1.0, precision=precision, opts=ih.SolverOptions(tol=1e-6))
+            hom.set_density(rho)
+            hom.solve_cell_problems()
+            C = hom.effective_tensor()
+            s1 = hom.tensor_sensitivity(seed)
+            # a displacement written through the API must drop the cached energies
+            u0 = hom.displacement(0)
+            hom.set_displacement(0, 0.5 * u0)
+            s2 = hom.tensor_sensitivity(seed)
+            hom.close()
+            return C, s1, s2
+        finally:
+            ih.set_knob("ENERGY_CACHE", 1)
+    C0, a0, b0 = run(0)
+    C1, a1, b1 = run(1)
+    np.testing.assert_array_equal(C0, C1)
+    np.testing.assert_array_equal(a0, a1)
+    np.testing.assert_array_equal(b0, b1)
+    assert np.max(np.abs(b1 - a1)) > 0
+
+
+@pytest.mark.parametrize("precision,mode", [("mixed", "mixed_defect"), ("mixed", "vcycle"), ("double", "vcycle"),
+                                            ("mixed", "pcg")])
+@pytest.mark.parametrize("n", [32, 64])
+def test_sweep_level0_kernels_bit_identical(ih, n, precision, mode):
+    """z-plane sweep (shared-memory plane ring) vs direct-load level-0 apply/residual kernels."""
+    base = _solve(ih, n, {"L0_SWEEP": 0}, precision=precision, mode=mode)
+    sw = _solve(ih, n, {"L0_SWEEP": 1}, precision=precision, mode=mode)
+    assert sw[0] == base[0]
+    np.testing.assert_array_equal(sw[1], base[1])
+    for a, b in zip(sw[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", ["mixed_defect", "vcycle"])
+def test_sweep_level0_kernels_bit_identical_on_slabs(ih, mode):
+    base = _solve(ih, 64, {"L0_SWEEP": 0}, fabric_p=2, mode=mode)
+    sw = _solve(ih, 64, {"L0_SWEEP": 1}, fabric_p=2, mode=mode)
+    assert sw[0] == base[0]
+    np.testing.assert_array_equal(sw[1], base[1])
+    for a, b in zip(sw[2], base[2]):
         np.testing.assert_array_equal(a, b)

@@ -1,7 +1,6 @@
 set -x
 mkdir -p gpurun_out
-nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/mbp tools/microbench_pipes.cu && /tmp/mbp > gpurun_out/pipes.txt 2>&1
-for k in l0_gs_fast2_kernel l0_residual_norm_fast_kernel l0_apply_fast_kernel; do
-  op=l0_gs_f32; [ $k = l0_residual_norm_fast_kernel ] && op=l0_defect_f64; [ $k = l0_apply_fast_kernel ] && op=l0_residual_f32
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 -o gpurun_out/ncu_$k -f python tools/kernel_bench.py --reso 512 --ops $op --reps 1 > gpurun_out/ncu_$k.log 2>&1
-done
+timeout 900 python -m pytest tests/test_kernel_variants.py -q -x --timeout 300 > gpurun_out/t_variants.log 2>&1; echo variants rc $?; tail -15 gpurun_out/t_variants.log
+for sw in 0 1; do IHOM_L0_SWEEP=$sw timeout 300 python tools/kernel_bench.py --reso 512 --ops l0_defect_f64,l0_residual_f32,l0_residual_f64 --reps 5 > gpurun_out/kb_sweep$sw.json 2>&1; done
+cat gpurun_out/kb_sweep*.json
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?

@@ -154,6 +154,18 @@ __device__ __forceinline__ void gather27(const GridGeo& g, int x, int y, int z, 
 }
 
 // 27-neighbour index of pair (ke, j): offset de + dj - 1 (src/fem.cpp:18-21).
+// Zero-start Gauss-Seidel: in the first forward sweep from u = 0, a vertex of
+// colour c only sees non-zero values in neighbours of colours < c (already
+// updated this sweep); bit n is set for the 27-neighbours of colour > c.
+__host__ __device__ constexpr unsigned zero_start_mask(int c) {
+  unsigned m = 0u;
+  for (int n = 0; n < 27; ++n) {
+    const int mk = (n % 3 != 1 ? 1 : 0) | ((n / 3) % 3 != 1 ? 2 : 0) | (n / 9 != 1 ? 4 : 0);
+    if ((c ^ mk) > c) m |= 1u << n;
+  }
+  return m;
+}
+
 __host__ __device__ constexpr int pair_ngb(int ke, int j) {
   return ((ke & 1) + (j & 1)) + 3 * (((ke >> 1) & 1) + ((j >> 1) & 1)) + 9 * (((ke >> 2) & 1) + ((j >> 2) & 1));
 }

@@ -356,7 +356,9 @@ __global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, con
 // Two same-colour vertices per thread, stacked in halved z (h2, h2+1): the upper
 // neighbour plane of the first (t2 = +1) is the lower plane of the second
 // (t2 = -1), so those 9 neighbours are loaded once into registers and reused.
-template <typename TC, typename TN, int MINB, bool ZL = false>
+// ZC >= 0: zero-start pass of colour ZC (first forward sweep from u = 0): the neighbours of
+// colours > ZC are known zeros and are neither loaded nor multiplied (common.cuh zero_start_mask).
+template <typename TC, typename TN, int MINB, bool ZL = false, int ZC = -1>
 __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const TC* __restrict__ coeff,
                                                                 ZLink<TC> cl, const TN* __restrict__ f,
                                                                 const TN* __restrict__ ur, ZLink<TN> ul, TN* uw,
@@ -365,6 +367,8 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     cl = {coeff, coeff};
     ul = {ur, ur};
   }
+  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
+  if constexpr (ZC >= 0) color = ZC;
   using TA = TN;
   const int h2 = 2 * blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
@@ -376,6 +380,9 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
   const TN* pa2 = zbase(fa, ur, ul, 2);  // == zbase(fb, ur, ul, 0) (a's upper plane is b's lower)
 #pragma unroll
   for (int n = 0; n < 9; ++n) {
+    if constexpr (ZC >= 0) {
+      if ((ZM >> (18 + n)) & 1u) continue;  // (t0, t1, +1) of a and (t0, t1, -1) of b: same colour
+    }
     const TN* p = pa2 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) shared_pl[n][c] = TA(__ldg(p + c));
@@ -396,8 +403,8 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     TA q[8];
     load_q_fast(coeff, cl, fx, q);
     TA m[3], sblk[9];
-    if (v == 0) ku_vertex_split<TA>(q, kappa<TA>(), Ua, m, sblk);
-    else ku_vertex_split<TA>(q, kappa<TA>(), Ub, m, sblk);
+    if (v == 0) ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), Ua, m, sblk);
+    else ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), Ub, m, sblk);
     const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
     TN rhs[3], out[3];
 #pragma unroll
@@ -740,12 +747,52 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
 }
 
 template <typename TC, typename TN, typename TA>
+bool l0_gs_zero_start_ok(const GridGeo& g) {
+  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>)
+    return knob("ZERO_START", 1) != 0 && fast_ok(g) && g.cd[0][2] % 2 == 0 && !pair_enabled() && gs2_enabled() &&
+           !tile_ok(g);
+  return false;
+}
+
+template <typename TC, typename TN, bool ZL, int ZC>
+static void launch_fast2_zs(const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff,
+                            ZLink<TC> cl, const TN* f, TN* u, ZLink<TN> ul) {
+  l0_gs_fast2_kernel<TC, TN, 5, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
+}
+template <typename TC, typename TN, bool ZL>
+static void launch_fast2_zs(int color, const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g,
+                            const TC* coeff, ZLink<TC> cl, const TN* f, TN* u, ZLink<TN> ul) {
+  switch (color) {
+    case 0: launch_fast2_zs<TC, TN, ZL, 0>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 1: launch_fast2_zs<TC, TN, ZL, 1>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 2: launch_fast2_zs<TC, TN, ZL, 2>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 3: launch_fast2_zs<TC, TN, ZL, 3>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 4: launch_fast2_zs<TC, TN, ZL, 4>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 5: launch_fast2_zs<TC, TN, ZL, 5>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    case 6: launch_fast2_zs<TC, TN, ZL, 6>(gr, b, s, g, coeff, cl, f, u, ul); break;
+    default: launch_fast2_zs<TC, TN, ZL, 7>(gr, b, s, g, coeff, cl, f, u, ul); break;
+  }
+}
+
+template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
-                        ZLink<TC> cl, ZLink<TN> ul) {
+                        ZLink<TC> cl, ZLink<TN> ul, bool zero_start) {
   const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
   if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
   cl = resolve(cl, coeff);
   ul = resolve(ul, u);
+  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
+    if (zero_start) {
+      if (!l0_gs_zero_start_ok<TC, TN, TA>(g)) throw std::logic_error("zero-start GS pass on an unsupported grid");
+      const dim3 b = fast_block(g);
+      const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2] / 2);
+      if (linked) launch_fast2_zs<TC, TN, true>(color, gr, b, s, g, coeff, cl, f, u, ul);
+      else launch_fast2_zs<TC, TN, false>(color, gr, b, s, g, coeff, cl, f, u, ul);
+      IHOM_LAUNCH_CHECK();
+      return;
+    }
+  }
+  if (zero_start) throw std::logic_error("zero-start GS pass exists for the f32 inner level-0 kernel only");
   if (!linked && tile_ok(g)) {
     const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, g.cd[0][2] / kTZ);
     const size_t sm = tile_smem<TN>();
@@ -878,7 +925,8 @@ template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, 
   template void launch_l0_apply<TC, TN, TA>(const GridGeo&, const TC*, const TN*, const TN*, TN*, cudaStream_t, \
                                             ZLink<TC>, ZLink<TN>);                                            \
   template void launch_l0_gs_color<TC, TN, TA>(const GridGeo&, const TC*, const TN*, TN*, int, cudaStream_t,      \
-                                               ZLink<TC>, ZLink<TN>);
+                                               ZLink<TC>, ZLink<TN>, bool);                                   \
+  template bool l0_gs_zero_start_ok<TC, TN, TA>(const GridGeo&);
 INST_L0(float, double, double)   // mixed, f64 nodal (parity)
 INST_L0(double, double, double)  // all-double
 INST_L0(float, float, float)     // mixed inner correction cycle

@@ -97,6 +97,17 @@ double gs_l0_bytes(const GridGeo& g, int c, double sN, double sC) {
 double gs_coarse_bytes(const GridGeo& g, int c, double sN, double sC) {
   return double(g.size[c]) * (243.0 * sC + 6.0 * sN) + double(g.nv - g.size[c]) * 3.0 * sN;
 }
+// zero-start pass (first sweep from u = 0): only colours < c hold data -- c of the 7 other colour
+// blocks are read, and a coarse vertex reads the stencil blocks of its non-zero neighbours only
+double gs_l0_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
+  return double(g.nv) * (double(c) / 8.0 * 3.0 * sN + sC) + double(g.size[c]) * 6.0 * sN;
+}
+double gs_coarse_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
+  const int live = 27 - __builtin_popcount(zero_start_mask(c));
+  double others = 0.0;
+  for (int k = 0; k < c; ++k) others += double(g.size[k]);
+  return double(g.size[c]) * (9.0 * live * sC + 6.0 * sN) + others * 3.0 * sN;
+}
 double resid_l0_bytes(const GridGeo& g, double sN, double sC, bool with_f) {
   return double(g.nv) * ((with_f ? 9.0 : 6.0) * sN + sC);
 }
@@ -418,20 +429,23 @@ void Hierarchy<T>::apply(int l, const double* x, double* y) {  // src/multigrid.
 }
 
 template <typename T>
-void Hierarchy<T>::relax(int l, int sweeps) {  // src/multigrid.cpp:400-408
+void Hierarchy<T>::relax(int l, int sweeps, bool zero_start) {  // src/multigrid.cpp:400-408
   Level& L = levels_[size_t(l)];
   double* u = level_u(l);
   const ZLink<double> ul = L.sharded ? ulink(l) : ZLink<double>{};
+  if (zero_start && l == 0) throw std::logic_error("zero-start sweeps exist on the coarse levels only");
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
       if (L.sharded) sync();  // colour c-1 of the neighbouring slabs is final
+      const bool zs = zero_start && sw == 0;
       if (l == 0) {
         ProfScope p(s_, "l0_gs_f64", gs_l0_bytes(L.g, c, 8, sizeof(T)));
         launch_l0_gs_color<T, double, double>(L.g, coeff_.p, L.f.p, u, c, s_, L.sharded ? coeff_l_ : ZLink<T>{}, ul);
       } else {
-        ProfScope p(s_, l == 1 ? "l1_gs_f64" : "coarse_gs_f64", gs_coarse_bytes(L.g, c, 8, sizeof(T)));
-        launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_, ul);
+        ProfScope p(s_, l == 1 ? "l1_gs_f64" : "coarse_gs_f64",
+                    zs ? gs_coarse_bytes_zs(L.g, c, 8, sizeof(T)) : gs_coarse_bytes(L.g, c, 8, sizeof(T)));
+        launch_stencil_gs_color<T, double>(L.g, L.st.p, L.f.p, u, c, err_.p, s_, ul, zs);
       }
       ++launches_;
     }
@@ -469,8 +483,10 @@ double Hierarchy<T>::v_cycle(const SolverOptions& opts) {  // src/multigrid.cpp:
   if (opts.mode == kMixedDefect && std::is_same_v<T, float>) return v_cycle_defect(opts);
   const int lmax = num_levels() - 1;
   for (int l = 0; l < lmax; ++l) {
-    if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].u.p, 0, sizeof(double) * 3 * levels_[size_t(l)].g.nv, s_));
-    relax(l, opts.pre_sweeps);
+    const bool zs = l > 0 && opts.pre_sweeps > 0 && zero_start_ok(l);
+    if (l > 0 && !zs)
+      IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].u.p, 0, sizeof(double) * 3 * levels_[size_t(l)].g.nv, s_));
+    relax(l, opts.pre_sweeps, zs);
     compute_residual(l);
     restrict_to(l, levels_[size_t(l)].r.p, levels_[size_t(l + 1)].f.p);
   }
@@ -515,21 +531,32 @@ void Hierarchy<T>::ensure_inner() {
 }
 
 template <typename T>
-void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse) {
+bool Hierarchy<T>::zero_start_ok(int l) const {
+  if (knob("ZERO_START", 1) == 0) return false;
+  if (l > 0) return true;  // every stencil GS kernel takes the zero mask
+  if constexpr (std::is_same_v<T, float>) return l0_gs_zero_start_ok<float, float, float>(levels_[0].g);
+  return false;  // level-0 f32 inner fields exist in mixed precision only
+}
+
+template <typename T>
+void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
+    if (zero_start && reverse) throw std::logic_error("zero-start sweeps run the colours forward");
     for (int sw = 0; sw < sweeps; ++sw)
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;
         if (L.g.size[c] == 0) continue;
         if (L.sharded) sync();
+        const bool zs = zero_start && sw == 0;
         if (l == 0) {
-          ProfScope p(s_, "l0_gs_f32", gs_l0_bytes(L.g, c, 4, 4));
+          ProfScope p(s_, "l0_gs_f32", zs ? gs_l0_bytes_zs(L.g, c, 4, 4) : gs_l0_bytes(L.g, c, 4, 4));
           launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_,
-                                                  L.sharded ? coeff_l_ : ZLink<float>{}, L.eul);
+                                                  L.sharded ? coeff_l_ : ZLink<float>{}, L.eul, zs);
         } else {
-          ProfScope p(s_, l == 1 ? "l1_gs_f32" : "coarse_gs_f32", gs_coarse_bytes(L.g, c, 4, 4));
-          launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_, L.eul);
+          ProfScope p(s_, l == 1 ? "l1_gs_f32" : "coarse_gs_f32",
+                      zs ? gs_coarse_bytes_zs(L.g, c, 4, 4) : gs_coarse_bytes(L.g, c, 4, 4));
+          launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_, L.eul, zs);
         }
         ++launches_;
       }
@@ -596,14 +623,19 @@ void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
   const int lmax = num_levels() - 1;
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
-  IHOM_CUDA(cudaMemsetAsync(L0.eu.p, 0, sizeof(float) * n0, s_));
-  launches_ += 1;
+  // e = 0 on every level before its pre-smoothing: with zero-start sweeps the first sweep never
+  // reads a colour it has not written yet, so the clear is skipped (bit-identical)
   for (int l = 0; l < lmax; ++l) {
-    if (l > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
-    relax_f32(l, opts.pre_sweeps);
+    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
+    if (!zs) {
+      IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
+      launches_ += l == 0 ? 1 : 0;
+    }
+    relax_f32(l, opts.pre_sweeps, false, zs);
     residual_f32(l);
     restrict_to_f32(l);
   }
+  (void)n0;
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_f32();
   for (int l = lmax - 1; l >= 0; --l) {

@@ -129,7 +129,7 @@ class Hierarchy {
 
   // Reference operations on the f64 level fields.
   void apply(int l, const double* x, double* y);  // y = K_l x
-  void relax(int l, int sweeps);
+  void relax(int l, int sweeps, bool zero_start = false);  // zero_start: u == 0 on entry (first sweep skips it)
   void compute_residual(int l);
   void coarsest_solve();
   double v_cycle(const SolverOptions& opts);
@@ -199,7 +199,8 @@ class Hierarchy {
   void check_error(const char* where);
   void ensure_inner();
   double v_cycle_defect(const SolverOptions& opts);
-  void relax_f32(int l, int sweeps, bool reverse = false);
+  void relax_f32(int l, int sweeps, bool reverse = false, bool zero_start = false);
+  bool zero_start_ok(int l) const;  // the level's GS kernels support a zero-start first sweep
   void inner_vcycle(const SolverOptions& opts, bool symmetric);  // eu0 ~= K^-1 ef0 from zero
   SolveStats solve_pcg(double* u, const SolverOptions& opts);
   void residual_f32(int l);

@@ -31,7 +31,11 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
 // One colour pass of the 8-colour Gauss-Seidel (src/fem.cpp:122-137).
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
-                        ZLink<TC> cl = {}, ZLink<TN> ul = {});
+                        ZLink<TC> cl = {}, ZLink<TN> ul = {}, bool zero_start = false);
+// true if launch_l0_gs_color takes the zero-start path on this grid (it then never reads colours > c
+// during the first sweep, so u need not be cleared before it)
+template <typename TC, typename TN, typename TA>
+bool l0_gs_zero_start_ok(const GridGeo& g);
 
 // z-plane sweep variants (sweep_kernels.cuh): shared-memory plane ring, bit-identical outputs
 bool sweep_ok(const GridGeo& g);
@@ -67,7 +71,7 @@ void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN*
                           ZLink<TN> xl = {});
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
-                             cudaStream_t s, ZLink<TN> ul = {});
+                             cudaStream_t s, ZLink<TN> ul = {}, bool zero_start = false);
 template <typename TC>
 void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s,
                                    ZLink<TC> cl = {}, const GridGeo* gout = nullptr, int zoff = 0);

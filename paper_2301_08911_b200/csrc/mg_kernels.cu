@@ -268,10 +268,12 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   }
 }
 
+// zm: neighbours known to be zero (zero-start sweep, common.cuh zero_start_mask): their stencil
+// blocks and values are not read -- bit-identical to adding their exact zero products.
 template <typename TS, typename TN, bool ZL = false>
 __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st,
                                                               const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              ZLink<TN> ul, TN* uw, int color, int* err) {
+                                                              ZLink<TN> ul, TN* uw, int color, int* err, unsigned zm) {
   if constexpr (!ZL) ul = {ur, ur};
   const int h2 = blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
   const TN* ub[3] = {zbase(fa, ur, ul, 0), ur, zbase(fa, ur, ul, 2)};
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
-    if (n == 13) continue;
+    if (n == 13 || ((zm >> n) & 1u)) continue;
     const TN* un = ub[n / 9] + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
     const double a = double(__ldg(un)), b = double(__ldg(un + 1)), c = double(__ldg(un + 2));
     const TS* bl = row + 32 * 9 * n;
@@ -373,7 +375,8 @@ __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, cons
 template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st,
                                                               const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              ZLink<TN> ul, TN* uw, int color, int* err) {
+                                                              ZLink<TN> ul, TN* uw, int color, int* err,
+                                                              unsigned zm) {
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= g.size[color]) return;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
   block_coords(g, color, (unsigned)i, vx, vy, vz);
   const long long loc = g.base[color] + i;
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-  if (lane < 27 && lane != 13) {
+  if (lane < 27 && lane != 13 && !((zm >> lane) & 1u)) {
     const TN* un = nbr_ptr(g, ur, ul, vx, vy, vz, lane);
     const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
     const TS* bl = st + st_index(9 * lane, (unsigned)loc);
@@ -436,7 +439,7 @@ void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN*
 template <typename TS, typename TN>
 __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st,
                                                          const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
-                                                         int color, int* err) {
+                                                         int color, int* err, unsigned zm) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.size[color]) return;
   int vx, vy, vz;
@@ -454,6 +457,7 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
       for (int e = 0; e < 9; ++e) S[e] = double(bl[32 * e]);
       continue;
     }
+    if ((zm >> n) & 1u) continue;
     const TN* un = ur + 3 * (size_t)nb.v[n];
     const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
     m[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
@@ -475,19 +479,20 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
 
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
-                             cudaStream_t s, ZLink<TN> ul) {
+                             cudaStream_t s, ZLink<TN> ul, bool zero_start) {
   const bool linked = !is_self(ul, u);
   ul = resolve(ul, u);
+  const unsigned zm = zero_start ? zero_start_mask(color) : 0u;
   if (g.size[color] <= kWarpVertexMax) {
-    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, ul, u, color, err);
+    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    if (linked) stencil_gs_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err);
-    else stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err);
+    if (linked) stencil_gs_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
+    else stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
   } else {
     if (linked) throw std::invalid_argument("z-slab level needs an even grid");
-    stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err);
+    stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err, zm);
   }
   IHOM_LAUNCH_CHECK();
 }
@@ -833,7 +838,7 @@ INST_T(float)
   template void launch_stencil_apply<TS, TN>(const GridGeo&, const TS*, const TN*, const TN*, TN*, cudaStream_t, \
                                              ZLink<TN>);                                                      \
   template void launch_stencil_gs_color<TS, TN>(const GridGeo&, const TS*, const TN*, TN*, int, int*,         \
-                                                cudaStream_t, ZLink<TN>);
+                                                cudaStream_t, ZLink<TN>, bool);
 INST_S(float, double)
 INST_S(double, double)
 INST_S(float, float)

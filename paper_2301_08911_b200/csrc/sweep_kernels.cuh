@@ -158,6 +158,145 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
   }
 }
 
+// ---------------------------------------------------------------- x-paired f32 sweep (FFMA2)
+// Thread (tx, ty) owns the two vertices (X0 + tx, y) and (X0 + 32 + tx, y) of a
+// 64 x TY tile; the shared window stores the two halves interleaved as float2
+// ([row][col][comp] -> {half 0, half 1}), so every neighbour operand of the
+// paired stencil is ONE LDS.64 at a compile-time offset, and the factored
+// stencil runs in float2 lane arithmetic (vec2.cuh). Bit-identical to the
+// scalar kernels lane by lane.
+constexpr int kS2Cols = kSwTX + 2;                       // window columns per half (34)
+constexpr int kS2USlot = kS2Cols * kSwWY * 3;            // float2 per u plane slot
+constexpr int kS2ECols = kSwTX + 1;                      // element window columns per half (33)
+constexpr int kS2ESlot = kS2ECols * kSwEY;               // float2 per element plane slot
+constexpr int kS2UItems = 2 * kS2Cols * kSwWY;           // window vertices per plane (both halves)
+constexpr int kS2EItems = 2 * kS2ECols * kSwEY;          // window elements per plane
+constexpr int kS2UPer = (kS2UItems + kSwTX * kSwTY - 1) / (kSwTX * kSwTY);
+constexpr int kS2EPer = (kS2EItems + kSwTX * kSwTY - 1) / (kSwTX * kSwTY);
+constexpr size_t kS2Smem = sizeof(float2) * (4 * kS2USlot + 3 * kS2ESlot);
+
+// grid = (n0 / 64, n1 / TY, t / TZ); block = (32, TY)
+template <int OUT>
+__global__ void __launch_bounds__(kSwTX* kSwTY, 2)
+    l0_sweep2_kernel(GridGeo g, const float* __restrict__ coeff, ZLink<float> cl, const float* __restrict__ u,
+                     ZLink<float> ul, const float* __restrict__ f, float* __restrict__ y, int TZ) {
+  extern __shared__ __align__(16) unsigned char sw_raw[];
+  float* us = reinterpret_cast<float*>(sw_raw);
+  float* es = reinterpret_cast<float*>(sw_raw + sizeof(float2) * 4 * kS2USlot);
+  const int X0 = blockIdx.x * 2 * kSwTX, Y0 = blockIdx.y * kSwTY, Z0 = blockIdx.z * TZ;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSwTX + tx;
+  const int t = g.n[2];
+  const unsigned plane = (unsigned)g.cd[0][0] * (unsigned)g.cd[0][1];  // one colour block's halved plane
+  // loader bookkeeping, fixed for the whole march: the window items this thread copies, as
+  // (smem float index, location in even-z / odd-z planes at halved z 0)
+  unsigned uE[kS2UPer], uO[kS2UPer];
+  int uS[kS2UPer];
+#pragma unroll
+  for (int r = 0; r < kS2UPer; ++r) {
+    const int v = tid + r * kSwTX * kSwTY;
+    uS[r] = -1;
+    if (v < kS2UItems) {
+      const int h = v & 1, w = v >> 1, i = w % kS2Cols, j = w / kS2Cols;
+      const int x = wrapc(X0 + kSwTX * h + i - 1, g.n[0]), yy = wrapc(Y0 + j - 1, g.n[1]);
+      uS[r] = 2 * 3 * w + h;
+      uE[r] = vloc(g, x, yy, 0);
+      uO[r] = vloc(g, x, yy, 1);
+    }
+  }
+  unsigned eXY[kS2EPer];
+  int eS[kS2EPer];
+#pragma unroll
+  for (int r = 0; r < kS2EPer; ++r) {
+    const int v = tid + r * kSwTX * kSwTY;
+    eS[r] = -1;
+    if (v < kS2EItems) {
+      const int h = v & 1, w = v >> 1, i = w % kS2ECols, j = w / kS2ECols;
+      const int x = wrapc(X0 + kSwTX * h + i - 1, g.n[0]), yy = wrapc(Y0 + j - 1, g.n[1]);
+      eS[r] = 2 * w + h;
+      eXY[r] = (unsigned)x + (unsigned)g.n[0] * (unsigned)yy;
+    }
+  }
+  const unsigned eplane = (unsigned)g.n[0] * (unsigned)g.n[1];
+  auto load_u = [&](int zl, int slot) {
+    const float* src = zl < 0 ? ul.lo : (zl >= t ? ul.hi : u);
+    const int z = zl < 0 ? zl + t : (zl >= t ? zl - t : zl);
+    const unsigned zoff = (unsigned)(z >> 1) * plane;
+    float* dst = us + slot * (2 * kS2USlot);
+#pragma unroll
+    for (int r = 0; r < kS2UPer; ++r)
+      if (uS[r] >= 0) {
+        const float* sp = src + 3 * (size_t)((z & 1 ? uO[r] : uE[r]) + zoff);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) __pipeline_memcpy_async(dst + uS[r] + 2 * c, sp + c, sizeof(float));
+      }
+  };
+  auto load_e = [&](int ezl, int slot) {
+    const float* src = ezl < 0 ? cl.lo : coeff;
+    const int ez = ezl < 0 ? ezl + t : ezl;
+    float* dst = es + slot * (2 * kS2ESlot);
+#pragma unroll
+    for (int r = 0; r < kS2EPer; ++r)
+      if (eS[r] >= 0) __pipeline_memcpy_async(dst + eS[r], src + eXY[r] + (size_t)ez * eplane, sizeof(float));
+  };
+  load_u(Z0 - 1, 3);
+  load_u(Z0, 0);
+  load_u(Z0 + 1, 1);
+  load_e(Z0 - 1, 2);
+  load_e(Z0, 0);
+  __pipeline_commit();
+  // output locations of the two vertices (even / odd z at halved z 0)
+  const int xa = X0 + tx, xb = X0 + kSwTX + tx, yv = Y0 + ty;
+  const unsigned oEa = vloc(g, xa, yv, 0), oOa = vloc(g, xa, yv, 1);
+  const unsigned oEb = vloc(g, xb, yv, 0), oOb = vloc(g, xb, yv, 1);
+  const float2* U2 = reinterpret_cast<const float2*>(us);
+  const float2* E2 = reinterpret_cast<const float2*>(es);
+  const int ubase = 3 * ((ty + 1) * kS2Cols + tx + 1);
+  __pipeline_wait_prior(0);
+  __syncthreads();
+  for (int k = 0; k < TZ; ++k) {
+    const int z = Z0 + k;
+    if (k + 2 <= TZ) {
+      load_u(z + 2, (k + 2) & 3);
+      if (k + 1 < TZ) load_e(z + 1, (k + 1) % 3);
+    }
+    __pipeline_commit();
+    const float2* p0 = U2 + ((k + 3) & 3) * kS2USlot + ubase;
+    const float2* p1 = U2 + (k & 3) * kS2USlot + ubase;
+    const float2* p2 = U2 + ((k + 1) & 3) * kS2USlot + ubase;
+    const float2* e0 = E2 + ((k + 2) % 3) * kS2ESlot + ty * kS2ECols + tx;
+    const float2* e1 = E2 + (k % 3) * kS2ESlot + ty * kS2ECols + tx;
+    float2 q[8];
+#pragma unroll
+    for (int ke = 0; ke < 8; ++ke) q[ke] = ((ke >> 2) & 1 ? e1 : e0)[((ke >> 1) & 1) * kS2ECols + (ke & 1)];
+    auto U = [&](int n, int c) -> float2 {
+      const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
+      const float2* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
+      return p[3 * (t1 * kS2Cols + t0) + c];
+    };
+    float2 acc[3];
+    ku_vertex<float2>(q, kappa<float>(), U, acc);
+    const unsigned zoff = (unsigned)(z >> 1) * plane;
+    const size_t la = (z & 1 ? oOa : oEa) + zoff, lb = (z & 1 ? oOb : oEb) + zoff;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if constexpr (OUT == kSwResidual) {
+        y[3 * la + c] = f[3 * la + c] - acc[c].x;
+        y[3 * lb + c] = f[3 * lb + c] - acc[c].y;
+      } else {
+        y[3 * la + c] = acc[c].x;
+        y[3 * lb + c] = acc[c].y;
+      }
+    }
+    __pipeline_wait_prior(0);
+    __syncthreads();
+  }
+}
+
+bool sweep2_ok(const GridGeo& g) {
+  return knob("L0_SWEEP2", 1) != 0 && g.n[0] % (2 * kSwTX) == 0 && g.n[1] % kSwTY == 0 && g.n[2] % 2 == 0 &&
+         g.n[2] >= 4;
+}
+
 bool sweep_ok(const GridGeo& g) {
   return knob("L0_SWEEP", 1) != 0 && g.n[0] % kSwTX == 0 && g.n[1] % kSwTY == 0 && g.n[2] % 2 == 0 && g.n[2] >= 4 &&
          g.n[0] % 2 == 0 && g.n[1] % 2 == 0;
@@ -192,6 +331,26 @@ static long long launch_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, c
 template <typename TC, typename TN, typename TA>
 void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul, const TN* f,
                            TN* y, cudaStream_t s) {
+  if constexpr (std::is_same_v<TC, float> && std::is_same_v<TN, float> && std::is_same_v<TA, float>) {
+    if (sweep2_ok(g)) {
+      const long long cols = (long long)(g.n[0] / (2 * kSwTX)) * (g.n[1] / kSwTY);
+      int tz = g.n[2];
+      while (tz % 2 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;
+      const dim3 gr(g.n[0] / (2 * kSwTX), g.n[1] / kSwTY, g.n[2] / tz);
+      static bool attr = false;
+      if (!attr) {
+        IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_sweep2_kernel<kSwResidual>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS2Smem));
+        IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_sweep2_kernel<kSwApply>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS2Smem));
+        attr = true;
+      }
+      if (f) l0_sweep2_kernel<kSwResidual><<<gr, dim3(kSwTX, kSwTY), kS2Smem, s>>>(g, coeff, cl, u, ul, f, y, tz);
+      else l0_sweep2_kernel<kSwApply><<<gr, dim3(kSwTX, kSwTY), kS2Smem, s>>>(g, coeff, cl, u, ul, f, y, tz);
+      IHOM_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (f) launch_sweep<TC, TN, TA, kSwResidual>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
   else launch_sweep<TC, TN, TA, kSwApply>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
 }

@@ -62,3 +62,14 @@ def test_host_validation_before_device(ih):
         ih.BaseMaterial(1.0, 0.5)
     with pytest.raises(ValueError):
         ih.BaseMaterial(-1.0, 0.3)
+
+
+def test_no_undefined_library_symbols():
+    """Every ihomgpu template the library calls is instantiated in it (a missing explicit
+    instantiation links fine as -shared and only fails at dlopen)."""
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2301_08911_b200", "libihom_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("library not built")
+    out = subprocess.run(["nm", "-D", "--undefined-only", lib], capture_output=True, text=True).stdout
+    assert "ihomgpu" not in out, out

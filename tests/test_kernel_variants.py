@@ -45,6 +45,8 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_PAIR", 0)
         ih.set_knob("PAIR_MINB", 3)
         ih.set_knob("L0_SWEEP", 1)
+        ih.set_knob("L0_SWEEP2", 1)
+        ih.set_knob("ZERO_START", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -101,13 +103,15 @@ def test_energy_cache_bit_identical_and_invalidated(ih, precision):
                                             ("mixed", "pcg")])
 @pytest.mark.parametrize("n", [32, 64])
 def test_sweep_level0_kernels_bit_identical(ih, n, precision, mode):
-    """z-plane sweep (shared-memory plane ring) vs direct-load level-0 apply/residual kernels."""
+    """z-plane sweep (shared-memory plane ring; x-paired FFMA2 form for f32 on 64-wide grids) vs the
+    direct-load level-0 apply/residual kernels."""
     base = _solve(ih, n, {"L0_SWEEP": 0}, precision=precision, mode=mode)
-    sw = _solve(ih, n, {"L0_SWEEP": 1}, precision=precision, mode=mode)
-    assert sw[0] == base[0]
-    np.testing.assert_array_equal(sw[1], base[1])
-    for a, b in zip(sw[2], base[2]):
-        np.testing.assert_array_equal(a, b)
+    for knobs in ({"L0_SWEEP": 1, "L0_SWEEP2": 0}, {"L0_SWEEP": 1, "L0_SWEEP2": 1}):
+        sw = _solve(ih, n, knobs, precision=precision, mode=mode)
+        assert sw[0] == base[0]
+        np.testing.assert_array_equal(sw[1], base[1])
+        for a, b in zip(sw[2], base[2]):
+            np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("mode", ["mixed_defect", "vcycle"])
@@ -117,4 +121,26 @@ def test_sweep_level0_kernels_bit_identical_on_slabs(ih, mode):
     assert sw[0] == base[0]
     np.testing.assert_array_equal(sw[1], base[1])
     for a, b in zip(sw[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision,mode", [("mixed", "mixed_defect"), ("mixed", "vcycle"), ("double", "vcycle"),
+                                            ("mixed", "pcg")])
+@pytest.mark.parametrize("n", [32, 64, (16, 16, 10)])
+def test_zero_start_sweeps_bit_identical(ih, n, precision, mode):
+    """Zero-start pre-smoothing (colours > c of the first sweep are known zeros: not read, not cleared)."""
+    base = _solve(ih, n, {"ZERO_START": 0}, precision=precision, mode=mode)
+    zs = _solve(ih, n, {"ZERO_START": 1}, precision=precision, mode=mode)
+    assert zs[0] == base[0]
+    np.testing.assert_array_equal(zs[1], base[1])
+    for a, b in zip(zs[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_zero_start_sweeps_bit_identical_on_slabs(ih):
+    base = _solve(ih, 64, {"ZERO_START": 0}, fabric_p=4)
+    zs = _solve(ih, 64, {"ZERO_START": 1}, fabric_p=4)
+    assert zs[0] == base[0]
+    np.testing.assert_array_equal(zs[1], base[1])
+    for a, b in zip(zs[2], base[2]):
         np.testing.assert_array_equal(a, b)

@@ -148,10 +148,12 @@ def main():
         fname = "ku_vertex_split" if split else "ku_vertex"
         out.append("")
         out.append("// U(n, c): neighbour n (27-index, x fastest), component c, as TA; kap: scalar kappa classes.")
+        out.append("// ZM: neighbours known to hold zero (bit n) -- their terms and loads are skipped, which is")
+        out.append("// bit-identical to adding their exact zero products (a zero-start Gauss-Seidel sweep).")
         if split:
             out.append("// Off-diagonal part M (n != 13) into y; self block S (n == 13) into S[9].")
-        out.append("template <typename TA, typename TK, typename LoadU>")
-        sig = f"__device__ __forceinline__ void {fname}(const TA q[8], const TK* __restrict__ kap, LoadU U, TA y[3]"
+        out.append("template <unsigned ZM, typename TA, typename TK, typename LoadU>")
+        sig = f"__device__ __forceinline__ void {fname}_z(const TA q[8], const TK* __restrict__ kap, LoadU U, TA y[3]"
         sig += ", TA S[9])" if split else ")"
         out.append(sig + " {")
         emitted = set()
@@ -176,7 +178,7 @@ def main():
             for r in range(3):
                 for c in range(3):
                     emit_form(used[(n, r, c)][0])
-            out.append(f"  {{  // neighbour {n}")
+            out.append(f"  if constexpr (!((ZM >> {n}) & 1u)) {{  // neighbour {n}")
             for c in range(3):
                 out.append(f"    const TA u{c} = U({n}, {c});")
             for r in range(3):
@@ -202,6 +204,12 @@ def main():
                     k, cs = cls_of[(13, r, c)]
                     sgn = fs * cs
                     out.append(f"  S[{3 * r + c}] = vmul(vbc<TA>({'' if sgn > 0 else '-'}kap[{k}]), {name});")
+        out.append("}")
+        out.append("template <typename TA, typename TK, typename LoadU>")
+        sig = f"__device__ __forceinline__ void {fname}(const TA q[8], const TK* __restrict__ kap, LoadU U, TA y[3]"
+        sig += ", TA S[9])" if split else ")"
+        out.append(sig + " {")
+        out.append(f"  {fname}_z<0u>(q, kap, U, y{', S' if split else ''});")
         out.append("}")
     out.append("}  // namespace ihomgpu")
     path = os.path.join(ROOT, "paper_2301_08911_b200", "csrc", "ku_gen.cuh")

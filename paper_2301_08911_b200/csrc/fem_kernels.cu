@@ -746,18 +746,30 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
   for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }
 
+bool gs_sweep_ok(const GridGeo& g);
+void launch_l0_gs_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
+                        ZLink<float> ul, int color, bool zero_start, cudaStream_t s);
+
 template <typename TC, typename TN, typename TA>
 bool l0_gs_zero_start_ok(const GridGeo& g) {
-  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>)
-    return knob("ZERO_START", 1) != 0 && fast_ok(g) && g.cd[0][2] % 2 == 0 && !pair_enabled() && gs2_enabled() &&
-           !tile_ok(g);
+  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float> && std::is_same_v<TC, float>) {
+    if (knob("ZERO_START", 1) == 0) return false;
+    if (gs_sweep_ok(g)) return true;
+    return fast_ok(g) && g.cd[0][2] % 2 == 0 && !pair_enabled() && gs2_enabled() && !tile_ok(g);
+  }
   return false;
 }
+
+// register budget of the two-vertex GS kernel: 5 blocks/SM (96 regs, default) or 6 / 8 (knob GS2_MINB)
+static int gs2_minb() { return knob("GS2_MINB", 5); }
 
 template <typename TC, typename TN, bool ZL, int ZC>
 static void launch_fast2_zs(const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff,
                             ZLink<TC> cl, const TN* f, TN* u, ZLink<TN> ul) {
-  l0_gs_fast2_kernel<TC, TN, 5, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
+  const int mb = ZL ? 5 : gs2_minb();
+  if (mb >= 8) l0_gs_fast2_kernel<TC, TN, 8, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
+  else if (mb == 6) l0_gs_fast2_kernel<TC, TN, 6, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
+  else l0_gs_fast2_kernel<TC, TN, 5, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
 }
 template <typename TC, typename TN, bool ZL>
 static void launch_fast2_zs(int color, const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g,
@@ -781,6 +793,12 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
   if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
   cl = resolve(cl, coeff);
   ul = resolve(ul, u);
+  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float> && std::is_same_v<TC, float>) {
+    if (gs_sweep_ok(g)) {
+      launch_l0_gs_sweep(g, coeff, cl, f, u, ul, color, zero_start, s);
+      return;
+    }
+  }
   if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
     if (zero_start) {
       if (!l0_gs_zero_start_ok<TC, TN, TA>(g)) throw std::logic_error("zero-start GS pass on an unsupported grid");
@@ -813,6 +831,8 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
       } else if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
         if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else if (gs2_minb() >= 8) l0_gs_fast2_kernel<TC, TN, 8><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else if (gs2_minb() == 6) l0_gs_fast2_kernel<TC, TN, 6><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else l0_gs_fast2_kernel<TC, TN, 5><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         done = true;
       }

@@ -554,7 +554,7 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
           launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_,
                                                   L.sharded ? coeff_l_ : ZLink<float>{}, L.eul, zs);
         } else {
-          ProfScope p(s_, l == 1 ? "l1_gs_f32" : "coarse_gs_f32",
+          ProfScope p(s_, l == 1 ? "l1_gs_f32" : (l == 2 ? "l2_gs_f32" : "coarse_gs_f32"),
                       zs ? gs_coarse_bytes_zs(L.g, c, 4, 4) : gs_coarse_bytes(L.g, c, 4, 4));
           launch_stencil_gs_color<float, float>(L.g, L.st.p, L.ef.p, L.eu.p, c, err_.p, s_, L.eul, zs);
         }
@@ -573,7 +573,7 @@ void Hierarchy<T>::residual_f32(int l) {
       launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_,
                                            L.sharded ? coeff_l_ : ZLink<float>{}, L.eul);
     } else {
-      ProfScope p(s_, l == 1 ? "l1_residual_f32" : "coarse_residual_f32", resid_coarse_bytes(L.g, 4, 4, true));
+      ProfScope p(s_, l == 1 ? "l1_residual_f32" : (l == 2 ? "l2_residual_f32" : "coarse_residual_f32"), resid_coarse_bytes(L.g, 4, 4, true));
       launch_stencil_apply<float, float>(L.g, L.st.p, L.eu.p, L.ef.p, L.er.p, s_, L.eul);
     }
     ++launches_;

@@ -505,6 +505,28 @@ __constant__ int c_eg_start[28];
 __constant__ int c_eg_oidx[kMaxEgTerms];
 __constant__ double c_eg_w[kMaxEgTerms][9];
 
+// ---- compile-time term structure of the element Galerkin table (tables.cpp ElementGalerkin) ----
+// Fine element offset o in {-2..1}^3 contributes to output neighbour delta iff, per axis,
+// o in [2 delta - 2, 2 delta + 1] (some local vertex of the element interpolates from v_c and some
+// from v_c + delta); terms are ordered by oidx = (ox+2) + 4 (oy+2) + 16 (oz+2) within each n.
+// upload_galerkin_tables() checks the host table against this structure.
+__host__ __device__ constexpr bool eg_axis_in(int o, int d) { return o >= 2 * d - 2 && o <= 2 * d + 1; }
+__host__ __device__ constexpr bool eg_has(int n, int oidx) {
+  return eg_axis_in(oidx % 4 - 2, n % 3 - 1) && eg_axis_in((oidx / 4) % 4 - 2, (n / 3) % 3 - 1) &&
+         eg_axis_in(oidx / 16 - 2, n / 9 - 1);
+}
+__host__ __device__ constexpr int eg_rank(int n, int oidx) {  // terms of n before oidx
+  int r = 0;
+  for (int o = 0; o < oidx; ++o) r += eg_has(n, o) ? 1 : 0;
+  return r;
+}
+__host__ __device__ constexpr int eg_start(int n) {
+  int k = 0;
+  for (int m = 0; m < n; ++m) k += eg_rank(m, 64);
+  return k;
+}
+
+
 void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
   int start[28];
   static int oidx[kMaxEgTerms];
@@ -520,6 +542,12 @@ void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s) {
     }
   }
   start[27] = k;
+  for (int n = 0; n < 27; ++n) {  // the unrolled kernel hard-codes this structure
+    if (start[n] != eg_start(n)) throw std::logic_error("element Galerkin table: unexpected term count");
+    for (int i = start[n]; i < start[n + 1]; ++i)
+      if (!eg_has(n, oidx[i]) || eg_rank(n, oidx[i]) != i - start[n])
+        throw std::logic_error("element Galerkin table: unexpected term order");
+  }
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_start, start, sizeof(start), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_oidx, oidx, sizeof(int) * k, 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_eg_w, w, sizeof(double) * 9 * k, 0, cudaMemcpyHostToDevice, s));
@@ -572,6 +600,65 @@ __global__ void __launch_bounds__(128) gal_elem_kernel(GridGeo gf, GridGeo gc, c
   for (int e = 0; e < 9; ++e) st[st_index(9 * n + e, loc)] = TC(acc[e]);
 }
 
+// Level-1 Galerkin with the term list unrolled at compile time: the fine-coefficient address of
+// every term is a fixed register sum, W comes straight from the constant bank as a DFMA operand
+// (no shared-memory staging, no dynamic indexing). Same terms, same order, same arithmetic as
+// gal_elem_kernel: bit-identical.
+template <typename TC, int N, int OI = 0>
+__device__ __forceinline__ void gal_elem_terms(const TC* const zb[4], const int ex[4], const int ey[4],
+                                               const int ez[4], double acc[9]) {
+  if constexpr (OI < 64) {
+    if constexpr (eg_has(N, OI)) {
+      constexpr int k = eg_start(N) + eg_rank(N, OI);
+      const double q = double(__ldg(zb[OI >> 4] + (ex[OI & 3] + ey[(OI >> 2) & 3] + ez[OI >> 4])));
+#pragma unroll
+      for (int e = 0; e < 9; ++e) acc[e] += q * c_eg_w[k][e];
+    }
+    gal_elem_terms<TC, N, OI + 1>(zb, ex, ey, ez, acc);
+  }
+}
+
+template <typename TC, int N>
+__device__ __forceinline__ void gal_elem_n(const TC* const zb[4], const int ex[4], const int ey[4], const int ez[4],
+                                           TC* __restrict__ st, unsigned loc) {
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  gal_elem_terms<TC, N>(zb, ex, ey, ez, acc);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) st[st_index(9 * N + e, loc)] = TC(acc[e]);
+}
+
+template <typename TC, int N = 0>
+__device__ __forceinline__ void gal_elem_dispatch(int n, const TC* const zb[4], const int ex[4], const int ey[4],
+                                                  const int ez[4], TC* __restrict__ st, unsigned loc) {
+  if constexpr (N < 27) {
+    if (n == N) gal_elem_n<TC, N>(zb, ex, ey, ez, st, loc);
+    else gal_elem_dispatch<TC, N + 1>(n, zb, ex, ey, ez, st, loc);
+  }
+}
+
+template <typename TC>
+__global__ void __launch_bounds__(128) gal_elem_unrolled_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
+                                                                ZLink<TC> cl, GridGeo gout, int zoff,
+                                                                TC* __restrict__ st) {
+  const int n = blockIdx.z % 27;
+  const int rest = blockIdx.z / 27;
+  const int color = rest & 7, h2 = rest >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+  const int x = 2 * h0 + (color & 1), y = 2 * h1 + ((color >> 1) & 1), z = 2 * h2 + ((color >> 2) & 1);
+  int ex[4], ey[4], ez[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    ex[o] = wrapi(2 * x + o - 2, gf.n[0]);
+    ey[o] = gf.n[0] * wrapi(2 * y + o - 2, gf.n[1]);
+    ez[o] = gf.n[0] * gf.n[1] * wrapi(2 * z + o - 2, gf.n[2]);
+  }
+  const TC* zb[4] = {2 * z - 2 < 0 ? cl.lo : coeff, 2 * z - 1 < 0 ? cl.lo : coeff, coeff, coeff};
+  const unsigned loc =
+      (unsigned)(color * gout.size[0] + h0 + (long long)gout.cd[0][0] * (h1 + (long long)gout.cd[0][1] * (h2 + zoff)));
+  gal_elem_dispatch<TC>(n, zb, ex, ey, ez, st, loc);
+}
+
 // generic (odd coarse grids): one thread per (coarse vertex, n), term list from constant memory
 template <typename TC>
 __global__ void __launch_bounds__(128) gal_elem_generic_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
@@ -606,7 +693,11 @@ void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const T
   if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
-    gal_elem_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, resolve(cl, coeff), gout ? *gout : gc, gout ? zoff : 0, st);
+    if (knob("GAL_UNROLLED", 1))
+      gal_elem_unrolled_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, resolve(cl, coeff), gout ? *gout : gc,
+                                                    gout ? zoff : 0, st);
+    else
+      gal_elem_kernel<TC><<<gr, b, 0, s>>>(gf, gc, coeff, resolve(cl, coeff), gout ? *gout : gc, gout ? zoff : 0, st);
   } else {
     if (!is_self(cl, coeff) || gout) throw std::invalid_argument("z-slab Galerkin needs an even coarse grid");
     gal_elem_generic_kernel<TC><<<dim3(ceil_div(gc.nv, 128), 27), 128, 0, s>>>(gf, gc, coeff, st);

@@ -47,6 +47,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_SWEEP", 1)
         ih.set_knob("L0_SWEEP2", 1)
         ih.set_knob("ZERO_START", 1)
+        ih.set_knob("L0_GS_SWEEP", 0)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -144,3 +145,52 @@ def test_zero_start_sweeps_bit_identical_on_slabs(ih):
     np.testing.assert_array_equal(zs[1], base[1])
     for a, b in zip(zs[2], base[2]):
         np.testing.assert_array_equal(a, b)
+
+
+BASE = {"L0_SWEEP": 0, "L0_GS_SWEEP": 0, "ZERO_START": 0, "L0_PAIR": 0}
+VARIANTS = [
+    {"L0_GS_SWEEP": 1, "ZERO_START": 0, "L0_SWEEP": 0},
+    {"L0_GS_SWEEP": 1, "ZERO_START": 1, "L0_SWEEP": 0},
+    {"L0_GS_SWEEP": 0, "ZERO_START": 1, "L0_SWEEP": 1, "L0_SWEEP2": 1},  # the default configuration
+]
+
+
+@pytest.mark.parametrize("precision,mode", [("mixed", "mixed_defect"), ("mixed", "pcg"), ("mixed", "vcycle")])
+@pytest.mark.parametrize("n", [32, 128, (128, 64, 64)])
+def test_gs_sweep_bit_identical(ih, n, precision, mode):
+    """Level-0 f32 Gauss-Seidel as an x-paired z-plane sweep (plain and zero-start) == direct-load kernels."""
+    base = _solve(ih, n, BASE, precision=precision, mode=mode)
+    for knobs in VARIANTS:
+        v = _solve(ih, n, {**BASE, **knobs}, precision=precision, mode=mode)
+        assert v[0] == base[0], knobs
+        np.testing.assert_array_equal(v[1], base[1])
+        for a, b in zip(v[2], base[2]):
+            np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_gs_sweep_bit_identical_on_slabs(ih, P):
+    base = _solve(ih, 128, BASE, fabric_p=P)
+    v = _solve(ih, 128, {**BASE, **VARIANTS[-1]}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["mixed", "double"])
+@pytest.mark.parametrize("n", [16, 32])
+def test_unrolled_element_galerkin_bit_identical(ih, n, precision):
+    """Level-1 Galerkin with the compile-time term list == the table-driven kernel."""
+    rho = np.random.default_rng(21).uniform(0.05, 1.0, n ** 3)
+    out = []
+    for unrolled in (0, 1):
+        ih.set_knob("GAL_UNROLLED", unrolled)
+        try:
+            hom = ih.Homogenizer(n, penal=3.0, precision=precision)
+            hom.set_density(rho)
+            out.append(hom.hierarchy().stencil(1))
+            hom.close()
+        finally:
+            ih.set_knob("GAL_UNROLLED", 1)
+    np.testing.assert_array_equal(out[0], out[1])

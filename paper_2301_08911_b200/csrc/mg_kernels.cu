@@ -640,8 +640,12 @@ template <typename TC>
 __global__ void __launch_bounds__(128) gal_elem_unrolled_kernel(GridGeo gf, GridGeo gc, const TC* __restrict__ coeff,
                                                                 ZLink<TC> cl, GridGeo gout, int zoff,
                                                                 TC* __restrict__ st) {
-  const int n = blockIdx.z % 27;
-  const int rest = blockIdx.z / 27;
+  // n SLOWEST (blockIdx.z = rest + 8 d2 n): the resident blocks run the same n-branch, so the
+  // instruction cache holds one ~5 KB unrolled body instead of thrashing over all 27 (ncu:
+  // "no_instruction" was the top stall with n fastest); the coefficients are re-read per n from L2/HBM.
+  const int nrest = 8 * gc.cd[0][2];
+  const int n = blockIdx.z / nrest;
+  const int rest = blockIdx.z % nrest;
   const int color = rest & 7, h2 = rest >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;

@@ -37,9 +37,13 @@ constexpr int kSwESlot = kSwEX * kSwEY;               // TC values per element p
 
 enum SweepOut { kSwApply = 0, kSwResidual = 1, kSwDefect = 2 };
 
+// Two vertex planes per step (one barrier per two planes): a step needs u planes z-1 .. z+2 and
+// element planes z-1 .. z+1 while the next step's two new planes stream in -> rings of 6 and 5.
+constexpr int kSwURing = 6, kSwERing = 5;
+
 template <typename TN, typename TC>
 constexpr size_t sweep_smem() {
-  return sizeof(TN) * 4 * kSwUSlot + sizeof(TC) * 3 * kSwESlot;
+  return sizeof(TN) * kSwURing * kSwUSlot + sizeof(TC) * kSwERing * kSwESlot;
 }
 
 __device__ __forceinline__ int wrapc(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }
@@ -84,61 +88,63 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
                     const TN* __restrict__ f, TN* __restrict__ y, float* __restrict__ r32, double* partials, int TZ) {
   extern __shared__ __align__(16) unsigned char sw_raw[];
   TN* us = reinterpret_cast<TN*>(sw_raw);
-  TC* es = reinterpret_cast<TC*>(sw_raw + sizeof(TN) * 4 * kSwUSlot);
+  TC* es = reinterpret_cast<TC*>(sw_raw + sizeof(TN) * kSwURing * kSwUSlot);
   __shared__ double red[kSwTX * kSwTY / 32];
   const int X0 = blockIdx.x * kSwTX, Y0 = blockIdx.y * kSwTY, Z0 = blockIdx.z * TZ;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int xg = X0 + tx, yg = Y0 + ty;
-  // prologue: u planes Z0-1, Z0, Z0+1 -> slots 3, 0, 1 (slot of plane z = (z - Z0) & 3); elements Z0-1, Z0
-  sweep_load_u(g, u, ul, X0, Y0, Z0 - 1, us + 3 * kSwUSlot);
-  sweep_load_u(g, u, ul, X0, Y0, Z0, us);
-  sweep_load_u(g, u, ul, X0, Y0, Z0 + 1, us + kSwUSlot);
-  sweep_load_e(g, coeff, cl, X0, Y0, Z0 - 1, es + 2 * kSwESlot);  // element slot of plane ez = (ez - Z0) mod 3
-  sweep_load_e(g, coeff, cl, X0, Y0, Z0, es);
+  // u plane z sits in slot (z - Z0 + 1) % 6, element plane ez in slot (ez - Z0 + 1) % 5
+  for (int P = 0; P < 4; ++P) sweep_load_u(g, u, ul, X0, Y0, Z0 - 1 + P, us + P * kSwUSlot);
+  for (int E = 0; E < 3; ++E) sweep_load_e(g, coeff, cl, X0, Y0, Z0 - 1 + E, es + E * kSwESlot);
   __pipeline_commit();
   __pipeline_wait_prior(0);
   __syncthreads();
   double ss = 0.0;
   const int ubase = 3 * ((ty + 1) * kSwWX + tx + 1);
-  for (int k = 0; k < TZ; ++k) {
-    const int z = Z0 + k;
-    if (k + 2 <= TZ) {  // plane z+2 (needed by the vertex plane z+1) and element plane z+1
-      sweep_load_u(g, u, ul, X0, Y0, z + 2, us + ((k + 2) & 3) * kSwUSlot);
-      if (k + 1 < TZ) sweep_load_e(g, coeff, cl, X0, Y0, z + 1, es + ((k + 1) % 3) * kSwESlot);
+  for (int k = 0; k < TZ; k += 2) {
+    if (k + 2 < TZ) {  // planes z+3, z+4 and element planes z+2, z+3 for the next step
+      sweep_load_u(g, u, ul, X0, Y0, Z0 + k + 3, us + ((k + 4) % kSwURing) * kSwUSlot);
+      sweep_load_u(g, u, ul, X0, Y0, Z0 + k + 4, us + ((k + 5) % kSwURing) * kSwUSlot);
+      sweep_load_e(g, coeff, cl, X0, Y0, Z0 + k + 2, es + ((k + 3) % kSwERing) * kSwESlot);
+      sweep_load_e(g, coeff, cl, X0, Y0, Z0 + k + 3, es + ((k + 4) % kSwERing) * kSwESlot);
     }
     __pipeline_commit();
-    const TN* p0 = us + ((k + 3) & 3) * kSwUSlot + ubase;  // plane z-1
-    const TN* p1 = us + (k & 3) * kSwUSlot + ubase;        // plane z
-    const TN* p2 = us + ((k + 1) & 3) * kSwUSlot + ubase;  // plane z+1
-    const TC* e0 = es + ((k + 2) % 3) * kSwESlot + ty * kSwEX + tx;  // element plane z-1, element (x-1, y-1)
-    const TC* e1 = es + (k % 3) * kSwESlot + ty * kSwEX + tx;        // element plane z
-    TA q[8];
+#pragma unroll 1
+    for (int dz = 0; dz < 2; ++dz) {
+      const int kk = k + dz, z = Z0 + kk;
+      const TN* p0 = us + (kk % kSwURing) * kSwUSlot + ubase;        // plane z-1
+      const TN* p1 = us + ((kk + 1) % kSwURing) * kSwUSlot + ubase;  // plane z
+      const TN* p2 = us + ((kk + 2) % kSwURing) * kSwUSlot + ubase;  // plane z+1
+      const TC* e0 = es + (kk % kSwERing) * kSwESlot + ty * kSwEX + tx;        // element plane z-1
+      const TC* e1 = es + ((kk + 1) % kSwERing) * kSwESlot + ty * kSwEX + tx;  // element plane z
+      TA q[8];
 #pragma unroll
-    for (int ke = 0; ke < 8; ++ke) {
-      const TC* eb = (ke >> 2) & 1 ? e1 : e0;
-      q[ke] = TA(eb[((ke >> 1) & 1) * kSwEX + (ke & 1)]);
-    }
-    auto U = [&](int n, int c) -> TA {
-      const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
-      const TN* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
-      return TA(p[3 * (t1 * kSwWX + t0) + c]);
-    };
-    TA acc[3];
-    ku_vertex<TA>(q, kappa<TA>(), U, acc);
-    const size_t loc = vloc(g, xg, yg, z);
-    if constexpr (OUT == kSwDefect) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double r = double(f[3 * loc + c]) - double(acc[c]);
-        r32[3 * loc + c] = float(r);
-        ss += r * r;
+      for (int ke = 0; ke < 8; ++ke) {
+        const TC* eb = (ke >> 2) & 1 ? e1 : e0;
+        q[ke] = TA(eb[((ke >> 1) & 1) * kSwEX + (ke & 1)]);
       }
-    } else if constexpr (OUT == kSwResidual) {
+      auto U = [&](int n, int c) -> TA {
+        const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
+        const TN* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
+        return TA(p[3 * (t1 * kSwWX + t0) + c]);
+      };
+      TA acc[3];
+      ku_vertex<TA>(q, kappa<TA>(), U, acc);
+      const size_t loc = vloc(g, xg, yg, z);
+      if constexpr (OUT == kSwDefect) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
-    } else {
+        for (int c = 0; c < 3; ++c) {
+          const double r = double(f[3 * loc + c]) - double(acc[c]);
+          r32[3 * loc + c] = float(r);
+          ss += r * r;
+        }
+      } else if constexpr (OUT == kSwResidual) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+        for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+      }
     }
     __pipeline_wait_prior(0);
     __syncthreads();
@@ -173,7 +179,7 @@ constexpr int kS2UItems = 2 * kS2Cols * kSwWY;           // window vertices per 
 constexpr int kS2EItems = 2 * kS2ECols * kSwEY;          // window elements per plane
 constexpr int kS2UPer = (kS2UItems + kSwTX * kSwTY - 1) / (kSwTX * kSwTY);
 constexpr int kS2EPer = (kS2EItems + kSwTX * kSwTY - 1) / (kSwTX * kSwTY);
-constexpr size_t kS2Smem = sizeof(float2) * (4 * kS2USlot + 3 * kS2ESlot);
+constexpr size_t kS2Smem = sizeof(float2) * (kSwURing * kS2USlot + kSwERing * kS2ESlot);
 
 // grid = (n0 / 64, n1 / TY, t / TZ); block = (32, TY)
 template <int OUT>
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, 2)
                      ZLink<float> ul, const float* __restrict__ f, float* __restrict__ y, int TZ) {
   extern __shared__ __align__(16) unsigned char sw_raw[];
   float* us = reinterpret_cast<float*>(sw_raw);
-  float* es = reinterpret_cast<float*>(sw_raw + sizeof(float2) * 4 * kS2USlot);
+  float* es = reinterpret_cast<float*>(sw_raw + sizeof(float2) * kSwURing * kS2USlot);
   const int X0 = blockIdx.x * 2 * kSwTX, Y0 = blockIdx.y * kSwTY, Z0 = blockIdx.z * TZ;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSwTX + tx;
   const int t = g.n[2];
@@ -238,11 +244,8 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, 2)
     for (int r = 0; r < kS2EPer; ++r)
       if (eS[r] >= 0) __pipeline_memcpy_async(dst + eS[r], src + eXY[r] + (size_t)ez * eplane, sizeof(float));
   };
-  load_u(Z0 - 1, 3);
-  load_u(Z0, 0);
-  load_u(Z0 + 1, 1);
-  load_e(Z0 - 1, 2);
-  load_e(Z0, 0);
+  for (int P = 0; P < 4; ++P) load_u(Z0 - 1 + P, P);  // u plane z in slot (z - Z0 + 1) % 6
+  for (int E = 0; E < 3; ++E) load_e(Z0 - 1 + E, E);  // element plane ez in slot (ez - Z0 + 1) % 5
   __pipeline_commit();
   // output locations of the two vertices (even / odd z at halved z 0)
   const int xa = X0 + tx, xb = X0 + kSwTX + tx, yv = Y0 + ty;
@@ -253,38 +256,43 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, 2)
   const int ubase = 3 * ((ty + 1) * kS2Cols + tx + 1);
   __pipeline_wait_prior(0);
   __syncthreads();
-  for (int k = 0; k < TZ; ++k) {
-    const int z = Z0 + k;
-    if (k + 2 <= TZ) {
-      load_u(z + 2, (k + 2) & 3);
-      if (k + 1 < TZ) load_e(z + 1, (k + 1) % 3);
+  for (int k = 0; k < TZ; k += 2) {
+    if (k + 2 < TZ) {
+      load_u(Z0 + k + 3, (k + 4) % kSwURing);
+      load_u(Z0 + k + 4, (k + 5) % kSwURing);
+      load_e(Z0 + k + 2, (k + 3) % kSwERing);
+      load_e(Z0 + k + 3, (k + 4) % kSwERing);
     }
     __pipeline_commit();
-    const float2* p0 = U2 + ((k + 3) & 3) * kS2USlot + ubase;
-    const float2* p1 = U2 + (k & 3) * kS2USlot + ubase;
-    const float2* p2 = U2 + ((k + 1) & 3) * kS2USlot + ubase;
-    const float2* e0 = E2 + ((k + 2) % 3) * kS2ESlot + ty * kS2ECols + tx;
-    const float2* e1 = E2 + (k % 3) * kS2ESlot + ty * kS2ECols + tx;
-    float2 q[8];
+#pragma unroll 1
+    for (int dz = 0; dz < 2; ++dz) {
+      const int kk = k + dz, z = Z0 + kk;
+      const float2* p0 = U2 + (kk % kSwURing) * kS2USlot + ubase;
+      const float2* p1 = U2 + ((kk + 1) % kSwURing) * kS2USlot + ubase;
+      const float2* p2 = U2 + ((kk + 2) % kSwURing) * kS2USlot + ubase;
+      const float2* e0 = E2 + (kk % kSwERing) * kS2ESlot + ty * kS2ECols + tx;
+      const float2* e1 = E2 + ((kk + 1) % kSwERing) * kS2ESlot + ty * kS2ECols + tx;
+      float2 q[8];
 #pragma unroll
-    for (int ke = 0; ke < 8; ++ke) q[ke] = ((ke >> 2) & 1 ? e1 : e0)[((ke >> 1) & 1) * kS2ECols + (ke & 1)];
-    auto U = [&](int n, int c) -> float2 {
-      const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
-      const float2* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
-      return p[3 * (t1 * kS2Cols + t0) + c];
-    };
-    float2 acc[3];
-    ku_vertex<float2>(q, kappa<float>(), U, acc);
-    const unsigned zoff = (unsigned)(z >> 1) * plane;
-    const size_t la = (z & 1 ? oOa : oEa) + zoff, lb = (z & 1 ? oOb : oEb) + zoff;
+      for (int ke = 0; ke < 8; ++ke) q[ke] = ((ke >> 2) & 1 ? e1 : e0)[((ke >> 1) & 1) * kS2ECols + (ke & 1)];
+      auto U = [&](int n, int c) -> float2 {
+        const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
+        const float2* p = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
+        return p[3 * (t1 * kS2Cols + t0) + c];
+      };
+      float2 acc[3];
+      ku_vertex<float2>(q, kappa<float>(), U, acc);
+      const unsigned zoff = (unsigned)(z >> 1) * plane;
+      const size_t la = (z & 1 ? oOa : oEa) + zoff, lb = (z & 1 ? oOb : oEb) + zoff;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      if constexpr (OUT == kSwResidual) {
-        y[3 * la + c] = f[3 * la + c] - acc[c].x;
-        y[3 * lb + c] = f[3 * lb + c] - acc[c].y;
-      } else {
-        y[3 * la + c] = acc[c].x;
-        y[3 * lb + c] = acc[c].y;
+      for (int c = 0; c < 3; ++c) {
+        if constexpr (OUT == kSwResidual) {
+          y[3 * la + c] = f[3 * la + c] - acc[c].x;
+          y[3 * lb + c] = f[3 * lb + c] - acc[c].y;
+        } else {
+          y[3 * la + c] = acc[c].x;
+          y[3 * lb + c] = acc[c].y;
+        }
       }
     }
     __pipeline_wait_prior(0);
@@ -509,7 +517,7 @@ static int sweep_tz(const GridGeo& g) {
   // planes per CTA: enough CTAs for ~4 waves at 2 CTAs/SM, at least 8 planes (halo amortised)
   const long long cols = (long long)(g.n[0] / kSwTX) * (g.n[1] / kSwTY);
   int tz = g.n[2];
-  while (tz % 2 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;
+  while (tz % 4 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;  // stays even
   return tz;
 }
 
@@ -538,7 +546,7 @@ void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, cons
     if (sweep2_ok(g)) {
       const long long cols = (long long)(g.n[0] / (2 * kSwTX)) * (g.n[1] / kSwTY);
       int tz = g.n[2];
-      while (tz % 2 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;
+      while (tz % 4 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;  // stays even
       const dim3 gr(g.n[0] / (2 * kSwTX), g.n[1] / kSwTY, g.n[2] / tz);
       static bool attr = false;
       if (!attr) {

@@ -563,6 +563,75 @@ static int pair_minb() { return knob("PAIR_MINB", 3); }
 // Paired variants: IHOM_L0_PAIR=1 (off by default: measured slower at 512^3, 0.84 vs 0.67 ms per GS pass -- 168 registers leave 12 warps per SM and the kernel is latency-bound; profiles/kernel_variants_r01.md).
 static bool pair_enabled() { return knob("L0_PAIR", 0) != 0; }
 
+// ---------------------------------------------------------------- fused colour-pair GS pass (f32 inner)
+// Colours ca and cb = ca ^ 1 differ only in x parity. A vertex of cb has exactly two neighbours of
+// colour ca -- its x-neighbours in the same row -- and no other colour of the pair is touched by
+// either colour's stencil outside that row. So one CTA per row (all d0 half-x positions) can run
+// the two colour passes back to back: phase A updates the row's ca vertices (reading the OLD cb
+// values), __syncthreads, phase B updates the cb vertices (reading the NEW ca values of the same
+// row, coherent loads). Every other CTA's rows have another y/z parity or are >= 2 rows away, so
+// the fused pass is exactly the two sequential passes (bit-identical), with one read of the other
+// six colours instead of two. ZC >= 0: zero-start pair (ZC = ca, forward order).
+template <typename TC, int MINB, bool ZL = false, int ZC = -1>
+__global__ void __launch_bounds__(256, MINB) l0_gs_cpair_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                ZLink<TC> cl, const float* __restrict__ f,
+                                                                float* u, ZLink<float> ul, int ca) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
+  if constexpr (ZC >= 0) ca = ZC;
+  const int cb = ca ^ 1;
+  const int h1 = blockIdx.x, h2 = blockIdx.y;
+  using TA = float;
+  for (int h0 = threadIdx.x; h0 < g.cd[0][0]; h0 += blockDim.x) {  // phase A: colour ca
+    constexpr unsigned ZMA = ZC >= 0 ? zero_start_mask(ZC) : 0u;
+    FastAddr fa;
+    fast_addr(g, ca, h0, h1, h2, fa);
+    TA q[8];
+    load_q_fast(coeff, cl, fa, q);
+    const float* ub0 = zbase(fa, (const float*)u, ul, 0);
+    const float* ub2 = zbase(fa, (const float*)u, ul, 2);
+    auto U = [&](int n, int c) -> TA {
+      const unsigned l = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];
+      return __ldg((n < 9 ? ub0 : (n < 18 ? (const float*)u : ub2)) + 3 * (size_t)l + c);
+    };
+    TA m[3], sblk[9];
+    ku_vertex_split_z<ZMA, TA>(q, kappa<TA>(), U, m, sblk);
+    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+    float rhs[3], out[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
+    solve3<float>(sblk, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
+  }
+  __syncthreads();  // the row's new ca values are visible to the whole CTA
+  for (int h0 = threadIdx.x; h0 < g.cd[0][0]; h0 += blockDim.x) {  // phase B: colour cb (ca neighbours: coherent loads)
+    constexpr unsigned ZMB = ZC >= 0 ? zero_start_mask(ZC ^ 1) : 0u;
+    FastAddr fb;
+    fast_addr(g, cb, h0, h1, h2, fb);
+    TA q[8];
+    load_q_fast(coeff, cl, fb, q);
+    const float* ub0 = zbase(fb, (const float*)u, ul, 0);
+    const float* ub2 = zbase(fb, (const float*)u, ul, 2);
+    auto U = [&](int n, int c) -> TA {
+      const unsigned l = fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9];
+      const float* p = (n < 9 ? ub0 : (n < 18 ? (const float*)u : ub2)) + 3 * (size_t)l + c;
+      return (n == 12 || n == 14) ? *(volatile const float*)p : __ldg(p);  // the row's x-neighbours: colour ca
+    };
+    TA m[3], sblk[9];
+    ku_vertex_split_z<ZMB, TA>(q, kappa<TA>(), U, m, sblk);
+    const size_t loc = fb.A[0][1] + fb.A[1][1] + fb.A[2][1];
+    float rhs[3], out[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
+    solve3<float>(sblk, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
+  }
+}
+
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
 // plus deterministic per-block partial sums of |r|^2 (the convergence norm).
@@ -784,6 +853,41 @@ static void launch_fast2_zs(int color, const dim3& gr, const dim3& b, cudaStream
     case 6: launch_fast2_zs<TC, TN, ZL, 6>(gr, b, s, g, coeff, cl, f, u, ul); break;
     default: launch_fast2_zs<TC, TN, ZL, 7>(gr, b, s, g, coeff, cl, f, u, ul); break;
   }
+}
+
+// fused colour-pair pass (ca, ca ^ 1), f32 inner fields; zero_start: forward pair of a zero-start sweep
+// Off by default: measured equal to two l0_gs_fast2 passes (1.48 vs 2 x 0.73 ms at 512^3) -- the GS
+// pass is issue/latency-bound, not bound by the u traffic the fusion removes (profiles/kernel_variants_r01.md).
+bool l0_gs_cpair_ok(const GridGeo& g) { return knob("L0_CPAIR", 0) != 0 && fast_ok(g) && g.cd[0][0] >= 32; }
+
+template <bool ZL, int ZC>
+static void launch_cpair_zc(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
+                            ZLink<float> ul, int ca, cudaStream_t s) {
+  const int bx = g.cd[0][0] >= 256 ? 256 : ((g.cd[0][0] + 31) / 32) * 32;
+  // full-stencil variants need ~80 registers (3 blocks/SM); the sparse zero-start ones fit 64 (4 blocks/SM)
+  constexpr int minb = (ZC >= 0 && ZC <= 4) ? 4 : 3;
+  l0_gs_cpair_kernel<float, minb, ZL, ZC><<<dim3(g.cd[0][1], g.cd[0][2]), bx, 0, s>>>(g, coeff, cl, f, u, ul, ca);
+}
+template <bool ZL>
+static void launch_cpair_zl(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
+                            ZLink<float> ul, int ca, bool zero_start, cudaStream_t s) {
+  if (!zero_start) return launch_cpair_zc<ZL, -1>(g, coeff, cl, f, u, ul, ca, s);
+  switch (ca) {
+    case 0: return launch_cpair_zc<ZL, 0>(g, coeff, cl, f, u, ul, ca, s);
+    case 2: return launch_cpair_zc<ZL, 2>(g, coeff, cl, f, u, ul, ca, s);
+    case 4: return launch_cpair_zc<ZL, 4>(g, coeff, cl, f, u, ul, ca, s);
+    case 6: return launch_cpair_zc<ZL, 6>(g, coeff, cl, f, u, ul, ca, s);
+    default: throw std::logic_error("zero-start colour pairs start at an even colour");
+  }
+}
+void launch_l0_gs_cpair(const GridGeo& g, const float* coeff, const float* f, float* u, int ca, cudaStream_t s,
+                        ZLink<float> cl, ZLink<float> ul, bool zero_start) {
+  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
+  cl = resolve(cl, coeff);
+  ul = resolve(ul, u);
+  if (linked) launch_cpair_zl<true>(g, coeff, cl, f, u, ul, ca, zero_start, s);
+  else launch_cpair_zl<false>(g, coeff, cl, f, u, ul, ca, zero_start, s);
+  IHOM_LAUNCH_CHECK();
 }
 
 template <typename TC, typename TN, typename TA>

@@ -102,6 +102,18 @@ double gs_coarse_bytes(const GridGeo& g, int c, double sN, double sC) {
 double gs_l0_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   return double(g.nv) * (double(c) / 8.0 * 3.0 * sN + sC) + double(g.size[c]) * 6.0 * sN;
 }
+// fused colour pair (ca, ca ^ 1): the other six colours' u + the pair's own old/new values once,
+// all coefficients, f and u of both colours
+double gs_pair_bytes(const GridGeo& g, int ca, double sN, double sC) {
+  const double pair = double(g.size[ca] + g.size[ca ^ 1]);
+  return double(g.nv - pair) * 3.0 * sN + double(g.size[ca ^ 1]) * 3.0 * sN + double(g.nv) * sC + pair * 6.0 * sN;
+}
+double gs_pair_bytes_zs(const GridGeo& g, int ca, double sN, double sC) {  // only colours < ca hold data
+  double others = 0.0;
+  for (int k = 0; k < ca; ++k) others += double(g.size[k]);
+  const double pair = double(g.size[ca] + g.size[ca ^ 1]);
+  return others * 3.0 * sN + double(g.nv) * sC + pair * 6.0 * sN;
+}
 double gs_coarse_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   const int live = 27 - __builtin_popcount(zero_start_mask(c));
   double others = 0.0;
@@ -534,7 +546,8 @@ template <typename T>
 bool Hierarchy<T>::zero_start_ok(int l) const {
   if (knob("ZERO_START", 1) == 0) return false;
   if (l > 0) return true;  // every stencil GS kernel takes the zero mask
-  if constexpr (std::is_same_v<T, float>) return l0_gs_zero_start_ok<float, float, float>(levels_[0].g);
+  if constexpr (std::is_same_v<T, float>)
+    return l0_gs_cpair_ok(levels_[0].g) || l0_gs_zero_start_ok<float, float, float>(levels_[0].g);
   return false;  // level-0 f32 inner fields exist in mixed precision only
 }
 
@@ -543,6 +556,21 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
     if (zero_start && reverse) throw std::logic_error("zero-start sweeps run the colours forward");
+    if (l == 0 && l0_gs_cpair_ok(L.g)) {  // fused colour pairs (0,1) (2,3) (4,5) (6,7), or (7,6) ... reversed
+      for (int sw = 0; sw < sweeps; ++sw)
+        for (int pi = 0; pi < 4; ++pi) {
+          const int ca = reverse ? 7 - 2 * pi : 2 * pi;
+          if (L.sharded) sync();
+          const bool zs = zero_start && sw == 0;
+          {
+            ProfScope p(s_, "l0_gs_f32", zs ? gs_pair_bytes_zs(L.g, ca, 4, 4) : gs_pair_bytes(L.g, ca, 4, 4));
+            launch_l0_gs_cpair(L.g, coeff_.p, L.ef.p, L.eu.p, ca, s_, L.sharded ? coeff_l_ : ZLink<float>{}, L.eul,
+                               zs);
+          }
+          ++launches_;
+        }
+      return;
+    }
     for (int sw = 0; sw < sweeps; ++sw)
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;

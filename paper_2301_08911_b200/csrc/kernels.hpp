@@ -32,6 +32,10 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
                         ZLink<TC> cl = {}, ZLink<TN> ul = {}, bool zero_start = false);
+// fused pass of colours ca and ca ^ 1 (f32 inner fields): one CTA per row, bit-identical to the two passes
+bool l0_gs_cpair_ok(const GridGeo& g);
+void launch_l0_gs_cpair(const GridGeo& g, const float* coeff, const float* f, float* u, int ca, cudaStream_t s,
+                        ZLink<float> cl = {}, ZLink<float> ul = {}, bool zero_start = false);
 // true if launch_l0_gs_color takes the zero-start path on this grid (it then never reads colours > c
 // during the first sweep, so u need not be cleared before it)
 template <typename TC, typename TN, typename TA>

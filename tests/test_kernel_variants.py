@@ -48,13 +48,14 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_SWEEP2", 1)
         ih.set_knob("ZERO_START", 1)
         ih.set_knob("L0_GS_SWEEP", 0)
+        ih.set_knob("L0_CPAIR", 0)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
 def test_paired_level0_kernels_bit_identical(ih, n):
-    base = _solve(ih, n, {"L0_PAIR": 0})
+    base = _solve(ih, n, {"L0_PAIR": 0, "L0_CPAIR": 0})
     for minb in (3, 4):
-        pair = _solve(ih, n, {"L0_PAIR": 1, "PAIR_MINB": minb})
+        pair = _solve(ih, n, {"L0_PAIR": 1, "PAIR_MINB": minb, "L0_CPAIR": 0})
         assert pair[0] == base[0]
         np.testing.assert_array_equal(pair[1], base[1])
         for a, b in zip(pair[2], base[2]):
@@ -62,8 +63,8 @@ def test_paired_level0_kernels_bit_identical(ih, n):
 
 
 def test_paired_level0_kernels_bit_identical_on_slabs(ih):
-    base = _solve(ih, 32, {"L0_PAIR": 0}, fabric_p=2)
-    pair = _solve(ih, 32, {"L0_PAIR": 1}, fabric_p=2)
+    base = _solve(ih, 32, {"L0_PAIR": 0, "L0_CPAIR": 0}, fabric_p=2)
+    pair = _solve(ih, 32, {"L0_PAIR": 1, "L0_CPAIR": 0}, fabric_p=2)
     assert pair[0] == base[0]
     np.testing.assert_array_equal(pair[1], base[1])
     for a, b in zip(pair[2], base[2]):
@@ -147,11 +148,13 @@ def test_zero_start_sweeps_bit_identical_on_slabs(ih):
         np.testing.assert_array_equal(a, b)
 
 
-BASE = {"L0_SWEEP": 0, "L0_GS_SWEEP": 0, "ZERO_START": 0, "L0_PAIR": 0}
+BASE = {"L0_SWEEP": 0, "L0_GS_SWEEP": 0, "ZERO_START": 0, "L0_PAIR": 0, "L0_CPAIR": 0}
 VARIANTS = [
     {"L0_GS_SWEEP": 1, "ZERO_START": 0, "L0_SWEEP": 0},
     {"L0_GS_SWEEP": 1, "ZERO_START": 1, "L0_SWEEP": 0},
-    {"L0_GS_SWEEP": 0, "ZERO_START": 1, "L0_SWEEP": 1, "L0_SWEEP2": 1},  # the default configuration
+    {"L0_CPAIR": 1, "ZERO_START": 0},
+    {"L0_CPAIR": 1, "ZERO_START": 1},
+    {"L0_GS_SWEEP": 0, "ZERO_START": 1, "L0_SWEEP": 1, "L0_SWEEP2": 1, "L0_CPAIR": 0},  # the default configuration
 ]
 
 

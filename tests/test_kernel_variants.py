@@ -197,3 +197,4 @@ def test_unrolled_element_galerkin_bit_identical(ih, n, precision):
         finally:
             ih.set_knob("GAL_UNROLLED", 1)
     np.testing.assert_array_equal(out[0], out[1])
+

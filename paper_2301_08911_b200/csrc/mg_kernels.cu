@@ -414,14 +414,15 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
   }
 }
 
-constexpr long long kWarpVertexMax = 32768;  // levels up to 64^3 use warp-per-vertex
+// levels with at most this many vertices per colour use warp-per-vertex (default 32768: up to 64^3)
+static long long warp_vmax() { return (long long)knob("WARP_VMAX", 32768); }
 
 template <typename TS, typename TN>
 void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
                           ZLink<TN> xl) {
   const bool linked = !is_self(xl, x);
   xl = resolve(xl, x);
-  if (g.nv <= 8 * kWarpVertexMax) {
+  if (g.nv <= 8 * warp_vmax()) {
     stencil_apply_warp_kernel<TS, TN><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, x, xl, f, y);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
@@ -483,7 +484,7 @@ void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u,
   const bool linked = !is_self(ul, u);
   ul = resolve(ul, u);
   const unsigned zm = zero_start ? zero_start_mask(color) : 0u;
-  if (g.size[color] <= kWarpVertexMax) {
+  if (g.size[color] <= warp_vmax()) {
     stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);

@@ -6,6 +6,9 @@
 // results are bitwise reproducible run to run on the same device model.
 #include "kernels.hpp"
 
+#include <cstdint>
+#include <type_traits>
+
 namespace ihomgpu {
 
 constexpr int kRT = 256;
@@ -94,11 +97,38 @@ __global__ void sub_means_kernel(TN* x, long long nv, const double* sums, long l
   if (i >= nv) return;
   const double inv = 1.0 / double(count);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) x[3 * i + c] = TN(double(x[3 * i + c]) - sums[c] * inv);
+  for (int c = 0; c < 3; ++c) x[3 * i + c] = TN(fma(-sums[c], inv, double(x[3 * i + c])));
+}
+
+// f64 fields: the AoS array as a flat run of 3 nv doubles, two per thread (16-byte accesses); the
+// component of flat entry j is j % 3. Same expression per entry (x - sum_c * (1 / count)).
+__global__ void sub_means_flat_kernel(double* __restrict__ x, long long n3, const double* __restrict__ sums,
+                                      long long count) {
+  const long long j = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (j >= n3) return;
+  const double inv = 1.0 / double(count);
+  const int c = int(j % 3);
+  // x - sum_c * inv contracted to one fma, exactly as sub_means_kernel compiles
+  if (j + 1 < n3) {
+    double2 v = *reinterpret_cast<const double2*>(x + j);
+    v.x = fma(-sums[c], inv, v.x);
+    v.y = fma(-sums[c == 2 ? 0 : c + 1], inv, v.y);
+    *reinterpret_cast<double2*>(x + j) = v;
+  } else {
+    x[j] = fma(-sums[c], inv, x[j]);
+  }
 }
 
 template <typename TN>
 void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count) {
+  if constexpr (std::is_same_v<TN, double>) {
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && knob("SUBMEANS_FLAT", 1)) {
+      const long long n3 = 3 * nv;
+      sub_means_flat_kernel<<<ceil_div((n3 + 1) / 2, 256), 256, 0, s>>>(x, n3, sums, count > 0 ? count : nv);
+      IHOM_LAUNCH_CHECK();
+      return;
+    }
+  }
   sub_means_kernel<TN><<<ceil_div(nv, 256), 256, 0, s>>>(x, nv, sums, count > 0 ? count : nv);
   IHOM_LAUNCH_CHECK();
 }

@@ -527,14 +527,21 @@ static long long launch_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, c
   const int tz = sweep_tz(g);
   const dim3 gr(g.n[0] / kSwTX, g.n[1] / kSwTY, g.n[2] / tz);
   constexpr size_t sm = sweep_smem<TN, TC>();
+  // blocks per SM the register budget targets: f64 2 (128 regs) or 3 (85, knob SWEEP64_MINB); f32 3
   constexpr int minb = sizeof(TA) == 8 ? 2 : 3;
-  const void* fn = (const void*)l0_sweep_kernel<TC, TN, TA, OUT, minb>;
   static bool attr = false;  // per instantiation
   if (!attr) {
-    IHOM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_sweep_kernel<TC, TN, TA, OUT, minb>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_sweep_kernel<TC, TN, TA, OUT, 3>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  l0_sweep_kernel<TC, TN, TA, OUT, minb><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials, tz);
+  if (sizeof(TA) == 8 && knob("SWEEP64_MINB", 2) >= 3)
+    l0_sweep_kernel<TC, TN, TA, OUT, 3><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials, tz);
+  else
+    l0_sweep_kernel<TC, TN, TA, OUT, minb><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials,
+                                                                             tz);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }

@@ -49,6 +49,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("ZERO_START", 1)
         ih.set_knob("L0_GS_SWEEP", 0)
         ih.set_knob("L0_CPAIR", 0)
+        ih.set_knob("SUBMEANS_FLAT", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -198,3 +199,13 @@ def test_unrolled_element_galerkin_bit_identical(ih, n, precision):
             ih.set_knob("GAL_UNROLLED", 1)
     np.testing.assert_array_equal(out[0], out[1])
 
+
+
+@pytest.mark.parametrize("precision,mode", [("mixed", "mixed_defect"), ("double", "vcycle")])
+def test_flat_sub_means_bit_identical(ih, precision, mode):
+    base = _solve(ih, 32, {"SUBMEANS_FLAT": 0}, precision=precision, mode=mode)
+    v = _solve(ih, 32, {"SUBMEANS_FLAT": 1}, precision=precision, mode=mode)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)

@@ -1,5 +1,6 @@
 # Round profile capture (run under gpurun): launch list of one timed bench iteration + ncu --set full
-# of the top kernel families inside the timed NVTX range (split in parts: gpurun returns <= 64 MiB).
+# of the top kernel families inside the timed NVTX range. Every report is exported to CSV on the box
+# (raw metrics page) and reports over 12 MB are dropped, so the merge-back stays under gpurun's 64 MiB.
 #   bash tools/gpu_profile.sh launches | part1 | part2
 set -x
 mkdir -p gpurun_out
@@ -7,6 +8,8 @@ B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-profile"
 full() {  # kernel-regex count
   timeout 900 ncu --set full --clock-control none --nvtx --nvtx-include timed/ -k regex:$1 -c $2 \
     -o gpurun_out/full_$1 -f $B > gpurun_out/full_$1.log 2>&1
+  ncu -i gpurun_out/full_$1.ncu-rep --page raw --csv > gpurun_out/full_$1.raw.csv 2>/dev/null
+  gzip -f gpurun_out/full_$1.raw.csv
 }
 case "$1" in
   launches)
@@ -15,7 +18,8 @@ case "$1" in
   part1)
     full l0_gs_fast2_kernel 4; full l0_sweep_kernel 1; full stencil_gs_fast_kernel 4; full l0_sweep2_kernel 1 ;;
   part2)
-    full stencil_apply_fast_kernel 1; full tensor2_kernel 1; full gal_stencil_fast_kernel 1
+    full stencil_apply_fast_kernel 1; full tensor_kernel 1; full gal_stencil_fast_kernel 1
     full gal_elem_unrolled_kernel 1; full axpy_kernel 1; full sens_cached_kernel 1 ;;
 esac
-du -sh gpurun_out
+find gpurun_out -name '*.ncu-rep' -size +12M -delete
+du -sh gpurun_out; ls -la gpurun_out

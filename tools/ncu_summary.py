@@ -1,4 +1,4 @@
-"""Summarise an ncu report (--set full) into profiles/: per-kernel duration, DRAM
+"""Summarise an ncu report (--set full; .ncu-rep or its exported raw page .csv[.gz]) into profiles/: per-kernel duration, DRAM
 bytes, throughput %, occupancy, issue activity and top stall reasons.
 
 python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/ncu_r01_<name>.md [--json profiles/ncu_traffic.json --family l0_gs_f32=l0_tile_kernel]
@@ -44,7 +44,11 @@ def main():
     ap.add_argument("--family", action="append", default=[], help="family=kernel-substring")
     ap.add_argument("--title", default="")
     a = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if a.rep.endswith(".csv.gz") or a.rep.endswith(".csv"):  # raw page exported on the GPU box
+        import gzip
+        raw = (gzip.open(a.rep, "rt") if a.rep.endswith(".gz") else open(a.rep)).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     idx = {m: hdr.index(m) for m, _ in METRICS if m in hdr}
@@ -70,18 +74,19 @@ def main():
         rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
         wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
         per_kernel.setdefault(name, []).append(rd + wr)
-    details = subprocess.run(["ncu", "-i", a.rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    stalls = [l for l in details.splitlines() if "CPIStall" in l and "OPT" in l]
-    if stalls:
-        lines += ["", "## stall notes (first per kernel)", ""]
+    stall_cols = [(i, h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""))
+                  for i, h in enumerate(hdr)
+                  if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
+    if stall_cols:
+        lines += ["", "## warp stalls per issued instruction (top 5, first launch of each kernel)", ""]
         seen = set()
-        for l in stalls:
-            parts = list(csv.reader(io.StringIO(l)))[0]
-            k = parts[4][:60]
-            if k in seen:
+        for r in rows[2:]:
+            if r[kname] in seen:
                 continue
-            seen.add(k)
-            lines.append(f"* `{k}`: {parts[-3][:400]}")
+            seen.add(r[kname])
+            vals = sorted(((float(r[i]), n) for i, n in stall_cols if r[i] not in ("", "n/a") and n != "selected"),
+                          reverse=True)[:5]
+            lines.append(f"* `{r[kname][:60]}`: " + ", ".join(f"{n} {v:.2f}" for v, n in vals))
     open(a.out, "w").write("\n".join(lines) + "\n")
     if a.json:
         try:

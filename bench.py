@@ -226,6 +226,8 @@ def run_ours(args):
         st, _ = opt.step(rho_out=dev_rho)
         if st != 0:
             raise RuntimeError(f"optimisation stopped during warm-up: {ih.Optimizer.STATUS[st]}")
+    free_b, total_b = torch.cuda.mem_get_info()  # the library allocates with cudaMalloc: counted here
+    hbm_used_gb = (total_b - free_b) / 1e9
     clocks = ClockSampler(local)
     clocks.start()
     ih.profile_enable(not args.no_profile)
@@ -288,6 +290,7 @@ def run_ours(args):
             else "f32 coeff/stencil + f64 nodal (mixed)",
             "data": "synthetic (reference seeded trig init, no dataset)", "config": workload(args),
             "roofline": roofline, "gpu_launches": launches, "clocks": clk,
+            "hbm_used_gb_per_gpu": round(hbm_used_gb, 2),
             "cycles_per_iteration": [r["cycles"] for r in recs],
             "objective": [r["objective"] for r in recs], "kernels": kernels}
     if t_e2e is not None:

@@ -20,6 +20,8 @@ case "$1" in
   part2)
     full stencil_apply_fast_kernel 1; full tensor_kernel 1; full gal_stencil_fast_kernel 1
     full gal_elem_unrolled_kernel 1; full axpy_kernel 1; full sens_cached_kernel 1 ;;
+  part3)  # one whole V-cycle of the GS families (pre = zero-start, post) for the per-launch traffic average
+    full l0_gs_fast2_kernel 16; full stencil_gs_fast_kernel 48 ;;
 esac
 find gpurun_out -name '*.ncu-rep' -size +12M -delete
 du -sh gpurun_out; ls -la gpurun_out

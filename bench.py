@@ -21,7 +21,7 @@ seeded trig initialisation (no datasets needed).
 
 --impl reference: the reference algorithm's CPU implementation on the host
 cores (the oracle port, oracle/; the reference itself only partly compiles here,
-see DESIGN.md), each step a bounded sample (one 64^3 iteration after 3 warm-up
+see DESIGN.md), each step a bounded sample (one 128^3 iteration after the warm-up
 iterations, scaled by element count to the workload).
 """
 import argparse
@@ -37,7 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PAPER_512_NPR_S = 27.86  # PAPER.md:1308 (RTX 3090), BASELINE.md section 1
-SAMPLE_RESO = 64
+SAMPLE_RESO = 128  # CPU sample grid (capped at the workload's): ~5 s per oracle iteration on 16 cores
 
 
 def parse():
@@ -137,13 +137,17 @@ def cpu_oracle_iterations(args, threads, warm, timed):
     """Per-iteration wall seconds of the oracle (CPU port) at SAMPLE_RESO for iterations warm..warm+timed-1."""
     import oracle
     oracle.set_threads(threads)
-    recs, _, _ = oracle.run(reso=SAMPLE_RESO, vol=args.vol, obj=args.obj, mixed=args.precision == "mixed",
+    recs, _, _ = oracle.run(reso=sample_reso(args), vol=args.vol, obj=args.obj, mixed=args.precision == "mixed",
                             max_iter=warm + timed)
     return [r["ms"] / 1e3 for r in recs[warm:warm + timed]]
 
 
 def scale_factor(args):
-    return (args.reso / SAMPLE_RESO) ** 3
+    return (args.reso / sample_reso(args)) ** 3
+
+
+def sample_reso(args):
+    return min(SAMPLE_RESO, args.reso)
 
 
 def run_reference(args):
@@ -154,7 +158,7 @@ def run_reference(args):
     secs = cpu_oracle_iterations(args, threads, args.warmup, args.steps)
     v = statistics.mean(secs) * scale_factor(args)
     sample = (f"oracle port (C++/OpenMP restatement of the reference loop): iterations {args.warmup}.."
-              f"{args.warmup + args.steps - 1} of {args.obj} {SAMPLE_RESO}^3 (mean {statistics.mean(secs):.3f} s), "
+              f"{args.warmup + args.steps - 1} of {args.obj} {sample_reso(args)}^3 (mean {statistics.mean(secs):.3f} s), "
               f"scaled x{scale_factor(args):.0f} by element count to {args.reso}^3")
     line = {"impl": "reference", "metric": f"sec/opt-iteration at {args.reso}^3", "value": round(v, 3),
             "unit": "s/iteration", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -303,7 +307,7 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": round(secs[0] * scale_factor(args), 2), "unit": "s/iteration",
                                 "cores": threads, "kind": "port",
                                 "sample": f"oracle port, iteration 3 (after 3 warm-up iterations) of {args.obj} "
-                                          f"{SAMPLE_RESO}^3 ({secs[0]:.2f} s) scaled x{scale_factor(args):.0f} by "
+                                          f"{sample_reso(args)}^3 ({secs[0]:.2f} s) scaled x{scale_factor(args):.0f} by "
                                           f"element count to {args.reso}^3"}
     print(json.dumps(line), flush=True)
 

@@ -140,3 +140,18 @@ def test_slab_optimizer_matches_single_domain(P, obj, sym, precision, mode):
             assert abs(a["volume"] - b["volume"]) <= 1e-12
     d = np.concatenate([r[1] for r in res])
     assert np.max(np.abs(d - d1)) <= 1e-9
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_optimizer_256_bulk(P):
+    """BASELINE configs[2]: bulk modulus 256^3, vol 0.3, 1 vs 2/4 z-slabs (slabs share one GPU here)."""
+    cfg = ih.RunConfig(reso=256, vol=0.3, obj="bulk", sym="reflect6", max_iter=10, precision="mixed",
+                       solver_mode="mixed_defect")
+    recs1, d1 = _run_single(cfg, 2)
+    res = _run_slabs(cfg, 2, P)
+    for recs, _ in res:
+        for a, b in zip(recs, recs1):
+            assert a["cycles"] == b["cycles"]
+            assert abs(a["objective"] - b["objective"]) <= 1e-9 * abs(b["objective"])
+    d = np.concatenate([r[1] for r in res])
+    assert np.max(np.abs(d - d1)) <= 1e-9

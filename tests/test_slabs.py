@@ -154,4 +154,6 @@ def test_slab_optimizer_256_bulk(P):
             assert a["cycles"] == b["cycles"]
             assert abs(a["objective"] - b["objective"]) <= 1e-9 * abs(b["objective"])
     d = np.concatenate([r[1] for r in res])
-    assert np.max(np.abs(d - d1)) <= 1e-9
+    # the cross-slab sums (norms, C^H, OC means) fold in another order: the OC multiplier, and with it
+    # every density, moves at the 1e-9 level per iteration on 16.7M elements
+    assert np.max(np.abs(d - d1)) <= 1e-7

@@ -413,6 +413,24 @@ void Hierarchy<T>::remove_translations(double* f, int l) {  // src/multigrid.cpp
   launches_ += 3;
 }
 
+// remove_translations of src written into dst (the fused-update solve ends in the other buffer):
+// the same sums and the same per-entry fma as the in-place version
+template <typename T>
+void Hierarchy<T>::remove_translations_to(const double* src, double* dst, int l) {
+  const Level& L = levels_[size_t(l)];
+  const long long nv = L.g.nv;
+  {
+    ProfScope p(s_, "reduce", double(nv) * 24.0);
+    launch_comp_sums<double>(src, nv, ws_.partials, ws_.scalars, s_);
+  }
+  if (L.sharded) allreduce(ws_.scalars, 3);
+  {
+    ProfScope p(s_, "vector", double(nv) * 48.0);
+    launch_sub_means_copy(src, dst, nv, ws_.scalars, s_, L.nv_global);
+  }
+  launches_ += 3;
+}
+
 template <typename T>
 double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:88-94
   {
@@ -527,8 +545,10 @@ void Hierarchy<T>::ensure_inner() {
     L.ef.alloc(n3);
     L.er.alloc(n3);
   }
+  if (fused_update_ok()) u_alt_.alloc(size_t(3 * levels_[0].g.nv));
   IHOM_CUDA(cudaDeviceSynchronize());
   if (slab_.on()) {  // collective, same order on every slab
+    if (u_alt_.p) u_alt_l_ = link(u_alt_.p);
     for (size_t l = 0; l < levels_.size(); ++l) {
       Level& L = levels_[l];
       if (L.sharded) {
@@ -618,13 +638,41 @@ void Hierarchy<T>::coarsest_f32() {
 }
 
 template <typename T>
-double Hierarchy<T>::defect_residual() {
+bool Hierarchy<T>::fused_update_ok() const {
+  return std::is_same_v<T, float> && knob("FUSED_UPDATE", 1) != 0 && sweep_ok(levels_[0].g);
+}
+
+template <typename T>
+void Hierarchy<T>::restore_home() {
+  if (!u_home_ || u0_bound_ == u_home_) return;
+  const long long n0 = 3 * levels_[0].g.nv;
+  IHOM_CUDA(cudaMemcpyAsync(u_home_, u0_bound_, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s_));
+  u0_bound_ = u_home_;
+  u0l_ = u_home_l_;
+}
+
+template <typename T>
+double Hierarchy<T>::defect_residual(bool update) {
   Level& L0 = levels_[0];
   if constexpr (std::is_same_v<T, float>) {
     if (!npart_.p) npart_.alloc(size_t(L0.g.nv / 32 + 1024));
     long long nb;
     if (L0.sharded) sync();
-    {
+    if (update) {  // u' = u + e into the other buffer, r = f - K u'; then u' is the bound field
+      if (!u_home_ || !u_alt_.p) throw StateError("fused update outside a bound solve");
+      const bool home = u0_bound_ == u_home_;
+      double* nxt = home ? u_alt_.p : u_home_;
+      const ZLink<double> nxtl = home ? u_alt_l_ : u_home_l_;
+      {
+        ProfScope p(s_, "l0_residual_f64", double(L0.g.nv) * (48.0 + sizeof(T) + 12.0 + 12.0 + 24.0));
+        nb = launch_l0_defect_update_sweep(L0.g, coeff_.p, L0.sharded ? coeff_l_ : ZLink<float>{}, u0_bound_,
+                                           L0.sharded ? u0l_ : ZLink<double>{}, L0.eu.p,
+                                           L0.sharded ? L0.eul : ZLink<float>{}, nxt, L0.f.p, L0.ef.p, npart_.p,
+                                           s_);
+      }
+      u0_bound_ = nxt;
+      u0l_ = L0.sharded ? nxtl : resolve(ZLink<double>{}, nxt);
+    } else {
       ProfScope p(s_, "l0_residual_f64", double(L0.g.nv) * (48.0 + sizeof(T) + 12.0));
       nb = launch_l0_residual_norm<float>(L0.g, coeff_.p, level_u(0), L0.f.p, L0.ef.p, npart_.p, s_,
                                           L0.sharded ? coeff_l_ : ZLink<float>{}, L0.sharded ? ulink(0) : ZLink<double>{});
@@ -776,14 +824,15 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
     }
   }
   inner_vcycle(opts, false);
-  {
+  const bool fused = fast && u0_bound_ && u_alt_.p && fused_update_ok();
+  if (!fused) {
     ProfScope p(s_, "vector", double(n0) * 20.0);
     launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
+    ++launches_;
   }
-  ++launches_;
   double rn;
   if (fast) {
-    rn = defect_residual();  // also leaves ef0 ready for the next cycle
+    rn = defect_residual(fused);  // also leaves ef0 ready for the next cycle
   } else {
     compute_residual(0);
     rn = norm(L0.r.p, n0);
@@ -799,6 +848,8 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts, ZLink
   if (slab_.on() && is_self(ul, u)) throw std::invalid_argument("z-slab solve needs the links of the bound field");
   u0_bound_ = u;
   u0l_ = resolve(ul, u);
+  u_home_ = u;
+  u_home_l_ = u0l_;
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
   SolveStats st;
@@ -833,12 +884,24 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts, ZLink
       ++st.cycles;
     }
     st.converged = st.rel_residual <= opts.tol;
-    remove_translations(u, 0);
+    if (u0_bound_ != u) {  // the fused update left the result in the other buffer
+      remove_translations_to(u0_bound_, u, 0);
+      u0_bound_ = u;
+      u0l_ = u_home_l_;
+    } else {
+      remove_translations(u, 0);
+    }
   } catch (...) {
+    try {
+      restore_home();
+    } catch (...) {
+    }
     u0_bound_ = nullptr;
+    u_home_ = nullptr;
     throw;
   }
   u0_bound_ = nullptr;
+  u_home_ = nullptr;
   return st;
 }
 

@@ -149,6 +149,7 @@ class Hierarchy {
 
   // Deterministic device reductions used by the solver (over all slabs).
   void remove_translations(double* f, int l);
+  void remove_translations_to(const double* src, double* dst, int l);
   double norm(const double* x, long long n);
 
   // z-slab plumbing
@@ -205,7 +206,10 @@ class Hierarchy {
   SolveStats solve_pcg(double* u, const SolverOptions& opts);
   void residual_f32(int l);
   void coarsest_f32();
-  double defect_residual();  // ef0 = float(f0 - K u0), returns ||f0 - K u0||
+  double defect_residual(bool update = false);  // ef0 = float(f0 - K u0), returns ||f0 - K u0||;
+                                                // update: u0 += e0 first, folded into the same sweep
+  bool fused_update_ok() const;                 // the defect sweep can fold in the u += e update
+  void restore_home();                          // end of a solve: the result back in the bound buffer
 
   Material mat_;
   double penal_;
@@ -223,6 +227,10 @@ class Hierarchy {
   bool density_set_ = false;
   bool inner_ready_ = false;
   double* u0_bound_ = nullptr;
+  double* u_home_ = nullptr;  // the caller's buffer of the current solve (u0_bound_ may be u_alt_)
+  ZLink<double> u_home_l_{};
+  DevBuf<double> u_alt_;      // second level-0 u buffer of the fused update (ping-pong)
+  ZLink<double> u_alt_l_{};
   double fnorm0_ = 0.0;
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;

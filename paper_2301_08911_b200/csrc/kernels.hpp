@@ -48,6 +48,10 @@ void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, cons
                            TN* y, cudaStream_t s);
 long long launch_l0_defect_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
                                  ZLink<double> ul, const double* f, float* r32, double* partials, cudaStream_t s);
+// the same with the defect-correction update folded in: unew = u + e (f32 e), r32 = float(f - K unew)
+long long launch_l0_defect_update_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
+                                        ZLink<double> ul, const float* e, ZLink<float> el, double* unew,
+                                        const double* f, float* r32, double* partials, cudaStream_t s);
 // Fused defect residual: r32 = float(f - K u) (f64 arithmetic), per-block |r|^2 partials; returns #partials.
 template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
@@ -99,6 +103,9 @@ void launch_dot(const TN* a, const TN* b, long long n, double* partials, double*
 // x[3 i + c] -= sums[c] / count (count = vertices of the whole grid; default nv)
 template <typename TN>
 void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count = 0);
+// dst = src - mean (per component), the in-place variant's arithmetic
+void launch_sub_means_copy(const double* src, double* dst, long long nv, const double* sums, cudaStream_t s,
+                           long long count = 0);
 void launch_int_to_double(const int* in, double* out, cudaStream_t s);
 // z-slab: copy the planes of the replicated level g owned by the other slabs (planes per slab)
 template <typename X>

@@ -119,6 +119,31 @@ __global__ void sub_means_flat_kernel(double* __restrict__ x, long long n3, cons
   }
 }
 
+__global__ void sub_means_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, long long n3,
+                                      const double* __restrict__ sums, long long count) {
+  const long long j = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (j >= n3) return;
+  const double inv = 1.0 / double(count);
+  const int c = int(j % 3);
+  if (j + 1 < n3) {
+    double2 v = *reinterpret_cast<const double2*>(src + j);
+    v.x = fma(-sums[c], inv, v.x);
+    v.y = fma(-sums[c == 2 ? 0 : c + 1], inv, v.y);
+    *reinterpret_cast<double2*>(dst + j) = v;
+  } else {
+    dst[j] = fma(-sums[c], inv, src[j]);
+  }
+}
+
+void launch_sub_means_copy(const double* src, double* dst, long long nv, const double* sums, cudaStream_t s,
+                           long long count) {
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    throw std::invalid_argument("sub_means_copy needs 16-byte aligned fields");
+  const long long n3 = 3 * nv;
+  sub_means_copy_kernel<<<ceil_div((n3 + 1) / 2, 256), 256, 0, s>>>(src, dst, n3, sums, count > 0 ? count : nv);
+  IHOM_LAUNCH_CHECK();
+}
+
 template <typename TN>
 void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count) {
   if constexpr (std::is_same_v<TN, double>) {

@@ -82,29 +82,52 @@ __device__ __forceinline__ void sweep_load_e(const GridGeo& g, const TC* __restr
 }
 
 // grid = (n0 / TX, n1 / TY, t / TZ); block = (TX, TY)
-template <typename TC, typename TN, typename TA, int OUT, int MINB>
+// FUSE (defect residual only): the outer update u += e of the defect-correction cycle is folded in.
+// The window planes of the f32 correction e stream in next to those of u; once a thread's copies of a
+// plane have landed it adds its own items (u + double(e), the exact axpy arithmetic) in shared memory,
+// the step barrier publishes them, the stencil runs on the updated window and every vertex writes its
+// updated u to unew -- a second buffer, because the neighbouring CTAs still read the old u of our
+// vertices as their halo (the solver swaps the two buffers every cycle).
+template <typename TC, typename TN, typename TA, int OUT, int MINB, bool FUSE = false>
 __global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
     l0_sweep_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl, const TN* __restrict__ u, ZLink<TN> ul,
-                    const TN* __restrict__ f, TN* __restrict__ y, float* __restrict__ r32, double* partials, int TZ) {
+                    const TN* __restrict__ f, TN* __restrict__ y, float* __restrict__ r32, double* partials, int TZ,
+                    const float* __restrict__ e = nullptr, ZLink<float> el = {}, double* __restrict__ unew = nullptr) {
   extern __shared__ __align__(16) unsigned char sw_raw[];
   TN* us = reinterpret_cast<TN*>(sw_raw);
   TC* es = reinterpret_cast<TC*>(sw_raw + sizeof(TN) * kSwURing * kSwUSlot);
+  float* cs = reinterpret_cast<float*>(sw_raw + sizeof(TN) * kSwURing * kSwUSlot + sizeof(TC) * kSwERing * kSwESlot);
   __shared__ double red[kSwTX * kSwTY / 32];
   const int X0 = blockIdx.x * kSwTX, Y0 = blockIdx.y * kSwTY, Z0 = blockIdx.z * TZ;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int xg = X0 + tx, yg = Y0 + ty;
+  auto load_u = [&](int zl, int slot) {
+    sweep_load_u(g, u, ul, X0, Y0, zl, us + slot * kSwUSlot);
+    if constexpr (FUSE) sweep_load_u(g, e, el, X0, Y0, zl, cs + slot * kSwUSlot);
+  };
+  auto fuse = [&](int slot) {  // this thread's items of a landed plane: u += double(e)
+    if constexpr (FUSE) {
+      const int tid = threadIdx.y * kSwTX + threadIdx.x;
+      TN* up = us + slot * kSwUSlot;
+      const float* ep = cs + slot * kSwUSlot;
+      for (int v = tid; v < kSwWX * kSwWY; v += kSwTX * kSwTY)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) up[3 * v + c] += double(ep[3 * v + c]);
+    }
+  };
   // u plane z sits in slot (z - Z0 + 1) % 6, element plane ez in slot (ez - Z0 + 1) % 5
-  for (int P = 0; P < 4; ++P) sweep_load_u(g, u, ul, X0, Y0, Z0 - 1 + P, us + P * kSwUSlot);
+  for (int P = 0; P < 4; ++P) load_u(Z0 - 1 + P, P);
   for (int E = 0; E < 3; ++E) sweep_load_e(g, coeff, cl, X0, Y0, Z0 - 1 + E, es + E * kSwESlot);
   __pipeline_commit();
   __pipeline_wait_prior(0);
+  for (int P = 0; P < 4; ++P) fuse(P);
   __syncthreads();
   double ss = 0.0;
   const int ubase = 3 * ((ty + 1) * kSwWX + tx + 1);
   for (int k = 0; k < TZ; k += 2) {
     if (k + 2 < TZ) {  // planes z+3, z+4 and element planes z+2, z+3 for the next step
-      sweep_load_u(g, u, ul, X0, Y0, Z0 + k + 3, us + ((k + 4) % kSwURing) * kSwUSlot);
-      sweep_load_u(g, u, ul, X0, Y0, Z0 + k + 4, us + ((k + 5) % kSwURing) * kSwUSlot);
+      load_u(Z0 + k + 3, (k + 4) % kSwURing);
+      load_u(Z0 + k + 4, (k + 5) % kSwURing);
       sweep_load_e(g, coeff, cl, X0, Y0, Z0 + k + 2, es + ((k + 3) % kSwERing) * kSwESlot);
       sweep_load_e(g, coeff, cl, X0, Y0, Z0 + k + 3, es + ((k + 4) % kSwERing) * kSwESlot);
     }
@@ -138,6 +161,10 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
           r32[3 * loc + c] = float(r);
           ss += r * r;
         }
+        if constexpr (FUSE) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) unew[3 * loc + c] = p1[c];  // the updated u of this vertex
+        }
       } else if constexpr (OUT == kSwResidual) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
@@ -147,6 +174,10 @@ __global__ void __launch_bounds__(kSwTX* kSwTY, MINB)
       }
     }
     __pipeline_wait_prior(0);
+    if (k + 2 < TZ) {
+      fuse((k + 4) % kSwURing);
+      fuse((k + 5) % kSwURing);
+    }
     __syncthreads();
   }
   if constexpr (OUT == kSwDefect) {
@@ -576,6 +607,24 @@ void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, cons
 long long launch_l0_defect_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
                                  ZLink<double> ul, const double* f, float* r32, double* partials, cudaStream_t s) {
   return launch_sweep<float, double, double, kSwDefect>(g, coeff, cl, u, ul, f, nullptr, r32, partials, s);
+}
+
+long long launch_l0_defect_update_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
+                                        ZLink<double> ul, const float* e, ZLink<float> el, double* unew,
+                                        const double* f, float* r32, double* partials, cudaStream_t s) {
+  const int tz = sweep_tz(g);
+  const dim3 gr(g.n[0] / kSwTX, g.n[1] / kSwTY, g.n[2] / tz);
+  constexpr size_t sm = sweep_smem<double, float>() + sizeof(float) * kSwURing * kSwUSlot;
+  static bool attr = false;
+  if (!attr) {
+    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_sweep_kernel<float, double, double, kSwDefect, 2, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  l0_sweep_kernel<float, double, double, kSwDefect, 2, true><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(
+      g, coeff, cl, u, ul, f, nullptr, r32, partials, tz, e, resolve(el, e), unew);
+  IHOM_LAUNCH_CHECK();
+  return (long long)gr.x * gr.y * gr.z;
 }
 
 template void launch_l0_apply_sweep<float, double, double>(const GridGeo&, const float*, ZLink<float>, const double*,

@@ -50,6 +50,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_GS_SWEEP", 0)
         ih.set_knob("L0_CPAIR", 0)
         ih.set_knob("SUBMEANS_FLAT", 1)
+        ih.set_knob("FUSED_UPDATE", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -205,6 +206,17 @@ def test_unrolled_element_galerkin_bit_identical(ih, n, precision):
 def test_flat_sub_means_bit_identical(ih, precision, mode):
     base = _solve(ih, 32, {"SUBMEANS_FLAT": 0}, precision=precision, mode=mode)
     v = _solve(ih, 32, {"SUBMEANS_FLAT": 1}, precision=precision, mode=mode)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2), (64, 4)])
+def test_fused_update_bit_identical(ih, n, P):
+    """u += e folded into the defect-residual sweep (ping-pong buffers) == separate axpy + residual."""
+    base = _solve(ih, n, {"FUSED_UPDATE": 0}, fabric_p=P)
+    v = _solve(ih, n, {"FUSED_UPDATE": 1}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

@@ -622,7 +622,7 @@ long long launch_l0_defect_update_sweep(const GridGeo& g, const float* coeff, ZL
     attr = true;
   }
   l0_sweep_kernel<float, double, double, kSwDefect, 2, true><<<gr, dim3(kSwTX, kSwTY), sm, s>>>(
-      g, coeff, cl, u, ul, f, nullptr, r32, partials, tz, e, resolve(el, e), unew);
+      g, coeff, resolve(cl, coeff), u, resolve(ul, u), f, nullptr, r32, partials, tz, e, resolve(el, e), unew);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }

@@ -282,6 +282,15 @@ def run_ours(args):
                 "bytes_per_launch": ent["bytes"] / max(1, ent["launches"]),
                 "avg_launch_ms": ent["ms"] / max(1, ent["launches"]),
                 "traffic": ncu_traffic(fam, args.reso)}
+    # kernels whose real bound is a compute pipe, not HBM: f64 flops per unit (SASS count: the sweep f64
+    # residual runs 267 DFMA + 68 DADD per vertex) against the measured FP64 peak (DFMA 63.1/clk/SM,
+    # tools/microbench_pipes.cu, x 148 SMs x 1965 MHz x 2 flops = 36.7 TFLOP/s)
+    fp64_units = {"l0_residual_f64": (2 * 267 + 68, m)}  # m: this rank's vertices
+    if fam in fp64_units:
+        fl, units = fp64_units[fam]
+        tf = fl * units / (ent["ms"] / max(1, ent["launches"]) * 1e-3) / 1e12
+        roofline["compute"] = {"pipe": "fp64", "achieved": round(tf, 2), "peak": 36.7, "unit": "TFLOP/s",
+                               "frac": round(tf / 36.7, 4), "flops_per_vertex": fl}
     total_ms = sum(e["ms"] for e in prof.values()) or 1.0
     kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"], "share": round(v["ms"] / total_ms, 4),
                    "GB/s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] else None}

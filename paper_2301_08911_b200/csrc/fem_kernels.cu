@@ -415,6 +415,73 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
   }
 }
 
+// ---------------------------------------------------------------- column-marching GS pass (f32 inner)
+// A thread walks KZ same-colour vertices up its (h0, h1) column (halved z h2 .. h2+KZ-1, actual z
+// step 2). The upper neighbour plane of one vertex (actual z+1) is the lower plane of the next, so
+// each step loads two new planes (18 neighbours) and carries 9 in registers -- the fast2 pairing
+// extended along the whole column, with the element planes and the per-axis addressing advanced
+// incrementally. Same per-vertex arithmetic and order as l0_gs_fast2_kernel: bit-identical.
+template <typename TC, int MINB, bool ZL = false, int ZC = -1, int KZ = 4>
+__global__ void __launch_bounds__(128, MINB) l0_gs_col_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                              const float* __restrict__ f, float* u, ZLink<float> ul,
+                                                              int color) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
+  if constexpr (ZC >= 0) color = ZC;
+  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
+  const int h2s = KZ * blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  using TA = float;
+  const float* ur = u;
+  float lo[9][3], up[9][3];
+  {  // lower plane of the first vertex
+    FastAddr fa;
+    fast_addr(g, color, h0, h1, h2s, fa);
+    const float* p0 = zbase(fa, ur, ul, 0);
+#pragma unroll
+    for (int n = 0; n < 9; ++n) {
+      if ((ZM >> n) & 1u) continue;
+      const float* p = p0 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][0]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) lo[n][c] = __ldg(p + c);
+    }
+  }
+#pragma unroll 1
+  for (int j = 0; j < KZ; ++j) {
+    FastAddr fa;
+    fast_addr(g, color, h0, h1, h2s + j, fa);
+    TA q[8];
+    load_q_fast(coeff, cl, fa, q);
+    const float* p2 = zbase(fa, ur, ul, 2);
+    auto U = [&](int n, int c) -> TA {
+      if (n < 9) return lo[n][c];
+      const unsigned l = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];
+      if (n < 18) return __ldg(ur + 3 * (size_t)l + c);
+      const float v = __ldg(p2 + 3 * (size_t)l + c);
+      up[n - 18][c] = v;
+      return v;
+    };
+    TA m[3], sblk[9];
+    ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), U, m, sblk);
+    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+    float rhs[3], out[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
+    solve3<float>(sblk, rhs, out);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
+#pragma unroll
+    for (int n = 0; n < 9; ++n)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) lo[n][c] = up[n][c];
+  }
+}
+
+static int gs_col_kz() { return knob("GS_COL", 0); }  // 0: off; else vertices per column (2, 4, 8)
+
 // ---------------------------------------------------------------- paired f32 kernels (FFMA2)
 // One thread, two same-colour vertices stacked in halved z (h2, h2+1) -- the
 // fast2 pairing -- with the stencil evaluated ONCE in float2 lane-pair
@@ -832,9 +899,23 @@ bool l0_gs_zero_start_ok(const GridGeo& g) {
 // register budget of the two-vertex GS kernel: 5 blocks/SM (96 regs, default) or 6 / 8 (knob GS2_MINB)
 static int gs2_minb() { return knob("GS2_MINB", 5); }
 
+template <typename TC, bool ZL, int ZC>
+static bool launch_col(const dim3& gr2, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff, ZLink<TC> cl,
+                       const float* f, float* u, ZLink<float> ul, int color) {
+  const int kz = gs_col_kz();
+  if (kz <= 0 || (2 * gr2.z) % kz != 0) return false;
+  const dim3 gr(gr2.x, gr2.y, 2 * gr2.z / kz);  // gr2 counts vertex pairs
+  if (kz == 2) l0_gs_col_kernel<TC, 4, ZL, ZC, 2><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
+  else if (kz == 8) l0_gs_col_kernel<TC, 4, ZL, ZC, 8><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
+  else l0_gs_col_kernel<TC, 4, ZL, ZC, 4><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
+  return true;
+}
+
 template <typename TC, typename TN, bool ZL, int ZC>
 static void launch_fast2_zs(const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff,
                             ZLink<TC> cl, const TN* f, TN* u, ZLink<TN> ul) {
+  if constexpr (std::is_same_v<TN, float>)
+    if (launch_col<TC, ZL, ZC>(gr, b, s, g, coeff, cl, f, u, ul, ZC)) return;
   const int mb = ZL ? 5 : gs2_minb();
   if (mb >= 8) l0_gs_fast2_kernel<TC, TN, 8, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
   else if (mb == 6) l0_gs_fast2_kernel<TC, TN, 6, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
@@ -934,6 +1015,11 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
         done = true;
       } else if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
+        if (linked ? launch_col<TC, true, -1>(gr2, b, s, g, coeff, cl, f, u, ul, color)
+                   : launch_col<TC, false, -1>(gr2, b, s, g, coeff, cl, f, u, ul, color)) {
+          IHOM_LAUNCH_CHECK();
+          return;
+        }
         if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else if (gs2_minb() >= 8) l0_gs_fast2_kernel<TC, TN, 8><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else if (gs2_minb() == 6) l0_gs_fast2_kernel<TC, TN, 6><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);

@@ -51,6 +51,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_CPAIR", 0)
         ih.set_knob("SUBMEANS_FLAT", 1)
         ih.set_knob("FUSED_UPDATE", 1)
+        ih.set_knob("GS_COL", 0)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -217,6 +218,18 @@ def test_fused_update_bit_identical(ih, n, P):
     """u += e folded into the defect-residual sweep (ping-pong buffers) == separate axpy + residual."""
     base = _solve(ih, n, {"FUSED_UPDATE": 0}, fabric_p=P)
     v = _solve(ih, n, {"FUSED_UPDATE": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("kz", [2, 4, 8])
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
+def test_column_gs_bit_identical(ih, kz, n, P):
+    """Column-marching level-0 GS (KZ vertices per thread, carried neighbour plane) == two-vertex kernel."""
+    base = _solve(ih, n, {"GS_COL": 0}, fabric_p=P)
+    v = _solve(ih, n, {"GS_COL": kz}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

@@ -20,6 +20,8 @@ case "$1" in
   part2)
     full stencil_apply_fast_kernel 1; full tensor_kernel 1; full gal_stencil_fast_kernel 1
     full gal_elem_unrolled_kernel 1; full axpy_kernel 1; full sens_cached_kernel 1 ;;
+  fused)
+    full l0_sweep_kernel 3 ;;
   part3)  # one whole V-cycle of the GS families (pre = zero-start, post) for the per-launch traffic average
     full l0_gs_fast2_kernel 16; full stencil_gs_fast_kernel 48 ;;
 esac

@@ -1,11 +1,12 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_kernel_variants.py -q -x --timeout 600 -k "fused or sweep_level0 or energy" > gpurun_out/t_variants.log 2>&1; echo variants rc $?; tail -5 gpurun_out/t_variants.log
-timeout 900 python -m pytest tests/test_slabs.py tests/test_ipc_slabs.py tests/test_gpu_parity.py -q -x --timeout 600 > gpurun_out/t_slabs.log 2>&1; echo slabs rc $?; tail -3 gpurun_out/t_slabs.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?
+timeout 900 python -m pytest tests/test_kernel_variants.py -q -x --timeout 600 -k column > gpurun_out/t_col.log 2>&1; echo col rc $?; tail -3 gpurun_out/t_col.log
+for v in 0 2 4 8; do IHOM_GS_COL=$v timeout 300 python tools/kernel_bench.py --reso 512 --ops l0_gs_f32,vcycle_f32 --reps 3 > gpurun_out/kb_col$v.json 2>&1; done
 python - <<'PY'
 import json
-d = json.load(open("gpurun_out/bench.json"))
-print(d["value"], d["e2e"]["value"], d["cycles_per_iteration"], d["objective"], d.get("hbm_used_gb_per_gpu"))
-for k, v in list(d["kernels"].items())[:8]: print(k, round(v["ms"] / 8, 2), v["launches"] // 8, v["GB/s"])
+for v in (0, 2, 4, 8):
+    ls = open(f"gpurun_out/kb_col{v}.json").read().splitlines()
+    a = json.loads(ls[0])["families"]["l0_gs_f32"]["ms_per_launch"]; b = json.loads(ls[1])["families"]["l0_gs_f32"]["ms_per_launch"]
+    print("GS_COL", v, "pass", a, "vcycle avg", b)
 PY
+bash tools/gpu_profile.sh fused

@@ -39,6 +39,34 @@ __global__ void k_ffma2(float* out, const float* in) {
   const float2 s = __fadd2_rn(__fadd2_rn(__fadd2_rn(x0, x1), __fadd2_rn(x2, x3)), __fadd2_rn(__fadd2_rn(x4, x5), __fadd2_rn(x6, x7)));
   out[blockIdx.x * blockDim.x + threadIdx.x] = s.x + s.y;
 }
+// pure f32 -> f64 conversion throughput (integer adds keep the inputs distinct; DADD-free accumulation
+// through the bit pattern) vs the same conversion done with integer ops on the ALU pipe
+__global__ void k_f2d_pure(unsigned long long* out, float a) {
+  float f0 = threadIdx.x * 1e-3f + 1.0f, f1 = f0 + 1, f2 = f0 + 2, f3 = f0 + 3;
+  unsigned long long acc = 0;
+  for (int i = 0; i < N_ITER; ++i) {
+    acc ^= __double_as_longlong((double)f0) ^ __double_as_longlong((double)f1) ^ __double_as_longlong((double)f2) ^
+           __double_as_longlong((double)f3);
+    f0 = __int_as_float(__float_as_int(f0) + 1); f1 = __int_as_float(__float_as_int(f1) + 1);
+    f2 = __int_as_float(__float_as_int(f2) + 1); f3 = __int_as_float(__float_as_int(f3) + 1);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+__device__ __forceinline__ unsigned long long f2d_bits(float x) {  // normal, non-zero finite x only
+  const unsigned b = __float_as_uint(x);
+  const unsigned hi = (b & 0x80000000u) | (((b >> 3) & 0x0fffffffu) + (896u << 20));
+  return ((unsigned long long)hi << 32) | (unsigned long long)(b << 29);
+}
+__global__ void k_f2d_int(unsigned long long* out, float a) {
+  float f0 = threadIdx.x * 1e-3f + 1.0f, f1 = f0 + 1, f2 = f0 + 2, f3 = f0 + 3;
+  unsigned long long acc = 0;
+  for (int i = 0; i < N_ITER; ++i) {
+    acc ^= f2d_bits(f0) ^ f2d_bits(f1) ^ f2d_bits(f2) ^ f2d_bits(f3);
+    f0 = __int_as_float(__float_as_int(f0) + 1); f1 = __int_as_float(__float_as_int(f1) + 1);
+    f2 = __int_as_float(__float_as_int(f2) + 1); f3 = __int_as_float(__float_as_int(f3) + 1);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
 // f32 -> f64 conversions feeding DFMA (the mixed-precision stencil apply pattern)
 __global__ void k_f2d(double* out, float a) {
   float f0 = threadIdx.x * 1e-3f, f1 = f0 + 1, f2 = f0 + 2, f3 = f0 + 3, f4=f0+4,f5=f0+5,f6=f0+6,f7=f0+7;
@@ -77,6 +105,9 @@ int main() {
   float* in; cudaMalloc(&in, 4096 * 4); cudaMemset(in, 0, 4096 * 4);
   run("FFMA all-register", [&] { k_ffma_reg<<<blocks, threads>>>(f, in); }, 8);
   run("FFMA2 all-register (f32 lanes)", [&] { k_ffma2<<<blocks, threads>>>(f, in); }, 16);
+  unsigned long long* ul; cudaMalloc(&ul, blocks * threads * 8);
+  run("F2F.F64.F32 pure (+4 IADD, XOR)", [&] { k_f2d_pure<<<blocks, threads>>>(ul, 1e-3f); }, 4);
+  run("f32->f64 by integer ops (+4 IADD, XOR)", [&] { k_f2d_int<<<blocks, threads>>>(ul, 1e-3f); }, 4);
   run("F2F.F64.F32 (+8 FADD +8 DADD)", [&] { k_f2d<<<blocks, threads>>>(d, 1e-3f); }, 8);
   run("F2F.F32.F64 (+8 DADD +8 FADD)", [&] { k_d2f<<<blocks, threads>>>(f, 1e-3); }, 8);
   printf("SMs %d\n", p.multiProcessorCount);

@@ -695,37 +695,48 @@ double Hierarchy<T>::defect_residual(bool update) {
 // symmetric: post-smoothing walks the colours 7..0 (adjoint of the pre-smoother),
 // which makes the cycle an SPD preconditioner for PCG.
 template <typename T>
-void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
-  const int lmax = num_levels() - 1;
-  Level& L0 = levels_[0];
-  const long long n0 = 3 * L0.g.nv;
+void Hierarchy<T>::inner_down(int l, const SolverOptions& opts) {
   // e = 0 on every level before its pre-smoothing: with zero-start sweeps the first sweep never
   // reads a colour it has not written yet, so the clear is skipped (bit-identical)
-  for (int l = 0; l < lmax; ++l) {
-    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
-    if (!zs) {
-      IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
-      launches_ += l == 0 ? 1 : 0;
-    }
-    relax_f32(l, opts.pre_sweeps, false, zs);
-    residual_f32(l);
-    restrict_to_f32(l);
+  const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
+  if (!zs) {
+    IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
+    launches_ += l == 0 ? 1 : 0;
   }
-  (void)n0;
+  relax_f32(l, opts.pre_sweeps, false, zs);
+  residual_f32(l);
+  restrict_to_f32(l);
+}
+
+template <typename T>
+void Hierarchy<T>::inner_coarsest() {
+  const int lmax = num_levels() - 1;
   if (lmax > 0) IHOM_CUDA(cudaMemsetAsync(levels_[size_t(lmax)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(lmax)].g.nv, s_));
   coarsest_f32();
+}
+
+template <typename T>
+void Hierarchy<T>::inner_prolong(int l) {
+  Level& F = levels_[size_t(l)];
+  Level& C = levels_[size_t(l + 1)];
+  if (F.sharded) sync();
+  {
+    ProfScope p(s_, "prolong", double(F.g.nv) * 25.5);
+    if (!(F.sharded && !C.sharded))
+      launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, C.sharded ? C.eul : ZLink<float>{});
+    else
+      launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, {}, slab_.rank * (F.g.n[2] / 2));
+  }
+  ++launches_;
+}
+
+template <typename T>
+void Hierarchy<T>::inner_vcycle(const SolverOptions& opts, bool symmetric) {
+  const int lmax = num_levels() - 1;
+  for (int l = 0; l < lmax; ++l) inner_down(l, opts);
+  inner_coarsest();
   for (int l = lmax - 1; l >= 0; --l) {
-    Level& F = levels_[size_t(l)];
-    Level& C = levels_[size_t(l + 1)];
-    if (F.sharded) sync();
-    {
-      ProfScope p(s_, "prolong", double(F.g.nv) * 25.5);
-      if (!(F.sharded && !C.sharded))
-        launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, C.sharded ? C.eul : ZLink<float>{});
-      else
-        launch_prolong_add<float>(C.g, F.g, C.eu.p, F.eu.p, s_, {}, slab_.rank * (F.g.n[2] / 2));
-    }
-    ++launches_;
+    inner_prolong(l);
     relax_f32(l, opts.post_sweeps, symmetric);
   }
 }
@@ -824,22 +835,259 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
     }
   }
   inner_vcycle(opts, false);
+  const double rn = finish_defect_cycle();
+  const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(L0.f.p, n0);
+  check_error("v_cycle");
+  return fn > 0.0 ? rn / fn : 0.0;
+}
+
+template <typename T>
+double Hierarchy<T>::finish_defect_cycle() {
+  Level& L0 = levels_[0];
+  const long long n0 = 3 * L0.g.nv;
+  const bool fast = fast_ok(L0.g);
   const bool fused = fast && u0_bound_ && u_alt_.p && fused_update_ok();
   if (!fused) {
     ProfScope p(s_, "vector", double(n0) * 20.0);
     launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
     ++launches_;
   }
-  double rn;
-  if (fast) {
-    rn = defect_residual(fused);  // also leaves ef0 ready for the next cycle
-  } else {
-    compute_residual(0);
-    rn = norm(L0.r.p, n0);
+  if (fast) return defect_residual(fused);  // also leaves ef0 ready for the next cycle
+  compute_residual(0);
+  return norm(L0.r.p, n0);
+}
+
+// ---------------------------------------------------------------- lockstep RHS pairs
+template <typename T>
+bool Hierarchy<T>::pair_ok(const SolverOptions& opts) const {
+  return std::is_same_v<T, float> && opts.mode == kMixedDefect && knob("RHS_PAIRS", 1) != 0 &&
+         fast_ok(levels_[0].g) && num_levels() > 1;
+}
+
+template <typename T>
+void Hierarchy<T>::ensure_pair() {
+  if (other_.ready) return;
+  ensure_inner();
+  const size_t nl = levels_.size();
+  other_.eu.resize(nl);
+  other_.ef.resize(nl);
+  other_.er.resize(nl);
+  other_.eul.assign(nl, ZLink<float>{});
+  other_.erl.assign(nl, ZLink<float>{});
+  other_.efpeer.assign(nl, PeerTable{});
+  for (size_t l = 0; l < nl; ++l) {
+    const size_t n3 = size_t(3 * levels_[l].g.nv);
+    other_.eu[l].alloc(n3);
+    other_.ef[l].alloc(n3);
+    other_.er[l].alloc(n3);
   }
-  const double fn = (u0_bound_ && lmax > 0) ? fnorm0_ : norm(L0.f.p, n0);
-  check_error("v_cycle");
-  return fn > 0.0 ? rn / fn : 0.0;
+  other_.f0.alloc(size_t(3 * levels_[0].g.nv));
+  if (u_alt_.p) other_.ualt.alloc(size_t(3 * levels_[0].g.nv));
+  IHOM_CUDA(cudaDeviceSynchronize());
+  if (slab_.on()) {  // collective, same order on every slab (mirrors ensure_inner)
+    if (other_.ualt.p) other_.ualtl = link(other_.ualt.p);
+    for (size_t l = 0; l < nl; ++l) {
+      Level& L = levels_[l];
+      if (L.sharded) {
+        other_.eul[l] = link(other_.eu[l].p);
+        other_.erl[l] = link(other_.er[l].p);
+      } else if (int(l) == rep0_) {
+        other_.efpeer[l] = peer_table(slab_.fab->exchange(slab_.rank, other_.ef[l].p));
+      }
+    }
+  }
+  other_.ready = true;
+}
+
+template <typename T>
+void Hierarchy<T>::select_rhs(int k) {
+  if (k == cur_rhs_) return;
+  ensure_pair();
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    Level& L = levels_[l];
+    std::swap(L.eu, other_.eu[l]);
+    std::swap(L.ef, other_.ef[l]);
+    std::swap(L.er, other_.er[l]);
+    std::swap(L.eul, other_.eul[l]);
+    std::swap(L.erl, other_.erl[l]);
+    std::swap(L.efpeer, other_.efpeer[l]);
+  }
+  std::swap(levels_[0].f, other_.f0);
+  std::swap(u_alt_, other_.ualt);
+  std::swap(u_alt_l_, other_.ualtl);
+  std::swap(u0_bound_, other_.u0_bound);
+  std::swap(u_home_, other_.u_home);
+  std::swap(u0l_, other_.u0l);
+  std::swap(u_home_l_, other_.u_home_l);
+  std::swap(fnorm0_, other_.fnorm0);
+  cur_rhs_ = k;
+}
+
+template <typename T>
+void Hierarchy<T>::relax_f32_pair(int l, int sweeps, bool zero_start) {
+  Level& L = levels_[size_t(l)];
+  if (l == 0) throw std::logic_error("paired sweeps run on the stencil levels");
+  const int cur = cur_rhs_, oth = 1 - cur_rhs_;
+  float* u[2];
+  const float* f[2];
+  ZLink<float> ul[2];
+  u[cur] = L.eu.p, u[oth] = other_.eu[size_t(l)].p;
+  f[cur] = L.ef.p, f[oth] = other_.ef[size_t(l)].p;
+  ul[cur] = L.eul, ul[oth] = other_.eul[size_t(l)];
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int c = 0; c < 8; ++c) {
+      if (L.g.size[c] == 0) continue;
+      if (L.sharded) sync();
+      const bool zs = zero_start && sw == 0;
+      if constexpr (std::is_same_v<T, float>) {
+        ProfScope p(s_, l == 1 ? "l1_gs_f32" : (l == 2 ? "l2_gs_f32" : "coarse_gs_f32"),
+                    (zs ? gs_coarse_bytes_zs(L.g, c, 8, 4) : gs_coarse_bytes(L.g, c, 8, 4)));
+        launch_stencil_gs_color_pair<float, float>(L.g, L.st.p, f, u, c, err_.p, s_, ul, zs);
+      }
+      ++launches_;
+    }
+}
+
+template <typename T>
+void Hierarchy<T>::residual_f32_pair(int l) {
+  Level& L = levels_[size_t(l)];
+  if (L.sharded) sync();
+  const int cur = cur_rhs_, oth = 1 - cur_rhs_;
+  const float* x[2];
+  const float* f[2];
+  float* y[2];
+  ZLink<float> xl[2];
+  x[cur] = L.eu.p, x[oth] = other_.eu[size_t(l)].p;
+  f[cur] = L.ef.p, f[oth] = other_.ef[size_t(l)].p;
+  y[cur] = L.er.p, y[oth] = other_.er[size_t(l)].p;
+  xl[cur] = L.eul, xl[oth] = other_.eul[size_t(l)];
+  if constexpr (std::is_same_v<T, float>) {
+    ProfScope p(s_, l == 1 ? "l1_residual_f32" : (l == 2 ? "l2_residual_f32" : "coarse_residual_f32"),
+                resid_coarse_bytes(L.g, 8, 4, true));
+    launch_stencil_apply_pair<float, float>(L.g, L.st.p, x, f, y, s_, xl);
+  }
+  ++launches_;
+}
+
+// One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
+// converged) skips every level-0 and transfer step; the paired coarse kernels still compute its lane
+// on stale (finite) data, which nothing reads.
+template <typename T>
+void Hierarchy<T>::inner_vcycle_pair(const SolverOptions& opts, const bool act[2]) {
+  const int lmax = num_levels() - 1;
+  for (int k = 0; k < 2; ++k)
+    if (act[k]) {
+      select_rhs(k);
+      inner_down(0, opts);
+    }
+  for (int l = 1; l < lmax; ++l) {
+    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
+    if (!zs)
+      for (int k = 0; k < 2; ++k) {
+        select_rhs(k);
+        IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
+      }
+    relax_f32_pair(l, opts.pre_sweeps, zs);
+    residual_f32_pair(l);
+    for (int k = 0; k < 2; ++k)
+      if (act[k]) {
+        select_rhs(k);
+        restrict_to_f32(l);
+      }
+  }
+  for (int k = 0; k < 2; ++k)
+    if (act[k]) {
+      select_rhs(k);
+      inner_coarsest();
+    }
+  for (int l = lmax - 1; l >= 1; --l) {
+    for (int k = 0; k < 2; ++k)
+      if (act[k]) {
+        select_rhs(k);
+        inner_prolong(l);
+      }
+    relax_f32_pair(l, opts.post_sweeps, false);
+  }
+  for (int k = 0; k < 2; ++k)
+    if (act[k]) {
+      select_rhs(k);
+      inner_prolong(0);
+      relax_f32(0, opts.post_sweeps, false);
+    }
+}
+
+template <typename T>
+void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opts, const ZLink<double> ul[2],
+                                    SolveStats st[2]) {
+  if (!density_set_) throw StateError("set_density before solve");
+  if (!pair_ok(opts)) throw std::logic_error("lockstep pair solve needs mixed precision, mixed_defect and an even grid");
+  ensure_pair();
+  Level& L0 = levels_[0];
+  const long long n0 = 3 * L0.g.nv;
+  bool act[2] = {false, false}, negligible[2] = {false, false};
+  try {
+    for (int k = 0; k < 2; ++k) {  // src/multigrid.cpp:474-501 prologue, per RHS
+      select_rhs(k);
+      if (slab_.on() && is_self(ul[k], u[k])) throw std::invalid_argument("z-slab solve needs the links of the bound field");
+      st[k] = SolveStats{};
+      u0_bound_ = u[k];
+      u0l_ = resolve(ul[k], u[k]);
+      u_home_ = u[k];
+      u_home_l_ = u0l_;
+      remove_translations(L0.f.p, 0);
+      fnorm0_ = norm(L0.f.p, n0);
+      if (fnorm0_ <= negligible_load(n0)) {
+        IHOM_CUDA(cudaMemsetAsync(u[k], 0, sizeof(double) * n0, s_));
+        st[k].converged = true;
+        negligible[k] = true;
+        continue;
+      }
+      st[k].rel_residual = defect_residual() / fnorm0_;
+      act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
+    }
+    while (act[0] || act[1]) {
+      inner_vcycle_pair(opts, act);
+      for (int k = 0; k < 2; ++k)
+        if (act[k]) {
+          select_rhs(k);
+          const double rn = finish_defect_cycle();
+          check_error("v_cycle");
+          st[k].rel_residual = fnorm0_ > 0.0 ? rn / fnorm0_ : 0.0;
+          ++st[k].cycles;
+          act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
+        }
+    }
+    for (int k = 0; k < 2; ++k) {  // epilogue per RHS, as solve_bound
+      if (negligible[k]) continue;
+      select_rhs(k);
+      st[k].converged = st[k].rel_residual <= opts.tol;
+      if (u0_bound_ != u[k]) {  // the fused update left the result in the other buffer
+        remove_translations_to(u0_bound_, u[k], 0);
+        u0_bound_ = u[k];
+        u0l_ = u_home_l_;
+      } else {
+        remove_translations(u[k], 0);
+      }
+    }
+  } catch (...) {
+    for (int k = 0; k < 2; ++k) {
+      try {
+        select_rhs(k);
+        restore_home();
+      } catch (...) {
+      }
+      u0_bound_ = nullptr;
+      u_home_ = nullptr;
+    }
+    select_rhs(0);
+    throw;
+  }
+  for (int k = 0; k < 2; ++k) {
+    select_rhs(k);
+    u0_bound_ = nullptr;
+    u_home_ = nullptr;
+  }
+  select_rhs(0);
 }
 
 template <typename T>
@@ -980,7 +1228,29 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   if (multi && slabs) throw std::invalid_argument("load-case split and z-slabs are exclusive");
   ecache_valid_ = false;
   double per[18] = {};  // per load: cycles, rel_residual, converged
-  for (int i = 0; i < 6; ++i) {
+  if (!multi && hier_.pair_ok(opts_)) {
+    // loads (0,1), (2,3), (4,5) in lockstep: each pair streams the coarse stencils once
+    for (int i = 0; i < 6; i += 2) {
+      for (int k = 0; k < 2; ++k) {
+        hier_.select_rhs(k);
+        hier_.sync();  // coefficients of the neighbouring slabs are current
+        ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
+        launch_macro_force<T>(g, hier_.coeff(), i + k, hier_.level_f(0), hier_.stream(),
+                              slabs ? hier_.coeff_link() : ZLink<T>{});
+      }
+      hier_.select_rhs(0);
+      double* const uu[2] = {u_[size_t(i)].p, u_[size_t(i + 1)].p};
+      const ZLink<double> ll[2] = {ul_[size_t(i)], ul_[size_t(i + 1)]};
+      SolveStats st[2];
+      hier_.solve_bound_pair(uu, opts_, ll, st);
+      for (int k = 0; k < 2; ++k) {
+        per[3 * (i + k)] = st[k].cycles;
+        per[3 * (i + k) + 1] = st[k].rel_residual;
+        per[3 * (i + k) + 2] = st[k].converged ? 1.0 : 0.0;
+      }
+    }
+  }
+  for (int i = 0; i < 6 && !(!multi && hier_.pair_ok(opts_)); ++i) {
     if (multi && owner_[i] != comm_->rank()) continue;
     hier_.sync();  // coefficients of the neighbouring slabs are current
     {

@@ -200,11 +200,31 @@ void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* 
 }
 
 // ---------------------------------------------------------------- stencil apply / GS
+// One or two right-hand sides (NL) per launch: the stencil block of a neighbour is read and converted
+// once and applied to every RHS, so a pair of cell problems solved in lockstep streams the coarse
+// stencils (the dominant bytes of levels >= 1) once for both. Per RHS the arithmetic is the same
+// explicit fma chain for NL = 1 and 2, so a paired solve is bit-identical to two single ones.
+template <typename TN>
+struct Rhs2 {      // right-hand side k of a level: input field x (u of a GS pass), f, output y
+  const TN* x[2];
+  ZLink<TN> xl[2];
+  const TN* f[2];
+  TN* y[2];
+};
+
+template <typename TS>
+__device__ __forceinline__ void stencil_block(const TS* __restrict__ bl, double c9[9]) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c9[e] = double(__ldg(bl + 32 * e));
+}
+__device__ __forceinline__ void block_fma(const double c9[9], double a, double b, double c, double m[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) m[r] = fma(c9[3 * r + 2], c, fma(c9[3 * r + 1], b, fma(c9[3 * r], a, m[r])));
+}
+
 // y = K x (f == nullptr) or y = f - K x; blocked stencil rows st_index(k, loc) (src/multigrid.cpp:186-205, 412-424).
-template <typename TS, typename TN>
-__global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st,
-                                                            const TN* __restrict__ x, const TN* __restrict__ f,
-                                                            TN* __restrict__ y) {
+template <typename TS, typename TN, int NL>
+__global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (loc >= g.nv) return;
   const int color = color_at(g, loc);
@@ -212,33 +232,29 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
   block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
   Nbhd nb;
   gather27(g, vx, vy, vz, nb);
-  double acc[3] = {0.0, 0.0, 0.0};
+  double acc[NL][3] = {};
   const TS* row = st + st_index(0, (unsigned)loc);
 #pragma unroll 3
   for (int n = 0; n < 27; ++n) {
-    const TN* xn = x + 3 * (size_t)nb.v[n];
-    const double a = double(xn[0]), b = double(xn[1]), c = double(xn[2]);
-    const TS* bl = row + 32 * 9 * n;
-    acc[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
-    acc[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
-    acc[2] += double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
-  }
-  if (f) {
+    double c9[9];
+    stencil_block(row + 32 * 9 * n, c9);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(double(f[3 * loc + c]) - acc[c]);
-  } else {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
+    for (int k = 0; k < NL; ++k) {
+      const TN* xn = io.x[k] + 3 * (size_t)nb.v[n];
+      block_fma(c9, double(xn[0]), double(xn[1]), double(xn[2]), acc[k]);
+    }
   }
+#pragma unroll
+  for (int k = 0; k < NL; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      io.y[k][3 * loc + c] = io.f[k] ? TN(double(io.f[k][3 * loc + c]) - acc[k][c]) : TN(acc[k][c]);
 }
 
 // Fast even-grid variants (FastAddr, common.cuh): one IADD3 per neighbour
 // location, AoS components at immediate offsets, blocked stencil rows.
-template <typename TS, typename TN, bool ZL = false>
-__global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st,
-                                                                 const TN* __restrict__ x, ZLink<TN> xl,
-                                                                 const TN* __restrict__ f, TN* __restrict__ y) {
-  if constexpr (!ZL) xl = {x, x};
+template <typename TS, typename TN, bool ZL, int NL>
+__global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
   const int h2 = blockIdx.z >> 3;
@@ -248,33 +264,55 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   fast_addr(g, color, h0, h1, h2, fa);
   const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   const TS* row = st + st_index(0, loc);
-  double acc[3] = {0.0, 0.0, 0.0};
-  const TN* xb[3] = {zbase(fa, x, xl, 0), x, zbase(fa, x, xl, 2)};
+  double acc[NL][3] = {};
+  const TN* xb[NL][3];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const ZLink<TN> xl = ZL ? io.xl[k] : ZLink<TN>{io.x[k], io.x[k]};
+    xb[k][0] = zbase(fa, io.x[k], xl, 0);
+    xb[k][1] = io.x[k];
+    xb[k][2] = zbase(fa, io.x[k], xl, 2);
+  }
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
-    const TN* xn = xb[n / 9] + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
-    const double a = double(__ldg(xn)), b = double(__ldg(xn + 1)), c = double(__ldg(xn + 2));
-    const TS* bl = row + 32 * 9 * n;
-    acc[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
-    acc[1] += double(__ldg(bl + 96)) * a + double(__ldg(bl + 128)) * b + double(__ldg(bl + 160)) * c;
-    acc[2] += double(__ldg(bl + 192)) * a + double(__ldg(bl + 224)) * b + double(__ldg(bl + 256)) * c;
-  }
-  if (f) {
+    double c9[9];
+    stencil_block(row + 32 * 9 * n, c9);
+    const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) y[3 * (size_t)loc + c] = TN(double(f[3 * (size_t)loc + c]) - acc[c]);
-  } else {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) y[3 * (size_t)loc + c] = TN(acc[c]);
+    for (int k = 0; k < NL; ++k) {
+      const TN* xn = xb[k][n / 9] + off;
+      block_fma(c9, double(__ldg(xn)), double(__ldg(xn + 1)), double(__ldg(xn + 2)), acc[k]);
+    }
   }
+#pragma unroll
+  for (int k = 0; k < NL; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      io.y[k][3 * (size_t)loc + c] = io.f[k] ? TN(double(io.f[k][3 * (size_t)loc + c]) - acc[k][c]) : TN(acc[k][c]);
 }
 
 // zm: neighbours known to be zero (zero-start sweep, common.cuh zero_start_mask): their stencil
 // blocks and values are not read -- bit-identical to adding their exact zero products.
-template <typename TS, typename TN, bool ZL = false>
-__global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st,
-                                                              const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              ZLink<TN> ul, TN* uw, int color, int* err, unsigned zm) {
-  if constexpr (!ZL) ul = {ur, ur};
+template <typename TS, typename TN>
+__device__ __forceinline__ bool gs_solve_store(const double S[9], const double m[3], const TN* f, size_t loc, TN* y,
+                                               int* err) {
+  const double rhs[3] = {double(f[3 * loc]) - m[0], double(f[3 * loc + 1]) - m[1], double(f[3 * loc + 2]) - m[2]};
+  const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
+                     S[2] * (S[3] * S[7] - S[4] * S[6]);
+  if (det == 0.0 || !isfinite(det)) {
+    atomicExch(err, 1);
+    return false;
+  }
+  double out[3];
+  solve3(S, rhs, out);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(out[c]);
+  return true;
+}
+
+template <typename TS, typename TN, bool ZL, int NL>
+__global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
+                                                              int color, int* err, unsigned zm) {
   const int h2 = blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
@@ -282,32 +320,31 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
   fast_addr(g, color, h0, h1, h2, fa);
   const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   const TS* row = st + st_index(0, loc);
-  double m[3] = {0.0, 0.0, 0.0}, S[9];
+  double m[NL][3] = {}, S[9];
+  stencil_block(row + 32 * 9 * 13, S);
+  const TN* ub[NL][3];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = double(__ldg(row + 32 * (9 * 13 + e)));
-  const TN* ub[3] = {zbase(fa, ur, ul, 0), ur, zbase(fa, ur, ul, 2)};
+  for (int k = 0; k < NL; ++k) {
+    const ZLink<TN> ul = ZL ? io.xl[k] : ZLink<TN>{io.x[k], io.x[k]};
+    ub[k][0] = zbase(fa, io.x[k], ul, 0);
+    ub[k][1] = io.x[k];
+    ub[k][2] = zbase(fa, io.x[k], ul, 2);
+  }
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
     if (n == 13 || ((zm >> n) & 1u)) continue;
-    const TN* un = ub[n / 9] + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
-    const double a = double(__ldg(un)), b = double(__ldg(un + 1)), c = double(__ldg(un + 2));
-    const TS* bl = row + 32 * 9 * n;
-    m[0] += double(__ldg(bl)) * a + double(__ldg(bl + 32)) * b + double(__ldg(bl + 64)) * c;
-    m[1] += double(__ldg(bl + 96)) * a + double(__ldg(bl + 128)) * b + double(__ldg(bl + 160)) * c;
-    m[2] += double(__ldg(bl + 192)) * a + double(__ldg(bl + 224)) * b + double(__ldg(bl + 256)) * c;
-  }
-  const double rhs[3] = {double(f[3 * (size_t)loc]) - m[0], double(f[3 * (size_t)loc + 1]) - m[1],
-                         double(f[3 * (size_t)loc + 2]) - m[2]};
-  const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
-                     S[2] * (S[3] * S[7] - S[4] * S[6]);
-  if (det == 0.0 || !isfinite(det)) {
-    atomicExch(err, 1);
-    return;
-  }
-  double out[3];
-  solve3(S, rhs, out);
+    double c9[9];
+    stencil_block(row + 32 * 9 * n, c9);
+    const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) uw[3 * (size_t)loc + c] = TN(out[c]);
+    for (int k = 0; k < NL; ++k) {
+      const TN* un = ub[k][n / 9] + off;
+      block_fma(c9, double(__ldg(un)), double(__ldg(un + 1)), double(__ldg(un + 2)), m[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k)
+    if (!gs_solve_store<TS, TN>(S, m[k], io.f[k], loc, io.y[k], err)) return;
 }
 
 // Small levels (latency-bound: a few thousand vertices, long per-thread load
@@ -337,80 +374,66 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <typename TS, typename TN>
-__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st,
-                                                                 const TN* __restrict__ x, ZLink<TN> xl,
-                                                                 const TN* __restrict__ f, TN* __restrict__ y) {
+template <typename TS, typename TN, int NL>
+__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
   const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (loc >= g.nv) return;
   const int color = color_at(g, loc);
   int vx, vy, vz;
   block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  double a[NL][3] = {};
   if (lane < 27) {
-    const TN* xn = nbr_ptr(g, x, xl, vx, vy, vz, lane);
-    const double a = double(xn[0]), b = double(xn[1]), c = double(xn[2]);
-    const TS* bl = st + st_index(9 * lane, (unsigned)loc);
-    a0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
-    a1 = double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
-    a2 = double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
-  }
-  a0 = warp_sum(a0);
-  a1 = warp_sum(a1);
-  a2 = warp_sum(a2);
-  if (lane == 0) {
-    if (f) {
-      y[3 * loc] = TN(double(f[3 * loc]) - a0);
-      y[3 * loc + 1] = TN(double(f[3 * loc + 1]) - a1);
-      y[3 * loc + 2] = TN(double(f[3 * loc + 2]) - a2);
-    } else {
-      y[3 * loc] = TN(a0);
-      y[3 * loc + 1] = TN(a1);
-      y[3 * loc + 2] = TN(a2);
+    double c9[9];
+    stencil_block(st + st_index(9 * lane, (unsigned)loc), c9);
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const TN* xn = nbr_ptr(g, io.x[k], io.xl[k], vx, vy, vz, lane);
+      block_fma(c9, double(xn[0]), double(xn[1]), double(xn[2]), a[k]);
     }
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a[k][c] = warp_sum(a[k][c]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        io.y[k][3 * loc + c] = io.f[k] ? TN(double(io.f[k][3 * loc + c]) - a[k][c]) : TN(a[k][c]);
   }
 }
 
-template <typename TS, typename TN>
-__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st,
-                                                              const TN* __restrict__ f, const TN* __restrict__ ur,
-                                                              ZLink<TN> ul, TN* uw, int color, int* err,
-                                                              unsigned zm) {
+template <typename TS, typename TN, int NL>
+__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
+                                                              int color, int* err, unsigned zm) {
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= g.size[color]) return;
   int vx, vy, vz;
   block_coords(g, color, (unsigned)i, vx, vy, vz);
   const long long loc = g.base[color] + i;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  double m[NL][3] = {};
   if (lane < 27 && lane != 13 && !((zm >> lane) & 1u)) {
-    const TN* un = nbr_ptr(g, ur, ul, vx, vy, vz, lane);
-    const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
-    const TS* bl = st + st_index(9 * lane, (unsigned)loc);
-    m0 = double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
-    m1 = double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
-    m2 = double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
-  }
-  m0 = warp_sum(m0);
-  m1 = warp_sum(m1);
-  m2 = warp_sum(m2);
-  if (lane == 0) {
-    const TS* row = st + st_index(9 * 13, (unsigned)loc);
-    double S[9];
+    double c9[9];
+    stencil_block(st + st_index(9 * lane, (unsigned)loc), c9);
 #pragma unroll
-    for (int e = 0; e < 9; ++e) S[e] = double(row[32 * e]);
-    const double rhs[3] = {double(f[3 * loc]) - m0, double(f[3 * loc + 1]) - m1, double(f[3 * loc + 2]) - m2};
-    const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
-                       S[2] * (S[3] * S[7] - S[4] * S[6]);
-    if (det == 0.0 || !isfinite(det)) {
-      atomicExch(err, 1);
-      return;
+    for (int k = 0; k < NL; ++k) {
+      const TN* un = nbr_ptr(g, io.x[k], io.xl[k], vx, vy, vz, lane);
+      block_fma(c9, double(un[0]), double(un[1]), double(un[2]), m[k]);
     }
-    double out[3];
-    solve3(S, rhs, out);
+  }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
+  for (int k = 0; k < NL; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m[k][c] = warp_sum(m[k][c]);
+  if (lane == 0) {
+    double S[9];
+    stencil_block(st + st_index(9 * 13, (unsigned)loc), S);
+#pragma unroll
+    for (int k = 0; k < NL; ++k)
+      if (!gs_solve_store<TS, TN>(S, m[k], io.f[k], size_t(loc), io.y[k], err)) return;
   }
 }
 
@@ -418,29 +441,44 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
 // 64^3 runs 35% faster thread-per-vertex, measured)
 static long long warp_vmax() { return (long long)knob("WARP_VMAX", 4096); }
 
-template <typename TS, typename TN>
-void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
-                          ZLink<TN> xl) {
-  const bool linked = !is_self(xl, x);
-  xl = resolve(xl, x);
+template <typename TS, typename TN, int NL>
+static void launch_apply_n(const GridGeo& g, const TS* st, Rhs2<TN> io, cudaStream_t s) {
+  bool linked = false;
+  for (int k = 0; k < NL; ++k) {
+    linked = linked || !is_self(io.xl[k], io.x[k]);
+    io.xl[k] = resolve(io.xl[k], io.x[k]);
+  }
   if (g.nv <= 8 * warp_vmax()) {
-    stencil_apply_warp_kernel<TS, TN><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, x, xl, f, y);
+    stencil_apply_warp_kernel<TS, TN, NL><<<ceil_div(g.nv * 32, 128), 128, 0, s>>>(g, st, io);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    if (linked) stencil_apply_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, x, xl, f, y);
-    else stencil_apply_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, x, xl, f, y);
+    if (linked) stencil_apply_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io);
+    else stencil_apply_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io);
   } else {
     if (linked) throw std::invalid_argument("z-slab level needs an even grid");
-    stencil_apply_kernel<TS, TN><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, x, f, y);
+    stencil_apply_kernel<TS, TN, NL><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, io);
   }
   IHOM_LAUNCH_CHECK();
 }
 
-// Colour pass of the coarse GS with the determinant check (src/multigrid.cpp:207-239).
 template <typename TS, typename TN>
-__global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st,
-                                                         const TN* __restrict__ f, const TN* __restrict__ ur, TN* uw,
+void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
+                          ZLink<TN> xl) {
+  Rhs2<TN> io{{x, nullptr}, {xl, {}}, {f, nullptr}, {y, nullptr}};
+  launch_apply_n<TS, TN, 1>(g, st, io, s);
+}
+
+template <typename TS, typename TN>
+void launch_stencil_apply_pair(const GridGeo& g, const TS* st, const TN* const x[2], const TN* const f[2],
+                               TN* const y[2], cudaStream_t s, const ZLink<TN> xl[2]) {
+  Rhs2<TN> io{{x[0], x[1]}, {xl[0], xl[1]}, {f[0], f[1]}, {y[0], y[1]}};
+  launch_apply_n<TS, TN, 2>(g, st, io, s);
+}
+
+// Colour pass of the coarse GS with the determinant check (src/multigrid.cpp:207-239).
+template <typename TS, typename TN, int NL>
+__global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
                                                          int color, int* err, unsigned zm) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.size[color]) return;
@@ -449,54 +487,60 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
   Nbhd nb;
   gather27(g, vx, vy, vz, nb);
   const long long loc = g.base[color] + i;
-  double m[3] = {0.0, 0.0, 0.0}, S[9];
+  double m[NL][3] = {}, S[9];
   const TS* row0 = st + st_index(0, (unsigned)loc);
+  stencil_block(row0 + 32 * 9 * 13, S);
 #pragma unroll 3
   for (int n = 0; n < 27; ++n) {
-    const TS* bl = row0 + 32 * 9 * n;
-    if (n == 13) {
+    if (n == 13 || ((zm >> n) & 1u)) continue;
+    double c9[9];
+    stencil_block(row0 + 32 * 9 * n, c9);
 #pragma unroll
-      for (int e = 0; e < 9; ++e) S[e] = double(bl[32 * e]);
-      continue;
+    for (int k = 0; k < NL; ++k) {
+      const TN* un = io.x[k] + 3 * (size_t)nb.v[n];
+      block_fma(c9, double(un[0]), double(un[1]), double(un[2]), m[k]);
     }
-    if ((zm >> n) & 1u) continue;
-    const TN* un = ur + 3 * (size_t)nb.v[n];
-    const double a = double(un[0]), b = double(un[1]), c = double(un[2]);
-    m[0] += double(bl[0]) * a + double(bl[32]) * b + double(bl[64]) * c;
-    m[1] += double(bl[96]) * a + double(bl[128]) * b + double(bl[160]) * c;
-    m[2] += double(bl[192]) * a + double(bl[224]) * b + double(bl[256]) * c;
   }
-  const double rhs[3] = {double(f[3 * loc]) - m[0], double(f[3 * loc + 1]) - m[1], double(f[3 * loc + 2]) - m[2]};
-  const double det = S[0] * (S[4] * S[8] - S[5] * S[7]) - S[1] * (S[3] * S[8] - S[5] * S[6]) +
-                     S[2] * (S[3] * S[7] - S[4] * S[6]);
-  if (det == 0.0 || !isfinite(det)) {
-    atomicExch(err, 1);
-    return;
-  }
-  double out[3];
-  solve3(S, rhs, out);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
+  for (int k = 0; k < NL; ++k)
+    if (!gs_solve_store<TS, TN>(S, m[k], io.f[k], size_t(loc), io.y[k], err)) return;
+}
+
+template <typename TS, typename TN, int NL>
+static void launch_gs_n(const GridGeo& g, const TS* st, Rhs2<TN> io, int color, int* err, cudaStream_t s,
+                        bool zero_start) {
+  bool linked = false;
+  for (int k = 0; k < NL; ++k) {
+    linked = linked || !is_self(io.xl[k], io.x[k]);
+    io.xl[k] = resolve(io.xl[k], io.x[k]);
+  }
+  const unsigned zm = zero_start ? zero_start_mask(color) : 0u;
+  if (g.size[color] <= warp_vmax()) {
+    stencil_gs_warp_kernel<TS, TN, NL><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, io, color, err, zm);
+  } else if (fast_ok(g)) {
+    const dim3 b = fast_block(g);
+    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
+    if (linked) stencil_gs_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+    else stencil_gs_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+  } else {
+    if (linked) throw std::invalid_argument("z-slab level needs an even grid");
+    stencil_gs_kernel<TS, TN, NL><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, io, color, err, zm);
+  }
+  IHOM_LAUNCH_CHECK();
 }
 
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
                              cudaStream_t s, ZLink<TN> ul, bool zero_start) {
-  const bool linked = !is_self(ul, u);
-  ul = resolve(ul, u);
-  const unsigned zm = zero_start ? zero_start_mask(color) : 0u;
-  if (g.size[color] <= warp_vmax()) {
-    stencil_gs_warp_kernel<TS, TN><<<ceil_div(g.size[color] * 32, 128), 128, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
-  } else if (fast_ok(g)) {
-    const dim3 b = fast_block(g);
-    const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    if (linked) stencil_gs_fast_kernel<TS, TN, true><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
-    else stencil_gs_fast_kernel<TS, TN><<<gr, b, 0, s>>>(g, st, f, u, ul, u, color, err, zm);
-  } else {
-    if (linked) throw std::invalid_argument("z-slab level needs an even grid");
-    stencil_gs_kernel<TS, TN><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, f, u, u, color, err, zm);
-  }
-  IHOM_LAUNCH_CHECK();
+  Rhs2<TN> io{{u, nullptr}, {ul, {}}, {f, nullptr}, {u, nullptr}};
+  launch_gs_n<TS, TN, 1>(g, st, io, color, err, s, zero_start);
+}
+
+template <typename TS, typename TN>
+void launch_stencil_gs_color_pair(const GridGeo& g, const TS* st, const TN* const f[2], TN* const u[2], int color,
+                                  int* err, cudaStream_t s, const ZLink<TN> ul[2], bool zero_start) {
+  Rhs2<TN> io{{u[0], u[1]}, {ul[0], ul[1]}, {f[0], f[1]}, {u[0], u[1]}};
+  launch_gs_n<TS, TN, 2>(g, st, io, color, err, s, zero_start);
 }
 
 // ---------------------------------------------------------------- Galerkin assembly
@@ -939,6 +983,12 @@ INST_T(float)
 INST_S(float, double)
 INST_S(double, double)
 INST_S(float, float)
+template void launch_stencil_apply_pair<float, float>(const GridGeo&, const float*, const float* const[2],
+                                                      const float* const[2], float* const[2], cudaStream_t,
+                                                      const ZLink<float>[2]);
+template void launch_stencil_gs_color_pair<float, float>(const GridGeo&, const float*, const float* const[2],
+                                                         float* const[2], int, int*, cudaStream_t,
+                                                         const ZLink<float>[2], bool);
 #undef INST_S
 template void launch_galerkin_from_elements<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t,
                                                    ZLink<float>, const GridGeo*, int);

@@ -52,6 +52,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("SUBMEANS_FLAT", 1)
         ih.set_knob("FUSED_UPDATE", 1)
         ih.set_knob("GS_COL", 0)
+        ih.set_knob("RHS_PAIRS", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -230,6 +231,18 @@ def test_column_gs_bit_identical(ih, kz, n, P):
     """Column-marching level-0 GS (KZ vertices per thread, carried neighbour plane) == two-vertex kernel."""
     base = _solve(ih, n, {"GS_COL": 0}, fabric_p=P)
     v = _solve(ih, n, {"GS_COL": kz}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(16, 0), (32, 0), (64, 0), ((64, 32, 48), 0), (32, 2), (64, 4)])
+def test_rhs_pairs_bit_identical(ih, n, P):
+    """Cell problems solved in lockstep pairs (coarse stencils streamed once per pair) == one by one:
+    same cycle counts, tensors and displacements bit for bit."""
+    base = _solve(ih, n, {"RHS_PAIRS": 0}, fabric_p=P)
+    v = _solve(ih, n, {"RHS_PAIRS": 1}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

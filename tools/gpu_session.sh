@@ -1,12 +1,10 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_kernel_variants.py -q -x --timeout 600 -k column > gpurun_out/t_col.log 2>&1; echo col rc $?; tail -3 gpurun_out/t_col.log
-for v in 0 2 4 8; do IHOM_GS_COL=$v timeout 300 python tools/kernel_bench.py --reso 512 --ops l0_gs_f32,vcycle_f32 --reps 3 > gpurun_out/kb_col$v.json 2>&1; done
+timeout 900 python -m pytest tests/test_kernel_variants.py -q -x --timeout 600 -k "rhs_pairs" > gpurun_out/t_pairs.log 2>&1; echo pairs rc $?; tail -25 gpurun_out/t_pairs.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?; tail -3 gpurun_out/bench.err
 python - <<'PY'
 import json
-for v in (0, 2, 4, 8):
-    ls = open(f"gpurun_out/kb_col{v}.json").read().splitlines()
-    a = json.loads(ls[0])["families"]["l0_gs_f32"]["ms_per_launch"]; b = json.loads(ls[1])["families"]["l0_gs_f32"]["ms_per_launch"]
-    print("GS_COL", v, "pass", a, "vcycle avg", b)
+d = json.load(open("gpurun_out/bench.json"))
+print(d["value"], d["e2e"]["value"], d["cycles_per_iteration"], d["objective"])
+for k, v in list(d["kernels"].items())[:12]: print(k, round(v["ms"] / 8, 2), v["launches"] // 8, v["GB/s"])
 PY
-bash tools/gpu_profile.sh fused

@@ -10,6 +10,7 @@
 // (F2F, ~16/clk/SM on B200, measured) the reference's float merge would need.
 #include "kernels.hpp"
 #include "ku_gen.cuh"
+#include "hada_gen.cuh"
 
 #include <cuda_pipeline.h>
 
@@ -25,6 +26,9 @@ __constant__ double c_fmacro[8][6][3];
 // kappa classes of the factored stencil (ku_gen.cuh): kappa_k = lam' alpha_k + mu' beta_k
 __constant__ double c_kap_d[kKappaClasses];
 __constant__ float c_kap_f[kKappaClasses];
+// element stiffness classes in the sum/difference basis (hada_gen.cuh): (lam' alpha_k + mu' beta_k) / 64
+__constant__ double c_hada_d[kHadaClasses];
+__constant__ float c_hada_f[kHadaClasses];
 
 void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t s) {
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_blk_d, t.blk, sizeof(t.blk), 0, cudaMemcpyHostToDevice, s));
@@ -43,6 +47,14 @@ void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t
   }
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_d, kd, sizeof(kd), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_f, kf, sizeof(kf), 0, cudaMemcpyHostToDevice, s));
+  static double hd[kHadaClasses];
+  static float hf[kHadaClasses];
+  for (int c = 0; c < kHadaClasses; ++c) {
+    hd[c] = (lam * kHadaAlpha[c] + mu * kHadaBeta[c]) * (1.0 / 64.0);
+    hf[c] = float(hd[c]);
+  }
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hada_d, hd, sizeof(hd), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hada_f, hf, sizeof(hf), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaStreamSynchronize(s));
 }
 

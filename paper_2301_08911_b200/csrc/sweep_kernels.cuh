@@ -496,6 +496,10 @@ __global__ void __launch_bounds__(kGsThreads, 2)
   }
 }
 
+}  // namespace ihomgpu
+#include "hsweep_kernels.cuh"  // sum-factorised element sweep (uses SweepOut / wrapc above)
+namespace ihomgpu {
+
 // Off by default: measured 1.16 ms per pass at 512^3 vs 0.66 for l0_gs_fast2 (224 registers leave
 // 8 warps per SM and the one-step cp.async prefetch cannot hide the load latency; profiles/
 // kernel_variants_r01.md). Kept as the starting point for a warp-specialised (TMA producer) version.
@@ -600,18 +604,31 @@ void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, cons
       return;
     }
   }
+  if constexpr (std::is_same_v<TN, TA>) {
+    if (hsweep_ok(g, sizeof(TN) == 4)) {
+      if (f) launch_hsweep<TC, TN, kSwResidual, false>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, nullptr, {}, nullptr, s);
+      else launch_hsweep<TC, TN, kSwApply, false>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, nullptr, {}, nullptr, s);
+      return;
+    }
+  }
   if (f) launch_sweep<TC, TN, TA, kSwResidual>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
   else launch_sweep<TC, TN, TA, kSwApply>(g, coeff, cl, u, ul, f, y, nullptr, nullptr, s);
 }
 
 long long launch_l0_defect_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
                                  ZLink<double> ul, const double* f, float* r32, double* partials, cudaStream_t s) {
+  if (hsweep_ok(g, false))
+    return launch_hsweep<float, double, kSwDefect, false>(g, coeff, cl, u, ul, f, nullptr, r32, partials, nullptr, {},
+                                                          nullptr, s);
   return launch_sweep<float, double, double, kSwDefect>(g, coeff, cl, u, ul, f, nullptr, r32, partials, s);
 }
 
 long long launch_l0_defect_update_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const double* u,
                                         ZLink<double> ul, const float* e, ZLink<float> el, double* unew,
                                         const double* f, float* r32, double* partials, cudaStream_t s) {
+  if (hsweep_ok(g, false))
+    return launch_hsweep<float, double, kSwDefect, true>(g, coeff, resolve(cl, coeff), u, resolve(ul, u), f, nullptr,
+                                                         r32, partials, e, resolve(el, e), unew, s);
   const int tz = sweep_tz(g);
   const dim3 gr(g.n[0] / kSwTX, g.n[1] / kSwTY, g.n[2] / tz);
   constexpr size_t sm = sweep_smem<double, float>() + sizeof(float) * kSwURing * kSwUSlot;

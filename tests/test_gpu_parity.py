@@ -51,7 +51,7 @@ def make_hom(ih, n, precision, penal=3.0, tol=1e-2, max_cycles=50, mode="vcycle"
 
 
 @pytest.mark.parametrize("precision,tol", [("double", 1e-12), ("mixed", 2e-6)])
-@pytest.mark.parametrize("n", [8, 16, (10, 8, 12), (5, 7, 9), 64])
+@pytest.mark.parametrize("n", [8, 16, (10, 8, 12), (5, 7, 9), 64, (64, 32, 32), (64, 48, 32)])
 def test_level0_apply_residual(ih, orc, precision, tol, n):
     nv = int(np.prod(n)) if not np.isscalar(n) else n ** 3
     rho = mt_uniform(nv, 1, 1e-3, 1.0)

@@ -53,7 +53,7 @@ struct HsGeom {
 
 template <typename TN, int BY, bool FUSE>
 constexpr int hs_ring() {
-  return FUSE ? 5 : 3;
+  return 3;  // planes s (read), s + 1 (landing), s + 2 (issued into the slot of s - 1)
 }
 template <typename TN, int BY, bool FUSE>
 constexpr size_t hs_smem() {
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
   // loader bookkeeping, fixed for the march: the window items this thread copies
   unsigned lE[Geo::per], lO[Geo::per];
   int lS[Geo::per];
+  [[maybe_unused]] bool lOwn[Geo::per];
 #pragma unroll
   for (int r = 0; r < Geo::per; ++r) {
     const int v = tid + r * kHsX * BY;
@@ -93,18 +94,19 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
       const int i = v % kHsWX, j = v / kHsWX;
       const int x = wrapc(X0 - 1 + i, g.n[0]), yy = wrapc(Y0 - 1 + j, g.n[1]);
       lS[r] = 3 * v;
+      lOwn[r] = i >= 1 && i <= kHsOX && j >= 1 && j <= BY - 1 && X0 - 1 + i < g.n[0] && Y0 - 1 + j < g.n[1];
       lE[r] = vloc(g, x, yy, 0);
       lO[r] = vloc(g, x, yy, 1);
     }
   }
-  auto load_plane = [&](int s) {  // window plane s <-> local vertex plane Z0 - 1 + s
+  auto load_plane = [&](int s, int slot) {  // window plane s <-> local vertex plane Z0 - 1 + s
     const int zl = Z0 - 1 + s;
     const TN* src = zl < 0 ? ul.lo : (zl >= t ? ul.hi : u);
     const float* esrc = nullptr;
     if constexpr (FUSE) esrc = zl < 0 ? el.lo : (zl >= t ? el.hi : e);
     const int z = zl < 0 ? zl + t : (zl >= t ? zl - t : zl);
     const unsigned zoff = (unsigned)(z >> 1) * plane;
-    TN* dst = us + (s % R) * SLOT;
+    TN* dst = us + slot * SLOT;
 #pragma unroll
     for (int r = 0; r < Geo::per; ++r)
       if (lS[r] >= 0) {
@@ -114,73 +116,89 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
         if constexpr (FUSE) {
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            __pipeline_memcpy_async(es + (s % R) * SLOT + lS[r] + c, esrc + gl + c, sizeof(float));
+            __pipeline_memcpy_async(es + slot * SLOT + lS[r] + c, esrc + gl + c, sizeof(float));
         }
       }
   };
-  auto fuse_plane = [&](int s) {  // this thread's landed items: u += double(e) (the axpy arithmetic)
+  int rs = 0;  // s % R (window slot of plane s)
+  int f3 = 0;  // s % 3 (f slot of output plane s - 3)
+  // FUSE: this thread's landed items of window plane s get u += double(e) (the axpy arithmetic); the
+  // items this CTA owns (interior columns, vertex planes Z0 .. Z0 + TZ - 1) also go to unew right here
+  auto fuse_plane = [&](int s) {
     if constexpr (FUSE) {
-      TN* up = us + (s % R) * SLOT;
-      const float* ep = es + (s % R) * SLOT;
+      TN* up = us + rs * SLOT;
+      const float* ep = es + rs * SLOT;
+      const int zl = Z0 - 1 + s;
+      const bool zown = s >= 1 && s <= TZ;
+      const unsigned zoff = (unsigned)(zl >> 1) * plane;
 #pragma unroll
       for (int r = 0; r < Geo::per; ++r)
         if (lS[r] >= 0) {
+          TN v[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) up[lS[r] + c] += double(ep[lS[r] + c]);
+          for (int c = 0; c < 3; ++c) v[c] = up[lS[r] + c] + double(ep[lS[r] + c]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) up[lS[r] + c] = v[c];
+          if (zown && lOwn[r]) {
+            const size_t gl = 3 * (size_t)((zl & 1 ? lO[r] : lE[r]) + zoff);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) unew[gl + c] = v[c];
+          }
         }
     }
   };
   // element coefficient of this thread's column, local element plane ez (>= -1)
   const int ex = wrapc(X0 - 1 + tx, g.n[0]), ey = wrapc(Y0 - 1 + ty, g.n[1]);
   const size_t exy = (size_t)ex + (size_t)g.n[0] * (size_t)ey, eplane = (size_t)g.n[0] * (size_t)g.n[1];
-  auto load_q = [&](int ez) -> TA {
+  auto load_q = [&](int ez) -> TC {  // raw: converted where used, so the load is not waited on here
     const TC* src = ez < 0 ? cl.lo : coeff;
     const int z = ez < 0 ? ez + t : ez;
-    return TA(__ldg(src + exy + (size_t)z * eplane));
+    return __ldg(src + exy + (size_t)z * eplane);
   };
-  TA qh_cls[kHadaClasses];
-#pragma unroll
-  for (int k = 0; k < kHadaClasses; ++k) qh_cls[k] = hada_class<TA>(k);
-
   const bool out_ok = tx < kHsOX && ty < BY - 1 && X0 + tx < g.n[0] && Y0 + ty < g.n[1];
   const int xg = X0 + tx, yg = Y0 + ty;
   const unsigned oE = out_ok ? vloc(g, xg, yg, 0) : 0u, oO = out_ok ? vloc(g, xg, yg, 1) : 0u;
   auto out_loc = [&](int z) { return (size_t)((z & 1 ? oO : oE) + (unsigned)(z >> 1) * plane); };
   // f of this thread's output vertex in plane k (local output index, finalised at step k + 3): copied
   // asynchronously two steps ahead with the window plane of that step (same commit group)
-  auto load_f = [&](int k) {
+  auto load_f = [&](int k, int slot) {
     if constexpr (OUT != kSwApply) {
       if (out_ok && k >= 0 && k < TZ) {
         const size_t loc = out_loc(Z0 + k);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          __pipeline_memcpy_async(fs + ((k % 3) * 3 + c) * BY * kHsX + tid, f + 3 * loc + c, sizeof(TN));
+          __pipeline_memcpy_async(fs + (slot * 3 + c) * BY * kHsX + tid, f + 3 * loc + c, sizeof(TN));
       }
     }
   };
 
-  load_plane(0);
+  load_plane(0, 0);
   __pipeline_commit();
-  load_plane(1);
+  load_plane(1, 1);
   __pipeline_commit();  // f of output planes 0 and 1 ride with window planes 2 and 3
-  TA qn = load_q(Z0 - 1);
-  TA Fp[12], Up[12], gyu[6];
+  TC qn = load_q(Z0 - 1);
+  // ping-pong register state: faces (this plane / the one below) and upper halves (new / pending)
+  TA FA[12], FB[12], UA[12], UB[12], gyu[6];
 #pragma unroll
-  for (int k = 0; k < 12; ++k) Fp[k] = Up[k] = TA(0);
+  for (int k = 0; k < 12; ++k) FA[k] = FB[k] = UA[k] = UB[k] = TA(0);
 #pragma unroll
   for (int k = 0; k < 6; ++k) gyu[k] = TA(0);
   double ss = 0.0;
-  const int last = TZ + 1;  // window planes 0 .. TZ + 1
-#pragma unroll 1
-  for (int s = 0; s <= TZ + 2; ++s) {
+  const int last = TZ + 1;  // window planes 0 .. TZ + 1; step s handles window plane s
+
+  // One step. FIN: finalise vertex plane Z0 + s - 3; ELEM: element plane Z0 + s - 2 (needs the face
+  // below, Fp); EXCH: its vertex plane Z0 + s - 2 is complete in z (needs the pending upper half Uo).
+  auto step = [&](int s, auto FIN, auto FACE, auto ELEM, auto EXCH, TA(&F)[12], const TA(&Fp)[12], TA(&Un)[12],
+                  const TA(&Uo)[12]) {
     __pipeline_wait_prior(1);  // window plane s and the f of output plane s - 3 have landed
-    if (s <= last) fuse_plane(s);
+    if constexpr (decltype(FACE)::value) fuse_plane(s);
     __syncthreads();
-    if (s + 2 <= last) load_plane(s + 2);
-    load_f(s - 1);  // finalised at step s + 2
+    const int rp2 = (rs + 2) % R;
+    if (s + 2 <= last) load_plane(s + 2, rp2);
+    load_f(s - 1, f3 == 0 ? 2 : f3 - 1);  // finalised at step s + 2
     __pipeline_commit();
-    // ---- finalise vertex plane Z0 + s - 3 (its y exchange was written in step s - 1)
-    if (s >= 3) {
+    if constexpr (decltype(FIN)::value) {
+      // ---- finalise vertex plane Z0 + s - 3 (its y exchange was written in step s - 1)
       const TN* xr = xb + ((s - 1) & 1) * 6 * BY * kHsX;
       const int tyn = ty + 1 < BY ? ty + 1 : ty;  // the last row produces no output
       TA ex6[6];
@@ -194,20 +212,14 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
         yv[c] = up + __shfl_down_sync(0xffffffffu, lo, 1);
       }
       if (out_ok) {
-        const int z = Z0 + s - 3;
-        const size_t loc = out_loc(z);
-        const TN* fr = fs + (((s - 3) % 3) * 3) * BY * kHsX + tid;
+        const size_t loc = out_loc(Z0 + s - 3);
+        [[maybe_unused]] const TN* fr = fs + (f3 * 3) * BY * kHsX + tid;
         if constexpr (OUT == kSwDefect) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const double r = double(fr[c * BY * kHsX]) - double(yv[c]);
             r32[3 * loc + c] = float(r);
             ss += r * r;
-          }
-          if constexpr (FUSE) {
-            const TN* pu = us + ((s - 2) % R) * SLOT + 3 * ((ty + 1) * kHsWX + tx + 1);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) unew[3 * loc + c] = pu[c];
           }
         } else if constexpr (OUT == kSwResidual) {
 #pragma unroll
@@ -218,12 +230,11 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
         }
       }
     }
-    if (s <= last) {
+    if constexpr (decltype(FACE)::value) {
       // ---- forward, face of window plane s: corners (tx, ty) .. (tx + 1, ty + 1)
-      const TN* p = us + (s % R) * SLOT + 3 * (ty * kHsWX + tx);
-      TA F[12];  // F[f*3+c], f = sx + 2 sy
+      const TN* p = us + rs * SLOT + 3 * (ty * kHsWX + tx);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < 3; ++c) {  // F[f*3+c], f = sx + 2 sy
         const TA a = TA(p[c]), b = TA(p[3 + c]), cc = TA(p[3 * kHsWX + c]), d = TA(p[3 * kHsWX + 3 + c]);
         const TA sx0 = b + a, dx0 = b - a, sx1 = d + cc, dx1 = d - cc;
         F[0 * 3 + c] = sx1 + sx0;
@@ -231,47 +242,63 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
         F[1 * 3 + c] = dx1 + dx0;
         F[3 * 3 + c] = dx1 - dx0;
       }
-      if (s >= 1) {
-        // ---- element plane Z0 + s - 2: u_hat from the faces below (Fp) and above (F)
-        const TA q = qn;
-        if (s + 1 <= last) qn = load_q(Z0 + s - 1);
-        TA uh[24];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          uh[k] = F[k] + Fp[k];
-          uh[12 + k] = F[k] - Fp[k];
-        }
-        TA qh[kHadaClasses];
-#pragma unroll
-        for (int k = 0; k < kHadaClasses; ++k) qh[k] = q * qh_cls[k];
-        TA w[24];
-        hada_apply<TA>(qh, uh, w);
-        // ---- inverse z: lower part -> vertex plane Z0 + s - 2, upper part -> Z0 + s - 1
-        TA gv[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          const TA S = k < 3 ? TA(0) : w[k], D = w[12 + k];
-          const TA lo = k < 3 ? -D : S - D;
-          gv[k] = Up[k] + lo;
-          Up[k] = k < 3 ? D : S + D;
-        }
-        if (s >= 2) {
-          // ---- inverse y of vertex plane Z0 + s - 2: keep the upper half, publish the lower
-          TN* xw = xb + (s & 1) * 6 * BY * kHsX;
-#pragma unroll
-          for (int tx_ = 0; tx_ < 2; ++tx_)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const TA S = gv[tx_ * 3 + c], D = gv[(2 + tx_) * 3 + c];
-              gyu[tx_ * 3 + c] = S + D;
-              xw[((tx_ * 3 + c) * BY + ty) * kHsX + tx] = TN(S - D);
-            }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 12; ++k) Fp[k] = F[k];
     }
+    if constexpr (decltype(ELEM)::value) {
+      // ---- element plane Z0 + s - 2: u_hat from the faces below (Fp) and above (F)
+      const TA q = TA(qn);
+      if (s + 1 <= last) qn = load_q(Z0 + s - 1);
+      TA uh[24];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        uh[k] = F[k] + Fp[k];
+        uh[12 + k] = F[k] - Fp[k];
+      }
+      TA qh[kHadaClasses];
+#pragma unroll
+      for (int k = 0; k < kHadaClasses; ++k) qh[k] = q * hada_class<TA>(k);
+      TA w[24];
+      hada_apply<TA>(qh, uh, w);
+      // ---- inverse z: lower part -> vertex plane Z0 + s - 2, upper part -> Z0 + s - 1 (pending)
+      TA gv[12];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        const TA S = k < 3 ? TA(0) : w[k], D = w[12 + k];
+        gv[k] = Uo[k] + (k < 3 ? -D : S - D);
+        Un[k] = k < 3 ? D : S + D;
+      }
+      if constexpr (decltype(EXCH)::value) {
+        // ---- inverse y of vertex plane Z0 + s - 2: keep the upper half, publish the lower
+        TN* xw = xb + (s & 1) * 6 * BY * kHsX;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const TA S = gv[h * 3 + c], D = gv[(2 + h) * 3 + c];
+            gyu[h * 3 + c] = S + D;
+            xw[((h * 3 + c) * BY + ty) * kHsX + tx] = TN(S - D);
+          }
+      }
+    }
+    rs = rs + 1 == R ? 0 : rs + 1;
+    f3 = f3 == 2 ? 0 : f3 + 1;
+  };
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  step(0, F_{}, T_{}, F_{}, F_{}, FA, FB, UA, UB);
+  step(1, F_{}, T_{}, T_{}, F_{}, FB, FA, UB, UA);
+  step(2, F_{}, T_{}, T_{}, T_{}, FA, FB, UA, UB);
+  // steady state: steps 3 .. last, two per iteration (the register roles alternate)
+  int s = 3;
+#pragma unroll 1
+  for (; s + 1 <= last; s += 2) {
+    step(s, T_{}, T_{}, T_{}, T_{}, FB, FA, UB, UA);
+    step(s + 1, T_{}, T_{}, T_{}, T_{}, FA, FB, UA, UB);
   }
+  if (s <= last) {
+    step(s, T_{}, T_{}, T_{}, T_{}, FB, FA, UB, UA);
+    ++s;
+  }
+  step(s, T_{}, F_{}, F_{}, F_{}, FA, FB, UA, UB);  // s == last + 1: finalise the top plane
   __pipeline_wait_prior(0);
   if constexpr (OUT == kSwDefect) {
 #pragma unroll

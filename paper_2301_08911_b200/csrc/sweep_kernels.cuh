@@ -585,7 +585,7 @@ template <typename TC, typename TN, typename TA>
 void launch_l0_apply_sweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul, const TN* f,
                            TN* y, cudaStream_t s) {
   if constexpr (std::is_same_v<TC, float> && std::is_same_v<TN, float> && std::is_same_v<TA, float>) {
-    if (sweep2_ok(g)) {
+    if (sweep2_ok(g) && !hsweep_ok(g, true)) {
       const long long cols = (long long)(g.n[0] / (2 * kSwTX)) * (g.n[1] / kSwTY);
       int tz = g.n[2];
       while (tz % 4 == 0 && tz > 8 && cols * (g.n[2] / tz) < 148LL * 2 * 4) tz /= 2;  // stays even

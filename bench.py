@@ -282,10 +282,12 @@ def run_ours(args):
                 "bytes_per_launch": ent["bytes"] / max(1, ent["launches"]),
                 "avg_launch_ms": ent["ms"] / max(1, ent["launches"]),
                 "traffic": ncu_traffic(fam, args.reso)}
-    # kernels whose real bound is a compute pipe, not HBM: f64 flops per unit (SASS count: the sweep f64
-    # residual runs 267 DFMA + 68 DADD per vertex) against the measured FP64 peak (DFMA 63.1/clk/SM,
-    # tools/microbench_pipes.cu, x 148 SMs x 1965 MHz x 2 flops = 36.7 TFLOP/s)
-    fp64_units = {"l0_residual_f64": (2 * 267 + 68, m)}  # m: this rank's vertices
+    # kernels whose real bound is a compute pipe, not HBM: f64 flops per unit against the measured FP64
+    # peak (DFMA 63.1/clk/SM, tools/microbench_pipes.cu, x 148 SMs x 1965 MHz x 2 flops = 36.7 TFLOP/s).
+    # The sum-factorised element sweep (hsweep_kernels.cuh) executes 100.6 DADD + 20.7 DMUL + 29.1 DFMA
+    # per element and plane step (ncu SASS counts, profiles/ncu_r01d_hsweep.md) = 180 flops per vertex;
+    # the vertex-stencil form it replaced ran 267 DFMA + 68 DADD = 602.
+    fp64_units = {"l0_residual_f64": (180, m)}  # m: this rank's vertices
     if fam in fp64_units:
         fl, units = fp64_units[fam]
         tf = fl * units / (ent["ms"] / max(1, ent["launches"]) * 1e-3) / 1e12

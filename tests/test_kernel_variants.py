@@ -1,4 +1,4 @@
-"""Kernel variants are bit-identical.
+"""Kernel variants are bit-identical, except the sum-factorised sweep (tolerance).
 
 The paired level-0 f32 kernels (two z-stacked vertices per thread in float2
 FFMA2/FADD2/FMUL2 arithmetic) must reproduce the scalar kernels bit for bit:
@@ -12,6 +12,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
+    # the bitwise comparisons below are between stencil-form variants: the sum-factorised element
+    # sweep (HSWEEP*, a different association of the same sums) is compared at tolerance separately
+    knobs = {"HSWEEP": 0, "HSWEEP32": 0, **knobs}
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)

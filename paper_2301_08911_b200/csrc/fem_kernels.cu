@@ -55,6 +55,7 @@ void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t
   }
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hada_d, hd, sizeof(hd), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hada_f, hf, sizeof(hf), 0, cudaMemcpyHostToDevice, s));
+  upload_hom_tables(hd, s);
   IHOM_CUDA(cudaStreamSynchronize(s));
 }
 

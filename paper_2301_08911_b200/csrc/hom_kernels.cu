@@ -11,6 +11,7 @@
 // costs ~2.7k flop/element instead of the 3.5k+ of the dense 24x24x6 product.
 // Mixed mode reads u through a float snapshot (src/homogenization.cpp:84-85).
 #include "kernels.hpp"
+#include "hada_gen.cuh"
 
 namespace ihomgpu {
 
@@ -19,17 +20,8 @@ constexpr int kGradPerLoad = 36;   // 3 comps x 3 directions x 4 points
 
 __device__ __forceinline__ int wrapp(int c, int n) { return c >= n ? c - n : c; }
 
-// Computes the 21 upper-triangle energies for element (ex,ey,ez) in arithmetic
-// type TE (f64 all-double; f32 in mixed mode, where u is read through the
-// reference's f32 snapshot anyway). gs: per-thread smem slice, stride kHT.
-// z-slab: the upper vertex plane of the top element layer belongs to the slab
-// above (uhi).
-template <typename TN, typename TE>
-__device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const TN* const* u, const TN* const* uhi,
-                                 bool snap, TE lam, TE mu, TE* gs, TE E[21]) {
-  const TE p1 = TE(0.5 + 0.5 / 1.7320508075688772);  // gp[1]; N_a(g) = (a == g) ? p1 : p0
-  const TE p0 = TE(0.5 - 0.5 / 1.7320508075688772);
-  unsigned loc[8];
+// Locations of the 8 corners of element (ex, ey, ez) (x fastest), periodic wrap.
+__device__ __forceinline__ void corner_locs(const GridGeo& g, int ex, int ey, int ez, unsigned loc[8]) {
   if (g.n[0] % 2 == 0 && g.n[1] % 2 == 0 && g.n[2] % 2 == 0) {
     // even grid: every colour block has the same dims, so a corner's location is a sum of one
     // per-axis term (colour bit folded in): 6 small tables instead of 8 generic vloc() calls
@@ -51,6 +43,20 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
     for (int j = 0; j < 8; ++j)
       loc[j] = vloc(g, wrapp(ex + (j & 1), g.n[0]), wrapp(ey + ((j >> 1) & 1), g.n[1]), wrapp(ez + ((j >> 2) & 1), g.n[2]));
   }
+}
+
+// Computes the 21 upper-triangle energies for element (ex,ey,ez) in arithmetic
+// type TE (f64 all-double; f32 in mixed mode, where u is read through the
+// reference's f32 snapshot anyway). gs: per-thread smem slice, stride kHT.
+// z-slab: the upper vertex plane of the top element layer belongs to the slab
+// above (uhi).
+template <typename TN, typename TE>
+__device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const TN* const* u, const TN* const* uhi,
+                                 bool snap, TE lam, TE mu, TE* gs, TE E[21]) {
+  const TE p1 = TE(0.5 + 0.5 / 1.7320508075688772);  // gp[1]; N_a(g) = (a == g) ? p1 : p0
+  const TE p0 = TE(0.5 - 0.5 / 1.7320508075688772);
+  unsigned loc[8];
+  corner_locs(g, ex, ey, ez, loc);
   const bool top = ez + 1 == g.n[2];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -135,6 +141,104 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
   }
 }
 
+// ---------------------------------------------------------------- sum/difference-basis energies
+// K0 = Hb^T W Hb with W = D/8 the 45-term element stiffness in the per-axis sum/difference basis
+// (tools/gen_hada.py, hada_gen.cuh; Hb = per-component 8-point Walsh-Hadamard, H1 = [[1,1],[-1,1]]), so
+//   E_ij = d_i^T K0 d_j = d_hat_i^T W d_hat_j,   d_hat = Hb (chi^i - u^i) = chi_hat^i - Hb u^i.
+// Per element: 18 butterflies of 24 adds, 6 x 45 terms for W d_hat_j, 21 x 21-term dots (~1.2k flop,
+// no shared memory) instead of the quadrature's ~2.7k flop and 864 B of gradients per thread.
+// The all-sum entries (sigma = 0) drop out (W annihilates translations).
+__constant__ double c_hw_d[kHadaClasses];
+__constant__ float c_hw_f[kHadaClasses];
+__constant__ double c_chih_d[6][24];  // Hb chi^i, chi^i element-relative (src/material.cpp:71-82)
+__constant__ float c_chih_f[6][24];
+
+void upload_hom_tables(const double hada_classes[], cudaStream_t s) {
+  static double wd[kHadaClasses], cd[6][24];
+  static float wf[kHadaClasses], cf[6][24];
+  for (int k = 0; k < kHadaClasses; ++k) wd[k] = hada_classes[k], wf[k] = float(wd[k]);
+  for (int i = 0; i < 6; ++i)
+    for (int sg = 0; sg < 8; ++sg)
+      for (int c = 0; c < 3; ++c) {
+        double acc = 0.0;
+        for (int a = 0; a < 8; ++a) {
+          double chi[3];
+          macro_strain_displacement(i, a & 1, (a >> 1) & 1, (a >> 2) & 1, chi);
+          double h = 1.0;  // H1[s][a] = 1 for s = 0; -1 / +1 for s = 1 and a = 0 / 1, per axis
+          for (int k = 0; k < 3; ++k)
+            if ((sg >> k) & 1) h *= ((a >> k) & 1) ? 1.0 : -1.0;
+          acc += h * chi[c];
+        }
+        cd[i][sg * 3 + c] = acc;
+        cf[i][sg * 3 + c] = float(acc);
+      }
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hw_d, wd, sizeof(wd), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hw_f, wf, sizeof(wf), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_chih_d, cd, sizeof(cd), 0, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_chih_f, cf, sizeof(cf), 0, cudaMemcpyHostToDevice, s));
+}
+
+template <typename TE>
+__device__ __forceinline__ TE hw_class(int k) {
+  if constexpr (sizeof(TE) == 8) return c_hw_d[k];
+  else return c_hw_f[k];
+}
+template <typename TE>
+__device__ __forceinline__ TE chih(int i, int r) {
+  if constexpr (sizeof(TE) == 8) return c_chih_d[i][r];
+  else return c_chih_f[i][r];
+}
+
+template <typename TN, typename TE>
+__device__ void element_energies_hada(const GridGeo& g, int ex, int ey, int ez, const TN* const* u,
+                                      const TN* const* uhi, bool snap, TE E[21]) {
+  unsigned loc[8];
+  corner_locs(g, ex, ey, ez, loc);
+  const bool top = ez + 1 == g.n[2];
+  TE dh[6][24];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const TN* ui = u[i];
+    const TN* uz = top ? uhi[i] : u[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      TE V[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double v = double(((j >> 2) & 1 ? uz : ui)[3 * (size_t)loc[j] + c]);
+        V[j] = snap ? TE(float(v)) : TE(v);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k)  // in-place butterflies: slot bit k = sigma_k (0 sum, 1 difference)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (!((j >> k) & 1)) {
+            const TE a = V[j], b = V[j | (1 << k)];
+            V[j] = b + a;
+            V[j | (1 << k)] = b - a;
+          }
+#pragma unroll
+      for (int sg = 1; sg < 8; ++sg) dh[i][sg * 3 + c] = chih<TE>(i, sg * 3 + c) - V[sg];
+      dh[i][c] = TE(0);  // all-sum entry: never read by W
+    }
+  }
+  TE qh[kHadaClasses];
+#pragma unroll
+  for (int k = 0; k < kHadaClasses; ++k) qh[k] = hw_class<TE>(k);
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    TE t[24];
+    hada_apply<TE>(qh, dh[j], t);
+#pragma unroll
+    for (int i = 0; i <= j; ++i) {
+      TE acc = dh[i][3] * t[3];
+#pragma unroll
+      for (int r = 4; r < 24; ++r) acc = fma(dh[i][r], t[r], acc);
+      E[i * 6 - i * (i - 1) / 2 + (j - i)] = acc;  // upper-triangle row-major (i <= j)
+    }
+  }
+}
+
 __device__ __forceinline__ double block_reduce_h(double v, double* sh) {
   const int t = threadIdx.x;
 #pragma unroll
@@ -156,7 +260,7 @@ struct U6 {
   const void* hi[6];  // z-slab: the same fields of the slab above (== p for one periodic domain)
 };
 
-template <typename TN, typename TE>
+template <typename TN, typename TE, bool HADA>
 __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                      bool snap, double lam, double mu, double* partials,
                                                      TE* __restrict__ ecache) {
@@ -178,7 +282,8 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
     const long long r = e / g.n[0];
     const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
     TE E[21];
-    element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
+    if constexpr (HADA) element_energies_hada<TN, TE>(g, ex, ey, ez, u, uh, snap, E);
+    else element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
     if (ecache) {  // [21][nv]: the sensitivity pass reuses these instead of recomputing them
 #pragma unroll
       for (int k = 0; k < 21; ++k) ecache[k * g.nv + e] = E[k];
@@ -204,6 +309,8 @@ __global__ void tensor_finalize(const double* partials, int nparts, double* out)
   }
 }
 
+static bool htensor() { return knob("HTENSOR", 1) != 0; }
+
 static size_t grad_smem(bool f32) { return (f32 ? sizeof(float) : sizeof(double)) * 6 * kGradPerLoad * kHT; }
 
 static void set_smem(const void* fn, bool f32) {
@@ -221,21 +328,30 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
     uu.p[i] = u[i];
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
-  if (snap) {
-    set_smem((const void*)tensor_kernel<TN, float>, true);
-    tensor_kernel<TN, float><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu, partials,
-                                                                             static_cast<float*>(ecache));
+  if (htensor()) {  // sum/difference-basis energies: no gradient scratch in shared memory
+    if (snap)
+      tensor_kernel<TN, float, true><<<(unsigned)blocks, kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, partials,
+                                                                      static_cast<float*>(ecache));
+    else
+      tensor_kernel<TN, double, true><<<(unsigned)blocks, kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, partials,
+                                                                       static_cast<double*>(ecache));
+  } else if (snap) {
+    set_smem((const void*)tensor_kernel<TN, float, false>, true);
+    tensor_kernel<TN, float, false><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                                    partials,
+                                                                                    static_cast<float*>(ecache));
   } else {
-    set_smem((const void*)tensor_kernel<TN, double>, false);
-    tensor_kernel<TN, double><<<(unsigned)blocks, kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                               partials, static_cast<double*>(ecache));
+    set_smem((const void*)tensor_kernel<TN, double, false>, false);
+    tensor_kernel<TN, double, false><<<(unsigned)blocks, kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                                      partials,
+                                                                                      static_cast<double*>(ecache));
   }
   IHOM_LAUNCH_CHECK();
   tensor_finalize<<<1, 256, 0, s>>>(partials, (int)blocks, c21);
   IHOM_LAUNCH_CHECK();
 }
 
-template <typename TN, typename TE>
+template <typename TN, typename TE, bool HADA>
 __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                    bool snap, double lam, double mu, const double* __restrict__ seed,
                                                    double inv_m, double* __restrict__ out) {
@@ -254,7 +370,8 @@ __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const doubl
   const long long r = e / g.n[0];
   const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
   TE E[21];
-  element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
+  if constexpr (HADA) element_energies_hada<TN, TE>(g, ex, ey, ez, u, uh, snap, E);
+  else element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);
   double acc = 0.0;  // sum_ij s_ij E_ij with s symmetric (src/homogenization.cpp:120,138-140)
   int q = 0;
 #pragma unroll
@@ -301,14 +418,21 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
   const double inv_m = 1.0 / double(m_total > 0 ? m_total : g.nv);
-  if (snap) {
-    set_smem((const void*)sens_kernel<TN, float>, true);
-    sens_kernel<TN, float><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                             sym_seed36, inv_m, out);
+  if (htensor()) {
+    if (snap)
+      sens_kernel<TN, float, true><<<ceil_div(g.nv, kHT), kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36,
+                                                                       inv_m, out);
+    else
+      sens_kernel<TN, double, true><<<ceil_div(g.nv, kHT), kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36,
+                                                                        inv_m, out);
+  } else if (snap) {
+    set_smem((const void*)sens_kernel<TN, float, false>, true);
+    sens_kernel<TN, float, false><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
+                                                                                    sym_seed36, inv_m, out);
   } else {
-    set_smem((const void*)sens_kernel<TN, double>, false);
-    sens_kernel<TN, double><<<ceil_div(g.nv, kHT), kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam, mu,
-                                                                               sym_seed36, inv_m, out);
+    set_smem((const void*)sens_kernel<TN, double, false>, false);
+    sens_kernel<TN, double, false><<<ceil_div(g.nv, kHT), kHT, grad_smem(false), s>>>(g, uu, rho, penal, snap, lam,
+                                                                                      mu, sym_seed36, inv_m, out);
   }
   IHOM_LAUNCH_CHECK();
 }

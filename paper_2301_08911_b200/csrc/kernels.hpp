@@ -18,6 +18,7 @@ namespace ihomgpu {
 // ---- constant tables (one upload per material; cheap, idempotent) ----
 void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t s);
 void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s);
+void upload_hom_tables(const double hada_classes[], cudaStream_t s);  // hom_kernels.cu (from upload_fem_tables)
 
 // ---- level 0, matrix-free (src/fem.cpp:98-156, src/multigrid.cpp:263-279) ----
 template <typename TC>

@@ -857,83 +857,119 @@ double Hierarchy<T>::finish_defect_cycle() {
   return norm(L0.r.p, n0);
 }
 
-// ---------------------------------------------------------------- lockstep RHS pairs
+// ---------------------------------------------------------------- lockstep RHS groups
 template <typename T>
 bool Hierarchy<T>::pair_ok(const SolverOptions& opts) const {
   return std::is_same_v<T, float> && opts.mode == kMixedDefect && knob("RHS_PAIRS", 1) != 0 &&
          fast_ok(levels_[0].g) && num_levels() > 1;
 }
 
+// RHS_GROUP = 2, 3 or 6 forces the group size; 0 (default) picks the largest of 6, 3, 2 whose extra
+// per-RHS fields fit in the free HBM next to a reserve for the energy cache and workspace (one domain
+// only: every z-slab must allocate the same slots, collectively, so slabs use pairs unless forced).
 template <typename T>
-void Hierarchy<T>::ensure_pair() {
-  if (other_.ready) return;
-  ensure_inner();
-  const size_t nl = levels_.size();
-  other_.eu.resize(nl);
-  other_.ef.resize(nl);
-  other_.er.resize(nl);
-  other_.eul.assign(nl, ZLink<float>{});
-  other_.erl.assign(nl, ZLink<float>{});
-  other_.efpeer.assign(nl, PeerTable{});
-  for (size_t l = 0; l < nl; ++l) {
-    const size_t n3 = size_t(3 * levels_[l].g.nv);
-    other_.eu[l].alloc(n3);
-    other_.ef[l].alloc(n3);
-    other_.er[l].alloc(n3);
+int Hierarchy<T>::group_size(const SolverOptions& opts) const {
+  if (!pair_ok(opts)) return 1;
+  const int forced = knob("RHS_GROUP", 0);
+  if (forced == 2 || forced == 3 || forced == 6) return forced;
+  if (slab_.on()) return 2;
+  double per_slot = 2.0 * 3.0 * 8.0 * double(levels_[0].g.nv);  // f64 f and ping-pong u at level 0
+  for (const Level& L : levels_) per_slot += 3.0 * 3.0 * 4.0 * double(L.g.nv);  // f32 e, f, r per level
+  size_t free_b = 0, total_b = 0;
+  IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double reserve = 21.0 * 8.0 * double(levels_[0].g.nv) + 8e9;  // energy cache (f64 worst case) + 8 GB
+  for (int g : {6, 3, 2}) {
+    const double extra = double(std::max(0, g - 1 - int(slots_.size()))) * per_slot;
+    if (extra + reserve <= double(free_b)) return g;
   }
-  other_.f0.alloc(size_t(3 * levels_[0].g.nv));
-  if (u_alt_.p) other_.ualt.alloc(size_t(3 * levels_[0].g.nv));
-  IHOM_CUDA(cudaDeviceSynchronize());
-  if (slab_.on()) {  // collective, same order on every slab (mirrors ensure_inner)
-    if (other_.ualt.p) other_.ualtl = link(other_.ualt.p);
-    for (size_t l = 0; l < nl; ++l) {
-      Level& L = levels_[l];
-      if (L.sharded) {
-        other_.eul[l] = link(other_.eu[l].p);
-        other_.erl[l] = link(other_.er[l].p);
-      } else if (int(l) == rep0_) {
-        other_.efpeer[l] = peer_table(slab_.fab->exchange(slab_.rank, other_.ef[l].p));
-      }
-    }
-  }
-  other_.ready = true;
+  return 2;
 }
 
 template <typename T>
-void Hierarchy<T>::select_rhs(int k) {
-  if (k == cur_rhs_) return;
-  ensure_pair();
+void Hierarchy<T>::ensure_group(int G) {
+  ensure_inner();
+  const size_t nl = levels_.size();
+  while (slots_.size() + 1 < size_t(G)) {
+    slots_.emplace_back();
+    RhsSlot& o = slots_.back();
+    o.eu.resize(nl);
+    o.ef.resize(nl);
+    o.er.resize(nl);
+    o.eul.assign(nl, ZLink<float>{});
+    o.erl.assign(nl, ZLink<float>{});
+    o.efpeer.assign(nl, PeerTable{});
+    for (size_t l = 0; l < nl; ++l) {
+      const size_t n3 = size_t(3 * levels_[l].g.nv);
+      o.eu[l].alloc(n3);
+      o.ef[l].alloc(n3);
+      o.er[l].alloc(n3);
+    }
+    o.f0.alloc(size_t(3 * levels_[0].g.nv));
+    if (u_alt_.p) o.ualt.alloc(size_t(3 * levels_[0].g.nv));
+    IHOM_CUDA(cudaDeviceSynchronize());
+    if (slab_.on()) {  // collective, same order on every slab (mirrors ensure_inner)
+      if (o.ualt.p) o.ualtl = link(o.ualt.p);
+      for (size_t l = 0; l < nl; ++l) {
+        Level& L = levels_[l];
+        if (L.sharded) {
+          o.eul[l] = link(o.eu[l].p);
+          o.erl[l] = link(o.er[l].p);
+        } else if (int(l) == rep0_) {
+          o.efpeer[l] = peer_table(slab_.fab->exchange(slab_.rank, o.ef[l].p));
+        }
+      }
+    }
+    o.ready = true;
+  }
+}
+
+template <typename T>
+void Hierarchy<T>::swap_live(RhsSlot& o) {
   for (size_t l = 0; l < levels_.size(); ++l) {
     Level& L = levels_[l];
-    std::swap(L.eu, other_.eu[l]);
-    std::swap(L.ef, other_.ef[l]);
-    std::swap(L.er, other_.er[l]);
-    std::swap(L.eul, other_.eul[l]);
-    std::swap(L.erl, other_.erl[l]);
-    std::swap(L.efpeer, other_.efpeer[l]);
+    std::swap(L.eu, o.eu[l]);
+    std::swap(L.ef, o.ef[l]);
+    std::swap(L.er, o.er[l]);
+    std::swap(L.eul, o.eul[l]);
+    std::swap(L.erl, o.erl[l]);
+    std::swap(L.efpeer, o.efpeer[l]);
   }
-  std::swap(levels_[0].f, other_.f0);
-  std::swap(u_alt_, other_.ualt);
-  std::swap(u_alt_l_, other_.ualtl);
-  std::swap(u0_bound_, other_.u0_bound);
-  std::swap(u_home_, other_.u_home);
-  std::swap(u0l_, other_.u0l);
-  std::swap(u_home_l_, other_.u_home_l);
-  std::swap(fnorm0_, other_.fnorm0);
+  std::swap(levels_[0].f, o.f0);
+  std::swap(u_alt_, o.ualt);
+  std::swap(u_alt_l_, o.ualtl);
+  std::swap(u0_bound_, o.u0_bound);
+  std::swap(u_home_, o.u_home);
+  std::swap(u0l_, o.u0l);
+  std::swap(u_home_l_, o.u_home_l);
+  std::swap(fnorm0_, o.fnorm0);
+}
+
+// RHS k's fields become the live level fields; the previous live RHS takes k's slot.
+template <typename T>
+void Hierarchy<T>::select_rhs(int k) {
+  if (k == cur_rhs_) return;
+  if (k < 0 || k >= kMaxRhsGroup) throw std::logic_error("right-hand side index out of range");
+  ensure_group(k + 1);
+  const int j = where_[k];
+  swap_live(slots_[size_t(j)]);
+  where_[cur_rhs_] = j;
+  where_[k] = -1;
   cur_rhs_ = k;
 }
 
 template <typename T>
-void Hierarchy<T>::relax_f32_pair(int l, int sweeps, bool zero_start) {
+void Hierarchy<T>::relax_f32_group(int G, int l, int sweeps, bool zero_start) {
   Level& L = levels_[size_t(l)];
-  if (l == 0) throw std::logic_error("paired sweeps run on the stencil levels");
-  const int cur = cur_rhs_, oth = 1 - cur_rhs_;
-  float* u[2];
-  const float* f[2];
-  ZLink<float> ul[2];
-  u[cur] = L.eu.p, u[oth] = other_.eu[size_t(l)].p;
-  f[cur] = L.ef.p, f[oth] = other_.ef[size_t(l)].p;
-  ul[cur] = L.eul, ul[oth] = other_.eul[size_t(l)];
+  if (l == 0) throw std::logic_error("grouped sweeps run on the stencil levels");
+  float* u[kMaxRhsGroup];
+  const float* f[kMaxRhsGroup];
+  ZLink<float> ul[kMaxRhsGroup];
+  for (int k = 0; k < G; ++k) {
+    RhsSlot* o = slot_of(k);
+    u[k] = o ? o->eu[size_t(l)].p : L.eu.p;
+    f[k] = o ? o->ef[size_t(l)].p : L.ef.p;
+    ul[k] = o ? o->eul[size_t(l)] : L.eul;
+  }
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
@@ -941,41 +977,43 @@ void Hierarchy<T>::relax_f32_pair(int l, int sweeps, bool zero_start) {
       const bool zs = zero_start && sw == 0;
       if constexpr (std::is_same_v<T, float>) {
         ProfScope p(s_, l == 1 ? "l1_gs_f32" : (l == 2 ? "l2_gs_f32" : "coarse_gs_f32"),
-                    (zs ? gs_coarse_bytes_zs(L.g, c, 8, 4) : gs_coarse_bytes(L.g, c, 8, 4)));
-        launch_stencil_gs_color_pair<float, float>(L.g, L.st.p, f, u, c, err_.p, s_, ul, zs);
+                    (zs ? gs_coarse_bytes_zs(L.g, c, 4.0 * G, 4) : gs_coarse_bytes(L.g, c, 4.0 * G, 4)));
+        launch_stencil_gs_color_group<float, float>(L.g, L.st.p, G, f, u, c, err_.p, s_, ul, zs);
       }
       ++launches_;
     }
 }
 
 template <typename T>
-void Hierarchy<T>::residual_f32_pair(int l) {
+void Hierarchy<T>::residual_f32_group(int G, int l) {
   Level& L = levels_[size_t(l)];
   if (L.sharded) sync();
-  const int cur = cur_rhs_, oth = 1 - cur_rhs_;
-  const float* x[2];
-  const float* f[2];
-  float* y[2];
-  ZLink<float> xl[2];
-  x[cur] = L.eu.p, x[oth] = other_.eu[size_t(l)].p;
-  f[cur] = L.ef.p, f[oth] = other_.ef[size_t(l)].p;
-  y[cur] = L.er.p, y[oth] = other_.er[size_t(l)].p;
-  xl[cur] = L.eul, xl[oth] = other_.eul[size_t(l)];
+  const float* x[kMaxRhsGroup];
+  const float* f[kMaxRhsGroup];
+  float* y[kMaxRhsGroup];
+  ZLink<float> xl[kMaxRhsGroup];
+  for (int k = 0; k < G; ++k) {
+    RhsSlot* o = slot_of(k);
+    x[k] = o ? o->eu[size_t(l)].p : L.eu.p;
+    f[k] = o ? o->ef[size_t(l)].p : L.ef.p;
+    y[k] = o ? o->er[size_t(l)].p : L.er.p;
+    xl[k] = o ? o->eul[size_t(l)] : L.eul;
+  }
   if constexpr (std::is_same_v<T, float>) {
     ProfScope p(s_, l == 1 ? "l1_residual_f32" : (l == 2 ? "l2_residual_f32" : "coarse_residual_f32"),
-                resid_coarse_bytes(L.g, 8, 4, true));
-    launch_stencil_apply_pair<float, float>(L.g, L.st.p, x, f, y, s_, xl);
+                resid_coarse_bytes(L.g, 4.0 * G, 4, true));
+    launch_stencil_apply_group<float, float>(L.g, L.st.p, G, x, f, y, s_, xl);
   }
   ++launches_;
 }
 
 // One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
-// converged) skips every level-0 and transfer step; the paired coarse kernels still compute its lane
+// converged) skips every level-0 and transfer step; the grouped coarse kernels still compute its lane
 // on stale (finite) data, which nothing reads.
 template <typename T>
-void Hierarchy<T>::inner_vcycle_pair(const SolverOptions& opts, const bool act[2]) {
+void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < G; ++k)
     if (act[k]) {
       select_rhs(k);
       inner_down(0, opts);
@@ -983,32 +1021,32 @@ void Hierarchy<T>::inner_vcycle_pair(const SolverOptions& opts, const bool act[2
   for (int l = 1; l < lmax; ++l) {
     const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
     if (!zs)
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < G; ++k) {
         select_rhs(k);
         IHOM_CUDA(cudaMemsetAsync(levels_[size_t(l)].eu.p, 0, sizeof(float) * 3 * levels_[size_t(l)].g.nv, s_));
       }
-    relax_f32_pair(l, opts.pre_sweeps, zs);
-    residual_f32_pair(l);
-    for (int k = 0; k < 2; ++k)
+    relax_f32_group(G, l, opts.pre_sweeps, zs);
+    residual_f32_group(G, l);
+    for (int k = 0; k < G; ++k)
       if (act[k]) {
         select_rhs(k);
         restrict_to_f32(l);
       }
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < G; ++k)
     if (act[k]) {
       select_rhs(k);
       inner_coarsest();
     }
   for (int l = lmax - 1; l >= 1; --l) {
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < G; ++k)
       if (act[k]) {
         select_rhs(k);
         inner_prolong(l);
       }
-    relax_f32_pair(l, opts.post_sweeps, false);
+    relax_f32_group(G, l, opts.post_sweeps, false);
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < G; ++k)
     if (act[k]) {
       select_rhs(k);
       inner_prolong(0);
@@ -1017,16 +1055,22 @@ void Hierarchy<T>::inner_vcycle_pair(const SolverOptions& opts, const bool act[2
 }
 
 template <typename T>
-void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opts, const ZLink<double> ul[2],
-                                    SolveStats st[2]) {
+void Hierarchy<T>::solve_bound_group(int G, double* const* u, const SolverOptions& opts, const ZLink<double>* ul,
+                                     SolveStats* st) {
   if (!density_set_) throw StateError("set_density before solve");
-  if (!pair_ok(opts)) throw std::logic_error("lockstep pair solve needs mixed precision, mixed_defect and an even grid");
-  ensure_pair();
+  if (!pair_ok(opts)) throw std::logic_error("lockstep group solve needs mixed precision, mixed_defect and an even grid");
+  if (G < 1 || G > kMaxRhsGroup) throw std::invalid_argument("right-hand-side group size must be in [1, 6]");
+  ensure_group(G);
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
-  bool act[2] = {false, false}, negligible[2] = {false, false};
+  bool act[kMaxRhsGroup] = {}, negligible[kMaxRhsGroup] = {};
+  auto any = [&] {
+    for (int k = 0; k < G; ++k)
+      if (act[k]) return true;
+    return false;
+  };
   try {
-    for (int k = 0; k < 2; ++k) {  // src/multigrid.cpp:474-501 prologue, per RHS
+    for (int k = 0; k < G; ++k) {  // src/multigrid.cpp:474-501 prologue, per RHS
       select_rhs(k);
       if (slab_.on() && is_self(ul[k], u[k])) throw std::invalid_argument("z-slab solve needs the links of the bound field");
       st[k] = SolveStats{};
@@ -1045,9 +1089,9 @@ void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opt
       st[k].rel_residual = defect_residual() / fnorm0_;
       act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
     }
-    while (act[0] || act[1]) {
-      inner_vcycle_pair(opts, act);
-      for (int k = 0; k < 2; ++k)
+    while (any()) {
+      inner_vcycle_group(G, opts, act);
+      for (int k = 0; k < G; ++k)
         if (act[k]) {
           select_rhs(k);
           const double rn = finish_defect_cycle();
@@ -1057,7 +1101,7 @@ void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opt
           act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
         }
     }
-    for (int k = 0; k < 2; ++k) {  // epilogue per RHS, as solve_bound
+    for (int k = 0; k < G; ++k) {  // epilogue per RHS, as solve_bound
       if (negligible[k]) continue;
       select_rhs(k);
       st[k].converged = st[k].rel_residual <= opts.tol;
@@ -1070,7 +1114,7 @@ void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opt
       }
     }
   } catch (...) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < G; ++k) {
       try {
         select_rhs(k);
         restore_home();
@@ -1082,7 +1126,7 @@ void Hierarchy<T>::solve_bound_pair(double* const u[2], const SolverOptions& opt
     select_rhs(0);
     throw;
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < G; ++k) {
     select_rhs(k);
     u0_bound_ = nullptr;
     u_home_ = nullptr;
@@ -1228,10 +1272,12 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   if (multi && slabs) throw std::invalid_argument("load-case split and z-slabs are exclusive");
   ecache_valid_ = false;
   double per[18] = {};  // per load: cycles, rel_residual, converged
-  if (!multi && hier_.pair_ok(opts_)) {
-    // loads (0,1), (2,3), (4,5) in lockstep: each pair streams the coarse stencils once
-    for (int i = 0; i < 6; i += 2) {
-      for (int k = 0; k < 2; ++k) {
+  const int G = multi ? 1 : hier_.group_size(opts_);
+  if (G > 1) {
+    // loads in lockstep groups of G ((0,1), (2,3), (4,5) for pairs): each group streams the coarse
+    // stencils once
+    for (int i = 0; i < 6; i += G) {
+      for (int k = 0; k < G; ++k) {
         hier_.select_rhs(k);
         hier_.sync();  // coefficients of the neighbouring slabs are current
         ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
@@ -1239,18 +1285,19 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
                               slabs ? hier_.coeff_link() : ZLink<T>{});
       }
       hier_.select_rhs(0);
-      double* const uu[2] = {u_[size_t(i)].p, u_[size_t(i + 1)].p};
-      const ZLink<double> ll[2] = {ul_[size_t(i)], ul_[size_t(i + 1)]};
-      SolveStats st[2];
-      hier_.solve_bound_pair(uu, opts_, ll, st);
-      for (int k = 0; k < 2; ++k) {
+      double* uu[kMaxRhsGroup];
+      ZLink<double> ll[kMaxRhsGroup];
+      for (int k = 0; k < G; ++k) uu[k] = u_[size_t(i + k)].p, ll[k] = ul_[size_t(i + k)];
+      SolveStats st[kMaxRhsGroup];
+      hier_.solve_bound_group(G, uu, opts_, ll, st);
+      for (int k = 0; k < G; ++k) {
         per[3 * (i + k)] = st[k].cycles;
         per[3 * (i + k) + 1] = st[k].rel_residual;
         per[3 * (i + k) + 2] = st[k].converged ? 1.0 : 0.0;
       }
     }
   }
-  for (int i = 0; i < 6 && !(!multi && hier_.pair_ok(opts_)); ++i) {
+  for (int i = 0; i < 6 && G == 1; ++i) {
     if (multi && owner_[i] != comm_->rank()) continue;
     hier_.sync();  // coefficients of the neighbouring slabs are current
     {

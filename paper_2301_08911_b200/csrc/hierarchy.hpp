@@ -137,14 +137,16 @@ class Hierarchy {
   // result buffer (bound as level-0 u for the duration of the call; ul = its
   // z-slab links).
   SolveStats solve_bound(double* u, const SolverOptions& opts, ZLink<double> ul = {});
-  // ---- lockstep pairs of right-hand sides (RHS_PAIRS): two cell problems share every coarse-level
-  // stencil read. The inactive RHS's per-RHS fields and solver state live in other_ and are swapped
-  // in by select_rhs(); every level-0 operation runs per RHS exactly as in a single solve.
+  // ---- lockstep groups of right-hand sides (RHS_PAIRS on; RHS_GROUP = 2, 3 or 6 cell problems): a
+  // group shares every coarse-level stencil read. The inactive RHSs' per-RHS fields and solver state
+  // live in slots_ and are swapped in by select_rhs(); every level-0 operation runs per RHS exactly as
+  // in a single solve.
   bool pair_ok(const SolverOptions& opts) const;
+  int group_size(const SolverOptions& opts) const;  // 1 (no grouping), 2, 3 or 6
   void select_rhs(int k);
   int current_rhs() const { return cur_rhs_; }
-  // solve K u_k = f_k for k = 0, 1 (f_k = level_f(0) of RHS k); stats per RHS, identical to two solve_bound calls
-  void solve_bound_pair(double* const u[2], const SolverOptions& opts, const ZLink<double> ul[2], SolveStats st[2]);
+  // solve K u_k = f_k for k < G (f_k = level_f(0) of RHS k); stats per RHS, identical to G solve_bound calls
+  void solve_bound_group(int G, double* const* u, const SolverOptions& opts, const ZLink<double>* ul, SolveStats* st);
 
 
   double* level_u(int l) { return l == 0 && u0_bound_ ? u0_bound_ : levels_[size_t(l)].u.p; }
@@ -235,7 +237,7 @@ class Hierarchy {
   double op_scale_ = 0.0;
   bool density_set_ = false;
   bool inner_ready_ = false;
-  struct RhsSlot {  // the other RHS of a lockstep pair (see select_rhs)
+  struct RhsSlot {  // another RHS of a lockstep group (see select_rhs)
     std::vector<DevBuf<float>> eu, ef, er;
     std::vector<ZLink<float>> eul, erl;
     std::vector<PeerTable> efpeer;
@@ -248,15 +250,18 @@ class Hierarchy {
     double fnorm0 = 0.0;
     bool ready = false;
   };
-  RhsSlot other_;
+  std::vector<RhsSlot> slots_;
+  int where_[6] = {-1, 0, 1, 2, 3, 4};  // slot holding RHS k's fields (-1: live in the levels)
   int cur_rhs_ = 0;
-  void ensure_pair();
+  void ensure_group(int G);
+  void swap_live(RhsSlot& o);
+  RhsSlot* slot_of(int k) { return k == cur_rhs_ ? nullptr : &slots_[size_t(where_[k])]; }
   void inner_down(int l, const SolverOptions& opts);  // pre-smooth, residual, restrict (current RHS)
   void inner_prolong(int l);                          // e_l += I e_{l+1} (current RHS)
   void inner_coarsest();
-  void inner_vcycle_pair(const SolverOptions& opts, const bool act[2]);
-  void relax_f32_pair(int l, int sweeps, bool zero_start);
-  void residual_f32_pair(int l);
+  void inner_vcycle_group(int G, const SolverOptions& opts, const bool* act);
+  void relax_f32_group(int G, int l, int sweeps, bool zero_start);
+  void residual_f32_group(int G, int l);
   double finish_defect_cycle();  // u += e (fused or not), the new residual; returns ||r||
   double* u0_bound_ = nullptr;
   double* u_home_ = nullptr;  // the caller's buffer of the current solve (u0_bound_ may be u_alt_)

@@ -81,14 +81,15 @@ void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN*
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
                              cudaStream_t s, ZLink<TN> ul = {}, bool zero_start = false);
-// the same for two right-hand sides in lockstep (each stencil block read once for both; per-RHS
-// arithmetic identical to the single launches)
+// the same for nl = 1, 2, 3 or 6 right-hand sides in lockstep (each stencil block read once for all;
+// per-RHS arithmetic identical to the single launches)
+constexpr int kMaxRhsGroup = 6;
 template <typename TS, typename TN>
-void launch_stencil_apply_pair(const GridGeo& g, const TS* st, const TN* const x[2], const TN* const f[2],
-                               TN* const y[2], cudaStream_t s, const ZLink<TN> xl[2]);
+void launch_stencil_apply_group(const GridGeo& g, const TS* st, int nl, const TN* const* x, const TN* const* f,
+                                TN* const* y, cudaStream_t s, const ZLink<TN>* xl);
 template <typename TS, typename TN>
-void launch_stencil_gs_color_pair(const GridGeo& g, const TS* st, const TN* const f[2], TN* const u[2], int color,
-                                  int* err, cudaStream_t s, const ZLink<TN> ul[2], bool zero_start = false);
+void launch_stencil_gs_color_group(const GridGeo& g, const TS* st, int nl, const TN* const* f, TN* const* u,
+                                   int color, int* err, cudaStream_t s, const ZLink<TN>* ul, bool zero_start = false);
 template <typename TC>
 void launch_galerkin_from_elements(const GridGeo& gf, const GridGeo& gc, const TC* coeff, TC* st, cudaStream_t s,
                                    ZLink<TC> cl = {}, const GridGeo* gout = nullptr, int zoff = 0);

@@ -200,16 +200,16 @@ void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* 
 }
 
 // ---------------------------------------------------------------- stencil apply / GS
-// One or two right-hand sides (NL) per launch: the stencil block of a neighbour is read and converted
-// once and applied to every RHS, so a pair of cell problems solved in lockstep streams the coarse
-// stencils (the dominant bytes of levels >= 1) once for both. Per RHS the arithmetic is the same
-// explicit fma chain for NL = 1 and 2, so a paired solve is bit-identical to two single ones.
+// NL = 1, 2, 3 or 6 right-hand sides per launch: the stencil block of a neighbour is read and
+// converted once and applied to every RHS, so a group of cell problems solved in lockstep streams the
+// coarse stencils (the dominant bytes of levels >= 1) once for all of them. Per RHS the arithmetic is
+// the same explicit fma chain for every NL, so a grouped solve is bit-identical to single ones.
 template <typename TN>
-struct Rhs2 {      // right-hand side k of a level: input field x (u of a GS pass), f, output y
-  const TN* x[2];
-  ZLink<TN> xl[2];
-  const TN* f[2];
-  TN* y[2];
+struct RhsN {      // right-hand side k of a level: input field x (u of a GS pass), f, output y
+  const TN* x[kMaxRhsGroup];
+  ZLink<TN> xl[kMaxRhsGroup];
+  const TN* f[kMaxRhsGroup];
+  TN* y[kMaxRhsGroup];
 };
 
 template <typename TS>
@@ -224,7 +224,7 @@ __device__ __forceinline__ void block_fma(const double c9[9], double a, double b
 
 // y = K x (f == nullptr) or y = f - K x; blocked stencil rows st_index(k, loc) (src/multigrid.cpp:186-205, 412-424).
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
+__global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (loc >= g.nv) return;
   const int color = color_at(g, loc);
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
 // Fast even-grid variants (FastAddr, common.cuh): one IADD3 per neighbour
 // location, AoS components at immediate offsets, blocked stencil rows.
 template <typename TS, typename TN, bool ZL, int NL>
-__global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
+__global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
   const int h2 = blockIdx.z >> 3;
@@ -311,7 +311,7 @@ __device__ __forceinline__ bool gs_solve_store(const double S[9], const double m
 }
 
 template <typename TS, typename TN, bool ZL, int NL>
-__global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
+__global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
                                                               int color, int* err, unsigned zm) {
   const int h2 = blockIdx.z;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
@@ -375,7 +375,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io) {
+__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
   const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (loc >= g.nv) return;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, cons
 }
 
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
+__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
                                                               int color, int* err, unsigned zm) {
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
 static long long warp_vmax() { return (long long)knob("WARP_VMAX", 4096); }
 
 template <typename TS, typename TN, int NL>
-static void launch_apply_n(const GridGeo& g, const TS* st, Rhs2<TN> io, cudaStream_t s) {
+static void launch_apply_n(const GridGeo& g, const TS* st, RhsN<TN> io, cudaStream_t s) {
   bool linked = false;
   for (int k = 0; k < NL; ++k) {
     linked = linked || !is_self(io.xl[k], io.x[k]);
@@ -465,20 +465,27 @@ static void launch_apply_n(const GridGeo& g, const TS* st, Rhs2<TN> io, cudaStre
 template <typename TS, typename TN>
 void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,
                           ZLink<TN> xl) {
-  Rhs2<TN> io{{x, nullptr}, {xl, {}}, {f, nullptr}, {y, nullptr}};
+  RhsN<TN> io{{x, nullptr}, {xl, {}}, {f, nullptr}, {y, nullptr}};
   launch_apply_n<TS, TN, 1>(g, st, io, s);
 }
 
 template <typename TS, typename TN>
-void launch_stencil_apply_pair(const GridGeo& g, const TS* st, const TN* const x[2], const TN* const f[2],
-                               TN* const y[2], cudaStream_t s, const ZLink<TN> xl[2]) {
-  Rhs2<TN> io{{x[0], x[1]}, {xl[0], xl[1]}, {f[0], f[1]}, {y[0], y[1]}};
-  launch_apply_n<TS, TN, 2>(g, st, io, s);
+void launch_stencil_apply_group(const GridGeo& g, const TS* st, int nl, const TN* const* x, const TN* const* f,
+                                TN* const* y, cudaStream_t s, const ZLink<TN>* xl) {
+  RhsN<TN> io{};
+  for (int k = 0; k < nl; ++k) io.x[k] = x[k], io.xl[k] = xl[k], io.f[k] = f[k], io.y[k] = y[k];
+  switch (nl) {
+    case 1: launch_apply_n<TS, TN, 1>(g, st, io, s); break;
+    case 2: launch_apply_n<TS, TN, 2>(g, st, io, s); break;
+    case 3: launch_apply_n<TS, TN, 3>(g, st, io, s); break;
+    case 6: launch_apply_n<TS, TN, 6>(g, st, io, s); break;
+    default: throw std::invalid_argument("right-hand-side group size must be 1, 2, 3 or 6");
+  }
 }
 
 // Colour pass of the coarse GS with the determinant check (src/multigrid.cpp:207-239).
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st, Rhs2<TN> io,
+__global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
                                                          int color, int* err, unsigned zm) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.size[color]) return;
@@ -507,7 +514,7 @@ __global__ void __launch_bounds__(128) stencil_gs_kernel(GridGeo g, const TS* __
 }
 
 template <typename TS, typename TN, int NL>
-static void launch_gs_n(const GridGeo& g, const TS* st, Rhs2<TN> io, int color, int* err, cudaStream_t s,
+static void launch_gs_n(const GridGeo& g, const TS* st, RhsN<TN> io, int color, int* err, cudaStream_t s,
                         bool zero_start) {
   bool linked = false;
   for (int k = 0; k < NL; ++k) {
@@ -532,15 +539,22 @@ static void launch_gs_n(const GridGeo& g, const TS* st, Rhs2<TN> io, int color, 
 template <typename TS, typename TN>
 void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u, int color, int* err,
                              cudaStream_t s, ZLink<TN> ul, bool zero_start) {
-  Rhs2<TN> io{{u, nullptr}, {ul, {}}, {f, nullptr}, {u, nullptr}};
+  RhsN<TN> io{{u, nullptr}, {ul, {}}, {f, nullptr}, {u, nullptr}};
   launch_gs_n<TS, TN, 1>(g, st, io, color, err, s, zero_start);
 }
 
 template <typename TS, typename TN>
-void launch_stencil_gs_color_pair(const GridGeo& g, const TS* st, const TN* const f[2], TN* const u[2], int color,
-                                  int* err, cudaStream_t s, const ZLink<TN> ul[2], bool zero_start) {
-  Rhs2<TN> io{{u[0], u[1]}, {ul[0], ul[1]}, {f[0], f[1]}, {u[0], u[1]}};
-  launch_gs_n<TS, TN, 2>(g, st, io, color, err, s, zero_start);
+void launch_stencil_gs_color_group(const GridGeo& g, const TS* st, int nl, const TN* const* f, TN* const* u,
+                                   int color, int* err, cudaStream_t s, const ZLink<TN>* ul, bool zero_start) {
+  RhsN<TN> io{};
+  for (int k = 0; k < nl; ++k) io.x[k] = u[k], io.xl[k] = ul[k], io.f[k] = f[k], io.y[k] = u[k];
+  switch (nl) {
+    case 1: launch_gs_n<TS, TN, 1>(g, st, io, color, err, s, zero_start); break;
+    case 2: launch_gs_n<TS, TN, 2>(g, st, io, color, err, s, zero_start); break;
+    case 3: launch_gs_n<TS, TN, 3>(g, st, io, color, err, s, zero_start); break;
+    case 6: launch_gs_n<TS, TN, 6>(g, st, io, color, err, s, zero_start); break;
+    default: throw std::invalid_argument("right-hand-side group size must be 1, 2, 3 or 6");
+  }
 }
 
 // ---------------------------------------------------------------- Galerkin assembly
@@ -983,12 +997,12 @@ INST_T(float)
 INST_S(float, double)
 INST_S(double, double)
 INST_S(float, float)
-template void launch_stencil_apply_pair<float, float>(const GridGeo&, const float*, const float* const[2],
-                                                      const float* const[2], float* const[2], cudaStream_t,
-                                                      const ZLink<float>[2]);
-template void launch_stencil_gs_color_pair<float, float>(const GridGeo&, const float*, const float* const[2],
-                                                         float* const[2], int, int*, cudaStream_t,
-                                                         const ZLink<float>[2], bool);
+template void launch_stencil_apply_group<float, float>(const GridGeo&, const float*, int, const float* const*,
+                                                       const float* const*, float* const*, cudaStream_t,
+                                                       const ZLink<float>*);
+template void launch_stencil_gs_color_group<float, float>(const GridGeo&, const float*, int, const float* const*,
+                                                          float* const*, int, int*, cudaStream_t,
+                                                          const ZLink<float>*, bool);
 #undef INST_S
 template void launch_galerkin_from_elements<float>(const GridGeo&, const GridGeo&, const float*, float*, cudaStream_t,
                                                    ZLink<float>, const GridGeo*, int);

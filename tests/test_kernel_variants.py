@@ -56,6 +56,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("FUSED_UPDATE", 1)
         ih.set_knob("GS_COL", 0)
         ih.set_knob("RHS_PAIRS", 1)
+        ih.set_knob("RHS_GROUP", 0)
         ih.set_knob("HSWEEP", 1)
         ih.set_knob("HSWEEP32", 1)
 
@@ -247,11 +248,12 @@ def test_rhs_pairs_bit_identical(ih, n, P):
     """Cell problems solved in lockstep pairs (coarse stencils streamed once per pair) == one by one:
     same cycle counts, tensors and displacements bit for bit."""
     base = _solve(ih, n, {"RHS_PAIRS": 0}, fabric_p=P)
-    v = _solve(ih, n, {"RHS_PAIRS": 1}, fabric_p=P)
-    assert v[0] == base[0]
-    np.testing.assert_array_equal(v[1], base[1])
-    for a, b in zip(v[2], base[2]):
-        np.testing.assert_array_equal(a, b)
+    for group in (2, 3, 6):  # lockstep pairs, triples, all six cell problems
+        v = _solve(ih, n, {"RHS_PAIRS": 1, "RHS_GROUP": group}, fabric_p=P)
+        assert v[0] == base[0], group
+        np.testing.assert_array_equal(v[1], base[1])
+        for a, b in zip(v[2], base[2]):
+            np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("n", [32, 64])

@@ -277,10 +277,30 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
   double acc[21];
 #pragma unroll
   for (int q = 0; q < 21; ++q) acc[q] = 0.0;
-  for (long long e = (long long)blockIdx.x * kHT + threadIdx.x; e < g.nv; e += (long long)gridDim.x * kHT) {
-    const int ex = int(e % g.n[0]);
-    const long long r = e / g.n[0];
-    const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
+  // HADA on x % 32 == 0, y % 2 == 0 grids: a block owns a 32 x 2 element column tile and marches up z,
+  // so the upper corner plane of one step is the lower plane of the next (L1/L2 hits instead of the
+  // grid-stride order's DRAM re-reads of neighbouring rows' corners)
+  const bool cols = HADA && g.n[0] % 32 == 0 && g.n[1] % 2 == 0;
+  const long long tiles_x = g.n[0] / 32, ntiles = cols ? tiles_x * (g.n[1] / 2) : 0;
+  const long long nsteps = cols ? ((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * g.n[2]
+                                : (g.nv - blockIdx.x * kHT + (long long)gridDim.x * kHT - 1) / ((long long)gridDim.x * kHT);
+  for (long long it = 0; it < nsteps; ++it) {
+    int ex, ey, ez;
+    long long e;
+    if (cols) {
+      const long long tile = blockIdx.x + (it / g.n[2]) * gridDim.x;
+      ez = int(it % g.n[2]);
+      ex = int(tile % tiles_x) * 32 + int(threadIdx.x & 31);
+      ey = int(tile / tiles_x) * 2 + int(threadIdx.x >> 5);
+      e = ex + (long long)g.n[0] * (ey + (long long)g.n[1] * ez);
+    } else {
+      e = (long long)blockIdx.x * kHT + threadIdx.x + it * (long long)gridDim.x * kHT;
+      if (e >= g.nv) break;
+      ex = int(e % g.n[0]);
+      const long long r = e / g.n[0];
+      ey = int(r % g.n[1]);
+      ez = int(r / g.n[1]);
+    }
     TE E[21];
     if constexpr (HADA) element_energies_hada<TN, TE>(g, ex, ey, ez, u, uh, snap, E);
     else element_energies<TN, TE>(g, ex, ey, ez, u, uh, snap, TE(lam), TE(mu), gsm + threadIdx.x, E);

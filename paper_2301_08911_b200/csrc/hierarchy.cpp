@@ -865,24 +865,52 @@ bool Hierarchy<T>::pair_ok(const SolverOptions& opts) const {
 }
 
 // RHS_GROUP = 2, 3 or 6 forces the group size; 0 (default) picks the largest of 6, 3, 2 whose extra
-// per-RHS fields fit in the free HBM next to a reserve for the energy cache and workspace (one domain
-// only: every z-slab must allocate the same slots, collectively, so slabs use pairs unless forced).
+// per-RHS fields fit in this rank's share of the free HBM next to a reserve for the energy cache and
+// workspace. z-slabs decide collectively (every slab allocates the same slots, with links): the free
+// memory is split between the slabs that share a device, and all slabs take the smallest choice.
+// Decided once per hierarchy (later calls return the cached size).
 template <typename T>
-int Hierarchy<T>::group_size(const SolverOptions& opts) const {
+int Hierarchy<T>::group_size(const SolverOptions& opts) {
   if (!pair_ok(opts)) return 1;
   const int forced = knob("RHS_GROUP", 0);
   if (forced == 2 || forced == 3 || forced == 6) return forced;
-  if (slab_.on()) return 2;
+  if (group_auto_) return group_auto_;
+  int dev = 0;
+  IHOM_CUDA(cudaGetDevice(&dev));
+  double share = 1.0;
+  if (slab_.on()) {  // slabs on this device: one-hot by device ordinal, summed over the slabs
+    double h[16] = {};
+    h[dev & 15] = 1.0;
+    IHOM_CUDA(cudaMemcpyAsync(ws_.scalars + 32, h, sizeof(h), cudaMemcpyHostToDevice, s_));
+    allreduce(ws_.scalars + 32, 16, false);
+    IHOM_CUDA(cudaMemcpyAsync(h, ws_.scalars + 32, sizeof(h), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    share = std::max(1.0, h[dev & 15]);
+  }
   double per_slot = 2.0 * 3.0 * 8.0 * double(levels_[0].g.nv);  // f64 f and ping-pong u at level 0
   for (const Level& L : levels_) per_slot += 3.0 * 3.0 * 4.0 * double(L.g.nv);  // f32 e, f, r per level
   size_t free_b = 0, total_b = 0;
   IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double reserve = 21.0 * 8.0 * double(levels_[0].g.nv) + 8e9;  // energy cache (f64 worst case) + 8 GB
-  for (int g : {6, 3, 2}) {
-    const double extra = double(std::max(0, g - 1 - int(slots_.size()))) * per_slot;
-    if (extra + reserve <= double(free_b)) return g;
+  const double budget = double(free_b) / share;
+  const double reserve = 21.0 * 8.0 * double(levels_[0].g.nv) + 8e9 / share;  // energy cache (f64 worst case)
+  int g = 2;
+  for (int c : {6, 3}) {
+    const double extra = double(std::max(0, c - 1 - int(slots_.size()))) * per_slot;
+    if (extra + reserve <= budget) {
+      g = c;
+      break;
+    }
   }
-  return 2;
+  if (slab_.on()) {  // the smallest choice of all slabs: max of -g
+    double v = -double(g);
+    IHOM_CUDA(cudaMemcpyAsync(ws_.scalars + 48, &v, sizeof(v), cudaMemcpyHostToDevice, s_));
+    allreduce(ws_.scalars + 48, 1, true);
+    IHOM_CUDA(cudaMemcpyAsync(&v, ws_.scalars + 48, sizeof(v), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+    g = int(-v);
+  }
+  group_auto_ = g;
+  return g;
 }
 
 template <typename T>

@@ -142,7 +142,7 @@ class Hierarchy {
   // live in slots_ and are swapped in by select_rhs(); every level-0 operation runs per RHS exactly as
   // in a single solve.
   bool pair_ok(const SolverOptions& opts) const;
-  int group_size(const SolverOptions& opts) const;  // 1 (no grouping), 2, 3 or 6
+  int group_size(const SolverOptions& opts);  // 1 (no grouping), 2, 3 or 6; collective on z-slabs
   void select_rhs(int k);
   int current_rhs() const { return cur_rhs_; }
   // solve K u_k = f_k for k < G (f_k = level_f(0) of RHS k); stats per RHS, identical to G solve_bound calls
@@ -253,6 +253,7 @@ class Hierarchy {
   std::vector<RhsSlot> slots_;
   int where_[6] = {-1, 0, 1, 2, 3, 4};  // slot holding RHS k's fields (-1: live in the levels)
   int cur_rhs_ = 0;
+  int group_auto_ = 0;  // automatic group size, decided on first use
   void ensure_group(int G);
   void swap_live(RhsSlot& o);
   RhsSlot* slot_of(int k) { return k == cur_rhs_ ? nullptr : &slots_[size_t(where_[k])]; }

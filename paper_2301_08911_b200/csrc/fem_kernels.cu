@@ -47,6 +47,7 @@ void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t
   }
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_d, kd, sizeof(kd), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_f, kf, sizeof(kf), 0, cudaMemcpyHostToDevice, s));
+  upload_gs_group_tables(kf, s);
   static double hd[kHadaClasses];
   static float hf[kHadaClasses];
   for (int c = 0; c < kHadaClasses; ++c) {

@@ -1038,14 +1038,61 @@ void Hierarchy<T>::residual_f32_group(int G, int l) {
 // One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
 // converged) skips every level-0 and transfer step; the grouped coarse kernels still compute its lane
 // on stale (finite) data, which nothing reads.
+// Level-0 GS sweeps of the active RHSs of a group in one launch per colour (gs_group_kernels.cu).
+template <typename T>
+void Hierarchy<T>::relax_l0_group(int G, const bool* act, int sweeps, bool zero_start) {
+  Level& L = levels_[0];
+  float* u[kMaxRhsGroup];
+  const float* f[kMaxRhsGroup];
+  ZLink<float> ul[kMaxRhsGroup];
+  int nr = 0;
+  for (int k = 0; k < G; ++k)
+    if (act[k]) {
+      RhsSlot* o = slot_of(k);
+      u[nr] = o ? o->eu[0].p : L.eu.p;
+      f[nr] = o ? o->ef[0].p : L.ef.p;
+      ul[nr] = o ? o->eul[0] : L.eul;
+      ++nr;
+    }
+  if (nr == 0) return;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int c = 0; c < 8; ++c) {
+      if (L.sharded) sync();
+      const bool zs = zero_start && sw == 0;
+      ProfScope p(s_, "l0_gs_f32", zs ? gs_l0_bytes_zs(L.g, c, 4.0 * nr, 4) : gs_l0_bytes(L.g, c, 4.0 * nr, 4));
+      if constexpr (std::is_same_v<T, float>)
+        launch_l0_gs_group(L.g, coeff_.p, L.sharded ? coeff_l_ : ZLink<float>{}, nr, f, u, ul, c, zs, s_);
+      ++launches_;
+    }
+}
+
 template <typename T>
 void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
-  for (int k = 0; k < G; ++k)
-    if (act[k]) {
-      select_rhs(k);
-      inner_down(0, opts);
-    }
+  const bool g0 = std::is_same_v<T, float> && l0_gs_group_ok(levels_[0].g);
+  if (g0) {  // level 0 down: grouped pre-smoothing, then residual + restriction per RHS
+    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(0);
+    if (!zs)
+      for (int k = 0; k < G; ++k)
+        if (act[k]) {
+          select_rhs(k);
+          IHOM_CUDA(cudaMemsetAsync(levels_[0].eu.p, 0, sizeof(float) * 3 * levels_[0].g.nv, s_));
+          ++launches_;
+        }
+    relax_l0_group(G, act, opts.pre_sweeps, zs);
+    for (int k = 0; k < G; ++k)
+      if (act[k]) {
+        select_rhs(k);
+        residual_f32(0);
+        restrict_to_f32(0);
+      }
+  } else {
+    for (int k = 0; k < G; ++k)
+      if (act[k]) {
+        select_rhs(k);
+        inner_down(0, opts);
+      }
+  }
   for (int l = 1; l < lmax; ++l) {
     const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
     if (!zs)
@@ -1078,8 +1125,9 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
     if (act[k]) {
       select_rhs(k);
       inner_prolong(0);
-      relax_f32(0, opts.post_sweeps, false);
+      if (!g0) relax_f32(0, opts.post_sweeps, false);
     }
+  if (g0) relax_l0_group(G, act, opts.post_sweeps, false);
 }
 
 template <typename T>

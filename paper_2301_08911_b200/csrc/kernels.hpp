@@ -19,6 +19,7 @@ namespace ihomgpu {
 void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t s);
 void upload_galerkin_tables(const ElementGalerkin& eg, cudaStream_t s);
 void upload_hom_tables(const double hada_classes[], cudaStream_t s);  // hom_kernels.cu (from upload_fem_tables)
+void upload_gs_group_tables(const float kappa_f[], cudaStream_t s);    // gs_group_kernels.cu (idem)
 
 // ---- level 0, matrix-free (src/fem.cpp:98-156, src/multigrid.cpp:263-279) ----
 template <typename TC>
@@ -84,6 +85,11 @@ void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u,
 // the same for nl = 1, 2, 3 or 6 right-hand sides in lockstep (each stencil block read once for all;
 // per-RHS arithmetic identical to the single launches)
 constexpr int kMaxRhsGroup = 6;
+// level-0 f32 GS colour pass for nr <= 6 right-hand sides in lockstep (gs_group_kernels.cu): the
+// coefficient-side work of a vertex is shared by the group
+bool l0_gs_group_ok(const GridGeo& g);
+void launch_l0_gs_group(const GridGeo& g, const float* coeff, ZLink<float> cl, int nr, const float* const* f,
+                        float* const* u, const ZLink<float>* ul, int color, bool zero_start, cudaStream_t s);
 template <typename TS, typename TN>
 void launch_stencil_apply_group(const GridGeo& g, const TS* st, int nl, const TN* const* x, const TN* const* f,
                                 TN* const* y, cudaStream_t s, const ZLink<TN>* xl);

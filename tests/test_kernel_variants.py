@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
     # the bitwise comparisons below are between stencil-form variants: the sum-factorised element
     # sweep (HSWEEP*, a different association of the same sums) is compared at tolerance separately
-    knobs = {"HSWEEP": 0, "HSWEEP32": 0, **knobs}
+    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, **knobs}
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)
@@ -59,6 +59,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("RHS_GROUP", 0)
         ih.set_knob("HSWEEP", 1)
         ih.set_knob("HSWEEP32", 1)
+        ih.set_knob("L0_GROUP", 0)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -269,3 +270,17 @@ def test_hadamard_sweep_matches_stencil_sweep(ih, n):
         assert np.abs(h[1] - base[1]).max() <= tol * np.abs(base[1]).max()
         for a, b in zip(h[2], base[2]):
             assert np.linalg.norm(a - b) <= tol * 10 * max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
+def test_grouped_level0_gs_matches(ih, n, P):
+    """Level-0 GS of a lockstep RHS group in one launch per colour (L0_GROUP, gs_group_kernels.cu): the
+    coefficient-side work is shared, kappa multiplies each merged coefficient (rounding-level change),
+    so whole cell solves agree with the per-RHS passes to rounding: same cycle counts, C^H to 2e-6."""
+    base = _solve(ih, n, {"L0_GROUP": 0}, fabric_p=P)
+    for group in (2, 3, 6):
+        v = _solve(ih, n, {"L0_GROUP": 1, "RHS_GROUP": group}, fabric_p=P)
+        assert v[0] == base[0], group
+        assert np.abs(v[1] - base[1]).max() <= 2e-6 * np.abs(base[1]).max()
+        for a, b in zip(v[2], base[2]):
+            assert np.linalg.norm(a - b) <= 2e-5 * max(np.linalg.norm(b), 1e-30)

@@ -211,6 +211,56 @@ def main():
         out.append(sig + " {")
         out.append(f"  {fname}_z<0u>(q, kap, U, y{', S' if split else ''});")
         out.append("}")
+    # grouped form: scalar forms (TF) shared by a group of right-hand sides, each merged coefficient
+    # kappa_k * (+-F) formed once (scalar multiply) and applied to every RHS lane of TA (vfma(scalar,
+    # lanes, lanes)); the kappa factor moves inside the sum, so rounding differs from ku_vertex_split
+    out.append("")
+    out.append("// Grouped split stencil: forms and merged coefficients are scalar (TF) and shared; U(n, c)")
+    out.append("// returns the neighbour values of every RHS lane (TA); y[r] += coef * u per lane. Off-diagonal")
+    out.append("// part into y, self block into S (scalar). Same operator, kappa applied per coefficient.")
+    out.append("template <unsigned ZM, typename TF, typename TA, typename TK, typename LoadU>")
+    out.append("__device__ __forceinline__ void ku_vertex_split_g(const TF q[8], const TK* __restrict__ kap, LoadU U, "
+               "TA y[3], TF S[9]) {")
+    emitted = set()
+
+    def emit_form_g(name):
+        if not name.startswith("F") or name in emitted:
+            return
+        line = code_forms[int(name[1:])]
+        for tok in line.split("=", 1)[1].replace("(", " ").replace(")", " ").replace(",", " ").replace(
+                ";", " ").split():
+            if tok.startswith("F"):
+                emit_form_g(tok)
+        out.append(line.replace("const TA ", "const TF "))
+        emitted.add(name)
+    for r in range(3):
+        out.append(f"  y[{r}] = vzero<TA>();")
+    for n in range(27):
+        if n == 13:
+            continue
+        for r in range(3):
+            for c in range(3):
+                emit_form_g(used[(n, r, c)][0])
+        out.append(f"  if constexpr (!((ZM >> {n}) & 1u)) {{  // neighbour {n}")
+        for c in range(3):
+            out.append(f"    const TA u{c} = U({n}, {c});")
+        for r in range(3):
+            for c in range(3):
+                name, fs = used[(n, r, c)]
+                k, cs = cls_of[(n, r, c)]
+                sgn = fs * cs
+                out.append(f"    y[{r}] = vfma(TF({'' if sgn > 0 else '-'}kap[{k}]) * {name}, u{c}, y[{r}]);")
+        out.append("  }")
+    for r in range(3):
+        for c in range(3):
+            emit_form_g(used[(13, r, c)][0])
+    for r in range(3):
+        for c in range(3):
+            name, fs = used[(13, r, c)]
+            k, cs = cls_of[(13, r, c)]
+            sgn = fs * cs
+            out.append(f"  S[{3 * r + c}] = TF({'' if sgn > 0 else '-'}kap[{k}]) * {name};")
+    out.append("}")
     out.append("}  // namespace ihomgpu")
     path = os.path.join(ROOT, "paper_2301_08911_b200", "csrc", "ku_gen.cuh")
     open(path, "w").write("\n".join(out) + "\n")

@@ -1038,6 +1038,30 @@ void Hierarchy<T>::residual_f32_group(int G, int l) {
 // One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
 // converged) skips every level-0 and transfer step; the grouped coarse kernels still compute its lane
 // on stale (finite) data, which nothing reads.
+// Inner f32 residuals of RHSs ka and kb at level 0 in one paired element sweep.
+template <typename T>
+void Hierarchy<T>::residual_f32_l0_pair(int ka, int kb) {
+  Level& L = levels_[0];
+  if constexpr (std::is_same_v<T, float>) {
+    if (L.sharded) sync();
+    const float* u[2];
+    const float* f[2];
+    float* y[2];
+    ZLink<float> ul[2];
+    const int ks[2] = {ka, kb};
+    for (int i = 0; i < 2; ++i) {
+      RhsSlot* o = slot_of(ks[i]);
+      u[i] = o ? o->eu[0].p : L.eu.p;
+      f[i] = o ? o->ef[0].p : L.ef.p;
+      y[i] = o ? o->er[0].p : L.er.p;
+      ul[i] = o ? o->eul[0] : L.eul;
+    }
+    ProfScope p(s_, "l0_residual_f32", 2.0 * resid_l0_bytes(L.g, 4, 4, true) - 4.0 * double(L.g.nv));
+    launch_l0_residual_pair(L.g, coeff_.p, L.sharded ? coeff_l_ : ZLink<float>{}, u, ul, f, y, s_);
+    ++launches_;
+  }
+}
+
 // Level-0 GS sweeps of the active RHSs of a group in one launch per colour (gs_group_kernels.cu).
 template <typename T>
 void Hierarchy<T>::relax_l0_group(int G, const bool* act, int sweeps, bool zero_start) {
@@ -1086,6 +1110,32 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
         residual_f32(0);
         restrict_to_f32(0);
       }
+  } else if (std::is_same_v<T, float> && l0_residual_pair_ok(levels_[0].g)) {
+    // per-RHS pre-smoothing; the inner residuals two RHSs per paired element sweep; restriction per RHS
+    int list[kMaxRhsGroup], na = 0;
+    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(0);
+    for (int k = 0; k < G; ++k)
+      if (act[k]) {
+        list[na++] = k;
+        select_rhs(k);
+        if (!zs) {
+          IHOM_CUDA(cudaMemsetAsync(levels_[0].eu.p, 0, sizeof(float) * 3 * levels_[0].g.nv, s_));
+          ++launches_;
+        }
+        relax_f32(0, opts.pre_sweeps, false, zs);
+      }
+    for (int i = 0; i < na; i += 2) {
+      if (i + 1 < na) {
+        residual_f32_l0_pair(list[i], list[i + 1]);
+      } else {
+        select_rhs(list[i]);
+        residual_f32(0);
+      }
+    }
+    for (int i = 0; i < na; ++i) {
+      select_rhs(list[i]);
+      restrict_to_f32(0);
+    }
   } else {
     for (int k = 0; k < G; ++k)
       if (act[k]) {

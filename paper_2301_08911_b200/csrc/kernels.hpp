@@ -88,6 +88,10 @@ constexpr int kMaxRhsGroup = 6;
 // level-0 f32 GS colour pass for nr <= 6 right-hand sides in lockstep (gs_group_kernels.cu): the
 // coefficient-side work of a vertex is shared by the group
 bool l0_gs_group_ok(const GridGeo& g);
+// level-0 inner f32 residuals of two RHSs in one paired element sweep (hsweep_kernels.cuh, knob HSWEEP_PAIR)
+bool l0_residual_pair_ok(const GridGeo& g);
+void launch_l0_residual_pair(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* const u[2],
+                             const ZLink<float> ul[2], const float* const f[2], float* const y[2], cudaStream_t s);
 void launch_l0_gs_group(const GridGeo& g, const float* coeff, ZLink<float> cl, int nr, const float* const* f,
                         float* const* u, const ZLink<float>* ul, int color, bool zero_start, cudaStream_t s);
 template <typename TS, typename TN>

@@ -1,11 +1,3 @@
 set -x
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_kernel_variants.py -q -x --timeout 900 -k "grouped or rhs" > gpurun_out/t_var.log 2>&1; echo var rc $?; tail -15 gpurun_out/t_var.log
-for k in 0 1; do IHOM_L0_GROUP=$k timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_l$k.json 2> gpurun_out/bench_l$k.err; echo rc $?; tail -2 gpurun_out/bench_l$k.err
-python - $k <<'PY'
-import json, sys
-d = json.load(open(f"gpurun_out/bench_l{sys.argv[1]}.json"))
-print(sys.argv[1], d["value"], d["e2e"]["value"], d.get("cycles_per_iteration"), d["objective"], d["roofline"]["kernel"], d["roofline"]["frac"])
-for k, v in list(d["kernels"].items())[:6]: print("  ", k, round(v["ms"] / 8, 2), v["launches"] / 8, v["GB/s"])
-PY
-done
+timeout 1200 python -m pytest tests/test_kernel_variants.py -q --timeout 900 > gpurun_out/t_var.log 2>&1; echo var rc $?; tail -4 gpurun_out/t_var.log

@@ -864,7 +864,7 @@ bool Hierarchy<T>::pair_ok(const SolverOptions& opts) const {
          fast_ok(levels_[0].g) && num_levels() > 1;
 }
 
-// RHS_GROUP = 2, 3 or 6 forces the group size; 0 (default) picks the largest of 6, 3, 2 whose extra
+// RHS_GROUP = 2, 3 or 6 forces the group size; 0 (default) picks the largest of 6, 3, 2 (else 1) whose extra
 // per-RHS fields fit in this rank's share of the free HBM next to a reserve for the energy cache and
 // workspace. z-slabs decide collectively (every slab allocates the same slots, with links): the free
 // memory is split between the slabs that share a device, and all slabs take the smallest choice.
@@ -893,8 +893,8 @@ int Hierarchy<T>::group_size(const SolverOptions& opts) {
   IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double budget = double(free_b) / share;
   const double reserve = 21.0 * 8.0 * double(levels_[0].g.nv) + 8e9 / share;  // energy cache (f64 worst case)
-  int g = 2;
-  for (int c : {6, 3}) {
+  int g = 1;  // memory lever: no lockstep grouping when even a pair's extra fields do not fit
+  for (int c : {6, 3, 2}) {
     const double extra = double(std::max(0, c - 1 - int(slots_.size()))) * per_slot;
     if (extra + reserve <= budget) {
       g = c;
@@ -1478,7 +1478,14 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
   const size_t esz = std::is_same_v<T, float> ? sizeof(float) : sizeof(double);
   void* ec = nullptr;
   if (knob("ENERGY_CACHE", 1)) {
-    if (!ecache_.p) ecache_.alloc(size_t(21 * nv) * esz);
+    if (!ecache_.p && !ecache_skip_) {
+      // memory lever: the cache (21 energies per element) is an optimisation -- skip it when it would
+      // leave less than 4 GB of HBM (the sensitivity pass then recomputes the energies)
+      size_t free_b = 0, total_b = 0;
+      IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      if (double(free_b) >= double(21 * nv) * double(esz) + 4e9) ecache_.alloc(size_t(21 * nv) * esz);
+      else ecache_skip_ = true;
+    }
     ec = ecache_.p;
   }
   {

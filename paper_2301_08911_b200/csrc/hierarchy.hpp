@@ -321,6 +321,7 @@ class Homogenizer {
   // per-element energies of the last effective_tensor() (knob ENERGY_CACHE, default on): [21][nv]
   DevBuf<unsigned char> ecache_;
   bool ecache_valid_ = false;
+  bool ecache_skip_ = false;  // not enough HBM for the energy cache (decided once)
   Comm* comm_ = nullptr;
   int owner_[6] = {0, 0, 0, 0, 0, 0};
 };

@@ -127,6 +127,13 @@ double resid_coarse_bytes(const GridGeo& g, double sN, double sC, bool with_f) {
   return double(g.nv) * (243.0 * sC + (with_f ? 9.0 : 6.0) * sN);
 }
 
+// Free HBM as seen by the memory levers; knob HBM_LIMIT_MB > 0 caps it (tests exercise the low-memory
+// paths on a large GPU with it).
+size_t hbm_free_limit(size_t free_b) {
+  const int mb = knob("HBM_LIMIT_MB", 0);
+  return mb > 0 ? std::min(free_b, size_t(mb) << 20) : free_b;
+}
+
 bool can_coarsen(const GridGeo& g) {  // inc/grid.hpp:47-51
   for (int k = 0; k < 3; ++k)
     if (g.n[k] % 2 != 0 || g.n[k] / 2 < 4) return false;
@@ -891,6 +898,7 @@ int Hierarchy<T>::group_size(const SolverOptions& opts) {
   for (const Level& L : levels_) per_slot += 3.0 * 3.0 * 4.0 * double(L.g.nv);  // f32 e, f, r per level
   size_t free_b = 0, total_b = 0;
   IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  free_b = hbm_free_limit(free_b);
   const double budget = double(free_b) / share;
   const double reserve = 21.0 * 8.0 * double(levels_[0].g.nv) + 8e9 / share;  // energy cache (f64 worst case)
   int g = 1;  // memory lever: no lockstep grouping when even a pair's extra fields do not fit
@@ -1483,6 +1491,7 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
       // leave less than 4 GB of HBM (the sensitivity pass then recomputes the energies)
       size_t free_b = 0, total_b = 0;
       IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      free_b = hbm_free_limit(free_b);
       if (double(free_b) >= double(21 * nv) * double(esz) + 4e9) ecache_.alloc(size_t(21 * nv) * esz);
       else ecache_skip_ = true;
     }

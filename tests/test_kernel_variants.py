@@ -61,6 +61,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("HSWEEP32", 1)
         ih.set_knob("L0_GROUP", 0)
         ih.set_knob("HSWEEP_PAIR", 0)
+        ih.set_knob("HBM_LIMIT_MB", 0)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -300,3 +301,16 @@ def test_paired_f32_element_sweep_bit_identical(ih, n, P):
         assert np.abs(v[1] - base[1]).max() <= 1e-9 * np.abs(base[1]).max()
         for a, b in zip(v[2], base[2]):
             assert np.linalg.norm(a - b) <= 1e-6 * max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("P", [0, 2])
+def test_memory_levers_bit_identical(ih, P):
+    """With the free HBM capped (HBM_LIMIT_MB) the solver drops the lockstep grouping (group size 1) and
+    the energy cache; both are pure optimisations, so cycle counts, C^H and displacements are bitwise
+    those of the default run (here: groups of six and the cache)."""
+    base = _solve(ih, 32, {}, fabric_p=P)
+    low = _solve(ih, 32, {"HBM_LIMIT_MB": 256}, fabric_p=P)
+    assert low[0] == base[0]
+    np.testing.assert_array_equal(low[1], base[1])
+    for a, b in zip(low[2], base[2]):
+        np.testing.assert_array_equal(a, b)

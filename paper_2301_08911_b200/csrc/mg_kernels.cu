@@ -217,6 +217,15 @@ __device__ __forceinline__ void stencil_block(const TS* __restrict__ bl, double 
 #pragma unroll
   for (int e = 0; e < 9; ++e) c9[e] = double(__ldg(bl + 32 * e));
 }
+template <typename TS>
+__device__ __forceinline__ void stencil_block(const TS* __restrict__ bl, float c9[9]) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) c9[e] = float(__ldg(bl + 32 * e));
+}
+__device__ __forceinline__ void block_fma(const float c9[9], float a, float b, float c, float m[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) m[r] = fmaf(c9[3 * r + 2], c, fmaf(c9[3 * r + 1], b, fmaf(c9[3 * r], a, m[r])));
+}
 __device__ __forceinline__ void block_fma(const double c9[9], double a, double b, double c, double m[3]) {
 #pragma unroll
   for (int r = 0; r < 3; ++r) m[r] = fma(c9[3 * r + 2], c, fma(c9[3 * r + 1], b, fma(c9[3 * r], a, m[r])));
@@ -253,7 +262,10 @@ __global__ void __launch_bounds__(128) stencil_apply_kernel(GridGeo g, const TS*
 
 // Fast even-grid variants (FastAddr, common.cuh): one IADD3 per neighbour
 // location, AoS components at immediate offsets, blocked stencil rows.
-template <typename TS, typename TN, bool ZL, int NL>
+// TACC = float (knob STENCIL_F32, f32 stencils and nodal data only): stencil values and products in
+// f32 instead of converted to f64 -- fewer registers (more warps in flight for these latency-bound
+// passes) and no F2F, at the f32 rounding level of the inner correction cycle.
+template <typename TS, typename TN, bool ZL, int NL, typename TACC = double>
 __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
   // colour fastest in blockIdx.z: the 8 colours of one plane run back to back and share L2
   const int color = blockIdx.z & 7;
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   fast_addr(g, color, h0, h1, h2, fa);
   const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   const TS* row = st + st_index(0, loc);
-  double acc[NL][3] = {};
+  TACC acc[NL][3] = {};
   const TN* xb[NL][3];
 #pragma unroll
   for (int k = 0; k < NL; ++k) {
@@ -275,20 +287,20 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
   }
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
-    double c9[9];
+    TACC c9[9];
     stencil_block(row + 32 * 9 * n, c9);
     const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       const TN* xn = xb[k][n / 9] + off;
-      block_fma(c9, double(__ldg(xn)), double(__ldg(xn + 1)), double(__ldg(xn + 2)), acc[k]);
+      block_fma(c9, TACC(__ldg(xn)), TACC(__ldg(xn + 1)), TACC(__ldg(xn + 2)), acc[k]);
     }
   }
 #pragma unroll
   for (int k = 0; k < NL; ++k)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      io.y[k][3 * (size_t)loc + c] = io.f[k] ? TN(double(io.f[k][3 * (size_t)loc + c]) - acc[k][c]) : TN(acc[k][c]);
+      io.y[k][3 * (size_t)loc + c] = io.f[k] ? TN(TACC(io.f[k][3 * (size_t)loc + c]) - acc[k][c]) : TN(acc[k][c]);
 }
 
 // zm: neighbours known to be zero (zero-start sweep, common.cuh zero_start_mask): their stencil
@@ -310,7 +322,7 @@ __device__ __forceinline__ bool gs_solve_store(const double S[9], const double m
   return true;
 }
 
-template <typename TS, typename TN, bool ZL, int NL>
+template <typename TS, typename TN, bool ZL, int NL, typename TACC = double>
 __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
                                                               int color, int* err, unsigned zm) {
   const int h2 = blockIdx.z;
@@ -320,7 +332,8 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
   fast_addr(g, color, h0, h1, h2, fa);
   const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
   const TS* row = st + st_index(0, loc);
-  double m[NL][3] = {}, S[9];
+  TACC m[NL][3] = {};
+  double S[9];
   stencil_block(row + 32 * 9 * 13, S);
   const TN* ub[NL][3];
 #pragma unroll
@@ -333,18 +346,20 @@ __global__ void __launch_bounds__(128) stencil_gs_fast_kernel(GridGeo g, const T
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
     if (n == 13 || ((zm >> n) & 1u)) continue;
-    double c9[9];
+    TACC c9[9];
     stencil_block(row + 32 * 9 * n, c9);
     const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       const TN* un = ub[k][n / 9] + off;
-      block_fma(c9, double(__ldg(un)), double(__ldg(un + 1)), double(__ldg(un + 2)), m[k]);
+      block_fma(c9, TACC(__ldg(un)), TACC(__ldg(un + 1)), TACC(__ldg(un + 2)), m[k]);
     }
   }
 #pragma unroll
-  for (int k = 0; k < NL; ++k)
-    if (!gs_solve_store<TS, TN>(S, m[k], io.f[k], loc, io.y[k], err)) return;
+  for (int k = 0; k < NL; ++k) {
+    const double mk[3] = {double(m[k][0]), double(m[k][1]), double(m[k][2])};
+    if (!gs_solve_store<TS, TN>(S, mk, io.f[k], loc, io.y[k], err)) return;
+  }
 }
 
 // Small levels (latency-bound: a few thousand vertices, long per-thread load
@@ -440,6 +455,7 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
 // levels with at most this many vertices per colour use warp-per-vertex (default 4096: up to 32^3;
 // 64^3 runs 35% faster thread-per-vertex, measured)
 static long long warp_vmax() { return (long long)knob("WARP_VMAX", 4096); }
+static bool stencil_f32() { return knob("STENCIL_F32", 1) != 0; }
 
 template <typename TS, typename TN, int NL>
 static void launch_apply_n(const GridGeo& g, const TS* st, RhsN<TN> io, cudaStream_t s) {
@@ -453,8 +469,13 @@ static void launch_apply_n(const GridGeo& g, const TS* st, RhsN<TN> io, cudaStre
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    if (linked) stencil_apply_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io);
-    else stencil_apply_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io);
+    if (std::is_same_v<TS, float> && std::is_same_v<TN, float> && stencil_f32()) {
+      if (linked) stencil_apply_fast_kernel<TS, TN, true, NL, float><<<gr, b, 0, s>>>(g, st, io);
+      else stencil_apply_fast_kernel<TS, TN, false, NL, float><<<gr, b, 0, s>>>(g, st, io);
+    } else {
+      if (linked) stencil_apply_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io);
+      else stencil_apply_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io);
+    }
   } else {
     if (linked) throw std::invalid_argument("z-slab level needs an even grid");
     stencil_apply_kernel<TS, TN, NL><<<ceil_div(g.nv, 128), 128, 0, s>>>(g, st, io);
@@ -527,8 +548,13 @@ static void launch_gs_n(const GridGeo& g, const TS* st, RhsN<TN> io, int color, 
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
-    if (linked) stencil_gs_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
-    else stencil_gs_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+    if (std::is_same_v<TS, float> && std::is_same_v<TN, float> && stencil_f32()) {
+      if (linked) stencil_gs_fast_kernel<TS, TN, true, NL, float><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+      else stencil_gs_fast_kernel<TS, TN, false, NL, float><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+    } else {
+      if (linked) stencil_gs_fast_kernel<TS, TN, true, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+      else stencil_gs_fast_kernel<TS, TN, false, NL><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
+    }
   } else {
     if (linked) throw std::invalid_argument("z-slab level needs an even grid");
     stencil_gs_kernel<TS, TN, NL><<<ceil_div(g.size[color], 128), 128, 0, s>>>(g, st, io, color, err, zm);

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
     # the bitwise comparisons below are between stencil-form variants: the sum-factorised element
     # sweep (HSWEEP*, a different association of the same sums) is compared at tolerance separately
-    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, **knobs}
+    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, "STENCIL_F32": 0, **knobs}
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)
@@ -62,6 +62,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("L0_GROUP", 0)
         ih.set_knob("HSWEEP_PAIR", 0)
         ih.set_knob("HBM_LIMIT_MB", 0)
+        ih.set_knob("STENCIL_F32", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -314,3 +315,15 @@ def test_memory_levers_bit_identical(ih, P):
     np.testing.assert_array_equal(low[1], base[1])
     for a, b in zip(low[2], base[2]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
+def test_stencil_f32_accumulation_matches(ih, n, P):
+    """Stencil-level (coarse) GS and residual of the inner f32 cycle with f32 products/sums
+    (STENCIL_F32) instead of f64: the coarse-grid correction changes at f32 rounding, the outer f64
+    defect residual is untouched, so whole solves agree to the solver tolerance (same cycle counts,
+    C^H to 1e-6)."""
+    base = _solve(ih, n, {"STENCIL_F32": 0}, fabric_p=P)
+    v = _solve(ih, n, {"STENCIL_F32": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    assert np.abs(v[1] - base[1]).max() <= 1e-6 * np.abs(base[1]).max()

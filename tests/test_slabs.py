@@ -152,7 +152,10 @@ def test_slab_optimizer_256_bulk(P):
     for recs, _ in res:
         for a, b in zip(recs, recs1):
             assert a["cycles"] == b["cycles"]
-            assert abs(a["objective"] - b["objective"]) <= 1e-9 * abs(b["objective"])
+            # 1e-8: the inner cycle's stencil levels accumulate in f32 (STENCIL_F32) and a slab's small
+            # levels may take the warp-per-vertex (f64) kernel where one domain takes the thread-per-
+            # vertex one, so the coarse corrections differ at f32 rounding (observed 1.2e-9 at P = 4)
+            assert abs(a["objective"] - b["objective"]) <= 1e-8 * abs(b["objective"])
     d = np.concatenate([r[1] for r in res])
     # the cross-slab sums (norms, C^H, OC means) fold in another order: the OC multiplier, and with it
     # every density, moves at the 1e-9 level per iteration on 16.7M elements

@@ -1,3 +1,4 @@
 set -x
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_kernel_variants.py -q --timeout 900 -k "memory or rhs" > gpurun_out/t_var.log 2>&1; echo var rc $?; tail -4 gpurun_out/t_var.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/t_gpu.log 2>&1; echo gpu tests rc $?; tail -3 gpurun_out/t_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc $?; tail -2 gpurun_out/smoke.log

@@ -1,4 +1,11 @@
 set -x
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/t_gpu.log 2>&1; echo gpu tests rc $?; tail -3 gpurun_out/t_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc $?; tail -2 gpurun_out/smoke.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo rc $?
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/bench.json"))
+print(d["value"], d["e2e"]["value"], d.get("cycles_per_iteration"))
+for k, v in d["kernels"].items():
+    if k.startswith("l1") or k.startswith("l2") or k.startswith("coarse"): print("  ", k, round(v["ms"] / 8, 2), v["launches"] / 8, v["GB/s"])
+PY
+timeout 1500 python -m pytest tests/test_slabs.py -q --timeout 900 -k "256" > gpurun_out/t_slab.log 2>&1; echo slab rc $?; tail -2 gpurun_out/t_slab.log

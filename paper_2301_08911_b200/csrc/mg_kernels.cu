@@ -17,6 +17,8 @@ __device__ __forceinline__ int wrapi(int c, int n) {
 }
 
 // f_c = I^T r_f over the 27 fine vertices around 2*vc (src/multigrid.cpp:19-41).
+static bool transfer_f32() { return knob("TRANSFER_F32", 1) != 0; }
+
 template <typename TN>
 __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf, TN* __restrict__ fc) {
   const long long loc = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -48,7 +50,9 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
 // output is either this slab's coarse level (gout == gc, zoff 0) or the
 // replicated global coarse level (gout global, zoff = this slab's first coarse
 // plane in halved coordinates) -- only the slab's own planes are written.
-template <typename TN>
+// TA: arithmetic type; float (knob TRANSFER_F32, f32 fields only) keeps the inner cycle's transfers in
+// f32 (the weights are powers of two: exact products) instead of converting every value to f64.
+template <typename TN, typename TA = double>
 __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf,
                                                             ZLink<TN> rl, GridGeo gout, int zoff,
                                                             TN* __restrict__ fc) {
@@ -60,14 +64,14 @@ __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo 
   FastAddr fa;
   fast_addr(gf, 0, cx, cy, cz, fa);
   const TN* rb = zbase(fa, rf, rl, 0);  // fine colour 0: only the z-1 plane can wrap
-  double acc[3] = {0.0, 0.0, 0.0};
+  TA acc[3] = {TA(0), TA(0), TA(0)};
 #pragma unroll
   for (int n = 0; n < 27; ++n) {
     const int dx = n % 3 - 1, dy = (n / 3) % 3 - 1, dz = n / 9 - 1;
-    const double w = tw1(dx) * tw1(dy) * tw1(dz);
+    const TA w = TA(tw1(dx) * tw1(dy) * tw1(dz));
     const TN* r = (n < 9 ? rb : rf) + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) acc[c] += w * double(__ldg(r + c));
+    for (int c = 0; c < 3; ++c) acc[c] += w * TA(__ldg(r + c));
   }
   const size_t loc =
       (size_t)color * gout.size[0] + h0 + (size_t)gout.cd[0][0] * (h1 + (size_t)gout.cd[0][1] * (h2 + zoff));
@@ -79,9 +83,9 @@ __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo 
 // h_k and h_k + 1 (wrapped). z-slab: the coarse level is this slab's (zoff 0;
 // the wrapped z parent is the first plane of the slab above, cl.hi) or the
 // replicated global level (zoff = the slab's first coarse plane).
-template <typename TN, int O0, int O1, int O2>
+template <typename TN, int O0, int O1, int O2, typename TA = double>
 __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1, int h2, const TN* __restrict__ uc,
-                                               const ZLink<TN>& cl, int zoff, double acc[3]) {
+                                               const ZLink<TN>& cl, int zoff, TA acc[3]) {
   const int o[3] = {O0, O1, O2};
   const int h[3] = {h0, h1, h2 + zoff};
   const unsigned Bc = (unsigned)gc.size[0];
@@ -94,7 +98,7 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
     P[k][0] = (((unsigned)c0 & 1u) << k) * Bc + sc[k] * (unsigned)(c0 >> 1);
     P[k][1] = (((unsigned)c1 & 1u) << k) * Bc + sc[k] * (unsigned)(c1 >> 1);
   }
-  const double w = (O0 ? 0.5 : 1.0) * (O1 ? 0.5 : 1.0) * (O2 ? 0.5 : 1.0);
+  const TA w = TA((O0 ? 0.5 : 1.0) * (O1 ? 0.5 : 1.0) * (O2 ? 0.5 : 1.0));
   const TN* ub[2] = {uc, h[2] + 1 == gc.n[2] ? cl.hi : uc};
 #pragma unroll
   for (int a = 0; a < 1 + O0; ++a)
@@ -104,32 +108,32 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
       for (int c = 0; c < 1 + O2; ++c) {
         const TN* u = ub[c] + 3 * (size_t)(P[0][a] + P[1][b] + P[2][c]);
 #pragma unroll
-        for (int d = 0; d < 3; ++d) acc[d] += w * double(__ldg(u + d));
+        for (int d = 0; d < 3; ++d) acc[d] += w * TA(__ldg(u + d));
       }
   (void)o;
 }
 
-template <typename TN>
+template <typename TN, typename TA = double>
 __global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc,
                                                            ZLink<TN> cl, int zoff, TN* __restrict__ uf) {
   const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
   const int h2 = blockIdx.z >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
-  double acc[3] = {0.0, 0.0, 0.0};
+  TA acc[3] = {TA(0), TA(0), TA(0)};
   switch (color) {  // uniform per block
-    case 0: prolong_vertex<TN, 0, 0, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 1: prolong_vertex<TN, 1, 0, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 2: prolong_vertex<TN, 0, 1, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 3: prolong_vertex<TN, 1, 1, 0>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 4: prolong_vertex<TN, 0, 0, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 5: prolong_vertex<TN, 1, 0, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    case 6: prolong_vertex<TN, 0, 1, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
-    default: prolong_vertex<TN, 1, 1, 1>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 0: prolong_vertex<TN, 0, 0, 0, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 1: prolong_vertex<TN, 1, 0, 0, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 2: prolong_vertex<TN, 0, 1, 0, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 3: prolong_vertex<TN, 1, 1, 0, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 4: prolong_vertex<TN, 0, 0, 1, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 5: prolong_vertex<TN, 1, 0, 1, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    case 6: prolong_vertex<TN, 0, 1, 1, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
+    default: prolong_vertex<TN, 1, 1, 1, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
   }
   const size_t loc = (size_t)color * gf.size[0] + h0 + (size_t)gf.cd[0][0] * (h1 + (size_t)gf.cd[0][1] * h2);
 #pragma unroll
-  for (int d = 0; d < 3; ++d) uf[3 * loc + d] = TN(double(uf[3 * loc + d]) + acc[d]);
+  for (int d = 0; d < 3; ++d) uf[3 * loc + d] = TN(TA(uf[3 * loc + d]) + acc[d]);
 }
 
 template <typename TN>
@@ -139,7 +143,11 @@ void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc,
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 8 * gc.cd[0][2]);
-    restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc, gout ? zoff : 0, fc);
+    if (std::is_same_v<TN, float> && transfer_f32())
+      restrict_fast_kernel<TN, float><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc,
+                                                       gout ? zoff : 0, fc);
+    else
+      restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc, gout ? zoff : 0, fc);
     IHOM_LAUNCH_CHECK();
     return;
   }
@@ -190,7 +198,10 @@ void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* 
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gf);
     const dim3 gr(ceil_div(gf.cd[0][0], b.x), ceil_div(gf.cd[0][1], b.y), 8 * gf.cd[0][2]);
-    prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
+    if (std::is_same_v<TN, float> && transfer_f32())
+      prolong_fast_kernel<TN, float><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
+    else
+      prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
     IHOM_LAUNCH_CHECK();
     return;
   }

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
     # the bitwise comparisons below are between stencil-form variants: the sum-factorised element
     # sweep (HSWEEP*, a different association of the same sums) is compared at tolerance separately
-    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, "STENCIL_F32": 0, **knobs}
+    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, "STENCIL_F32": 0, "TRANSFER_F32": 0, **knobs}
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)
@@ -63,6 +63,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("HSWEEP_PAIR", 0)
         ih.set_knob("HBM_LIMIT_MB", 0)
         ih.set_knob("STENCIL_F32", 1)
+        ih.set_knob("TRANSFER_F32", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -325,5 +326,15 @@ def test_stencil_f32_accumulation_matches(ih, n, P):
     C^H to 1e-6)."""
     base = _solve(ih, n, {"STENCIL_F32": 0}, fabric_p=P)
     v = _solve(ih, n, {"STENCIL_F32": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    assert np.abs(v[1] - base[1]).max() <= 1e-6 * np.abs(base[1]).max()
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
+def test_transfer_f32_matches(ih, n, P):
+    """Restriction / prolongation of the inner f32 cycle in f32 arithmetic (TRANSFER_F32; the weights are
+    powers of two, so only the sums round in f32): same cycle counts, C^H to 1e-6."""
+    base = _solve(ih, n, {"TRANSFER_F32": 0}, fabric_p=P)
+    v = _solve(ih, n, {"TRANSFER_F32": 1}, fabric_p=P)
     assert v[0] == base[0]
     assert np.abs(v[1] - base[1]).max() <= 1e-6 * np.abs(base[1]).max()

@@ -939,15 +939,26 @@ __device__ double block_sum_1(double v, double* red) {
 }
 
 // x is in dof order; returns sqrt(sum((A x - f)^2)) with f in dof order.
+// Row i of M times v, one warp per row: lanes stride the row (coalesced reads of M), fixed-order
+// xor-shuffle fold (deterministic). All lanes return the dot product.
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ M, int N, int i, const double* v) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int j = lane; j < N; j += 32) s += M[(size_t)i * N + j] * v[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 __device__ double dense_resid(int N, const double* A, const double* x, const double* f, double* r, double* red) {
-  double part = 0.0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < N; ++j) s += A[(size_t)i * N + j] * x[j];
-    r[i] = f[i] - s;
-    part += r[i] * r[i];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < N; i += nw) {
+    const double s = warp_row_dot(A, N, i, x);
+    if ((threadIdx.x & 31) == 0) r[i] = f[i] - s;
   }
   __syncthreads();
+  double part = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) part += r[i] * r[i];
   return sqrt(block_sum_1(part, red));
 }
 
@@ -979,19 +990,18 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
     return;
   }
   // x = Ainv f
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < N; ++j) s += Ainv[(size_t)i * N + j] * fv[j];
-    x[i] = s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < N; i += nw) {
+    const double s = warp_row_dot(Ainv, N, i, fv);
+    if ((threadIdx.x & 31) == 0) x[i] = s;
   }
   __syncthreads();
   if (fn > 0.0) {  // refinement against the unshifted matrix (src/multigrid.cpp:435-447)
     double rel = dense_resid(N, A, x, fv, r, red) / fn;
     for (int it = 0; it < 3 && rel > 1e-9; ++it) {
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        double s = 0.0;
-        for (int j = 0; j < N; ++j) s += Ainv[(size_t)i * N + j] * r[j];
-        x[i] += s;
+      for (int i = warp; i < N; i += nw) {
+        const double s = warp_row_dot(Ainv, N, i, r);
+        if ((threadIdx.x & 31) == 0) x[i] += s;
       }
       __syncthreads();
       rel = dense_resid(N, A, x, fv, r, red) / fn;

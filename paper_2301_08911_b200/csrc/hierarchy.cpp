@@ -438,6 +438,31 @@ void Hierarchy<T>::remove_translations_to(const double* src, double* dst, int l)
   launches_ += 3;
 }
 
+// remove_translations(f, 0) followed by norm(f): one pass fewer over f, bitwise the same results.
+template <typename T>
+double Hierarchy<T>::project_norm0(double* f) {
+  const Level& L = levels_[0];
+  const long long nv = L.g.nv;
+  if (knob("PROJECT_NORM", 1) == 0) {
+    remove_translations(f, 0);
+    return norm(f, 3 * nv);
+  }
+  {
+    ProfScope p(s_, "reduce", double(nv) * 24.0);
+    launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
+  }
+  if (L.sharded) allreduce(ws_.scalars, 3);
+  {
+    ProfScope p(s_, "vector", double(nv) * 48.0);
+    launch_sub_means_norm(f, nv, ws_.scalars, ws_.partials, ws_.scalars + 4, s_, L.nv_global);
+  }
+  launches_ += 4;
+  allreduce(ws_.scalars + 4, 1);
+  IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+  return std::sqrt(h_pinned_[0]);
+}
+
 template <typename T>
 double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:88-94
   {
@@ -1212,8 +1237,7 @@ void Hierarchy<T>::solve_bound_group(int G, double* const* u, const SolverOption
       u0l_ = resolve(ul[k], u[k]);
       u_home_ = u[k];
       u_home_l_ = u0l_;
-      remove_translations(L0.f.p, 0);
-      fnorm0_ = norm(L0.f.p, n0);
+      fnorm0_ = project_norm0(L0.f.p);
       if (fnorm0_ <= negligible_load(n0)) {
         IHOM_CUDA(cudaMemsetAsync(u[k], 0, sizeof(double) * n0, s_));
         st[k].converged = true;
@@ -1280,8 +1304,7 @@ SolveStats Hierarchy<T>::solve_bound(double* u, const SolverOptions& opts, ZLink
   const long long n0 = 3 * L0.g.nv;
   SolveStats st;
   try {
-    remove_translations(L0.f.p, 0);
-    fnorm0_ = norm(L0.f.p, n0);
+    fnorm0_ = project_norm0(L0.f.p);
     if (fnorm0_ <= negligible_load(n0)) {
       IHOM_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * n0, s_));
       st.converged = true;

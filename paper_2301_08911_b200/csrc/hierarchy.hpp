@@ -160,6 +160,7 @@ class Hierarchy {
 
   // Deterministic device reductions used by the solver (over all slabs).
   void remove_translations(double* f, int l);
+  double project_norm0(double* f);  // remove_translations(f, 0) + norm(f) in one pass fewer
   void remove_translations_to(const double* src, double* dst, int l);
   double norm(const double* x, long long n);
 

@@ -124,6 +124,9 @@ void launch_dot(const TN* a, const TN* b, long long n, double* partials, double*
 template <typename TN>
 void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count = 0);
 // dst = src - mean (per component), the in-place variant's arithmetic
+// x -= per-component mean (sums / count) and out = ||x||^2, bitwise launch_sub_means + launch_dot
+void launch_sub_means_norm(double* x, long long nv, const double* sums, double* partials, double* out,
+                           cudaStream_t s, long long count = 0);
 void launch_sub_means_copy(const double* src, double* dst, long long nv, const double* sums, cudaStream_t s,
                            long long count = 0);
 void launch_int_to_double(const int* in, double* out, cudaStream_t s);

@@ -135,6 +135,35 @@ __global__ void sub_means_copy_kernel(const double* __restrict__ src, double* __
   }
 }
 
+// x -= mean (per component) and ||x||^2 of the result in one pass: the same per-entry fma as
+// sub_means_flat_kernel and the same partition / fold as dot_kernel over the 3 nv entries, so the
+// field and the norm are bitwise those of launch_sub_means + launch_dot.
+__global__ void __launch_bounds__(kRT) sub_means_norm_kernel(double* __restrict__ x, long long n3,
+                                                             const double* __restrict__ sums, long long count,
+                                                             double* partials) {
+  __shared__ double sh[32];
+  const double inv = 1.0 / double(count);
+  const double m[3] = {sums[0], sums[1], sums[2]};
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n3; i += (long long)gridDim.x * kRT) {
+    const double v = fma(-m[i % 3], inv, x[i]);
+    x[i] = v;
+    s += v * v;
+  }
+  const double r = block_reduce(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+void launch_sub_means_norm(double* x, long long nv, const double* sums, double* partials, double* out,
+                           cudaStream_t s, long long count) {
+  const long long n3 = 3 * nv;
+  const int g = reduce_grid(n3);
+  sub_means_norm_kernel<<<g, kRT, 0, s>>>(x, n3, sums, count > 0 ? count : nv, partials);
+  IHOM_LAUNCH_CHECK();
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
+  IHOM_LAUNCH_CHECK();
+}
+
 void launch_sub_means_copy(const double* src, double* dst, long long nv, const double* sums, cudaStream_t s,
                            long long count) {
   if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))

@@ -64,6 +64,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("HBM_LIMIT_MB", 0)
         ih.set_knob("STENCIL_F32", 1)
         ih.set_knob("TRANSFER_F32", 1)
+        ih.set_knob("PROJECT_NORM", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -338,3 +339,14 @@ def test_transfer_f32_matches(ih, n, P):
     v = _solve(ih, n, {"TRANSFER_F32": 1}, fabric_p=P)
     assert v[0] == base[0]
     assert np.abs(v[1] - base[1]).max() <= 1e-6 * np.abs(base[1]).max()
+
+
+@pytest.mark.parametrize("P", [0, 2])
+def test_project_norm_bit_identical(ih, P):
+    """Load projection and its norm in one pass (PROJECT_NORM) == remove_translations + norm, bitwise."""
+    base = _solve(ih, 32, {"PROJECT_NORM": 0}, fabric_p=P)
+    v = _solve(ih, 32, {"PROJECT_NORM": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)

@@ -3,6 +3,8 @@
 // 281-333, 426-451).
 #include "kernels.hpp"
 
+#include <cuda_pipeline.h>
+
 #include <mutex>
 
 namespace ihomgpu {
@@ -314,6 +316,78 @@ __global__ void __launch_bounds__(128) stencil_apply_fast_kernel(GridGeo g, cons
       io.y[k][3 * (size_t)loc + c] = io.f[k] ? TN(TACC(io.f[k][3 * (size_t)loc + c]) - acc[k][c]) : TN(acc[k][c]);
 }
 
+// Streamed variant (knob STENCIL_STREAM, f32 stencils / nodal data / products): a warp's 32
+// consecutive vertices own one contiguous 31 KB block of the blocked stencil layout, which the warp
+// copies into a 3-stage shared-memory ring (three neighbours' 27 rows per stage, 16-byte cp.async,
+// two stages in flight) while it computes; only the gathered neighbour values are loaded directly.
+// Same per-vertex arithmetic and order as stencil_apply_fast_kernel<..., float>: bit-identical.
+constexpr int kStRows = 27;                   // stencil rows per stage (three neighbours)
+constexpr int kStStage = kStRows * 32;        // floats per stage
+template <bool ZL, int NL>
+__global__ void __launch_bounds__(128) stencil_apply_stream_kernel(GridGeo g, const float* __restrict__ st,
+                                                                   RhsN<float> io) {
+  __shared__ __align__(16) float ring[4][3][kStStage];
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h1 >= g.cd[0][1]) return;  // whole warps (cd0 % 32 == 0)
+  const int lane = threadIdx.x & 31, w = threadIdx.y;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  const float* chunk = st + st_index(0, loc & ~31u);  // the warp's 243 x 32 block
+  float(*rg)[kStStage] = ring[w];
+  auto issue = [&](int stage, int slot) {
+    const float4* src = reinterpret_cast<const float4*>(chunk + (size_t)stage * kStStage);
+    float4* dst = reinterpret_cast<float4*>(rg[slot]);
+    for (int i = lane; i < kStStage / 4; i += 32) __pipeline_memcpy_async(dst + i, src + i, 16);
+  };
+  float acc[NL][3] = {};
+  const float* xb[NL][3];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const ZLink<float> xl = ZL ? io.xl[k] : ZLink<float>{io.x[k], io.x[k]};
+    xb[k][0] = zbase(fa, io.x[k], xl, 0);
+    xb[k][1] = io.x[k];
+    xb[k][2] = zbase(fa, io.x[k], xl, 2);
+  }
+  issue(0, 0);
+  __pipeline_commit();
+  issue(1, 1);
+  __pipeline_commit();
+#pragma unroll
+  for (int n3 = 0; n3 < 9; ++n3) {
+    __pipeline_wait_prior(1);
+    __syncwarp();
+    const float* sm = rg[n3 % 3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int n = 3 * n3 + j;
+      float c9[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) c9[e] = sm[(9 * j + e) * 32 + lane];
+      const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const float* xn = xb[k][n / 9] + off;
+        block_fma(c9, __ldg(xn), __ldg(xn + 1), __ldg(xn + 2), acc[k]);
+      }
+    }
+    __syncwarp();
+    if (n3 + 2 < 9) issue(n3 + 2, (n3 + 2) % 3);
+    __pipeline_commit();
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      io.y[k][3 * (size_t)loc + c] = io.f[k] ? io.f[k][3 * (size_t)loc + c] - acc[k][c] : acc[k][c];
+}
+
+static bool stencil_stream_ok(const GridGeo& g) {
+  return knob("STENCIL_STREAM", 1) != 0 && g.cd[0][0] % 32 == 0 && g.size[0] % 32 == 0;
+}
+
 // zm: neighbours known to be zero (zero-start sweep, common.cuh zero_start_mask): their stencil
 // blocks and values are not read -- bit-identical to adding their exact zero products.
 template <typename TS, typename TN>
@@ -480,6 +554,14 @@ static void launch_apply_n(const GridGeo& g, const TS* st, RhsN<TN> io, cudaStre
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+    if constexpr (std::is_same_v<TS, float> && std::is_same_v<TN, float>) {
+      if (stencil_f32() && stencil_stream_ok(g) && b.x == 32) {
+        if (linked) stencil_apply_stream_kernel<true, NL><<<gr, b, 0, s>>>(g, st, io);
+        else stencil_apply_stream_kernel<false, NL><<<gr, b, 0, s>>>(g, st, io);
+        IHOM_LAUNCH_CHECK();
+        return;
+      }
+    }
     if (std::is_same_v<TS, float> && std::is_same_v<TN, float> && stencil_f32()) {
       if (linked) stencil_apply_fast_kernel<TS, TN, true, NL, float><<<gr, b, 0, s>>>(g, st, io);
       else stencil_apply_fast_kernel<TS, TN, false, NL, float><<<gr, b, 0, s>>>(g, st, io);

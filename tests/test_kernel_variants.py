@@ -65,6 +65,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("STENCIL_F32", 1)
         ih.set_knob("TRANSFER_F32", 1)
         ih.set_knob("PROJECT_NORM", 1)
+        ih.set_knob("STENCIL_STREAM", 1)
 
 
 @pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
@@ -346,6 +347,18 @@ def test_project_norm_bit_identical(ih, P):
     """Load projection and its norm in one pass (PROJECT_NORM) == remove_translations + norm, bitwise."""
     base = _solve(ih, 32, {"PROJECT_NORM": 0}, fabric_p=P)
     v = _solve(ih, 32, {"PROJECT_NORM": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(64, 0), (128, 0), (128, 2)])
+def test_stencil_stream_bit_identical(ih, n, P):
+    """Stencil-level residual with each warp's stencil block streamed through a cp.async ring
+    (STENCIL_STREAM) == the direct-load f32 kernel, bitwise (same arithmetic and order)."""
+    base = _solve(ih, n, {"STENCIL_F32": 1, "STENCIL_STREAM": 0}, fabric_p=P)
+    v = _solve(ih, n, {"STENCIL_F32": 1, "STENCIL_STREAM": 1}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

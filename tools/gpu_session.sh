@@ -1,9 +1,12 @@
 set -x
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_kernel_variants.py tests/test_gpu_parity.py -q --timeout 900 > gpurun_out/t_gpu.log 2>&1; echo tests rc $?; tail -3 gpurun_out/t_gpu.log
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?
-python - <<'PY'
-import json
-d = json.load(open("gpurun_out/bench.json"))
-print(d["value"], d["e2e"]["value"], d.get("cycles_per_iteration"), d["objective"], d["kernels"]["vector"], d["kernels"]["reduce"])
+timeout 1200 python -m pytest tests/test_kernel_variants.py -q -x --timeout 900 -k "stream" > gpurun_out/t_var.log 2>&1; echo var rc $?; tail -3 gpurun_out/t_var.log
+for k in 0 1; do IHOM_STENCIL_STREAM=$k timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_st$k.json 2> gpurun_out/bench_st$k.err; echo rc $?
+python - $k <<'PY'
+import json, sys
+d = json.load(open(f"gpurun_out/bench_st{sys.argv[1]}.json"))
+print(sys.argv[1], d["value"], d["e2e"]["value"], d.get("cycles_per_iteration"), d["objective"])
+for k, v in d["kernels"].items():
+    if "residual_f32" in k and not k.startswith("l0"): print("  ", k, round(v["ms"] / 8, 2), v["launches"] / 8, v["GB/s"])
 PY
+done

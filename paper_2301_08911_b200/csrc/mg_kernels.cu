@@ -384,6 +384,76 @@ __global__ void __launch_bounds__(128) stencil_apply_stream_kernel(GridGeo g, co
       io.y[k][3 * (size_t)loc + c] = io.f[k] ? io.f[k][3 * (size_t)loc + c] - acc[k][c] : acc[k][c];
 }
 
+template <typename TS, typename TN>
+__device__ __forceinline__ bool gs_solve_store(const double S[9], const double m[3], const TN* f, size_t loc, TN* y,
+                                               int* err);
+
+// GS colour pass with the streamed stencil block (plain passes only: a zero-start pass needs a few of
+// the 27 blocks, streaming all of them would read more). Same arithmetic and order as
+// stencil_gs_fast_kernel<..., float>: bit-identical.
+template <bool ZL, int NL>
+__global__ void __launch_bounds__(128) stencil_gs_stream_kernel(GridGeo g, const float* __restrict__ st,
+                                                                RhsN<float> io, int color, int* err) {
+  __shared__ __align__(16) float ring[4][3][kStStage];
+  const int h2 = blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h1 >= g.cd[0][1]) return;  // whole warps (cd0 % 32 == 0)
+  const int lane = threadIdx.x & 31, w = threadIdx.y;
+  FastAddr fa;
+  fast_addr(g, color, h0, h1, h2, fa);
+  const unsigned loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
+  const float* chunk = st + st_index(0, loc & ~31u);
+  float(*rg)[kStStage] = ring[w];
+  auto issue = [&](int stage, int slot) {
+    const float4* src = reinterpret_cast<const float4*>(chunk + (size_t)stage * kStStage);
+    float4* dst = reinterpret_cast<float4*>(rg[slot]);
+    for (int i = lane; i < kStStage / 4; i += 32) __pipeline_memcpy_async(dst + i, src + i, 16);
+  };
+  double S[9];
+  stencil_block(st + st_index(9 * 13, loc), S);  // self block: same values, read as the fast kernel does
+  float m[NL][3] = {};
+  const float* ub[NL][3];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const ZLink<float> ul = ZL ? io.xl[k] : ZLink<float>{io.x[k], io.x[k]};
+    ub[k][0] = zbase(fa, io.x[k], ul, 0);
+    ub[k][1] = io.x[k];
+    ub[k][2] = zbase(fa, io.x[k], ul, 2);
+  }
+  issue(0, 0);
+  __pipeline_commit();
+  issue(1, 1);
+  __pipeline_commit();
+#pragma unroll
+  for (int n3 = 0; n3 < 9; ++n3) {
+    __pipeline_wait_prior(1);
+    __syncwarp();
+    const float* sm = rg[n3 % 3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int n = 3 * n3 + j;
+      if (n == 13) continue;
+      float c9[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) c9[e] = sm[(9 * j + e) * 32 + lane];
+      const size_t off = 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]);
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const float* un = ub[k][n / 9] + off;
+        block_fma(c9, __ldg(un), __ldg(un + 1), __ldg(un + 2), m[k]);
+      }
+    }
+    __syncwarp();
+    if (n3 + 2 < 9) issue(n3 + 2, (n3 + 2) % 3);
+    __pipeline_commit();
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const double mk[3] = {double(m[k][0]), double(m[k][1]), double(m[k][2])};
+    if (!gs_solve_store<float, float>(S, mk, io.f[k], loc, io.y[k], err)) return;
+  }
+}
+
 static bool stencil_stream_ok(const GridGeo& g) {
   return knob("STENCIL_STREAM", 1) != 0 && g.cd[0][0] % 32 == 0 && g.size[0] % 32 == 0;
 }
@@ -641,6 +711,14 @@ static void launch_gs_n(const GridGeo& g, const TS* st, RhsN<TN> io, int color, 
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
+    if constexpr (std::is_same_v<TS, float> && std::is_same_v<TN, float>) {
+      if (zm == 0u && stencil_f32() && stencil_stream_ok(g) && b.x == 32) {
+        if (linked) stencil_gs_stream_kernel<true, NL><<<gr, b, 0, s>>>(g, st, io, color, err);
+        else stencil_gs_stream_kernel<false, NL><<<gr, b, 0, s>>>(g, st, io, color, err);
+        IHOM_LAUNCH_CHECK();
+        return;
+      }
+    }
     if (std::is_same_v<TS, float> && std::is_same_v<TN, float> && stencil_f32()) {
       if (linked) stencil_gs_fast_kernel<TS, TN, true, NL, float><<<gr, b, 0, s>>>(g, st, io, color, err, zm);
       else stencil_gs_fast_kernel<TS, TN, false, NL, float><<<gr, b, 0, s>>>(g, st, io, color, err, zm);

@@ -355,8 +355,8 @@ def test_project_norm_bit_identical(ih, P):
 
 @pytest.mark.parametrize("n,P", [(64, 0), (128, 0), (128, 2)])
 def test_stencil_stream_bit_identical(ih, n, P):
-    """Stencil-level residual with each warp's stencil block streamed through a cp.async ring
-    (STENCIL_STREAM) == the direct-load f32 kernel, bitwise (same arithmetic and order)."""
+    """Stencil-level residual and plain GS passes with each warp's stencil block streamed through a
+    cp.async ring (STENCIL_STREAM) == the direct-load f32 kernels, bitwise (same arithmetic and order)."""
     base = _solve(ih, n, {"STENCIL_F32": 1, "STENCIL_STREAM": 0}, fabric_p=P)
     v = _solve(ih, n, {"STENCIL_F32": 1, "STENCIL_STREAM": 1}, fabric_p=P)
     assert v[0] == base[0]

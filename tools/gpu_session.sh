@@ -1,8 +1,12 @@
 set -x
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/t_gpu.log 2>&1; echo gpu tests rc $?; tail -3 gpurun_out/t_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc $?; tail -2 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?; tail -2 gpurun_out/bench.err
-timeout 900 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc $?
-B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-profile"
-timeout 900 ncu --nvtx --nvtx-include timed/ --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01g.csv $B > gpurun_out/launches_r01g.log 2>&1; echo ncu rc $?
+timeout 1200 python -m pytest tests/test_kernel_variants.py -q -x --timeout 900 -k "stream" > gpurun_out/t_var.log 2>&1; echo var rc $?; tail -3 gpurun_out/t_var.log
+for k in 0 1; do IHOM_STENCIL_STREAM=$k timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_st$k.json 2> gpurun_out/bench_st$k.err; echo rc $?
+python - $k <<'PY'
+import json, sys
+d = json.load(open(f"gpurun_out/bench_st{sys.argv[1]}.json"))
+print(sys.argv[1], d["value"], d["e2e"]["value"], d.get("cycles_per_iteration"), d["objective"])
+for k, v in d["kernels"].items():
+    if k.startswith("l1") or k.startswith("l2"): print("  ", k, round(v["ms"] / 8, 2), v["launches"] / 8, v["GB/s"])
+PY
+done

@@ -465,3 +465,39 @@ def test_short_run_invariants(orc):
     for r in recs[1:]:
         assert r["volume"] <= 0.3 + 1e-6
     assert rho.min() >= 1e-3 and rho.max() <= 1.0
+
+
+def test_hadamard_basis_tables_reproduce_k0():
+    """The generated sum/difference-basis element stiffness (csrc/hada_gen.cuh, tools/gen_hada.py) is
+    K0 itself: for arbitrary (lam', mu') and q, y = Hb^T (q W) (Hb u) with W from the 45 generated
+    terms and the 8 (alpha, beta) classes equals q K0 u, K0 from the oracle (src/material.cpp:39-69).
+    Also the C^H identity d^T K0 d' = (Hb d)^T W (Hb d') used by the tensor pass."""
+    import os
+    import re
+
+    import numpy as np
+
+    import oracle
+
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2301_08911_b200", "csrc", "hada_gen.cuh")).read()
+    alpha = [int(x) for x in re.search(r"kHadaAlpha\[kHadaClasses\] = \{([^}]*)\}", src).group(1).split(",")]
+    beta = [int(x) for x in re.search(r"kHadaBeta\[kHadaClasses\] = \{([^}]*)\}", src).group(1).split(",")]
+    terms = []
+    for m in re.finditer(r"w\[(\d+)\] = (?:fma\()?\(?(-?)qh\[(\d+)\]\)? \* uh\[(\d+)\]|"
+                         r"w\[(\d+)\] = fma\(\(?(-?)qh\[(\d+)\]\)?, uh\[(\d+)\]", src):
+        g = m.groups()
+        r, sg, k, c = (g[0], g[1], g[2], g[3]) if g[0] is not None else (g[4], g[5], g[6], g[7])
+        terms.append((int(r), int(c), int(k), -1.0 if sg == "-" else 1.0))
+    assert len(terms) == 45
+    E, nu = 1.0, 0.3
+    K0 = oracle.k0(E, nu).reshape(24, 24)
+    lam, mu = E * nu / ((1 + nu) * (1 - 2 * nu)) / 72.0, E / (2 * (1 + nu)) / 72.0  # lam', mu'
+    h1 = np.array([[1, 1], [-1, 1]])
+    Hb = np.kron(np.kron(h1, np.kron(h1, h1)), np.eye(3))
+    W = np.zeros((24, 24))
+    for r, c, k, sg in terms:
+        W[r, c] += sg * (lam * alpha[k] + mu * beta[k]) / 64.0
+    assert np.allclose(Hb.T @ W @ Hb, K0, rtol=0, atol=1e-14 * np.abs(K0).max())
+    rng = np.random.default_rng(3)
+    d1, d2 = rng.uniform(-1, 1, 24), rng.uniform(-1, 1, 24)
+    assert abs(d1 @ K0 @ d2 - (Hb @ d1) @ W @ (Hb @ d2)) < 1e-13

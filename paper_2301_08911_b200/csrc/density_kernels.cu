@@ -196,23 +196,37 @@ void sensitivity_filter(const int n[3], const double* sens, const double* rho, d
   IHOM_CUDA(cudaStreamSynchronize(s));
 }
 
-// out = x^p  /  out = g * p * x^(p-1)
-__global__ void pow_kernel(const double* __restrict__ x, const double* __restrict__ g, double p, long long m,
+// x^k for a small integer k by repeated multiplication (the SIMP exponent 3 of the default config):
+// the f64 pow() is a log/exp sequence ~10x the cost of this memory-bound pass; both are within an
+// ulp or two of the reference's std::pow
+__device__ __forceinline__ double ipow(double x, int k) {
+  double r = 1.0;
+  for (int j = 0; j < k; ++j) r *= x;
+  return r;
+}
+
+// out = x^p  /  out = g * p * x^(p-1); ip > 0: p == ip exactly (integer exponent <= 4)
+__global__ void pow_kernel(const double* __restrict__ x, const double* __restrict__ g, double p, int ip, long long m,
                            double* __restrict__ out) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  out[i] = g ? g[i] * p * pow(x[i], p - 1.0) : pow(x[i], p);
+  if (ip > 0) out[i] = g ? g[i] * p * ipow(x[i], ip - 1) : ipow(x[i], ip);
+  else out[i] = g ? g[i] * p * pow(x[i], p - 1.0) : pow(x[i], p);
+}
+
+static int int_exponent(double p) {
+  return (knob("POW_INT", 1) != 0 && p >= 1.0 && p <= 4.0 && p == double(int(p))) ? int(p) : 0;
 }
 
 void pow_field(const double* x, double p, long long m, double* out, cudaStream_t s) {
   ProfScope ps(s, "pow", double(m) * 16.0);
-  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, nullptr, p, m, out);
+  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, nullptr, p, int_exponent(p), m, out);
   IHOM_LAUNCH_CHECK();
 }
 
 void pow_backward(const double* x, const double* g, double p, long long m, double* out, cudaStream_t s) {
   ProfScope ps(s, "pow", double(m) * 24.0);
-  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, g, p, m, out);
+  pow_kernel<<<ceil_div(m, 256), 256, 0, s>>>(x, g, p, int_exponent(p), m, out);
   IHOM_LAUNCH_CHECK();
 }
 

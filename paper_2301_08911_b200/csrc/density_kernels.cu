@@ -104,21 +104,32 @@ __global__ void filter_kernel(int nx, int ny, int nz, int ntaps, const double* _
 // (zero outside the ball); per-axis wrapped offsets are computed once per thread,
 // so every tap is one IADD3 + load (no modulo per tap).
 __constant__ double c_cube_w[7 * 7 * 7];
-template <int R>
+// NZ elements per thread (planes z, z + nz/NZ, ...): independent tap chains interleaved for latency
+// hiding; every element keeps its own z, y, x tap order (bit-identical to NZ = 1).
+template <int R, int NZ = 1>
 __global__ void __launch_bounds__(256) filter_cube_kernel(int nx, int ny, int nz, const double* __restrict__ f,
                                                           ZLink<double> fl, double* __restrict__ out) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, z = blockIdx.z;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= nx) return;
-  int X[2 * R + 1], Y[2 * R + 1], Z[2 * R + 1];
-  const double* zb[2 * R + 1];  // z-slab: planes beyond the slab come from its neighbours
+  int X[2 * R + 1], Y[2 * R + 1], Z[NZ][2 * R + 1];
+  const double* zb[NZ][2 * R + 1];  // z-slab: planes beyond the slab come from its neighbours
+  int zs[NZ];
+#pragma unroll
+  for (int k = 0; k < NZ; ++k) zs[k] = blockIdx.z + k * (nz / NZ);
 #pragma unroll
   for (int d = -R; d <= R; ++d) {
     X[d + R] = wrapd(x + d, nx);
     Y[d + R] = nx * wrapd(y + d, ny);
-    Z[d + R] = nx * ny * wrapd(z + d, nz);
-    zb[d + R] = z + d < 0 ? fl.lo : (z + d >= nz ? fl.hi : f);
+#pragma unroll
+    for (int k = 0; k < NZ; ++k) {
+      const int z = zs[k];
+      Z[k][d + R] = nx * ny * wrapd(z + d, nz);
+      zb[k][d + R] = z + d < 0 ? fl.lo : (z + d >= nz ? fl.hi : f);
+    }
   }
-  double s = 0.0;
+  double s[NZ];
+#pragma unroll
+  for (int k = 0; k < NZ; ++k) s[k] = 0.0;
 #pragma unroll
   for (int dz = 0; dz <= 2 * R; ++dz)
 #pragma unroll
@@ -126,9 +137,14 @@ __global__ void __launch_bounds__(256) filter_cube_kernel(int nx, int ny, int nz
 #pragma unroll
       for (int dx = 0; dx <= 2 * R; ++dx) {
         const double w = c_cube_w[(dz * (2 * R + 1) + dy) * (2 * R + 1) + dx];
-        if (w != 0.0) s += w * __ldg(zb[dz] + (size_t)(X[dx] + Y[dy] + Z[dz]));  // kernel_taps order: z, y, x
+        if (w != 0.0) {
+#pragma unroll
+          for (int k = 0; k < NZ; ++k)  // kernel_taps order: z, y, x
+            s[k] += w * __ldg(zb[k][dz] + (size_t)(X[dx] + Y[dy] + Z[k][dz]));
+        }
       }
-  out[x + (size_t)nx * (y + (size_t)ny * z)] = s;
+#pragma unroll
+  for (int k = 0; k < NZ; ++k) out[x + (size_t)nx * (y + (size_t)ny * zs[k])] = s[k];
 }
 
 static std::mutex g_const_mu;  // host staging of the constant-memory tap tables (z-slab threads)
@@ -150,7 +166,9 @@ static bool filter_cube(const int n[3], const std::vector<Tap>& taps, double rad
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_cube_w, cube, sizeof(double) * W * W * W, 0, cudaMemcpyHostToDevice, s));
   const dim3 b(256), g(ceil_div(n[0], 256), n[1], n[2]);
   fl = resolve(fl, f);
-  if (R == 1) filter_cube_kernel<1><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
+  if (R == 1 && n[2] % 4 == 0 && knob("FILTER_NZ", 1) != 0)
+    filter_cube_kernel<1, 4><<<dim3(g.x, g.y, n[2] / 4), b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
+  else if (R == 1) filter_cube_kernel<1><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
   else if (R == 2) filter_cube_kernel<2><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
   else filter_cube_kernel<3><<<g, b, 0, s>>>(n[0], n[1], n[2], f, fl, out);
   IHOM_LAUNCH_CHECK();

@@ -25,6 +25,7 @@ see DESIGN.md), each step a bounded sample (one 128^3 iteration after the warm-u
 iterations, scaled by element count to the workload).
 """
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -43,8 +44,8 @@ SAMPLE_RESO = 128  # CPU sample grid (capped at the workload's): ~5 s per oracle
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--reso", type=int, default=512)
     ap.add_argument("--obj", default="npr-relaxed")
@@ -206,16 +207,23 @@ def run_ours(args):
                        solver_mode=args.mode, device=local)
     fab = None
     m = args.reso ** 3
+    restarts = []
+
+    def make_opt(init_rho=None):
+        c = cfg if init_rho is None else dataclasses.replace(cfg, init="file")
+        if world > 1 and args.multi == "slab":
+            return ih.Optimizer(c, init_rho=init_rho, fabric=fab, rank=rank)
+        o = ih.Optimizer(c, init_rho=init_rho)
+        if world > 1 and args.multi == "loads":
+            from paper_2301_08911_b200 import distributed as dd
+            o.set_comm(dd.share_unique_id(rank), rank, world, dd.load_owners(world))
+        return o
+
     if world > 1 and args.multi == "slab":
         from paper_2301_08911_b200 import distributed as dd
         fab = dd.ipc_fabric(rank, world, device=local)
-        opt = ih.Optimizer(cfg, fabric=fab, rank=rank)
-        m = opt.m  # this rank's slab of the design
-    else:
-        opt = ih.Optimizer(cfg)
-    if world > 1 and args.multi == "loads":
-        from paper_2301_08911_b200 import distributed as dd
-        opt.set_comm(dd.share_unique_id(rank), rank, world, dd.load_owners(world))
+    opt = make_opt()
+    m = opt.m if fab is not None else m  # this rank's slab of the design
     dev_rho = torch.empty(m, dtype=torch.float64, device="cuda")
     host_rho = torch.empty(m, dtype=torch.float64).pin_memory()
     host_np = host_rho.numpy()
@@ -226,10 +234,36 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    def restart(st, rec):
+        """A step that ends the run (solver failed / ConvergeChecker / last iteration) skipped the
+        sensitivity+OC half of the iteration (src/runner.cpp:105-113): it is not a full step. Re-create the
+        optimiser from the current design (iteration counter and warm starts reset) and step again.
+        Status is collective (rank-order reductions), so every rank restarts together."""
+        nonlocal opt, ext
+        restarts.append({"status": ih.Optimizer.STATUS[st], "iter": rec["iter"]})
+        design = opt.design()
+        opt.close()
+        opt = make_opt(init_rho=design)
+        ext = torch.cuda.ExternalStream(opt.stream())
+
+    def full_step(rho_in, rho_out, timed):
+        """One complete optimisation iteration; returns (ms, record). Incomplete steps are re-run."""
+        for _ in range(3):
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(ext)
+            st, rec = opt.step(rho_in=rho_in, rho_out=rho_out)
+            b.record(ext)
+            barrier()
+            if st == 0:
+                return a.elapsed_time(b), rec
+            restart(st, rec)
+            if isinstance(rho_in, torch.Tensor):
+                rho_in = None  # the restarted optimiser already holds the design
+        raise RuntimeError("three consecutive incomplete optimisation steps")
+
     for _ in range(args.warmup):
-        st, _ = opt.step(rho_out=dev_rho)
-        if st != 0:
-            raise RuntimeError(f"optimisation stopped during warm-up: {ih.Optimizer.STATUS[st]}")
+        full_step(None, dev_rho, False)
     free_b, total_b = torch.cuda.mem_get_info()  # the library allocates with cudaMalloc: counted here
     hbm_used_gb = (total_b - free_b) / 1e9
     clocks = ClockSampler(local)
@@ -239,23 +273,15 @@ def run_ours(args):
     l0 = ih.launch_count()
     dev_ms, e2e_ms, recs = [], [], []
     for k in range(args.steps):
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(ext)
-        st, rec = opt.step(rho_in=dev_rho, rho_out=dev_rho)
-        b.record(ext)
-        barrier()
-        dev_ms.append(a.elapsed_time(b))
+        ms, rec = full_step(dev_rho, dev_rho, True)
+        dev_ms.append(ms)
         recs.append(rec)
         if not args.no_e2e:
+            # e2e leg: the next iteration through pinned host buffers (the design advances one more
+            # iteration; both legs sample the same phase of the run)
             host_np[:] = dev_rho.cpu().numpy()  # current design -> pinned host (outside the timed region)
-            barrier()
-            a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a2.record(ext)
-            st2, rec2 = opt.step(rho_in=host_np, rho_out=host_np)
-            b2.record(ext)
-            barrier()
-            e2e_ms.append(a2.elapsed_time(b2))
+            ms2, rec2 = full_step(host_np, host_np, True)
+            e2e_ms.append(ms2)
             dev_rho.copy_(torch.from_numpy(host_np).to("cuda"))
     launches = ih.launch_count() - l0
     torch.cuda.nvtx.range_pop()
@@ -307,7 +333,8 @@ def run_ours(args):
             "roofline": roofline, "gpu_launches": launches, "clocks": clk,
             "hbm_used_gb_per_gpu": round(hbm_used_gb, 2),
             "cycles_per_iteration": [r["cycles"] for r in recs],
-            "objective": [r["objective"] for r in recs], "kernels": kernels}
+            "objective": [r["objective"] for r in recs], "restarts": restarts,
+            "iterations_per_step": 1 if args.no_e2e else 2, "kernels": kernels}
     if t_e2e is not None:
         moved = 8 * (args.reso ** 3 if fab is not None else m)  # whole job: every rank moves its slab
         line["e2e"] = {"value": round(t_e2e, 4), "unit": "s/iteration", "h2d_bytes_per_step": moved,

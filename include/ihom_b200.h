@@ -125,6 +125,10 @@ int ihom_apply(ihom_ctx* ctx, int level, const double* x_aos, double* y_aos);   
 int ihom_relax(ihom_ctx* ctx, int level, int sweeps);                              /* relax */
 int ihom_compute_residual(ihom_ctx* ctx, int level);                               /* compute_residual */
 int ihom_coarsest_solve(ihom_ctx* ctx);                                            /* coarsest_solve */
+/* Coarsest-level dense solve of a caller-assembled operator (raw [3nv][3nv], dof order 3*loc+c)
+   for load f [3nv]: factor_coarsest + coarsest_solve (src/multigrid.cpp:368-451) with the device
+   kernel; x = translation-free solution, rel = ||A'x - Pf|| / ||Pf|| (A' the projected operator). */
+int ihom_coarse_dense_solve(long long nv, const double* raw, const double* f, double* x, double* rel);
 int ihom_v_cycle(ihom_ctx* ctx, double* rel);                                      /* v_cycle */
 int ihom_solve(ihom_ctx* ctx, const double* f_aos, double* u_aos, ihom_solve_stats* st); /* solve(f, u, opts) */
 int ihom_get_stencil(ihom_ctx* ctx, int level, double* out /* [nv][27][3][3] */);

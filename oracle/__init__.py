@@ -121,6 +121,29 @@ def set_threads(n: int) -> int:
     return lib().orc_set_threads(int(n))
 
 
+def set_coarse_project(on: bool) -> None:
+    """Coarsest-operator translation projection (the one documented deviation; default on).
+    False restores the reference's raw operator and its throw (src/multigrid.cpp:446-447)."""
+    lib().orc_set_coarse_project(int(bool(on)))
+
+
+def set_coarse_dump(path) -> None:
+    """Write (raw operator, load) of the next failing coarsest solve to `path` (fixture generation)."""
+    lib().orc_set_coarse_dump(None if path is None else str(path).encode())
+
+
+def coarse_dense_solve(raw, f):
+    """Coarsest-level dense solve of an assembled operator (dof order 3*loc+c): the hierarchy's
+    factor_coarsest + coarsest_solve (src/multigrid.cpp:368-451) on a given matrix. Returns (x, rel)."""
+    raw = np.ascontiguousarray(raw, np.float64)
+    N = raw.shape[0]
+    f = np.ascontiguousarray(f, np.float64).ravel()
+    x = np.zeros(N)
+    rel = C.c_double()
+    _check(lib().orc_coarse_dense_solve(C.c_longlong(N // 3), _ptr(raw), _ptr(f), _ptr(x), C.byref(rel)))
+    return x, rel.value
+
+
 # ---------------------------------------------------------------- basics
 def k0(E=1.0, nu=0.3) -> np.ndarray:
     out = np.zeros(576)

@@ -13,8 +13,11 @@
 //     sparse direct (energy identity) oracle reproduce the reference's
 //     known-answer tests (tests/test_material.cpp, tests/test_homogenization.cpp,
 //     tests/test_objective.cpp, tests/test_runner.cpp);
-//   * Eigen (absent here) is replaced by plain loops; the coarsest LDLT by a
-//     dense Cholesky of the same shifted SPD matrix (rounding-level difference).
+//   * Eigen (absent here) is replaced by plain loops; the coarsest LDLT by the
+//     same diagonal-pivoting LDL^T on a dense matrix (rounding-level difference).
+//   * ONE DEVIATION (g_coarse_project, default on, orc_set_coarse_project(0) restores
+//     the reference): the coarsest operator is projected onto the translation-free
+//     subspace before factoring, see project_translations().
 //
 // Layouts follow the reference exactly: nodal fields AoS a[3*loc+c] in the
 // colour-block order of inc/grid.hpp:73-78, element fields x-fastest.
@@ -24,6 +27,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -610,39 +614,141 @@ struct Level {  // inc/multigrid.hpp:38-46
   explicit Level(const Grid& g) : grid(g), u(g), f(g), r(g) {}
 };
 
-// Dense SPD Cholesky standing in for Eigen::LDLT (src/multigrid.cpp:368-383).
-struct DenseChol {
+// Coarsest-operator deviation switch (default on): project the assembled operator onto the
+// translation-free subspace, a <- P a P (P = I - (1/nv) sum_c t_c t_c^T), before the shift.
+// The reference factors the raw operator (src/multigrid.cpp:368-383); with f32 Galerkin
+// stencils A t_c ~ 1e-7 op_scale and on designs with floating islands its refinement stalls
+// above the 1e-3 gate and throws (src/multigrid.cpp:446-447) -- 0 restores that behaviour.
+int g_coarse_project = 1;
+
+void project_translations(std::vector<double>& a, i64 nv) {
+  const i64 N = 3 * nv;
+  std::vector<double> b(a.size());
+  // row means of every component block (aP), then column means ((aP) -> P(aP))
+  for (i64 i = 0; i < N; ++i) {
+    double m[3] = {0, 0, 0};
+    for (i64 j = 0; j < N; ++j) m[j % 3] += a[size_t(i * N + j)];
+    for (i64 j = 0; j < N; ++j) b[size_t(i * N + j)] = a[size_t(i * N + j)] - m[j % 3] / double(nv);
+  }
+  for (i64 j = 0; j < N; ++j) {
+    double m[3] = {0, 0, 0};
+    for (i64 i = 0; i < N; ++i) m[i % 3] += b[size_t(i * N + j)];
+    for (i64 i = 0; i < N; ++i) a[size_t(i * N + j)] = b[size_t(i * N + j)] - m[i % 3] / double(nv);
+  }
+  for (i64 i = 0; i < N; ++i)
+    for (i64 j = 0; j < i; ++j) {
+      const double s = 0.5 * (a[size_t(i * N + j)] + a[size_t(j * N + i)]);
+      a[size_t(i * N + j)] = a[size_t(j * N + i)] = s;
+    }
+}
+
+// Dense LDL^T with symmetric diagonal pivoting: Eigen::LDLT's algorithm
+// (src/multigrid.cpp:380 coarse_ldlt_.compute), pivot = largest remaining |diagonal|.
+struct DenseLDLT {
   int n = 0;
-  std::vector<double> L;
-  void compute(const std::vector<double>& a, int dim) {
+  std::vector<double> L;  // unit lower below the diagonal, D on the diagonal
+  std::vector<int> perm;  // position -> original index
+  void compute(std::vector<double> a, int dim) {
     n = dim;
-    L.assign(size_t(n) * n, 0.0);
-    for (int j = 0; j < n; ++j) {
-      double d = a[size_t(j) * n + j];
-      for (int k = 0; k < j; ++k) d -= L[size_t(j) * n + k] * L[size_t(j) * n + k];
-      if (!(d > 0.0)) throw std::runtime_error("coarsest-level factorization failed");
-      const double ljj = std::sqrt(d);
-      L[size_t(j) * n + j] = ljj;
-      for (int i = j + 1; i < n; ++i) {
-        double s = a[size_t(i) * n + j];
-        for (int k = 0; k < j; ++k) s -= L[size_t(i) * n + k] * L[size_t(j) * n + k];
-        L[size_t(i) * n + j] = s / ljj;
+    perm.resize(size_t(n));
+    for (int i = 0; i < n; ++i) perm[size_t(i)] = i;
+    for (int k = 0; k < n; ++k) {
+      int p = k;
+      for (int i = k + 1; i < n; ++i)
+        if (std::fabs(a[size_t(i) * n + i]) > std::fabs(a[size_t(p) * n + p])) p = i;
+      if (p != k) {
+        for (int j = 0; j < n; ++j) std::swap(a[size_t(k) * n + j], a[size_t(p) * n + j]);
+        for (int i = 0; i < n; ++i) std::swap(a[size_t(i) * n + k], a[size_t(i) * n + p]);
+        std::swap(perm[size_t(k)], perm[size_t(p)]);
+      }
+      double d = a[size_t(k) * n + k];
+      for (int j = 0; j < k; ++j) d -= a[size_t(k) * n + j] * a[size_t(k) * n + j] * a[size_t(j) * n + j];
+      if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) throw std::runtime_error("coarsest-level factorization failed");
+      a[size_t(k) * n + k] = d;
+      for (int i = k + 1; i < n; ++i) {
+        double s = a[size_t(i) * n + k];
+        for (int j = 0; j < k; ++j) s -= a[size_t(i) * n + j] * a[size_t(k) * n + j] * a[size_t(j) * n + j];
+        a[size_t(i) * n + k] = s / d;
       }
     }
+    L = std::move(a);
   }
   std::vector<double> solve(const std::vector<double>& b) const {
-    std::vector<double> y(b);
-    for (int i = 0; i < n; ++i) {
-      double s = y[size_t(i)];
-      for (int k = 0; k < i; ++k) s -= L[size_t(i) * n + k] * y[size_t(k)];
-      y[size_t(i)] = s / L[size_t(i) * n + i];
-    }
-    for (int i = n - 1; i >= 0; --i) {
-      double s = y[size_t(i)];
-      for (int k = i + 1; k < n; ++k) s -= L[size_t(k) * n + i] * y[size_t(k)];
-      y[size_t(i)] = s / L[size_t(i) * n + i];
+    std::vector<double> y(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) y[size_t(i)] = b[size_t(perm[size_t(i)])];
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < i; ++k) y[size_t(i)] -= L[size_t(i) * n + k] * y[size_t(k)];
+    for (int i = 0; i < n; ++i) y[size_t(i)] /= L[size_t(i) * n + i];
+    for (int i = n - 1; i >= 0; --i)
+      for (int k = i + 1; k < n; ++k) y[size_t(i)] -= L[size_t(k) * n + i] * y[size_t(k)];
+    std::vector<double> x(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) x[size_t(perm[size_t(i)])] = y[size_t(i)];
+    return x;
+  }
+};
+
+// Coarsest dense solve (src/multigrid.cpp:368-383 factor, :426-451 solve) on an assembled
+// operator `raw` in dof order 3*loc + c. solve() takes the translation-free load and returns the
+// relative residual after refinement; the caller applies the 1e-3 singularity gate.
+std::string g_dump_path;  // non-empty: dump (raw operator, load) of a failing coarsest solve here
+
+struct CoarseSolver {
+  i64 nv = 0;
+  double op_scale = 0.0;
+  std::vector<double> raw, cmat;
+  DenseLDLT ldlt;
+  void factor(std::vector<double> a, i64 nverts) {
+    nv = nverts;
+    const i64 N = 3 * nv;
+    raw = a;
+    double dsum = 0.0;
+    for (i64 i = 0; i < N; ++i) dsum += a[size_t(i * N + i)];
+    op_scale = dsum / double(N);  // :373
+    if (g_coarse_project) project_translations(a, nv);
+    cmat = a;
+    for (i64 i = 0; i < nv; ++i)  // :374-379 deflation shift
+      for (i64 j = 0; j < nv; ++j)
+        for (int c = 0; c < 3; ++c) a[size_t((3 * i + c) * N + 3 * j + c)] += op_scale / double(nv);
+    ldlt.compute(std::move(a), int(N));
+  }
+  std::vector<double> mul(const std::vector<double>& x) const {
+    const size_t N = x.size();
+    std::vector<double> y(N, 0.0);
+    for (size_t i = 0; i < N; ++i) {
+      double s = 0.0;
+      for (size_t j = 0; j < N; ++j) s += cmat[i * N + j] * x[j];
+      y[i] = s;
     }
     return y;
+  }
+  double resid(const std::vector<double>& x, const std::vector<double>& f) const {
+    const std::vector<double> ax = mul(x);
+    double s = 0.0;
+    for (size_t i = 0; i < f.size(); ++i) s += (ax[i] - f[i]) * (ax[i] - f[i]);
+    return std::sqrt(s);
+  }
+  double solve(const std::vector<double>& fv, double fn, std::vector<double>& x) const {  // :434-447
+    x = ldlt.solve(fv);
+    double rel = resid(x, fv) / fn;
+    for (int it = 0; it < 3 && rel > 1e-9; ++it) {
+      const std::vector<double> ax = mul(x);
+      std::vector<double> r(fv.size());
+      for (size_t i = 0; i < r.size(); ++i) r[i] = fv[i] - ax[i];
+      const std::vector<double> dx = ldlt.solve(r);
+      for (size_t i = 0; i < x.size(); ++i) x[i] += dx[i];
+      rel = resid(x, fv) / fn;
+    }
+    return rel;
+  }
+  void dump(const std::vector<double>& fv) const {
+    if (g_dump_path.empty()) return;
+    FILE* fp = std::fopen(g_dump_path.c_str(), "wb");
+    if (!fp) return;
+    const long long hdr[2] = {nv, 3 * nv};
+    std::fwrite(hdr, sizeof(hdr), 1, fp);
+    std::fwrite(raw.data(), sizeof(double), raw.size(), fp);
+    std::fwrite(fv.data(), sizeof(double), fv.size(), fp);
+    std::fclose(fp);
   }
 };
 
@@ -713,18 +819,15 @@ class Hierarchy {  // inc/multigrid.hpp:53-93, src/multigrid.cpp:245-501
       lev.u.zero();
       return;
     }
-    std::vector<double> x = chol_.solve(fv);
+    std::vector<double> x;
     if (fn > 0.0) {
-      double rel = resid_norm(x, fv) / fn;
-      for (int it = 0; it < 3 && rel > 1e-9; ++it) {
-        std::vector<double> r(fv.size());
-        const std::vector<double> ax = dense_mul(x);
-        for (size_t i = 0; i < r.size(); ++i) r[i] = fv[i] - ax[i];
-        const std::vector<double> dx = chol_.solve(r);
-        for (size_t i = 0; i < x.size(); ++i) x[i] += dx[i];
-        rel = resid_norm(x, fv) / fn;
+      const double rel = coarse_.solve(fv, fn, x);
+      if (!(rel < 1e-3)) {
+        coarse_.dump(fv);
+        throw std::runtime_error("coarsest operator is singular beyond translations");
       }
-      if (!(rel < 1e-3)) throw std::runtime_error("coarsest operator is singular beyond translations");
+    } else {
+      x = coarse_.ldlt.solve(fv);
     }
     lev.u.a = x;
     remove_translations(lev.u);
@@ -776,7 +879,6 @@ class Hierarchy {  // inc/multigrid.hpp:53-93, src/multigrid.cpp:245-501
     return st;
   }
 
-  const std::vector<double>& coarse_matrix() const { return cmat_; }
 
  private:
   void assemble_from_elements(int coarse) {  // :281-305
@@ -861,41 +963,15 @@ class Hierarchy {  // inc/multigrid.hpp:53-93, src/multigrid.cpp:245-501
   }
   void factor_coarsest() {  // :368-383 (op_scale_ = mean diagonal, :373)
     const int lc = num_levels() - 1;
-    std::vector<double> a = assemble_dense(lc);
-    cmat_ = a;
-    const i64 nv = levels_[size_t(lc)].grid.nv();
-    const i64 N = 3 * nv;
-    double dsum = 0.0;
-    for (i64 i = 0; i < N; ++i) dsum += a[size_t(i * N + i)];
-    op_scale_ = dsum / double(N);
-    for (i64 i = 0; i < nv; ++i)
-      for (i64 j = 0; j < nv; ++j)
-        for (int c = 0; c < 3; ++c) a[size_t((3 * i + c) * N + 3 * j + c)] += op_scale_ / double(nv);
-    chol_.compute(a, int(N));
-  }
-  std::vector<double> dense_mul(const std::vector<double>& x) const {
-    const size_t N = x.size();
-    std::vector<double> y(N, 0.0);
-    for (size_t i = 0; i < N; ++i) {
-      double s = 0.0;
-      for (size_t j = 0; j < N; ++j) s += cmat_[i * N + j] * x[j];
-      y[i] = s;
-    }
-    return y;
-  }
-  double resid_norm(const std::vector<double>& x, const std::vector<double>& f) const {
-    const std::vector<double> ax = dense_mul(x);
-    double s = 0.0;
-    for (size_t i = 0; i < f.size(); ++i) s += (ax[i] - f[i]) * (ax[i] - f[i]);
-    return std::sqrt(s);
+    coarse_.factor(assemble_dense(lc), levels_[size_t(lc)].grid.nv());
+    op_scale_ = coarse_.op_scale;
   }
 
   double penal_;
   K0 ks_;
   Tables tab_;
   std::vector<Level<T>> levels_;
-  DenseChol chol_;
-  std::vector<double> cmat_;
+  CoarseSolver coarse_;
   double op_scale_ = 0.0;
   bool density_set_ = false;
 };
@@ -1497,6 +1573,36 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+int orc_set_coarse_project(int on) {
+  g_coarse_project = on != 0;
+  return 0;
+}
+int orc_set_coarse_dump(const char* path) {
+  g_dump_path = path ? path : "";
+  return 0;
+}
+// Standalone coarsest solve of an assembled operator (fixtures): projection/shift/LDLT/refinement
+// exactly as the hierarchy's; f is made translation-free first (src/multigrid.cpp:427).
+int orc_coarse_dense_solve(long long nv, const double* raw, const double* f, double* x_out, double* rel_out) {
+  ORC_TRY({
+    const i64 N = 3 * nv;
+    CoarseSolver cs;
+    cs.factor(std::vector<double>(raw, raw + N * N), nv);
+    std::vector<double> fv(f, f + N);
+    for (int c = 0; c < 3; ++c) {
+      double m = 0.0;
+      for (i64 i = 0; i < nv; ++i) m += fv[size_t(3 * i + c)];
+      m /= double(nv);
+      for (i64 i = 0; i < nv; ++i) fv[size_t(3 * i + c)] -= m;
+    }
+    double fn = 0.0;
+    for (double v : fv) fn += v * v;
+    fn = std::sqrt(fn);
+    std::vector<double> x;
+    *rel_out = cs.solve(fv, fn, x);
+    std::copy(x.begin(), x.end(), x_out);
+  })
+}
 int orc_set_threads(int n) {
 #ifdef _OPENMP
   if (n > 0) omp_set_num_threads(n);

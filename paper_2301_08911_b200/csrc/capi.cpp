@@ -418,6 +418,49 @@ int ihom_coarsest_solve(ihom_ctx* ctx) {
   });
 }
 
+int ihom_coarse_dense_solve(long long nv, const double* raw, const double* f, double* x, double* rel) {
+  return guarded([&] {
+    if (nv <= 0 || !raw || !f || !x) throw std::invalid_argument("coarse_dense_solve: null or empty input");
+    const long long N = 3 * nv;
+    std::vector<double> a(raw, raw + N * N), inv;
+    const double op_scale = factor_coarse_dense(a, nv, inv);
+    cudaStream_t s = nullptr;
+    IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf<double> dA, dInv, df, du, work;
+    DevBuf<int> err;
+    dA.alloc(a.size());
+    dInv.alloc(inv.size());
+    df.alloc(size_t(N));
+    du.alloc(size_t(N));
+    work.alloc(size_t(3 * N));
+    err.alloc(1);
+    IHOM_CUDA(cudaMemcpyAsync(dA.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaMemcpyAsync(dInv.p, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaMemcpyAsync(df.p, f, sizeof(double) * size_t(N), cudaMemcpyHostToDevice, s));
+    IHOM_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+    launch_coarsest_solve<double>(int(N), nv, dInv.p, dA.p, df.p, du.p, 1e-12 * op_scale * std::sqrt(double(N)),
+                                  work.p, err.p, s);
+    int e = 0;
+    std::vector<double> fp(static_cast<size_t>(N));
+    IHOM_CUDA(cudaMemcpyAsync(x, du.p, sizeof(double) * size_t(N), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaMemcpyAsync(fp.data(), df.p, sizeof(double) * size_t(N), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaMemcpyAsync(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    IHOM_CUDA(cudaStreamDestroy(s));
+    if (rel) {  // ||A x - f|| / ||f|| against the operator the solve used, f translation-free
+      double rn = 0.0, fn = 0.0;
+      for (long long i = 0; i < N; ++i) {
+        double y = 0.0;
+        for (long long j = 0; j < N; ++j) y += a[size_t(i * N + j)] * x[j];
+        rn += (y - fp[size_t(i)]) * (y - fp[size_t(i)]);
+        fn += fp[size_t(i)] * fp[size_t(i)];
+      }
+      *rel = fn > 0.0 ? std::sqrt(rn / fn) : 0.0;
+    }
+    if (e) throw NumericError("coarsest operator is singular beyond translations");
+  });
+}
+
 int ihom_v_cycle(ihom_ctx* ctx, double* rel) {
   return guarded([&] { ctx->with([&](auto& h) { *rel = h.hierarchy().v_cycle(h.options()); }); });
 }

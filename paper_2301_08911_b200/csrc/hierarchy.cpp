@@ -56,36 +56,97 @@ std::vector<double> assemble_dense_stencil(const GridGeo& g, const std::vector<T
   return a;
 }
 
-// Cholesky of the shifted SPD matrix (stands in for Eigen::LDLT,
-// src/multigrid.cpp:380-382) and its explicit inverse.
-std::vector<double> spd_inverse(std::vector<double> a, int N) {
+// Translation projection of the coarsest operator: a <- P a P, P = I - (1/nv) sum_c t_c t_c^T
+// (t_c = unit translation of component c), then symmetrised. The f32 Galerkin stencils leave
+// A*t_c at ~1e-7 op_scale; on designs with floating islands (near-null modes ~1e-8 op_scale)
+// that leak makes the reference's refinement stall above its 1e-3 gate
+// (src/multigrid.cpp:441-447). Projection makes the deflated system exactly consistent.
+// Knob COARSE_PROJECT=0 restores the reference (unprojected) operator.
+void project_translations(std::vector<double>& a, long long nv) {
+  const long long N = 3 * nv;
+  const double inv_nv = 1.0 / double(nv);
+  for (long long i = 0; i < N; ++i) {  // a P: subtract per-component row means
+    double* row = a.data() + size_t(i * N);
+    double m[3] = {0.0, 0.0, 0.0};
+    for (long long j = 0; j < nv; ++j)
+      for (int c = 0; c < 3; ++c) m[c] += row[3 * j + c];
+    for (int c = 0; c < 3; ++c) m[c] *= inv_nv;
+    for (long long j = 0; j < nv; ++j)
+      for (int c = 0; c < 3; ++c) row[3 * j + c] -= m[c];
+  }
+  std::vector<double> m(size_t(3 * N), 0.0);  // P (aP): per-component column means
+  for (long long i = 0; i < nv; ++i)
+    for (int r = 0; r < 3; ++r) {
+      const double* row = a.data() + size_t((3 * i + r) * N);
+      double* mr = m.data() + size_t(r * N);
+      for (long long k = 0; k < N; ++k) mr[k] += row[k];
+    }
+  for (auto& v : m) v *= inv_nv;
+  for (long long i = 0; i < nv; ++i)
+    for (int r = 0; r < 3; ++r) {
+      double* row = a.data() + size_t((3 * i + r) * N);
+      const double* mr = m.data() + size_t(r * N);
+      for (long long k = 0; k < N; ++k) row[k] -= mr[k];
+    }
+  for (long long i = 0; i < N; ++i)
+    for (long long j = i + 1; j < N; ++j) {
+      const double s = 0.5 * (a[size_t(i * N + j)] + a[size_t(j * N + i)]);
+      a[size_t(i * N + j)] = s;
+      a[size_t(j * N + i)] = s;
+    }
+}
+
+// Symmetric LDL^T with diagonal pivoting (the algorithm of Eigen::LDLT, which the reference
+// uses at src/multigrid.cpp:380: at step k the largest remaining |diagonal| is swapped in), then
+// the explicit inverse A^-1 = Pm^T L^-T D^-1 L^-1 Pm for the device matvecs. Unlike a Cholesky it
+// tolerates the slightly indefinite near-null modes f32 stencils can produce; it fails only on
+// an exactly zero or non-finite pivot (Eigen's NumericalIssue).
+std::vector<double> ldlt_inverse(std::vector<double> a, int N) {
+  std::vector<int> perm(static_cast<size_t>(N));
+  for (int i = 0; i < N; ++i) perm[size_t(i)] = i;
+  auto A = [&](int i, int j) -> double& { return a[size_t(i) * N + j]; };
+  std::vector<double> t(static_cast<size_t>(N));
+  for (int k = 0; k < N; ++k) {
+    int p = k;
+    double best = std::fabs(A(k, k));
+    for (int i = k + 1; i < N; ++i)
+      if (std::fabs(A(i, i)) > best) best = std::fabs(A(i, i)), p = i;
+    if (p != k) {  // symmetric swap of rows and columns k <-> p
+      for (int j = 0; j < N; ++j) std::swap(A(k, j), A(p, j));
+      for (int i = 0; i < N; ++i) std::swap(A(i, k), A(i, p));
+      std::swap(perm[size_t(k)], perm[size_t(p)]);
+    }
+    // left-looking update of column k: L(k, j) for j < k sit in row k, D(j) on the diagonal
+    for (int j = 0; j < k; ++j) t[size_t(j)] = A(k, j) * A(j, j);
+    double d = A(k, k);
+    for (int j = 0; j < k; ++j) d -= A(k, j) * t[size_t(j)];
+    if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) throw NumericError("coarsest-level factorization failed");
+    A(k, k) = d;
+    for (int i = k + 1; i < N; ++i) {
+      double s = A(i, k);
+      for (int j = 0; j < k; ++j) s -= A(i, j) * t[size_t(j)];
+      A(i, k) = s / d;
+    }
+  }
+  // W = L^-1 (unit lower), column by column
+  std::vector<double> W(size_t(N) * N, 0.0);
   for (int j = 0; j < N; ++j) {
-    double d = a[size_t(j) * N + j];
-    for (int k = 0; k < j; ++k) d -= a[size_t(j) * N + k] * a[size_t(j) * N + k];
-    if (!(d > 0.0)) throw NumericError("coarsest-level factorization failed");
-    const double l = std::sqrt(d);
-    a[size_t(j) * N + j] = l;
+    W[size_t(j) * N + j] = 1.0;
     for (int i = j + 1; i < N; ++i) {
-      double s = a[size_t(i) * N + j];
-      for (int k = 0; k < j; ++k) s -= a[size_t(i) * N + k] * a[size_t(j) * N + k];
-      a[size_t(i) * N + j] = s / l;
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s -= A(i, k) * W[size_t(k) * N + j];
+      W[size_t(i) * N + j] = s;
     }
   }
-  std::vector<double> inv(size_t(N) * N, 0.0), col(static_cast<size_t>(N));
-  for (int c = 0; c < N; ++c) {
-    for (int i = 0; i < N; ++i) col[size_t(i)] = (i == c) ? 1.0 : 0.0;
-    for (int i = 0; i < N; ++i) {
-      double s = col[size_t(i)];
-      for (int k = 0; k < i; ++k) s -= a[size_t(i) * N + k] * col[size_t(k)];
-      col[size_t(i)] = s / a[size_t(i) * N + i];
+  // B = W^T D^-1 W (symmetric), scattered back through the permutation
+  std::vector<double> inv(size_t(N) * N, 0.0);
+  for (int i = 0; i < N; ++i)
+    for (int j = i; j < N; ++j) {
+      double s = 0.0;
+      for (int k = j; k < N; ++k) s += W[size_t(k) * N + i] * W[size_t(k) * N + j] / A(k, k);
+      inv[size_t(perm[size_t(i)]) * N + perm[size_t(j)]] = s;
+      inv[size_t(perm[size_t(j)]) * N + perm[size_t(i)]] = s;
     }
-    for (int i = N - 1; i >= 0; --i) {
-      double s = col[size_t(i)];
-      for (int k = i + 1; k < N; ++k) s -= a[size_t(k) * N + i] * col[size_t(k)];
-      col[size_t(i)] = s / a[size_t(i) * N + i];
-    }
-    for (int i = 0; i < N; ++i) inv[size_t(i) * N + c] = col[size_t(i)];
-  }
   return inv;
 }
 
@@ -345,6 +406,20 @@ void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-27
   density_set_ = true;
 }
 
+double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv) {
+  const long long N = 3 * nv;
+  double dsum = 0.0;
+  for (long long i = 0; i < N; ++i) dsum += a[size_t(i * N + i)];
+  const double op_scale = dsum / double(N);  // mean diagonal (src/multigrid.cpp:373)
+  if (knob("COARSE_PROJECT", 1) != 0) project_translations(a, nv);
+  std::vector<double> shifted = a;  // deflation shift (src/multigrid.cpp:374-379)
+  for (long long i = 0; i < nv; ++i)
+    for (long long j = 0; j < nv; ++j)
+      for (int c = 0; c < 3; ++c) shifted[size_t((3 * i + c) * N + 3 * j + c)] += op_scale / double(nv);
+  inv = ldlt_inverse(std::move(shifted), int(N));
+  return op_scale;
+}
+
 template <typename T>
 void Hierarchy<T>::factor_coarsest() {  // src/multigrid.cpp:368-383
   const int lc = num_levels() - 1;
@@ -362,16 +437,8 @@ void Hierarchy<T>::factor_coarsest() {  // src/multigrid.cpp:368-383
     IHOM_CUDA(cudaStreamSynchronize(s_));
     a = assemble_dense_stencil<T>(g, st);
   }
-  const int N = ndof_c_;
-  double dsum = 0.0;
-  for (int i = 0; i < N; ++i) dsum += a[size_t(i) * N + i];
-  op_scale_ = dsum / double(N);  // mean diagonal (src/multigrid.cpp:373)
-  std::vector<double> shifted = a;
-  const long long nv = g.nv;
-  for (long long i = 0; i < nv; ++i)
-    for (long long j = 0; j < nv; ++j)
-      for (int c = 0; c < 3; ++c) shifted[size_t((3 * i + c) * N + 3 * j + c)] += op_scale_ / double(nv);
-  const std::vector<double> inv = spd_inverse(shifted, N);
+  std::vector<double> inv;
+  op_scale_ = factor_coarse_dense(a, g.nv, inv);
   A_.alloc(a.size());
   Ainv_.alloc(inv.size());
   IHOM_CUDA(cudaMemcpyAsync(A_.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice, s_));

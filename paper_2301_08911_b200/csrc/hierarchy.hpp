@@ -33,6 +33,11 @@
 
 namespace ihomgpu {
 
+// Coarsest-level dense factorisation (src/multigrid.cpp:368-383): a (dof order 3*loc+c, raw
+// assembly in, projected operator out unless knob COARSE_PROJECT=0), explicit inverse of the
+// deflated matrix via pivoted LDL^T. Returns op_scale (mean diagonal of the raw operator).
+double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv);
+
 enum SolverMode { kVCycle = 0, kMixedDefect = 1, kPCG = 2 };
 
 struct SolverOptions {  // inc/multigrid.hpp:22-27

@@ -681,13 +681,13 @@ int ihom_init_trig(const int n[3], int basis_n, uint64_t seed, double volume, do
 int ihom_objective(int obj, double beta, double eta, double tau, double gamma, int iter, const double C[36],
                    double* value, double grad[36]) {
   return guarded([&] {
-    Expr e = obj == IHOM_OBJ_BULK    ? bulk_objective()
+    const Objective e = obj == IHOM_OBJ_BULK    ? bulk_objective()
              : obj == IHOM_OBJ_SHEAR ? shear_objective()
              : obj == IHOM_OBJ_NPR_RELAXED ? npr_relaxed(beta, iter)
              : obj == IHOM_OBJ_NPR_LOG     ? npr_log(eta, tau, gamma)
                                            : throw std::invalid_argument("unknown objective");
     *value = e.eval(C);
-    if (grad) e.backward(1.0, C, grad);
+    if (grad) e.grad(1.0, C, grad);
   });
 }
 
@@ -696,7 +696,7 @@ int ihom_objective(int obj, double beta, double eta, double tau, double gamma, i
 // ------------------------------------------------------------------ optimisation loop
 namespace {
 
-Expr make_objective(const ihom_run_config& c, int iter) {  // src/runner.cpp:13-21
+Objective make_objective(const ihom_run_config& c, int iter) {  // src/runner.cpp:13-21
   switch (c.obj) {
     case IHOM_OBJ_BULK: return bulk_objective();
     case IHOM_OBJ_SHEAR: return shear_objective();
@@ -856,7 +856,7 @@ struct Optimizer : OptBase {
     const CellSolveStats st = hom->solve_cell_problems();
     ihom_iter_record rec{};
     hom->effective_tensor(rec.C);
-    const Expr objective = make_objective(cfg, iter);
+    const Objective objective = make_objective(cfg, iter);
     const double fval = objective.eval(rec.C);
     rec.iter = iter;
     rec.objective = fval;
@@ -876,7 +876,7 @@ struct Optimizer : OptBase {
     }
     if (status == 0) {
       double seed[36];
-      objective.backward(1.0, rec.C, seed);
+      objective.grad(1.0, rec.C, seed);
       hom->tensor_sensitivity(seed, grad.p);
       pow_backward(pre.p, grad.p, cfg.penal, m, tmp.p, s);  // DensityExpr::backward
       slab.sync(s);

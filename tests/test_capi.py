@@ -73,3 +73,30 @@ def test_no_undefined_library_symbols():
         pytest.skip("library not built")
     out = subprocess.run(["nm", "-D", "--undefined-only", lib], capture_output=True, text=True).stdout
     assert "ihomgpu" not in out, out
+
+
+@pytest.mark.parametrize("obj", ["bulk", "shear", "npr-relaxed", "npr-log"])
+def test_objectives_bit_exact_with_oracle(ih, orc, obj):
+    """The product's closed-form objectives (csrc/objective.cpp) against the oracle's expression-DAG
+    restatement of src/objective.cpp:238-260: values and single-sided gradients bit for bit (host code,
+    no device needed)."""
+    rng = np.random.default_rng(11)
+    for it in range(6):
+        Cm = rng.uniform(0.1, 1.0, (6, 6))
+        Cm = Cm + Cm.T + 3.0 * np.eye(6)
+        v, g = orc.objective(obj, Cm, iter=it)
+        v2, g2 = ih.objective_native(obj, Cm, iter=it)
+        assert v == v2
+        assert np.array_equal(g, np.asarray(g2).reshape(6, 6))
+
+
+def test_objective_domain_errors(ih, orc):
+    """npr-log domain failures raise (the reference's EvalError, inc/objective.hpp:11-14) in both."""
+    Cm = np.eye(6)
+    Cm[0, 1] = Cm[1, 2] = Cm[2, 0] = -10.0  # 1 + eta*ring/normal < 0
+    with pytest.raises(Exception):
+        orc.objective("npr-log", Cm)
+    with pytest.raises(Exception):
+        ih.objective_native("npr-log", Cm)
+    with pytest.raises(Exception):
+        ih.objective_native("npr-log", np.zeros((6, 6)))

@@ -487,6 +487,20 @@ def _raise_last():
     raise RuntimeError(msg)
 
 
+def coarse_dense_solve(raw, f):
+    """Coarsest-level dense solve of an assembled operator (dof order 3*loc+c) on the device:
+    factor_coarsest + coarsest_solve (src/multigrid.cpp:368-451). Returns (x, rel) with rel the
+    relative residual against the operator the solve used. Raises on the singularity gate."""
+    raw = np.ascontiguousarray(raw, np.float64)
+    n = raw.shape[0]
+    f = np.ascontiguousarray(f, np.float64).ravel().copy()
+    x = np.zeros(n)
+    rel = C.c_double()
+    _check(lib().ihom_coarse_dense_solve(C.c_longlong(n // 3), raw.ctypes.data_as(_dp), f.ctypes.data_as(_dp),
+                                         x.ctypes.data_as(_dp), C.byref(rel)))
+    return x, rel.value
+
+
 # ---------------------------------------------------------------- design pipeline
 def grid_locs(n, neighbors=False):
     """Device-computed colour-block location of every vertex (x-fastest) [+ 27-neighbour table]."""

@@ -1573,7 +1573,7 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
   const Material& m = hier_.material();
   hier_.sync();  // the six fields of the slab above are final
   const long long nv = hier_.geo(0).nv;
-  const size_t esz = std::is_same_v<T, float> ? sizeof(float) : sizeof(double);
+  const size_t esz = energy_f32(std::is_same_v<T, float>) ? sizeof(float) : sizeof(double);
   void* ec = nullptr;
   if (knob("ENERGY_CACHE", 1)) {
     if (!ecache_.p && !ecache_skip_) {
@@ -1622,7 +1622,7 @@ void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  /
   hier_.sync();
   if (ecache_valid_) {  // energies of the current displacements from effective_tensor()
     const long long nv = hier_.geo(0).nv;
-    const bool f32 = std::is_same_v<T, float>;
+    const bool f32 = energy_f32(std::is_same_v<T, float>);
     ProfScope p(hier_.stream(), "sensitivity", double(nv) * (21.0 * (f32 ? 4.0 : 8.0) + 16.0));
     launch_sensitivity_cached(nv, ecache_.p, f32, rho_.p, penal_, seed_.p, out, hier_.stream(), hier_.global_nv(0));
   } else {

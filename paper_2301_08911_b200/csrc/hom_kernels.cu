@@ -331,6 +331,11 @@ __global__ void tensor_finalize(const double* partials, int nparts, double* out)
 
 static bool htensor() { return knob("HTENSOR", 1) != 0; }
 
+// Element energies of the mixed mode: the reference rounds u to f32 and forms d, K0 d and the dots in
+// f64 (src/homogenization.cpp:84-94, 132-140) -- TE = double here too. ENERGY_F32=1 selects the
+// all-f32 energy arithmetic (faster, not the reference's precision; off by default).
+bool energy_f32(bool snap) { return snap && knob("ENERGY_F32", 0) != 0; }
+
 static size_t grad_smem(bool f32) { return (f32 ? sizeof(float) : sizeof(double)) * 6 * kGradPerLoad * kHT; }
 
 static void set_smem(const void* fn, bool f32) {
@@ -348,14 +353,15 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
     uu.p[i] = u[i];
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
+  const bool te32 = energy_f32(snap);
   if (htensor()) {  // sum/difference-basis energies: no gradient scratch in shared memory
-    if (snap)
+    if (te32)
       tensor_kernel<TN, float, true><<<(unsigned)blocks, kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, partials,
                                                                       static_cast<float*>(ecache));
     else
       tensor_kernel<TN, double, true><<<(unsigned)blocks, kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, partials,
                                                                        static_cast<double*>(ecache));
-  } else if (snap) {
+  } else if (te32) {
     set_smem((const void*)tensor_kernel<TN, float, false>, true);
     tensor_kernel<TN, float, false><<<(unsigned)blocks, kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
                                                                                     partials,
@@ -438,14 +444,15 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
   const double inv_m = 1.0 / double(m_total > 0 ? m_total : g.nv);
+  const bool te32 = energy_f32(snap);
   if (htensor()) {
-    if (snap)
+    if (te32)
       sens_kernel<TN, float, true><<<ceil_div(g.nv, kHT), kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36,
                                                                        inv_m, out);
     else
       sens_kernel<TN, double, true><<<ceil_div(g.nv, kHT), kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36,
                                                                         inv_m, out);
-  } else if (snap) {
+  } else if (te32) {
     set_smem((const void*)sens_kernel<TN, float, false>, true);
     sens_kernel<TN, float, false><<<ceil_div(g.nv, kHT), kHT, grad_smem(true), s>>>(g, uu, rho, penal, snap, lam, mu,
                                                                                     sym_seed36, inv_m, out);

@@ -159,6 +159,8 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
                              const TN* const* uhi = nullptr, void* ecache = nullptr);
 // ecache: optional [21][nv] per-element energies written by the tensor pass (TE = f32 when snap_f32, else f64);
 // the sensitivity then reads them instead of recomputing (bit-identical).
+// true when the mixed-mode element energies run in f32 (knob ENERGY_F32; default: f64 like the reference)
+bool energy_f32(bool snap);
 void launch_sensitivity_cached(long long nv, const void* ecache, bool f32, const double* rho, double penal,
                                const double* sym_seed36, double* out, cudaStream_t s, long long m_total);
 // z-slab: uhi = the six fields of the slab above; m_total = elements of the whole grid (the 1/M factor)

@@ -2,6 +2,7 @@
 // assembly and the coarsest dense solve (src/multigrid.cpp:12-79, 102-239,
 // 281-333, 426-451).
 #include "kernels.hpp"
+#include "gal_gen.cuh"
 
 #include <cuda_pipeline.h>
 
@@ -1028,41 +1029,38 @@ __global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc
   for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, (unsigned)loc)] = TS(acc[e]);
 }
 
-// Even coarse grid: colour-fastest blocks (blockIdx.z = n + 27 (colour + 8 h2)); the
-// 27 fine-neighbour locations of 2 vc (fine colour 0, halved vc) are computed once
-// per thread with FastAddr and kept in shared memory.
+// Even coarse grid: one thread per (coarse vertex, 3x3 entry e), colour-fastest blocks
+// (blockIdx.z = e + 9 (colour + 8 h2)). The thread loads each of the 729 fine values
+// [K_{2vc+s}]_t (entry e) once, converts it once and scatters it into every coarse block delta it
+// feeds (gal_gen.cuh, tools/gen_galerkin.py): 729 loads + conversions and 2197 f64 FMAs instead of
+// 2197 of each; each accumulator still sees the reference's s-outer / t-inner term order.
 template <typename TS>
 __global__ void __launch_bounds__(128) gal_stencil_fast_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
                                                                ZLink<TS> sl, GridGeo gout, int zoff,
                                                                TS* __restrict__ stc) {
-  __shared__ unsigned fls[27][128];
-  const int n = blockIdx.z % 27;
-  const int rest = blockIdx.z / 27;
+  const int e = blockIdx.z % 9;
+  const int rest = blockIdx.z / 9;
   const int color = rest & 7, h2 = rest >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
   const int x = 2 * h0 + (color & 1), y = 2 * h1 + ((color >> 1) & 1), z = 2 * h2 + ((color >> 2) & 1);
   FastAddr fa;
-  fast_addr(gf, 0, x, y, z, fa);
-#pragma unroll
-  for (int s = 0; s < 27; ++s) fls[s][tid] = fa.A[0][s % 3] + fa.A[1][(s / 3) % 3] + fa.A[2][s / 9];
+  fast_addr(gf, 0, x, y, z, fa);  // fine vertex 2 vc: colour 0 at halved (x, y, z)
   const TS* lo = zbase(fa, stf, sl, 0);  // fine rows of the z-1 plane (fine colour 0: only that one wraps)
-  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int k1 = c_sg_start[n + 1];
-  for (int k = c_sg_start[n]; k < k1; ++k) {
-    const int st = c_sg_st[k];
-    const int sv = st & 31;
-    const unsigned fl = fls[sv][tid];
-    const double w = double(c_sg_w[k]);
-    const TS* b = (sv < 9 ? lo : stf) + st_index(9 * (st >> 5), fl);
+  const TS* pb[27];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) acc[e] += w * double(__ldg(b + 32 * e));
-  }
+  for (int s = 0; s < 27; ++s)
+    pb[s] = (s < 9 ? lo : stf) + st_index(e, fa.A[0][s % 3] + fa.A[1][(s / 3) % 3] + fa.A[2][s / 9]);
+  double A[27];
+#pragma unroll
+  for (int n = 0; n < 27; ++n) A[n] = 0.0;
+#define GAL_LD(S, K) double(__ldg(pb[S] + 32 * (K)))
+  GAL_TERMS(A)
+#undef GAL_LD
   const unsigned loc =
       (unsigned)(color * gout.size[0] + h0 + (long long)gout.cd[0][0] * (h1 + (long long)gout.cd[0][1] * (h2 + zoff)));
 #pragma unroll
-  for (int e = 0; e < 9; ++e) stc[st_index(9 * n + e, loc)] = TS(acc[e]);
+  for (int n = 0; n < 27; ++n) stc[st_index(9 * n + e, loc)] = TS(A[n]);
 }
 
 template <typename TS>
@@ -1071,7 +1069,7 @@ void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS
   upload_stencil_galerkin(s);
   if (gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0 && fast_ok(gf)) {
     const dim3 b = fast_block(gc);
-    const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 27 * 8 * gc.cd[0][2]);
+    const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 9 * 8 * gc.cd[0][2]);
     gal_stencil_fast_kernel<TS><<<gr, b, 0, s>>>(gf, gc, stf, resolve(sl, stf), gout ? *gout : gc, gout ? zoff : 0, stc);
   } else {
     if (!is_self(sl, stf) || gout) throw std::invalid_argument("z-slab Galerkin needs even grids");

@@ -1,0 +1,96 @@
+"""Coarsest-level solve on the operator that breaks the reference algorithm.
+
+tests/golden/coarse_fail_npr128.npz (tests/golden/make_coarse_fixture.py) is the 4^3 operator and load
+at which the reference's coarsest solve (src/multigrid.cpp:368-451: raw operator + translation shift,
+LDLT, <=3 refinements, 1e-3 singularity gate) throws on the npr-relaxed 128^3 workload: the f32 Galerkin
+stencils leave A t_c ~ 1e-7 op_scale and the design has floating-island modes ~1e-8 op_scale. With the
+documented deviation -- the operator projected onto the translation-free subspace -- the same
+factorisation solves it to ~1e-10.
+"""
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def fixture():
+    d = np.load(os.path.join(HERE, "golden", "coarse_fail_npr128.npz"))
+    return d["raw"], d["f"]
+
+
+def test_fixture_shape_and_spectrum(fixture):
+    raw, f = fixture
+    assert raw.shape == (192, 192) and f.shape == (192,)
+    op = np.diag(raw).mean()
+    assert np.abs(raw - raw.T).max() < 1e-14 * op
+    w = np.linalg.eigvalsh(0.5 * (raw + raw.T)) / op
+    # three translation modes leaked to O(1e-8) (f32 stencils), three floating-island modes ~1e-8
+    assert np.sum(np.abs(w) < 1e-6) == 6
+
+
+def test_reference_operator_fails_the_gate(orc, fixture):
+    raw, f = fixture
+    orc.set_coarse_project(False)
+    try:
+        _, rel = orc.coarse_dense_solve(raw, f)
+    finally:
+        orc.set_coarse_project(True)
+    assert rel > 1e-3  # src/multigrid.cpp:446-447 would throw
+
+
+def test_projected_operator_solves(orc, fixture):
+    raw, f = fixture
+    x, rel = orc.coarse_dense_solve(raw, f)
+    assert rel < 1e-9
+    # independent check with numpy: P A P x = P f, x translation-free
+    n = raw.shape[0]
+    T = np.zeros((n, 3))
+    for c in range(3):
+        T[c::3, c] = 1.0 / np.sqrt(n // 3)
+    P = np.eye(n) - T @ T.T
+    Ap = P @ raw @ P
+    fp = P @ f
+    assert np.linalg.norm(Ap @ x - fp) / np.linalg.norm(fp) < 1e-8
+    assert np.abs(T.T @ x).max() < 1e-12 * np.abs(x).max()
+
+
+@pytest.mark.gpu
+def test_device_coarsest_solves_the_failing_operator(ih, orc, fixture):
+    raw, f = fixture
+    x, rel = ih.coarse_dense_solve(raw, f)
+    assert rel < 1e-9
+    xo, _ = orc.coarse_dense_solve(raw, f)
+    # the near-null island modes amplify rounding by ~1e8; the solutions agree far below the solver tol
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) < 1e-5
+
+
+@pytest.mark.gpu
+def test_device_reference_operator_raises(ih, fixture):
+    raw, f = fixture
+    ih.set_knob("COARSE_PROJECT", 0)
+    try:
+        with pytest.raises(Exception, match="singular"):
+            ih.coarse_dense_solve(raw, f)
+    finally:
+        ih.set_knob("COARSE_PROJECT", 1)
+
+
+def test_small_spd_operator_matches_dense_solve(orc):
+    """On a well-conditioned operator the projection changes nothing: x solves A x = P f exactly."""
+    rng = np.random.default_rng(5)
+    nv = 8
+    n = 3 * nv
+    B = rng.normal(size=(n, n))
+    T = np.zeros((n, 3))
+    for c in range(3):
+        T[c::3, c] = 1.0 / np.sqrt(nv)
+    P = np.eye(n) - T @ T.T
+    A = P @ (B @ B.T + n * np.eye(n)) @ P  # SPD on the complement, translations exactly null
+    f = rng.normal(size=n)
+    x, rel = orc.coarse_dense_solve(A, f)
+    assert rel < 1e-12
+    xr = np.linalg.lstsq(A, P @ f, rcond=None)[0]
+    assert np.allclose(x, P @ xr, rtol=1e-10, atol=1e-12)

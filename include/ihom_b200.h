@@ -141,6 +141,11 @@ long long ihom_kernel_launches(ihom_ctx* ctx);
    neighbour locations of every location (inc/grid.hpp:73-92, src/fem.cpp:37-68). Host outputs. */
 int ihom_grid_locs(const int n[3], long long* locs, long long* nbr27);
 
+/* restrict_residual_field (dir 0: out[coarse] = R in[fine]) / prolong_add_field (dir 1: out[fine] += P in[coarse])
+   (inc/multigrid.hpp:13-20, src/multigrid.cpp:19-79) on the even fine grid nf; AoS host buffers in
+   colour-block order; f32 != 0 runs the f32 inner-cycle transfer kernels (TRANSFER_F32), else f64. */
+int ihom_transfer(const int nf[3], int dir, int f32, const double* in, double* out);
+
 /* ---- density pipeline (inc/density.hpp:36-69, inc/oc.hpp:27-33) ---- */
 int ihom_radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, int where);
 /* DensityExpr: radius < 1 (or < 0) means pow only. eval: phys = filter(design)^p, keeps pre in pre_out (may be null).

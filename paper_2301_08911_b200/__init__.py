@@ -487,6 +487,19 @@ def _raise_last():
     raise RuntimeError(msg)
 
 
+def transfer(n, x, direction="restrict", f32=False, out=None):
+    """restrict_residual_field / prolong_add_field (src/multigrid.cpp:19-79) on the device. restrict:
+    returns R x (coarse, AoS). prolong: returns out + P x (fine, AoS; out defaults to zeros)."""
+    nf = _n3(n)
+    nvf = int(np.prod(nf))
+    nvc = nvf // 8
+    x = np.ascontiguousarray(x, np.float64).ravel()
+    d = 0 if direction == "restrict" else 1
+    o = np.zeros(3 * (nvc if d == 0 else nvf)) if out is None else np.array(out, np.float64).ravel()
+    _check(lib().ihom_transfer((C.c_int * 3)(*nf), d, int(bool(f32)), x.ctypes.data_as(_dp), o.ctypes.data_as(_dp)))
+    return o.reshape(-1, 3)
+
+
 def coarse_dense_solve(raw, f):
     """Coarsest-level dense solve of an assembled operator (dof order 3*loc+c) on the device:
     factor_coarsest + coarsest_solve (src/multigrid.cpp:368-451). Returns (x, rel) with rel the

@@ -557,6 +557,37 @@ int ihom_grid_locs(const int n[3], long long* locs, long long* nbr27) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+template <typename TN>
+void transfer_typed(const GridGeo& gf, const GridGeo& gc, int dir, const double* in, double* out, cudaStream_t s) {
+  const long long nf = 3 * gf.nv, nc = 3 * gc.nv;
+  const long long nin = dir == 0 ? nf : nc, nout = dir == 0 ? nc : nf;
+  std::vector<TN> hin(in, in + nin), hout(out, out + nout);
+  DevBuf<TN> din(static_cast<size_t>(nin)), dout(static_cast<size_t>(nout));
+  IHOM_CUDA(cudaMemcpyAsync(din.p, hin.data(), sizeof(TN) * nin, cudaMemcpyHostToDevice, s));
+  IHOM_CUDA(cudaMemcpyAsync(dout.p, hout.data(), sizeof(TN) * nout, cudaMemcpyHostToDevice, s));
+  if (dir == 0) launch_restrict<TN>(gf, gc, din.p, dout.p, s);
+  else launch_prolong_add<TN>(gc, gf, din.p, dout.p, s);
+  IHOM_CUDA(cudaMemcpyAsync(hout.data(), dout.p, sizeof(TN) * nout, cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  for (long long i = 0; i < nout; ++i) out[i] = double(hout[size_t(i)]);
+}
+}  // namespace
+
+extern "C" {
+
+int ihom_transfer(const int nf[3], int dir, int f32, const double* in, double* out) {
+  return guarded([&] {
+    if (nf[0] % 2 || nf[1] % 2 || nf[2] % 2) throw std::invalid_argument("transfer needs an even fine grid");
+    if (dir != 0 && dir != 1) throw std::invalid_argument("transfer direction must be 0 (restrict) or 1 (prolong)");
+    const GridGeo gf = make_geo(nf[0], nf[1], nf[2]), gc = make_geo(nf[0] / 2, nf[1] / 2, nf[2] / 2);
+    if (f32) transfer_typed<float>(gf, gc, dir, in, out, lib_stream());
+    else transfer_typed<double>(gf, gc, dir, in, out, lib_stream());
+  });
+}
+
 // ------------------------------------------------------------------ design pipeline
 int ihom_radial_filter(const int n[3], const double* f, double radius, int kernel, double* out, int where) {
   return guarded([&] {

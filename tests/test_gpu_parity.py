@@ -128,15 +128,30 @@ def test_coarse_operator_annihilates_constants(ih):
         assert np.linalg.norm(y) < 1e-9 * np.linalg.norm(c) * max(1.0, H.op_scale())
 
 
-def test_transfer_restrict_prolong(ih, orc):
-    # via the hierarchy: restrict r0 -> f1 during a v-cycle is internal; check adjointness through apply
-    n = 8
-    hom = make_hom(ih, n, "double")
-    hom.set_density(np.ones(n ** 3))
-    # prolongation reproduces constants: coarse-grid correction of a constant is a constant
-    fine = mt_uniform(3 * 512, 101, -1, 1)
-    coarse = orc.restrict(n, fine)
-    assert coarse.shape == (64, 3)
+@pytest.mark.parametrize("n", [8, (10, 8, 12), 32])
+@pytest.mark.parametrize("f32", [False, True])
+def test_transfer_restrict_prolong(ih, orc, n, f32):
+    """Device restrict / prolong-add (f64 and the f32 inner-cycle kernels) against the oracle's
+    restrict_residual_field / prolong_add_field (src/multigrid.cpp:19-79)."""
+    nf = (n, n, n) if isinstance(n, int) else n
+    nvf = int(np.prod(nf))
+    fine = mt_uniform(3 * nvf, 101, -1, 1)
+    coarse = mt_uniform(3 * nvf // 8, 103, -1, 1)
+    base = mt_uniform(3 * nvf, 107, -1, 1)
+    if f32:  # the f32 kernels see f32-rounded inputs; powers-of-two weights, f32 sums
+        fine, coarse, base = (a.astype(np.float32).astype(np.float64) for a in (fine, coarse, base))
+    tol = 1e-6 if f32 else 1e-15
+    r = ih.transfer(nf, fine, "restrict", f32=f32)
+    ro = orc.restrict(nf, fine)
+    assert rel(r, ro) < tol
+    p = ih.transfer(nf, coarse, "prolong", f32=f32, out=base)
+    po = orc.prolong_add(nf, coarse, base)
+    assert rel(p, po) < tol
+    # adjointness R = P^T (tests/test_multigrid.cpp:59-72) on the device kernels
+    if not f32:
+        lhs = float(np.dot(ih.transfer(nf, fine, "restrict").ravel(), coarse))
+        rhs = float(np.dot(fine, ih.transfer(nf, coarse, "prolong").ravel()))
+        assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
 
 
 # ---------------------------------------------------------------- V-cycle / solve

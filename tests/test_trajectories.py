@@ -47,7 +47,7 @@ def test_gpu_trajectory_matches_oracle(ih, name, mode):
         Cg, Co = np.asarray(r["C"]), g["C"][k]
         assert np.abs(Cg - Co).max() <= 1e-4 * np.abs(Co).max(), (k, np.abs(Cg - Co).max() / np.abs(Co).max())
         assert abs(r["objective"] - g["objective"][k]) <= 1e-4 * abs(g["objective"][k]), k
-        assert abs(r["volume"] - g["volume"][k]) <= 1e-6
+        assert abs(r["volume"] - g["volume"][k]) <= 2e-6 + 1e-12  # both within the OC stop rule 1e-6 of V
     stride = int(g["stride"])
     assert np.abs(rep.density[::stride] - g["rho_sample"]).max() <= 1e-3
     assert abs(rep.density.mean() - float(g["rho_mean"])) <= 1e-6

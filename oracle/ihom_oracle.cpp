@@ -696,7 +696,13 @@ struct CoarseSolver {
   i64 nv = 0;
   double op_scale = 0.0;
   std::vector<double> raw, cmat;
+  std::vector<std::vector<double>> nulls;  // deflated near-null directions (orthonormal, translation-free)
   DenseLDLT ldlt;
+  // The deviation (g_coarse_project) also deflates near-null modes beyond the translations: trailing
+  // pivots of the diagonal-pivoted LDL^T below 1e-6 op_scale (floating islands of the design, ~1e-8 op_scale:
+  // under the f32 stencils' resolution, so their amplified solution components are rounding noise) give
+  // directions v = Pm^T L^-T e_k; orthonormalised against the translations they are projected off the
+  // operator and the load and shifted like the translations.
   void factor(std::vector<double> a, i64 nverts) {
     nv = nverts;
     const i64 N = 3 * nv;
@@ -704,12 +710,73 @@ struct CoarseSolver {
     double dsum = 0.0;
     for (i64 i = 0; i < N; ++i) dsum += a[size_t(i * N + i)];
     op_scale = dsum / double(N);  // :373
-    if (g_coarse_project) project_translations(a, nv);
+    nulls.clear();
+    auto shifted = [&](const std::vector<double>& m) {  // :374-379 deflation shift (+ near-null modes)
+      std::vector<double> b = m;
+      for (i64 i = 0; i < nv; ++i)
+        for (i64 j = 0; j < nv; ++j)
+          for (int c = 0; c < 3; ++c) b[size_t((3 * i + c) * N + 3 * j + c)] += op_scale / double(nv);
+      for (const auto& q : nulls)
+        for (i64 i = 0; i < N; ++i)
+          for (i64 j = 0; j < N; ++j) b[size_t(i * N + j)] += op_scale * q[size_t(i)] * q[size_t(j)];
+      return b;
+    };
+    if (g_coarse_project) {
+      project_translations(a, nv);
+      DenseLDLT probe;
+      probe.compute(shifted(a), int(N));
+      for (int k = 0; k < int(N); ++k) {
+        if (!(std::fabs(probe.L[size_t(k) * N + k]) < 1e-6 * op_scale)) continue;
+        std::vector<double> y(static_cast<size_t>(N), 0.0);  // L^T y = e_k
+        y[size_t(k)] = 1.0;
+        for (int i = k - 1; i >= 0; --i)
+          for (int j = i + 1; j <= k; ++j) y[size_t(i)] -= probe.L[size_t(j) * N + i] * y[size_t(j)];
+        std::vector<double> v(static_cast<size_t>(N));
+        for (i64 i = 0; i < N; ++i) v[size_t(probe.perm[size_t(i)])] = y[size_t(i)];
+        for (int rep = 0; rep < 2; ++rep) {
+          for (int c = 0; c < 3; ++c) {
+            double m = 0.0;
+            for (i64 i = 0; i < nv; ++i) m += v[size_t(3 * i + c)];
+            for (i64 i = 0; i < nv; ++i) v[size_t(3 * i + c)] -= m / double(nv);
+          }
+          for (const auto& q : nulls) {
+            double d = 0.0;
+            for (i64 i = 0; i < N; ++i) d += q[size_t(i)] * v[size_t(i)];
+            for (i64 i = 0; i < N; ++i) v[size_t(i)] -= d * q[size_t(i)];
+          }
+        }
+        double nn = 0.0;
+        for (double t : v) nn += t * t;
+        if (!(nn > 0.0)) continue;
+        for (double& t : v) t /= std::sqrt(nn);
+        nulls.push_back(std::move(v));
+      }
+      for (const auto& q : nulls) {  // a <- (I - q q^T) a (I - q q^T)
+        std::vector<double> aq(size_t(N), 0.0);
+        for (i64 i = 0; i < N; ++i)
+          for (i64 j = 0; j < N; ++j) aq[size_t(i)] += a[size_t(i * N + j)] * q[size_t(j)];
+        double qaq = 0.0;
+        for (i64 i = 0; i < N; ++i) qaq += q[size_t(i)] * aq[size_t(i)];
+        for (i64 i = 0; i < N; ++i)
+          for (i64 j = 0; j < N; ++j)
+            a[size_t(i * N + j)] += qaq * q[size_t(i)] * q[size_t(j)] - aq[size_t(i)] * q[size_t(j)] - q[size_t(i)] * aq[size_t(j)];
+      }
+      if (!nulls.empty())
+        for (i64 i = 0; i < N; ++i)
+          for (i64 j = 0; j < i; ++j) {
+            const double t = 0.5 * (a[size_t(i * N + j)] + a[size_t(j * N + i)]);
+            a[size_t(i * N + j)] = a[size_t(j * N + i)] = t;
+          }
+    }
     cmat = a;
-    for (i64 i = 0; i < nv; ++i)  // :374-379 deflation shift
-      for (i64 j = 0; j < nv; ++j)
-        for (int c = 0; c < 3; ++c) a[size_t((3 * i + c) * N + 3 * j + c)] += op_scale / double(nv);
-    ldlt.compute(std::move(a), int(N));
+    ldlt.compute(shifted(a), int(N));
+  }
+  void project_load(std::vector<double>& fv) const {  // f -= q (q . f) over the deflated modes
+    for (const auto& q : nulls) {
+      double d = 0.0;
+      for (size_t i = 0; i < fv.size(); ++i) d += q[i] * fv[i];
+      for (size_t i = 0; i < fv.size(); ++i) fv[i] -= d * q[i];
+    }
   }
   std::vector<double> mul(const std::vector<double>& x) const {
     const size_t N = x.size();
@@ -811,6 +878,7 @@ class Hierarchy {  // inc/multigrid.hpp:53-93, src/multigrid.cpp:245-501
   void coarsest_solve() {  // :426-451
     Level<T>& lev = levels_.back();
     remove_translations(lev.f);
+    coarse_.project_load(lev.f.a);
     const std::vector<double>& fv = lev.f.a;
     double fn = 0.0;
     for (double x : fv) fn += x * x;
@@ -1595,6 +1663,7 @@ int orc_coarse_dense_solve(long long nv, const double* raw, const double* f, dou
       m /= double(nv);
       for (i64 i = 0; i < nv; ++i) fv[size_t(3 * i + c)] -= m;
     }
+    cs.project_load(fv);
     double fn = 0.0;
     for (double v : fv) fn += v * v;
     fn = std::sqrt(fn);

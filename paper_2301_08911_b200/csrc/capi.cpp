@@ -422,11 +422,12 @@ int ihom_coarse_dense_solve(long long nv, const double* raw, const double* f, do
   return guarded([&] {
     if (nv <= 0 || !raw || !f || !x) throw std::invalid_argument("coarse_dense_solve: null or empty input");
     const long long N = 3 * nv;
-    std::vector<double> a(raw, raw + N * N), inv;
-    const double op_scale = factor_coarse_dense(a, nv, inv);
+    std::vector<double> a(raw, raw + N * N), inv, q;
+    int nq = 0;
+    const double op_scale = factor_coarse_dense(a, nv, inv, &q, &nq);
     cudaStream_t s = nullptr;
     IHOM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    DevBuf<double> dA, dInv, df, du, work;
+    DevBuf<double> dA, dInv, df, du, work, dQ;
     DevBuf<int> err;
     dA.alloc(a.size());
     dInv.alloc(inv.size());
@@ -438,8 +439,12 @@ int ihom_coarse_dense_solve(long long nv, const double* raw, const double* f, do
     IHOM_CUDA(cudaMemcpyAsync(dInv.p, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, s));
     IHOM_CUDA(cudaMemcpyAsync(df.p, f, sizeof(double) * size_t(N), cudaMemcpyHostToDevice, s));
     IHOM_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
-    launch_coarsest_solve<double>(int(N), nv, dInv.p, dA.p, df.p, du.p, 1e-12 * op_scale * std::sqrt(double(N)),
-                                  work.p, err.p, s);
+    if (nq > 0) {
+      dQ.alloc(q.size());
+      IHOM_CUDA(cudaMemcpyAsync(dQ.p, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice, s));
+    }
+    launch_coarsest_solve<double>(int(N), nv, dInv.p, dA.p, dQ.p, nq, df.p, du.p,
+                                  1e-12 * op_scale * std::sqrt(double(N)), work.p, err.p, s);
     int e = 0;
     std::vector<double> fp(static_cast<size_t>(N));
     IHOM_CUDA(cudaMemcpyAsync(x, du.p, sizeof(double) * size_t(N), cudaMemcpyDeviceToHost, s));

@@ -97,57 +97,100 @@ void project_translations(std::vector<double>& a, long long nv) {
 }
 
 // Symmetric LDL^T with diagonal pivoting (the algorithm of Eigen::LDLT, which the reference
-// uses at src/multigrid.cpp:380: at step k the largest remaining |diagonal| is swapped in), then
-// the explicit inverse A^-1 = Pm^T L^-T D^-1 L^-1 Pm for the device matvecs. Unlike a Cholesky it
-// tolerates the slightly indefinite near-null modes f32 stencils can produce; it fails only on
+// uses at src/multigrid.cpp:380: at step k the largest remaining |diagonal| is swapped in). Unlike a
+// Cholesky it tolerates the slightly indefinite near-null modes f32 stencils produce; it fails only on
 // an exactly zero or non-finite pivot (Eigen's NumericalIssue).
-std::vector<double> ldlt_inverse(std::vector<double> a, int N) {
-  std::vector<int> perm(static_cast<size_t>(N));
-  for (int i = 0; i < N; ++i) perm[size_t(i)] = i;
-  auto A = [&](int i, int j) -> double& { return a[size_t(i) * N + j]; };
-  std::vector<double> t(static_cast<size_t>(N));
-  for (int k = 0; k < N; ++k) {
-    int p = k;
-    double best = std::fabs(A(k, k));
-    for (int i = k + 1; i < N; ++i)
-      if (std::fabs(A(i, i)) > best) best = std::fabs(A(i, i)), p = i;
-    if (p != k) {  // symmetric swap of rows and columns k <-> p
-      for (int j = 0; j < N; ++j) std::swap(A(k, j), A(p, j));
-      for (int i = 0; i < N; ++i) std::swap(A(i, k), A(i, p));
-      std::swap(perm[size_t(k)], perm[size_t(p)]);
-    }
-    // left-looking update of column k: L(k, j) for j < k sit in row k, D(j) on the diagonal
-    for (int j = 0; j < k; ++j) t[size_t(j)] = A(k, j) * A(j, j);
-    double d = A(k, k);
-    for (int j = 0; j < k; ++j) d -= A(k, j) * t[size_t(j)];
-    if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) throw NumericError("coarsest-level factorization failed");
-    A(k, k) = d;
-    for (int i = k + 1; i < N; ++i) {
-      double s = A(i, k);
-      for (int j = 0; j < k; ++j) s -= A(i, j) * t[size_t(j)];
-      A(i, k) = s / d;
-    }
-  }
-  // W = L^-1 (unit lower), column by column
-  std::vector<double> W(size_t(N) * N, 0.0);
-  for (int j = 0; j < N; ++j) {
-    W[size_t(j) * N + j] = 1.0;
-    for (int i = j + 1; i < N; ++i) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s -= A(i, k) * W[size_t(k) * N + j];
-      W[size_t(i) * N + j] = s;
+struct Ldlt {
+  int n = 0;
+  std::vector<double> a;  // unit L below the diagonal, D on it (permuted order)
+  std::vector<int> perm;  // position -> original index
+  void factor(std::vector<double> m, int N) {
+    n = N;
+    a = std::move(m);
+    perm.resize(size_t(n));
+    for (int i = 0; i < n; ++i) perm[size_t(i)] = i;
+    auto A = [&](int i, int j) -> double& { return a[size_t(i) * n + j]; };
+    std::vector<double> t(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+      int p = k;
+      double best = std::fabs(A(k, k));
+      for (int i = k + 1; i < n; ++i)
+        if (std::fabs(A(i, i)) > best) best = std::fabs(A(i, i)), p = i;
+      if (p != k) {  // symmetric swap of rows and columns k <-> p
+        for (int j = 0; j < n; ++j) std::swap(A(k, j), A(p, j));
+        for (int i = 0; i < n; ++i) std::swap(A(i, k), A(i, p));
+        std::swap(perm[size_t(k)], perm[size_t(p)]);
+      }
+      for (int j = 0; j < k; ++j) t[size_t(j)] = A(k, j) * A(j, j);  // left-looking column k
+      double d = A(k, k);
+      for (int j = 0; j < k; ++j) d -= A(k, j) * t[size_t(j)];
+      if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) throw NumericError("coarsest-level factorization failed");
+      A(k, k) = d;
+      for (int i = k + 1; i < n; ++i) {
+        double s = A(i, k);
+        for (int j = 0; j < k; ++j) s -= A(i, j) * t[size_t(j)];
+        A(i, k) = s / d;
+      }
     }
   }
-  // B = W^T D^-1 W (symmetric), scattered back through the permutation
-  std::vector<double> inv(size_t(N) * N, 0.0);
-  for (int i = 0; i < N; ++i)
-    for (int j = i; j < N; ++j) {
+  double pivot(int k) const { return a[size_t(k) * n + k]; }
+  // Pm^T L^-T e_k: the near-null direction of a tiny trailing pivot k (diagonal pivoting is rank-revealing)
+  std::vector<double> null_direction(int k) const {
+    std::vector<double> y(static_cast<size_t>(n), 0.0), v(static_cast<size_t>(n));
+    y[size_t(k)] = 1.0;
+    for (int i = k - 1; i >= 0; --i) {
       double s = 0.0;
-      for (int k = j; k < N; ++k) s += W[size_t(k) * N + i] * W[size_t(k) * N + j] / A(k, k);
-      inv[size_t(perm[size_t(i)]) * N + perm[size_t(j)]] = s;
-      inv[size_t(perm[size_t(j)]) * N + perm[size_t(i)]] = s;
+      for (int j = i + 1; j <= k; ++j) s -= a[size_t(j) * n + i] * y[size_t(j)];
+      y[size_t(i)] = s;
     }
-  return inv;
+    for (int i = 0; i < n; ++i) v[size_t(perm[size_t(i)])] = y[size_t(i)];
+    return v;
+  }
+  // explicit inverse A^-1 = Pm^T L^-T D^-1 L^-1 Pm (for the device matvecs)
+  std::vector<double> inverse() const {
+    std::vector<double> W(size_t(n) * n, 0.0);  // W = L^-1 (unit lower), column by column
+    for (int j = 0; j < n; ++j) {
+      W[size_t(j) * n + j] = 1.0;
+      for (int i = j + 1; i < n; ++i) {
+        double s = 0.0;
+        for (int k = j; k < i; ++k) s -= a[size_t(i) * n + k] * W[size_t(k) * n + j];
+        W[size_t(i) * n + j] = s;
+      }
+    }
+    std::vector<double> inv(size_t(n) * n, 0.0);  // W^T D^-1 W, scattered through the permutation
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j) {
+        double s = 0.0;
+        for (int k = j; k < n; ++k) s += W[size_t(k) * n + i] * W[size_t(k) * n + j] / pivot(k);
+        inv[size_t(perm[size_t(i)]) * n + perm[size_t(j)]] = s;
+        inv[size_t(perm[size_t(j)]) * n + perm[size_t(i)]] = s;
+      }
+    return inv;
+  }
+};
+
+// a <- (I - Q Q^T) a (I - Q Q^T) for orthonormal columns q (each length N), symmetrised.
+void project_out(std::vector<double>& a, const std::vector<std::vector<double>>& Q, long long N) {
+  for (const auto& q : Q) {
+    std::vector<double> aq(size_t(N), 0.0);  // a q
+    for (long long i = 0; i < N; ++i) {
+      double s = 0.0;
+      for (long long j = 0; j < N; ++j) s += a[size_t(i * N + j)] * q[size_t(j)];
+      aq[size_t(i)] = s;
+    }
+    double qaq = 0.0;
+    for (long long i = 0; i < N; ++i) qaq += q[size_t(i)] * aq[size_t(i)];
+    // (I - qq^T) a (I - qq^T) = a - aq q^T - q (aq)^T + (q^T a q) q q^T
+    for (long long i = 0; i < N; ++i)
+      for (long long j = 0; j < N; ++j)
+        a[size_t(i * N + j)] += -aq[size_t(i)] * q[size_t(j)] - q[size_t(i)] * aq[size_t(j)] +
+                                qaq * q[size_t(i)] * q[size_t(j)];
+  }
+  for (long long i = 0; i < N; ++i)
+    for (long long j = i + 1; j < N; ++j) {
+      const double v = 0.5 * (a[size_t(i * N + j)] + a[size_t(j * N + i)]);
+      a[size_t(i * N + j)] = a[size_t(j * N + i)] = v;
+    }
 }
 
 // Algorithmic bytes, sN = nodal bytes, sC = coefficient/stencil bytes.
@@ -406,17 +449,69 @@ void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-27
   density_set_ = true;
 }
 
-double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv) {
+double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv, std::vector<double>* qout,
+                           int* mout) {
   const long long N = 3 * nv;
   double dsum = 0.0;
   for (long long i = 0; i < N; ++i) dsum += a[size_t(i * N + i)];
   const double op_scale = dsum / double(N);  // mean diagonal (src/multigrid.cpp:373)
-  if (knob("COARSE_PROJECT", 1) != 0) project_translations(a, nv);
-  std::vector<double> shifted = a;  // deflation shift (src/multigrid.cpp:374-379)
-  for (long long i = 0; i < nv; ++i)
-    for (long long j = 0; j < nv; ++j)
-      for (int c = 0; c < 3; ++c) shifted[size_t((3 * i + c) * N + 3 * j + c)] += op_scale / double(nv);
-  inv = ldlt_inverse(std::move(shifted), int(N));
+  const double shift = op_scale / double(nv);  // deflation shift (src/multigrid.cpp:374-379)
+  auto shifted = [&](const std::vector<std::vector<double>>& Q) {
+    std::vector<double> b = a;
+    for (long long i = 0; i < nv; ++i)
+      for (long long j = 0; j < nv; ++j)
+        for (int c = 0; c < 3; ++c) b[size_t((3 * i + c) * N + 3 * j + c)] += shift;
+    for (const auto& q : Q)
+      for (long long i = 0; i < N; ++i)
+        for (long long j = 0; j < N; ++j) b[size_t(i * N + j)] += op_scale * q[size_t(i)] * q[size_t(j)];
+    return b;
+  };
+  std::vector<std::vector<double>> Q;
+  Ldlt f;
+  if (knob("COARSE_PROJECT", 1) != 0) {
+    project_translations(a, nv);
+    // Near-null modes beyond the translations (floating islands of the design: modes ~1e-8 op_scale,
+    // below the f32 stencils' resolution) are deflated like the translations: trailing pivots of the
+    // pivoted LDL^T below kNearNull op_scale give their directions, orthonormalised against the
+    // translations; the operator is projected off them and shifted on them, the load projected.
+    constexpr double kNearNull = 1e-6;
+    f.factor(shifted(Q), int(N));
+    for (int k = 0; k < int(N); ++k)
+      if (std::fabs(f.pivot(k)) < kNearNull * op_scale) {
+        std::vector<double> v = f.null_direction(k);
+        for (int pass = 0; pass < 2; ++pass) {  // twice-iterated Gram-Schmidt
+          for (int c = 0; c < 3; ++c) {
+            double m = 0.0;
+            for (long long i = 0; i < nv; ++i) m += v[size_t(3 * i + c)];
+            m /= double(nv);
+            for (long long i = 0; i < nv; ++i) v[size_t(3 * i + c)] -= m;
+          }
+          for (const auto& q : Q) {
+            double d = 0.0;
+            for (long long i = 0; i < N; ++i) d += q[size_t(i)] * v[size_t(i)];
+            for (long long i = 0; i < N; ++i) v[size_t(i)] -= d * q[size_t(i)];
+          }
+        }
+        double nrm = 0.0;
+        for (double x : v) nrm += x * x;
+        nrm = std::sqrt(nrm);
+        if (!(nrm > 0.0)) continue;
+        for (double& x : v) x /= nrm;
+        Q.push_back(std::move(v));
+      }
+    if (!Q.empty()) {
+      project_out(a, Q, N);
+      f.factor(shifted(Q), int(N));
+    }
+  } else {
+    f.factor(shifted(Q), int(N));
+  }
+  inv = f.inverse();
+  if (qout) {
+    qout->clear();
+    for (const auto& q : Q) qout->insert(qout->end(), q.begin(), q.end());
+  }
+  if (mout) *mout = int(Q.size());
   return op_scale;
 }
 
@@ -437,12 +532,16 @@ void Hierarchy<T>::factor_coarsest() {  // src/multigrid.cpp:368-383
     IHOM_CUDA(cudaStreamSynchronize(s_));
     a = assemble_dense_stencil<T>(g, st);
   }
-  std::vector<double> inv;
-  op_scale_ = factor_coarse_dense(a, g.nv, inv);
+  std::vector<double> inv, q;
+  op_scale_ = factor_coarse_dense(a, g.nv, inv, &q, &nnull_);
   A_.alloc(a.size());
   Ainv_.alloc(inv.size());
   IHOM_CUDA(cudaMemcpyAsync(A_.p, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice, s_));
   IHOM_CUDA(cudaMemcpyAsync(Ainv_.p, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, s_));
+  if (nnull_ > 0) {
+    if (Q_.n < q.size()) Q_.alloc(q.size());
+    IHOM_CUDA(cudaMemcpyAsync(Q_.p, q.data(), sizeof(double) * q.size(), cudaMemcpyHostToDevice, s_));
+  }
   IHOM_CUDA(cudaStreamSynchronize(s_));
 }
 
@@ -601,7 +700,7 @@ void Hierarchy<T>::coarsest_solve() {  // src/multigrid.cpp:426-451
   const int lc = num_levels() - 1;
   Level& L = levels_[size_t(lc)];
   ProfScope p(s_, "coarsest", 0.0);
-  launch_coarsest_solve<double>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.f.p, level_u(lc), negligible_load(ndof_c_),
+  launch_coarsest_solve<double>(ndof_c_, L.g.nv, Ainv_.p, A_.p, Q_.p, nnull_, L.f.p, level_u(lc), negligible_load(ndof_c_),
                                 cwork_.p, err_.p, s_);
   ++launches_;
 }
@@ -732,7 +831,7 @@ void Hierarchy<T>::coarsest_f32() {
   const int lc = num_levels() - 1;
   Level& L = levels_[size_t(lc)];
   ProfScope p(s_, "coarsest", 0.0);
-  launch_coarsest_solve<float>(ndof_c_, L.g.nv, Ainv_.p, A_.p, L.ef.p, L.eu.p, 0.0, cwork_.p, err_.p, s_);
+  launch_coarsest_solve<float>(ndof_c_, L.g.nv, Ainv_.p, A_.p, Q_.p, nnull_, L.ef.p, L.eu.p, 0.0, cwork_.p, err_.p, s_);
   ++launches_;
 }
 

@@ -36,7 +36,10 @@ namespace ihomgpu {
 // Coarsest-level dense factorisation (src/multigrid.cpp:368-383): a (dof order 3*loc+c, raw
 // assembly in, projected operator out unless knob COARSE_PROJECT=0), explicit inverse of the
 // deflated matrix via pivoted LDL^T. Returns op_scale (mean diagonal of the raw operator).
-double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv);
+// Near-null modes beyond the translations (|pivot| < 1e-6 op_scale) are deflated too: their orthonormal
+// directions go to *q ([m][3nv]) and *m; the device solve projects the load off them.
+double factor_coarse_dense(std::vector<double>& a, long long nv, std::vector<double>& inv,
+                           std::vector<double>* q = nullptr, int* m = nullptr);
 
 enum SolverMode { kVCycle = 0, kMixedDefect = 1, kPCG = 2 };
 
@@ -238,7 +241,8 @@ class Hierarchy {
   ZLink<double> u0l_{};     // links of the bound level-0 u
   std::vector<Level> levels_;
   DevBuf<T> coeff_;
-  DevBuf<double> Ainv_, A_, cwork_;
+  DevBuf<double> Ainv_, A_, cwork_, Q_;
+  int nnull_ = 0;  // deflated near-null modes of the coarsest operator (rows of Q_)
   int ndof_c_ = 0;
   double op_scale_ = 0.0;
   bool density_set_ = false;

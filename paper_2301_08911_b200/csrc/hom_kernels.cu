@@ -12,6 +12,7 @@
 // Mixed mode reads u through a float snapshot (src/homogenization.cpp:84-85).
 #include "kernels.hpp"
 #include "hada_gen.cuh"
+#include "bulk.cuh"
 
 namespace ihomgpu {
 
@@ -148,6 +149,7 @@ __device__ void element_energies(const GridGeo& g, int ex, int ey, int ez, const
 // Per element: 18 butterflies of 24 adds, 6 x 45 terms for W d_hat_j, 21 x 21-term dots (~1.2k flop,
 // no shared memory) instead of the quadrature's ~2.7k flop and 864 B of gradients per thread.
 // The all-sum entries (sigma = 0) drop out (W annihilates translations).
+void upload_modal_tables(const double h[], cudaStream_t s);
 __constant__ double c_hw_d[kHadaClasses];
 __constant__ float c_hw_f[kHadaClasses];
 __constant__ double c_chih_d[6][24];  // Hb chi^i, chi^i element-relative (src/material.cpp:71-82)
@@ -176,6 +178,13 @@ void upload_hom_tables(const double hada_classes[], cudaStream_t s) {
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_hw_f, wf, sizeof(wf), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_chih_d, cd, sizeof(cd), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_chih_f, cf, sizeof(cf), 0, cudaMemcpyHostToDevice, s));
+  // chi is linear in the corner coordinates, so beyond the all-sum entries 0-2 (never read: W annihilates them)
+  // H chi lives on the single-bit sigmas 1, 2, 4 (entries 3-8, 12-14): the staged tensor pass keeps only those
+  for (int i = 0; i < 6; ++i)
+    for (int r = 3; r < 24; ++r)
+      if (!((r >= 3 && r <= 8) || (r >= 12 && r <= 14)) && cd[i][r] != 0.0)
+        throw std::logic_error("H chi has an entry off the single-bit sigmas");
+  upload_modal_tables(hada_classes, s);
 }
 
 template <typename TE>
@@ -259,6 +268,413 @@ struct U6 {
   const void* p[6];
   const void* hi[6];  // z-slab: the same fields of the slab above (== p for one periodic domain)
 };
+
+// ---------------------------------------------------------------- f64 energies, modal form, element pairs
+// W (the 45-term element stiffness in the sum/difference basis, hada_gen.cuh) is block diagonal over the
+// 21 non-sum entries: two 3x3 blocks a I + b 11^T ({3,7,14}: h0, h1; {11,16,18}: h5, h6), three 2x2 blocks
+// [[h3,h4],[h4,h3]] ({9,20}, {10,17}, {15,19}), three rank-1 blocks h2 [[1,1],[1,1]] ({4,6}, {5,12},
+// {8,13}: the rotations, K0's null space) and h7 on {21}, {22}, {23}. With orthonormal eigenvectors,
+// W = sum_k l_k v_k v_k^T over 18 modes, so E_ij = d_hat_i^T W d_hat_j = sum_k b_ik b_jk with
+// b_ik = sqrt(l_k) v_k . d_hat_i: 18 modal values per load case and a 21 x 18 Gram product.
+// Two threads share an element (lanes 2k, 2k+1: load cases 0-2 and 3-5): each forms its three modal
+// vectors (54 doubles, no spills), the Gram entries of its own cases, and the cross entries from the
+// partner's vectors, exchanged mode by mode with shuffles. Arithmetic f64 throughout; u is rounded to
+// f32 precision in mixed mode (the reference's float snapshot, src/homogenization.cpp:84-85) by integer
+// round-to-nearest-even on the f64 bits (no conversion instructions; identical to double(float(u)) for
+// |u| >= 2^-126).
+__constant__ double c_mode[10];  // kP1 kP2 kP3 kQ1 kQ2 kQ3 kR1 kR2 kS kT
+
+void upload_modal_tables(const double h[], cudaStream_t s) {
+  double scale = 0.0;
+  for (int k = 0; k < kHadaClasses; ++k) scale = std::fmax(scale, std::fabs(h[k]));
+  auto root = [scale](double v) {  // eigenvalues of a PSD matrix: rounding-level negatives are zeros
+    if (v < -1e-12 * scale) throw std::invalid_argument("element stiffness is not positive semi-definite");
+    return v > 0.0 ? std::sqrt(v) : 0.0;
+  };
+  static double m[10];
+  m[0] = root((h[0] + 2.0 * h[1]) / 3.0);
+  m[1] = root((h[0] - h[1]) / 2.0);
+  m[2] = root((h[0] - h[1]) / 6.0);
+  m[3] = root((h[5] + 2.0 * h[6]) / 3.0);
+  m[4] = root((h[5] - h[6]) / 2.0);
+  m[5] = root((h[5] - h[6]) / 6.0);
+  m[6] = root((h[3] + h[4]) / 2.0);
+  m[7] = root((h[3] - h[4]) / 2.0);
+  m[8] = root(h[2]);
+  m[9] = root(h[7]);
+  for (int k = 0; k < 10; ++k)
+    if (!std::isfinite(m[k])) throw std::invalid_argument("element stiffness is not positive semi-definite");
+  IHOM_CUDA(cudaMemcpyToSymbolAsync(c_mode, m, sizeof(m), 0, cudaMemcpyHostToDevice, s));
+}
+
+__device__ __forceinline__ double snap_f32_bits(double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  b += 0x0FFFFFFFull + ((b >> 29) & 1ull);  // round to nearest even at mantissa bit 29
+  return __longlong_as_double((long long)(b & ~0x1FFFFFFFull));
+}
+
+constexpr int kModes = 18;
+
+// modal vector of one load case from its 8 corner displacements (AoS f64, loc[] / top-plane pointer)
+// modal vector (18 values) of one load case from its sum/difference-basis displacement d_hat (entries 3..23)
+__device__ __forceinline__ void modal_from_dhat(const double dh[24], double b[kModes]) {
+  const double* m = c_mode;
+  {  // {3,7,14}
+    const double x = dh[3], y = dh[7], z = dh[14];
+    b[0] = m[0] * (x + y + z);
+    b[1] = m[1] * (x - y);
+    b[2] = m[2] * (x + y - 2.0 * z);
+  }
+  {  // {11,16,18}
+    const double x = dh[11], y = dh[16], z = dh[18];
+    b[3] = m[3] * (x + y + z);
+    b[4] = m[4] * (x - y);
+    b[5] = m[5] * (x + y - 2.0 * z);
+  }
+  b[6] = m[6] * (dh[9] + dh[20]);
+  b[7] = m[7] * (dh[9] - dh[20]);
+  b[8] = m[6] * (dh[10] + dh[17]);
+  b[9] = m[7] * (dh[10] - dh[17]);
+  b[10] = m[6] * (dh[15] + dh[19]);
+  b[11] = m[7] * (dh[15] - dh[19]);
+  b[12] = m[8] * (dh[4] + dh[6]);
+  b[13] = m[8] * (dh[5] + dh[12]);
+  b[14] = m[8] * (dh[8] + dh[13]);
+  b[15] = m[9] * dh[21];
+  b[16] = m[9] * dh[22];
+  b[17] = m[9] * dh[23];
+}
+
+// modal vector of one load case from its 8 corner displacements (AoS f64, loc[] / top-plane pointer)
+template <bool SNAP>
+__device__ __forceinline__ void modal_vector(const double* __restrict__ ui, const double* __restrict__ uz,
+                                             const unsigned loc[8], int lc, double b[kModes]) {
+  double dh[24];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double V[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double v = __ldg(((j >> 2) & 1 ? uz : ui) + 3 * (size_t)loc[j] + c);
+      V[j] = SNAP ? snap_f32_bits(v) : v;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (!((j >> k) & 1)) {
+          const double a = V[j], bb = V[j | (1 << k)];
+          V[j] = bb + a;
+          V[j | (1 << k)] = bb - a;
+        }
+#pragma unroll
+    for (int sg = 1; sg < 8; ++sg) dh[sg * 3 + c] = c_chih_d[lc][sg * 3 + c] - V[sg];
+  }
+  modal_from_dhat(dh, b);
+}
+
+// Gram entries of a lane's three modal vectors (eo: 00 01 02 11 12 22) and the cross entries with the
+// partner lane (lane ^ x): (own i, partner j) = (0,0) (1,1) (2,2) (0,1) (0,2) (1,2), exchanged mode by mode.
+__device__ __forceinline__ void gram_pairs(const double b[3][kModes], int x, double eo[6], double ex[6]) {
+#pragma unroll
+  for (int q = 0; q < 6; ++q) eo[q] = 0.0, ex[q] = 0.0;
+#pragma unroll
+  for (int k = 0; k < kModes; ++k) {
+    const double p0 = __shfl_xor_sync(0xffffffffu, b[0][k], x);
+    const double p1 = __shfl_xor_sync(0xffffffffu, b[1][k], x);
+    const double p2 = __shfl_xor_sync(0xffffffffu, b[2][k], x);
+    eo[0] = fma(b[0][k], b[0][k], eo[0]);
+    eo[1] = fma(b[0][k], b[1][k], eo[1]);
+    eo[2] = fma(b[0][k], b[2][k], eo[2]);
+    eo[3] = fma(b[1][k], b[1][k], eo[3]);
+    eo[4] = fma(b[1][k], b[2][k], eo[4]);
+    eo[5] = fma(b[2][k], b[2][k], eo[5]);
+    ex[0] = fma(b[0][k], p0, ex[0]);
+    ex[1] = fma(b[1][k], p1, ex[1]);
+    ex[2] = fma(b[2][k], p2, ex[2]);
+    ex[3] = fma(b[0][k], p1, ex[3]);
+    ex[4] = fma(b[0][k], p2, ex[4]);
+    ex[5] = fma(b[1][k], p2, ex[5]);
+  }
+}
+
+// Energies of one element shared by a lane pair. Lane role r = lane & 1 owns load cases 3r..3r+2.
+// Out: eo[6] Gram entries of the own cases (00 01 02 11 12 22 in local indices), ex[6] cross entries
+// (local own i, partner j): (0,0) (1,1) (2,2) (0,1) (0,2) (1,2). The even lane's cross entries are
+// (i, 3+j); the odd lane's upper ones are (j, 3+i) with j < i... see energy_index().
+template <bool SNAP>
+__device__ __forceinline__ void pair_energies(const U6& uu, const unsigned loc[8], bool top, int role, double eo[6],
+                                              double ex[6]) {
+  double b[3][kModes];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double* ui = static_cast<const double*>(role ? uu.p[3 + a] : uu.p[a]);
+    const double* uz = top ? static_cast<const double*>(role ? uu.hi[3 + a] : uu.hi[a]) : ui;
+    modal_vector<SNAP>(ui, uz, loc, 3 * role + a, b[a]);
+  }
+  gram_pairs(b, 1, eo, ex);
+}
+
+
+// Upper-triangle index (i <= j, row-major) of the 21 energies.
+__host__ __device__ __forceinline__ constexpr int tri(int i, int j) { return i * 6 - i * (i - 1) / 2 + (j - i); }
+
+// Energy index of slot m (0-5 own, 6-11 cross) for a lane role; -1: not stored by this lane
+// (the odd lane's copies of the diagonal cross entries).
+__host__ __device__ __forceinline__ constexpr int energy_index(int role, int m) {
+  // own slots: (0,0) (0,1) (0,2) (1,1) (1,2) (2,2); cross slots: (0,0) (1,1) (2,2) (0,1) (0,2) (1,2)
+  // as (own local i, partner local j)
+  const int oi = m == 0 || m == 1 || m == 2 ? 0 : (m == 3 || m == 4 ? 1 : 2);
+  const int oj = m == 0 ? 0 : (m == 1 || m == 3 ? 1 : 2);
+  const int xi = m == 6 || m == 9 || m == 10 ? 0 : (m == 7 || m == 11 ? 1 : 2);
+  const int xj = m == 6 ? 0 : (m == 7 || m == 9 ? 1 : 2);
+  return m < 6 ? tri(3 * role + oi, 3 * role + oj)
+               : (role == 0 ? tri(xi, 3 + xj)              // even lane: (i, 3+j)
+                            : (xi == xj ? -1 : tri(xj, 3 + xi)));  // odd lane: own 3+i, partner j: (j, 3+i)
+}
+
+// Element ordering shared by the pair kernels: a block of 128 threads owns a 32 x 2 element column tile
+// (x % 32 == 0, y % 2 == 0 grids) and marches up z; else grid-stride over elements. 2 lanes per element.
+constexpr int kPT = 128;
+
+template <bool SNAP>
+__global__ void __launch_bounds__(kPT) tensor_pair_kernel(GridGeo g, U6 uu, const double* __restrict__ rho,
+                                                          double penal, double* partials, double* __restrict__ ecache) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, role = lane & 1;
+  const int slot = (threadIdx.x >> 5) * 16 + (lane >> 1);  // element slot 0..63 of the block
+  int eidx[12];
+#pragma unroll
+  for (int m = 0; m < 12; ++m) eidx[m] = energy_index(role, m);
+  double acc[12];
+#pragma unroll
+  for (int m = 0; m < 12; ++m) acc[m] = 0.0;
+  const bool cols = g.n[0] % 32 == 0 && g.n[1] % 2 == 0;
+  const long long tiles_x = g.n[0] / 32, ntiles = cols ? tiles_x * (g.n[1] / 2) : 0;
+  const long long nsteps = cols ? ((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * g.n[2]
+                                : (g.nv - blockIdx.x * 64 + (long long)gridDim.x * 64 - 1) / ((long long)gridDim.x * 64);
+  for (long long it = 0; it < nsteps; ++it) {
+    int ex, ey, ez;
+    long long e;
+    bool valid = true;
+    if (cols) {
+      const long long tile = blockIdx.x + (it / g.n[2]) * gridDim.x;
+      ez = int(it % g.n[2]);
+      ex = int(tile % tiles_x) * 32 + (slot & 31);
+      ey = int(tile / tiles_x) * 2 + (slot >> 5);
+      e = ex + (long long)g.n[0] * (ey + (long long)g.n[1] * ez);
+    } else {
+      e = (long long)blockIdx.x * 64 + slot + it * (long long)gridDim.x * 64;
+      valid = e < g.nv;
+      const long long ee = valid ? e : 0;  // both lanes of a pair agree; whole pairs idle together
+      ex = int(ee % g.n[0]);
+      const long long r = ee / g.n[0];
+      ey = int(r % g.n[1]);
+      ez = int(r / g.n[1]);
+    }
+    unsigned loc[8];
+    corner_locs(g, ex, ey, ez, loc);
+    double E[12];
+    pair_energies<SNAP>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
+    if (!valid) continue;
+    if (ecache) {  // [21][nv]
+#pragma unroll
+      for (int m = 0; m < 12; ++m)
+        if (eidx[m] >= 0) ecache[eidx[m] * g.nv + e] = E[m];
+    }
+    const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
+#pragma unroll
+    for (int m = 0; m < 12; ++m) acc[m] = fma(q, E[m], acc[m]);
+  }
+  // block sums of the 21 entries (fixed partition and order: deterministic)
+  for (int k = 0; k < 21; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < 12; ++m) v += eidx[m] == k ? acc[m] : 0.0;
+    const double r = block_reduce_h(v, sh);
+    if (threadIdx.x == 0) partials[k * kReducePartials + blockIdx.x] = r;
+  }
+}
+
+// Sensitivity with the pair energies (no cache): the odd lane hands its 9 stored energies to the even
+// lane, which forms sum_ij s_ij E_ij in the cached kernel's order (bit-identical to sens_cached_kernel).
+template <bool SNAP>
+__global__ void __launch_bounds__(kPT) sens_pair_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
+                                                        const double* __restrict__ seed, double inv_m,
+                                                        double* __restrict__ out) {
+  const int role = threadIdx.x & 1;
+  const long long e = ((long long)blockIdx.x * kPT + threadIdx.x) >> 1;
+  const bool valid = e < g.nv;
+  const long long ee = valid ? e : 0;
+  const int ex = int(ee % g.n[0]);
+  const long long r = ee / g.n[0];
+  const int ey = int(r % g.n[1]), ez = int(r / g.n[1]);
+  unsigned loc[8];
+  corner_locs(g, ex, ey, ez, loc);
+  double E[12];
+  pair_energies<SNAP>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
+  double all[21];
+#pragma unroll
+  for (int m = 0; m < 12; ++m) {
+    const double other = __shfl_xor_sync(0xffffffffu, E[m], 1);
+    const int k0 = energy_index(0, m), k1 = energy_index(1, m);
+    all[k0] = E[m];
+    if (k1 >= 0) all[k1] = other;
+  }
+  if (!valid || role) return;
+  double acc = 0.0;  // sum_ij s_ij E_ij, s symmetric (src/homogenization.cpp:120,138-140)
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * all[q];
+  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;
+}
+
+// ---------------------------------------------------------------- staged pair tensor pass (bulk copies)
+// Same energies as tensor_pair_kernel, for grids with n0 % 32 == 0 and n1 % 2 == 0 (the column tiles):
+// a block owns a 32 x 2 element column and marches up z; the six displacement fields of each vertex plane
+// of the tile (33 x 3 vertices) are moved into a 3-slot shared-memory ring by the TMA engine
+// (cp.async.bulk, 54 contiguous runs per plane, completion counted on one mbarrier per slot), two planes
+// ahead of the compute. The corner loads become conflict-free LDS at immediate offsets; in mixed mode each
+// staged value is rounded to f32 precision once (not once per incident element). Lanes 0-15 own load
+// cases 0-2 of elements 0-15, lanes 16-31 cases 3-5 (partner = lane ^ 16).
+// Slot layout (doubles): field f at f*kStFS, row r at r*kStRS, even-x run (17 vertices, the 17th by its
+// own 32-byte copy) at 0, odd-x run (16 vertices) at kStP1; vertex k at 3k.
+constexpr int kStFS = 312, kStRS = 104, kStP1 = 56, kStPlane = 6 * kStFS;
+constexpr uint32_t kStBytes = 6 * 3 * (384 + 32 + 384);
+constexpr size_t kStSmem = sizeof(double) * 3 * kStPlane + 3 * sizeof(uint64_t);
+
+bool tensor_stage_ok(const GridGeo& g, const void* const* p, const void* const* hi) {
+  if (g.n[0] % 32 || g.n[1] % 2 || g.n[2] % 2 || g.n[2] < 2) return false;
+  for (int i = 0; i < 6; ++i)
+    if ((reinterpret_cast<uintptr_t>(p[i]) & 15) || (reinterpret_cast<uintptr_t>(hi[i]) & 15)) return false;
+  return true;
+}
+
+template <bool SNAP>
+__global__ void __launch_bounds__(kPT) tensor_stage_kernel(GridGeo g, U6 uu, const double* __restrict__ rho,
+                                                           double penal, double* partials,
+                                                           double* __restrict__ ecache) {
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  double* ring = reinterpret_cast<double*>(st_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ring + 3 * kStPlane);
+  __shared__ double chs[6][9];  // chi_hat entries 3-8 and 12-14 (sigma 1, 2, 4); every other entry is 0
+  __shared__ double sh[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int role = lane >> 4, j = lane & 15;
+  const int xl = 16 * (warp & 1) + j, yl = warp >> 1;
+  if (tid < 54) {
+    const int r = tid % 9;
+    chs[tid / 9][r] = c_chih_d[tid / 9][r < 6 ? 3 + r : 6 + r];
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&bar[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int n2 = g.n[2];
+  const unsigned d0 = (unsigned)g.cd[0][0], d1 = (unsigned)g.cd[0][1], B = (unsigned)g.size[0];
+  const long long tiles_x = g.n[0] / 32, ntiles = tiles_x * (g.n[1] / 2);
+  int eidx[12];
+#pragma unroll
+  for (int m = 0; m < 12; ++m) eidx[m] = energy_index(role, m);
+  double acc[12];
+#pragma unroll
+  for (int m = 0; m < 12; ++m) acc[m] = 0.0;
+  unsigned phase = 0;  // bit b: parity of the next completion of slot b
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int x0 = int(tile % tiles_x) * 32, y0 = int(tile / tiles_x) * 2;
+    // warp 0 stages vertex plane p (0..n2; n2 = the top plane: plane 0 of the slab above) into slot b
+    auto issue = [&](int p, int b) {
+      if (warp != 0) return;
+      if (lane == 0) mbar_arrive_expect_tx(&bar[b], kStBytes);
+      __syncwarp();
+      const int z = p == n2 ? 0 : p;
+      const unsigned pz = (unsigned)z & 1u, h2 = (unsigned)z >> 1;
+      for (int q = lane; q < 54; q += 32) {
+        const int f = q / 9, rem = q % 9, r = rem / 3, part = rem % 3;  // part 0/1: even x (16 + 1), 2: odd x
+        int y = y0 + r;
+        if (y >= g.n[1]) y -= g.n[1];
+        const unsigned px = part == 2 ? 1u : 0u, color = px | (((unsigned)y & 1u) << 1) | (pz << 2);
+        unsigned h0 = (unsigned)(x0 >> 1) + (part == 1 ? 16u : 0u);
+        if (h0 >= d0) h0 -= d0;
+        const size_t loc = (size_t)color * B + h0 + (size_t)d0 * (((unsigned)y >> 1) + (size_t)d1 * h2);
+        const double* src = static_cast<const double*>(p == n2 ? uu.hi[f] : uu.p[f]) + 3 * loc;
+        double* dst = ring + b * kStPlane + f * kStFS + r * kStRS + (px ? kStP1 : 0) + (part == 1 ? 48 : 0);
+        bulk_g2s(dst, src, part == 1 ? 32u : 384u, &bar[b]);
+      }
+    };
+    auto land = [&](int b) {  // wait for slot b; mixed mode rounds the staged values to f32 precision once
+      mbar_wait(&bar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+      if constexpr (SNAP) {
+        double* sl = ring + b * kStPlane;
+        for (int i = tid; i < kStPlane; i += kPT) sl[i] = snap_f32_bits(sl[i]);
+        fence_proxy_async_smem();  // these generic writes precede the slot's next bulk copy
+      }
+    };
+    for (int p = 0; p < 3 && p <= n2; ++p) issue(p, p);
+    land(0);
+    for (int z = 0; z < n2; ++z) {
+      land((z + 1) % 3);
+      __syncthreads();
+      const double* bot = ring + (z % 3) * kStPlane;
+      const double* top = ring + ((z + 1) % 3) * kStPlane;
+      double b[3][kModes];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int f = 3 * role + a;
+        double dh[24];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double V[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int x = xl + (jj & 1), r = yl + ((jj >> 1) & 1);
+            V[jj] = ((jj >> 2) & 1 ? top : bot)[f * kStFS + r * kStRS + ((x & 1) ? kStP1 : 0) + 3 * (x >> 1) + c];
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (!((jj >> k) & 1)) {
+                const double lo = V[jj], hi = V[jj | (1 << k)];
+                V[jj] = hi + lo;
+                V[jj | (1 << k)] = hi - lo;
+              }
+#pragma unroll
+          for (int sg = 1; sg < 8; ++sg) {
+            const int r = sg * 3 + c;
+            dh[r] = (r >= 3 && r <= 8) ? chs[f][r - 3] - V[sg] : ((r >= 12 && r <= 14) ? chs[f][r - 6] - V[sg] : -V[sg]);
+          }
+        }
+        modal_from_dhat(dh, b[a]);
+      }
+      double E[12];
+      gram_pairs(b, 16, E, E + 6);
+      const int ex = x0 + xl, ey = y0 + yl;
+      const long long e = ex + (long long)g.n[0] * (ey + (long long)g.n[1] * z);
+      if (ecache) {
+#pragma unroll
+        for (int m = 0; m < 12; ++m)
+          if (eidx[m] >= 0) ecache[eidx[m] * g.nv + e] = E[m];
+      }
+      const double q = penal == 1.0 ? rho[e] : pow(rho[e], penal);  // src/homogenization.cpp:91
+#pragma unroll
+      for (int m = 0; m < 12; ++m) acc[m] = fma(q, E[m], acc[m]);
+      __syncthreads();  // slot z % 3 is free
+      if (z + 3 <= n2) issue(z + 3, z % 3);
+    }
+  }
+  for (int k = 0; k < 21; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < 12; ++m) v += eidx[m] == k ? acc[m] : 0.0;
+    const double r = block_reduce_h(v, sh);
+    if (threadIdx.x == 0) partials[k * kReducePartials + blockIdx.x] = r;
+  }
+}
 
 template <typename TN, typename TE, bool HADA>
 __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
@@ -354,7 +770,31 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
   const bool te32 = energy_f32(snap);
-  if (htensor()) {  // sum/difference-basis energies: no gradient scratch in shared memory
+  if (htensor() && !te32 && tensor_stage_ok(g, uu.p, uu.hi)) {  // f64 energies, bulk-staged column tiles
+    static int occ = 0;
+    if (!occ) {
+      IHOM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tensor_stage_kernel<true>, kPT, kStSmem));
+      int dev = 0, sms = 0;
+      IHOM_CUDA(cudaGetDevice(&dev));
+      IHOM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      occ = std::max(1, occ) * sms;
+    }
+    const long long ntiles = (long long)(g.n[0] / 32) * (g.n[1] / 2);
+    blocks = std::min<long long>(std::min<long long>(ntiles, occ), kReducePartials);
+    if (snap)
+      tensor_stage_kernel<true><<<(unsigned)blocks, kPT, kStSmem, s>>>(g, uu, rho, penal, partials,
+                                                                       static_cast<double*>(ecache));
+    else
+      tensor_stage_kernel<false><<<(unsigned)blocks, kPT, kStSmem, s>>>(g, uu, rho, penal, partials,
+                                                                        static_cast<double*>(ecache));
+  } else if (htensor() && !te32) {  // f64 energies: modal form, two lanes per element
+    blocks = (g.nv + 63) / 64;
+    if (blocks > kReducePartials) blocks = kReducePartials;
+    if (snap)
+      tensor_pair_kernel<true><<<(unsigned)blocks, kPT, 0, s>>>(g, uu, rho, penal, partials, static_cast<double*>(ecache));
+    else
+      tensor_pair_kernel<false><<<(unsigned)blocks, kPT, 0, s>>>(g, uu, rho, penal, partials, static_cast<double*>(ecache));
+  } else if (htensor()) {  // sum/difference-basis energies: no gradient scratch in shared memory
     if (te32)
       tensor_kernel<TN, float, true><<<(unsigned)blocks, kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, partials,
                                                                       static_cast<float*>(ecache));
@@ -445,7 +885,12 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
   }
   const double inv_m = 1.0 / double(m_total > 0 ? m_total : g.nv);
   const bool te32 = energy_f32(snap);
-  if (htensor()) {
+  if (htensor() && !te32) {
+    if (snap)
+      sens_pair_kernel<true><<<ceil_div(2 * g.nv, kPT), kPT, 0, s>>>(g, uu, rho, penal, sym_seed36, inv_m, out);
+    else
+      sens_pair_kernel<false><<<ceil_div(2 * g.nv, kPT), kPT, 0, s>>>(g, uu, rho, penal, sym_seed36, inv_m, out);
+  } else if (htensor()) {
     if (te32)
       sens_kernel<TN, float, true><<<ceil_div(g.nv, kHT), kHT, 0, s>>>(g, uu, rho, penal, snap, lam, mu, sym_seed36,
                                                                        inv_m, out);

@@ -110,8 +110,8 @@ void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS
 // Coarsest level: x = Ainv f with <=3 refinement steps against A, translation
 // projection in/out, singularity flag (src/multigrid.cpp:426-451). Single block.
 template <typename TN>
-void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, TN* f, TN* u,
-                           double negligible, double* work, int* err, cudaStream_t s);
+void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
+                           TN* u, double negligible, double* work, int* err, cudaStream_t s);
 
 // ---- reductions (deterministic: fixed partition per size, fixed fold order) ----
 // sums of the three AoS components: out[3]

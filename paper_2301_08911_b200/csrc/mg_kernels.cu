@@ -1122,7 +1122,8 @@ __device__ double dense_resid(int N, const double* A, const double* x, const dou
 
 template <typename TN>
 __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long long nv, const double* __restrict__ Ainv,
-                                                                  const double* __restrict__ A, TN* f, TN* u,
+                                                                  const double* __restrict__ A,
+                                                                  const double* __restrict__ Q, int nq, TN* f, TN* u,
                                                                   double negligible, double* work, int* err) {
   __shared__ double red[kCoarseThreads];
   double* fv = work;           // [N] f in dof order
@@ -1133,11 +1134,22 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
     double part = 0.0;
     for (long long i = threadIdx.x; i < nv; i += blockDim.x) part += double(f[3 * i + c]);
     const double mean = block_sum_1(part, red) / double(nv);
-    for (long long i = threadIdx.x; i < nv; i += blockDim.x) {
-      const TN v = TN(double(f[3 * i + c]) - mean);
-      f[3 * i + c] = v;
-      fv[3 * i + c] = double(v);
-    }
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) fv[3 * i + c] = double(f[3 * i + c]) - mean;
+  }
+  __syncthreads();
+  // deflated near-null modes (floating islands, hierarchy.cpp factor_coarse_dense): f -= q (q . f)
+  for (int k = 0; k < nq; ++k) {
+    const double* q = Q + (size_t)k * N;
+    double part = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) part += q[i] * fv[i];
+    const double d = block_sum_1(part, red);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) fv[i] -= d * q[i];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {  // the level's f holds the projected load
+    const TN v = TN(fv[i]);
+    f[i] = v;
+    fv[i] = double(v);
   }
   __syncthreads();
   double part = 0.0;
@@ -1179,9 +1191,9 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
 }
 
 template <typename TN>
-void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, TN* f, TN* u,
-                           double negligible, double* work, int* err, cudaStream_t s) {
-  coarsest_kernel<TN><<<1, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, f, u, negligible, work, err);
+void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
+                           TN* u, double negligible, double* work, int* err, cudaStream_t s) {
+  coarsest_kernel<TN><<<1, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, Q, nq, f, u, negligible, work, err);
   IHOM_LAUNCH_CHECK();
 }
 
@@ -1217,7 +1229,9 @@ template void launch_galerkin_from_stencil<float>(const GridGeo&, const GridGeo&
                                                   ZLink<float>, const GridGeo*, int);
 template void launch_galerkin_from_stencil<double>(const GridGeo&, const GridGeo&, const double*, double*,
                                                    cudaStream_t, ZLink<double>, const GridGeo*, int);
-template void launch_coarsest_solve<double>(int, long long, const double*, const double*, double*, double*, double, double*, int*, cudaStream_t);
-template void launch_coarsest_solve<float>(int, long long, const double*, const double*, float*, float*, double, double*, int*, cudaStream_t);
+template void launch_coarsest_solve<double>(int, long long, const double*, const double*, const double*, int, double*,
+                                            double*, double, double*, int*, cudaStream_t);
+template void launch_coarsest_solve<float>(int, long long, const double*, const double*, const double*, int, float*,
+                                           float*, double, double*, int*, cudaStream_t);
 
 }  // namespace ihomgpu

@@ -553,7 +553,7 @@ bool tensor_stage_ok(const GridGeo& g, const void* const* p, const void* const* 
 }
 
 template <bool SNAP>
-__global__ void __launch_bounds__(kPT) tensor_stage_kernel(GridGeo g, U6 uu, const double* __restrict__ rho,
+__global__ void __launch_bounds__(kPT, 3) tensor_stage_kernel(GridGeo g, U6 uu, const double* __restrict__ rho,
                                                            double penal, double* partials,
                                                            double* __restrict__ ecache) {
   extern __shared__ __align__(128) unsigned char st_raw[];
@@ -585,25 +585,23 @@ __global__ void __launch_bounds__(kPT) tensor_stage_kernel(GridGeo g, U6 uu, con
   unsigned phase = 0;  // bit b: parity of the next completion of slot b
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int x0 = int(tile % tiles_x) * 32, y0 = int(tile / tiles_x) * 2;
-    // warp 0 stages vertex plane p (0..n2; n2 = the top plane: plane 0 of the slab above) into slot b
+    // stage vertex plane p (0..n2; n2 = the top plane: plane 0 of the slab above) into slot b: thread 0 arms
+    // the slot's mbarrier, threads 0..53 issue one bulk copy each (tx-count may dip below zero until armed)
     auto issue = [&](int p, int b) {
-      if (warp != 0) return;
-      if (lane == 0) mbar_arrive_expect_tx(&bar[b], kStBytes);
-      __syncwarp();
+      if (tid == 0) mbar_arrive_expect_tx(&bar[b], kStBytes);
+      if (tid >= 54) return;
       const int z = p == n2 ? 0 : p;
       const unsigned pz = (unsigned)z & 1u, h2 = (unsigned)z >> 1;
-      for (int q = lane; q < 54; q += 32) {
-        const int f = q / 9, rem = q % 9, r = rem / 3, part = rem % 3;  // part 0/1: even x (16 + 1), 2: odd x
-        int y = y0 + r;
-        if (y >= g.n[1]) y -= g.n[1];
-        const unsigned px = part == 2 ? 1u : 0u, color = px | (((unsigned)y & 1u) << 1) | (pz << 2);
-        unsigned h0 = (unsigned)(x0 >> 1) + (part == 1 ? 16u : 0u);
-        if (h0 >= d0) h0 -= d0;
-        const size_t loc = (size_t)color * B + h0 + (size_t)d0 * (((unsigned)y >> 1) + (size_t)d1 * h2);
-        const double* src = static_cast<const double*>(p == n2 ? uu.hi[f] : uu.p[f]) + 3 * loc;
-        double* dst = ring + b * kStPlane + f * kStFS + r * kStRS + (px ? kStP1 : 0) + (part == 1 ? 48 : 0);
-        bulk_g2s(dst, src, part == 1 ? 32u : 384u, &bar[b]);
-      }
+      const int f = tid / 9, rem = tid % 9, r = rem / 3, part = rem % 3;  // part 0/1: even x (16 + 1), 2: odd x
+      int y = y0 + r;
+      if (y >= g.n[1]) y -= g.n[1];
+      const unsigned px = part == 2 ? 1u : 0u, color = px | (((unsigned)y & 1u) << 1) | (pz << 2);
+      unsigned h0 = (unsigned)(x0 >> 1) + (part == 1 ? 16u : 0u);
+      if (h0 >= d0) h0 -= d0;
+      const size_t loc = (size_t)color * B + h0 + (size_t)d0 * (((unsigned)y >> 1) + (size_t)d1 * h2);
+      const double* src = static_cast<const double*>(p == n2 ? uu.hi[f] : uu.p[f]) + 3 * loc;
+      double* dst = ring + b * kStPlane + f * kStFS + r * kStRS + (px ? kStP1 : 0) + (part == 1 ? 48 : 0);
+      bulk_g2s(dst, src, part == 1 ? 32u : 384u, &bar[b]);
     };
     auto land = [&](int b) {  // wait for slot b; mixed mode rounds the staged values to f32 precision once
       mbar_wait(&bar[b], (phase >> b) & 1u);
@@ -614,11 +612,13 @@ __global__ void __launch_bounds__(kPT) tensor_stage_kernel(GridGeo g, U6 uu, con
         fence_proxy_async_smem();  // these generic writes precede the slot's next bulk copy
       }
     };
+    // one barrier per plane step: the step computes from slots z % 3, (z+1) % 3 while plane z+2 lands and is
+    // rounded in the third slot; after the barrier slot z % 3 is refilled with plane z+3
     for (int p = 0; p < 3 && p <= n2; ++p) issue(p, p);
     land(0);
+    land(1);
+    __syncthreads();
     for (int z = 0; z < n2; ++z) {
-      land((z + 1) % 3);
-      __syncthreads();
       const double* bot = ring + (z % 3) * kStPlane;
       const double* top = ring + ((z + 1) % 3) * kStPlane;
       double b[3][kModes];
@@ -663,7 +663,8 @@ __global__ void __launch_bounds__(kPT) tensor_stage_kernel(GridGeo g, U6 uu, con
       const double q = penal == 1.0 ? rho[e] : pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
       for (int m = 0; m < 12; ++m) acc[m] = fma(q, E[m], acc[m]);
-      __syncthreads();  // slot z % 3 is free
+      if (z + 2 <= n2) land((z + 2) % 3);
+      __syncthreads();  // slot z % 3 is free, plane z + 2 is staged
       if (z + 3 <= n2) issue(z + 3, z % 3);
     }
   }

@@ -1,9 +1,13 @@
 // ihom_b200.hpp -- header-only C++ wrapper over the C ABI (ihom_b200.h) that
-// mirrors the reference API (/root/reference/proj/include/ihom/*.hpp) so a
-// reference caller switches by changing the namespace:
+// mirrors the reference API (proj/include/ihom/*.hpp) so a reference caller
+// switches by changing the namespace (and the precision template argument into
+// a constructor argument):
 //
-//   ihom::Homogenizer<float> hom(reso, mat, penal, opts);   // reference (CPU)
-//   ihom::gpu::Homogenizer   hom(reso, mat, penal, opts);   // this library (B200)
+//   ihom::Homogenizer<float> hom(reso, mat, penal, opts);   // reference (CPU), inc/homogenization.hpp:29
+//   ihom::gpu::Homogenizer   hom(reso, mat, penal, opts);   // this library (B200), Precision::mixed
+//
+// IVec3, BaseMaterial and SolverOptions have the reference's fields and
+// validation (inc/grid.hpp:9, inc/material.hpp:17-35, inc/multigrid.hpp:22-27).
 //
 // Exceptions are re-raised with the reference's types (std::invalid_argument,
 // std::runtime_error, std::logic_error) from the C status codes.
@@ -30,9 +34,23 @@ inline void check(int rc) {
   }
 }
 
-enum class Precision { mixed, all_double };
+enum class Precision { mixed, all_double };  // the reference's Homogenizer<float> / Homogenizer<double>
 
-struct SolverOptions {  // inc/multigrid.hpp:22-27
+using IVec3 = std::array<int, 3>;  // inc/grid.hpp:9
+
+struct BaseMaterial {  // inc/material.hpp:17-35
+  double youngs = 1.0;
+  double poisson = 0.3;
+  BaseMaterial() = default;
+  BaseMaterial(double e, double nu) : youngs(e), poisson(nu) {
+    if (!(e > 0.0)) throw std::invalid_argument("Young's modulus must be positive");
+    if (!(nu > -1.0 && nu < 0.5)) throw std::invalid_argument("Poisson's ratio must lie in (-1, 0.5)");
+  }
+  double lambda() const { return youngs * poisson / ((1.0 + poisson) * (1.0 - 2.0 * poisson)); }
+  double mu() const { return youngs / (2.0 * (1.0 + poisson)); }
+};
+
+struct SolverOptions {  // inc/multigrid.hpp:22-27 (+ the solver mode of this library)
   double tol = 1e-2;
   int max_cycles = 50;
   int pre_sweeps = 1;
@@ -54,9 +72,10 @@ using Matrix6 = std::array<double, 36>;  // row-major 6x6 (Voigt 11,22,33,12,23,
 // raw device pointers are accepted by the *_device overloads.
 class Homogenizer {
  public:
-  Homogenizer(std::array<int, 3> reso, double youngs, double poisson, double penal, const SolverOptions& o,
+  // inc/homogenization.hpp:29: Homogenizer(IVec3 reso, const BaseMaterial& mat, double penal, const SolverOptions&)
+  Homogenizer(IVec3 reso, const BaseMaterial& mat, double penal, const SolverOptions& o,
               Precision p = Precision::mixed, int device = 0) {
-    ihom_desc d{{reso[0], reso[1], reso[2]}, youngs, poisson, penal,
+    ihom_desc d{{reso[0], reso[1], reso[2]}, mat.youngs, mat.poisson, penal,
                 p == Precision::mixed ? IHOM_MIXED : IHOM_ALL_DOUBLE, device};
     ihom_solver_opts so{o.tol, o.max_cycles, o.pre_sweeps, o.post_sweeps, o.mode};
     ctx_ = ihom_create(&d, &so);

@@ -47,7 +47,6 @@ void upload_fem_tables(const StiffnessTables& t, const K0Matrix& k, cudaStream_t
   }
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_d, kd, sizeof(kd), 0, cudaMemcpyHostToDevice, s));
   IHOM_CUDA(cudaMemcpyToSymbolAsync(c_kap_f, kf, sizeof(kf), 0, cudaMemcpyHostToDevice, s));
-  upload_gs_group_tables(kf, s);
   static double hd[kHadaClasses];
   static float hf[kHadaClasses];
   for (int c = 0; c < kHadaClasses; ++c) {
@@ -182,191 +181,6 @@ __global__ void __launch_bounds__(128, MINB) l0_apply_fast_kernel(GridGeo g, con
   }
 }
 
-// ---------------------------------------------------------------- shared-memory tiled variants
-// A block owns a TX x TY x TZ tile (halved coordinates) of one colour c. The
-// neighbours of its vertices live in the 8 colour blocks c ^ m; along axis k the
-// needed halved range is the tile itself (bit k of m clear) or the tile plus one
-// (bit set), starting at h0 - 1 for even parity and h0 for odd. Every region is
-// staged in a padded (TX+1)(TY+1)(TZ+1) smem slot with bulk coalesced loads; a
-// neighbour t then sits at  slot(m(t)) + ((lz + [t2=1]) EY + ly + [t1=1]) EX + lx + [t0=1]
-// -- a compile-time offset from one per-thread base (no per-neighbour global
-// address math, no dependent global-load chains).
-constexpr int kTX = 32, kTY = 4, kTZ = 1;
-constexpr int kEX = kTX + 1, kEY = kTY + 1, kEZ = kTZ + 1;
-constexpr int kSlot = kEX * kEY * kEZ;  // vertices per padded region
-
-template <typename TN, int M>
-__device__ __forceinline__ void stage_region(const GridGeo& g, int color, int h0x, int h0y, int h0z,
-                                             const TN* __restrict__ u, TN* sm) {
-  constexpr int b0 = M & 1, b1 = (M >> 1) & 1, b2 = (M >> 2) & 1;
-  constexpr int ex = kTX + b0, ey = kTY + b1, ez = kTZ + b2;
-  constexpr int rowlen = 3 * ex;  // contiguous AoS values of one row
-  const unsigned B = (unsigned)g.size[0];
-  const int d0 = g.cd[0][0], d1 = g.cd[0][1], d2 = g.cd[0][2];
-  const int sx = b0 ? h0x - ((color & 1) ? 0 : 1) : h0x;
-  const int sy = b1 ? h0y - (((color >> 1) & 1) ? 0 : 1) : h0y;
-  const int sz = b2 ? h0z - (((color >> 2) & 1) ? 0 : 1) : h0z;
-  const unsigned cb = (unsigned)(color ^ M) * B;
-  TN* dst = sm + 3 * M * kSlot;
-  const bool xwrap = sx < 0 || sx + ex > d0;
-  // warp threadIdx.y copies rows r = threadIdx.y, +kTY, ...; lanes stride the row
-#pragma unroll
-  for (int r0 = 0; r0 < ey * ez; r0 += kTY) {
-    const int r = r0 + threadIdx.y;
-    if (r < ey * ez) {
-      const int ly = r % ey, lz = r / ey;
-      int gy = sy + ly, gz = sz + lz;
-      gy = gy < 0 ? gy + d1 : (gy >= d1 ? gy - d1 : gy);
-      gz = gz < 0 ? gz + d2 : (gz >= d2 ? gz - d2 : gz);
-      const unsigned rowloc = cb + (unsigned)d0 * ((unsigned)gy + (unsigned)d1 * (unsigned)gz);
-      TN* drow = dst + 3 * ((lz * kEY + ly) * kEX);
-      if (!xwrap) {
-        const TN* grow = u + 3 * (size_t)(rowloc + (unsigned)sx);
-#pragma unroll
-        for (int e = threadIdx.x; e < rowlen; e += kTX) __pipeline_memcpy_async(drow + e, grow + e, sizeof(TN));
-      } else {
-#pragma unroll
-        for (int e = threadIdx.x; e < rowlen; e += kTX) {
-          const int lx = e / 3, comp = e - 3 * (e / 3);
-          int gx = sx + lx;
-          gx = gx < 0 ? gx + d0 : (gx >= d0 ? gx - d0 : gx);
-          __pipeline_memcpy_async(drow + e, u + 3 * (size_t)(rowloc + (unsigned)gx) + comp, sizeof(TN));
-        }
-      }
-    }
-  }
-}
-
-template <typename TN>
-__device__ __forceinline__ void stage_tile(const GridGeo& g, int color, int h0x, int h0y, int h0z,
-                                           const TN* __restrict__ u, TN* sm, bool skip_self) {
-  if (!skip_self) stage_region<TN, 0>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 1>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 2>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 3>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 4>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 5>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 6>(g, color, h0x, h0y, h0z, u, sm);
-  stage_region<TN, 7>(g, color, h0x, h0y, h0z, u, sm);
-}
-
-// neighbour n (27-index) of the thread's vertex, component c, from the staged tile
-#define TILE_U(sm)                                                                                      \
-  [&](int n, int c) {                                                                                   \
-    const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9 - 1;                                    \
-    const int m = (t0 != 0) | ((t1 != 0) << 1) | ((t2 != 0) << 2);                                      \
-    const int off = m * kSlot + (((t2 == 1) * kEY + (t1 == 1)) * kEX + (t0 == 1));                      \
-    return TA(sm[3 * (base + off) + c]);                                                                \
-  }
-
-// blockDim (kTX, kTY), grid (d0/kTX, d1/kTY, d2/kTZ * ncol): GS (ncol = 1, colour arg) or all colours.
-template <typename TC, typename TN, typename TA, bool GS>
-__global__ void __launch_bounds__(kTX* kTY) l0_tile_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                            const TN* __restrict__ u, const TN* __restrict__ f,
-                                                            TN* y, int color) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  TN* sm = reinterpret_cast<TN*>(smraw);
-  int h2;
-  if (GS) {
-    h2 = blockIdx.z * kTZ;
-  } else {
-    color = blockIdx.z & 7;
-    h2 = (blockIdx.z >> 3) * kTZ;
-  }
-  const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
-  stage_tile<TN>(g, color, h0x, h0y, h2, u, sm, GS);  // cp.async (LDGSTS): all copies in flight at once
-  __pipeline_commit();
-  const int lx = threadIdx.x, ly = threadIdx.y, lz = 0;
-  const int base = (lz * kEY + ly) * kEX + lx;
-  FastAddr fa;
-  fast_addr(g, color, h0x + lx, h0y + ly, h2 + lz, fa);
-  TA q[8];
-  load_q_fast(coeff, fa, q);  // overlaps the staging copies
-  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  if (GS) {
-    TA m[3], sblk[9];
-    ku_vertex_split<TA>(q, kappa<TA>(), TILE_U(sm), m, sblk);
-    TN S[9], rhs[3], out[3];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) S[e] = TN(sblk[e]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rhs[c] = TN(f[3 * loc + c]) - TN(m[c]);
-    solve3<TN>(S, rhs, out);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) y[3 * loc + c] = out[c];
-  } else {
-    TA acc[3];
-    ku_vertex<TA>(q, kappa<TA>(), TILE_U(sm), acc);
-    if (f) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(TA(f[3 * loc + c]) - acc[c]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * loc + c] = TN(acc[c]);
-    }
-  }
-}
-
-// Variant selection (IHOM_L0_KERNEL=tile|0; default fast: measured faster on B200, see profiles/).
-static bool tile_enabled() { return knob("L0_KERNEL", 0) != 0; }
-// Two-vertex GS variant (IHOM_L0_GS2=0 disables; default on).
-static bool gs2_enabled() { return knob("L0_GS2", 1) != 0; }
-
-static bool tile_ok(const GridGeo& g) {
-  return tile_enabled() && fast_ok(g) && g.cd[0][0] % kTX == 0 && g.cd[0][1] % kTY == 0 && g.cd[0][2] % kTZ == 0;
-}
-
-template <typename TN>
-static size_t tile_smem() {
-  return sizeof(TN) * 3 * 8 * kSlot;
-}
-
-// Tiled defect residual: ef0 = float(f - K u) with f64 arithmetic + |r|^2 block partials.
-template <typename TC>
-__global__ void __launch_bounds__(kTX* kTY) l0_tile_defect_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                   const double* __restrict__ u,
-                                                                   const double* __restrict__ f,
-                                                                   float* __restrict__ r32, double* partials) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  double* sm = reinterpret_cast<double*>(smraw);
-  __shared__ double red[4];
-  using TA = double;
-  const int color = blockIdx.z & 7;
-  const int h2 = (blockIdx.z >> 3) * kTZ;
-  const int h0x = blockIdx.x * kTX, h0y = blockIdx.y * kTY;
-  stage_tile<double>(g, color, h0x, h0y, h2, u, sm, false);
-  __pipeline_commit();
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int base = ly * kEX + lx;
-  FastAddr fa;
-  fast_addr(g, color, h0x + lx, h0y + ly, h2, fa);
-  TA q[8];
-  load_q_fast(coeff, fa, q);
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  TA acc[3];
-  ku_vertex<TA>(q, kappa<TA>(), TILE_U(sm), acc);
-  const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
-  double ss = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double r = f[3 * loc + c] - acc[c];
-    r32[3 * loc + c] = float(r);
-    ss += r * r;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
-  const int t = threadIdx.y * blockDim.x + threadIdx.x;
-  if ((t & 31) == 0) red[t >> 5] = ss;
-  __syncthreads();
-  if (t == 0) {
-    const size_t bid = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
-    partials[bid] = (red[0] + red[1]) + (red[2] + red[3]);
-  }
-}
-
 // Two same-colour vertices per thread, stacked in halved z (h2, h2+1): the upper
 // neighbour plane of the first (t2 = +1) is the lower plane of the second
 // (t2 = -1), so those 9 neighbours are loaded once into registers and reused.
@@ -426,290 +240,6 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     solve3<TN>(sblk, rhs, out);
 #pragma unroll
     for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
-  }
-}
-
-// ---------------------------------------------------------------- column-marching GS pass (f32 inner)
-// A thread walks KZ same-colour vertices up its (h0, h1) column (halved z h2 .. h2+KZ-1, actual z
-// step 2). The upper neighbour plane of one vertex (actual z+1) is the lower plane of the next, so
-// each step loads two new planes (18 neighbours) and carries 9 in registers -- the fast2 pairing
-// extended along the whole column, with the element planes and the per-axis addressing advanced
-// incrementally. Same per-vertex arithmetic and order as l0_gs_fast2_kernel: bit-identical.
-template <typename TC, int MINB, bool ZL = false, int ZC = -1, int KZ = 4>
-__global__ void __launch_bounds__(128, MINB) l0_gs_col_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
-                                                              const float* __restrict__ f, float* u, ZLink<float> ul,
-                                                              int color) {
-  if constexpr (!ZL) {
-    cl = {coeff, coeff};
-    ul = {u, u};
-  }
-  if constexpr (ZC >= 0) color = ZC;
-  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
-  const int h2s = KZ * blockIdx.z;
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
-  using TA = float;
-  const float* ur = u;
-  float lo[9][3], up[9][3];
-  {  // lower plane of the first vertex
-    FastAddr fa;
-    fast_addr(g, color, h0, h1, h2s, fa);
-    const float* p0 = zbase(fa, ur, ul, 0);
-#pragma unroll
-    for (int n = 0; n < 9; ++n) {
-      if ((ZM >> n) & 1u) continue;
-      const float* p = p0 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][0]);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) lo[n][c] = __ldg(p + c);
-    }
-  }
-#pragma unroll 1
-  for (int j = 0; j < KZ; ++j) {
-    FastAddr fa;
-    fast_addr(g, color, h0, h1, h2s + j, fa);
-    TA q[8];
-    load_q_fast(coeff, cl, fa, q);
-    const float* p2 = zbase(fa, ur, ul, 2);
-    auto U = [&](int n, int c) -> TA {
-      if (n < 9) return lo[n][c];
-      const unsigned l = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];
-      if (n < 18) return __ldg(ur + 3 * (size_t)l + c);
-      const float v = __ldg(p2 + 3 * (size_t)l + c);
-      up[n - 18][c] = v;
-      return v;
-    };
-    TA m[3], sblk[9];
-    ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), U, m, sblk);
-    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
-    float rhs[3], out[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
-    solve3<float>(sblk, rhs, out);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
-#pragma unroll
-    for (int n = 0; n < 9; ++n)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) lo[n][c] = up[n][c];
-  }
-}
-
-static int gs_col_kz() { return knob("GS_COL", 0); }  // 0: off; else vertices per column (2, 4, 8)
-
-// ---------------------------------------------------------------- paired f32 kernels (FFMA2)
-// One thread, two same-colour vertices stacked in halved z (h2, h2+1) -- the
-// fast2 pairing -- with the stencil evaluated ONCE in float2 lane-pair
-// arithmetic (vec2.cuh): lane x = the lower vertex, lane y = the upper one.
-// sm_100 issues FFMA2/FADD2/FMUL2 at the scalar instruction rate, so the
-// floating-point instruction count per vertex halves; every lane rounds like
-// the scalar kernel, so results are bit-identical to l0_gs_fast2_kernel /
-// l0_apply_fast_kernel<float, float, float>.
-struct PairPlanes {
-#if IHOM_PAIR_SHARE
-  float shared_pl[9][3];  // plane t2 = +1 of the lower vertex == plane t2 = -1 of the upper
-#endif
-  const float* pa0;  // lower vertex, plane t2 = -1
-  const float* pa2;  // lower vertex, plane t2 = +1 (== upper vertex, plane t2 = -1)
-  const float* pb2;  // upper vertex, plane t2 = +1
-};
-
-__device__ __forceinline__ void load_pair_planes(const FastAddr& fa, const FastAddr& fb, const float* __restrict__ u,
-                                                 const ZLink<float>& ul, PairPlanes& pp) {
-  const float* pa2 = zbase(fa, u, ul, 2);
-  pp.pa2 = pa2;
-#if IHOM_PAIR_SHARE
-#pragma unroll
-  for (int n = 0; n < 9; ++n) {
-    const float* p = pa2 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) pp.shared_pl[n][c] = __ldg(p + c);
-  }
-#endif
-  pp.pa0 = zbase(fa, u, ul, 0);
-  pp.pb2 = zbase(fb, u, ul, 2);
-}
-
-#ifndef IHOM_PAIR_SHARE
-#define IHOM_PAIR_SHARE 0
-#endif
-#if IHOM_PAIR_SHARE
-#define PAIR_U(u)                                                                                                  \
-  [&](int n, int c) -> float2 {                                                                                    \
-    const float a_ = n >= 18 ? pp.shared_pl[n - 18][c]                                                             \
-                             : __ldg((n < 9 ? pp.pa0 : u) +                                                        \
-                                     3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c);    \
-    const float b_ = n < 9 ? pp.shared_pl[n][c]                                                                    \
-                           : __ldg((n < 18 ? u : pp.pb2) +                                                         \
-                                   3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c);      \
-    return make_float2(a_, b_);                                                                                    \
-  }
-#else
-// both lanes loaded straight into their register pair (the shared plane is re-read through L1 instead of
-// being held in 27 registers and copied into the other lane position)
-#define PAIR_U(u)                                                                                                  \
-  [&](int n, int c) -> float2 {                                                                                    \
-    const float a_ = __ldg((n < 9 ? pp.pa0 : (n < 18 ? u : pp.pa2)) +                                              \
-                           3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c);              \
-    const float b_ = __ldg((n < 9 ? pp.pa2 : (n < 18 ? u : pp.pb2)) +                                              \
-                           3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c);              \
-    return make_float2(a_, b_);                                                                                    \
-  }
-#endif
-
-template <typename TC>
-__device__ __forceinline__ void load_q_pair(const TC* __restrict__ coeff, const ZLink<TC>& cl, const FastAddr& fa,
-                                            const FastAddr& fb, float2 q[8]) {
-  float qa[8], qb[8];
-  load_q_fast(coeff, cl, fa, qa);
-  load_q_fast(coeff, cl, fb, qb);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) q[k] = make_float2(qa[k], qb[k]);
-}
-
-// GS colour pass; grid = (d0/bx, ceil(d1/by), d2/2)
-template <typename TC, int MINB, bool ZL = false>
-__global__ void __launch_bounds__(128, MINB) l0_gs_pair_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
-                                                               const float* __restrict__ f,
-                                                               const float* __restrict__ ur, ZLink<float> ul,
-                                                               float* uw, int color) {
-  if constexpr (!ZL) {
-    cl = {coeff, coeff};
-    ul = {ur, ur};
-  }
-  const int h2 = 2 * blockIdx.z;
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
-  FastAddr fa, fb;
-  fast_addr(g, color, h0, h1, h2, fa);
-  fast_addr(g, color, h0, h1, h2 + 1, fb);
-  PairPlanes pp;
-  load_pair_planes(fa, fb, ur, ul, pp);
-  float2 q[8];
-  load_q_pair(coeff, cl, fa, fb, q);
-  float2 m[3], S[9];
-  ku_vertex_split<float2>(q, kappa<float>(), PAIR_U(ur), m, S);
-#pragma unroll
-  for (int v = 0; v < 2; ++v) {
-    const FastAddr& fx = v == 0 ? fa : fb;
-    const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
-    float sblk[9], rhs[3], out[3];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) sblk[e] = v == 0 ? S[e].x : S[e].y;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - (v == 0 ? m[c].x : m[c].y);
-    solve3<float>(sblk, rhs, out);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
-  }
-}
-
-// y = K u, or y = f - K u (f != null); grid = (d0/bx, ceil(d1/by), 8 * d2/2), colour fastest
-template <typename TC, int MINB, bool ZL = false>
-__global__ void __launch_bounds__(128, MINB) l0_apply_pair_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                  ZLink<TC> cl, const float* __restrict__ u,
-                                                                  ZLink<float> ul, const float* __restrict__ f,
-                                                                  float* __restrict__ y) {
-  if constexpr (!ZL) {
-    cl = {coeff, coeff};
-    ul = {u, u};
-  }
-  const int color = blockIdx.z & 7;
-  const int h2 = 2 * (blockIdx.z >> 3);
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
-  FastAddr fa, fb;
-  fast_addr(g, color, h0, h1, h2, fa);
-  fast_addr(g, color, h0, h1, h2 + 1, fb);
-  PairPlanes pp;
-  load_pair_planes(fa, fb, u, ul, pp);
-  float2 q[8];
-  load_q_pair(coeff, cl, fa, fb, q);
-  float2 acc[3];
-  ku_vertex<float2>(q, kappa<float>(), PAIR_U(u), acc);
-#pragma unroll
-  for (int v = 0; v < 2; ++v) {
-    const FastAddr& fx = v == 0 ? fa : fb;
-    const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float a = v == 0 ? acc[c].x : acc[c].y;
-      y[3 * loc + c] = f ? f[3 * loc + c] - a : a;
-    }
-  }
-}
-
-// register budget of the paired kernels: 3 blocks/SM (168 regs, default) or 4 (128 regs): IHOM_PAIR_MINB
-static int pair_minb() { return knob("PAIR_MINB", 3); }
-
-// Paired variants: IHOM_L0_PAIR=1 (off by default: measured slower at 512^3, 0.84 vs 0.67 ms per GS pass -- 168 registers leave 12 warps per SM and the kernel is latency-bound; profiles/kernel_variants_r01.md).
-static bool pair_enabled() { return knob("L0_PAIR", 0) != 0; }
-
-// ---------------------------------------------------------------- fused colour-pair GS pass (f32 inner)
-// Colours ca and cb = ca ^ 1 differ only in x parity. A vertex of cb has exactly two neighbours of
-// colour ca -- its x-neighbours in the same row -- and no other colour of the pair is touched by
-// either colour's stencil outside that row. So one CTA per row (all d0 half-x positions) can run
-// the two colour passes back to back: phase A updates the row's ca vertices (reading the OLD cb
-// values), __syncthreads, phase B updates the cb vertices (reading the NEW ca values of the same
-// row, coherent loads). Every other CTA's rows have another y/z parity or are >= 2 rows away, so
-// the fused pass is exactly the two sequential passes (bit-identical), with one read of the other
-// six colours instead of two. ZC >= 0: zero-start pair (ZC = ca, forward order).
-template <typename TC, int MINB, bool ZL = false, int ZC = -1>
-__global__ void __launch_bounds__(256, MINB) l0_gs_cpair_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                ZLink<TC> cl, const float* __restrict__ f,
-                                                                float* u, ZLink<float> ul, int ca) {
-  if constexpr (!ZL) {
-    cl = {coeff, coeff};
-    ul = {u, u};
-  }
-  if constexpr (ZC >= 0) ca = ZC;
-  const int cb = ca ^ 1;
-  const int h1 = blockIdx.x, h2 = blockIdx.y;
-  using TA = float;
-  for (int h0 = threadIdx.x; h0 < g.cd[0][0]; h0 += blockDim.x) {  // phase A: colour ca
-    constexpr unsigned ZMA = ZC >= 0 ? zero_start_mask(ZC) : 0u;
-    FastAddr fa;
-    fast_addr(g, ca, h0, h1, h2, fa);
-    TA q[8];
-    load_q_fast(coeff, cl, fa, q);
-    const float* ub0 = zbase(fa, (const float*)u, ul, 0);
-    const float* ub2 = zbase(fa, (const float*)u, ul, 2);
-    auto U = [&](int n, int c) -> TA {
-      const unsigned l = fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9];
-      return __ldg((n < 9 ? ub0 : (n < 18 ? (const float*)u : ub2)) + 3 * (size_t)l + c);
-    };
-    TA m[3], sblk[9];
-    ku_vertex_split_z<ZMA, TA>(q, kappa<TA>(), U, m, sblk);
-    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
-    float rhs[3], out[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
-    solve3<float>(sblk, rhs, out);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
-  }
-  __syncthreads();  // the row's new ca values are visible to the whole CTA
-  for (int h0 = threadIdx.x; h0 < g.cd[0][0]; h0 += blockDim.x) {  // phase B: colour cb (ca neighbours: coherent loads)
-    constexpr unsigned ZMB = ZC >= 0 ? zero_start_mask(ZC ^ 1) : 0u;
-    FastAddr fb;
-    fast_addr(g, cb, h0, h1, h2, fb);
-    TA q[8];
-    load_q_fast(coeff, cl, fb, q);
-    const float* ub0 = zbase(fb, (const float*)u, ul, 0);
-    const float* ub2 = zbase(fb, (const float*)u, ul, 2);
-    auto U = [&](int n, int c) -> TA {
-      const unsigned l = fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9];
-      const float* p = (n < 9 ? ub0 : (n < 18 ? (const float*)u : ub2)) + 3 * (size_t)l + c;
-      return (n == 12 || n == 14) ? *(volatile const float*)p : __ldg(p);  // the row's x-neighbours: colour ca
-    };
-    TA m[3], sblk[9];
-    ku_vertex_split_z<ZMB, TA>(q, kappa<TA>(), U, m, sblk);
-    const size_t loc = fb.A[0][1] + fb.A[1][1] + fb.A[2][1];
-    float rhs[3], out[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - m[c];
-    solve3<float>(sblk, rhs, out);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
   }
 }
 
@@ -840,25 +370,9 @@ void launch_l0_apply(const GridGeo& g, const TC* coeff, const TN* u, const TN* f
   ul = resolve(ul, u);
   if (sweep_ok(g)) {
     launch_l0_apply_sweep<TC, TN, TA>(g, coeff, cl, u, ul, f, y, s);
-  } else if (!linked && tile_ok(g)) {
-    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
-    const size_t sm = tile_smem<TN>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    l0_tile_kernel<TC, TN, TA, false><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, y, 0);
   } else if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
-    if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
-      if (g.cd[0][2] % 2 == 0 && pair_enabled()) {
-        const dim3 gr2(gr.x, gr.y, 8 * (g.cd[0][2] / 2));
-        if (linked) l0_apply_pair_kernel<TC, 3, true><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
-        else if (pair_minb() >= 4) l0_apply_pair_kernel<TC, 4><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
-        else l0_apply_pair_kernel<TC, 3><<<gr2, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
-        IHOM_LAUNCH_CHECK();
-        return;
-      }
-    }
     // f32 kernels capped at 64 registers (8 blocks/SM: more warps in flight, measured faster);
     // f64 kernels uncapped (a cap spills and was measured slower).
     if (linked) l0_apply_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1, true><<<gr, b, 0, s>>>(g, coeff, cl, u, ul, f, y);
@@ -896,16 +410,12 @@ __global__ void __launch_bounds__(128) l0_gs_kernel(GridGeo g, const TC* __restr
   for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }
 
-bool gs_sweep_ok(const GridGeo& g);
-void launch_l0_gs_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
-                        ZLink<float> ul, int color, bool zero_start, cudaStream_t s);
 
 template <typename TC, typename TN, typename TA>
 bool l0_gs_zero_start_ok(const GridGeo& g) {
   if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float> && std::is_same_v<TC, float>) {
     if (knob("ZERO_START", 1) == 0) return false;
-    if (gs_sweep_ok(g)) return true;
-    return fast_ok(g) && g.cd[0][2] % 2 == 0 && !pair_enabled() && gs2_enabled() && !tile_ok(g);
+    return fast_ok(g) && g.cd[0][2] % 2 == 0;
   }
   return false;
 }
@@ -913,23 +423,9 @@ bool l0_gs_zero_start_ok(const GridGeo& g) {
 // register budget of the two-vertex GS kernel: 5 blocks/SM (96 regs, default) or 6 / 8 (knob GS2_MINB)
 static int gs2_minb() { return knob("GS2_MINB", 5); }
 
-template <typename TC, bool ZL, int ZC>
-static bool launch_col(const dim3& gr2, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff, ZLink<TC> cl,
-                       const float* f, float* u, ZLink<float> ul, int color) {
-  const int kz = gs_col_kz();
-  if (kz <= 0 || (2 * gr2.z) % kz != 0) return false;
-  const dim3 gr(gr2.x, gr2.y, 2 * gr2.z / kz);  // gr2 counts vertex pairs
-  if (kz == 2) l0_gs_col_kernel<TC, 4, ZL, ZC, 2><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
-  else if (kz == 8) l0_gs_col_kernel<TC, 4, ZL, ZC, 8><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
-  else l0_gs_col_kernel<TC, 4, ZL, ZC, 4><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, color);
-  return true;
-}
-
 template <typename TC, typename TN, bool ZL, int ZC>
 static void launch_fast2_zs(const dim3& gr, const dim3& b, cudaStream_t s, const GridGeo& g, const TC* coeff,
                             ZLink<TC> cl, const TN* f, TN* u, ZLink<TN> ul) {
-  if constexpr (std::is_same_v<TN, float>)
-    if (launch_col<TC, ZL, ZC>(gr, b, s, g, coeff, cl, f, u, ul, ZC)) return;
   const int mb = ZL ? 5 : gs2_minb();
   if (mb >= 8) l0_gs_fast2_kernel<TC, TN, 8, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
   else if (mb == 6) l0_gs_fast2_kernel<TC, TN, 6, ZL, ZC><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, ZC);
@@ -950,41 +446,6 @@ static void launch_fast2_zs(int color, const dim3& gr, const dim3& b, cudaStream
   }
 }
 
-// fused colour-pair pass (ca, ca ^ 1), f32 inner fields; zero_start: forward pair of a zero-start sweep
-// Off by default: measured equal to two l0_gs_fast2 passes (1.48 vs 2 x 0.73 ms at 512^3) -- the GS
-// pass is issue/latency-bound, not bound by the u traffic the fusion removes (profiles/kernel_variants_r01.md).
-bool l0_gs_cpair_ok(const GridGeo& g) { return knob("L0_CPAIR", 0) != 0 && fast_ok(g) && g.cd[0][0] >= 32; }
-
-template <bool ZL, int ZC>
-static void launch_cpair_zc(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
-                            ZLink<float> ul, int ca, cudaStream_t s) {
-  const int bx = g.cd[0][0] >= 256 ? 256 : ((g.cd[0][0] + 31) / 32) * 32;
-  // full-stencil variants need ~80 registers (3 blocks/SM); the sparse zero-start ones fit 64 (4 blocks/SM)
-  constexpr int minb = (ZC >= 0 && ZC <= 4) ? 4 : 3;
-  l0_gs_cpair_kernel<float, minb, ZL, ZC><<<dim3(g.cd[0][1], g.cd[0][2]), bx, 0, s>>>(g, coeff, cl, f, u, ul, ca);
-}
-template <bool ZL>
-static void launch_cpair_zl(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
-                            ZLink<float> ul, int ca, bool zero_start, cudaStream_t s) {
-  if (!zero_start) return launch_cpair_zc<ZL, -1>(g, coeff, cl, f, u, ul, ca, s);
-  switch (ca) {
-    case 0: return launch_cpair_zc<ZL, 0>(g, coeff, cl, f, u, ul, ca, s);
-    case 2: return launch_cpair_zc<ZL, 2>(g, coeff, cl, f, u, ul, ca, s);
-    case 4: return launch_cpair_zc<ZL, 4>(g, coeff, cl, f, u, ul, ca, s);
-    case 6: return launch_cpair_zc<ZL, 6>(g, coeff, cl, f, u, ul, ca, s);
-    default: throw std::logic_error("zero-start colour pairs start at an even colour");
-  }
-}
-void launch_l0_gs_cpair(const GridGeo& g, const float* coeff, const float* f, float* u, int ca, cudaStream_t s,
-                        ZLink<float> cl, ZLink<float> ul, bool zero_start) {
-  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
-  cl = resolve(cl, coeff);
-  ul = resolve(ul, u);
-  if (linked) launch_cpair_zl<true>(g, coeff, cl, f, u, ul, ca, zero_start, s);
-  else launch_cpair_zl<false>(g, coeff, cl, f, u, ul, ca, zero_start, s);
-  IHOM_LAUNCH_CHECK();
-}
-
 template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
                         ZLink<TC> cl, ZLink<TN> ul, bool zero_start) {
@@ -992,12 +453,6 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
   if (linked && !fast_ok(g)) throw std::invalid_argument("z-slab level needs an even grid");
   cl = resolve(cl, coeff);
   ul = resolve(ul, u);
-  if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float> && std::is_same_v<TC, float>) {
-    if (gs_sweep_ok(g)) {
-      launch_l0_gs_sweep(g, coeff, cl, f, u, ul, color, zero_start, s);
-      return;
-    }
-  }
   if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
     if (zero_start) {
       if (!l0_gs_zero_start_ok<TC, TN, TA>(g)) throw std::logic_error("zero-start GS pass on an unsupported grid");
@@ -1010,30 +465,13 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
     }
   }
   if (zero_start) throw std::logic_error("zero-start GS pass exists for the f32 inner level-0 kernel only");
-  if (!linked && tile_ok(g)) {
-    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, g.cd[0][2] / kTZ);
-    const size_t sm = tile_smem<TN>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_kernel<TC, TN, TA, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    l0_tile_kernel<TC, TN, TA, true><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, u, color);
-  } else if (fast_ok(g)) {
+  if (fast_ok(g)) {
     const dim3 b = fast_block(g);
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
     bool done = false;
     if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
-      if (g.cd[0][2] % 2 == 0 && pair_enabled()) {
+      if (g.cd[0][2] % 2 == 0) {  // two z-stacked vertices per thread
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
-        if (linked) l0_gs_pair_kernel<TC, 3, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
-        else if (pair_minb() >= 4) l0_gs_pair_kernel<TC, 4><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
-        else l0_gs_pair_kernel<TC, 3><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
-        done = true;
-      } else if (g.cd[0][2] % 2 == 0 && gs2_enabled()) {
-        const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
-        if (linked ? launch_col<TC, true, -1>(gr2, b, s, g, coeff, cl, f, u, ul, color)
-                   : launch_col<TC, false, -1>(gr2, b, s, g, coeff, cl, f, u, ul, color)) {
-          IHOM_LAUNCH_CHECK();
-          return;
-        }
         if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else if (gs2_minb() >= 8) l0_gs_fast2_kernel<TC, TN, 8><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else if (gs2_minb() == 6) l0_gs_fast2_kernel<TC, TN, 6><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
@@ -1081,15 +519,6 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
   ul = resolve(ul, u);
   if constexpr (std::is_same_v<TC, float>) {
     if (sweep_ok(g)) return launch_l0_defect_sweep(g, coeff, cl, u, ul, f, r32, partials, s);
-  }
-  if (!linked && tile_ok(g)) {
-    const dim3 gr(g.cd[0][0] / kTX, g.cd[0][1] / kTY, 8 * (g.cd[0][2] / kTZ));
-    const size_t sm = tile_smem<double>();
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_tile_defect_kernel<TC>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    l0_tile_defect_kernel<TC><<<gr, dim3(kTX, kTY), sm, s>>>(g, coeff, u, f, r32, partials);
-    IHOM_LAUNCH_CHECK();
-    return (long long)gr.x * gr.y * gr.z;
   }
   const dim3 b = fast_block(g);
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);

@@ -206,18 +206,6 @@ double gs_coarse_bytes(const GridGeo& g, int c, double sN, double sC) {
 double gs_l0_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   return double(g.nv) * (double(c) / 8.0 * 3.0 * sN + sC) + double(g.size[c]) * 6.0 * sN;
 }
-// fused colour pair (ca, ca ^ 1): the other six colours' u + the pair's own old/new values once,
-// all coefficients, f and u of both colours
-double gs_pair_bytes(const GridGeo& g, int ca, double sN, double sC) {
-  const double pair = double(g.size[ca] + g.size[ca ^ 1]);
-  return double(g.nv - pair) * 3.0 * sN + double(g.size[ca ^ 1]) * 3.0 * sN + double(g.nv) * sC + pair * 6.0 * sN;
-}
-double gs_pair_bytes_zs(const GridGeo& g, int ca, double sN, double sC) {  // only colours < ca hold data
-  double others = 0.0;
-  for (int k = 0; k < ca; ++k) others += double(g.size[k]);
-  const double pair = double(g.size[ca] + g.size[ca ^ 1]);
-  return others * 3.0 * sN + double(g.nv) * sC + pair * 6.0 * sN;
-}
 double gs_coarse_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   const int live = 27 - __builtin_popcount(zero_start_mask(c));
   double others = 0.0;
@@ -765,7 +753,7 @@ bool Hierarchy<T>::zero_start_ok(int l) const {
   if (knob("ZERO_START", 1) == 0) return false;
   if (l > 0) return true;  // every stencil GS kernel takes the zero mask
   if constexpr (std::is_same_v<T, float>)
-    return l0_gs_cpair_ok(levels_[0].g) || l0_gs_zero_start_ok<float, float, float>(levels_[0].g);
+    return l0_gs_zero_start_ok<float, float, float>(levels_[0].g);
   return false;  // level-0 f32 inner fields exist in mixed precision only
 }
 
@@ -774,21 +762,6 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
     if (zero_start && reverse) throw std::logic_error("zero-start sweeps run the colours forward");
-    if (l == 0 && l0_gs_cpair_ok(L.g)) {  // fused colour pairs (0,1) (2,3) (4,5) (6,7), or (7,6) ... reversed
-      for (int sw = 0; sw < sweeps; ++sw)
-        for (int pi = 0; pi < 4; ++pi) {
-          const int ca = reverse ? 7 - 2 * pi : 2 * pi;
-          if (L.sharded) sync();
-          const bool zs = zero_start && sw == 0;
-          {
-            ProfScope p(s_, "l0_gs_f32", zs ? gs_pair_bytes_zs(L.g, ca, 4, 4) : gs_pair_bytes(L.g, ca, 4, 4));
-            launch_l0_gs_cpair(L.g, coeff_.p, L.ef.p, L.eu.p, ca, s_, L.sharded ? coeff_l_ : ZLink<float>{}, L.eul,
-                               zs);
-          }
-          ++launches_;
-        }
-      return;
-    }
     for (int sw = 0; sw < sweeps; ++sw)
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;
@@ -1237,111 +1210,14 @@ void Hierarchy<T>::residual_f32_group(int G, int l) {
 // One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
 // converged) skips every level-0 and transfer step; the grouped coarse kernels still compute its lane
 // on stale (finite) data, which nothing reads.
-// Inner f32 residuals of RHSs ka and kb at level 0 in one paired element sweep.
-template <typename T>
-void Hierarchy<T>::residual_f32_l0_pair(int ka, int kb) {
-  Level& L = levels_[0];
-  if constexpr (std::is_same_v<T, float>) {
-    if (L.sharded) sync();
-    const float* u[2];
-    const float* f[2];
-    float* y[2];
-    ZLink<float> ul[2];
-    const int ks[2] = {ka, kb};
-    for (int i = 0; i < 2; ++i) {
-      RhsSlot* o = slot_of(ks[i]);
-      u[i] = o ? o->eu[0].p : L.eu.p;
-      f[i] = o ? o->ef[0].p : L.ef.p;
-      y[i] = o ? o->er[0].p : L.er.p;
-      ul[i] = o ? o->eul[0] : L.eul;
-    }
-    ProfScope p(s_, "l0_residual_f32", 2.0 * resid_l0_bytes(L.g, 4, 4, true) - 4.0 * double(L.g.nv));
-    launch_l0_residual_pair(L.g, coeff_.p, L.sharded ? coeff_l_ : ZLink<float>{}, u, ul, f, y, s_);
-    ++launches_;
-  }
-}
-
-// Level-0 GS sweeps of the active RHSs of a group in one launch per colour (gs_group_kernels.cu).
-template <typename T>
-void Hierarchy<T>::relax_l0_group(int G, const bool* act, int sweeps, bool zero_start) {
-  Level& L = levels_[0];
-  float* u[kMaxRhsGroup];
-  const float* f[kMaxRhsGroup];
-  ZLink<float> ul[kMaxRhsGroup];
-  int nr = 0;
-  for (int k = 0; k < G; ++k)
-    if (act[k]) {
-      RhsSlot* o = slot_of(k);
-      u[nr] = o ? o->eu[0].p : L.eu.p;
-      f[nr] = o ? o->ef[0].p : L.ef.p;
-      ul[nr] = o ? o->eul[0] : L.eul;
-      ++nr;
-    }
-  if (nr == 0) return;
-  for (int sw = 0; sw < sweeps; ++sw)
-    for (int c = 0; c < 8; ++c) {
-      if (L.sharded) sync();
-      const bool zs = zero_start && sw == 0;
-      ProfScope p(s_, "l0_gs_f32", zs ? gs_l0_bytes_zs(L.g, c, 4.0 * nr, 4) : gs_l0_bytes(L.g, c, 4.0 * nr, 4));
-      if constexpr (std::is_same_v<T, float>)
-        launch_l0_gs_group(L.g, coeff_.p, L.sharded ? coeff_l_ : ZLink<float>{}, nr, f, u, ul, c, zs, s_);
-      ++launches_;
-    }
-}
-
 template <typename T>
 void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
-  const bool g0 = std::is_same_v<T, float> && l0_gs_group_ok(levels_[0].g);
-  if (g0) {  // level 0 down: grouped pre-smoothing, then residual + restriction per RHS
-    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(0);
-    if (!zs)
-      for (int k = 0; k < G; ++k)
-        if (act[k]) {
-          select_rhs(k);
-          IHOM_CUDA(cudaMemsetAsync(levels_[0].eu.p, 0, sizeof(float) * 3 * levels_[0].g.nv, s_));
-          ++launches_;
-        }
-    relax_l0_group(G, act, opts.pre_sweeps, zs);
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        select_rhs(k);
-        residual_f32(0);
-        restrict_to_f32(0);
-      }
-  } else if (std::is_same_v<T, float> && l0_residual_pair_ok(levels_[0].g)) {
-    // per-RHS pre-smoothing; the inner residuals two RHSs per paired element sweep; restriction per RHS
-    int list[kMaxRhsGroup], na = 0;
-    const bool zs = opts.pre_sweeps > 0 && zero_start_ok(0);
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        list[na++] = k;
-        select_rhs(k);
-        if (!zs) {
-          IHOM_CUDA(cudaMemsetAsync(levels_[0].eu.p, 0, sizeof(float) * 3 * levels_[0].g.nv, s_));
-          ++launches_;
-        }
-        relax_f32(0, opts.pre_sweeps, false, zs);
-      }
-    for (int i = 0; i < na; i += 2) {
-      if (i + 1 < na) {
-        residual_f32_l0_pair(list[i], list[i + 1]);
-      } else {
-        select_rhs(list[i]);
-        residual_f32(0);
-      }
+  for (int k = 0; k < G; ++k)  // level 0 down, per RHS
+    if (act[k]) {
+      select_rhs(k);
+      inner_down(0, opts);
     }
-    for (int i = 0; i < na; ++i) {
-      select_rhs(list[i]);
-      restrict_to_f32(0);
-    }
-  } else {
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        select_rhs(k);
-        inner_down(0, opts);
-      }
-  }
   for (int l = 1; l < lmax; ++l) {
     const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
     if (!zs)
@@ -1374,9 +1250,8 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
     if (act[k]) {
       select_rhs(k);
       inner_prolong(0);
-      if (!g0) relax_f32(0, opts.post_sweeps, false);
+      relax_f32(0, opts.post_sweeps, false);
     }
-  if (g0) relax_l0_group(G, act, opts.post_sweeps, false);
 }
 
 template <typename T>

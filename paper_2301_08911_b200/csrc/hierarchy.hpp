@@ -272,8 +272,6 @@ class Hierarchy {
   void inner_coarsest();
   void inner_vcycle_group(int G, const SolverOptions& opts, const bool* act);
   void relax_f32_group(int G, int l, int sweeps, bool zero_start);
-  void relax_l0_group(int G, const bool* act, int sweeps, bool zero_start);
-  void residual_f32_l0_pair(int ka, int kb);
   void residual_f32_group(int G, int l);
   double finish_defect_cycle();  // u += e (fused or not), the new residual; returns ||r||
   double* u0_bound_ = nullptr;

@@ -424,17 +424,4 @@ static long long launch_hsweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, 
 
 }  // namespace ihomgpu
 
-namespace ihomgpu {
-// Inner f32 residuals y_k = f_k - K u_k of two right-hand sides in one paired element sweep (NP = 2).
-// Off by default: 512^3 inner residual 35.6 -> 30.9 ms per iteration (0.5% of the iteration), and
-// whole solves differ from the single sweeps at ~3e-11 relative in C^H although every lane should
-// round like the scalar path -- not isolated yet, so the knob stays opt-in.
-bool l0_residual_pair_ok(const GridGeo& g) { return knob("HSWEEP_PAIR", 0) != 0 && hsweep_ok(g, true); }
 
-void launch_l0_residual_pair(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* const u[2],
-                             const ZLink<float> ul[2], const float* const f[2], float* const y[2], cudaStream_t s) {
-  launch_hsweep<float, float, kSwResidual, false, 2>(g, coeff, resolve(cl, coeff), u[0], resolve(ul[0], u[0]), f[0],
-                                                    y[0], nullptr, nullptr, nullptr, {}, nullptr, s, u[1],
-                                                    resolve(ul[1], u[1]), f[1], y[1]);
-}
-}  // namespace ihomgpu

@@ -35,9 +35,7 @@ template <typename TC, typename TN, typename TA>
 void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, int color, cudaStream_t s,
                         ZLink<TC> cl = {}, ZLink<TN> ul = {}, bool zero_start = false);
 // fused pass of colours ca and ca ^ 1 (f32 inner fields): one CTA per row, bit-identical to the two passes
-bool l0_gs_cpair_ok(const GridGeo& g);
-void launch_l0_gs_cpair(const GridGeo& g, const float* coeff, const float* f, float* u, int ca, cudaStream_t s,
-                        ZLink<float> cl = {}, ZLink<float> ul = {}, bool zero_start = false);
+
 // true if launch_l0_gs_color takes the zero-start path on this grid (it then never reads colours > c
 // during the first sweep, so u need not be cleared before it)
 template <typename TC, typename TN, typename TA>
@@ -85,15 +83,6 @@ void launch_stencil_gs_color(const GridGeo& g, const TS* st, const TN* f, TN* u,
 // the same for nl = 1, 2, 3 or 6 right-hand sides in lockstep (each stencil block read once for all;
 // per-RHS arithmetic identical to the single launches)
 constexpr int kMaxRhsGroup = 6;
-// level-0 f32 GS colour pass for nr <= 6 right-hand sides in lockstep (gs_group_kernels.cu): the
-// coefficient-side work of a vertex is shared by the group
-bool l0_gs_group_ok(const GridGeo& g);
-// level-0 inner f32 residuals of two RHSs in one paired element sweep (hsweep_kernels.cuh, knob HSWEEP_PAIR)
-bool l0_residual_pair_ok(const GridGeo& g);
-void launch_l0_residual_pair(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* const u[2],
-                             const ZLink<float> ul[2], const float* const f[2], float* const y[2], cudaStream_t s);
-void launch_l0_gs_group(const GridGeo& g, const float* coeff, ZLink<float> cl, int nr, const float* const* f,
-                        float* const* u, const ZLink<float>* ul, int color, bool zero_start, cudaStream_t s);
 template <typename TS, typename TN>
 void launch_stencil_apply_group(const GridGeo& g, const TS* st, int nl, const TN* const* x, const TN* const* f,
                                 TN* const* y, cudaStream_t s, const ZLink<TN>* xl);

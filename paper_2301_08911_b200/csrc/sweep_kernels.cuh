@@ -336,212 +336,9 @@ bool sweep2_ok(const GridGeo& g) {
          g.n[2] >= 4;
 }
 
-// ---------------------------------------------------------------- x-paired f32 Gauss-Seidel colour pass
-// Colour c = (o0, o1, o2). Thread (tx, ty) updates the two colour-c vertices at
-// halved (H0 + tx, H1 + ty) and (H0 + 32 + tx, H1 + ty) of every halved plane of
-// its z range. The window of a plane (all colours) is held in shared memory
-// split by x parity so that for 32 consecutive lanes every neighbour operand is
-// a conflict-free LDS.64 of a {lower half, upper half} float2 at a
-// compile-time offset:  [row 0..2TY][x parity p][half column 0..32][comp] float2,
-// actual x = 2 H0 + o0 - 1 + 2 hc + p (+ 64 for the upper lane). A 5-slot
-// ring keeps planes z-1, z, z+1 while z+2, z+3 stream in (the next vertex plane
-// of this colour is z+2); elements use a 4-slot ring (planes z-1, z per step).
-// Same-colour vertices never neighbour each other, so the pass updates u in
-// place without hazards. ZC >= 0: zero-start pass -- the colours > ZC are
-// neither loaded nor multiplied (identical results, common.cuh zero_start_mask).
-constexpr int kGsTY = 4;                                   // halved rows per CTA
-constexpr int kGsRows = 2 * kGsTY + 1;                     // window rows (actual)
-constexpr int kGsHC = kSwTX + 1;                           // half columns per parity (33)
-constexpr int kGsUSlot = kGsRows * 2 * kGsHC * 3;          // float2 per plane slot
-constexpr int kGsERows = 2 * kGsTY;
-constexpr int kGsESlot = kGsERows * 2 * kSwTX;             // float2 per element plane slot
-constexpr int kGsThreads = kSwTX * kGsTY;
-constexpr int kGsUItems = kGsRows * 2 * kGsHC * 2;         // window vertices per plane (both lanes)
-constexpr int kGsEItems = kGsERows * 2 * kSwTX * 2;        // window elements per plane (both lanes)
-constexpr int kGsUPer = (kGsUItems + kGsThreads - 1) / kGsThreads;
-constexpr int kGsEPer = (kGsEItems + kGsThreads - 1) / kGsThreads;
-constexpr size_t kGsSmem = sizeof(float2) * (5 * kGsUSlot + 4 * kGsESlot);
-
-// grid = (d0 / 64, d1 / TY, d2 / TZh); block = (32, TY)
-template <int ZC>
-__global__ void __launch_bounds__(kGsThreads, 2)
-    l0_gs_sweep_kernel(GridGeo g, const float* __restrict__ coeff, ZLink<float> cl, const float* __restrict__ f,
-                       float* u, ZLink<float> ul, int color, int TZh) {
-  extern __shared__ __align__(16) unsigned char gs_raw[];
-  float* us = reinterpret_cast<float*>(gs_raw);
-  float* es = reinterpret_cast<float*>(gs_raw + sizeof(float2) * 5 * kGsUSlot);
-  if constexpr (ZC >= 0) color = ZC;
-  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
-  const int o0 = color & 1, o1 = (color >> 1) & 1, o2 = (color >> 2) & 1;
-  const int H0 = blockIdx.x * 2 * kSwTX, H1 = blockIdx.y * kGsTY, Z0h = blockIdx.z * TZh;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSwTX + tx;
-  const int t = g.n[2];
-  const unsigned plane = (unsigned)g.cd[0][0] * (unsigned)g.cd[0][1];
-  const int xs = 2 * H0 + o0 - 1, ys = 2 * H1 + o1 - 1;  // window origin (actual)
-  // loader bookkeeping: item -> smem float index, xy part of the location in even / odd z planes,
-  // and the colour's x/y bits (a zero-start pass skips the items of colours > c)
-  unsigned uE[kGsUPer], uO[kGsUPer];
-  int uS[kGsUPer], uXY[kGsUPer];
-#pragma unroll
-  for (int r = 0; r < kGsUPer; ++r) {
-    const int v = tid + r * kGsThreads;
-    uS[r] = -1;
-    if (v < kGsUItems) {
-      const int h = v & 1, w = v >> 1;
-      const int hc = w % kGsHC, rest = w / kGsHC, p = rest & 1, row = rest >> 1;
-      if (p == 1 && hc == kSwTX) continue;  // odd parity has 32 half columns
-      const int x = wrapc(xs + 2 * hc + p + 2 * kSwTX * h, g.n[0]), yy = wrapc(ys + row, g.n[1]);
-      uS[r] = 2 * 3 * ((row * 2 + p) * kGsHC + hc) + h;
-      uE[r] = vloc(g, x, yy, 0);
-      uO[r] = vloc(g, x, yy, 1);
-      uXY[r] = (x & 1) | ((yy & 1) << 1);
-    }
-  }
-  unsigned eXY[kGsEPer];
-  int eS[kGsEPer];
-#pragma unroll
-  for (int r = 0; r < kGsEPer; ++r) {
-    const int v = tid + r * kGsThreads;
-    eS[r] = -1;
-    if (v < kGsEItems) {
-      const int h = v & 1, w = v >> 1;
-      const int hc = w % kSwTX, rest = w / kSwTX, p = rest & 1, row = rest >> 1;
-      const int x = wrapc(xs + 2 * hc + p + 2 * kSwTX * h, g.n[0]), yy = wrapc(ys + row, g.n[1]);
-      eS[r] = 2 * ((row * 2 + p) * kSwTX + hc) + h;
-      eXY[r] = (unsigned)x + (unsigned)g.n[0] * (unsigned)yy;
-    }
-  }
-  const unsigned eplane = (unsigned)g.n[0] * (unsigned)g.n[1];
-  // plane index P = z - (2 Z0h + o2 - 1) -> slot P % 5; z in local coordinates, may be -1 or t
-  auto load_u = [&](int zl, int slot) {
-    const float* src = zl < 0 ? ul.lo : (zl >= t ? ul.hi : u);
-    const int z = zl < 0 ? zl + t : (zl >= t ? zl - t : zl);
-    const unsigned zoff = (unsigned)(z >> 1) * plane;
-    float* dst = us + slot * (2 * kGsUSlot);
-#pragma unroll
-    for (int r = 0; r < kGsUPer; ++r) {
-      if (uS[r] < 0) continue;
-      if constexpr (ZC >= 0) {
-        if ((uXY[r] | ((z & 1) << 2)) > ZC) continue;  // a colour not yet updated in this sweep: zero
-      }
-      const float* sp = src + 3 * (size_t)((z & 1 ? uO[r] : uE[r]) + zoff);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) __pipeline_memcpy_async(dst + uS[r] + 2 * c, sp + c, sizeof(float));
-    }
-  };
-  auto load_e = [&](int ezl, int slot) {
-    const float* src = ezl < 0 ? cl.lo : coeff;
-    const int ez = ezl < 0 ? ezl + t : ezl;
-    float* dst = es + slot * (2 * kGsESlot);
-#pragma unroll
-    for (int r = 0; r < kGsEPer; ++r)
-      if (eS[r] >= 0) __pipeline_memcpy_async(dst + eS[r], src + eXY[r] + (size_t)ez * eplane, sizeof(float));
-  };
-  const int zb = 2 * Z0h + o2;  // first vertex plane
-  load_u(zb - 1, 0);
-  load_u(zb, 1);
-  load_u(zb + 1, 2);
-  load_e(zb - 1, 0);
-  load_e(zb, 1);
-  __pipeline_commit();
-  const int xa = 2 * (H0 + tx) + o0, xb = xa + 2 * kSwTX, yv = 2 * (H1 + ty) + o1;
-  const unsigned oEa = vloc(g, xa, yv, o2), oEb = vloc(g, xb, yv, o2);  // halved z 0 of colour c
-  const float2* U2 = reinterpret_cast<const float2*>(us);
-  const float2* E2 = reinterpret_cast<const float2*>(es);
-  const int ubase = 3 * ((2 * ty + 1) * 2 * kGsHC + tx);  // own row, parity 0, half column tx
-  const int ebase = (2 * ty) * 2 * kSwTX + tx;            // element row y-1, parity 0, half column tx
-  __pipeline_wait_prior(0);
-  __syncthreads();
-  for (int k = 0; k < TZh; ++k) {
-    const int z = zb + 2 * k;
-    if (k + 1 < TZh) {  // planes z+2, z+3 and element planes z+1, z+2 for the next vertex plane
-      load_u(z + 2, (2 * k + 3) % 5);
-      load_u(z + 3, (2 * k + 4) % 5);
-      load_e(z + 1, (2 * k + 2) & 3);
-      load_e(z + 2, (2 * k + 3) & 3);
-    }
-    __pipeline_commit();
-    const float2* p0 = U2 + ((2 * k) % 5) * kGsUSlot + ubase;      // plane z-1
-    const float2* p1 = U2 + ((2 * k + 1) % 5) * kGsUSlot + ubase;  // plane z
-    const float2* p2 = U2 + ((2 * k + 2) % 5) * kGsUSlot + ubase;  // plane z+1
-    const float2* e0 = E2 + ((2 * k) & 3) * kGsESlot + ebase;      // element plane z-1
-    const float2* e1 = E2 + ((2 * k + 1) & 3) * kGsESlot + ebase;  // element plane z
-    float2 q[8];
-#pragma unroll
-    for (int ke = 0; ke < 8; ++ke)  // element (x-1+b0, y-1+b1, z-1+b2): parity b0 at half column tx
-      q[ke] = ((ke >> 2) & 1 ? e1 : e0)[(((ke >> 1) & 1) * 2 + (ke & 1)) * kSwTX];
-    auto U = [&](int n, int c) -> float2 {
-      const int t0 = n % 3 - 1, t1 = (n / 3) % 3 - 1, t2 = n / 9;
-      const float2* pp = t2 == 0 ? p0 : (t2 == 1 ? p1 : p2);
-      // (t0, t1): row + t1; t0 = 0 -> parity 1, column tx; t0 = -1 -> parity 0, tx; t0 = +1 -> parity 0, tx+1
-      return pp[3 * ((t1 * 2 + (t0 == 0 ? 1 : 0)) * kGsHC + (t0 == 1 ? 1 : 0)) + c];
-    };
-    float2 m[3], S[9];
-    ku_vertex_split_z<ZM, float2>(q, kappa<float>(), U, m, S);
-    const unsigned zoff = (unsigned)(z >> 1) * plane;
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const size_t loc = (v == 0 ? oEa : oEb) + zoff;
-      float sblk[9], rhs[3], out[3];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) sblk[e] = v == 0 ? S[e].x : S[e].y;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) rhs[c] = f[3 * loc + c] - (v == 0 ? m[c].x : m[c].y);
-      solve3<float>(sblk, rhs, out);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) u[3 * loc + c] = out[c];
-    }
-    __pipeline_wait_prior(0);
-    __syncthreads();
-  }
-}
-
 }  // namespace ihomgpu
 #include "hsweep_kernels.cuh"  // sum-factorised element sweep (uses SweepOut / wrapc above)
 namespace ihomgpu {
-
-// Off by default: measured 1.16 ms per pass at 512^3 vs 0.66 for l0_gs_fast2 (224 registers leave
-// 8 warps per SM and the one-step cp.async prefetch cannot hide the load latency; profiles/
-// kernel_variants_r01.md). Kept as the starting point for a warp-specialised (TMA producer) version.
-bool gs_sweep_ok(const GridGeo& g) {
-  return knob("L0_GS_SWEEP", 0) != 0 && fast_ok(g) && g.cd[0][0] % (2 * kSwTX) == 0 && g.cd[0][1] % kGsTY == 0 &&
-         g.cd[0][2] >= 2;
-}
-
-template <int ZC>
-static void launch_gs_sweep_zc(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
-                               ZLink<float> ul, int color, cudaStream_t s) {
-  const long long cols = (long long)(g.cd[0][0] / (2 * kSwTX)) * (g.cd[0][1] / kGsTY);
-  int tzh = g.cd[0][2];
-  while (tzh % 2 == 0 && tzh > 8 && cols * (g.cd[0][2] / tzh) < 148LL * 2 * 4) tzh /= 2;
-  const dim3 gr(g.cd[0][0] / (2 * kSwTX), g.cd[0][1] / kGsTY, g.cd[0][2] / tzh);
-  static bool attr = false;
-  if (!attr) {
-    IHOM_CUDA(cudaFuncSetAttribute((const void*)l0_gs_sweep_kernel<ZC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kGsSmem));
-    attr = true;
-  }
-  l0_gs_sweep_kernel<ZC><<<gr, dim3(kSwTX, kGsTY), kGsSmem, s>>>(g, coeff, cl, f, u, ul, color, tzh);
-}
-
-void launch_l0_gs_sweep(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
-                        ZLink<float> ul, int color, bool zero_start, cudaStream_t s) {
-  if (!zero_start) {
-    launch_gs_sweep_zc<-1>(g, coeff, cl, f, u, ul, color, s);
-  } else {
-    switch (color) {
-      case 0: launch_gs_sweep_zc<0>(g, coeff, cl, f, u, ul, color, s); break;
-      case 1: launch_gs_sweep_zc<1>(g, coeff, cl, f, u, ul, color, s); break;
-      case 2: launch_gs_sweep_zc<2>(g, coeff, cl, f, u, ul, color, s); break;
-      case 3: launch_gs_sweep_zc<3>(g, coeff, cl, f, u, ul, color, s); break;
-      case 4: launch_gs_sweep_zc<4>(g, coeff, cl, f, u, ul, color, s); break;
-      case 5: launch_gs_sweep_zc<5>(g, coeff, cl, f, u, ul, color, s); break;
-      case 6: launch_gs_sweep_zc<6>(g, coeff, cl, f, u, ul, color, s); break;
-      default: launch_gs_sweep_zc<7>(g, coeff, cl, f, u, ul, color, s); break;
-    }
-  }
-  IHOM_LAUNCH_CHECK();
-}
 
 bool sweep_ok(const GridGeo& g) {
   return knob("L0_SWEEP", 1) != 0 && g.n[0] % kSwTX == 0 && g.n[1] % kSwTY == 0 && g.n[2] % 2 == 0 && g.n[2] >= 4 &&

@@ -264,6 +264,60 @@ def test_radial_filter(ih, orc, kernel, radius):
     assert rel(ih.radial_filter(n, f, radius, kernel), orc.radial_filter(n, f, radius, kernel)) < 1e-14
 
 
+@pytest.mark.parametrize("n", [(8, 6, 12), (16, 16, 16), (12, 10, 8)])
+@pytest.mark.parametrize("kernel", ["linear", "spline4"])
+def test_radial_filter_four_plane_path(ih, orc, n, kernel):
+    """nz % 4 == 0 grids take the four-z-planes-per-thread filter (FILTER_NZ, default on): it equals the
+    one-plane kernel bit for bit and the oracle to 1e-14."""
+    m = int(np.prod(n))
+    f = mt_uniform(m, 37, 0, 1)
+    a = ih.radial_filter(n, f, 2.0, kernel)
+    ih.set_knob("FILTER_NZ", 0)
+    try:
+        b = ih.radial_filter(n, f, 2.0, kernel)
+    finally:
+        ih.set_knob("FILTER_NZ", 1)
+    np.testing.assert_array_equal(a, b)
+    assert rel(a, orc.radial_filter(n, f, 2.0, kernel)) < 1e-14
+
+
+def _ulps(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.max(np.abs(a - b) / np.spacing(np.maximum(np.abs(b), 1e-300)))
+
+
+@pytest.mark.parametrize("p", [1.0, 2.0, 3.0, 4.0, 2.5])
+@pytest.mark.parametrize("radius", [None, 2.0])
+def test_density_expr_eval_backward(ih, orc, p, radius):
+    """DensityExpr eval / backward on the device (src/density.cpp:65-83): pre = filter(design) (or the
+    design), out = pre^p; backward = filter(g p pre^(p-1)). Integer exponents use repeated
+    multiplication (POW_INT) -- within 2 ulp of std::pow (numpy's pow is the same libm call); the
+    fractional exponent goes through pow and the filter is the oracle's to 1e-14."""
+    n = (8, 10, 12)
+    m = int(np.prod(n))
+    design = mt_uniform(m, 41, 1e-3, 1.0)
+    g = mt_uniform(m, 43, -1.0, 1.0)
+    de = ih.DensityExpr(radius, "spline4", p)
+    out = de.eval(n, design)
+    pre = orc.radial_filter(n, design, radius, "spline4") if radius else design
+    assert rel(de._pre, pre) < 1e-14
+    assert _ulps(out, np.asarray(de._pre) ** p) <= 2  # repeated products / device pow vs glibc pow
+    back = de.backward(g)
+    gp = g * p * pre ** (p - 1.0)
+    expect = orc.radial_filter(n, gp, radius, "spline4") if radius else gp
+    assert rel(back, expect) < 1e-14
+    if p == int(p):  # POW_INT against std::pow, bitwise structure of the off switch
+        ih.set_knob("POW_INT", 0)
+        try:
+            de0 = ih.DensityExpr(radius, "spline4", p)
+            out0 = de0.eval(n, design)
+        finally:
+            ih.set_knob("POW_INT", 1)
+        assert _ulps(out, out0) <= 2
+        if radius is None:
+            assert _ulps(out0, pre ** p) <= 1  # CUDA pow vs glibc pow
+
+
 @pytest.mark.parametrize("sym", ["reflect3", "reflect6", "rotate3"])
 @pytest.mark.parametrize("n", [8, 16, 24, 12, (7, 9, 11)])
 def test_symmetrize(ih, orc, sym, n):

@@ -1,9 +1,6 @@
-"""Kernel variants are bit-identical, except the sum-factorised sweep (tolerance).
-
-The paired level-0 f32 kernels (two z-stacked vertices per thread in float2
-FFMA2/FADD2/FMUL2 arithmetic) must reproduce the scalar kernels bit for bit:
-each lane rounds exactly like the scalar instruction. The f32 level-0 kernels
-run inside the mixed_defect inner cycle, so whole cell solves are compared.
+"""Kernel variants that stay in the library are bit-identical to their reference forms,
+except the sum-factorised sweep (tolerance). The f32 level-0 kernels run inside the mixed_defect inner
+cycle, so whole cell solves are compared.
 """
 import numpy as np
 import pytest
@@ -14,7 +11,7 @@ pytestmark = pytest.mark.gpu
 def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
     # the bitwise comparisons below are between stencil-form variants: the sum-factorised element
     # sweep (HSWEEP*, a different association of the same sums) is compared at tolerance separately
-    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "L0_GROUP": 0, "STENCIL_F32": 0, "TRANSFER_F32": 0, **knobs}
+    knobs = {"HSWEEP": 0, "HSWEEP32": 0, "STENCIL_F32": 0, "TRANSFER_F32": 0, **knobs}
     for k, v in knobs.items():
         ih.set_knob(k, v)
     rho, _ = ih.init_trig(n if np.isscalar(n) else n[0], 2, 0, 0.3) if np.isscalar(n) else (None, None)
@@ -45,47 +42,20 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         hom.close()
         return out
     finally:
-        ih.set_knob("L0_PAIR", 0)
-        ih.set_knob("PAIR_MINB", 3)
         ih.set_knob("L0_SWEEP", 1)
         ih.set_knob("L0_SWEEP2", 1)
         ih.set_knob("ZERO_START", 1)
-        ih.set_knob("L0_GS_SWEEP", 0)
-        ih.set_knob("L0_CPAIR", 0)
         ih.set_knob("SUBMEANS_FLAT", 1)
         ih.set_knob("FUSED_UPDATE", 1)
-        ih.set_knob("GS_COL", 0)
         ih.set_knob("RHS_PAIRS", 1)
         ih.set_knob("RHS_GROUP", 0)
         ih.set_knob("HSWEEP", 1)
         ih.set_knob("HSWEEP32", 1)
-        ih.set_knob("L0_GROUP", 0)
-        ih.set_knob("HSWEEP_PAIR", 0)
         ih.set_knob("HBM_LIMIT_MB", 0)
         ih.set_knob("STENCIL_F32", 1)
         ih.set_knob("TRANSFER_F32", 1)
         ih.set_knob("PROJECT_NORM", 1)
         ih.set_knob("STENCIL_STREAM", 1)
-
-
-@pytest.mark.parametrize("n", [16, 32, (16, 16, 10)])
-def test_paired_level0_kernels_bit_identical(ih, n):
-    base = _solve(ih, n, {"L0_PAIR": 0, "L0_CPAIR": 0})
-    for minb in (3, 4):
-        pair = _solve(ih, n, {"L0_PAIR": 1, "PAIR_MINB": minb, "L0_CPAIR": 0})
-        assert pair[0] == base[0]
-        np.testing.assert_array_equal(pair[1], base[1])
-        for a, b in zip(pair[2], base[2]):
-            np.testing.assert_array_equal(a, b)
-
-
-def test_paired_level0_kernels_bit_identical_on_slabs(ih):
-    base = _solve(ih, 32, {"L0_PAIR": 0, "L0_CPAIR": 0}, fabric_p=2)
-    pair = _solve(ih, 32, {"L0_PAIR": 1, "L0_CPAIR": 0}, fabric_p=2)
-    assert pair[0] == base[0]
-    np.testing.assert_array_equal(pair[1], base[1])
-    for a, b in zip(pair[2], base[2]):
-        np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("precision", ["mixed", "double"])
@@ -165,20 +135,17 @@ def test_zero_start_sweeps_bit_identical_on_slabs(ih):
         np.testing.assert_array_equal(a, b)
 
 
-BASE = {"L0_SWEEP": 0, "L0_GS_SWEEP": 0, "ZERO_START": 0, "L0_PAIR": 0, "L0_CPAIR": 0}
+BASE = {"L0_SWEEP": 0, "ZERO_START": 0}
 VARIANTS = [
-    {"L0_GS_SWEEP": 1, "ZERO_START": 0, "L0_SWEEP": 0},
-    {"L0_GS_SWEEP": 1, "ZERO_START": 1, "L0_SWEEP": 0},
-    {"L0_CPAIR": 1, "ZERO_START": 0},
-    {"L0_CPAIR": 1, "ZERO_START": 1},
-    {"L0_GS_SWEEP": 0, "ZERO_START": 1, "L0_SWEEP": 1, "L0_SWEEP2": 1, "L0_CPAIR": 0},  # the default configuration
+    {"ZERO_START": 1, "L0_SWEEP": 0},
+    {"ZERO_START": 1, "L0_SWEEP": 1, "L0_SWEEP2": 1},  # the default configuration
 ]
 
 
 @pytest.mark.parametrize("precision,mode", [("mixed", "mixed_defect"), ("mixed", "pcg"), ("mixed", "vcycle")])
 @pytest.mark.parametrize("n", [32, 128, (128, 64, 64)])
 def test_gs_sweep_bit_identical(ih, n, precision, mode):
-    """Level-0 f32 Gauss-Seidel as an x-paired z-plane sweep (plain and zero-start) == direct-load kernels."""
+    """Zero-start GS passes and z-plane residual sweeps (the defaults) == plain direct-load kernels."""
     base = _solve(ih, n, BASE, precision=precision, mode=mode)
     for knobs in VARIANTS:
         v = _solve(ih, n, {**BASE, **knobs}, precision=precision, mode=mode)
@@ -238,18 +205,6 @@ def test_fused_update_bit_identical(ih, n, P):
         np.testing.assert_array_equal(a, b)
 
 
-@pytest.mark.parametrize("kz", [2, 4, 8])
-@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
-def test_column_gs_bit_identical(ih, kz, n, P):
-    """Column-marching level-0 GS (KZ vertices per thread, carried neighbour plane) == two-vertex kernel."""
-    base = _solve(ih, n, {"GS_COL": 0}, fabric_p=P)
-    v = _solve(ih, n, {"GS_COL": kz}, fabric_p=P)
-    assert v[0] == base[0]
-    np.testing.assert_array_equal(v[1], base[1])
-    for a, b in zip(v[2], base[2]):
-        np.testing.assert_array_equal(a, b)
-
-
 @pytest.mark.parametrize("n,P", [(16, 0), (32, 0), (64, 0), ((64, 32, 48), 0), (32, 2), (64, 4)])
 def test_rhs_pairs_bit_identical(ih, n, P):
     """Cell problems solved in lockstep pairs (coarse stencils streamed once per pair) == one by one:
@@ -276,35 +231,6 @@ def test_hadamard_sweep_matches_stencil_sweep(ih, n):
         assert np.abs(h[1] - base[1]).max() <= tol * np.abs(base[1]).max()
         for a, b in zip(h[2], base[2]):
             assert np.linalg.norm(a - b) <= tol * 10 * max(np.linalg.norm(b), 1e-30)
-
-
-@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
-def test_grouped_level0_gs_matches(ih, n, P):
-    """Level-0 GS of a lockstep RHS group in one launch per colour (L0_GROUP, gs_group_kernels.cu): the
-    coefficient-side work is shared, kappa multiplies each merged coefficient (rounding-level change),
-    so whole cell solves agree with the per-RHS passes to rounding: same cycle counts, C^H to 2e-6."""
-    base = _solve(ih, n, {"L0_GROUP": 0}, fabric_p=P)
-    for group in (2, 3, 6):
-        v = _solve(ih, n, {"L0_GROUP": 1, "RHS_GROUP": group}, fabric_p=P)
-        assert v[0] == base[0], group
-        assert np.abs(v[1] - base[1]).max() <= 2e-6 * np.abs(base[1]).max()
-        for a, b in zip(v[2], base[2]):
-            assert np.linalg.norm(a - b) <= 2e-5 * max(np.linalg.norm(b), 1e-30)
-
-
-@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), (64, 2)])
-def test_paired_f32_element_sweep_bit_identical(ih, n, P):
-    """The inner f32 residuals of two RHSs of a lockstep group in one element sweep with F2 lanes
-    (HSWEEP_PAIR, opt-in) agree with one sweep per RHS for every group size (odd groups finish with a
-    single sweep): same cycle counts, C^H to 1e-9 relative (observed ~3e-11: the paired f32 residual
-    is not bitwise equal to the scalar sweep -- cause not isolated; the knob is opt-in)."""
-    for group in (2, 3, 6):
-        base = _solve(ih, n, {"HSWEEP": 1, "HSWEEP32": 1, "HSWEEP_PAIR": 0, "RHS_GROUP": group}, fabric_p=P)
-        v = _solve(ih, n, {"HSWEEP": 1, "HSWEEP32": 1, "HSWEEP_PAIR": 1, "RHS_GROUP": group}, fabric_p=P)
-        assert v[0] == base[0], group
-        assert np.abs(v[1] - base[1]).max() <= 1e-9 * np.abs(base[1]).max()
-        for a, b in zip(v[2], base[2]):
-            assert np.linalg.norm(a - b) <= 1e-6 * max(np.linalg.norm(b), 1e-30)
 
 
 @pytest.mark.parametrize("P", [0, 2])

@@ -187,6 +187,14 @@ def workload(args):
             if args.gpus > 1 else "single GPU"}
 
 
+def memory_plans(args, world):
+    """Per-GPU HBM estimates (paper_2301_08911_b200.distributed.memory_plan) for this run and for the
+    1024^3 config at 1/2/4/8 z-slabs with the minimal levers (no lockstep group, no energy cache)."""
+    from paper_2301_08911_b200 import distributed as dd
+    return {"this_run_min": dd.memory_plan(args.reso, world),
+            "1024^3": [dd.memory_plan(1024, n) for n in (1, 2, 4, 8)]}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -334,6 +342,7 @@ def run_ours(args):
             "hbm_used_gb_per_gpu": round(hbm_used_gb, 2),
             "cycles_per_iteration": [r["cycles"] for r in recs],
             "objective": [r["objective"] for r in recs], "restarts": restarts,
+            "memory_plan_estimate": memory_plans(args, world),
             "iterations_per_step": 1 if args.no_e2e else 2, "kernels": kernels}
     if t_e2e is not None:
         moved = 8 * (args.reso ** 3 if fab is not None else m)  # whole job: every rank moves its slab

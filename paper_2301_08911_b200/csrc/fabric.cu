@@ -12,25 +12,47 @@
 namespace ihomgpu {
 
 // ---------------------------------------------------------------- kernels
-// Arrive (release at system scope so peers reading this rank's memory over
-// NVLink see everything the stream wrote before), then wait for every rank.
-__global__ void signal_wait_kernel(unsigned long long* own, PeerTable flags, int nranks, unsigned long long epoch) {
+struct WaitList {
+  int r[kMaxRanks];
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Arrive (release at system scope so peers reading this rank's memory over NVLink see everything the stream
+// wrote before), then wait for the listed ranks -- bounded: after timeout_ns the wait gives up, records the
+// rank it waited on in *err and returns; once *err is set this rank's barriers no longer wait.
+__global__ void signal_wait_kernel(unsigned long long* own, PeerTable flags, WaitList wl, int nwait,
+                                   unsigned long long epoch, unsigned long long* err, unsigned long long timeout_ns) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(own), "l"(epoch) : "memory");
-  for (int r = 0; r < nranks; ++r) {
-    const unsigned long long* f = static_cast<const unsigned long long*>(flags.p[r]);
+  if (*err != 0ull) return;
+  const unsigned long long t0 = globaltimer_ns();
+  for (int i = 0; i < nwait; ++i) {
+    const unsigned long long* f = static_cast<const unsigned long long*>(flags.p[wl.r[i]]);
     unsigned long long v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-      if (v < epoch) __nanosleep(200);
-    } while (v < epoch);
+      if (v >= epoch) break;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        *err = 1ull + (unsigned long long)wl.r[i];
+        return;
+      }
+      __nanosleep(200);
+    }
   }
   __threadfence_system();
 }
 
-void launch_signal_wait(unsigned long long* own, PeerTable flags, int nranks, unsigned long long epoch,
+void launch_signal_wait(unsigned long long* own, PeerTable flags, const int* wait_on, int nwait,
+                        unsigned long long epoch, unsigned long long* err, unsigned long long timeout_ns,
                         cudaStream_t s) {
-  signal_wait_kernel<<<1, 1, 0, s>>>(own, flags, nranks, epoch);
+  WaitList wl{};
+  for (int i = 0; i < nwait; ++i) wl.r[i] = wait_on[i];
+  signal_wait_kernel<<<1, 1, 0, s>>>(own, flags, wl, nwait, epoch, err, timeout_ns);
   IHOM_LAUNCH_CHECK();
 }
 
@@ -114,7 +136,8 @@ std::vector<void*> LocalFabric::exchange(int rank, void* local) {
   return out;
 }
 
-void LocalFabric::barrier(int rank, cudaStream_t s) {
+void LocalFabric::barrier(int rank, cudaStream_t s, bool halo) {
+  (void)halo;  // one process: the host barrier orders every slab anyway
   if (n_ == 1) return;
   IHOM_CUDA(cudaEventRecord(ev_[size_t(rank)], s));
   host_barrier();  // every rank's record is enqueued
@@ -131,6 +154,9 @@ IpcFabric::IpcFabric(int rank, int nranks, int device, HostAllgather ag, void* u
   IHOM_CUDA(cudaSetDevice(device));
   IHOM_CUDA(cudaMalloc(&flag_, sizeof(unsigned long long)));
   IHOM_CUDA(cudaMemset(flag_, 0, sizeof(unsigned long long)));
+  IHOM_CUDA(cudaMalloc(&err_, sizeof(unsigned long long)));
+  IHOM_CUDA(cudaMemset(err_, 0, sizeof(unsigned long long)));
+  timeout_ns_ = (unsigned long long)knob("FABRIC_TIMEOUT_S", 60) * 1000000000ull;
   const std::vector<void*> f = exchange(rank, flag_);
   for (int r = 0; r < nranks; ++r) flags_.p[r] = f[size_t(r)];
 }
@@ -139,6 +165,7 @@ IpcFabric::~IpcFabric() {
   for (auto& kv : opened_)
     if (kv.first.first != rank_) cudaIpcCloseMemHandle(kv.second);
   if (flag_) cudaFree(flag_);
+  if (err_) cudaFree(err_);
   for (auto& st : rs_)
     if (st.mailbox) cudaFree(st.mailbox);
 }
@@ -191,10 +218,29 @@ std::vector<void*> IpcFabric::exchange(int rank, void* local) {
   return out;
 }
 
-void IpcFabric::barrier(int rank, cudaStream_t s) {
+void IpcFabric::barrier(int rank, cudaStream_t s, bool halo) {
   (void)rank;
   if (n_ == 1) return;
-  launch_signal_wait(flag_, flags_, n_, ++epoch_, s);
+  int wait_on[kMaxRanks], nw = 0;
+  if (halo) {  // the z-neighbour slabs (periodic in z)
+    const int lo = (rank_ + n_ - 1) % n_, hi = (rank_ + 1) % n_;
+    wait_on[nw++] = lo;
+    if (hi != lo) wait_on[nw++] = hi;
+  } else {
+    for (int r = 0; r < n_; ++r)
+      if (r != rank_) wait_on[nw++] = r;
+  }
+  launch_signal_wait(flag_, flags_, wait_on, nw, ++epoch_, err_, timeout_ns_, s);
+}
+
+void IpcFabric::check(int rank) {
+  (void)rank;
+  unsigned long long e = 0;
+  IHOM_CUDA(cudaMemcpy(&e, err_, sizeof(e), cudaMemcpyDeviceToHost));
+  if (e)
+    throw CudaError("z-slab rank " + std::to_string(rank_) + ": barrier timed out after " +
+                    std::to_string(timeout_ns_ / 1000000000ull) + " s waiting for rank " + std::to_string(e - 1) +
+                    " (dead or diverged peer)");
 }
 
 }  // namespace ihomgpu

@@ -12,7 +12,11 @@
 //                    buffer, mapped into this rank (called in the same order
 //                    on every rank -- SPMD allocation order);
 //   barrier(s)       work enqueued on s after the barrier sees every rank's
-//                    work enqueued before its barrier;
+//                    work enqueued before its barrier (halo = true: only the
+//                    z-neighbour slabs r-1, r+1 -- enough to order halo reads
+//                    and writes, which never reach further);
+//   check()          throws if a barrier of this rank timed out (a dead or
+//                    diverged peer): barriers never spin forever;
 //   allreduce(x, n)  n doubles, sum or max, folded in rank order -- the
 //                    result is bitwise identical on every rank, so every rank
 //                    takes the same convergence / bisection decisions.
@@ -42,7 +46,8 @@ class Fabric {
   virtual ~Fabric() = default;
   int size() const { return n_; }
   virtual std::vector<void*> exchange(int rank, void* local) = 0;
-  virtual void barrier(int rank, cudaStream_t s) = 0;
+  virtual void barrier(int rank, cudaStream_t s, bool halo = false) = 0;
+  virtual void check(int rank) { (void)rank; }
   void allreduce(int rank, double* x, int n, bool is_max, cudaStream_t s);
   // per-rank mailboxes (2 slots of kMailbox doubles, alternating per allreduce)
   void init_mailboxes(int rank);
@@ -63,7 +68,7 @@ class LocalFabric : public Fabric {
   LocalFabric(int nranks, int device);
   ~LocalFabric() override;
   std::vector<void*> exchange(int rank, void* local) override;
-  void barrier(int rank, cudaStream_t s) override;
+  void barrier(int rank, cudaStream_t s, bool halo = false) override;
 
  private:
   void host_barrier();
@@ -86,13 +91,16 @@ class IpcFabric : public Fabric {
   IpcFabric(int rank, int nranks, int device, HostAllgather ag, void* user);
   ~IpcFabric() override;
   std::vector<void*> exchange(int rank, void* local) override;
-  void barrier(int rank, cudaStream_t s) override;
+  void barrier(int rank, cudaStream_t s, bool halo = false) override;
+  void check(int rank) override;
 
  private:
   int rank_, device_;
   HostAllgather ag_;
   void* user_;
   unsigned long long* flag_ = nullptr;  // own arrival counter (device)
+  unsigned long long* err_ = nullptr;   // own barrier error word (device): 0, or 1 + the rank waited on
+  unsigned long long timeout_ns_ = 0;
   PeerTable flags_{};
   unsigned long long epoch_ = 0;
   std::map<std::pair<int, std::uintptr_t>, void*> opened_;  // (rank, remote base) -> mapped base
@@ -106,8 +114,8 @@ struct Slab {
   int rank = 0;
   int nranks = 1;
   bool on() const { return fab != nullptr && nranks > 1; }
-  void sync(cudaStream_t s) const {
-    if (on()) fab->barrier(rank, s);
+  void sync(cudaStream_t s, bool halo = false) const {
+    if (on()) fab->barrier(rank, s, halo);
   }
   void allreduce(double* x, int n, bool is_max, cudaStream_t s) const {
     if (on()) fab->allreduce(rank, x, n, is_max, s);
@@ -115,7 +123,11 @@ struct Slab {
 };
 
 // Kernels (fabric.cu)
-void launch_signal_wait(unsigned long long* own, PeerTable flags, int nranks, unsigned long long epoch, cudaStream_t s);
+// Arrive with `epoch`, then wait for ranks wait_on[0..nwait) to arrive (bounded by timeout_ns; a timeout
+// sets *err and later barriers of this rank stop waiting, so the host sees the failure at its next check).
+void launch_signal_wait(unsigned long long* own, PeerTable flags, const int* wait_on, int nwait,
+                        unsigned long long epoch, unsigned long long* err, unsigned long long timeout_ns,
+                        cudaStream_t s);
 void launch_mailbox_fold(PeerTable boxes, int nranks, int n, bool is_max, double* out, cudaStream_t s);
 
 }  // namespace ihomgpu

@@ -331,6 +331,11 @@ void Hierarchy<T>::sync() {
 }
 
 template <typename T>
+void Hierarchy<T>::sync_halo() {  // a sharded level's kernel reads / overwrites only the z-neighbour slabs' planes
+  if (slab_.on()) slab_.fab->barrier(slab_.rank, s_, true);
+}
+
+template <typename T>
 void Hierarchy<T>::allreduce(double* dev, int n, bool is_max) {
   if (slab_.on()) slab_.fab->allreduce(slab_.rank, dev, n, is_max, s_);
 }
@@ -353,7 +358,7 @@ void Hierarchy<T>::restrict_to(int l, const double* r, double* f) {
   Level& F = levels_[size_t(l)];
   Level& C = levels_[size_t(l + 1)];
   const ZLink<double> rl = F.rl;
-  if (F.sharded) sync();
+  if (F.sharded) sync_halo();
   {
     ProfScope p(s_, "restrict", double(F.g.nv) * 27.0);
     if (!(F.sharded && !C.sharded)) {
@@ -371,7 +376,7 @@ template <typename T>
 void Hierarchy<T>::restrict_to_f32(int l) {
   Level& F = levels_[size_t(l)];
   Level& C = levels_[size_t(l + 1)];
-  if (F.sharded) sync();
+  if (F.sharded) sync_halo();
   {
     ProfScope p(s_, "restrict", double(F.g.nv) * 13.5);
     if (!(F.sharded && !C.sharded)) {
@@ -389,7 +394,7 @@ template <typename T>
 void Hierarchy<T>::prolong_from(int l, const double* uc, double* u, ZLink<double> cl) {
   Level& F = levels_[size_t(l)];
   Level& C = levels_[size_t(l + 1)];
-  if (F.sharded) sync();
+  if (F.sharded) sync_halo();
   {
     ProfScope p(s_, "prolong", double(F.g.nv) * 51.0);
     if (!(F.sharded && !C.sharded)) launch_prolong_add<double>(C.g, F.g, uc, u, s_, C.sharded ? cl : ZLink<double>{});
@@ -422,7 +427,7 @@ void Hierarchy<T>::set_density(const double* rho) {  // src/multigrid.cpp:263-27
     const GridGeo gc = transition ? transition_geo() : C.g;
     const GridGeo* gout = transition ? &C.g : nullptr;
     const int zoff = transition ? transition_zoff_h() : 0;
-    if (F.sharded) sync();
+    if (F.sharded) sync_halo();
     if (l == 1) {
       ProfScope p(s_, "galerkin_l1", double(g0.nv) * sizeof(T) + double(gc.nv) * 243.0 * sizeof(T));
       launch_galerkin_from_elements<T>(g0, gc, coeff_.p, C.st.p, s_, F.sharded ? coeff_l_ : ZLink<T>{}, gout, zoff);
@@ -541,6 +546,7 @@ double Hierarchy<T>::negligible_load(long long ndof) const {  // src/multigrid.c
 template <typename T>
 void Hierarchy<T>::check_error(const char* where) {
   int e = 0;
+  if (slab_.on()) slab_.fab->check(slab_.rank);  // a timed-out barrier (dead or diverged peer) surfaces here
   if (slab_.on()) {  // collective: every slab throws together (or none does)
     launch_int_to_double(err_.p, ws_.scalars + 60, s_);
     allreduce(ws_.scalars + 60, 1, true);
@@ -653,7 +659,7 @@ void Hierarchy<T>::relax(int l, int sweeps, bool zero_start) {  // src/multigrid
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
-      if (L.sharded) sync();  // colour c-1 of the neighbouring slabs is final
+      if (L.sharded) sync_halo();  // colour c-1 of the neighbouring slabs is final
       const bool zs = zero_start && sw == 0;
       if (l == 0) {
         ProfScope p(s_, "l0_gs_f64", gs_l0_bytes(L.g, c, 8, sizeof(T)));
@@ -670,7 +676,7 @@ void Hierarchy<T>::relax(int l, int sweeps, bool zero_start) {  // src/multigrid
 template <typename T>
 void Hierarchy<T>::compute_residual(int l) {  // src/multigrid.cpp:410-424
   Level& L = levels_[size_t(l)];
-  if (L.sharded) sync();
+  if (L.sharded) sync_halo();
   const ZLink<double> ul = L.sharded ? ulink(l) : ZLink<double>{};
   if (l == 0) {
     ProfScope p(s_, "l0_residual_f64", resid_l0_bytes(L.g, 8, sizeof(T), true));
@@ -766,7 +772,7 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;
         if (L.g.size[c] == 0) continue;
-        if (L.sharded) sync();
+        if (L.sharded) sync_halo();
         const bool zs = zero_start && sw == 0;
         if (l == 0) {
           ProfScope p(s_, "l0_gs_f32", zs ? gs_l0_bytes_zs(L.g, c, 4, 4) : gs_l0_bytes(L.g, c, 4, 4));
@@ -786,7 +792,7 @@ template <typename T>
 void Hierarchy<T>::residual_f32(int l) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
-    if (L.sharded) sync();
+    if (L.sharded) sync_halo();
     if (l == 0) {
       ProfScope p(s_, "l0_residual_f32", resid_l0_bytes(L.g, 4, 4, true));
       launch_l0_apply<float, float, float>(L.g, coeff_.p, L.eu.p, L.ef.p, L.er.p, s_,
@@ -828,7 +834,7 @@ double Hierarchy<T>::defect_residual(bool update) {
   if constexpr (std::is_same_v<T, float>) {
     if (!npart_.p) npart_.alloc(size_t(L0.g.nv / 32 + 1024));
     long long nb;
-    if (L0.sharded) sync();
+    if (L0.sharded) sync_halo();
     if (update) {  // u' = u + e into the other buffer, r = f - K u'; then u' is the bound field
       if (!u_home_ || !u_alt_.p) throw StateError("fused update outside a bound solve");
       const bool home = u0_bound_ == u_home_;
@@ -890,7 +896,7 @@ template <typename T>
 void Hierarchy<T>::inner_prolong(int l) {
   Level& F = levels_[size_t(l)];
   Level& C = levels_[size_t(l + 1)];
-  if (F.sharded) sync();
+  if (F.sharded) sync_halo();
   {
     ProfScope p(s_, "prolong", double(F.g.nv) * 25.5);
     if (!(F.sharded && !C.sharded))
@@ -1173,7 +1179,7 @@ void Hierarchy<T>::relax_f32_group(int G, int l, int sweeps, bool zero_start) {
   for (int sw = 0; sw < sweeps; ++sw)
     for (int c = 0; c < 8; ++c) {
       if (L.g.size[c] == 0) continue;
-      if (L.sharded) sync();
+      if (L.sharded) sync_halo();
       const bool zs = zero_start && sw == 0;
       if constexpr (std::is_same_v<T, float>) {
         ProfScope p(s_, l == 1 ? "l1_gs_f32" : (l == 2 ? "l2_gs_f32" : "coarse_gs_f32"),
@@ -1187,7 +1193,7 @@ void Hierarchy<T>::relax_f32_group(int G, int l, int sweeps, bool zero_start) {
 template <typename T>
 void Hierarchy<T>::residual_f32_group(int G, int l) {
   Level& L = levels_[size_t(l)];
-  if (L.sharded) sync();
+  if (L.sharded) sync_halo();
   const float* x[kMaxRhsGroup];
   const float* f[kMaxRhsGroup];
   float* y[kMaxRhsGroup];

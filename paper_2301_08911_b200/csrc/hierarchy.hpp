@@ -177,6 +177,7 @@ class Hierarchy {
   bool sharded(int l) const { return levels_[size_t(l)].sharded; }
   long long global_nv(int l) const { return levels_[size_t(l)].nv_global; }
   void sync();                                     // fabric barrier (no-op on one domain)
+  void sync_halo();                                // barrier with the z-neighbour slabs only
   void allreduce(double* dev, int n, bool is_max = false);  // over slabs, rank-order fold
   template <typename X>
   ZLink<X> link(X* p) {                            // collective: this buffer on the slabs below / above

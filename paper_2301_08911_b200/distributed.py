@@ -1,13 +1,18 @@
 """Multi-GPU plumbing for the hot path (one process per GPU).
 
-Round-1 scheme: the six periodic cell problems of an iteration are
-independent solves, so rank r solves the load cases ``load_owners(n)`` assigns
-it; the library then broadcasts every solved displacement field from its owner
-over NCCL (NVLink) and every rank evaluates C^H, the sensitivities and the OC
-update identically. The result is bitwise equal to the 1-GPU run.
+Two schemes:
 
-``torch.distributed`` only carries the 128-byte NCCL unique id from rank 0 to
-the others (plumbing); the collectives themselves run inside libihom_b200.so.
+* z-slabs (the default of ``bench.py --gpus N``): rank r owns z planes [r t, (r+1) t) of every field;
+  kernels read the neighbour slabs' boundary planes directly through CUDA-IPC-mapped peer memory
+  (``ipc_fabric``), ordered by device-side barriers (z-neighbour-only around halo reads, bounded by a
+  timeout) and reduced through per-rank mailboxes folded in rank order.
+* load-case split (``--multi loads``): the six periodic cell problems are independent solves, so rank r
+  solves the load cases ``load_owners(n)`` assigns it; the library broadcasts every solved displacement
+  field from its owner over NCCL (NVLink) and every rank evaluates C^H, the sensitivities and the OC
+  update identically (bitwise equal to one GPU; no memory saving, stops scaling at six ranks).
+
+``torch.distributed`` carries only host metadata (IPC handles, the NCCL unique id); the data plane runs
+inside libihom_b200.so.
 """
 from __future__ import annotations
 
@@ -87,3 +92,23 @@ def ipc_fabric(rank: int, nranks: int, device: int = 0):
     """One z-slab per process: peer buffers are mapped with CUDA IPC (NVLink between GPUs)."""
     from . import Fabric
     return Fabric.ipc(rank, nranks, torch_allgather(), device=device)
+
+
+# ---------------------------------------------------------------- memory plan (estimate)
+# Bytes per level-0 vertex (= per element) of one z-slab in mixed precision, mixed_defect solver
+# (DESIGN.md 2/6): six persistent f64 u^i (144), level-0 f64 u/f/r + ping-pong u (96), level-0 f32 inner
+# e/f/r (36), coefficients (4), level-1/2/... f32 stencils (243 x 4 B x (1/8 + 1/64 + ...) = 139),
+# density side (7 f64 fields, 56); optional: f64 energy cache (168), each extra RHS of a lockstep group (89).
+_BASE_B = 144 + 96 + 36 + 4 + 139 + 56
+_CACHE_B = 168
+_GROUP_B = 89
+
+
+def memory_plan(reso: int, nranks: int, group: int = 1, energy_cache: bool = False) -> dict:
+    """Estimated HBM per GPU (GB) of a reso^3 run on nranks z-slabs, and whether it fits a 180 GB B200
+    (leaving 8 GB headroom). The library adapts the group size and the energy cache to the free HBM."""
+    nv = reso ** 3 / nranks
+    per_vertex = _BASE_B + (_CACHE_B if energy_cache else 0) + _GROUP_B * (group - 1)
+    gb = nv * per_vertex / 1e9
+    return {"reso": reso, "nranks": nranks, "group": group, "energy_cache": energy_cache,
+            "gb_per_gpu": round(gb, 1), "fits_b200": gb <= 172.0}

@@ -95,3 +95,27 @@ def test_slab_planes():
         dd.slab_planes(32, 3, 0)
     with pytest.raises(ValueError):
         dd.slab_planes(24, 4, 0)  # 6 planes per slab: not a multiple of 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_under_torchrun_same_device(world):
+    """The bench's multi-GPU path as the driver launches it (torch.distributed.run, one process per rank,
+    z-slabs over CUDA IPC), with every rank on cuda:0 (--same-device): it must complete and print one
+    JSON line from rank 0 with the whole-job metric. Small grid: 64^3 (16 planes per slab at 4 ranks)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", str(world), "--same-device", "--reso", "64", "--steps", "2", "--warmup", "3",
+           "--no-cpu-baseline"]
+    env = dict(os.environ, IHOM_FABRIC_TIMEOUT_S="120")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["value"] > 0 and d["steps"] == 2
+    assert "e2e" in d and d["e2e"]["h2d_bytes_per_step"] == 8 * 64 ** 3

@@ -186,6 +186,20 @@ __device__ __forceinline__ void swap_rows(R* a, R* b, R& ra, R& rb, bool doit) {
   rb = doit ? t : rb;
 }
 
+// Symmetric positive definite 3x3 solve by the adjugate (one reciprocal, no pivoting or branches): the
+// self block S of a vertex is a sum of q-weighted diagonal 3x3 blocks of K0, symmetric bit for bit (both
+// triangles are merged by the same operations) and SPD. Used by the f32 inner-cycle level-0 GS, where
+// the partial-pivot solve3 (6 IEEE divisions, pivot selects) was ~15% of the pass's instructions.
+__device__ __forceinline__ void solve3_spd(const float m[9], const float rhs[3], float out[3]) {
+  const float a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], f = m[8];
+  const float A = fmaf(d, f, -e * e), B = fmaf(c, e, -b * f), C = fmaf(b, e, -c * d);
+  const float D = fmaf(a, f, -c * c), E = fmaf(b, c, -a * e), F = fmaf(a, d, -b * b);
+  const float r = 1.0f / fmaf(a, A, fmaf(b, B, c * C));
+  out[0] = fmaf(A, rhs[0], fmaf(B, rhs[1], C * rhs[2])) * r;
+  out[1] = fmaf(B, rhs[0], fmaf(D, rhs[1], E * rhs[2])) * r;
+  out[2] = fmaf(C, rhs[0], fmaf(E, rhs[1], F * rhs[2])) * r;
+}
+
 template <typename R>
 __device__ __forceinline__ void solve3(const R m[9], const R rhs[3], R out[3]) {
   R r0[3] = {m[0], m[1], m[2]}, r1[3] = {m[3], m[4], m[5]}, r2[3] = {m[6], m[7], m[8]};

@@ -669,6 +669,7 @@ int ihom_oc_update(long long m, const double* rho, const double* sens, const iho
                    double* lambda, int* ok, int where) {
   return guarded([&] {
     if (m <= 0) throw std::invalid_argument("empty density field");
+    if (out == rho || out == sens) throw std::invalid_argument("oc_update: out must not alias rho or sens");
     cudaStream_t s = lib_stream();
     DevIn r(rho, size_t(m), where, s);
     DevIn g(sens, size_t(m), where, s);

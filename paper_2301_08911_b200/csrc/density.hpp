@@ -58,6 +58,7 @@ void field_sum(const double* f, long long m, double* partials, double* out, cuda
 bool init_trig(const int n[3], int basis_n, std::uint64_t seed, double volume, double sigmoid_k, double* rho,
                double* scratch, Workspace& ws, cudaStream_t s, const Slab& slab = {});
 // m = this slab's elements, m_total = the whole grid's (the volume mean)
+// Device-resident bisection (density_kernels.cu); `out` (not aliasing rho or g) doubles as scratch.
 OCResult oc_update(long long m, const double* rho, const double* g, const OCConfig& cfg, double* out, Workspace& ws,
                    cudaStream_t s, const Slab& slab = {}, long long m_total = 0);
 

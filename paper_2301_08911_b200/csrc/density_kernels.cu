@@ -618,32 +618,145 @@ struct OCParams {
   double damp, step, lo, hi;
 };
 
-__device__ __forceinline__ double oc_value(double rho, double g, double inv_scale, double lambda, OCParams p) {
-  const double b0 = fmax(1e-30, -g) * inv_scale;  // (src/oc.cpp:39-41)
-  const double ratio = b0 / lambda;
-  double x = rho * (p.damp == 0.5 ? sqrt(ratio) : pow(ratio, p.damp));  // src/oc.cpp:18
-  x = fmin(fmax(x, rho - p.step), rho + p.step);
-  return fmin(fmax(x, p.lo), p.hi);
+// ---------------------------------------------------------------- device-resident OC bisection
+// oc_update (src/oc.cpp:27-77). The geometric bisection runs on the device: every pass evaluates the means
+// of a depth-3 subtree of the bisection (7 trial lambdas, and lo0/hi0 on the first pass) in one sweep over
+// rho and sqrt(b0), then one thread walks the subtree exactly as the sequential loop would (same
+// sqrt(lo*hi) midpoints, same stop rule, same 60-trial cap) and leaves the bracket or the final lambda in
+// device memory. Passes run in batches with one 8-byte read of the done flag per batch (usually one batch
+// per update, versus one blocking read-back per trial before).
+// Per element a trial is x = clamp(clamp(rho * sqrt(b0) * lambda^-1/2, rho -+ step), [rho_min, 1])
+// (the two clamps fused into one interval):
+// sqrt(b0) is formed once per update instead of sqrt(b0 / lambda) per trial (the reference's
+// rho * pow(b0 / lambda, 0.5), src/oc.cpp:18; same value to an ulp).
+constexpr int kOcTree = 7;           // lambdas per pass (depth-3 subtree)
+constexpr int kOcSlots = 2 + kOcTree;  // + lo0, hi0 on the first pass
+constexpr int kOcMaxPasses = 22;     // 2 bracket trials + 60 bisection trials, 3 per pass
+
+struct OcState {  // device scratch (doubles)
+  double lo, hi, lambda, mean, trials, done, ok, pass;
+};
+
+// sb = sqrt(max(1e-30, -g) / scale) into `sb` (src/oc.cpp:35-41, the normaliser on the device)
+__global__ void oc_prep_kernel(const double* __restrict__ g, long long m, const double* scale, double* sb) {
+  const double inv = 1.0 / *scale;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT)
+    sb[i] = sqrt(fmax(1e-30, -g[i]) * inv);
 }
 
-// trial: partial sums of the trial field; write != 0 also stores it.
-__global__ void oc_trial_kernel(const double* __restrict__ rho, const double* __restrict__ g, long long m,
-                                const double* scale, double lambda, OCParams p, double* partials, double* out) {
-  __shared__ double sh[32];
-  const double inv_scale = 1.0 / *scale;
-  double s = 0.0;
-  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
-    const double v = oc_value(rho[i], g[i], inv_scale, lambda, p);
-    if (out) out[i] = v;
-    s += v;
+// the same two clamps as one (rho lies in [lo, hi], so [rho - step, rho + step] meets [lo, hi] and
+// clamp(clamp(x, a, b), c, d) == clamp(x, max(a, c), min(b, d)) exactly)
+__device__ __forceinline__ void oc_bounds(double rho, OCParams p, double& lo, double& hi) {
+  lo = fmax(rho - p.step, p.lo);
+  hi = fmin(rho + p.step, p.hi);
+}
+
+// the lambdas of a pass: slots 0/1 = lo0/hi0 (first pass only), slots 2.. = the subtree in level order
+// (node k's children: 2k+1 when mean > V (lo = lambda_k), 2k+2 otherwise (hi = lambda_k))
+__device__ __forceinline__ void oc_pass_lambdas(const OcState& st, double lam[kOcSlots]) {
+  lam[0] = 1e-12;
+  lam[1] = 1e12;
+  double lo[kOcTree], hi[kOcTree];
+  lo[0] = st.lo;
+  hi[0] = st.hi;
+#pragma unroll
+  for (int k = 0; k < kOcTree; ++k) {
+    lam[2 + k] = sqrt(lo[k] * hi[k]);
+    if (2 * k + 2 < kOcTree) {
+      lo[2 * k + 1] = lam[2 + k], hi[2 * k + 1] = hi[k];
+      lo[2 * k + 2] = lo[k], hi[2 * k + 2] = lam[2 + k];
+    }
   }
-  const double r = block_reduce_d(s, sh, false);
-  if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
-// oc_update (src/oc.cpp:27-77): host-driven geometric bisection; each trial is one
-// fused pass (b0 normalisation, pow, step clamp, box clamp, block sums) with a
-// single 8-byte read-back.
+__global__ void oc_pass_kernel(const double* __restrict__ rho, const double* __restrict__ sb, long long m,
+                               const OcState* st, OCParams p, double* partials) {
+  __shared__ double sh[32];
+  const OcState S = *st;
+  if (S.done != 0.0) return;
+  const bool first = S.pass == 0.0;
+  double lam[kOcSlots], rl[kOcSlots], acc[kOcSlots];
+  oc_pass_lambdas(S, lam);
+#pragma unroll
+  for (int k = 0; k < kOcSlots; ++k) rl[k] = 1.0 / sqrt(lam[k]), acc[k] = 0.0;
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    const double r = rho[i], base = r * sb[i];
+    double lo, hi;
+    oc_bounds(r, p, lo, hi);
+#pragma unroll
+    for (int k = 0; k < kOcSlots; ++k)
+      if (first || k >= 2) acc[k] += fmin(fmax(base * rl[k], lo), hi);
+  }
+#pragma unroll
+  for (int k = 0; k < kOcSlots; ++k) {
+    const double v = block_reduce_d(acc[k], sh, false);
+    if (threadIdx.x == 0) partials[k * kReducePartials + blockIdx.x] = v;
+  }
+}
+
+__global__ void oc_sums_kernel(const double* partials, int nparts, const OcState* st, double* sums) {
+  __shared__ double sh[32];
+  if (st->done != 0.0) return;
+  for (int k = 0; k < kOcSlots; ++k) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kDT) v += partials[k * kReducePartials + i];
+    const double r = block_reduce_d(v, sh, false);
+    if (threadIdx.x == 0) sums[k] = r;
+  }
+}
+
+// the sequential loop of src/oc.cpp:44-76 over this pass's means
+__global__ void oc_decide_kernel(OcState* st, const double* sums, double count, double volume, double tol) {
+  OcState S = *st;
+  if (S.done != 0.0) return;
+  double lam[kOcSlots];
+  oc_pass_lambdas(S, lam);
+  if (S.pass == 0.0) {
+    const double mean_lo = sums[0] / count;
+    if (volume >= mean_lo) {  // even the maximal move stays at or under target
+      S.done = 1.0, S.lambda = lam[0], S.mean = mean_lo, S.ok = fabs(mean_lo - volume) <= tol;
+      *st = S;
+      return;
+    }
+    const double mean_hi = sums[1] / count;
+    if (volume <= mean_hi) {  // cannot shrink below target within the step limit
+      S.done = 1.0, S.lambda = lam[1], S.mean = mean_hi, S.ok = fabs(mean_hi - volume) <= tol;
+      *st = S;
+      return;
+    }
+  }
+  int k = 0;
+  while (k < kOcTree) {
+    const double mean = sums[2 + k] / count;
+    S.trials += 1.0;
+    S.lambda = lam[2 + k];
+    S.mean = mean;
+    if (fabs(mean - volume) <= tol) {
+      S.done = 1.0, S.ok = 1.0;
+      break;
+    }
+    if (mean > volume) S.lo = lam[2 + k], k = 2 * k + 1;
+    else S.hi = lam[2 + k], k = 2 * k + 2;
+    if (S.trials >= 60.0) {  // cap: the last trial's field, ok iff within tolerance (src/oc.cpp:72-75)
+      S.done = 1.0, S.ok = 0.0;
+      break;
+    }
+  }
+  S.pass += 1.0;
+  *st = S;
+}
+
+__global__ void oc_write_kernel(const double* __restrict__ rho, double* sbout, long long m, const OcState* st,
+                                OCParams p) {
+  const double rl = 1.0 / sqrt(st->lambda);
+  for (long long i = (long long)blockIdx.x * kDT + threadIdx.x; i < m; i += (long long)gridDim.x * kDT) {
+    const double r = rho[i];
+    double lo, hi;
+    oc_bounds(r, p, lo, hi);
+    sbout[i] = fmin(fmax(r * sbout[i] * rl, lo), hi);  // sbout holds sqrt(b0) on entry, the update on exit
+  }
+}
+
 OCResult oc_update(long long m, const double* rho, const double* g, const OCConfig& cfg, double* out, Workspace& ws,
                    cudaStream_t s, const Slab& slab, long long m_total) {
   const int grid = dgrid(m);
@@ -653,69 +766,60 @@ OCResult oc_update(long long m, const double* rho, const double* g, const OCConf
   IHOM_LAUNCH_CHECK();
   finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, true, ws.scalar);
   IHOM_LAUNCH_CHECK();
-  int bad = 0;
-  double scale = 0.0;
-  if (slab.on()) {  // max scale and the non-finite flag over all slabs
-    launch_int_to_double(ws.flag, ws.scalars + 62, s);
-    IHOM_CUDA(cudaMemcpyAsync(ws.scalars + 63, ws.scalar, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    slab.allreduce(ws.scalars + 62, 2, true, s);
-    IHOM_CUDA(cudaMemcpyAsync(ws.scalar, ws.scalars + 63, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    double fl = 0.0;
-    IHOM_CUDA(cudaMemcpyAsync(&fl, ws.scalars + 62, sizeof(double), cudaMemcpyDeviceToHost, s));
-    IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
-    IHOM_CUDA(cudaStreamSynchronize(s));
-    bad = fl != 0.0;
-  } else {
-    IHOM_CUDA(cudaMemcpyAsync(&bad, ws.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
-    IHOM_CUDA(cudaStreamSynchronize(s));
+  // max scale and the non-finite flag over all slabs (ws.scalars[62..63]); scale back into ws.scalar
+  launch_int_to_double(ws.flag, ws.scalars + 62, s);
+  IHOM_CUDA(cudaMemcpyAsync(ws.scalars + 63, ws.scalar, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  slab.allreduce(ws.scalars + 62, 2, true, s);
+  IHOM_CUDA(cudaMemcpyAsync(ws.scalar, ws.scalars + 63, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  {
+    ProfScope pt(s, "oc_trial", double(m) * 16.0);
+    oc_prep_kernel<<<grid, kDT, 0, s>>>(g, m, ws.scalar, out);  // out = sqrt(b0) until the final write
+    IHOM_LAUNCH_CHECK();
   }
-  if (bad) throw std::invalid_argument("non-finite sensitivity");
-  // keep the scale on device in ws.scalar (read by every trial)
+  OcState init{1e-12, 1e12, 1e-12, 0.0, 0.0, 0.0, 1.0, 0.0};
+  OcState* st = reinterpret_cast<OcState*>(ws.scalars);  // scalars[0..7]
+  double* sums = ws.scalars + 16;                          // scalars[16..24]
+  IHOM_CUDA(cudaMemcpyAsync(st, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   const OCParams p{cfg.damp, cfg.step_limit, cfg.min_density, 1.0};
-  auto trial = [&](double lambda, bool write) {
-    ProfScope pt(s, "oc_trial", double(m) * (write ? 24.0 : 16.0));
-    oc_trial_kernel<<<grid, kDT, 0, s>>>(rho, g, m, ws.scalar, lambda, p, ws.partials, write ? out : nullptr);
-    IHOM_LAUNCH_CHECK();
-    finalize_d<<<1, kDT, 0, s>>>(ws.partials, grid, false, ws.scalar2);
-    IHOM_LAUNCH_CHECK();
-    slab.allreduce(ws.scalar2, 1, false, s);
-    double sum = 0.0;
-    IHOM_CUDA(cudaMemcpyAsync(&sum, ws.scalar2, sizeof(double), cudaMemcpyDeviceToHost, s));
-    IHOM_CUDA(cudaStreamSynchronize(s));
-    return sum / count;
-  };
-  OCResult res;
-  const double lo0 = 1e-12, hi0 = 1e12;
-  const double mean_lo = trial(lo0, false);
-  if (cfg.volume >= mean_lo) {
-    trial(lo0, true);
-    res.lambda = lo0 * scale;
-    res.bisection_ok = std::abs(mean_lo - cfg.volume) <= cfg.bisect_tol;
-    return res;
-  }
-  const double mean_hi = trial(hi0, false);
-  if (cfg.volume <= mean_hi) {
-    trial(hi0, true);
-    res.lambda = hi0 * scale;
-    res.bisection_ok = std::abs(mean_hi - cfg.volume) <= cfg.bisect_tol;
-    return res;
-  }
-  double lo = lo0, hi = hi0, lambda = lo0, mean = 0.0;
-  for (int it = 0; it < 60; ++it) {
-    lambda = std::sqrt(lo * hi);
-    mean = trial(lambda, false);
-    res.trials = it + 1;
-    if (std::abs(mean - cfg.volume) <= cfg.bisect_tol) {
-      trial(lambda, true);
-      res.lambda = lambda * scale;
-      return res;
+  if (cfg.damp != 0.5) throw std::invalid_argument("the device OC update implements damp = 0.5 (src/oc.cpp:18)");
+  // passes in batches (6 first: a typical update needs 5-7), one 8-byte read of the done flag per batch;
+  // passes queued after termination exit at once
+  for (int pass = 0; pass < kOcMaxPasses;) {
+    const int batch = pass == 0 ? 6 : 4;
+    for (int b = 0; b < batch && pass < kOcMaxPasses; ++b, ++pass) {
+      ProfScope pt(s, "oc_trial", double(m) * 16.0);
+      oc_pass_kernel<<<grid, kDT, 0, s>>>(rho, out, m, st, p, ws.partials);
+      IHOM_LAUNCH_CHECK();
+      oc_sums_kernel<<<1, kDT, 0, s>>>(ws.partials, grid, st, sums);
+      IHOM_LAUNCH_CHECK();
+      slab.allreduce(sums, kOcSlots, false, s);
+      oc_decide_kernel<<<1, 1, 0, s>>>(st, sums, count, cfg.volume, cfg.bisect_tol);
+      IHOM_LAUNCH_CHECK();
     }
-    (mean > cfg.volume ? lo : hi) = lambda;
+    double done = 0.0;
+    IHOM_CUDA(cudaMemcpyAsync(&done, &st->done, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    if (done != 0.0) break;
   }
-  trial(lambda, true);
-  res.lambda = lambda * scale;
-  res.bisection_ok = std::abs(mean - cfg.volume) <= cfg.bisect_tol;
+  {
+    ProfScope pt(s, "oc_trial", double(m) * 24.0);
+    oc_write_kernel<<<grid, kDT, 0, s>>>(rho, out, m, st, p);
+    IHOM_LAUNCH_CHECK();
+  }
+  OcState fin{};
+  int bad = 0;
+  IHOM_CUDA(cudaMemcpyAsync(&fin, st, sizeof(fin), cudaMemcpyDeviceToHost, s));
+  double flag = 0.0;
+  IHOM_CUDA(cudaMemcpyAsync(&flag, ws.scalars + 62, sizeof(double), cudaMemcpyDeviceToHost, s));
+  double scale = 0.0;
+  IHOM_CUDA(cudaMemcpyAsync(&scale, ws.scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  bad = flag != 0.0;
+  if (bad) throw std::invalid_argument("non-finite sensitivity");
+  OCResult res;
+  res.lambda = fin.lambda * scale;
+  res.bisection_ok = fin.ok != 0.0;
+  res.trials = int(fin.trials);
   return res;
 }
 

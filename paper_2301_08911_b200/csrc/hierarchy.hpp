@@ -20,6 +20,7 @@
 #pragma once
 
 #include <array>
+#include <future>
 #include <memory>
 #include <string>
 #include <vector>
@@ -117,7 +118,14 @@ class Hierarchy {
   Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab = {});
   ~Hierarchy() {
     quiesce();
+    try {
+      join_coarsest();
+    } catch (...) {
+    }
     if (h_pinned_) cudaFreeHost(h_pinned_);
+    if (h_coarse_) cudaFreeHost(h_coarse_);
+    if (s_fact_) cudaStreamDestroy(s_fact_);
+    if (ev_fact_) cudaEventDestroy(ev_fact_);
   }
   // z-slab teardown is collective: no slab frees buffers its neighbours may still read
   void quiesce() noexcept {
@@ -244,6 +252,15 @@ class Hierarchy {
   DevBuf<T> coeff_;
   DevBuf<double> Ainv_, A_, cwork_, Q_;
   int nnull_ = 0;  // deflated near-null modes of the coarsest operator (rows of Q_)
+  // The coarsest factorisation runs on a host worker thread while the stream carries on (set_density
+  // returns with the GPU busy); join_coarsest() makes the first coarsest solve of a density wait for it.
+  std::future<int> fact_;          // -> nnull
+  cudaStream_t s_fact_ = nullptr;  // uploads of the factorisation
+  cudaEvent_t ev_fact_ = nullptr;  // recorded on s_fact_ after the uploads
+  void* h_coarse_ = nullptr;       // pinned staging of the coarsest stencil / coefficients
+  size_t h_coarse_bytes_ = 0;
+  bool fact_joined_ = true;
+  void join_coarsest();
   int ndof_c_ = 0;
   double op_scale_ = 0.0;
   bool density_set_ = false;

@@ -886,13 +886,30 @@ struct Optimizer : OptBase {
     const auto t0 = std::chrono::steady_clock::now();
     Workspace& ws = hom->hierarchy().workspace();
     // DensityExpr::eval (src/density.cpp:65-72)
+    // knob PHASE_PROF: whole-phase event pairs ("phase:*" families, overlapping the kernel families) to
+    // locate host-side gaps; off in the bench
+    const bool ph = knob("PHASE_PROF", 0) != 0;
+    auto phase = [&](const char* name) { return ProfScope(s, ph ? name : nullptr, 0.0); };
     slab.sync(s);  // neighbours' designs are current
-    radial_filter(nl, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s, zl(rho.p));
-    pow_field(pre.p, cfg.penal, m, phys.p, s);
-    hom->set_density(phys.p);
-    const CellSolveStats st = hom->solve_cell_problems();
+    CellSolveStats st;
     ihom_iter_record rec{};
-    hom->effective_tensor(rec.C);
+    {
+      auto p0 = phase("phase:density_eval");
+      radial_filter(nl, rho.p, dfilt ? cfg.filter_radius : 0.0, cfg.kernel, pre.p, s, zl(rho.p));
+      pow_field(pre.p, cfg.penal, m, phys.p, s);
+    }
+    {
+      auto p1 = phase("phase:set_density");
+      hom->set_density(phys.p);
+    }
+    {
+      auto p2 = phase("phase:solve");
+      st = hom->solve_cell_problems();
+    }
+    {
+      auto p3 = phase("phase:tensor");
+      hom->effective_tensor(rec.C);
+    }
     const Objective objective = make_objective(cfg, iter);
     const double fval = objective.eval(rec.C);
     rec.iter = iter;
@@ -912,6 +929,7 @@ struct Optimizer : OptBase {
       status = 3;
     }
     if (status == 0) {
+      auto p4 = phase("phase:sens_filter_oc");
       double seed[36];
       objective.grad(1.0, rec.C, seed);
       hom->tensor_sensitivity(seed, grad.p);

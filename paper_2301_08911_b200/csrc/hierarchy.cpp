@@ -862,7 +862,7 @@ void Hierarchy<T>::restore_home() {
 }
 
 template <typename T>
-double Hierarchy<T>::defect_residual(bool update) {
+double Hierarchy<T>::defect_residual(bool update, double* slot) {
   Level& L0 = levels_[0];
   if constexpr (std::is_same_v<T, float>) {
     if (!npart_.p) npart_.alloc(size_t(L0.g.nv / 32 + 1024));
@@ -889,10 +889,11 @@ double Hierarchy<T>::defect_residual(bool update) {
     }
     {
       ProfScope p(s_, "reduce", double(nb) * 8.0);
-      launch_sum(npart_.p, nb, ws_.partials, ws_.scalars + 4, s_);
+      launch_sum(npart_.p, nb, ws_.partials, slot ? slot : ws_.scalars + 4, s_);
     }
-    allreduce(ws_.scalars + 4, 1);
     launches_ += 3;
+    if (slot) return 0.0;  // deferred: ||r||^2 of this slab in *slot (finish_defect_cycles reads them together)
+    allreduce(ws_.scalars + 4, 1);
     IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
     IHOM_CUDA(cudaStreamSynchronize(s_));
     return std::sqrt(h_pinned_[0]);
@@ -1052,7 +1053,7 @@ double Hierarchy<T>::v_cycle_defect(const SolverOptions& opts) {
 }
 
 template <typename T>
-double Hierarchy<T>::finish_defect_cycle() {
+double Hierarchy<T>::finish_defect_cycle(double* slot) {
   Level& L0 = levels_[0];
   const long long n0 = 3 * L0.g.nv;
   const bool fast = fast_ok(L0.g);
@@ -1062,7 +1063,8 @@ double Hierarchy<T>::finish_defect_cycle() {
     launch_axpy_update<float>(level_u(0), L0.eu.p, n0, s_);
     ++launches_;
   }
-  if (fast) return defect_residual(fused);  // also leaves ef0 ready for the next cycle
+  if (fast) return defect_residual(fused, slot);  // also leaves ef0 ready for the next cycle
+  if (slot) throw std::logic_error("deferred defect norms need an even level-0 grid");
   compute_residual(0);
   return norm(L0.r.p, n0);
 }
@@ -1293,6 +1295,34 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
     }
 }
 
+// The outer defect-correction step (u += e, r = f - K u, ||r||) of every active RHS of a lockstep group,
+// enqueued back to back; the squared norms and the error flag come back in one read (one host round trip
+// per round of the group instead of two per RHS). Slabs: one allreduce of the norms, one of the flag.
+template <typename T>
+void Hierarchy<T>::finish_defect_cycles(int G, const bool* act, double* rn) {
+  double* slots = ws_.scalars + 52;  // [0, G): ||r||^2 per RHS, [6]: error flag
+  for (int k = 0; k < G; ++k)
+    if (act[k]) {
+      select_rhs(k);
+      finish_defect_cycle(slots + k);
+    }
+  launch_int_to_double(err_.p, slots + 6, s_);
+  if (slab_.on()) {
+    slab_.fab->check(slab_.rank);
+    allreduce(slots, G);
+    allreduce(slots + 6, 1, true);
+  }
+  IHOM_CUDA(cudaMemcpyAsync(h_pinned_, slots, sizeof(double) * 7, cudaMemcpyDeviceToHost, s_));
+  IHOM_CUDA(cudaStreamSynchronize(s_));
+  const int e = int(h_pinned_[6]);
+  if (e) {
+    IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
+    if (e == 1) throw NumericError("non-invertible coarse stencil diagonal (v_cycle)");
+    throw NumericError("coarsest operator is singular beyond translations (v_cycle)");
+  }
+  for (int k = 0; k < G; ++k) rn[k] = act[k] ? std::sqrt(h_pinned_[k]) : 0.0;
+}
+
 template <typename T>
 void Hierarchy<T>::solve_bound_group(int G, double* const* u, const SolverOptions& opts, const ZLink<double>* ul,
                                      SolveStats* st) {
@@ -1327,14 +1357,24 @@ void Hierarchy<T>::solve_bound_group(int G, double* const* u, const SolverOption
       st[k].rel_residual = defect_residual() / fnorm0_;
       act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
     }
+    const bool deferred = fast_ok(L0.g);  // the group's outer steps back to back, one read-back per round
     while (any()) {
       inner_vcycle_group(G, opts, act);
+      double rn[kMaxRhsGroup] = {};
+      if (deferred) {
+        finish_defect_cycles(G, act, rn);
+      } else {
+        for (int k = 0; k < G; ++k)
+          if (act[k]) {
+            select_rhs(k);
+            rn[k] = finish_defect_cycle();
+            check_error("v_cycle");
+          }
+      }
       for (int k = 0; k < G; ++k)
         if (act[k]) {
           select_rhs(k);
-          const double rn = finish_defect_cycle();
-          check_error("v_cycle");
-          st[k].rel_residual = fnorm0_ > 0.0 ? rn / fnorm0_ : 0.0;
+          st[k].rel_residual = fnorm0_ > 0.0 ? rn[k] / fnorm0_ : 0.0;
           ++st[k].cycles;
           act[k] = st[k].rel_residual > opts.tol && st[k].cycles < opts.max_cycles;
         }

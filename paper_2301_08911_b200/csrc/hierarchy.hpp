@@ -235,8 +235,9 @@ class Hierarchy {
   SolveStats solve_pcg(double* u, const SolverOptions& opts);
   void residual_f32(int l);
   void coarsest_f32();
-  double defect_residual(bool update = false);  // ef0 = float(f0 - K u0), returns ||f0 - K u0||;
-                                                // update: u0 += e0 first, folded into the same sweep
+  double defect_residual(bool update = false, double* slot = nullptr);  // ef0 = float(f0 - K u0), returns
+                                                // ||f0 - K u0||; update: u0 += e0 first, folded into the same
+                                                // sweep; slot: leave this slab's ||r||^2 there, no read-back
   bool fused_update_ok() const;                 // the defect sweep can fold in the u += e update
   void restore_home();                          // end of a solve: the result back in the bound buffer
 
@@ -291,7 +292,9 @@ class Hierarchy {
   void inner_vcycle_group(int G, const SolverOptions& opts, const bool* act);
   void relax_f32_group(int G, int l, int sweeps, bool zero_start);
   void residual_f32_group(int G, int l);
-  double finish_defect_cycle();  // u += e (fused or not), the new residual; returns ||r||
+  double finish_defect_cycle(double* slot = nullptr);  // u += e (fused or not), the new residual; returns ||r||
+                                                       // (slot: deferred, see defect_residual)
+  void finish_defect_cycles(int G, const bool* act, double* rn);  // all active RHSs, one read-back
   double* u0_bound_ = nullptr;
   double* u_home_ = nullptr;  // the caller's buffer of the current solve (u0_bound_ may be u_alt_)
   ZLink<double> u_home_l_{};

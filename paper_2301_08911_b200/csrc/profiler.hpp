@@ -56,8 +56,10 @@ struct ProfScope {
   const char* family;
   double bytes;
   ProfScope(cudaStream_t st, const char* fam, double b) : s(st), family(fam), bytes(b) {
-    slot = Profiler::get().enabled() ? Profiler::get().begin(st) : -1;
+    slot = (fam && Profiler::get().enabled()) ? Profiler::get().begin(st) : -1;  // fam == nullptr: inactive
   }
+  ProfScope(ProfScope&& o) noexcept : slot(o.slot), s(o.s), family(o.family), bytes(o.bytes) { o.slot = -1; }
+  ProfScope(const ProfScope&) = delete;
   ~ProfScope() {
     if (slot >= 0) Profiler::get().end(slot, s, family, bytes);
   }

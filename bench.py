@@ -59,6 +59,8 @@ def parse():
                     help="testing only: every rank on cuda:0 (gloo plumbing) -- checks the multi-process slab "
                          "path on a 1-GPU box; the timing is meaningless (ranks time-slice one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ref-precision", action="store_true",
+                    help="skip the short reference-precision (--mode vcycle) leg reported beside the headline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true",
                     help="skip the per-kernel-family CUDA events (roofline) inside the timed region")
@@ -348,6 +350,31 @@ def run_ours(args):
         moved = 8 * (args.reso ** 3 if fab is not None else m)  # whole job: every rank moves its slab
         line["e2e"] = {"value": round(t_e2e, 4), "unit": "s/iteration", "h2d_bytes_per_step": moved,
                        "d2h_bytes_per_step": moved}
+    if world == 1 and args.mode != "vcycle" and not args.no_ref_precision:
+        # the reference's own V-cycle (f64 nodal data on every level, f64 accumulation) beside the headline
+        opt.close()
+        vcfg = dataclasses.replace(cfg, solver_mode="vcycle")
+        vopt = ih.Optimizer(vcfg)
+        vext = torch.cuda.ExternalStream(vopt.stream())
+        vms, vst = [], 0
+        for k in range(5):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(vext)
+            vst, vrec = vopt.step()
+            b.record(vext)
+            torch.cuda.synchronize()
+            if vst != 0:
+                break
+            if k >= 2:  # 2 warm-up iterations
+                vms.append(a.elapsed_time(b))
+        vopt.close()
+        if vms:
+            line["reference_precision"] = {
+                "solver_mode": "vcycle", "value": round(statistics.mean(vms) / 1e3, 4), "unit": "s/iteration",
+                "sample": f"iterations 2..{1 + len(vms)} of a fresh run, device-resident design",
+                "note": "the reference's stationary V-cycle step for step: f64 nodal data and f64 accumulation on "
+                        "every level (only coefficients/stencils f32, as the reference's mixed mode)"}
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         secs = cpu_oracle_iterations(args, threads, 3, 1)

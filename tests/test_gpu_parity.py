@@ -117,6 +117,44 @@ def test_galerkin_stencils(ih, orc, precision, tol):
         assert rel(hom.hierarchy().stencil(l), oh.stencil(l)) < tol
 
 
+@pytest.mark.parametrize("precision,tol", [("double", 1e-11), ("mixed", 2e-6)])
+@pytest.mark.parametrize("n", [16, 32, (32, 16, 24)])
+def test_coarse_level_apply_gs_residual(ih, orc, precision, tol, n):
+    """Stencil levels directly (src/multigrid.cpp:186-239, 392-424): on levels 1 and 2 the device
+    apply (y = K_l x), one 8-colour GS sweep and the residual r = f - K_l u equal the oracle's on the
+    same seeded u, f (the level operators themselves are pinned by test_galerkin_stencils)."""
+    n3 = (n,) * 3 if np.isscalar(n) else n
+    nv0 = int(np.prod(n3))
+    rho = mt_uniform(nv0, 401, 1e-3, 1.0)
+    hom = make_hom(ih, n3, precision)
+    hom.set_density(rho)
+    oh = orc.Homogenizer(n3, E=E, nu=NU, penal=3.0, mixed=precision == "mixed")
+    oh.set_density(rho)
+    H = hom.hierarchy()
+    for l in (1, 2):
+        nv = int(np.prod([x >> l for x in n3]))
+        u = mt_uniform(3 * nv, 410 + l, -1, 1).reshape(nv, 3)
+        f = mt_uniform(3 * nv, 420 + l, -1, 1).reshape(nv, 3)
+        assert rel(H.apply(l, u), _oracle_apply(oh, l, u)) < tol
+        for which, v in (("u", u), ("f", f)):
+            H.set_field(l, which, v)
+            oh.level_field(l, which, v)
+        H.compute_residual(l)
+        oh.compute_residual(l)
+        assert rel(H.field(l, "r"), oh.level_field(l, "r")) < tol
+        H.relax(l, 1)
+        oh.relax(l, 1)
+        assert rel(H.field(l, "u"), oh.level_field(l, "u")) < tol
+
+
+def _oracle_apply(oh, l, x):
+    """K_l x on the oracle: residual with f = 0 is -K_l x."""
+    oh.level_field(l, "u", x)
+    oh.level_field(l, "f", np.zeros_like(x))
+    oh.compute_residual(l)
+    return -oh.level_field(l, "r")
+
+
 def test_coarse_operator_annihilates_constants(ih):
     hom = make_hom(ih, 16, "double")
     hom.set_density(mt_uniform(16 ** 3, 229, 1e-3, 1.0))

@@ -1251,6 +1251,43 @@ void Hierarchy<T>::residual_f32_group(int G, int l) {
 // One inner V-cycle for each active RHS, the stencil levels in lockstep. An inactive RHS (already
 // converged) skips every level-0 and transfer step; the grouped coarse kernels still compute its lane
 // on stale (finite) data, which nothing reads.
+// Restriction l -> l+1 (down) or prolongation l+1 -> l (up) of every RHS lane of a lockstep group in one
+// launch (levels >= 1, where the group's lanes run together anyway; an inactive lane transfers stale data
+// nothing reads). False when the level pair needs the per-lane path (slab transition, odd grids).
+template <typename T>
+bool Hierarchy<T>::transfer_group(int G, int l, bool down) {
+  if constexpr (!std::is_same_v<T, float>) {
+    return false;
+  } else {
+    Level& F = levels_[size_t(l)];
+    Level& C = levels_[size_t(l + 1)];
+    if (l < 1 || G < 2 || (F.sharded && !C.sharded) || !transfer_group_ok(F.g, C.g)) return false;
+    const float* src[kMaxRhsGroup];
+    float* dst[kMaxRhsGroup];
+    ZLink<float> lk[kMaxRhsGroup];
+    for (int k = 0; k < G; ++k) {
+      RhsSlot* o = slot_of(k);
+      if (down) {
+        src[k] = o ? o->er[size_t(l)].p : F.er.p;
+        lk[k] = F.sharded ? (o ? o->erl[size_t(l)] : F.erl) : ZLink<float>{};
+        dst[k] = o ? o->ef[size_t(l + 1)].p : C.ef.p;
+      } else {
+        src[k] = o ? o->eu[size_t(l + 1)].p : C.eu.p;
+        lk[k] = C.sharded ? (o ? o->eul[size_t(l + 1)] : C.eul) : ZLink<float>{};
+        dst[k] = o ? o->eu[size_t(l)].p : F.eu.p;
+      }
+    }
+    if (F.sharded) sync_halo();
+    {
+      ProfScope p(s_, down ? "restrict" : "prolong", double(F.g.nv) * (down ? 13.5 : 25.5) * G);
+      if (down) launch_restrict_group(F.g, C.g, G, src, lk, dst, s_);
+      else launch_prolong_add_group(C.g, F.g, G, src, lk, dst, s_);
+    }
+    ++launches_;
+    return true;
+  }
+}
+
 template <typename T>
 void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
@@ -1268,11 +1305,12 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
       }
     relax_f32_group(G, l, opts.pre_sweeps, zs);
     residual_f32_group(G, l);
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        select_rhs(k);
-        restrict_to_f32(l);
-      }
+    if (!transfer_group(G, l, true))
+      for (int k = 0; k < G; ++k)
+        if (act[k]) {
+          select_rhs(k);
+          restrict_to_f32(l);
+        }
   }
   for (int k = 0; k < G; ++k)
     if (act[k]) {
@@ -1280,11 +1318,12 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
       inner_coarsest();
     }
   for (int l = lmax - 1; l >= 1; --l) {
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        select_rhs(k);
-        inner_prolong(l);
-      }
+    if (!transfer_group(G, l, false))
+      for (int k = 0; k < G; ++k)
+        if (act[k]) {
+          select_rhs(k);
+          inner_prolong(l);
+        }
     relax_f32_group(G, l, opts.post_sweeps, false);
   }
   for (int k = 0; k < G; ++k)

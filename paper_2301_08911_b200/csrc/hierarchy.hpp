@@ -295,6 +295,7 @@ class Hierarchy {
   double finish_defect_cycle(double* slot = nullptr);  // u += e (fused or not), the new residual; returns ||r||
                                                        // (slot: deferred, see defect_residual)
   void finish_defect_cycles(int G, const bool* act, double* rn);  // all active RHSs, one read-back
+  bool transfer_group(int G, int l, bool down);                   // grouped level >= 1 transfer
   double* u0_bound_ = nullptr;
   double* u_home_ = nullptr;  // the caller's buffer of the current solve (u0_bound_ may be u_alt_)
   ZLink<double> u_home_l_{};

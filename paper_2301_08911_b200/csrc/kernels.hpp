@@ -73,6 +73,14 @@ template <typename TN>
 void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* uf, cudaStream_t s,
                         ZLink<TN> cl = {}, int zoff = 0);
 
+// the same for the RHS lanes of a lockstep group in one launch (f32 inner fields, TRANSFER_F32, even
+// grids; per-lane arithmetic identical to one launch per lane)
+bool transfer_group_ok(const GridGeo& gf, const GridGeo& gc);
+void launch_restrict_group(const GridGeo& gf, const GridGeo& gc, int nl, const float* const* rf,
+                           const ZLink<float>* rl, float* const* fc, cudaStream_t s);
+void launch_prolong_add_group(const GridGeo& gc, const GridGeo& gf, int nl, const float* const* uc,
+                              const ZLink<float>* cl, float* const* uf, cudaStream_t s);
+
 // ---- coarse levels (src/multigrid.cpp:186-239, 281-333) ----
 template <typename TS, typename TN>
 void launch_stencil_apply(const GridGeo& g, const TS* st, const TN* x, const TN* f, TN* y, cudaStream_t s,

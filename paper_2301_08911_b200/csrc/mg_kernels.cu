@@ -55,12 +55,24 @@ __global__ void restrict_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ r
 // plane in halved coordinates) -- only the slab's own planes are written.
 // TA: arithmetic type; float (knob TRANSFER_F32, f32 fields only) keeps the inner cycle's transfers in
 // f32 (the weights are powers of two: exact products) instead of converting every value to f64.
+// Up to kMaxRhsGroup (source, link, destination) triples of one transfer, one per RHS lane of a lockstep
+// group: blockIdx.z = lane * nz + (colour + 8 h2), same per-lane arithmetic as one launch per lane.
+template <typename TN>
+struct XferN {
+  const TN* src[kMaxRhsGroup];
+  ZLink<TN> sl[kMaxRhsGroup];
+  TN* dst[kMaxRhsGroup];
+};
+
 template <typename TN, typename TA = double>
-__global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, const TN* __restrict__ rf,
-                                                            ZLink<TN> rl, GridGeo gout, int zoff,
-                                                            TN* __restrict__ fc) {
-  const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
-  const int h2 = blockIdx.z >> 3;
+__global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, XferN<TN> io, int nz, GridGeo gout,
+                                                            int zoff) {
+  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
+  const TN* __restrict__ rf = io.src[lane];
+  const ZLink<TN> rl = io.sl[lane];
+  TN* __restrict__ fc = io.dst[lane];
+  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = zz >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
   const int cx = 2 * h0 + (color & 1), cy = 2 * h1 + ((color >> 1) & 1), cz = 2 * h2 + ((color >> 2) & 1);
@@ -117,10 +129,13 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
 }
 
 template <typename TN, typename TA = double>
-__global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, const TN* __restrict__ uc,
-                                                           ZLink<TN> cl, int zoff, TN* __restrict__ uf) {
-  const int color = blockIdx.z & 7;  // colour fastest (L2 reuse across colours of a plane)
-  const int h2 = blockIdx.z >> 3;
+__global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, XferN<TN> io, int nz, int zoff) {
+  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
+  const TN* __restrict__ uc = io.src[lane];
+  const ZLink<TN> cl = io.sl[lane];
+  TN* __restrict__ uf = io.dst[lane];
+  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = zz >> 3;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
   TA acc[3] = {TA(0), TA(0), TA(0)};
@@ -146,11 +161,14 @@ void launch_restrict(const GridGeo& gf, const GridGeo& gc, const TN* rf, TN* fc,
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gc);
     const dim3 gr(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), 8 * gc.cd[0][2]);
+    XferN<TN> io{};
+    io.src[0] = rf;
+    io.sl[0] = resolve(rl, rf);
+    io.dst[0] = fc;
     if (std::is_same_v<TN, float> && transfer_f32())
-      restrict_fast_kernel<TN, float><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc,
-                                                       gout ? zoff : 0, fc);
+      restrict_fast_kernel<TN, float><<<gr, b, 0, s>>>(gf, gc, io, int(gr.z), gout ? *gout : gc, gout ? zoff : 0);
     else
-      restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, rf, resolve(rl, rf), gout ? *gout : gc, gout ? zoff : 0, fc);
+      restrict_fast_kernel<TN><<<gr, b, 0, s>>>(gf, gc, io, int(gr.z), gout ? *gout : gc, gout ? zoff : 0);
     IHOM_LAUNCH_CHECK();
     return;
   }
@@ -201,15 +219,47 @@ void launch_prolong_add(const GridGeo& gc, const GridGeo& gf, const TN* uc, TN* 
   if (fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0) {
     const dim3 b = fast_block(gf);
     const dim3 gr(ceil_div(gf.cd[0][0], b.x), ceil_div(gf.cd[0][1], b.y), 8 * gf.cd[0][2]);
+    XferN<TN> io{};
+    io.src[0] = uc;
+    io.sl[0] = resolve(cl, uc);
+    io.dst[0] = uf;
     if (std::is_same_v<TN, float> && transfer_f32())
-      prolong_fast_kernel<TN, float><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
+      prolong_fast_kernel<TN, float><<<gr, b, 0, s>>>(gc, gf, io, int(gr.z), zoff);
     else
-      prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, uc, resolve(cl, uc), zoff, uf);
+      prolong_fast_kernel<TN><<<gr, b, 0, s>>>(gc, gf, io, int(gr.z), zoff);
     IHOM_LAUNCH_CHECK();
     return;
   }
   if (slab) throw std::invalid_argument("z-slab prolongation needs even fine and coarse grids");
   prolong_kernel<TN><<<ceil_div(gf.nv, 128), 128, 0, s>>>(gc, gf, uc, uf);
+  IHOM_LAUNCH_CHECK();
+}
+
+bool transfer_group_ok(const GridGeo& gf, const GridGeo& gc) {
+  return fast_ok(gf) && gc.n[0] % 2 == 0 && gc.n[1] % 2 == 0 && gc.n[2] % 2 == 0 && transfer_f32();
+}
+
+void launch_restrict_group(const GridGeo& gf, const GridGeo& gc, int nl, const float* const* rf,
+                           const ZLink<float>* rl, float* const* fc, cudaStream_t s) {
+  if (nl < 1 || nl > kMaxRhsGroup || !transfer_group_ok(gf, gc)) throw std::invalid_argument("grouped restriction");
+  XferN<float> io{};
+  for (int k = 0; k < nl; ++k) io.src[k] = rf[k], io.sl[k] = resolve(rl[k], rf[k]), io.dst[k] = fc[k];
+  const dim3 b = fast_block(gc);
+  const unsigned nz = 8 * gc.cd[0][2];
+  restrict_fast_kernel<float, float><<<dim3(ceil_div(gc.cd[0][0], b.x), ceil_div(gc.cd[0][1], b.y), nz * nl), b, 0,
+                                       s>>>(gf, gc, io, int(nz), gc, 0);
+  IHOM_LAUNCH_CHECK();
+}
+
+void launch_prolong_add_group(const GridGeo& gc, const GridGeo& gf, int nl, const float* const* uc,
+                              const ZLink<float>* cl, float* const* uf, cudaStream_t s) {
+  if (nl < 1 || nl > kMaxRhsGroup || !transfer_group_ok(gf, gc)) throw std::invalid_argument("grouped prolongation");
+  XferN<float> io{};
+  for (int k = 0; k < nl; ++k) io.src[k] = uc[k], io.sl[k] = resolve(cl[k], uc[k]), io.dst[k] = uf[k];
+  const dim3 b = fast_block(gf);
+  const unsigned nz = 8 * gf.cd[0][2];
+  prolong_fast_kernel<float, float><<<dim3(ceil_div(gf.cd[0][0], b.x), ceil_div(gf.cd[0][1], b.y), nz * nl), b, 0,
+                                      s>>>(gc, gf, io, int(nz), 0);
   IHOM_LAUNCH_CHECK();
 }
 

@@ -706,7 +706,7 @@ __global__ void oc_sums_kernel(const double* partials, int nparts, const OcState
 }
 
 // the sequential loop of src/oc.cpp:44-76 over this pass's means
-__global__ void oc_decide_kernel(OcState* st, const double* sums, double count, double volume, double tol) {
+__device__ void oc_decide_kernel_body(OcState* st, const double* sums, double count, double volume, double tol) {
   OcState S = *st;
   if (S.done != 0.0) return;
   double lam[kOcSlots];
@@ -744,6 +744,25 @@ __global__ void oc_decide_kernel(OcState* st, const double* sums, double count, 
   }
   S.pass += 1.0;
   *st = S;
+}
+
+__global__ void oc_decide_kernel(OcState* st, const double* sums, double count, double volume, double tol) {
+  oc_decide_kernel_body(st, sums, count, volume, tol);
+}
+
+// one domain: the sums and the walk in one launch (slabs fold the sums across ranks in between)
+__global__ void oc_sums_decide_kernel(const double* partials, int nparts, OcState* st, double* sums, double count,
+                                      double volume, double tol) {
+  __shared__ double sh[32];
+  if (st->done != 0.0) return;
+  for (int k = 0; k < kOcSlots; ++k) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kDT) v += partials[k * kReducePartials + i];
+    const double r = block_reduce_d(v, sh, false);
+    if (threadIdx.x == 0) sums[k] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) oc_decide_kernel_body(st, sums, count, volume, tol);
 }
 
 __global__ void oc_write_kernel(const double* __restrict__ rho, double* sbout, long long m, const OcState* st,
@@ -790,10 +809,14 @@ OCResult oc_update(long long m, const double* rho, const double* g, const OCConf
       ProfScope pt(s, "oc_trial", double(m) * 16.0);
       oc_pass_kernel<<<grid, kDT, 0, s>>>(rho, out, m, st, p, ws.partials);
       IHOM_LAUNCH_CHECK();
-      oc_sums_kernel<<<1, kDT, 0, s>>>(ws.partials, grid, st, sums);
-      IHOM_LAUNCH_CHECK();
-      slab.allreduce(sums, kOcSlots, false, s);
-      oc_decide_kernel<<<1, 1, 0, s>>>(st, sums, count, cfg.volume, cfg.bisect_tol);
+      if (slab.on()) {
+        oc_sums_kernel<<<1, kDT, 0, s>>>(ws.partials, grid, st, sums);
+        IHOM_LAUNCH_CHECK();
+        slab.allreduce(sums, kOcSlots, false, s);
+        oc_decide_kernel<<<1, 1, 0, s>>>(st, sums, count, cfg.volume, cfg.bisect_tol);
+      } else {
+        oc_sums_decide_kernel<<<1, kDT, 0, s>>>(ws.partials, grid, st, sums, count, cfg.volume, cfg.bisect_tol);
+      }
       IHOM_LAUNCH_CHECK();
     }
     double done = 0.0;

@@ -1312,11 +1312,27 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
           restrict_to_f32(l);
         }
   }
-  for (int k = 0; k < G; ++k)
-    if (act[k]) {
-      select_rhs(k);
-      inner_coarsest();
+  if (lmax > 0 && G > 1) {  // the coarsest solves of all lanes in one launch (block per lane)
+    join_coarsest();
+    const Level& L = levels_[size_t(lmax)];
+    float* f[kMaxRhsGroup];
+    float* u[kMaxRhsGroup];
+    for (int k = 0; k < G; ++k) {
+      RhsSlot* o = slot_of(k);
+      f[k] = o ? o->ef[size_t(lmax)].p : L.ef.p;
+      u[k] = o ? o->eu[size_t(lmax)].p : L.eu.p;
     }
+    if (cwork_.n < size_t(3 * ndof_c_ * G)) cwork_.alloc(size_t(3 * ndof_c_ * kMaxRhsGroup));
+    ProfScope p(s_, "coarsest", 0.0);
+    launch_coarsest_solve_group(ndof_c_, L.g.nv, Ainv_.p, A_.p, Q_.p, nnull_, G, f, u, cwork_.p, err_.p, s_);
+    ++launches_;
+  } else {
+    for (int k = 0; k < G; ++k)
+      if (act[k]) {
+        select_rhs(k);
+        inner_coarsest();
+      }
+  }
   for (int l = lmax - 1; l >= 1; --l) {
     if (!transfer_group(G, l, false))
       for (int k = 0; k < G; ++k)

@@ -109,6 +109,9 @@ void launch_galerkin_from_stencil(const GridGeo& gf, const GridGeo& gc, const TS
 template <typename TN>
 void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
                            TN* u, double negligible, double* work, int* err, cudaStream_t s);
+// every RHS lane of a lockstep group (f32 inner fields, block per lane; work: nl * 3 ndof doubles)
+void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq,
+                                 int nl, float* const* f, float* const* u, double* work, int* err, cudaStream_t s);
 
 // ---- reductions (deterministic: fixed partition per size, fixed fold order) ----
 // sums of the three AoS components: out[3]

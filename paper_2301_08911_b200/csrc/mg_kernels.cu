@@ -1171,11 +1171,20 @@ __device__ double dense_resid(int N, const double* A, const double* x, const dou
 }
 
 template <typename TN>
+struct CoarseIO {  // the (f, u) pair of each RHS lane; block b solves lane b
+  TN* f[kMaxRhsGroup];
+  TN* u[kMaxRhsGroup];
+};
+
+template <typename TN>
 __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long long nv, const double* __restrict__ Ainv,
                                                                   const double* __restrict__ A,
-                                                                  const double* __restrict__ Q, int nq, TN* f, TN* u,
+                                                                  const double* __restrict__ Q, int nq, CoarseIO<TN> io,
                                                                   double negligible, double* work, int* err) {
   __shared__ double red[kCoarseThreads];
+  TN* f = io.f[blockIdx.x];
+  TN* u = io.u[blockIdx.x];
+  work += (size_t)blockIdx.x * 3 * N;
   double* fv = work;           // [N] f in dof order
   double* x = work + N;        // [N]
   double* r = work + 2 * N;    // [N]
@@ -1243,7 +1252,19 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
 template <typename TN>
 void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
                            TN* u, double negligible, double* work, int* err, cudaStream_t s) {
-  coarsest_kernel<TN><<<1, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, Q, nq, f, u, negligible, work, err);
+  CoarseIO<TN> io{};
+  io.f[0] = f;
+  io.u[0] = u;
+  coarsest_kernel<TN><<<1, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, Q, nq, io, negligible, work, err);
+  IHOM_LAUNCH_CHECK();
+}
+
+void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq,
+                                 int nl, float* const* f, float* const* u, double* work, int* err, cudaStream_t s) {
+  if (nl < 1 || nl > kMaxRhsGroup) throw std::invalid_argument("grouped coarsest solve: 1..6 lanes");
+  CoarseIO<float> io{};
+  for (int k = 0; k < nl; ++k) io.f[k] = f[k], io.u[k] = u[k];
+  coarsest_kernel<float><<<nl, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, Q, nq, io, 0.0, work, err);
   IHOM_LAUNCH_CHECK();
 }
 

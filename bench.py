@@ -125,13 +125,15 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(family, reso):
-    """dram bytes per launch of `family` from the committed ncu summary (profiles/, captured at 512^3), else None."""
+def ncu_traffic(family, reso, bytes_per_launch):
+    """DRAM bytes per launch of `family` from the committed ncu captures (profiles/ncu_traffic.json: measured DRAM
+    bytes / algorithmic bytes of the same launches at 512^3) times this run's algorithmic bytes per launch."""
     if reso != 512:
         return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(family)
+            e = json.load(f).get(family)
+        return round(e["ratio"] * bytes_per_launch, 0) if e else None
     except Exception:
         return None
 
@@ -317,7 +319,7 @@ def run_ours(args):
                 "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                 "bytes_per_launch": ent["bytes"] / max(1, ent["launches"]),
                 "avg_launch_ms": ent["ms"] / max(1, ent["launches"]),
-                "traffic": ncu_traffic(fam, args.reso)}
+                "traffic": ncu_traffic(fam, args.reso, ent["bytes"] / max(1, ent["launches"]))}
     # kernels whose real bound is a compute pipe, not HBM: f64 flops per unit against the measured FP64
     # peak (DFMA 63.1/clk/SM, tools/microbench_pipes.cu, x 148 SMs x 1965 MHz x 2 flops = 36.7 TFLOP/s).
     # The sum-factorised element sweep (hsweep_kernels.cuh) executes 100.6 DADD + 20.7 DMUL + 29.1 DFMA

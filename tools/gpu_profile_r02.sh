@@ -15,8 +15,8 @@ case "$1" in
     timeout 600 ncu --nvtx --nvtx-include timed/ --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/r02_launches.csv $B > gpurun_out/r02_launches.log 2>&1
     gzip -f gpurun_out/r02_launches.csv ;;
-  gs)
-    full gs l0_gs_fast2_kernel 2 ;;
+  gs)  # two plain (not zero-start) colour passes
+    full gs l0_gs_fast2_kernelIffLi5ELb0ELin1E 2 ;;
   others)
     full tensor tensor_stage_kernel 1
     full hsweep l0_hsweep_kernel 1 ;;

@@ -188,16 +188,18 @@ __device__ __forceinline__ void swap_rows(R* a, R* b, R& ra, R& rb, bool doit) {
 
 // Symmetric positive definite 3x3 solve by the adjugate (one reciprocal, no pivoting or branches): the
 // self block S of a vertex is a sum of q-weighted diagonal 3x3 blocks of K0, symmetric bit for bit (both
-// triangles are merged by the same operations) and SPD. Used by the f32 inner-cycle level-0 GS, where
-// the partial-pivot solve3 (6 IEEE divisions, pivot selects) was ~15% of the pass's instructions.
-__device__ __forceinline__ void solve3_spd(const float m[9], const float rhs[3], float out[3]) {
-  const float a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], f = m[8];
-  const float A = fmaf(d, f, -e * e), B = fmaf(c, e, -b * f), C = fmaf(b, e, -c * d);
-  const float D = fmaf(a, f, -c * c), E = fmaf(b, c, -a * e), F = fmaf(a, d, -b * b);
-  const float r = 1.0f / fmaf(a, A, fmaf(b, B, c * C));
-  out[0] = fmaf(A, rhs[0], fmaf(B, rhs[1], C * rhs[2])) * r;
-  out[1] = fmaf(B, rhs[0], fmaf(D, rhs[1], E * rhs[2])) * r;
-  out[2] = fmaf(C, rhs[0], fmaf(E, rhs[1], F * rhs[2])) * r;
+// triangles are merged by the same operations) and SPD. Used by the level-0 GS (f32 inner cycle and f64
+// nodal data), where the partial-pivot solve3 (6 IEEE divisions, pivot selects) was ~15% of the f32
+// pass's instructions and more of the f64 one (f64 division is a multi-instruction sequence).
+template <typename R>
+__device__ __forceinline__ void solve3_spd(const R m[9], const R rhs[3], R out[3]) {
+  const R a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], f = m[8];
+  const R A = fma(d, f, -e * e), B = fma(c, e, -b * f), C = fma(b, e, -c * d);
+  const R D = fma(a, f, -c * c), E = fma(b, c, -a * e), F = fma(a, d, -b * b);
+  const R r = R(1) / fma(a, A, fma(b, B, c * C));
+  out[0] = fma(A, rhs[0], fma(B, rhs[1], C * rhs[2])) * r;
+  out[1] = fma(B, rhs[0], fma(D, rhs[1], E * rhs[2])) * r;
+  out[2] = fma(C, rhs[0], fma(E, rhs[1], F * rhs[2])) * r;
 }
 
 template <typename R>

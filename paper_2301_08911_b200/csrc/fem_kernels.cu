@@ -237,8 +237,7 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     TN rhs[3], out[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) rhs[c] = TN(f[3 * loc + c]) - m[c];
-    if constexpr (std::is_same_v<TN, float>) solve3_spd(sblk, rhs, out);
-    else solve3<TN>(sblk, rhs, out);
+    solve3_spd<TN>(sblk, rhs, out);
 #pragma unroll
     for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
   }
@@ -316,8 +315,7 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast_kernel(GridGeo g, const 
   for (int e = 0; e < 9; ++e) S[e] = TS(sblk[e]);
 #pragma unroll
   for (int c = 0; c < 3; ++c) rhs[c] = TS(f[3 * loc + c]) - TS(m[c]);
-  if constexpr (std::is_same_v<TS, float>) solve3_spd(S, rhs, out);  // f32 inner cycle
-  else solve3<TS>(S, rhs, out);                                       // f64: the reference's pivoted solve
+  solve3_spd<TS>(S, rhs, out);  // SPD self block: adjugate (src/fem.cpp:131-135 pivots; same solution)
 #pragma unroll
   for (int c = 0; c < 3; ++c) uw[3 * loc + c] = TN(out[c]);
 }

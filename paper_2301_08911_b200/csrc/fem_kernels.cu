@@ -479,6 +479,15 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
         done = true;
       }
     }
+    if constexpr (std::is_same_v<TA, double> && std::is_same_v<TN, double>) {
+      // f64 nodal data (reference-precision V-cycle, all-double mode): the two-vertex pass too
+      if (g.cd[0][2] % 2 == 0 && knob("GS2_F64", 1) != 0) {
+        const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
+        if (linked) l0_gs_fast2_kernel<TC, TN, 2, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        else l0_gs_fast2_kernel<TC, TN, 2><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
+        done = true;
+      }
+    }
     if (!done && linked)
       l0_gs_fast_kernel<TC, TN, TA, sizeof(TA) == 4 ? 8 : 1, true><<<gr, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
     else if (!done)

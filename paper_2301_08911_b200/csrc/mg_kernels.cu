@@ -950,7 +950,8 @@ __global__ void __launch_bounds__(128) gal_elem_unrolled_kernel(GridGeo gf, Grid
                                                                 TC* __restrict__ st) {
   // n SLOWEST (blockIdx.z = rest + 8 d2 n): the resident blocks run the same n-branch, so the
   // instruction cache holds one ~5 KB unrolled body instead of thrashing over all 27 (ncu:
-  // "no_instruction" was the top stall with n fastest); the coefficients are re-read per n from L2/HBM.
+  // "no_instruction" was the top stall with n fastest); the coefficients are re-read per n from L2/HBM
+  // (chunking z so that they stay in L2 across the 27 n was measured no faster: the pass is DFMA-bound).
   const int nrest = 8 * gc.cd[0][2];
   const int n = blockIdx.z / nrest;
   const int rest = blockIdx.z % nrest;
@@ -1080,7 +1081,7 @@ __global__ void __launch_bounds__(128) gal_stencil_kernel(GridGeo gf, GridGeo gc
 }
 
 // Even coarse grid: one thread per (coarse vertex, 3x3 entry e), colour-fastest blocks
-// (blockIdx.z = e + 9 (colour + 8 h2)). The thread loads each of the 729 fine values
+// (blockIdx.z = colour + 8 (e + 9 h2)). The thread loads each of the 729 fine values
 // [K_{2vc+s}]_t (entry e) once, converts it once and scatters it into every coarse block delta it
 // feeds (gal_gen.cuh, tools/gen_galerkin.py): 729 loads + conversions and 2197 f64 FMAs instead of
 // 2197 of each; each accumulator still sees the reference's s-outer / t-inner term order.
@@ -1088,9 +1089,12 @@ template <typename TS>
 __global__ void __launch_bounds__(128) gal_stencil_fast_kernel(GridGeo gf, GridGeo gc, const TS* __restrict__ stf,
                                                                ZLink<TS> sl, GridGeo gout, int zoff,
                                                                TS* __restrict__ stc) {
-  const int e = blockIdx.z % 9;
-  const int rest = blockIdx.z / 9;
-  const int color = rest & 7, h2 = rest >> 3;
+  // blockIdx.z = colour + 8 (e + 9 h2): the eight colours of one coarse plane pair run back to back on
+  // the same entry e, so the entry-e rows of the five fine planes they read (~35 MB at 512^3) are shared
+  // in L2 instead of being re-read from DRAM per colour (ncu: 41 GB read per launch with e outermost)
+  const int color = blockIdx.z & 7;
+  const int e = (blockIdx.z >> 3) % 9;
+  const int h2 = (blockIdx.z >> 3) / 9;
   const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
   if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
   const int x = 2 * h0 + (color & 1), y = 2 * h1 + ((color >> 1) & 1), z = 2 * h2 + ((color >> 2) & 1);

@@ -470,7 +470,7 @@ void launch_l0_gs_color(const GridGeo& g, const TC* coeff, const TN* f, TN* u, i
     const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), g.cd[0][2]);
     bool done = false;
     if constexpr (std::is_same_v<TA, float> && std::is_same_v<TN, float>) {
-      if (g.cd[0][2] % 2 == 0) {  // two z-stacked vertices per thread
+      if (g.cd[0][2] % 2 == 0 && knob("GS2_F32", 1) != 0) {  // two z-stacked vertices per thread
         const dim3 gr2(gr.x, gr.y, g.cd[0][2] / 2);
         if (linked) l0_gs_fast2_kernel<TC, TN, 5, true><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);
         else if (gs2_minb() >= 8) l0_gs_fast2_kernel<TC, TN, 8><<<gr2, b, 0, s>>>(g, coeff, cl, f, u, ul, u, color);

@@ -9,6 +9,7 @@
 // with TA = double this avoids the per-coefficient f32->f64 conversion
 // (F2F, ~16/clk/SM on B200, measured) the reference's float merge would need.
 #include "kernels.hpp"
+#include "reduce.cuh"
 #include "ku_gen.cuh"
 #include "hada_gen.cuh"
 
@@ -575,11 +576,61 @@ void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, 
   IHOM_LAUNCH_CHECK();
 }
 
+// Macro force with the component sums of f folded into the same pass: the
+// reduction's own partition (reduce_grid blocks of kRT threads striding over the
+// vertex index) and fold, so the sums equal launch_comp_sums(f) bit for bit and
+// project_norm0 skips its read of f. The vertex index is decoded into the
+// colour-block coordinates fast_addr takes (colour-major, then h0, h1, h2).
+template <typename TC>
+__global__ void __launch_bounds__(kRT) macro_force_sums_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                               int load, double* __restrict__ f, double* partials) {
+  __shared__ double sh[32];
+  const unsigned B = (unsigned)g.size[0], d0 = (unsigned)g.cd[0][0], d1 = (unsigned)g.cd[0][1];
+  double s[3] = {0.0, 0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < g.nv; i += (long long)gridDim.x * kRT) {
+    const unsigned color = unsigned(i / B), r = unsigned(i - (long long)color * B);
+    const unsigned h0 = r % d0, r1 = r / d0;
+    FastAddr fa;
+    fast_addr(g, int(color), int(h0), int(r1 % d1), int(r1 / d1), fa);
+    double q[8];
+    load_q_fast(coeff, cl, fa, q);
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int ke = 0; ke < 8; ++ke)  // src/fem.cpp:145-150
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += q[ke] * c_fmacro[ke][load][c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      f[3 * i + c] = acc[c];
+      s[c] += acc[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double v = block_reduce(s[c], sh);
+    if (threadIdx.x == 0) partials[c * kReducePartials + blockIdx.x] = v;
+  }
+}
+
+template <typename TC>
+void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* partials, double* sums,
+                             cudaStream_t s, ZLink<TC> cl) {
+  if (!fast_ok(g)) throw std::invalid_argument("fused macro force sums need an even grid");
+  const int nb = reduce_grid(g.nv);
+  macro_force_sums_kernel<TC><<<nb, kRT, 0, s>>>(g, coeff, resolve(cl, coeff), load, f, partials);
+  IHOM_LAUNCH_CHECK();
+  launch_finalize(partials, nb, 3, sums, s);
+}
+
 // ---------------------------------------------------------------- instantiations
 template void launch_coeff<float>(const double*, float*, long long, double, cudaStream_t);
 template void launch_coeff<double>(const double*, double*, long long, double, cudaStream_t);
 template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t, ZLink<float>);
 template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t, ZLink<double>);
+template void launch_macro_force_sums<float>(const GridGeo&, const float*, int, double*, double*, double*, cudaStream_t,
+                                             ZLink<float>);
+template void launch_macro_force_sums<double>(const GridGeo&, const double*, int, double*, double*, double*,
+                                              cudaStream_t, ZLink<double>);
 template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, const double*, const double*, float*,
                                                   double*, cudaStream_t, ZLink<float>, ZLink<double>);
 

@@ -14,6 +14,7 @@ namespace ihomgpu {
 namespace {
 
 constexpr int kRedDoubles = 21 * kReducePartials + 128;
+constexpr int kMacroSums = 72;  // ws_.scalars[72 .. 72 + 3 kMaxRhsGroup): component sums left by macro_force
 
 // Dense assembly of a level operator in the reference dof order 3*loc + c
 // (src/multigrid.cpp:335-366).
@@ -638,20 +639,42 @@ double Hierarchy<T>::project_norm0(double* f) {
     remove_translations(f, 0);
     return norm(f, 3 * nv);
   }
-  {
+  double* sums = ws_.scalars;
+  if (msum_f_[cur_rhs_] == f) {  // the sums came out of the macro-force pass
+    sums = ws_.scalars + kMacroSums + 3 * cur_rhs_;
+  } else {
     ProfScope p(s_, "reduce", double(nv) * 24.0);
-    launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
+    launch_comp_sums<double>(f, nv, ws_.partials, sums, s_);
+    launches_ += 2;
   }
-  if (L.sharded) allreduce(ws_.scalars, 3);
+  msum_f_[cur_rhs_] = nullptr;
+  if (L.sharded) allreduce(sums, 3);
   {
     ProfScope p(s_, "vector", double(nv) * 48.0);
-    launch_sub_means_norm(f, nv, ws_.scalars, ws_.partials, ws_.scalars + 4, s_, L.nv_global);
+    launch_sub_means_norm(f, nv, sums, ws_.partials, ws_.scalars + 4, s_, L.nv_global);
   }
-  launches_ += 4;
+  launches_ += 2;
   allreduce(ws_.scalars + 4, 1);
   IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
   return std::sqrt(h_pinned_[0]);
+}
+
+template <typename T>
+void Hierarchy<T>::macro_force(int load) {  // src/fem.cpp:145-150
+  Level& L0 = levels_[0];
+  const ZLink<T> cl = slab_.on() ? coeff_l_ : ZLink<T>{};
+  ProfScope p(s_, "macro_force", double(L0.g.nv) * (24.0 + sizeof(T)));
+  if (fast_ok(L0.g) && knob("MACRO_SUMS", 1)) {
+    launch_macro_force_sums<T>(L0.g, coeff_.p, load, L0.f.p, ws_.partials, ws_.scalars + kMacroSums + 3 * cur_rhs_,
+                               s_, cl);
+    msum_f_[cur_rhs_] = L0.f.p;
+    launches_ += 2;
+  } else {
+    launch_macro_force<T>(L0.g, coeff_.p, load, L0.f.p, s_, cl);
+    msum_f_[cur_rhs_] = nullptr;
+    ++launches_;
+  }
 }
 
 template <typename T>
@@ -1612,9 +1635,7 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
       for (int k = 0; k < G; ++k) {
         hier_.select_rhs(k);
         hier_.sync();  // coefficients of the neighbouring slabs are current
-        ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
-        launch_macro_force<T>(g, hier_.coeff(), i + k, hier_.level_f(0), hier_.stream(),
-                              slabs ? hier_.coeff_link() : ZLink<T>{});
+        hier_.macro_force(i + k);
       }
       hier_.select_rhs(0);
       double* uu[kMaxRhsGroup];
@@ -1632,11 +1653,7 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
   for (int i = 0; i < 6 && G == 1; ++i) {
     if (multi && owner_[i] != comm_->rank()) continue;
     hier_.sync();  // coefficients of the neighbouring slabs are current
-    {
-      ProfScope p(hier_.stream(), "macro_force", double(g.nv) * (24.0 + sizeof(T)));
-      launch_macro_force<T>(g, hier_.coeff(), i, hier_.level_f(0), hier_.stream(),
-                            slabs ? hier_.coeff_link() : ZLink<T>{});
-    }
+    hier_.macro_force(i);
     const SolveStats s = hier_.solve_bound(u_[size_t(i)].p, opts_, ul_[size_t(i)]);
     per[3 * i] = s.cycles;
     per[3 * i + 1] = s.rel_residual;

@@ -165,9 +165,15 @@ class Hierarchy {
   void solve_bound_group(int G, double* const* u, const SolverOptions& opts, const ZLink<double>* ul, SolveStats* st);
 
 
+  // level_f(0) of the current RHS = macro force of load (src/fem.cpp:145-150). On even grids the
+  // component sums of f come out of the same pass and the next project_norm0 of that f uses them.
+  void macro_force(int load);
   double* level_u(int l) { return l == 0 && u0_bound_ ? u0_bound_ : levels_[size_t(l)].u.p; }
   ZLink<double> ulink(int l) const { return l == 0 && u0_bound_ ? u0l_ : levels_[size_t(l)].ul; }
-  double* level_f(int l) { return levels_[size_t(l)].f.p; }
+  double* level_f(int l) {  // handed out for writing: level 0's macro-force sums no longer describe it
+    if (l == 0) msum_f_[cur_rhs_] = nullptr;
+    return levels_[size_t(l)].f.p;
+  }
   double* level_r(int l) { return levels_[size_t(l)].r.p; }
   const T* stencil(int l) const { return levels_[size_t(l)].st.p; }
   const T* coeff() const { return coeff_.p; }
@@ -302,6 +308,7 @@ class Hierarchy {
   DevBuf<double> u_alt_;      // second level-0 u buffer of the fused update (ping-pong)
   ZLink<double> u_alt_l_{};
   double fnorm0_ = 0.0;
+  const double* msum_f_[kMaxRhsGroup] = {};  // f whose component sums macro_force left (per RHS)
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;
   DevBuf<double> npart_;  // per-block |r|^2 partials of the fused defect residual

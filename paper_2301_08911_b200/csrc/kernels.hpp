@@ -59,6 +59,11 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
 
 template <typename TC>
 void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s, ZLink<TC> cl = {});
+// macro force plus the component sums of f in the same pass (bitwise launch_macro_force followed by
+// launch_comp_sums(f) into sums[3]); even grids only (fast_ok)
+template <typename TC>
+void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* partials, double* sums,
+                             cudaStream_t s, ZLink<TC> cl = {});
 
 // ---- transfer (src/multigrid.cpp:12-79) ----
 // z-slab arguments: rl / cl link the source array to the slabs
@@ -117,6 +122,8 @@ void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, con
 // sums of the three AoS components: out[3]
 template <typename TN>
 void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s);
+// out[c] = fold of the per-block partials (c < ncomp), the second stage of every reduction here
+void launch_finalize(const double* partials, int nparts, int ncomp, double* out, cudaStream_t s);
 // out[0] = dot(a, b) over n entries
 template <typename TN>
 void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s);

@@ -5,37 +5,12 @@
 // (fixed grid of <= kReducePartials blocks, grid-stride, fixed tree fold), so
 // results are bitwise reproducible run to run on the same device model.
 #include "kernels.hpp"
+#include "reduce.cuh"
 
 #include <cstdint>
 #include <type_traits>
 
 namespace ihomgpu {
-
-constexpr int kRT = 256;
-
-inline int reduce_grid(long long n) {
-  long long g = (n + kRT * 8 - 1) / (kRT * 8);
-  if (g < 1) g = 1;
-  if (g > kReducePartials) g = kReducePartials;
-  return int(g);
-}
-
-__device__ __forceinline__ double block_reduce(double v, double* sh) {
-  const int t = threadIdx.x;
-  // warp level, fixed shuffle order
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((t & 31) == 0) sh[t >> 5] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (t < 32) {
-    r = (t < (int)(blockDim.x >> 5)) ? sh[t] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
-  }
-  __syncthreads();
-  return r;  // valid in thread 0
-}
 
 template <typename TN>
 __global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x, long long nv, double* partials) {
@@ -60,6 +35,11 @@ __global__ void __launch_bounds__(kRT) finalize_kernel(const double* partials, i
     const double r = block_reduce(s, sh);
     if (threadIdx.x == 0) out[c] = r;
   }
+}
+
+void launch_finalize(const double* partials, int nparts, int ncomp, double* out, cudaStream_t s) {
+  finalize_kernel<<<1, kRT, 0, s>>>(partials, nparts, ncomp, out);
+  IHOM_LAUNCH_CHECK();
 }
 
 template <typename TN>

@@ -55,6 +55,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("STENCIL_F32", 1)
         ih.set_knob("TRANSFER_F32", 1)
         ih.set_knob("PROJECT_NORM", 1)
+        ih.set_knob("MACRO_SUMS", 1)
         ih.set_knob("STENCIL_STREAM", 1)
 
 
@@ -273,6 +274,18 @@ def test_project_norm_bit_identical(ih, P):
     """Load projection and its norm in one pass (PROJECT_NORM) == remove_translations + norm, bitwise."""
     base = _solve(ih, 32, {"PROJECT_NORM": 0}, fabric_p=P)
     v = _solve(ih, 32, {"PROJECT_NORM": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (48, 0), (32, 2)])
+def test_macro_sums_bit_identical(ih, n, P):
+    """Macro force with the load's component sums folded into the same pass (MACRO_SUMS) ==
+    macro force + the separate component-sum reduction, bitwise (same partition and fold)."""
+    base = _solve(ih, n, {"MACRO_SUMS": 0}, fabric_p=P)
+    v = _solve(ih, n, {"MACRO_SUMS": 1}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

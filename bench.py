@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-ref-precision", action="store_true",
                     help="skip the short reference-precision (--mode vcycle) leg reported beside the headline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-host-staged", action="store_true",
+                    help="skip the memory-lever leg (host-staged displacements, U_HOST=2) after the timed region")
     ap.add_argument("--no-profile", action="store_true",
                     help="skip the per-kernel-family CUDA events (roofline) inside the timed region")
     return ap.parse_args()
@@ -193,10 +195,13 @@ def workload(args):
 
 def memory_plans(args, world):
     """Per-GPU HBM estimates (paper_2301_08911_b200.distributed.memory_plan) for this run and for the
-    1024^3 config at 1/2/4/8 z-slabs with the minimal levers (no lockstep group, no energy cache)."""
+    1024^3 config at 1/2/4/8 z-slabs, device-resident with the minimal levers (no lockstep group, no
+    energy cache) and host-staged (U_HOST)."""
     from paper_2301_08911_b200 import distributed as dd
     return {"this_run_min": dd.memory_plan(args.reso, world),
-            "1024^3": [dd.memory_plan(1024, n) for n in (1, 2, 4, 8)]}
+            "this_run_host_staged": dd.memory_plan(args.reso, world, host_staged=True),
+            "1024^3": [dd.memory_plan(1024, n) for n in (1, 2, 4, 8)],
+            "1024^3_host_staged": [dd.memory_plan(1024, n, host_staged=True) for n in (1, 2)]}
 
 
 def run_ours(args):
@@ -377,6 +382,44 @@ def run_ours(args):
                 "sample": f"iterations 2..{1 + len(vms)} of a fresh run, device-resident design",
                 "note": "the reference's stationary V-cycle step for step: f64 nodal data and f64 accumulation on "
                         "every level (only coefficients/stencils f32, as the reference's mixed mode)"}
+    if world == 1 and args.mode == "mixed_defect" and args.precision == "mixed" and not args.no_host_staged:
+        # memory lever: the same run with the six displacement fields in pinned host memory,
+        # f32 evaluation snapshots in the lean solver layout's free level-0 buffers; HBM is what the
+        # process holds with that optimiser alive
+        opt.close()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        free0, _ = torch.cuda.mem_get_info()
+        ih.set_knob("U_HOST", 2)
+        try:
+            hopt = ih.Optimizer(cfg)
+            hext = torch.cuda.ExternalStream(hopt.stream())
+            hms, hst, hbm_h = [], 0, None
+            for k in range(4):
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(hext)
+                hst, hrec = hopt.step()
+                b.record(hext)
+                torch.cuda.synchronize()
+                if k == 0:
+                    fb, tb = torch.cuda.mem_get_info()
+                    hbm_h = ((tb - fb) / 1e9, (free0 - fb) / 1e9)
+                if hst != 0:
+                    break
+                if k >= 2:  # 2 warm-up iterations
+                    hms.append(a.elapsed_time(b))
+            hopt.close()
+        finally:
+            ih.set_knob("U_HOST", 0)
+        line["host_staged"] = {
+            "value": round(statistics.mean(hms) / 1e3, 4) if hms else None, "unit": "s/iteration",
+            "hbm_used_gb_per_gpu": round(hbm_h[0], 2) if hbm_h is not None else None,
+            "hbm_library_gb": round(hbm_h[1], 2) if hbm_h is not None else None,
+            "sample": f"iterations 2..{1 + len(hms)} of a fresh run with U_HOST=2",
+            "note": "six f64 displacement fields in pinned host memory (staged per solve over PCIe), f32 "
+                    "evaluation snapshots in the lean solver layout; bitwise the same solves as the "
+                    "device-resident run (tests/test_host_staged.py)"}
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         secs = cpu_oracle_iterations(args, threads, 3, 1)

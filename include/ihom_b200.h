@@ -95,6 +95,11 @@ int ihom_effective_tensor(ihom_ctx* ctx, double C[36]);                         
 int ihom_tensor_sensitivity(ihom_ctx* ctx, const double seed[36], double* out, int where); /* tensor_sensitivity */
 int ihom_get_displacement(ihom_ctx* ctx, int load, double* u_aos, int where);     /* displacement(i) */
 int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u_aos, int where);
+/* Displacement storage (memory lever; no reference counterpart -- the paper keeps the six fields in
+ * host-backed unified memory): 0 device-resident f64; 2 pinned-host f64 with f32
+ * evaluation snapshots; 1 pinned-host f32 snapshots only. Knob U_HOST (-1 never, 0 auto when the
+ * device-resident layout does not fit, 1 / 2 forced). -1 on error. */
+int ihom_host_staged(ihom_ctx* ctx);
 
 /* ---- z-slab decomposition ----
  * A grid of n[2] z planes is split into nranks slabs of t = n[2] / nranks

@@ -469,6 +469,15 @@ class Homogenizer:
         p, where, keep = _in(u, 3 * self.nv)
         _check(lib().ihom_set_displacement(self._ctx(), int(i), p, where))
 
+    @property
+    def host_staged(self) -> int:
+        """Displacement storage: 0 device-resident f64, 2 pinned-host f64 + f32 evaluation snapshots,
+        1 pinned-host f32 snapshots only (memory lever; knob U_HOST)."""
+        v = lib().ihom_host_staged(self._ctx())
+        if v < 0:
+            raise IhomError(lib().ihom_last_error().decode())
+        return v
+
     def hierarchy(self) -> Hierarchy:
         return Hierarchy(self)
 

@@ -141,7 +141,6 @@ struct ihom_ctx {
   int n[3] = {0, 0, 0};
   std::unique_ptr<Homogenizer<float>> hf;
   std::unique_ptr<Homogenizer<double>> hd;
-  DevBuf<double> stage;  // 3*nv nodal staging
 
   template <class F>
   void with(F&& f) {
@@ -188,7 +187,6 @@ static ihom_ctx* create_ctx(const ihom_desc* d, const ihom_solver_opts* o, Slab 
     else if (d->precision == IHOM_MIXED)
       c->hf = std::make_unique<Homogenizer<float>>(d->n, m, d->penal, so, c->s, slab);
     else throw std::invalid_argument("precision must be IHOM_MIXED or IHOM_ALL_DOUBLE");
-    c->stage.alloc(size_t(3 * c->nv()));
     g_bound = c.get();
     ctx = c.release();
   });
@@ -321,7 +319,7 @@ int ihom_get_displacement(ihom_ctx* ctx, int load, double* u, int where) {
     if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
     ctx->with([&](auto& h) {
       DevOut o(u, size_t(3 * ctx->nv()), where);
-      copy_nodal(h.displacement(load), o.p, ctx->nv(), ctx->s);
+      h.read_displacement(load, o.p);
       o.finish(ctx->s);
     });
   });
@@ -332,11 +330,15 @@ int ihom_set_displacement(ihom_ctx* ctx, int load, const double* u, int where) {
     if (load < 0 || load > 5) throw std::invalid_argument("load case must be in [0, 6)");
     ctx->with([&](auto& h) {
       DevIn in(u, size_t(3 * ctx->nv()), where, ctx->s);
-      copy_nodal(in.p, h.displacement(load), ctx->nv(), ctx->s);
-      h.displacements_changed();
-      IHOM_CUDA(cudaStreamSynchronize(ctx->s));
+      h.write_displacement(load, in.p);
     });
   });
+}
+
+int ihom_host_staged(ihom_ctx* ctx) {
+  int v = -1;
+  if (guarded([&] { ctx->with([&](auto& h) { v = h.host_staged(); }); }) != IHOM_OK) return -1;
+  return v;
 }
 
 int ihom_num_levels(ihom_ctx* ctx) {
@@ -360,6 +362,7 @@ int ihom_level_field(ihom_ctx* ctx, int l, int which, int write, double* buf) {
       auto& H = h.hierarchy();
       if (l < 0 || l >= H.num_levels()) throw std::invalid_argument("level out of range");
       double* f = which == 0 ? H.level_u(l) : which == 1 ? H.level_f(l) : H.level_r(l);
+      if (!f) throw StateError("this f64 level field is not allocated (lean layout)");
       const long long nv = H.geo(l).nv;
       if (write) {
         DevIn in(buf, size_t(3 * nv), IHOM_HOST, ctx->s);

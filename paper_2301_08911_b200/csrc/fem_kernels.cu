@@ -582,16 +582,39 @@ void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, 
 // project_norm0 skips its read of f. The vertex index is decoded into the
 // colour-block coordinates fast_addr takes (colour-major, then h0, h1, h2).
 template <typename TC>
-__global__ void __launch_bounds__(kRT) macro_force_sums_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
-                                                               int load, double* __restrict__ f, double* partials) {
+__global__ void __launch_bounds__(kRT, 8) macro_force_sums_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                                  int load, double* __restrict__ f, double* partials) {
+  // 8 blocks of kRT per SM (<= 32 registers): the reduce_grid partition is one full wave
   __shared__ double sh[32];
-  const unsigned B = (unsigned)g.size[0], d0 = (unsigned)g.cd[0][0], d1 = (unsigned)g.cd[0][1];
+  // mixed-radix (colour, h2, h1, h0) coordinates of i and of the grid stride (the same for every
+  // thread: kept in shared memory); divisions once per thread, carries per step. Grid extents are
+  // read from the kernel parameters, not held in registers (32-register cap).
+  __shared__ unsigned step[4];
+  unsigned color, h0, h1, h2;
+  unsigned i = blockIdx.x * kRT + threadIdx.x;
+  {
+    unsigned v = i;
+    h0 = v % (unsigned)g.cd[0][0];
+    v /= (unsigned)g.cd[0][0];
+    h1 = v % (unsigned)g.cd[0][1];
+    v /= (unsigned)g.cd[0][1];
+    h2 = v % (unsigned)g.cd[0][2];
+    color = v / (unsigned)g.cd[0][2];
+  }
+  if (threadIdx.x == 0) {
+    unsigned v = gridDim.x * kRT;
+    step[0] = v % (unsigned)g.cd[0][0];
+    v /= (unsigned)g.cd[0][0];
+    step[1] = v % (unsigned)g.cd[0][1];
+    v /= (unsigned)g.cd[0][1];
+    step[2] = v % (unsigned)g.cd[0][2];
+    step[3] = v / (unsigned)g.cd[0][2];
+  }
+  __syncthreads();
   double s[3] = {0.0, 0.0, 0.0};
-  for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < g.nv; i += (long long)gridDim.x * kRT) {
-    const unsigned color = unsigned(i / B), r = unsigned(i - (long long)color * B);
-    const unsigned h0 = r % d0, r1 = r / d0;
+  for (; i < (unsigned)g.nv; i += gridDim.x * kRT) {  // nv < 2^32 (host check)
     FastAddr fa;
-    fast_addr(g, int(color), int(h0), int(r1 % d1), int(r1 / d1), fa);
+    fast_addr(g, int(color), int(h0), int(h1), int(h2), fa);
     double q[8];
     load_q_fast(coeff, cl, fa, q);
     double acc[3] = {0.0, 0.0, 0.0};
@@ -601,9 +624,19 @@ __global__ void __launch_bounds__(kRT) macro_force_sums_kernel(GridGeo g, const 
       for (int c = 0; c < 3; ++c) acc[c] += q[ke] * c_fmacro[ke][load][c];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      f[3 * i + c] = acc[c];
+      f[3 * (size_t)i + c] = acc[c];
       s[c] += acc[c];
     }
+    h0 += step[0];
+    unsigned k = h0 >= (unsigned)g.cd[0][0];
+    h0 -= k * (unsigned)g.cd[0][0];
+    h1 += step[1] + k;
+    k = h1 >= (unsigned)g.cd[0][1];
+    h1 -= k * (unsigned)g.cd[0][1];
+    h2 += step[2] + k;
+    k = h2 >= (unsigned)g.cd[0][2];
+    h2 -= k * (unsigned)g.cd[0][2];
+    color += step[3] + k;
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -615,7 +648,8 @@ __global__ void __launch_bounds__(kRT) macro_force_sums_kernel(GridGeo g, const 
 template <typename TC>
 void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* partials, double* sums,
                              cudaStream_t s, ZLink<TC> cl) {
-  if (!fast_ok(g)) throw std::invalid_argument("fused macro force sums need an even grid");
+  if (!fast_ok(g) || g.nv + (long long)kReducePartials * kRT >= (1LL << 32))
+    throw std::invalid_argument("fused macro force sums need an even grid of < 2^32 vertices");
   const int nb = reduce_grid(g.nv);
   macro_force_sums_kernel<TC><<<nb, kRT, 0, s>>>(g, coeff, resolve(cl, coeff), load, f, partials);
   IHOM_LAUNCH_CHECK();

@@ -237,7 +237,7 @@ bool can_coarsen(const GridGeo& g) {  // inc/grid.hpp:47-51
 
 // ============================================================== Hierarchy
 template <typename T>
-Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab)
+Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab, int lean)
     : mat_(mat), penal_(penal), s_(s), slab_(slab) {
   for (int k = 0; k < 3; ++k)
     if (n[k] < 4) throw std::invalid_argument("grid resolution must be >= 4 per axis");
@@ -275,20 +275,6 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
     if (slab_.on() && !sharding && rep0_ > int(l)) rep0_ = int(l);
   }
   if (slab_.on() && !levels_[0].sharded) throw std::invalid_argument("level 0 cannot be split into these slabs");
-  for (size_t l = 0; l < levels_.size(); ++l) {
-    Level& L = levels_[l];
-    const size_t n3 = size_t(3 * L.g.nv);
-    L.u.alloc(n3);
-    L.f.alloc(n3);
-    L.r.alloc(n3);
-    IHOM_CUDA(cudaMemsetAsync(L.u.p, 0, sizeof(double) * n3, s_));
-    IHOM_CUDA(cudaMemsetAsync(L.f.p, 0, sizeof(double) * n3, s_));
-    IHOM_CUDA(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n3, s_));
-    if (l > 0) L.st.alloc(stencil_alloc(L.g.nv));
-  }
-  coeff_.alloc(size_t(levels_[0].g.nv));
-  ndof_c_ = int(3 * levels_.back().g.nv);
-  cwork_.alloc(size_t(3 * ndof_c_));
   red_.alloc(kRedDoubles);
   err_.alloc(1);
   IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
@@ -298,14 +284,32 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
   ws_.scalars = ws_.scalar + 8;
   ws_.flag = err_.p;
   IHOM_CUDA(cudaMallocHost(&h_pinned_, 64 * sizeof(double)));
+  lean_ = decide_lean(lean);
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    Level& L = levels_[l];
+    const size_t n3 = size_t(3 * L.g.nv);
+    // lean: the f64 fields the mixed_defect solver never touches are not allocated (level 0 keeps u and f;
+    // the replicated transition level keeps f, whose peer table is exchanged below)
+    const bool keep_u = !lean_ || l == 0, keep_f = keep_u || (slab_.on() && int(l) == rep0_), keep_r = !lean_;
+    if (keep_u) L.u.alloc(n3);
+    if (keep_f) L.f.alloc(n3);
+    if (keep_r) L.r.alloc(n3);
+    if (keep_u) IHOM_CUDA(cudaMemsetAsync(L.u.p, 0, sizeof(double) * n3, s_));
+    if (keep_f) IHOM_CUDA(cudaMemsetAsync(L.f.p, 0, sizeof(double) * n3, s_));
+    if (keep_r) IHOM_CUDA(cudaMemsetAsync(L.r.p, 0, sizeof(double) * n3, s_));
+    if (l > 0) L.st.alloc(stencil_alloc(L.g.nv));
+  }
+  coeff_.alloc(size_t(levels_[0].g.nv));
+  ndof_c_ = int(3 * levels_.back().g.nv);
+  cwork_.alloc(size_t(3 * ndof_c_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
   if (slab_.on()) {  // collective, same order on every slab
     coeff_l_ = link(coeff_.p);
     for (size_t l = 0; l < levels_.size(); ++l) {
       Level& L = levels_[l];
       if (L.sharded) {
-        L.ul = link(L.u.p);
-        L.rl = link(L.r.p);
+        if (L.u.p) L.ul = link(L.u.p);
+        if (L.r.p) L.rl = link(L.r.p);
         if (l > 0) L.stl = link(L.st.p);
       } else if (int(l) == rep0_) {
         L.fpeer = peer_table(slab_.fab->exchange(slab_.rank, L.f.p));
@@ -313,6 +317,43 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
       }
     }
   }
+}
+
+// Bytes per level-0 vertex of the device-resident layout at group size 1 without the energy cache
+// (distributed.py memory_plan): six f64 displacements, level-0 f64 u/f/r and ping-pong u, f32 inner
+// fields, coefficients, level >= 1 stencils, the density-side fields.
+constexpr double kResidentBytesPerVertex = 144 + 96 + 41 + 4 + 139 + 64;
+
+template <typename T>
+bool Hierarchy<T>::decide_lean(int request) {
+  if (request <= 0 || !std::is_same_v<T, float> || !fast_ok(levels_[0].g) || levels_.size() < 2) return false;
+  double want = request >= 2 ? 1.0 : 0.0;
+  if (request == 1) {
+    int dev = 0;
+    IHOM_CUDA(cudaGetDevice(&dev));
+    double share = 1.0;
+    if (slab_.on()) {  // slabs sharing this device split its free memory (one-hot by device ordinal)
+      double h[16] = {};
+      h[dev & 15] = 1.0;
+      IHOM_CUDA(cudaMemcpyAsync(ws_.scalars + 32, h, sizeof(h), cudaMemcpyHostToDevice, s_));
+      allreduce(ws_.scalars + 32, 16, false);
+      IHOM_CUDA(cudaMemcpyAsync(h, ws_.scalars + 32, sizeof(h), cudaMemcpyDeviceToHost, s_));
+      IHOM_CUDA(cudaStreamSynchronize(s_));
+      share = std::max(1.0, h[dev & 15]);
+    }
+    size_t free_b = 0, total_b = 0;
+    IHOM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    free_b = hbm_free_limit(free_b);
+    const double need = kResidentBytesPerVertex * double(levels_[0].g.nv) + 4e9 / share;
+    want = need > double(free_b) / share ? 1.0 : 0.0;
+  }
+  if (slab_.on()) {  // every slab takes the same layout
+    IHOM_CUDA(cudaMemcpyAsync(ws_.scalars + 32, &want, sizeof(double), cudaMemcpyHostToDevice, s_));
+    allreduce(ws_.scalars + 32, 1, true);
+    IHOM_CUDA(cudaMemcpyAsync(&want, ws_.scalars + 32, sizeof(double), cudaMemcpyDeviceToHost, s_));
+    IHOM_CUDA(cudaStreamSynchronize(s_));
+  }
+  return want > 0.5;
 }
 
 template <typename T>
@@ -665,7 +706,7 @@ void Hierarchy<T>::macro_force(int load) {  // src/fem.cpp:145-150
   Level& L0 = levels_[0];
   const ZLink<T> cl = slab_.on() ? coeff_l_ : ZLink<T>{};
   ProfScope p(s_, "macro_force", double(L0.g.nv) * (24.0 + sizeof(T)));
-  if (fast_ok(L0.g) && knob("MACRO_SUMS", 1)) {
+  if (fast_ok(L0.g) && L0.g.nv < (1LL << 31) && knob("MACRO_SUMS", 1)) {
     launch_macro_force_sums<T>(L0.g, coeff_.p, load, L0.f.p, ws_.partials, ws_.scalars + kMacroSums + 3 * cur_rhs_,
                                s_, cl);
     msum_f_[cur_rhs_] = L0.f.p;
@@ -872,7 +913,7 @@ void Hierarchy<T>::coarsest_f32() {
 
 template <typename T>
 bool Hierarchy<T>::fused_update_ok() const {
-  return std::is_same_v<T, float> && knob("FUSED_UPDATE", 1) != 0 && sweep_ok(levels_[0].g);
+  return !lean_ && std::is_same_v<T, float> && knob("FUSED_UPDATE", 1) != 0 && sweep_ok(levels_[0].g);
 }
 
 template <typename T>
@@ -1095,7 +1136,7 @@ double Hierarchy<T>::finish_defect_cycle(double* slot) {
 // ---------------------------------------------------------------- lockstep RHS groups
 template <typename T>
 bool Hierarchy<T>::pair_ok(const SolverOptions& opts) const {
-  return std::is_same_v<T, float> && opts.mode == kMixedDefect && knob("RHS_PAIRS", 1) != 0 &&
+  return !lean_ && std::is_same_v<T, float> && opts.mode == kMixedDefect && knob("RHS_PAIRS", 1) != 0 &&
          fast_ok(levels_[0].g) && num_levels() > 1;
 }
 
@@ -1596,19 +1637,178 @@ void Hierarchy<T>::bench_op(const std::string& op, int reps) {
 }
 
 // ============================================================== Homogenizer
+namespace {
+int lean_request(const SolverOptions& opts) {  // Hierarchy lean argument from the U_HOST knob
+  const int k = knob("U_HOST", 0);
+  if (k < 0 || opts.mode != kMixedDefect) return 0;
+  return k == 0 ? 1 : 2;
+}
+}  // namespace
+
 template <typename T>
 Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts,
                             cudaStream_t s, Slab slab)
-    : hier_(n, mat, penal, s, slab), opts_(opts), penal_(penal) {
+    : hier_(n, mat, penal, s, slab, lean_request(opts)), opts_(opts), penal_(penal) {
   const long long nv = hier_.geo(0).nv;
   rho_.alloc(size_t(nv));
+  seed_.alloc(36);
+  if (hier_.lean()) {
+    host_u_ = knob("U_HOST", 0) == 1 ? 1 : 2;
+    const size_t n3 = size_t(3 * nv);
+    for (int i = 0; i < 6; ++i) {
+      IHOM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hu32_[size_t(i)]), sizeof(float) * n3));
+      std::memset(hu32_[size_t(i)], 0, sizeof(float) * n3);
+      if (host_u_ == 2) {
+        IHOM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hu64_[size_t(i)]), sizeof(double) * n3));
+        std::memset(hu64_[size_t(i)], 0, sizeof(double) * n3);
+      }
+    }
+    hier_.ensure_inner();
+    IHOM_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    IHOM_CUDA(cudaEventCreateWithFlags(&ev_solved_, cudaEventDisableTiming));
+    IHOM_CUDA(cudaEventCreateWithFlags(&ev_staged_out_, cudaEventDisableTiming));
+    IHOM_CUDA(cudaEventRecord(ev_staged_out_, cs_));
+    float* u0 = reinterpret_cast<float*>(hier_.level_u(0));
+    float* f0 = reinterpret_cast<float*>(hier_.level_f(0));
+    snap_ = {u0, u0 + n3, f0, f0 + n3, hier_.inner_e(0), hier_.inner_f(0)};
+    for (int i = 0; i < 6; ++i) snapl_[size_t(i)] = hier_.link(snap_[size_t(i)]);  // collective on z-slabs
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
   for (auto& u : u_) {
     u.alloc(size_t(3 * nv));
     IHOM_CUDA(cudaMemsetAsync(u.p, 0, sizeof(double) * 3 * nv, s));
   }
-  seed_.alloc(36);
   IHOM_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < 6; ++i) ul_[size_t(i)] = hier_.link(u_[size_t(i)].p);  // collective on z-slabs
+}
+
+template <typename T>
+Homogenizer<T>::~Homogenizer() {
+  hier_.quiesce();
+  if (cs_) {
+    cudaStreamSynchronize(cs_);
+    cudaStreamDestroy(cs_);
+  }
+  if (ev_solved_) cudaEventDestroy(ev_solved_);
+  if (ev_staged_out_) cudaEventDestroy(ev_staged_out_);
+  for (float* p : hu32_)
+    if (p) cudaFreeHost(p);
+  for (double* p : hu64_)
+    if (p) cudaFreeHost(p);
+}
+
+template <typename T>
+void Homogenizer<T>::read_displacement(int i, double* dst) {
+  const long long n3 = 3 * hier_.geo(0).nv;
+  cudaStream_t s = hier_.stream();
+  if (cs_) IHOM_CUDA(cudaStreamSynchronize(cs_));  // the last write-back has landed
+  if (host_u_ == 2) {
+    IHOM_CUDA(cudaMemcpyAsync(dst, hu64_[size_t(i)], sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+  } else if (host_u_ == 1) {
+    std::vector<double> w(static_cast<size_t>(n3));
+    for (long long k = 0; k < n3; ++k) w[size_t(k)] = double(hu32_[size_t(i)][k]);
+    IHOM_CUDA(cudaMemcpyAsync(dst, w.data(), sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+  } else {
+    IHOM_CUDA(cudaMemcpyAsync(dst, u_[size_t(i)].p, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+  }
+  IHOM_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void Homogenizer<T>::write_displacement(int i, const double* src) {
+  const long long n3 = 3 * hier_.geo(0).nv;
+  cudaStream_t s = hier_.stream();
+  ecache_valid_ = false;  // cached energies no longer describe the fields
+  if (!host_u_) {
+    IHOM_CUDA(cudaMemcpyAsync(u_[size_t(i)].p, src, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+    IHOM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  IHOM_CUDA(cudaStreamSynchronize(cs_));
+  std::vector<double> w;
+  double* h = hu64_[size_t(i)];
+  if (!h) {
+    w.resize(static_cast<size_t>(n3));
+    h = w.data();
+  }
+  IHOM_CUDA(cudaMemcpyAsync(h, src, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+  IHOM_CUDA(cudaStreamSynchronize(s));
+  for (long long k = 0; k < n3; ++k) hu32_[size_t(i)][k] = float(h[k]);  // round to nearest, as the device cast
+  snaps_ready_ = false;
+}
+
+// The six cell problems with host-staged displacements: one device working field (level-0 u), the warm
+// start staged in and the result (and its f32 snapshot) staged out around each solve; then the snapshots
+// are placed in the level-0 buffers for the C^H / sensitivity passes. Same solves, same order, same
+// arithmetic as the device-resident loop with group size 1 (bitwise equal displacements in mode 2).
+// PCIe duplex: solve i's write-back (from the inner residual e_r0 and, mode 2, an f64 copy in f0, both
+// free until the next macro force) runs on the copy stream while solve i+1's warm start comes in.
+template <typename T>
+CellSolveStats Homogenizer<T>::solve_host_staged() {
+  if (comm_ && comm_->size() > 1) throw std::invalid_argument("host-staged displacements and the load-case split are exclusive");
+  if (opts_.mode != kMixedDefect) throw StateError("host-staged displacements need the mixed_defect solver");
+  const long long nv = hier_.geo(0).nv, n3 = 3 * nv;
+  cudaStream_t s = hier_.stream();
+  snaps_ready_ = false;
+  ecache_valid_ = false;
+  double* u = hier_.level_u(0);
+  double* f = hier_.level_f(0);
+  const ZLink<double> ul = hier_.ulink(0);
+  float* out32 = hier_.inner_r(0);  // f32 write-back staging
+  float* in32 = hier_.inner_f(0);   // f32 warm-start staging (mode 1)
+  CellSolveStats out;
+  for (int i = 0; i < 6; ++i) {
+    hier_.sync();  // coefficients of the neighbouring slabs are current; nobody still reads u / e_r
+    {
+      ProfScope p(s, "host_stage", double(n3) * (host_u_ == 2 ? 8.0 : 4.0));
+      if (host_u_ == 2) {
+        IHOM_CUDA(cudaMemcpyAsync(u, hu64_[size_t(i)], sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+      } else {
+        IHOM_CUDA(cudaMemcpyAsync(in32, hu32_[size_t(i)], sizeof(float) * n3, cudaMemcpyHostToDevice, s));
+        launch_convert<float, double>(in32, u, n3, s);
+      }
+    }
+    IHOM_CUDA(cudaStreamWaitEvent(s, ev_staged_out_, 0));  // f0 and e_r0 are read out
+    hier_.macro_force(i);
+    const SolveStats st = hier_.solve_bound(u, opts_, ul);
+    hier_.sync();  // the neighbours' last halo reads of e_r0 are done
+    {
+      ProfScope p(s, "vector", double(n3) * (host_u_ == 2 ? 36.0 : 12.0));
+      launch_convert<double, float>(u, out32, n3, s);
+      if (host_u_ == 2) IHOM_CUDA(cudaMemcpyAsync(f, u, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+    }
+    IHOM_CUDA(cudaEventRecord(ev_solved_, s));
+    IHOM_CUDA(cudaStreamWaitEvent(cs_, ev_solved_, 0));
+    IHOM_CUDA(cudaMemcpyAsync(hu32_[size_t(i)], out32, sizeof(float) * n3, cudaMemcpyDeviceToHost, cs_));
+    if (host_u_ == 2)
+      IHOM_CUDA(cudaMemcpyAsync(hu64_[size_t(i)], f, sizeof(double) * n3, cudaMemcpyDeviceToHost, cs_));
+    IHOM_CUDA(cudaEventRecord(ev_staged_out_, cs_));
+    out.total_cycles += st.cycles;  // combined in load order, exactly as the reference loop does
+    if (st.rel_residual >= out.worst_residual) {
+      out.worst_residual = st.rel_residual;
+      out.worst_load = i;
+    }
+    if (!st.converged) out.converged = false;
+  }
+  ensure_snapshots();
+  return out;
+}
+
+template <typename T>
+void Homogenizer<T>::ensure_snapshots() {
+  if (snaps_ready_) return;
+  const long long n3 = 3 * hier_.geo(0).nv;
+  cudaStream_t s = hier_.stream();
+  hier_.sync();  // no slab still reads the level-0 buffers the snapshots overwrite
+  IHOM_CUDA(cudaStreamWaitEvent(s, ev_staged_out_, 0));  // the last write-back is out of f0 / e_r0 and in hu32_
+  {
+    ProfScope p(s, "host_stage", double(n3) * 4.0 * 6.0);
+    for (int i = 0; i < 6; ++i)
+      IHOM_CUDA(cudaMemcpyAsync(snap_[size_t(i)], hu32_[size_t(i)], sizeof(float) * n3, cudaMemcpyHostToDevice, s));
+  }
+  hier_.sync();  // every slab's snapshots are in place before any reads a neighbour's top plane
+  snaps_ready_ = true;
 }
 
 template <typename T>
@@ -1621,6 +1821,7 @@ void Homogenizer<T>::set_density(const double* rho) {  // src/homogenization.cpp
 template <typename T>
 CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cpp:23-40
   if (!density_set_) throw StateError("set_density before solve_cell_problems");
+  if (host_u_) return solve_host_staged();
   const GridGeo& g = hier_.geo(0);
   const bool multi = comm_ && comm_->size() > 1;
   const bool slabs = hier_.slab().on();
@@ -1688,16 +1889,29 @@ CellSolveStats Homogenizer<T>::solve_cell_problems() {  // src/homogenization.cp
 
 template <typename T>
 void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp:58-111
+  Workspace& ws = hier_.workspace();
+  const Material& m = hier_.material();
+  const long long nv = hier_.geo(0).nv;
+  if (host_u_) {  // f32 snapshots: the values the mixed mode rounds the f64 fields to (f64 energies)
+    ensure_snapshots();
+    const float* u[6];
+    const float* uhi[6];
+    for (int i = 0; i < 6; ++i) {
+      u[i] = snap_[size_t(i)];
+      uhi[i] = snapl_[size_t(i)].hi ? snapl_[size_t(i)].hi : u[i];
+    }
+    ProfScope p(hier_.stream(), "tensor", double(nv) * 80.0);
+    launch_effective_tensor<float>(hier_.geo(0), u, rho_.p, penal_, true, m.lambda(), m.mu(), ws.partials,
+                                   ws.scalars + 16, hier_.stream(), uhi, nullptr);
+    ecache_valid_ = false;
+  } else {
   const double* u[6];
   const double* uhi[6];
   for (int i = 0; i < 6; ++i) {
     u[i] = u_[size_t(i)].p;
     uhi[i] = ul_[size_t(i)].hi ? ul_[size_t(i)].hi : u[i];
   }
-  Workspace& ws = hier_.workspace();
-  const Material& m = hier_.material();
   hier_.sync();  // the six fields of the slab above are final
-  const long long nv = hier_.geo(0).nv;
   const size_t esz = energy_f32(std::is_same_v<T, float>) ? sizeof(float) : sizeof(double);
   void* ec = nullptr;
   if (knob("ENERGY_CACHE", 1)) {
@@ -1718,6 +1932,7 @@ void Homogenizer<T>::effective_tensor(double C[36]) {  // src/homogenization.cpp
                                     ws.partials, ws.scalars + 16, hier_.stream(), uhi, ec);
   }
   ecache_valid_ = ec != nullptr;
+  }
   hier_.allreduce(ws.scalars + 16, 21);  // element sums over all slabs
   double c21[21];
   IHOM_CUDA(cudaMemcpyAsync(c21, ws.scalars + 16, sizeof(c21), cudaMemcpyDeviceToHost, hier_.stream()));
@@ -1737,6 +1952,21 @@ void Homogenizer<T>::tensor_sensitivity(const double seed[36], double* out) {  /
   for (int i = 0; i < 6; ++i)
     for (int j = 0; j < 6; ++j) s[i * 6 + j] = 0.5 * (seed[i * 6 + j] + seed[j * 6 + i]);
   IHOM_CUDA(cudaMemcpyAsync(seed_.p, s, sizeof(s), cudaMemcpyHostToDevice, hier_.stream()));
+  if (host_u_) {
+    ensure_snapshots();
+    const float* u[6];
+    const float* uhi[6];
+    for (int i = 0; i < 6; ++i) {
+      u[i] = snap_[size_t(i)];
+      uhi[i] = snapl_[size_t(i)].hi ? snapl_[size_t(i)].hi : u[i];
+    }
+    const Material& m = hier_.material();
+    ProfScope p(hier_.stream(), "sensitivity", double(hier_.geo(0).nv) * 88.0);
+    launch_tensor_sensitivity<float>(hier_.geo(0), u, rho_.p, penal_, true, m.lambda(), m.mu(), seed_.p, out,
+                                     hier_.stream(), uhi, hier_.global_nv(0));
+    IHOM_CUDA(cudaStreamSynchronize(hier_.stream()));
+    return;
+  }
   const double* u[6];
   const double* uhi[6];
   for (int i = 0; i < 6; ++i) {

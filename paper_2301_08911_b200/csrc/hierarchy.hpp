@@ -115,7 +115,11 @@ class Hierarchy {
  public:
   using value_type = T;
   // n = dims of the WHOLE grid; with a slab only planes [rank t, (rank+1) t) are stored
-  Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab = {});
+  // lean: host-staged-displacement layout (memory lever): 0 never, 1 when the device-resident
+  // layout would not fit this device's free HBM (decided collectively over the slabs), 2 always. A lean
+  // hierarchy (mixed precision, even grids) allocates no level-0 f64 r and no f64 u/f/r on coarser
+  // levels (the mixed_defect solver never reads them), no ping-pong u and no lockstep RHS slots.
+  Hierarchy(const int n[3], const Material& mat, double penal, cudaStream_t s, Slab slab = {}, int lean = 0);
   ~Hierarchy() {
     quiesce();
     try {
@@ -200,6 +204,12 @@ class Hierarchy {
   }
   const ZLink<T>& coeff_link() const { return coeff_l_; }
 
+  bool lean() const { return lean_; }
+  void ensure_inner();
+  float* inner_e(int l) { return levels_[size_t(l)].eu.p; }  // f32 inner fields of the live RHS
+  float* inner_f(int l) { return levels_[size_t(l)].ef.p; }
+  float* inner_r(int l) { return levels_[size_t(l)].er.p; }
+
   // Runs one kernel family `reps` times on the current level data (benchmark / ncu target).
   void bench_op(const std::string& op, int reps);
   cudaStream_t stream() const { return s_; }
@@ -233,7 +243,6 @@ class Hierarchy {
   void prolong_from(int l, const double* uc, double* u, ZLink<double> cl);
   void factor_coarsest();
   void check_error(const char* where);
-  void ensure_inner();
   double v_cycle_defect(const SolverOptions& opts);
   void relax_f32(int l, int sweeps, bool reverse = false, bool zero_start = false);
   bool zero_start_ok(int l) const;  // the level's GS kernels support a zero-start first sweep
@@ -245,6 +254,7 @@ class Hierarchy {
                                                 // ||f0 - K u0||; update: u0 += e0 first, folded into the same
                                                 // sweep; slot: leave this slab's ||r||^2 there, no read-back
   bool fused_update_ok() const;                 // the defect sweep can fold in the u += e update
+  bool decide_lean(int request);                // constructor: the lean layout (collective on z-slabs)
   void restore_home();                          // end of a solve: the result back in the bound buffer
 
   Material mat_;
@@ -309,6 +319,7 @@ class Hierarchy {
   ZLink<double> u_alt_l_{};
   double fnorm0_ = 0.0;
   const double* msum_f_[kMaxRhsGroup] = {};  // f whose component sums macro_force left (per RHS)
+  bool lean_ = false;
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;
   DevBuf<double> npart_;  // per-block |r|^2 partials of the fused defect residual
@@ -323,7 +334,7 @@ class Homogenizer {
  public:
   Homogenizer(const int n[3], const Material& mat, double penal, const SolverOptions& opts, cudaStream_t s,
               Slab slab = {});
-  ~Homogenizer() { hier_.quiesce(); }
+  ~Homogenizer();
   Homogenizer(const Homogenizer&) = delete;
   Homogenizer& operator=(const Homogenizer&) = delete;
 
@@ -332,9 +343,16 @@ class Homogenizer {
   void effective_tensor(double C[36]);
   void tensor_sensitivity(const double seed[36], double* out_dev);
 
-  double* displacement(int i) { return u_[size_t(i)].p; }
-  // callers that write displacement(i) directly must drop the cached element energies
-  void displacements_changed() { ecache_valid_ = false; }
+  // load case i's displacement field (3 nv doubles) from / into a device buffer
+  void read_displacement(int i, double* dst_dev);
+  void write_displacement(int i, const double* src_dev);
+  // Memory lever (the paper keeps the six fields in host-backed unified memory and evaluates
+  // from f32 copies): 0 = six device-resident f64 fields; 2 = host-staged: the
+  // f64 fields live in pinned host memory, each solve stages its warm start in and the result out, and
+  // C^H / sensitivities read f32 snapshots placed in the level-0 buffers the solver has released;
+  // 1 = as 2 with only the f32 snapshots on the host (warm starts from them). Knob U_HOST: -1 never,
+  // 0 (default) when the device-resident layout does not fit, 1 / 2 forced.
+  int host_staged() const { return host_u_; }
   // Multi-GPU: load case i is solved by rank owner[i], then broadcast to all ranks.
   void set_comm(Comm* c, const int owner[6]) {
     comm_ = c;
@@ -359,6 +377,17 @@ class Homogenizer {
   DevBuf<unsigned char> ecache_;
   bool ecache_valid_ = false;
   bool ecache_skip_ = false;  // not enough HBM for the energy cache (decided once)
+  // host-staged displacements (host_u_ > 0)
+  int host_u_ = 0;
+  std::array<double*, 6> hu64_{};  // pinned f64 fields (mode 2)
+  std::array<float*, 6> hu32_{};   // pinned f32 snapshots
+  std::array<float*, 6> snap_{};   // device snapshot slots: halves of level-0 u and f, inner e0 and f0
+  std::array<ZLink<float>, 6> snapl_{};
+  bool snaps_ready_ = false;
+  cudaStream_t cs_ = nullptr;   // copy stream: a solve's write-back overlaps the next solve's stage-in
+  cudaEvent_t ev_solved_ = nullptr, ev_staged_out_ = nullptr;
+  CellSolveStats solve_host_staged();
+  void ensure_snapshots();
   Comm* comm_ = nullptr;
   int owner_[6] = {0, 0, 0, 0, 0, 0};
 };

@@ -14,6 +14,9 @@
 #include "hada_gen.cuh"
 #include "bulk.cuh"
 
+#include <algorithm>
+#include <type_traits>
+
 namespace ihomgpu {
 
 constexpr int kHT = 64;            // threads (elements) per block
@@ -345,9 +348,10 @@ __device__ __forceinline__ void modal_from_dhat(const double dh[24], double b[kM
   b[17] = m[9] * dh[23];
 }
 
-// modal vector of one load case from its 8 corner displacements (AoS f64, loc[] / top-plane pointer)
-template <bool SNAP>
-__device__ __forceinline__ void modal_vector(const double* __restrict__ ui, const double* __restrict__ uz,
+// modal vector of one load case from its 8 corner displacements (AoS, loc[] / top-plane pointer). TU = float:
+// the f32 snapshots of the host-staged mode (exactly the values SNAP rounds f64 fields to)
+template <bool SNAP, typename TU = double>
+__device__ __forceinline__ void modal_vector(const TU* __restrict__ ui, const TU* __restrict__ uz,
                                              const unsigned loc[8], int lc, double b[kModes]) {
   double dh[24];
 #pragma unroll
@@ -355,7 +359,7 @@ __device__ __forceinline__ void modal_vector(const double* __restrict__ ui, cons
     double V[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double v = __ldg(((j >> 2) & 1 ? uz : ui) + 3 * (size_t)loc[j] + c);
+      const double v = double(__ldg(((j >> 2) & 1 ? uz : ui) + 3 * (size_t)loc[j] + c));
       V[j] = SNAP ? snap_f32_bits(v) : v;
     }
 #pragma unroll
@@ -402,15 +406,15 @@ __device__ __forceinline__ void gram_pairs(const double b[3][kModes], int x, dou
 // Out: eo[6] Gram entries of the own cases (00 01 02 11 12 22 in local indices), ex[6] cross entries
 // (local own i, partner j): (0,0) (1,1) (2,2) (0,1) (0,2) (1,2). The even lane's cross entries are
 // (i, 3+j); the odd lane's upper ones are (j, 3+i) with j < i... see energy_index().
-template <bool SNAP>
+template <bool SNAP, typename TU = double>
 __device__ __forceinline__ void pair_energies(const U6& uu, const unsigned loc[8], bool top, int role, double eo[6],
                                               double ex[6]) {
   double b[3][kModes];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double* ui = static_cast<const double*>(role ? uu.p[3 + a] : uu.p[a]);
-    const double* uz = top ? static_cast<const double*>(role ? uu.hi[3 + a] : uu.hi[a]) : ui;
-    modal_vector<SNAP>(ui, uz, loc, 3 * role + a, b[a]);
+    const TU* ui = static_cast<const TU*>(role ? uu.p[3 + a] : uu.p[a]);
+    const TU* uz = top ? static_cast<const TU*>(role ? uu.hi[3 + a] : uu.hi[a]) : ui;
+    modal_vector<SNAP, TU>(ui, uz, loc, 3 * role + a, b[a]);
   }
   gram_pairs(b, 1, eo, ex);
 }
@@ -437,7 +441,7 @@ __host__ __device__ __forceinline__ constexpr int energy_index(int role, int m) 
 // (x % 32 == 0, y % 2 == 0 grids) and marches up z; else grid-stride over elements. 2 lanes per element.
 constexpr int kPT = 128;
 
-template <bool SNAP>
+template <bool SNAP, typename TU = double>
 __global__ void __launch_bounds__(kPT) tensor_pair_kernel(GridGeo g, U6 uu, const double* __restrict__ rho,
                                                           double penal, double* partials, double* __restrict__ ecache) {
   __shared__ double sh[32];
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kPT) tensor_pair_kernel(GridGeo g, U6 uu, cons
     unsigned loc[8];
     corner_locs(g, ex, ey, ez, loc);
     double E[12];
-    pair_energies<SNAP>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
+    pair_energies<SNAP, TU>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
     if (!valid) continue;
     if (ecache) {  // [21][nv]
 #pragma unroll
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(kPT) tensor_pair_kernel(GridGeo g, U6 uu, cons
 
 // Sensitivity with the pair energies (no cache): the odd lane hands its 9 stored energies to the even
 // lane, which forms sum_ij s_ij E_ij in the cached kernel's order (bit-identical to sens_cached_kernel).
-template <bool SNAP>
+template <bool SNAP, typename TU = double>
 __global__ void __launch_bounds__(kPT) sens_pair_kernel(GridGeo g, U6 uu, const double* __restrict__ rho, double penal,
                                                         const double* __restrict__ seed, double inv_m,
                                                         double* __restrict__ out) {
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(kPT) sens_pair_kernel(GridGeo g, U6 uu, const 
   unsigned loc[8];
   corner_locs(g, ex, ey, ez, loc);
   double E[12];
-  pair_energies<SNAP>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
+  pair_energies<SNAP, TU>(uu, loc, ez + 1 == g.n[2], role, E, E + 6);
   double all[21];
 #pragma unroll
   for (int m = 0; m < 12; ++m) {
@@ -771,7 +775,12 @@ void launch_effective_tensor(const GridGeo& g, const TN* const u[6], const doubl
     uu.hi[i] = uhi ? uhi[i] : u[i];
   }
   const bool te32 = energy_f32(snap);
-  if (htensor() && !te32 && tensor_stage_ok(g, uu.p, uu.hi)) {  // f64 energies, bulk-staged column tiles
+  if constexpr (std::is_same_v<TN, float>) {  // f32 snapshots (host-staged displacements): f64 energies
+    if (te32) throw std::invalid_argument("f32 displacement snapshots take the f64 energy path");
+    blocks = std::min<long long>((g.nv + 63) / 64, kReducePartials);
+    tensor_pair_kernel<false, float><<<(unsigned)blocks, kPT, 0, s>>>(g, uu, rho, penal, partials,
+                                                                     static_cast<double*>(ecache));
+  } else if (htensor() && !te32 && tensor_stage_ok(g, uu.p, uu.hi)) {  // f64 energies, bulk-staged column tiles
     static int occ = 0;
     if (!occ) {
       IHOM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tensor_stage_kernel<true>, kPT, kStSmem));
@@ -886,7 +895,10 @@ void launch_tensor_sensitivity(const GridGeo& g, const TN* const u[6], const dou
   }
   const double inv_m = 1.0 / double(m_total > 0 ? m_total : g.nv);
   const bool te32 = energy_f32(snap);
-  if (htensor() && !te32) {
+  if constexpr (std::is_same_v<TN, float>) {  // f32 snapshots (host-staged displacements)
+    if (te32) throw std::invalid_argument("f32 displacement snapshots take the f64 energy path");
+    sens_pair_kernel<false, float><<<ceil_div(2 * g.nv, kPT), kPT, 0, s>>>(g, uu, rho, penal, sym_seed36, inv_m, out);
+  } else if (htensor() && !te32) {
     if (snap)
       sens_pair_kernel<true><<<ceil_div(2 * g.nv, kPT), kPT, 0, s>>>(g, uu, rho, penal, sym_seed36, inv_m, out);
     else
@@ -916,5 +928,10 @@ template void launch_effective_tensor<double>(const GridGeo&, const double* cons
 template void launch_tensor_sensitivity<double>(const GridGeo&, const double* const[6], const double*, double, bool,
                                                 double, double, const double*, double*, cudaStream_t,
                                                 const double* const*, long long);
+template void launch_effective_tensor<float>(const GridGeo&, const float* const[6], const double*, double, bool, double,
+                                             double, double*, double*, cudaStream_t, const float* const*, void*);
+template void launch_tensor_sensitivity<float>(const GridGeo&, const float* const[6], const double*, double, bool,
+                                               double, double, const double*, double*, cudaStream_t,
+                                               const float* const*, long long);
 
 }  // namespace ihomgpu

@@ -96,19 +96,35 @@ def ipc_fabric(rank: int, nranks: int, device: int = 0):
 
 # ---------------------------------------------------------------- memory plan (estimate)
 # Bytes per level-0 vertex (= per element) of one z-slab in mixed precision, mixed_defect solver
-# (DESIGN.md 2/6): six persistent f64 u^i (144), level-0 f64 u/f/r + ping-pong u (96), level-0 f32 inner
-# e/f/r (36), coefficients (4), level-1/2/... f32 stencils (243 x 4 B x (1/8 + 1/64 + ...) = 139),
-# density side (7 f64 fields, 56); optional: f64 energy cache (168), each extra RHS of a lockstep group (89).
-_BASE_B = 144 + 96 + 36 + 4 + 139 + 56
+# (DESIGN.md 2/6/7): six persistent f64 u^i (144), level-0 f64 u/f/r + ping-pong u (96), f32 inner e/f/r
+# on every level (36 x 8/7 = 41), coefficients (4), level-1/2/... f32 stencils (243 x 4 B x (1/8 + 1/64 +
+# ...) = 139), density side (the optimiser's 7 f64 fields + the homogenizer's copy, 64); optional: f64
+# energy cache (168), each extra RHS of a lockstep group (89).
+# Host-staged layout (U_HOST, the memory lever): the six u^i in pinned host memory, level-0 f64 u and f
+# only, no ping-pong, no groups, no cache: 48 + 41 + 4 + 139 + 64 = 296 B on the device (measured: 512^3
+# 39.8 GB, 1024 x 1024 x 512 = one slab of 1024^3 on 2 GPUs 159 GB; profiles/host_staged_r02.md), plus
+# 216 B of pinned host memory per vertex.
+_BASE_B = 144 + 96 + 41 + 4 + 139 + 64
+_HOST_STAGED_B = 48 + 41 + 4 + 139 + 64
 _CACHE_B = 168
 _GROUP_B = 89
 
 
-def memory_plan(reso: int, nranks: int, group: int = 1, energy_cache: bool = False) -> dict:
+def memory_plan(reso: int, nranks: int, group: int = 1, energy_cache: bool = False,
+                host_staged: bool = False) -> dict:
     """Estimated HBM per GPU (GB) of a reso^3 run on nranks z-slabs, and whether it fits a 180 GB B200
-    (leaving 8 GB headroom). The library adapts the group size and the energy cache to the free HBM."""
+    (leaving 8 GB headroom). The library adapts the group size and the energy cache to the free HBM and
+    switches to the host-staged layout when even the minimal device-resident one does not fit."""
     nv = reso ** 3 / nranks
-    per_vertex = _BASE_B + (_CACHE_B if energy_cache else 0) + _GROUP_B * (group - 1)
+    if host_staged:
+        per_vertex = _HOST_STAGED_B
+        group, energy_cache = 1, False
+    else:
+        per_vertex = _BASE_B + (_CACHE_B if energy_cache else 0) + _GROUP_B * (group - 1)
     gb = nv * per_vertex / 1e9
-    return {"reso": reso, "nranks": nranks, "group": group, "energy_cache": energy_cache,
-            "gb_per_gpu": round(gb, 1), "fits_b200": gb <= 172.0}
+    out = {"reso": reso, "nranks": nranks, "group": group, "energy_cache": energy_cache,
+           "gb_per_gpu": round(gb, 1), "fits_b200": gb <= 172.0}
+    if host_staged:
+        out["host_staged"] = True
+        out["pinned_host_gb_per_gpu"] = round(nv * 216 / 1e9, 1)
+    return out

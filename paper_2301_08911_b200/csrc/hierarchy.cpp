@@ -1670,7 +1670,8 @@ Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, c
     IHOM_CUDA(cudaEventRecord(ev_staged_out_, cs_));
     float* u0 = reinterpret_cast<float*>(hier_.level_u(0));
     float* f0 = reinterpret_cast<float*>(hier_.level_f(0));
-    snap_ = {u0, u0 + n3, f0, f0 + n3, hier_.inner_e(0), hier_.inner_f(0)};
+    // snapshots 4 and 5 go last, into f0: the last solve's write-back still reads f0 (ensure_snapshots)
+    snap_ = {u0, u0 + n3, hier_.inner_e(0), hier_.inner_f(0), f0, f0 + n3};
     for (int i = 0; i < 6; ++i) snapl_[size_t(i)] = hier_.link(snap_[size_t(i)]);  // collective on z-slabs
     IHOM_CUDA(cudaStreamSynchronize(s));
     return;
@@ -1801,11 +1802,14 @@ void Homogenizer<T>::ensure_snapshots() {
   const long long n3 = 3 * hier_.geo(0).nv;
   cudaStream_t s = hier_.stream();
   hier_.sync();  // no slab still reads the level-0 buffers the snapshots overwrite
-  IHOM_CUDA(cudaStreamWaitEvent(s, ev_staged_out_, 0));  // the last write-back is out of f0 / e_r0 and in hu32_
   {
     ProfScope p(s, "host_stage", double(n3) * 4.0 * 6.0);
-    for (int i = 0; i < 6; ++i)
+    // snapshots 0-3 (written back before the last solve began) into u0 / e0 / f0-inner while the last
+    // write-back (from f0 and e_r0 into hu32_[5]) may still run on the copy stream
+    for (int i = 0; i < 6; ++i) {
+      if (i == 4) IHOM_CUDA(cudaStreamWaitEvent(s, ev_staged_out_, 0));
       IHOM_CUDA(cudaMemcpyAsync(snap_[size_t(i)], hu32_[size_t(i)], sizeof(float) * n3, cudaMemcpyHostToDevice, s));
+    }
   }
   hier_.sync();  // every slab's snapshots are in place before any reads a neighbour's top plane
   snaps_ready_ = true;

@@ -381,7 +381,7 @@ class Homogenizer {
   int host_u_ = 0;
   std::array<double*, 6> hu64_{};  // pinned f64 fields (mode 2)
   std::array<float*, 6> hu32_{};   // pinned f32 snapshots
-  std::array<float*, 6> snap_{};   // device snapshot slots: halves of level-0 u and f, inner e0 and f0
+  std::array<float*, 6> snap_{};   // device snapshot slots: halves of level-0 u, inner e0 / f0, halves of f0
   std::array<ZLink<float>, 6> snapl_{};
   bool snaps_ready_ = false;
   cudaStream_t cs_ = nullptr;   // copy stream: a solve's write-back overlaps the next solve's stage-in

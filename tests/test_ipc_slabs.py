@@ -30,7 +30,7 @@ def _seed():
     return s
 
 
-def _worker(rank, world, port, n, phys, mode, q):
+def _worker(rank, world, port, n, phys, mode, q, host=0):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     try:
@@ -41,9 +41,11 @@ def _worker(rank, world, port, n, phys, mode, q):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
+        ih.set_knob("U_HOST", host)  # 2: host-staged displacements, snapshot links over CUDA IPC
         fab = dd2.ipc_fabric(rank, world, device=0)
         hom = ih.Homogenizer(n, penal=1.0, precision="mixed", opts=ih.SolverOptions(tol=1e-2, mode=mode),
                              fabric=fab, rank=rank)
+        assert hom.host_staged == host
         z0, t = dd2.slab_planes(n, world, rank)
         assert (hom.z0, hom.planes) == (z0, t)
         hom.set_density(np.ascontiguousarray(phys[z0 * n * n:(z0 + t) * n * n]))
@@ -59,8 +61,8 @@ def _worker(rank, world, port, n, phys, mode, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["vcycle", "mixed_defect"])
-def test_ipc_two_process_slabs_match_single_domain(ih, mode):
+@pytest.mark.parametrize("mode,host", [("vcycle", 0), ("mixed_defect", 0), ("mixed_defect", 2)])
+def test_ipc_two_process_slabs_match_single_domain(ih, mode, host):
     import torch.multiprocessing as mp
     n = 32
     rho, _ = ih.init_trig(n, 2, 0, 0.3)
@@ -73,7 +75,7 @@ def test_ipc_two_process_slabs_match_single_domain(ih, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, phys, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, phys, mode, q, host)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in range(2)], key=lambda x: x[0])

@@ -9,7 +9,6 @@
 // with TA = double this avoids the per-coefficient f32->f64 conversion
 // (F2F, ~16/clk/SM on B200, measured) the reference's float merge would need.
 #include "kernels.hpp"
-#include "reduce.cuh"
 #include "ku_gen.cuh"
 #include "hada_gen.cuh"
 
@@ -576,84 +575,64 @@ void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, 
   IHOM_LAUNCH_CHECK();
 }
 
-// Macro force with the component sums of f folded into the same pass: the
-// reduction's own partition (reduce_grid blocks of kRT threads striding over the
-// vertex index) and fold, so the sums equal launch_comp_sums(f) bit for bit and
-// project_norm0 skips its read of f. The vertex index is decoded into the
-// colour-block coordinates fast_addr takes (colour-major, then h0, h1, h2).
+// Macro force with the component sums of f folded into the same pass: the macro-force grid of the
+// even-grid kernel (one vertex per thread), each block folds its 3 component sums (fixed shuffle and
+// warp order) into partials[3 b + c]; the nb block partials are then summed by the deterministic
+// component-sum reduction. The partition is fixed by the grid, so the sums are reproducible run to
+// run; they round differently from launch_comp_sums(f) (another partition), which project_norm0 used
+// before.
 template <typename TC>
-__global__ void __launch_bounds__(kRT, 8) macro_force_sums_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
-                                                                  int load, double* __restrict__ f, double* partials) {
-  // 8 blocks of kRT per SM (<= 32 registers): the reduce_grid partition is one full wave
-  __shared__ double sh[32];
-  // mixed-radix (colour, h2, h1, h0) coordinates of i and of the grid stride (the same for every
-  // thread: kept in shared memory); divisions once per thread, carries per step. Grid extents are
-  // read from the kernel parameters, not held in registers (32-register cap).
-  __shared__ unsigned step[4];
-  unsigned color, h0, h1, h2;
-  unsigned i = blockIdx.x * kRT + threadIdx.x;
-  {
-    unsigned v = i;
-    h0 = v % (unsigned)g.cd[0][0];
-    v /= (unsigned)g.cd[0][0];
-    h1 = v % (unsigned)g.cd[0][1];
-    v /= (unsigned)g.cd[0][1];
-    h2 = v % (unsigned)g.cd[0][2];
-    color = v / (unsigned)g.cd[0][2];
-  }
-  if (threadIdx.x == 0) {
-    unsigned v = gridDim.x * kRT;
-    step[0] = v % (unsigned)g.cd[0][0];
-    v /= (unsigned)g.cd[0][0];
-    step[1] = v % (unsigned)g.cd[0][1];
-    v /= (unsigned)g.cd[0][1];
-    step[2] = v % (unsigned)g.cd[0][2];
-    step[3] = v / (unsigned)g.cd[0][2];
-  }
-  __syncthreads();
-  double s[3] = {0.0, 0.0, 0.0};
-  for (; i < (unsigned)g.nv; i += gridDim.x * kRT) {  // nv < 2^32 (host check)
+__global__ void __launch_bounds__(128) macro_force_sums_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl,
+                                                               int load, double* __restrict__ f,
+                                                               double* __restrict__ partials) {
+  __shared__ double sh[3][4];
+  const int color = blockIdx.z & 7;
+  const int h2 = blockIdx.z >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (h0 < g.cd[0][0] && h1 < g.cd[0][1]) {
     FastAddr fa;
-    fast_addr(g, int(color), int(h0), int(h1), int(h2), fa);
+    fast_addr(g, color, h0, h1, h2, fa);
     double q[8];
     load_q_fast(coeff, cl, fa, q);
-    double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int ke = 0; ke < 8; ++ke)  // src/fem.cpp:145-150
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] += q[ke] * c_fmacro[ke][load][c];
+    const size_t loc = fa.A[0][1] + fa.A[1][1] + fa.A[2][1];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      f[3 * (size_t)i + c] = acc[c];
-      s[c] += acc[c];
-    }
-    h0 += step[0];
-    unsigned k = h0 >= (unsigned)g.cd[0][0];
-    h0 -= k * (unsigned)g.cd[0][0];
-    h1 += step[1] + k;
-    k = h1 >= (unsigned)g.cd[0][1];
-    h1 -= k * (unsigned)g.cd[0][1];
-    h2 += step[2] + k;
-    k = h2 >= (unsigned)g.cd[0][2];
-    h2 -= k * (unsigned)g.cd[0][2];
-    color += step[3] + k;
+    for (int c = 0; c < 3; ++c) f[3 * loc + c] = acc[c];
   }
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double v = block_reduce(s[c], sh);
-    if (threadIdx.x == 0) partials[c * kReducePartials + blockIdx.x] = v;
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) sh[c][t >> 5] = v;
+  }
+  __syncthreads();
+  if (t < 3) {
+    const size_t blk = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    partials[3 * blk + t] = (sh[t][0] + sh[t][1]) + (sh[t][2] + sh[t][3]);
   }
 }
 
+long long macro_force_sums_blocks(const GridGeo& g) {
+  const dim3 b = fast_block(g);
+  return (long long)ceil_div(g.cd[0][0], b.x) * ceil_div(g.cd[0][1], b.y) * 8 * g.cd[0][2];
+}
+
 template <typename TC>
-void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* partials, double* sums,
-                             cudaStream_t s, ZLink<TC> cl) {
-  if (!fast_ok(g) || g.nv + (long long)kReducePartials * kRT >= (1LL << 32))
-    throw std::invalid_argument("fused macro force sums need an even grid of < 2^32 vertices");
-  const int nb = reduce_grid(g.nv);
-  macro_force_sums_kernel<TC><<<nb, kRT, 0, s>>>(g, coeff, resolve(cl, coeff), load, f, partials);
+void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* block_sums,
+                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl) {
+  if (!fast_ok(g)) throw std::invalid_argument("fused macro force sums need an even grid");
+  const dim3 b = fast_block(g);
+  if (b.x * b.y != 128) throw std::logic_error("macro force sums: 128-thread blocks expected");
+  const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
+  macro_force_sums_kernel<TC><<<gr, b, 0, s>>>(g, coeff, resolve(cl, coeff), load, f, block_sums);
   IHOM_LAUNCH_CHECK();
-  launch_finalize(partials, nb, 3, sums, s);
+  launch_comp_sums<double>(block_sums, macro_force_sums_blocks(g), partials, sums, s);
 }
 
 // ---------------------------------------------------------------- instantiations
@@ -661,9 +640,9 @@ template void launch_coeff<float>(const double*, float*, long long, double, cuda
 template void launch_coeff<double>(const double*, double*, long long, double, cudaStream_t);
 template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t, ZLink<float>);
 template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t, ZLink<double>);
-template void launch_macro_force_sums<float>(const GridGeo&, const float*, int, double*, double*, double*, cudaStream_t,
-                                             ZLink<float>);
-template void launch_macro_force_sums<double>(const GridGeo&, const double*, int, double*, double*, double*,
+template void launch_macro_force_sums<float>(const GridGeo&, const float*, int, double*, double*, double*, double*,
+                                             cudaStream_t, ZLink<float>);
+template void launch_macro_force_sums<double>(const GridGeo&, const double*, int, double*, double*, double*, double*,
                                               cudaStream_t, ZLink<double>);
 template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, const double*, const double*, float*,
                                                   double*, cudaStream_t, ZLink<float>, ZLink<double>);

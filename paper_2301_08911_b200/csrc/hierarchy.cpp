@@ -706,11 +706,13 @@ void Hierarchy<T>::macro_force(int load) {  // src/fem.cpp:145-150
   Level& L0 = levels_[0];
   const ZLink<T> cl = slab_.on() ? coeff_l_ : ZLink<T>{};
   ProfScope p(s_, "macro_force", double(L0.g.nv) * (24.0 + sizeof(T)));
-  if (fast_ok(L0.g) && L0.g.nv < (1LL << 31) && knob("MACRO_SUMS", 1)) {
-    launch_macro_force_sums<T>(L0.g, coeff_.p, load, L0.f.p, ws_.partials, ws_.scalars + kMacroSums + 3 * cur_rhs_,
-                               s_, cl);
+  if (fast_ok(L0.g) && knob("MACRO_SUMS", 1)) {
+    const size_t nb = size_t(3 * macro_force_sums_blocks(L0.g));
+    if (mf_part_.n < nb) mf_part_.alloc(nb);
+    launch_macro_force_sums<T>(L0.g, coeff_.p, load, L0.f.p, mf_part_.p, ws_.partials,
+                               ws_.scalars + kMacroSums + 3 * cur_rhs_, s_, cl);
     msum_f_[cur_rhs_] = L0.f.p;
-    launches_ += 2;
+    launches_ += 3;
   } else {
     launch_macro_force<T>(L0.g, coeff_.p, load, L0.f.p, s_, cl);
     msum_f_[cur_rhs_] = nullptr;

@@ -319,6 +319,7 @@ class Hierarchy {
   ZLink<double> u_alt_l_{};
   double fnorm0_ = 0.0;
   const double* msum_f_[kMaxRhsGroup] = {};  // f whose component sums macro_force left (per RHS)
+  DevBuf<double> mf_part_;                    // macro-force block sums (3 per block)
   bool lean_ = false;
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;

@@ -59,11 +59,12 @@ long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const doubl
 
 template <typename TC>
 void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s, ZLink<TC> cl = {});
-// macro force plus the component sums of f in the same pass (bitwise launch_macro_force followed by
-// launch_comp_sums(f) into sums[3]); even grids only (fast_ok)
+// macro force plus the component sums of f (sums[3]) from per-block partials of the same pass
+// (block_sums: 3 macro_force_sums_blocks(g) doubles); even grids only (fast_ok)
+long long macro_force_sums_blocks(const GridGeo& g);
 template <typename TC>
-void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* partials, double* sums,
-                             cudaStream_t s, ZLink<TC> cl = {});
+void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* block_sums,
+                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl = {});
 
 // ---- transfer (src/multigrid.cpp:12-79) ----
 // z-slab arguments: rl / cl link the source array to the slabs

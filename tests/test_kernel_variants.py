@@ -56,6 +56,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("TRANSFER_F32", 1)
         ih.set_knob("PROJECT_NORM", 1)
         ih.set_knob("MACRO_SUMS", 1)
+        ih.set_knob("U_HOST", 0)
         ih.set_knob("STENCIL_STREAM", 1)
 
 
@@ -239,8 +240,9 @@ def test_memory_levers_bit_identical(ih, P):
     """With the free HBM capped (HBM_LIMIT_MB) the solver drops the lockstep grouping (group size 1) and
     the energy cache; both are pure optimisations, so cycle counts, C^H and displacements are bitwise
     those of the default run (here: groups of six and the cache)."""
-    base = _solve(ih, 32, {}, fabric_p=P)
-    low = _solve(ih, 32, {"HBM_LIMIT_MB": 256}, fabric_p=P)
+    # U_HOST=-1: the host-staged layout (which the cap would also select) is tested in test_host_staged.py
+    base = _solve(ih, 32, {"U_HOST": -1}, fabric_p=P)
+    low = _solve(ih, 32, {"HBM_LIMIT_MB": 256, "U_HOST": -1}, fabric_p=P)
     assert low[0] == base[0]
     np.testing.assert_array_equal(low[1], base[1])
     for a, b in zip(low[2], base[2]):
@@ -272,8 +274,8 @@ def test_transfer_f32_matches(ih, n, P):
 @pytest.mark.parametrize("P", [0, 2])
 def test_project_norm_bit_identical(ih, P):
     """Load projection and its norm in one pass (PROJECT_NORM) == remove_translations + norm, bitwise."""
-    base = _solve(ih, 32, {"PROJECT_NORM": 0}, fabric_p=P)
-    v = _solve(ih, 32, {"PROJECT_NORM": 1}, fabric_p=P)
+    base = _solve(ih, 32, {"PROJECT_NORM": 0, "MACRO_SUMS": 0}, fabric_p=P)  # both legs sum f separately
+    v = _solve(ih, 32, {"PROJECT_NORM": 1, "MACRO_SUMS": 0}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):
@@ -281,14 +283,19 @@ def test_project_norm_bit_identical(ih, P):
 
 
 @pytest.mark.parametrize("n,P", [(32, 0), (48, 0), (32, 2)])
-def test_macro_sums_bit_identical(ih, n, P):
-    """Macro force with the load's component sums folded into the same pass (MACRO_SUMS) ==
-    macro force + the separate component-sum reduction, bitwise (same partition and fold)."""
+def test_macro_sums_match(ih, n, P):
+    """Macro force with the load's component sums folded into the same pass (MACRO_SUMS: per-block
+    partials of the macro-force grid, then the deterministic component-sum reduction) == macro force +
+    the separate component-sum pass up to the order of the sums: same cycles, fields to rounding."""
     base = _solve(ih, n, {"MACRO_SUMS": 0}, fabric_p=P)
     v = _solve(ih, n, {"MACRO_SUMS": 1}, fabric_p=P)
+    v2 = _solve(ih, n, {"MACRO_SUMS": 1}, fabric_p=P)
     assert v[0] == base[0]
-    np.testing.assert_array_equal(v[1], base[1])
-    for a, b in zip(v[2], base[2]):
+    assert np.abs(v[1] - base[1]).max() <= 1e-12 * np.abs(base[1]).max()
+    for a, b in zip(v[2], base[2]):  # f32 inner corrections turn last-bit load changes into ~1e-10
+        assert np.linalg.norm(a - b) <= 1e-8 * max(np.linalg.norm(b), 1e-30)
+    np.testing.assert_array_equal(v[1], v2[1])  # reproducible run to run
+    for a, b in zip(v[2], v2[2]):
         np.testing.assert_array_equal(a, b)
 
 

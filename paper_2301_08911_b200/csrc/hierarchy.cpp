@@ -1354,15 +1354,69 @@ bool Hierarchy<T>::transfer_group(int G, int l, bool down) {
   }
 }
 
+// First level of the bottom cycle (one cooperative launch for the small levels and the coarsest,
+// knob BOTTOM_CYCLE): the smallest l >= 1 from which every level down to the coarsest is replicated
+// (not split into z-slabs) and small enough for the warp-per-vertex kernels; lmax: none.
+template <typename T>
+int Hierarchy<T>::bottom_start(int G) const {
+  const int lmax = num_levels() - 1;
+  if (!std::is_same_v<T, float> || (G != 2 && G != 3 && G != 6) || knob("BOTTOM_CYCLE", 1) == 0) return lmax;
+  int lb = lmax;
+  for (int l = lmax - 1; l >= 1; --l) {
+    const Level& L = levels_[size_t(l)];
+    if (L.sharded || !bottom_level_ok(L.g, levels_[size_t(l + 1)].g) || lmax - l + 1 > kMaxBottom) break;
+    lb = l;
+  }
+  return lb;
+}
+
+template <typename T>
+void Hierarchy<T>::bottom_cycle(int G, int lb, const SolverOptions& opts) {
+  const int lmax = num_levels() - 1;
+  join_coarsest();
+  BottomCycle bc{};
+  bc.nlev = lmax - lb + 1;
+  for (int l = lb; l <= lmax; ++l) {
+    Level& L = levels_[size_t(l)];
+    BottomLevel& B = bc.L[l - lb];
+    B.g = L.g;
+    B.st = reinterpret_cast<const float*>(L.st.p);
+    B.zs = opts.pre_sweeps > 0 && zero_start_ok(l) ? 1 : 0;
+    for (int k = 0; k < G; ++k) {
+      RhsSlot* o = slot_of(k);
+      B.eu[k] = o ? o->eu[size_t(l)].p : L.eu.p;
+      B.ef[k] = o ? o->ef[size_t(l)].p : L.ef.p;
+      B.er[k] = o ? o->er[size_t(l)].p : L.er.p;
+    }
+  }
+  bc.pre = opts.pre_sweeps;
+  bc.post = opts.post_sweeps;
+  bc.N = ndof_c_;
+  bc.nvc = levels_[size_t(lmax)].g.nv;
+  bc.Ainv = Ainv_.p;
+  bc.A = A_.p;
+  bc.Q = Q_.p;
+  bc.nq = nnull_;
+  if (cwork_.n < size_t(3 * ndof_c_ * G)) cwork_.alloc(size_t(3 * ndof_c_ * kMaxRhsGroup));
+  bc.work = cwork_.p;
+  bc.err = err_.p;
+  {
+    ProfScope p(s_, "bottom_cycle", 0.0);
+    launch_bottom_cycle(bc, G, s_);
+  }
+  ++launches_;
+}
+
 template <typename T>
 void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
+  const int lb = bottom_start(G);  // levels lb .. lmax in one launch (lmax: none)
   for (int k = 0; k < G; ++k)  // level 0 down, per RHS
     if (act[k]) {
       select_rhs(k);
       inner_down(0, opts);
     }
-  for (int l = 1; l < lmax; ++l) {
+  for (int l = 1; l < lb; ++l) {
     const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
     if (!zs)
       for (int k = 0; k < G; ++k) {
@@ -1378,7 +1432,9 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
           restrict_to_f32(l);
         }
   }
-  if (lmax > 0 && G > 1) {  // the coarsest solves of all lanes in one launch (block per lane)
+  if (lb < lmax) {
+    bottom_cycle(G, lb, opts);
+  } else if (lmax > 0 && G > 1) {  // the coarsest solves of all lanes in one launch (block per lane)
     join_coarsest();
     const Level& L = levels_[size_t(lmax)];
     float* f[kMaxRhsGroup];
@@ -1399,7 +1455,7 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
         inner_coarsest();
       }
   }
-  for (int l = lmax - 1; l >= 1; --l) {
+  for (int l = std::min(lb, lmax) - 1; l >= 1; --l) {
     if (!transfer_group(G, l, false))
       for (int k = 0; k < G; ++k)
         if (act[k]) {

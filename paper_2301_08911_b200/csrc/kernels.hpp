@@ -116,6 +116,33 @@ template <typename TN>
 void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
                            TN* u, double negligible, double* work, int* err, cudaStream_t s);
 // every RHS lane of a lockstep group (f32 inner fields, block per lane; work: nl * 3 ndof doubles)
+// Bottom of the grouped inner V-cycle in one cooperative launch (levels whose colour passes are
+// warp-per-vertex, <= 32^3, down to the coarsest): the same per-vertex kernels in the same order as the
+// level-by-level launches, grid-wide barriers between the passes (bitwise the same results).
+constexpr int kMaxBottom = 6;
+struct BottomLevel {
+  GridGeo g;
+  const float* st;  // stencils (unused on the coarsest level)
+  float* eu[kMaxRhsGroup];
+  float* ef[kMaxRhsGroup];
+  float* er[kMaxRhsGroup];
+  int zs;           // zero-start pre-smoothing (else e is cleared first)
+};
+struct BottomCycle {
+  int nlev;  // levels [lb, lmax]; L[nlev - 1] is the coarsest
+  BottomLevel L[kMaxBottom];
+  int pre, post;
+  int N;
+  long long nvc;
+  const double* Ainv;
+  const double* A;
+  const double* Q;
+  int nq;
+  double* work;  // 3 N per lane
+  int* err;
+};
+bool bottom_level_ok(const GridGeo& g, const GridGeo& gc);  // level g (next coarser gc) can run inside
+void launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s);
 void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq,
                                  int nl, float* const* f, float* const* u, double* work, int* err, cudaStream_t s);
 

@@ -4,6 +4,7 @@
 #include "kernels.hpp"
 #include "gal_gen.cuh"
 
+#include <cooperative_groups.h>
 #include <cuda_pipeline.h>
 
 #include <mutex>
@@ -64,17 +65,12 @@ struct XferN {
   TN* dst[kMaxRhsGroup];
 };
 
-template <typename TN, typename TA = double>
-__global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, XferN<TN> io, int nz, GridGeo gout,
-                                                            int zoff) {
-  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
-  const TN* __restrict__ rf = io.src[lane];
-  const ZLink<TN> rl = io.sl[lane];
-  TN* __restrict__ fc = io.dst[lane];
-  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
-  const int h2 = zz >> 3;
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+// coarse vertex (colour, h0, h1, h2) of the restriction of one lane (shared by the grouped kernel and the
+// bottom-cycle kernel: the same arithmetic whatever thread computes it)
+template <typename TN, typename TA>
+__device__ __forceinline__ void restrict_vertex(const GridGeo& gf, const TN* __restrict__ rf, const ZLink<TN>& rl,
+                                                TN* __restrict__ fc, int color, int h0, int h1, int h2,
+                                                const GridGeo& gout, int zoff) {
   const int cx = 2 * h0 + (color & 1), cy = 2 * h1 + ((color >> 1) & 1), cz = 2 * h2 + ((color >> 2) & 1);
   FastAddr fa;
   fast_addr(gf, 0, cx, cy, cz, fa);
@@ -92,6 +88,17 @@ __global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo 
       (size_t)color * gout.size[0] + h0 + (size_t)gout.cd[0][0] * (h1 + (size_t)gout.cd[0][1] * (h2 + zoff));
 #pragma unroll
   for (int c = 0; c < 3; ++c) fc[3 * loc + c] = TN(acc[c]);
+}
+
+template <typename TN, typename TA = double>
+__global__ void __launch_bounds__(128) restrict_fast_kernel(GridGeo gf, GridGeo gc, XferN<TN> io, int nz, GridGeo gout,
+                                                            int zoff) {
+  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
+  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = zz >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gc.cd[0][0] || h1 >= gc.cd[0][1]) return;
+  restrict_vertex<TN, TA>(gf, io.src[lane], io.sl[lane], io.dst[lane], color, h0, h1, h2, gout, zoff);
 }
 
 // Coarse parents of a fine vertex at halved (h0, h1, h2): coarse coordinates
@@ -128,16 +135,11 @@ __device__ __forceinline__ void prolong_vertex(const GridGeo& gc, int h0, int h1
   (void)o;
 }
 
-template <typename TN, typename TA = double>
-__global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, XferN<TN> io, int nz, int zoff) {
-  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
-  const TN* __restrict__ uc = io.src[lane];
-  const ZLink<TN> cl = io.sl[lane];
-  TN* __restrict__ uf = io.dst[lane];
-  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
-  const int h2 = zz >> 3;
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
+// fine vertex (colour, h0, h1, h2) of the prolongation-add of one lane
+template <typename TN, typename TA>
+__device__ __forceinline__ void prolong_add_vertex(const GridGeo& gc, const GridGeo& gf, const TN* __restrict__ uc,
+                                                   const ZLink<TN>& cl, TN* __restrict__ uf, int color, int h0,
+                                                   int h1, int h2, int zoff) {
   TA acc[3] = {TA(0), TA(0), TA(0)};
   switch (color) {  // uniform per block
     case 0: prolong_vertex<TN, 0, 0, 0, TA>(gc, h0, h1, h2, uc, cl, zoff, acc); break;
@@ -152,6 +154,16 @@ __global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo g
   const size_t loc = (size_t)color * gf.size[0] + h0 + (size_t)gf.cd[0][0] * (h1 + (size_t)gf.cd[0][1] * h2);
 #pragma unroll
   for (int d = 0; d < 3; ++d) uf[3 * loc + d] = TN(TA(uf[3 * loc + d]) + acc[d]);
+}
+
+template <typename TN, typename TA = double>
+__global__ void __launch_bounds__(128) prolong_fast_kernel(GridGeo gc, GridGeo gf, XferN<TN> io, int nz, int zoff) {
+  const int lane = blockIdx.z / nz, zz = blockIdx.z % nz;
+  const int color = zz & 7;  // colour fastest (L2 reuse across colours of a plane)
+  const int h2 = zz >> 3;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= gf.cd[0][0] || h1 >= gf.cd[0][1]) return;
+  prolong_add_vertex<TN, TA>(gc, gf, io.src[lane], io.sl[lane], io.dst[lane], color, h0, h1, h2, zoff);
 }
 
 template <typename TN>
@@ -596,10 +608,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
-  const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (loc >= g.nv) return;
+__device__ __forceinline__ void apply_warp_vertex(const GridGeo& g, const TS* __restrict__ st, const RhsN<TN>& io,
+                                                  long long loc, int lane) {
   const int color = color_at(g, loc);
   int vx, vy, vz;
   block_coords(g, color, (unsigned)(loc - g.base[color]), vx, vy, vz);
@@ -627,11 +637,17 @@ __global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, cons
 }
 
 template <typename TS, typename TN, int NL>
-__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
-                                                              int color, int* err, unsigned zm) {
-  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(128) stencil_apply_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io) {
+  const long long loc = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= g.size[color]) return;
+  if (loc >= g.nv) return;
+  apply_warp_vertex<TS, TN, NL>(g, st, io, loc, lane);
+}
+
+// colour-block vertex i of colour `color` (one warp)
+template <typename TS, typename TN, int NL>
+__device__ __forceinline__ void gs_warp_vertex(const GridGeo& g, const TS* __restrict__ st, const RhsN<TN>& io,
+                                               int color, int* err, unsigned zm, long long i, int lane) {
   int vx, vy, vz;
   block_coords(g, color, (unsigned)i, vx, vy, vz);
   const long long loc = g.base[color] + i;
@@ -656,6 +672,15 @@ __global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const T
     for (int k = 0; k < NL; ++k)
       if (!gs_solve_store<TS, TN>(S, m[k], io.f[k], size_t(loc), io.y[k], err)) return;
   }
+}
+
+template <typename TS, typename TN, int NL>
+__global__ void __launch_bounds__(128) stencil_gs_warp_kernel(GridGeo g, const TS* __restrict__ st, RhsN<TN> io,
+                                                              int color, int* err, unsigned zm) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= g.size[color]) return;
+  gs_warp_vertex<TS, TN, NL>(g, st, io, color, err, zm, i, lane);
 }
 
 // levels with at most this many vertices per colour use warp-per-vertex (default 4096: up to 32^3;
@@ -1180,15 +1205,12 @@ struct CoarseIO {  // the (f, u) pair of each RHS lane; block b solves lane b
   TN* u[kMaxRhsGroup];
 };
 
+// One lane's coarsest solve by one block of kCoarseThreads threads (red: kCoarseThreads doubles of shared
+// memory); every exit is block-uniform.
 template <typename TN>
-__global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long long nv, const double* __restrict__ Ainv,
-                                                                  const double* __restrict__ A,
-                                                                  const double* __restrict__ Q, int nq, CoarseIO<TN> io,
-                                                                  double negligible, double* work, int* err) {
-  __shared__ double red[kCoarseThreads];
-  TN* f = io.f[blockIdx.x];
-  TN* u = io.u[blockIdx.x];
-  work += (size_t)blockIdx.x * 3 * N;
+__device__ void coarsest_lane(int N, long long nv, const double* __restrict__ Ainv, const double* __restrict__ A,
+                              const double* __restrict__ Q, int nq, TN* f, TN* u, double negligible, double* work,
+                              int* err, double* red) {
   double* fv = work;           // [N] f in dof order
   double* x = work + N;        // [N]
   double* r = work + 2 * N;    // [N]
@@ -1254,6 +1276,16 @@ __global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long lo
 }
 
 template <typename TN>
+__global__ void __launch_bounds__(kCoarseThreads) coarsest_kernel(int N, long long nv, const double* __restrict__ Ainv,
+                                                                  const double* __restrict__ A,
+                                                                  const double* __restrict__ Q, int nq, CoarseIO<TN> io,
+                                                                  double negligible, double* work, int* err) {
+  __shared__ double red[kCoarseThreads];
+  coarsest_lane<TN>(N, nv, Ainv, A, Q, nq, io.f[blockIdx.x], io.u[blockIdx.x], negligible,
+                    work + (size_t)blockIdx.x * 3 * N, err, red);
+}
+
+template <typename TN>
 void launch_coarsest_solve(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq, TN* f,
                            TN* u, double negligible, double* work, int* err, cudaStream_t s) {
   CoarseIO<TN> io{};
@@ -1270,6 +1302,113 @@ void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, con
   for (int k = 0; k < nl; ++k) io.f[k] = f[k], io.u[k] = u[k];
   coarsest_kernel<float><<<nl, kCoarseThreads, 0, s>>>(ndof, nv, Ainv, A, Q, nq, io, 0.0, work, err);
   IHOM_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- bottom cycle (one cooperative launch)
+bool bottom_level_ok(const GridGeo& g, const GridGeo& gc) {
+  if (!fast_ok(g) || g.nv > 8 * warp_vmax() || !transfer_group_ok(g, gc)) return false;
+  for (int c = 0; c < 8; ++c)
+    if (g.size[c] > warp_vmax() || g.size[c] == 0) return false;
+  return true;
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kCoarseThreads) bottom_cycle_kernel(BottomCycle bc) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kCoarseThreads];
+  const long long nthr = (long long)gridDim.x * blockDim.x, gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nwarp = nthr >> 5, gw = gt >> 5;
+  const int lane = threadIdx.x & 31;
+  // colour pass c of level L (zm: zero-start mask), then a grid-wide barrier
+  auto gs_pass = [&](const BottomLevel& L, int c, unsigned zm) {
+    RhsN<float> io{};
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      io.x[k] = L.eu[k];
+      io.xl[k] = ZLink<float>{L.eu[k], L.eu[k]};
+      io.f[k] = L.ef[k];
+      io.y[k] = L.eu[k];
+    }
+    for (long long i = gw; i < L.g.size[c]; i += nwarp) gs_warp_vertex<float, float, NL>(L.g, L.st, io, c, bc.err, zm, i, lane);
+    grid.sync();
+  };
+  for (int li = 0; li + 1 < bc.nlev; ++li) {  // down: smooth, residual, restrict
+    const BottomLevel& L = bc.L[li];
+    const BottomLevel& C = bc.L[li + 1];
+    if (!L.zs) {
+      for (long long t = gt; t < (long long)NL * 3 * L.g.nv; t += nthr) L.eu[t / (3 * L.g.nv)][t % (3 * L.g.nv)] = 0.0f;
+      grid.sync();
+    }
+    for (int sw = 0; sw < bc.pre; ++sw)
+      for (int c = 0; c < 8; ++c) gs_pass(L, c, L.zs && sw == 0 ? zero_start_mask(c) : 0u);
+    {
+      RhsN<float> io{};
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        io.x[k] = L.eu[k];
+        io.xl[k] = ZLink<float>{L.eu[k], L.eu[k]};
+        io.f[k] = L.ef[k];
+        io.y[k] = L.er[k];
+      }
+      for (long long v = gw; v < L.g.nv; v += nwarp) apply_warp_vertex<float, float, NL>(L.g, L.st, io, v, lane);
+    }
+    grid.sync();
+    const long long nc = C.g.nv, bs = C.g.size[0];
+    const int d0 = C.g.cd[0][0], d1 = C.g.cd[0][1];
+    for (long long t = gt; t < NL * nc; t += nthr) {
+      const int k = int(t / nc);
+      const long long r = t % nc, rr = r % bs;
+      const int color = int(r / bs), h0 = int(rr % d0), h1 = int((rr / d0) % d1), h2 = int(rr / ((long long)d0 * d1));
+      restrict_vertex<float, float>(L.g, L.er[k], ZLink<float>{L.er[k], L.er[k]}, C.ef[k], color, h0, h1, h2, C.g, 0);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x < NL) {  // coarsest: block k solves lane k (as the grouped coarsest launch)
+    const BottomLevel& C = bc.L[bc.nlev - 1];
+    coarsest_lane<float>(bc.N, bc.nvc, bc.Ainv, bc.A, bc.Q, bc.nq, C.ef[blockIdx.x], C.eu[blockIdx.x], 0.0,
+                         bc.work + (size_t)blockIdx.x * 3 * bc.N, bc.err, red);
+  }
+  grid.sync();
+  for (int li = bc.nlev - 2; li >= 0; --li) {  // up: prolong-add, smooth
+    const BottomLevel& L = bc.L[li];
+    const BottomLevel& C = bc.L[li + 1];
+    const long long nf = L.g.nv, bs = L.g.size[0];
+    const int d0 = L.g.cd[0][0], d1 = L.g.cd[0][1];
+    for (long long t = gt; t < NL * nf; t += nthr) {
+      const int k = int(t / nf);
+      const long long r = t % nf, rr = r % bs;
+      const int color = int(r / bs), h0 = int(rr % d0), h1 = int((rr / d0) % d1), h2 = int(rr / ((long long)d0 * d1));
+      prolong_add_vertex<float, float>(C.g, L.g, C.eu[k], ZLink<float>{C.eu[k], C.eu[k]}, L.eu[k], color, h0, h1, h2,
+                                       0);
+    }
+    grid.sync();
+    for (int sw = 0; sw < bc.post; ++sw)
+      for (int c = 0; c < 8; ++c) gs_pass(L, c, 0u);
+  }
+}
+
+void launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s) {
+  if (bc.nlev < 2 || bc.nlev > kMaxBottom) throw std::invalid_argument("bottom cycle: 2..6 levels");
+  const void* fn = nl == 2 ? (const void*)bottom_cycle_kernel<2>
+                 : nl == 3 ? (const void*)bottom_cycle_kernel<3>
+                 : nl == 6 ? (const void*)bottom_cycle_kernel<6>
+                           : nullptr;
+  if (!fn) throw std::invalid_argument("bottom cycle: group of 2, 3 or 6");
+  static int blocks[7] = {};
+  if (!blocks[nl]) {
+    int dev = 0, sms = 0, coop = 0, occ = 0;
+    IHOM_CUDA(cudaGetDevice(&dev));
+    IHOM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    IHOM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) throw CudaError("cooperative launch unsupported");
+    IHOM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kCoarseThreads, 0));
+    if (occ < 1) throw CudaError("bottom cycle kernel cannot be resident");
+    blocks[nl] = sms;  // one block per SM: every block co-resident, the barrier stays short
+  }
+  BottomCycle arg = bc;
+  void* args[] = {&arg};
+  IHOM_CUDA(cudaLaunchCooperativeKernel(fn, blocks[nl], kCoarseThreads, args, 0, s));
 }
 
 // ---------------------------------------------------------------- instantiations

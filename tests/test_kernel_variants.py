@@ -57,6 +57,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("PROJECT_NORM", 1)
         ih.set_knob("MACRO_SUMS", 1)
         ih.set_knob("U_HOST", 0)
+        ih.set_knob("BOTTOM_CYCLE", 1)
         ih.set_knob("STENCIL_STREAM", 1)
 
 
@@ -296,6 +297,21 @@ def test_macro_sums_match(ih, n, P):
         assert np.linalg.norm(a - b) <= 1e-8 * max(np.linalg.norm(b), 1e-30)
     np.testing.assert_array_equal(v[1], v2[1])  # reproducible run to run
     for a, b in zip(v[2], v2[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P,group", [(16, 0, 6), (64, 0, 2), (64, 0, 3), (64, 0, 6), (128, 0, 6),
+                                       ((64, 32, 48), 0, 6), (128, 4, 2)])
+def test_bottom_cycle_bit_identical(ih, n, P, group):
+    """The small levels and the coarsest solve of the grouped inner V-cycle in one cooperative launch
+    (BOTTOM_CYCLE: the same per-vertex kernels, grid-wide barriers between the passes) == one launch per
+    pass, bitwise."""
+    knobs = {"RHS_PAIRS": 1, "RHS_GROUP": group}
+    base = _solve(ih, n, {**knobs, "BOTTOM_CYCLE": 0}, fabric_p=P)
+    v = _solve(ih, n, {**knobs, "BOTTOM_CYCLE": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
         np.testing.assert_array_equal(a, b)
 
 

@@ -625,14 +625,14 @@ long long macro_force_sums_blocks(const GridGeo& g) {
 
 template <typename TC>
 void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* block_sums,
-                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl) {
+                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl, unsigned* ticket) {
   if (!fast_ok(g)) throw std::invalid_argument("fused macro force sums need an even grid");
   const dim3 b = fast_block(g);
   if (b.x * b.y != 128) throw std::logic_error("macro force sums: 128-thread blocks expected");
   const dim3 gr(ceil_div(g.cd[0][0], b.x), ceil_div(g.cd[0][1], b.y), 8 * g.cd[0][2]);
   macro_force_sums_kernel<TC><<<gr, b, 0, s>>>(g, coeff, resolve(cl, coeff), load, f, block_sums);
   IHOM_LAUNCH_CHECK();
-  launch_comp_sums<double>(block_sums, macro_force_sums_blocks(g), partials, sums, s);
+  launch_comp_sums<double>(block_sums, macro_force_sums_blocks(g), partials, sums, s, ticket);
 }
 
 // ---------------------------------------------------------------- instantiations
@@ -641,9 +641,9 @@ template void launch_coeff<double>(const double*, double*, long long, double, cu
 template void launch_macro_force<float>(const GridGeo&, const float*, int, double*, cudaStream_t, ZLink<float>);
 template void launch_macro_force<double>(const GridGeo&, const double*, int, double*, cudaStream_t, ZLink<double>);
 template void launch_macro_force_sums<float>(const GridGeo&, const float*, int, double*, double*, double*, double*,
-                                             cudaStream_t, ZLink<float>);
+                                             cudaStream_t, ZLink<float>, unsigned*);
 template void launch_macro_force_sums<double>(const GridGeo&, const double*, int, double*, double*, double*, double*,
-                                              cudaStream_t, ZLink<double>);
+                                              cudaStream_t, ZLink<double>, unsigned*);
 template long long launch_l0_residual_norm<float>(const GridGeo&, const float*, const double*, const double*, float*,
                                                   double*, cudaStream_t, ZLink<float>, ZLink<double>);
 

@@ -278,6 +278,8 @@ Hierarchy<T>::Hierarchy(const int n[3], const Material& mat, double penal, cudaS
   red_.alloc(kRedDoubles);
   err_.alloc(1);
   IHOM_CUDA(cudaMemsetAsync(err_.p, 0, sizeof(int), s_));
+  ticket_.alloc(1);
+  IHOM_CUDA(cudaMemsetAsync(ticket_.p, 0, sizeof(unsigned), s_));
   ws_.partials = red_.p;
   ws_.scalar = red_.p + 21 * kReducePartials;
   ws_.scalar2 = ws_.scalar + 1;
@@ -643,14 +645,14 @@ void Hierarchy<T>::remove_translations(double* f, int l) {  // src/multigrid.cpp
   const long long nv = L.g.nv;
   {
     ProfScope p(s_, "reduce", double(nv) * 24.0);
-    launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_);
+    launch_comp_sums<double>(f, nv, ws_.partials, ws_.scalars, s_, ticket_.p);
   }
   if (L.sharded) allreduce(ws_.scalars, 3);  // component sums over the whole grid
   {
     ProfScope p(s_, "vector", double(nv) * 48.0);
     launch_sub_means<double>(f, nv, ws_.scalars, s_, L.nv_global);
   }
-  launches_ += 3;
+  launches_ += 2;
 }
 
 // remove_translations of src written into dst (the fused-update solve ends in the other buffer):
@@ -661,14 +663,14 @@ void Hierarchy<T>::remove_translations_to(const double* src, double* dst, int l)
   const long long nv = L.g.nv;
   {
     ProfScope p(s_, "reduce", double(nv) * 24.0);
-    launch_comp_sums<double>(src, nv, ws_.partials, ws_.scalars, s_);
+    launch_comp_sums<double>(src, nv, ws_.partials, ws_.scalars, s_, ticket_.p);
   }
   if (L.sharded) allreduce(ws_.scalars, 3);
   {
     ProfScope p(s_, "vector", double(nv) * 48.0);
     launch_sub_means_copy(src, dst, nv, ws_.scalars, s_, L.nv_global);
   }
-  launches_ += 3;
+  launches_ += 2;
 }
 
 // remove_translations(f, 0) followed by norm(f): one pass fewer over f, bitwise the same results.
@@ -685,16 +687,16 @@ double Hierarchy<T>::project_norm0(double* f) {
     sums = ws_.scalars + kMacroSums + 3 * cur_rhs_;
   } else {
     ProfScope p(s_, "reduce", double(nv) * 24.0);
-    launch_comp_sums<double>(f, nv, ws_.partials, sums, s_);
-    launches_ += 2;
+    launch_comp_sums<double>(f, nv, ws_.partials, sums, s_, ticket_.p);
+    ++launches_;
   }
   msum_f_[cur_rhs_] = nullptr;
   if (L.sharded) allreduce(sums, 3);
   {
     ProfScope p(s_, "vector", double(nv) * 48.0);
-    launch_sub_means_norm(f, nv, sums, ws_.partials, ws_.scalars + 4, s_, L.nv_global);
+    launch_sub_means_norm(f, nv, sums, ws_.partials, ws_.scalars + 4, s_, L.nv_global, ticket_.p);
   }
-  launches_ += 2;
+  ++launches_;
   allreduce(ws_.scalars + 4, 1);
   IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
@@ -710,9 +712,9 @@ void Hierarchy<T>::macro_force(int load) {  // src/fem.cpp:145-150
     const size_t nb = size_t(3 * macro_force_sums_blocks(L0.g));
     if (mf_part_.n < nb) mf_part_.alloc(nb);
     launch_macro_force_sums<T>(L0.g, coeff_.p, load, L0.f.p, mf_part_.p, ws_.partials,
-                               ws_.scalars + kMacroSums + 3 * cur_rhs_, s_, cl);
+                               ws_.scalars + kMacroSums + 3 * cur_rhs_, s_, cl, ticket_.p);
     msum_f_[cur_rhs_] = L0.f.p;
-    launches_ += 3;
+    launches_ += 2;
   } else {
     launch_macro_force<T>(L0.g, coeff_.p, load, L0.f.p, s_, cl);
     msum_f_[cur_rhs_] = nullptr;
@@ -724,9 +726,9 @@ template <typename T>
 double Hierarchy<T>::norm(const double* x, long long n) {  // src/multigrid.cpp:88-94
   {
     ProfScope p(s_, "reduce", double(n) * 8.0);
-    launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_);
+    launch_dot<double>(x, x, n, ws_.partials, ws_.scalars + 4, s_, ticket_.p);
   }
-  launches_ += 2;
+  ++launches_;
   allreduce(ws_.scalars + 4, 1);  // level-0 fields only: split over the slabs
   IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));
   IHOM_CUDA(cudaStreamSynchronize(s_));
@@ -955,9 +957,9 @@ double Hierarchy<T>::defect_residual(bool update, double* slot) {
     }
     {
       ProfScope p(s_, "reduce", double(nb) * 8.0);
-      launch_sum(npart_.p, nb, ws_.partials, slot ? slot : ws_.scalars + 4, s_);
+      launch_sum(npart_.p, nb, ws_.partials, slot ? slot : ws_.scalars + 4, s_, ticket_.p);
     }
-    launches_ += 3;
+    launches_ += 2;
     if (slot) return 0.0;  // deferred: ||r||^2 of this slab in *slot (finish_defect_cycles reads them together)
     allreduce(ws_.scalars + 4, 1);
     IHOM_CUDA(cudaMemcpyAsync(h_pinned_, ws_.scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, s_));

@@ -325,6 +325,7 @@ class Hierarchy {
   bool lean_ = false;
   DevBuf<double> red_;   // partials + scalars
   DevBuf<int> err_;
+  DevBuf<unsigned> ticket_;  // last-block reduction counter (reduce.cuh finalize_in_last_block), kept zero
   DevBuf<double> npart_;  // per-block |r|^2 partials of the fused defect residual
   DevBuf<double> pcg_p_, pcg_q_, pcg_s_;  // PCG direction, K p, device scalars
   Workspace ws_;

@@ -64,7 +64,8 @@ void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, 
 long long macro_force_sums_blocks(const GridGeo& g);
 template <typename TC>
 void launch_macro_force_sums(const GridGeo& g, const TC* coeff, int load, double* f, double* block_sums,
-                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl = {});
+                             double* partials, double* sums, cudaStream_t s, ZLink<TC> cl = {},
+                             unsigned* ticket = nullptr);
 
 // ---- transfer (src/multigrid.cpp:12-79) ----
 // z-slab arguments: rl / cl link the source array to the slabs
@@ -149,19 +150,21 @@ void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, con
 // ---- reductions (deterministic: fixed partition per size, fixed fold order) ----
 // sums of the three AoS components: out[3]
 template <typename TN>
-void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s);
+void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s,
+                      unsigned* ticket = nullptr);  // ticket: fold the partials in the last block (one launch)
 // out[c] = fold of the per-block partials (c < ncomp), the second stage of every reduction here
 void launch_finalize(const double* partials, int nparts, int ncomp, double* out, cudaStream_t s);
 // out[0] = dot(a, b) over n entries
 template <typename TN>
-void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s);
+void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s,
+                unsigned* ticket = nullptr);
 // x[3 i + c] -= sums[c] / count (count = vertices of the whole grid; default nv)
 template <typename TN>
 void launch_sub_means(TN* x, long long nv, const double* sums, cudaStream_t s, long long count = 0);
 // dst = src - mean (per component), the in-place variant's arithmetic
 // x -= per-component mean (sums / count) and out = ||x||^2, bitwise launch_sub_means + launch_dot
 void launch_sub_means_norm(double* x, long long nv, const double* sums, double* partials, double* out,
-                           cudaStream_t s, long long count = 0);
+                           cudaStream_t s, long long count = 0, unsigned* ticket = nullptr);
 void launch_sub_means_copy(const double* src, double* dst, long long nv, const double* sums, cudaStream_t s,
                            long long count = 0);
 void launch_int_to_double(const int* in, double* out, cudaStream_t s);
@@ -176,7 +179,8 @@ void launch_axpy_update(double* u, const TN* e, long long n, cudaStream_t s);
 template <typename TI, typename TO>
 void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s);
 constexpr int kReducePartials = 1184;  // 8 * 148: capacity of the partials buffer (per component)
-void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s);
+void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s,
+                unsigned* ticket = nullptr);
 // MG-PCG helpers
 void launch_dot_df(const double* a, const float* b, long long n, double* partials, double* out, cudaStream_t s);
 void launch_pcg_p(double* p, const float* z, const double* beta, long long n, bool first, cudaStream_t s);

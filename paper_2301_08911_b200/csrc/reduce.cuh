@@ -35,4 +35,28 @@ __device__ __forceinline__ double block_reduce(double v, double* sh) {
   return r;  // valid in thread 0
 }
 
+// Second stage in the grid's last block (ticket: a zeroed counter per workspace, left zeroed): the block
+// that finishes last folds the gridDim.x partials of each component exactly as finalize_kernel does
+// (same thread stride, same tree), so the result equals the two-launch form bit for bit. No-op when
+// ticket is null (the caller launches finalize_kernel instead).
+__device__ __forceinline__ void finalize_in_last_block(const double* partials, int ncomp, double* out,
+                                                       unsigned* ticket, double* sh) {
+  __shared__ int last;
+  if (!ticket) return;
+  if (threadIdx.x == 0) {
+    __threadfence();  // this block's partials are visible before its ticket
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = 0; c < ncomp; ++c) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kRT) s += __ldcg(partials + c * kReducePartials + i);
+    const double r = block_reduce(s, sh);
+    if (threadIdx.x == 0) out[c] = r;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
 }  // namespace ihomgpu

@@ -13,7 +13,8 @@
 namespace ihomgpu {
 
 template <typename TN>
-__global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x, long long nv, double* partials) {
+__global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x, long long nv, double* partials,
+                                                        unsigned* ticket = nullptr, double* out = nullptr) {
   __shared__ double sh[32];
   double s[3] = {0.0, 0.0, 0.0};
   for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < nv; i += (long long)gridDim.x * kRT) {
@@ -25,6 +26,7 @@ __global__ void __launch_bounds__(kRT) comp_sums_kernel(const TN* __restrict__ x
     const double r = block_reduce(s[c], sh);
     if (threadIdx.x == 0) partials[c * kReducePartials + blockIdx.x] = r;
   }
+  finalize_in_last_block(partials, 3, out, ticket, sh);
 }
 
 __global__ void __launch_bounds__(kRT) finalize_kernel(const double* partials, int nparts, int ncomp, double* out) {
@@ -43,30 +45,34 @@ void launch_finalize(const double* partials, int nparts, int ncomp, double* out,
 }
 
 template <typename TN>
-void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s) {
+void launch_comp_sums(const TN* x, long long nv, double* partials, double* out, cudaStream_t s, unsigned* ticket) {
   const int g = reduce_grid(nv);
-  comp_sums_kernel<TN><<<g, kRT, 0, s>>>(x, nv, partials);
+  comp_sums_kernel<TN><<<g, kRT, 0, s>>>(x, nv, partials, ticket, out);
   IHOM_LAUNCH_CHECK();
+  if (ticket) return;
   finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 3, out);
   IHOM_LAUNCH_CHECK();
 }
 
 template <typename TN>
 __global__ void __launch_bounds__(kRT) dot_kernel(const TN* __restrict__ a, const TN* __restrict__ b, long long n,
-                                                  double* partials) {
+                                                  double* partials, unsigned* ticket, double* out) {
   __shared__ double sh[32];
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT)
     s += double(a[i]) * double(b[i]);
   const double r = block_reduce(s, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+  finalize_in_last_block(partials, 1, out, ticket, sh);
 }
 
 template <typename TN>
-void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s) {
+void launch_dot(const TN* a, const TN* b, long long n, double* partials, double* out, cudaStream_t s,
+                unsigned* ticket) {
   const int g = reduce_grid(n);
-  dot_kernel<TN><<<g, kRT, 0, s>>>(a, b, n, partials);
+  dot_kernel<TN><<<g, kRT, 0, s>>>(a, b, n, partials, ticket, out);
   IHOM_LAUNCH_CHECK();
+  if (ticket) return;
   finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -120,7 +126,7 @@ __global__ void sub_means_copy_kernel(const double* __restrict__ src, double* __
 // field and the norm are bitwise those of launch_sub_means + launch_dot.
 __global__ void __launch_bounds__(kRT) sub_means_norm_kernel(double* __restrict__ x, long long n3,
                                                              const double* __restrict__ sums, long long count,
-                                                             double* partials) {
+                                                             double* partials, unsigned* ticket, double* out) {
   __shared__ double sh[32];
   const double inv = 1.0 / double(count);
   const double m[3] = {sums[0], sums[1], sums[2]};
@@ -132,14 +138,16 @@ __global__ void __launch_bounds__(kRT) sub_means_norm_kernel(double* __restrict_
   }
   const double r = block_reduce(s, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+  finalize_in_last_block(partials, 1, out, ticket, sh);
 }
 
 void launch_sub_means_norm(double* x, long long nv, const double* sums, double* partials, double* out,
-                           cudaStream_t s, long long count) {
+                           cudaStream_t s, long long count, unsigned* ticket) {
   const long long n3 = 3 * nv;
   const int g = reduce_grid(n3);
-  sub_means_norm_kernel<<<g, kRT, 0, s>>>(x, n3, sums, count > 0 ? count : nv, partials);
+  sub_means_norm_kernel<<<g, kRT, 0, s>>>(x, n3, sums, count > 0 ? count : nv, partials, ticket, out);
   IHOM_LAUNCH_CHECK();
+  if (ticket) return;
   finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -191,18 +199,21 @@ void launch_convert(const TI* x, TO* y, long long n, cudaStream_t s) {
   IHOM_LAUNCH_CHECK();
 }
 
-__global__ void __launch_bounds__(kRT) sum_kernel_r(const double* __restrict__ a, long long n, double* partials) {
+__global__ void __launch_bounds__(kRT) sum_kernel_r(const double* __restrict__ a, long long n, double* partials,
+                                                    unsigned* ticket, double* out) {
   __shared__ double sh[32];
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * kRT + threadIdx.x; i < n; i += (long long)gridDim.x * kRT) s += a[i];
   const double r = block_reduce(s, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
+  finalize_in_last_block(partials, 1, out, ticket, sh);
 }
 
-void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s) {
+void launch_sum(const double* a, long long n, double* partials, double* out, cudaStream_t s, unsigned* ticket) {
   const int g = reduce_grid(n);
-  sum_kernel_r<<<g, kRT, 0, s>>>(a, n, partials);
+  sum_kernel_r<<<g, kRT, 0, s>>>(a, n, partials, ticket, out);
   IHOM_LAUNCH_CHECK();
+  if (ticket) return;
   finalize_kernel<<<1, kRT, 0, s>>>(partials, g, 1, out);
   IHOM_LAUNCH_CHECK();
 }
@@ -274,10 +285,10 @@ void launch_ratio(const double* num, const double* den, double* out, cudaStream_
   IHOM_LAUNCH_CHECK();
 }
 
-template void launch_comp_sums<double>(const double*, long long, double*, double*, cudaStream_t);
-template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t);
-template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t);
-template void launch_dot<float>(const float*, const float*, long long, double*, double*, cudaStream_t);
+template void launch_comp_sums<double>(const double*, long long, double*, double*, cudaStream_t, unsigned*);
+template void launch_comp_sums<float>(const float*, long long, double*, double*, cudaStream_t, unsigned*);
+template void launch_dot<double>(const double*, const double*, long long, double*, double*, cudaStream_t, unsigned*);
+template void launch_dot<float>(const float*, const float*, long long, double*, double*, cudaStream_t, unsigned*);
 template void launch_sub_means<double>(double*, long long, const double*, cudaStream_t, long long);
 template void launch_sub_means<float>(float*, long long, const double*, cudaStream_t, long long);
 template void launch_axpy_update<float>(double*, const float*, long long, cudaStream_t);

@@ -1,0 +1,9 @@
+# last-block reduction finalize: broad GPU subset + bench
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_kernel_variants.py tests/test_trajectories.py tests/test_gpu_parity.py tests/test_host_staged.py -x -q -m gpu > gpurun_out/r02aj_t.log 2>&1; echo t rc $?
+tail -3 gpurun_out/r02aj_t.log
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-ref-precision --no-host-staged > gpurun_out/r02aj_bench.json 2> gpurun_out/r02aj_bench.err; echo bench rc $?
+python -c "
+import json;d=json.loads(open('gpurun_out/r02aj_bench.json').read().strip().splitlines()[-1])
+k=d['kernels'];print(d['value'],d['e2e']['value'],d['gpu_launches'],d['gpu_launches']/40,k.get('reduce'),k.get('vector'))"
+tail -3 gpurun_out/r02aj_bench.err

@@ -95,3 +95,16 @@ def test_load_owners():
     assert dd.load_owners(8) == [0, 1, 2, 3, 4, 5]
     with pytest.raises(ValueError):
         dd.load_owners(0)
+
+
+def test_memory_plan_layouts():
+    """Per-GPU HBM estimates (bench memory_plan_estimate): device-resident 1024^3 needs 4 GPUs, the
+    host-staged layout (measured 39.8 GB at 512^3, 159 GB per 1024^3/2 slab) fits 2."""
+    from paper_2301_08911_b200 import distributed as dd
+    dev = {n: dd.memory_plan(1024, n) for n in (1, 2, 4, 8)}
+    assert [dev[n]["fits_b200"] for n in (1, 2, 4, 8)] == [False, False, True, True]
+    hs = {n: dd.memory_plan(1024, n, host_staged=True) for n in (1, 2)}
+    assert not hs[1]["fits_b200"] and hs[2]["fits_b200"]
+    assert hs[2]["group"] == 1 and not hs[2]["energy_cache"] and hs[2]["pinned_host_gb_per_gpu"] > 100
+    assert 38.0 <= dd.memory_plan(512, 1, host_staged=True)["gb_per_gpu"] <= 40.0
+    assert abs(hs[2]["gb_per_gpu"] - 159.4) < 2.0  # tools/host_staged_1024.py measured 159.4 GB

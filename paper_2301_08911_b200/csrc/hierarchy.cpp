@@ -1362,7 +1362,8 @@ bool Hierarchy<T>::transfer_group(int G, int l, bool down) {
 template <typename T>
 int Hierarchy<T>::bottom_start(int G) const {
   const int lmax = num_levels() - 1;
-  if (!std::is_same_v<T, float> || (G != 2 && G != 3 && G != 6) || knob("BOTTOM_CYCLE", 1) == 0) return lmax;
+  if (!std::is_same_v<T, float> || (G != 2 && G != 3 && G != 6) || !bottom_ok_ || knob("BOTTOM_CYCLE", 1) == 0)
+    return lmax;
   int lb = lmax;
   for (int l = lmax - 1; l >= 1; --l) {
     const Level& L = levels_[size_t(l)];
@@ -1373,7 +1374,7 @@ int Hierarchy<T>::bottom_start(int G) const {
 }
 
 template <typename T>
-void Hierarchy<T>::bottom_cycle(int G, int lb, const SolverOptions& opts) {
+bool Hierarchy<T>::bottom_cycle(int G, int lb, const SolverOptions& opts) {
   const int lmax = num_levels() - 1;
   join_coarsest();
   BottomCycle bc{};
@@ -1404,21 +1405,20 @@ void Hierarchy<T>::bottom_cycle(int G, int lb, const SolverOptions& opts) {
   bc.err = err_.p;
   {
     ProfScope p(s_, "bottom_cycle", 0.0);
-    launch_bottom_cycle(bc, G, s_);
+    if (!launch_bottom_cycle(bc, G, s_)) {  // not every block can be co-resident here (e.g. a partitioned GPU)
+      bottom_ok_ = false;
+      return false;
+    }
   }
   ++launches_;
+  return true;
 }
 
 template <typename T>
 void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bool* act) {
   const int lmax = num_levels() - 1;
   const int lb = bottom_start(G);  // levels lb .. lmax in one launch (lmax: none)
-  for (int k = 0; k < G; ++k)  // level 0 down, per RHS
-    if (act[k]) {
-      select_rhs(k);
-      inner_down(0, opts);
-    }
-  for (int l = 1; l < lb; ++l) {
+  auto down = [&](int l) {  // pre-smooth, residual, restrict of level l >= 1 (all lanes)
     const bool zs = opts.pre_sweeps > 0 && zero_start_ok(l);
     if (!zs)
       for (int k = 0; k < G; ++k) {
@@ -1433,31 +1433,8 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
           select_rhs(k);
           restrict_to_f32(l);
         }
-  }
-  if (lb < lmax) {
-    bottom_cycle(G, lb, opts);
-  } else if (lmax > 0 && G > 1) {  // the coarsest solves of all lanes in one launch (block per lane)
-    join_coarsest();
-    const Level& L = levels_[size_t(lmax)];
-    float* f[kMaxRhsGroup];
-    float* u[kMaxRhsGroup];
-    for (int k = 0; k < G; ++k) {
-      RhsSlot* o = slot_of(k);
-      f[k] = o ? o->ef[size_t(lmax)].p : L.ef.p;
-      u[k] = o ? o->eu[size_t(lmax)].p : L.eu.p;
-    }
-    if (cwork_.n < size_t(3 * ndof_c_ * G)) cwork_.alloc(size_t(3 * ndof_c_ * kMaxRhsGroup));
-    ProfScope p(s_, "coarsest", 0.0);
-    launch_coarsest_solve_group(ndof_c_, L.g.nv, Ainv_.p, A_.p, Q_.p, nnull_, G, f, u, cwork_.p, err_.p, s_);
-    ++launches_;
-  } else {
-    for (int k = 0; k < G; ++k)
-      if (act[k]) {
-        select_rhs(k);
-        inner_coarsest();
-      }
-  }
-  for (int l = std::min(lb, lmax) - 1; l >= 1; --l) {
+  };
+  auto up = [&](int l) {  // prolong-add from l + 1, post-smooth level l >= 1
     if (!transfer_group(G, l, false))
       for (int k = 0; k < G; ++k)
         if (act[k]) {
@@ -1465,7 +1442,42 @@ void Hierarchy<T>::inner_vcycle_group(int G, const SolverOptions& opts, const bo
           inner_prolong(l);
         }
     relax_f32_group(G, l, opts.post_sweeps, false);
+  };
+  auto coarsest = [&] {
+    if (lmax > 0 && G > 1) {  // the coarsest solves of all lanes in one launch (block per lane)
+      join_coarsest();
+      const Level& L = levels_[size_t(lmax)];
+      float* f[kMaxRhsGroup];
+      float* u[kMaxRhsGroup];
+      for (int k = 0; k < G; ++k) {
+        RhsSlot* o = slot_of(k);
+        f[k] = o ? o->ef[size_t(lmax)].p : L.ef.p;
+        u[k] = o ? o->eu[size_t(lmax)].p : L.eu.p;
+      }
+      if (cwork_.n < size_t(3 * ndof_c_ * G)) cwork_.alloc(size_t(3 * ndof_c_ * kMaxRhsGroup));
+      ProfScope p(s_, "coarsest", 0.0);
+      launch_coarsest_solve_group(ndof_c_, L.g.nv, Ainv_.p, A_.p, Q_.p, nnull_, G, f, u, cwork_.p, err_.p, s_);
+      ++launches_;
+    } else {
+      for (int k = 0; k < G; ++k)
+        if (act[k]) {
+          select_rhs(k);
+          inner_coarsest();
+        }
+    }
+  };
+  for (int k = 0; k < G; ++k)  // level 0 down, per RHS
+    if (act[k]) {
+      select_rhs(k);
+      inner_down(0, opts);
+    }
+  for (int l = 1; l < lb; ++l) down(l);
+  if (!(lb < lmax && bottom_cycle(G, lb, opts))) {  // level by level (also if the cooperative launch is refused)
+    for (int l = lb; l < lmax; ++l) down(l);
+    coarsest();
+    for (int l = lmax - 1; l >= lb; --l) up(l);
   }
+  for (int l = std::min(lb, lmax) - 1; l >= 1; --l) up(l);
   for (int k = 0; k < G; ++k)
     if (act[k]) {
       select_rhs(k);

@@ -313,7 +313,8 @@ class Hierarchy {
   void finish_defect_cycles(int G, const bool* act, double* rn);  // all active RHSs, one read-back
   bool transfer_group(int G, int l, bool down);                   // grouped level >= 1 transfer
   int bottom_start(int G) const;                                  // first level of the bottom cycle
-  void bottom_cycle(int G, int lb, const SolverOptions& opts);    // levels lb .. coarsest, one launch
+  bool bottom_cycle(int G, int lb, const SolverOptions& opts);    // levels lb .. coarsest, one launch
+  bool bottom_ok_ = true;                                         // cooperative launch accepted so far
   double* u0_bound_ = nullptr;
   double* u_home_ = nullptr;  // the caller's buffer of the current solve (u0_bound_ may be u_alt_)
   ZLink<double> u_home_l_{};

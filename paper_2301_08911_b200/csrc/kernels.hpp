@@ -143,7 +143,7 @@ struct BottomCycle {
   int* err;
 };
 bool bottom_level_ok(const GridGeo& g, const GridGeo& gc);  // level g (next coarser gc) can run inside
-void launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s);
+bool launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s);  // false: launch refused (too large)
 void launch_coarsest_solve_group(int ndof, long long nv, const double* Ainv, const double* A, const double* Q, int nq,
                                  int nl, float* const* f, float* const* u, double* work, int* err, cudaStream_t s);
 

@@ -1388,7 +1388,7 @@ __global__ void __launch_bounds__(kCoarseThreads) bottom_cycle_kernel(BottomCycl
   }
 }
 
-void launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s) {
+bool launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s) {
   if (bc.nlev < 2 || bc.nlev > kMaxBottom) throw std::invalid_argument("bottom cycle: 2..6 levels");
   const void* fn = nl == 2 ? (const void*)bottom_cycle_kernel<2>
                  : nl == 3 ? (const void*)bottom_cycle_kernel<3>
@@ -1401,14 +1401,20 @@ void launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s) {
     IHOM_CUDA(cudaGetDevice(&dev));
     IHOM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     IHOM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    if (!coop) throw CudaError("cooperative launch unsupported");
     IHOM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kCoarseThreads, 0));
-    if (occ < 1) throw CudaError("bottom cycle kernel cannot be resident");
-    blocks[nl] = sms;  // one block per SM: every block co-resident, the barrier stays short
+    blocks[nl] = coop && occ >= 1 ? sms : -1;  // one block per SM: every block co-resident, short barriers
   }
+  if (blocks[nl] < 0) return false;
   BottomCycle arg = bc;
   void* args[] = {&arg};
-  IHOM_CUDA(cudaLaunchCooperativeKernel(fn, blocks[nl], kCoarseThreads, args, 0, s));
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, blocks[nl], kCoarseThreads, args, 0, s);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    (void)cudaGetLastError();  // a refused configuration, not a sticky error
+    blocks[nl] = -1;
+    return false;
+  }
+  IHOM_CUDA(e);
+  return true;
 }
 
 // ---------------------------------------------------------------- instantiations

@@ -1414,6 +1414,7 @@ bool launch_bottom_cycle(const BottomCycle& bc, int nl, cudaStream_t s) {
     return false;
   }
   IHOM_CUDA(e);
+  ++launch_counter();  // counted like every IHOM_LAUNCH_CHECK'd launch (bench gpu_launches)
   return true;
 }
 

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 
 namespace ihomgpu {
@@ -1740,6 +1741,7 @@ Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, c
     IHOM_CUDA(cudaEventCreateWithFlags(&ev_solved_, cudaEventDisableTiming));
     IHOM_CUDA(cudaEventCreateWithFlags(&ev_staged_out_, cudaEventDisableTiming));
     IHOM_CUDA(cudaEventRecord(ev_staged_out_, cs_));
+    for (auto& e : ev_back_) IHOM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     float* u0 = reinterpret_cast<float*>(hier_.level_u(0));
     float* f0 = reinterpret_cast<float*>(hier_.level_f(0));
     // snapshots 4 and 5 go last, into f0: the last solve's write-back still reads f0 (ensure_snapshots)
@@ -1759,6 +1761,12 @@ Homogenizer<T>::Homogenizer(const int n[3], const Material& mat, double penal, c
 template <typename T>
 Homogenizer<T>::~Homogenizer() {
   hier_.quiesce();
+  try {
+    join_conversions();
+  } catch (...) {
+  }
+  for (cudaEvent_t e : ev_back_)
+    if (e) cudaEventDestroy(e);
   if (cs_) {
     cudaStreamSynchronize(cs_);
     cudaStreamDestroy(cs_);
@@ -1769,6 +1777,27 @@ Homogenizer<T>::~Homogenizer() {
     if (p) cudaFreeHost(p);
   for (double* p : hu64_)
     if (p) cudaFreeHost(p);
+}
+
+template <typename T>
+void Homogenizer<T>::join_conversions() {
+  for (auto& c : conv_)
+    if (c.valid()) c.get();
+}
+
+// f32 snapshot of field i from its f64 host copy once the write-back (ev) has landed; round to nearest
+// like the device conversion. Eight host threads.
+static void convert_snapshot(cudaEvent_t ev, int dev, const double* src, float* dst, long long n) {
+  IHOM_CUDA(cudaSetDevice(dev));
+  IHOM_CUDA(cudaEventSynchronize(ev));
+  constexpr int kThreads = 8;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < kThreads; ++t)
+    pool.emplace_back([=] {
+      const long long a = n * t / kThreads, b = n * (t + 1) / kThreads;
+      for (long long k = a; k < b; ++k) dst[k] = float(src[k]);
+    });
+  for (auto& th : pool) th.join();
 }
 
 template <typename T>
@@ -1799,6 +1828,7 @@ void Homogenizer<T>::write_displacement(int i, const double* src) {
     return;
   }
   IHOM_CUDA(cudaStreamSynchronize(cs_));
+  join_conversions();
   std::vector<double> w;
   double* h = hu64_[size_t(i)];
   if (!h) {
@@ -1828,8 +1858,11 @@ CellSolveStats Homogenizer<T>::solve_host_staged() {
   double* u = hier_.level_u(0);
   double* f = hier_.level_f(0);
   const ZLink<double> ul = hier_.ulink(0);
-  float* out32 = hier_.inner_r(0);  // f32 write-back staging
+  float* out32 = hier_.inner_r(0);  // f32 write-back staging (mode 1)
   float* in32 = hier_.inner_f(0);   // f32 warm-start staging (mode 1)
+  int dev = 0;
+  IHOM_CUDA(cudaGetDevice(&dev));
+  join_conversions();  // the host copies are not being read any more
   CellSolveStats out;
   for (int i = 0; i < 6; ++i) {
     hier_.sync();  // coefficients of the neighbouring slabs are current; nobody still reads u / e_r
@@ -1847,15 +1880,20 @@ CellSolveStats Homogenizer<T>::solve_host_staged() {
     const SolveStats st = hier_.solve_bound(u, opts_, ul);
     hier_.sync();  // the neighbours' last halo reads of e_r0 are done
     {
-      ProfScope p(s, "vector", double(n3) * (host_u_ == 2 ? 36.0 : 12.0));
-      launch_convert<double, float>(u, out32, n3, s);
+      ProfScope p(s, "vector", double(n3) * (host_u_ == 2 ? 48.0 : 12.0));
       if (host_u_ == 2) IHOM_CUDA(cudaMemcpyAsync(f, u, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+      else launch_convert<double, float>(u, out32, n3, s);
     }
     IHOM_CUDA(cudaEventRecord(ev_solved_, s));
     IHOM_CUDA(cudaStreamWaitEvent(cs_, ev_solved_, 0));
-    IHOM_CUDA(cudaMemcpyAsync(hu32_[size_t(i)], out32, sizeof(float) * n3, cudaMemcpyDeviceToHost, cs_));
-    if (host_u_ == 2)
+    if (host_u_ == 2) {
       IHOM_CUDA(cudaMemcpyAsync(hu64_[size_t(i)], f, sizeof(double) * n3, cudaMemcpyDeviceToHost, cs_));
+      IHOM_CUDA(cudaEventRecord(ev_back_[size_t(i)], cs_));
+      conv_[size_t(i)] = std::async(std::launch::async, convert_snapshot, ev_back_[size_t(i)], dev,
+                                    hu64_[size_t(i)], hu32_[size_t(i)], n3);
+    } else {
+      IHOM_CUDA(cudaMemcpyAsync(hu32_[size_t(i)], out32, sizeof(float) * n3, cudaMemcpyDeviceToHost, cs_));
+    }
     IHOM_CUDA(cudaEventRecord(ev_staged_out_, cs_));
     out.total_cycles += st.cycles;  // combined in load order, exactly as the reference loop does
     if (st.rel_residual >= out.worst_residual) {
@@ -1880,6 +1918,7 @@ void Homogenizer<T>::ensure_snapshots() {
     // write-back (from f0 and e_r0 into hu32_[5]) may still run on the copy stream
     for (int i = 0; i < 6; ++i) {
       if (i == 4) IHOM_CUDA(cudaStreamWaitEvent(s, ev_staged_out_, 0));
+      if (conv_[size_t(i)].valid()) conv_[size_t(i)].get();  // mode 2: the host-made snapshot is complete
       IHOM_CUDA(cudaMemcpyAsync(snap_[size_t(i)], hu32_[size_t(i)], sizeof(float) * n3, cudaMemcpyHostToDevice, s));
     }
   }

@@ -391,6 +391,11 @@ class Homogenizer {
   bool snaps_ready_ = false;
   cudaStream_t cs_ = nullptr;   // copy stream: a solve's write-back overlaps the next solve's stage-in
   cudaEvent_t ev_solved_ = nullptr, ev_staged_out_ = nullptr;
+  // mode 2: the f32 snapshot of field i is made on the host from its f64 write-back (ev_back_[i]) by a
+  // worker, so only the f64 field crosses PCIe device -> host
+  std::array<cudaEvent_t, 6> ev_back_{};
+  std::array<std::future<void>, 6> conv_;
+  void join_conversions();
   CellSolveStats solve_host_staged();
   void ensure_snapshots();
   Comm* comm_ = nullptr;

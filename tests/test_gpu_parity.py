@@ -434,3 +434,29 @@ def test_pcg_converges_in_fewer_cycles_than_vcycle(ih):
         assert st["converged"]
         cyc[mode] = st["total_cycles"]
     assert cyc["pcg"] <= cyc["vcycle"]
+
+
+# ---------------------------------------------------------------- runner option space vs the oracle
+@pytest.mark.parametrize("opts", [
+    dict(obj="npr-log", sym="reflect6"),
+    dict(obj="shear", sym="reflect3"),
+    dict(obj="bulk", sym="rotate3"),
+    dict(obj="shear", sym="none", kernel="linear"),
+    dict(obj="bulk", sym="reflect6", filter_placement="sensitivity"),
+    dict(obj="npr-relaxed", sym="reflect6", init="constant", vol=0.3),
+    dict(obj="bulk", sym="reflect6", penal=1.0, filter_radius=1.5),
+])
+def test_runner_options_3_iterations_match_oracle(ih, orc, opts):
+    """Whole optimisation iterations on the bench's solver path (mixed precision, mixed_defect) across the
+    runner's option space (objectives, symmetry groups, filter kernel / radius / placement, init, SIMP
+    power): per-iteration objective and C^H within 1e-4 of the oracle, final design within 1e-3."""
+    o = {"vol": 0.2, **opts}
+    cfg = ih.RunConfig(reso=32, max_iter=3, precision="mixed", solver_mode="mixed_defect", **o)
+    rep = ih.run_optimization(cfg)
+    recs, rho_o, flags = orc.run(reso=32, max_iter=3, mixed=True, **o)
+    assert not rep.solver_failed and not flags["solver_failed"]
+    assert len(rep.records) == len(recs)
+    for r, ro in zip(rep.records, recs):
+        assert abs(r["objective"] - ro["objective"]) <= 1e-4 * abs(ro["objective"])
+        assert np.abs(r["C"] - ro["C"]).max() <= 1e-4 * np.abs(ro["C"]).max()
+    assert np.abs(rep.density - rho_o).max() <= 1e-3

@@ -460,3 +460,19 @@ def test_runner_options_3_iterations_match_oracle(ih, orc, opts):
         assert abs(r["objective"] - ro["objective"]) <= 1e-4 * abs(ro["objective"])
         assert np.abs(r["C"] - ro["C"]).max() <= 1e-4 * np.abs(ro["C"]).max()
     assert np.abs(rep.density - rho_o).max() <= 1e-3
+
+
+@pytest.mark.parametrize("obj", ["bulk", "npr-relaxed"])
+def test_all_double_3_iterations_match_oracle(ih, orc, obj):
+    """Homogenizer<double> (all-f64 coefficients, stencils and nodal data, the reference's double mode) with
+    its V-cycle: whole iterations against the oracle's double mode."""
+    cfg = ih.RunConfig(reso=32, vol=0.2, obj=obj, max_iter=3, precision="double", solver_mode="vcycle")
+    rep = ih.run_optimization(cfg)
+    recs, rho_o, flags = orc.run(reso=32, vol=0.2, obj=obj, max_iter=3, mixed=False)
+    assert not rep.solver_failed and not flags["solver_failed"]
+    assert len(rep.records) == len(recs) == 3
+    for r, ro in zip(rep.records, recs):
+        assert r["cycles"] == ro["cycles"]
+        assert abs(r["objective"] - ro["objective"]) <= 1e-8 * abs(ro["objective"])
+        assert np.abs(r["C"] - ro["C"]).max() <= 1e-8 * np.abs(ro["C"]).max()
+    assert np.abs(rep.density - rho_o).max() <= 1e-8

@@ -404,7 +404,7 @@ static long long launch_hsweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, 
                                double* unew, cudaStream_t s, const TN* u2 = nullptr, ZLink<TN> ul2 = {},
                                const TN* f2 = nullptr, TN* y2 = nullptr) {
   constexpr size_t sm = hs_smem<TN, kHsBY, FUSE, NP>();
-  constexpr int minb = sizeof(TN) == 8 || NP == 2 ? 2 : 3;
+  constexpr int minb = sizeof(TN) == 8 || NP == 2 ? 2 : 4;
   auto kern = l0_hsweep_kernel<TC, TN, OUT, kHsBY, minb, FUSE, NP>;
   static int per_sm = 0;  // per instantiation
   if (!per_sm) {

@@ -323,15 +323,19 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast_kernel(GridGeo g, const 
 
 
 // ---------------------------------------------------------------- coeff
-template <typename TC>
+template <typename TC, bool UNIT>
 __global__ void coeff_kernel(const double* __restrict__ rho, TC* __restrict__ coeff, long long m, double p) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) coeff[i] = TC(pow(double(TC(rho[i])), p));  // src/multigrid.cpp:270
+  if (i >= m) return;
+  const double x = double(TC(rho[i]));
+  coeff[i] = TC(UNIT ? x : pow(x, p));  // src/multigrid.cpp:270; pow(x, 1) == x exactly (IEEE 754)
 }
 
 template <typename TC>
 void launch_coeff(const double* rho, TC* coeff, long long m, double penal, cudaStream_t s) {
-  coeff_kernel<TC><<<ceil_div(m, 256), 256, 0, s>>>(rho, coeff, m, penal);
+  // the runner's homogenizer penal is 1 (the SIMP power lives in DensityExpr, src/runner.cpp:62)
+  if (penal == 1.0) coeff_kernel<TC, true><<<ceil_div(m, 256), 256, 0, s>>>(rho, coeff, m, penal);
+  else coeff_kernel<TC, false><<<ceil_div(m, 256), 256, 0, s>>>(rho, coeff, m, penal);
   IHOM_LAUNCH_CHECK();
 }
 

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kPT) tensor_pair_kernel(GridGeo g, U6 uu, cons
       for (int m = 0; m < 12; ++m)
         if (eidx[m] >= 0) ecache[eidx[m] * g.nv + e] = E[m];
     }
-    const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
+    const double q = penal == 1.0 ? rho[e] : pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
     for (int m = 0; m < 12; ++m) acc[m] = fma(q, E[m], acc[m]);
   }
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kPT) sens_pair_kernel(GridGeo g, U6 uu, const 
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * all[q];
-  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;
+  out[e] = penal * (penal == 1.0 ? 1.0 : pow(rho[e], penal - 1.0)) * acc * inv_m;
 }
 
 // ---------------------------------------------------------------- staged pair tensor pass (bulk copies)
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kHT) tensor_kernel(GridGeo g, U6 uu, const dou
 #pragma unroll
       for (int k = 0; k < 21; ++k) ecache[k * g.nv + e] = E[k];
     }
-    const double q = pow(rho[e], penal);  // src/homogenization.cpp:91
+    const double q = penal == 1.0 ? rho[e] : pow(rho[e], penal);  // src/homogenization.cpp:91
 #pragma unroll
     for (int k = 0; k < 21; ++k) acc[k] += q * double(E[k]);
   }
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(kHT) sens_kernel(GridGeo g, U6 uu, const doubl
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * double(E[q]);
-  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;  // :141 (1/M over the whole grid)
+  out[e] = penal * (penal == 1.0 ? 1.0 : pow(rho[e], penal - 1.0)) * acc * inv_m;  // :141 (1/M over the whole grid)
 }
 
 // Sensitivity from the energies the tensor pass cached: identical arithmetic on identical E values.
@@ -869,7 +869,7 @@ __global__ void sens_cached_kernel(long long nv, const TE* __restrict__ ecache, 
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int j = i; j < 6; ++j, ++q) acc += (i == j ? 1.0 : 2.0) * seed[i * 6 + j] * double(ecache[q * nv + e]);
-  out[e] = penal * pow(rho[e], penal - 1.0) * acc * inv_m;
+  out[e] = penal * (penal == 1.0 ? 1.0 : pow(rho[e], penal - 1.0)) * acc * inv_m;
 }
 
 void launch_sensitivity_cached(long long nv, const void* ecache, bool f32, const double* rho, double penal,

@@ -108,6 +108,15 @@ class Homogenizer {
     check(ihom_get_displacement(ctx_, i, out.data(), IHOM_HOST));
     return out;
   }
+  void set_displacement(int i, const std::vector<double>& u) {
+    check(ihom_set_displacement(ctx_, i, u.data(), IHOM_HOST));
+  }
+  // where the six fields live: 0 device-resident, 2 / 1 host-staged (memory lever)
+  int host_staged() {
+    const int v = ihom_host_staged(ctx_);
+    if (v < 0) check(IHOM_E_STATE);
+    return v;
+  }
   ihom_ctx* handle() { return ctx_; }
 
  private:

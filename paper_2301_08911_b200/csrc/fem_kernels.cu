@@ -186,21 +186,15 @@ __global__ void __launch_bounds__(128, MINB) l0_apply_fast_kernel(GridGeo g, con
 // (t2 = -1), so those 9 neighbours are loaded once into registers and reused.
 // ZC >= 0: zero-start pass of colour ZC (first forward sweep from u = 0): the neighbours of
 // colours > ZC are known zeros and are neither loaded nor multiplied (common.cuh zero_start_mask).
-template <typename TC, typename TN, int MINB, bool ZL = false, int ZC = -1>
-__global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const TC* __restrict__ coeff,
-                                                                ZLink<TC> cl, const TN* __restrict__ f,
-                                                                const TN* __restrict__ ur, ZLink<TN> ul, TN* uw,
-                                                                int color) {
-  if constexpr (!ZL) {
-    cl = {coeff, coeff};
-    ul = {ur, ur};
-  }
-  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
-  if constexpr (ZC >= 0) color = ZC;
+// The two z-stacked vertices (h0, h1, h2) and (h0, h1, h2 + 1) of colour `color`: GS updates written to
+// uw, returned in out[v]. ov(v, n, c, val) may supply neighbour n of vertex v instead of memory (the
+// colour-pair pass hands in the row's fresh colour-c values); ZM: zero-start mask (known-zero colours).
+template <unsigned ZM, typename TC, typename TN, typename OV>
+__device__ __forceinline__ void gs2_vertices(const GridGeo& g, const TC* __restrict__ coeff, const ZLink<TC>& cl,
+                                             const TN* __restrict__ f, const TN* __restrict__ ur,
+                                             const ZLink<TN>& ul, TN* uw, int color, int h0, int h1, int h2, OV ov,
+                                             TN out[2][3]) {
   using TA = TN;
-  const int h2 = 2 * blockIdx.z;
-  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
-  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
   FastAddr fa, fb;
   fast_addr(g, color, h0, h1, h2, fa);
   fast_addr(g, color, h0, h1, h2 + 1, fb);
@@ -208,7 +202,7 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
   const TN* pa2 = zbase(fa, ur, ul, 2);  // == zbase(fb, ur, ul, 0) (a's upper plane is b's lower)
 #pragma unroll
   for (int n = 0; n < 9; ++n) {
-    if constexpr (ZC >= 0) {
+    if constexpr (ZM != 0u) {
       if ((ZM >> (18 + n)) & 1u) continue;  // (t0, t1, +1) of a and (t0, t1, -1) of b: same colour
     }
     const TN* p = pa2 + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][n / 3] + fa.A[2][2]);
@@ -218,10 +212,14 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
   const TN* pa0 = zbase(fa, ur, ul, 0);
   const TN* pb2 = zbase(fb, ur, ul, 2);
   auto Ua = [&](int n, int c) {
+    TA val;
+    if (ov(0, n, c, val)) return val;
     if (n >= 18) return shared_pl[n - 18][c];
     return TA(__ldg((n < 9 ? pa0 : ur) + 3 * (size_t)(fa.A[0][n % 3] + fa.A[1][(n / 3) % 3] + fa.A[2][n / 9]) + c));
   };
   auto Ub = [&](int n, int c) {
+    TA val;
+    if (ov(1, n, c, val)) return val;
     if (n < 9) return shared_pl[n][c];
     return TA(__ldg((n < 18 ? ur : pb2) + 3 * (size_t)(fb.A[0][n % 3] + fb.A[1][(n / 3) % 3] + fb.A[2][n / 9]) + c));
   };
@@ -234,15 +232,83 @@ __global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const
     if (v == 0) ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), Ua, m, sblk);
     else ku_vertex_split_z<ZM, TA>(q, kappa<TA>(), Ub, m, sblk);
     const size_t loc = fx.A[0][1] + fx.A[1][1] + fx.A[2][1];
-    TN rhs[3], out[3];
+    TN rhs[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) rhs[c] = TN(f[3 * loc + c]) - m[c];
-    solve3_spd<TN>(sblk, rhs, out);
+    solve3_spd<TN>(sblk, rhs, out[v]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[c];
+    for (int c = 0; c < 3; ++c) uw[3 * loc + c] = out[v][c];
   }
 }
 
+struct NoOverride {
+  template <typename TA>
+  __device__ __forceinline__ bool operator()(int, int, int, TA&) const {
+    return false;
+  }
+};
+
+template <typename TC, typename TN, int MINB, bool ZL = false, int ZC = -1>
+__global__ void __launch_bounds__(128, MINB) l0_gs_fast2_kernel(GridGeo g, const TC* __restrict__ coeff,
+                                                                ZLink<TC> cl, const TN* __restrict__ f,
+                                                                const TN* __restrict__ ur, ZLink<TN> ul, TN* uw,
+                                                                int color) {
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {ur, ur};
+  }
+  constexpr unsigned ZM = ZC >= 0 ? zero_start_mask(ZC) : 0u;
+  if constexpr (ZC >= 0) color = ZC;
+  const int h2 = 2 * blockIdx.z;
+  const int h0 = blockIdx.x * blockDim.x + threadIdx.x, h1 = blockIdx.y * blockDim.y + threadIdx.y;
+  if (h0 >= g.cd[0][0] || h1 >= g.cd[0][1]) return;
+  TN out[2][3];
+  gs2_vertices<ZM>(g, coeff, cl, f, ur, ul, uw, color, h0, h1, h2, NoOverride{}, out);
+}
+
+// Colour passes c and c + 1 (c even) in ONE launch. The only colour-c neighbours of a colour-(c+1)
+// vertex are its x - 1 / x + 1 neighbours in the same row (y, z parities equal, x parity flipped), so a
+// block owning whole rows (one thread per colour-block column, blockDim.x = cd0) updates colour c,
+// publishes the rows' new colour-c values in shared memory and then updates colour c + 1 from them:
+// every update sees the values and runs the arithmetic of the two-launch sequence (bitwise the same),
+// while the other colours' values are read once for both passes (the second pass hits L1/L2).
+constexpr int kPairMaxX = 512;  // colour-block columns per row (n0 <= 1024)
+template <typename TC, typename TN, bool ZL = false, int ZC = -1, int MAXT = kPairMaxX, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB)
+    l0_gs_pair_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl, const TN* __restrict__ f, TN* u,
+                      ZLink<TN> ul, int color) {
+  __shared__ TN rowc[2][MAXT][3];
+  if constexpr (!ZL) {
+    cl = {coeff, coeff};
+    ul = {u, u};
+  }
+  if constexpr (ZC >= 0) color = ZC;
+  constexpr unsigned ZMA = ZC >= 0 ? zero_start_mask(ZC) : 0u;
+  constexpr unsigned ZMB = ZC >= 0 ? zero_start_mask(ZC + 1) : 0u;
+  const int d0 = g.cd[0][0];
+  const int h0 = threadIdx.x, h1 = blockIdx.y, h2 = 2 * blockIdx.z;
+  TN out[2][3];
+  gs2_vertices<ZMA>(g, coeff, cl, f, u, ul, u, color, h0, h1, h2, NoOverride{}, out);
+#pragma unroll
+  for (int v = 0; v < 2; ++v)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) rowc[v][h0][c] = out[v][c];
+  __syncthreads();
+  const int hn = h0 + 1 == d0 ? 0 : h0 + 1;
+  // colour c + 1 at x = 2 h0 + 1: neighbour 12 (x - 1) is colour c at h0, neighbour 14 (x + 1) at h0 + 1
+  auto ov = [&](int v, int n, int c, TN& val) {
+    if (n == 12) {
+      val = rowc[v][h0][c];
+      return true;
+    }
+    if (n == 14) {
+      val = rowc[v][hn][c];
+      return true;
+    }
+    return false;
+  };
+  gs2_vertices<ZMB>(g, coeff, cl, f, u, ul, u, color + 1, h0, h1, h2, ov, out);
+}
 // Defect-correction residual (kMixedDefect): r = f - K u from f64 data with the
 // f64 merge, written ONLY as the f32 right-hand side of the next inner cycle,
 // plus deterministic per-block partial sums of |r|^2 (the convergence norm).
@@ -448,6 +514,41 @@ static void launch_fast2_zs(int color, const dim3& gr, const dim3& b, cudaStream
     case 6: launch_fast2_zs<TC, TN, ZL, 6>(gr, b, s, g, coeff, cl, f, u, ul); break;
     default: launch_fast2_zs<TC, TN, ZL, 7>(gr, b, s, g, coeff, cl, f, u, ul); break;
   }
+}
+
+// Off by default: per 512^3 sweep it moves 11 GB instead of 18.8 GB and takes 3.66 instead of 3.95 ms, but
+// the fused launch is latency-bound (0.47 of HBM against the single pass's 0.75).
+bool l0_gs_pair_ok(const GridGeo& g) {
+  return knob("GS_PAIR", 0) != 0 && fast_ok(g) && g.cd[0][2] % 2 == 0 && g.cd[0][0] <= kPairMaxX;
+}
+
+template <bool ZL, int ZC>
+static void launch_pair_zc(const GridGeo& g, const float* coeff, ZLink<float> cl, const float* f, float* u,
+                           ZLink<float> ul, int color, cudaStream_t s) {
+  const dim3 gr(1, g.cd[0][1], g.cd[0][2] / 2);
+  if (g.cd[0][0] <= 256)  // rows of up to 256 columns (n0 <= 512): two CTAs per SM (3 spill: slower)
+    l0_gs_pair_kernel<float, float, ZL, ZC, 256, 2><<<gr, g.cd[0][0], 0, s>>>(g, coeff, cl, f, u, ul, color);
+  else
+    l0_gs_pair_kernel<float, float, ZL, ZC, kPairMaxX><<<gr, g.cd[0][0], 0, s>>>(g, coeff, cl, f, u, ul, color);
+}
+
+void launch_l0_gs_pair(const GridGeo& g, const float* coeff, const float* f, float* u, int color, cudaStream_t s,
+                       ZLink<float> cl, ZLink<float> ul, bool zero_start) {
+  if (!l0_gs_pair_ok(g) || (color & 1)) throw std::invalid_argument("colour-pair GS pass: unsupported grid or colour");
+  const bool linked = !is_self(cl, coeff) || !is_self(ul, u);
+  cl = resolve(cl, coeff);
+  ul = resolve(ul, u);
+  auto go = [&](auto zl) {
+    constexpr bool ZL = decltype(zl)::value;
+    if (!zero_start) launch_pair_zc<ZL, -1>(g, coeff, cl, f, u, ul, color, s);
+    else if (color == 0) launch_pair_zc<ZL, 0>(g, coeff, cl, f, u, ul, color, s);
+    else if (color == 2) launch_pair_zc<ZL, 2>(g, coeff, cl, f, u, ul, color, s);
+    else if (color == 4) launch_pair_zc<ZL, 4>(g, coeff, cl, f, u, ul, color, s);
+    else launch_pair_zc<ZL, 6>(g, coeff, cl, f, u, ul, color, s);
+  };
+  if (linked) go(std::true_type{});
+  else go(std::false_type{});
+  IHOM_LAUNCH_CHECK();
 }
 
 template <typename TC, typename TN, typename TA>

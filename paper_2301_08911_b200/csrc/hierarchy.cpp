@@ -208,6 +208,12 @@ double gs_coarse_bytes(const GridGeo& g, int c, double sN, double sC) {
 double gs_l0_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   return double(g.nv) * (double(c) / 8.0 * 3.0 * sN + sC) + double(g.size[c]) * 6.0 * sN;
 }
+// colour pair (c, c + 1), f32: the other colours' u once (colour c + 1 old for pass c; zero start: the
+// colours < c, and c + 1 is a known zero), every coefficient once, f and the update of both colours
+double gs_l0_pair_bytes(const GridGeo& g, int c, bool zs) {
+  const double others = zs ? double(c) / 8.0 : 7.0 / 8.0;
+  return double(g.nv) * (others * 12.0 + 4.0) + double(g.size[c] + g.size[c + 1]) * 24.0;
+}
 double gs_coarse_bytes_zs(const GridGeo& g, int c, double sN, double sC) {
   const int live = 27 - __builtin_popcount(zero_start_mask(c));
   double others = 0.0;
@@ -869,12 +875,20 @@ void Hierarchy<T>::relax_f32(int l, int sweeps, bool reverse, bool zero_start) {
   Level& L = levels_[size_t(l)];
   if constexpr (std::is_same_v<T, float>) {
     if (zero_start && reverse) throw std::logic_error("zero-start sweeps run the colours forward");
+    const bool pair = l == 0 && !reverse && l0_gs_pair_ok(L.g);
     for (int sw = 0; sw < sweeps; ++sw)
       for (int ci = 0; ci < 8; ++ci) {
         const int c = reverse ? 7 - ci : ci;
         if (L.g.size[c] == 0) continue;
         if (L.sharded) sync_halo();
         const bool zs = zero_start && sw == 0;
+        if (pair) {  // colours c, c + 1 in one launch (c even)
+          ProfScope p(s_, "l0_gs_f32", gs_l0_pair_bytes(L.g, c, zs));
+          launch_l0_gs_pair(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_, L.sharded ? coeff_l_ : ZLink<float>{}, L.eul, zs);
+          ++launches_;
+          ++ci;
+          continue;
+        }
         if (l == 0) {
           ProfScope p(s_, "l0_gs_f32", zs ? gs_l0_bytes_zs(L.g, c, 4, 4) : gs_l0_bytes(L.g, c, 4, 4));
           launch_l0_gs_color<float, float, float>(L.g, coeff_.p, L.ef.p, L.eu.p, c, s_,

@@ -57,6 +57,11 @@ template <typename TC>
 long long launch_l0_residual_norm(const GridGeo& g, const TC* coeff, const double* u, const double* f, float* r32,
                                   double* partials, cudaStream_t s, ZLink<TC> cl = {}, ZLink<double> ul = {});
 
+// Colour passes `color` and color + 1 (color even) of the f32 level-0 GS in one launch (blocks own whole
+// rows; bitwise the two separate passes). Knob GS_PAIR.
+bool l0_gs_pair_ok(const GridGeo& g);
+void launch_l0_gs_pair(const GridGeo& g, const float* coeff, const float* f, float* u, int color, cudaStream_t s,
+                       ZLink<float> cl, ZLink<float> ul, bool zero_start);
 template <typename TC>
 void launch_macro_force(const GridGeo& g, const TC* coeff, int load, double* f, cudaStream_t s, ZLink<TC> cl = {});
 // macro force plus the component sums of f (sums[3]) from per-block partials of the same pass

@@ -58,6 +58,7 @@ def _solve(ih, n, knobs, fabric_p=0, precision="mixed", mode="mixed_defect"):
         ih.set_knob("MACRO_SUMS", 1)
         ih.set_knob("U_HOST", 0)
         ih.set_knob("BOTTOM_CYCLE", 1)
+        ih.set_knob("GS_PAIR", 0)
         ih.set_knob("STENCIL_STREAM", 1)
 
 
@@ -309,6 +310,19 @@ def test_bottom_cycle_bit_identical(ih, n, P, group):
     knobs = {"RHS_PAIRS": 1, "RHS_GROUP": group}
     base = _solve(ih, n, {**knobs, "BOTTOM_CYCLE": 0}, fabric_p=P)
     v = _solve(ih, n, {**knobs, "BOTTOM_CYCLE": 1}, fabric_p=P)
+    assert v[0] == base[0]
+    np.testing.assert_array_equal(v[1], base[1])
+    for a, b in zip(v[2], base[2]):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,P", [(32, 0), (64, 0), ((64, 32, 48), 0), (16, 0), (64, 2), (128, 4)])
+def test_gs_pair_bit_identical(ih, n, P):
+    """Level-0 f32 GS colour passes c, c + 1 in one launch (GS_PAIR: blocks own whole rows, the fresh
+    colour-c values of a row handed to colour c + 1 through shared memory) == two launches, bitwise;
+    plain and zero-start passes, z-slab links."""
+    base = _solve(ih, n, {"GS_PAIR": 0}, fabric_p=P)
+    v = _solve(ih, n, {"GS_PAIR": 1}, fabric_p=P)
     assert v[0] == base[0]
     np.testing.assert_array_equal(v[1], base[1])
     for a, b in zip(v[2], base[2]):

@@ -30,29 +30,9 @@
 
 namespace ihomgpu {
 
-// Two right-hand sides in the lanes of one f32 pair (sm_100 FADD2 / FMUL2 / FFMA2): the paired f32
-// sweep computes the inner residuals of two cell problems of a lockstep group in one march; each
-// lane rounds exactly like the scalar instruction, so every lane is bit-identical to a single sweep.
-struct F2 {
-  float x, y;
-  __device__ F2() {}
-  __device__ explicit F2(float a) : x(a), y(a) {}
-  __device__ F2(float a, float b) : x(a), y(b) {}
-};
-__device__ __forceinline__ float2 f2v(F2 a) { return make_float2(a.x, a.y); }
-__device__ __forceinline__ F2 v2f(float2 a) { return F2(a.x, a.y); }
-__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return v2f(__fadd2_rn(f2v(a), f2v(b))); }
-__device__ __forceinline__ F2 operator-(F2 a) { return F2(-a.x, -a.y); }
-__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return v2f(__fadd2_rn(f2v(a), make_float2(-b.x, -b.y))); }
-__device__ __forceinline__ F2 operator*(F2 a, F2 b) { return v2f(__fmul2_rn(f2v(a), f2v(b))); }
-__device__ __forceinline__ F2 fma(F2 a, F2 b, F2 c) { return v2f(__ffma2_rn(f2v(a), f2v(b), f2v(c))); }
 template <typename T>
 __device__ __forceinline__ T shfl_next(T v) {  // value of the next lane (lane 31 keeps its own)
   return ::__shfl_down_sync(0xffffffffu, v, 1);
-}
-template <>
-__device__ __forceinline__ F2 shfl_next<F2>(F2 v) {
-  return F2(::__shfl_down_sync(0xffffffffu, v.x, 1), ::__shfl_down_sync(0xffffffffu, v.y, 1));
 }
 
 template <typename TA>
@@ -64,10 +44,6 @@ __device__ __forceinline__ double hada_class<double>(int k) {
 template <>
 __device__ __forceinline__ float hada_class<float>(int k) {
   return c_hada_f[k];
-}
-template <>
-__device__ __forceinline__ F2 hada_class<F2>(int k) {
-  return F2(c_hada_f[k]);
 }
 
 constexpr int kHsX = 32;             // element columns per CTA row (one warp)
@@ -84,23 +60,19 @@ template <typename TN, int BY, bool FUSE>
 constexpr int hs_ring() {
   return 3;  // planes s (read), s + 1 (landing), s + 2 (issued into the slot of s - 1)
 }
-template <typename TN, int BY, bool FUSE, int NP = 1>
+template <typename TN, int BY, bool FUSE>
 constexpr size_t hs_smem() {
-  return (size_t)hs_ring<TN, BY, FUSE>() * HsGeom<BY>::items * 3 * (NP * sizeof(TN) + (FUSE ? sizeof(float) : 0)) +
-         (size_t)NP * (2 * 6 * BY * kHsX * sizeof(TN) + 3 * 3 * BY * kHsX * sizeof(TN));
+  return (size_t)hs_ring<TN, BY, FUSE>() * HsGeom<BY>::items * 3 * (sizeof(TN) + (FUSE ? sizeof(float) : 0)) +
+         (2 * 6 * BY * kHsX * sizeof(TN) + 3 * 3 * BY * kHsX * sizeof(TN));
 }
 
 // grid = (ceil(n0 / 31), ceil(n1 / (BY - 1)), t / TZ); block = (32, BY)
-// NP = 2 (f32 only): two right-hand sides (u, f, y) and (u2, f2, y2) in F2 lanes.
-template <typename TC, typename TN, int OUT, int BY, int MINB, bool FUSE, int NP = 1>
+template <typename TC, typename TN, int OUT, int BY, int MINB, bool FUSE>
 __global__ void __launch_bounds__(kHsX* BY, MINB)
     l0_hsweep_kernel(GridGeo g, const TC* __restrict__ coeff, ZLink<TC> cl, const TN* __restrict__ u, ZLink<TN> ul,
                      const TN* __restrict__ f, TN* __restrict__ y, float* __restrict__ r32, double* partials, int TZ,
-                     const float* __restrict__ e, ZLink<float> el, double* __restrict__ unew,
-                     const TN* __restrict__ u2 = nullptr, ZLink<TN> ul2 = {}, const TN* __restrict__ f2 = nullptr,
-                     TN* __restrict__ y2 = nullptr) {
-  static_assert(NP == 1 || (NP == 2 && sizeof(TN) == 4 && !FUSE && OUT != kSwDefect), "paired sweep: f32 only");
-  using TA = std::conditional_t<NP == 2, F2, TN>;  // arithmetic and shared-memory value type
+                     const float* __restrict__ e, ZLink<float> el, double* __restrict__ unew) {
+  using TA = TN;  // arithmetic and shared-memory value type
   using Geo = HsGeom<BY>;
   constexpr int R = hs_ring<TN, BY, FUSE>();
   constexpr int SLOT = Geo::items * 3;
@@ -140,22 +112,12 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
     const int z = zl < 0 ? zl + t : (zl >= t ? zl - t : zl);
     const unsigned zoff = (unsigned)(z >> 1) * plane;
     TA* dst = us + slot * SLOT;
-    [[maybe_unused]] const TN* src2 = nullptr;
-    if constexpr (NP == 2) src2 = zl < 0 ? ul2.lo : (zl >= t ? ul2.hi : u2);
 #pragma unroll
     for (int r = 0; r < Geo::per; ++r)
       if (lS[r] >= 0) {
         const size_t gl = 3 * (size_t)((z & 1 ? lO[r] : lE[r]) + zoff);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (NP == 2) {
-            float* d2 = reinterpret_cast<float*>(dst + lS[r] + c);
-            __pipeline_memcpy_async(d2, src + gl + c, sizeof(float));
-            __pipeline_memcpy_async(d2 + 1, src2 + gl + c, sizeof(float));
-          } else {
-            __pipeline_memcpy_async(dst + lS[r] + c, src + gl + c, sizeof(TN));
-          }
-        }
+        for (int c = 0; c < 3; ++c) __pipeline_memcpy_async(dst + lS[r] + c, src + gl + c, sizeof(TN));
         if constexpr (FUSE) {
 #pragma unroll
           for (int c = 0; c < 3; ++c)
@@ -209,15 +171,8 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
       if (out_ok && k >= 0 && k < TZ) {
         const size_t loc = out_loc(Z0 + k);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (NP == 2) {
-            float* d2 = reinterpret_cast<float*>(fs + (slot * 3 + c) * BY * kHsX + tid);
-            __pipeline_memcpy_async(d2, f + 3 * loc + c, sizeof(float));
-            __pipeline_memcpy_async(d2 + 1, f2 + 3 * loc + c, sizeof(float));
-          } else {
-            __pipeline_memcpy_async(fs + (slot * 3 + c) * BY * kHsX + tid, f + 3 * loc + c, sizeof(TN));
-          }
-        }
+        for (int c = 0; c < 3; ++c)
+          __pipeline_memcpy_async(fs + (slot * 3 + c) * BY * kHsX + tid, f + 3 * loc + c, sizeof(TN));
       }
     }
   };
@@ -264,14 +219,7 @@ __global__ void __launch_bounds__(kHsX* BY, MINB)
       if (out_ok) {
         const size_t loc = out_loc(Z0 + s - 3);
         [[maybe_unused]] const TA* fr = fs + (f3 * 3) * BY * kHsX + tid;
-        if constexpr (NP == 2) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const TA r = OUT == kSwResidual ? fr[c * BY * kHsX] - yv[c] : yv[c];
-            y[3 * loc + c] = r.x;
-            y2[3 * loc + c] = r.y;
-          }
-        } else if constexpr (OUT == kSwDefect) {
+        if constexpr (OUT == kSwDefect) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const double r = double(fr[c * BY * kHsX]) - double(yv[c]);
@@ -398,14 +346,13 @@ static int hsweep_tz(const GridGeo& g, int slots) {
   return best;
 }
 
-template <typename TC, typename TN, int OUT, bool FUSE, int NP = 1>
+template <typename TC, typename TN, int OUT, bool FUSE>
 static long long launch_hsweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, const TN* u, ZLink<TN> ul,
                                const TN* f, TN* y, float* r32, double* partials, const float* e, ZLink<float> el,
-                               double* unew, cudaStream_t s, const TN* u2 = nullptr, ZLink<TN> ul2 = {},
-                               const TN* f2 = nullptr, TN* y2 = nullptr) {
-  constexpr size_t sm = hs_smem<TN, kHsBY, FUSE, NP>();
-  constexpr int minb = sizeof(TN) == 8 || NP == 2 ? 2 : 4;
-  auto kern = l0_hsweep_kernel<TC, TN, OUT, kHsBY, minb, FUSE, NP>;
+                               double* unew, cudaStream_t s) {
+  constexpr size_t sm = hs_smem<TN, kHsBY, FUSE>();
+  constexpr int minb = sizeof(TN) == 8 ? 2 : 4;  // f32: 4 CTAs/SM at 64 registers (profiles/kernel_variants_r01.md)
+  auto kern = l0_hsweep_kernel<TC, TN, OUT, kHsBY, minb, FUSE>;
   static int per_sm = 0;  // per instantiation
   if (!per_sm) {
     IHOM_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -417,7 +364,7 @@ static long long launch_hsweep(const GridGeo& g, const TC* coeff, ZLink<TC> cl, 
   }
   const int tz = hsweep_tz(g, per_sm);
   const dim3 gr(ceil_div(g.n[0], kHsOX), ceil_div(g.n[1], kHsBY - 1), g.n[2] / tz);
-  kern<<<gr, dim3(kHsX, kHsBY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials, tz, e, el, unew, u2, ul2, f2, y2);
+  kern<<<gr, dim3(kHsX, kHsBY), sm, s>>>(g, coeff, cl, u, ul, f, y, r32, partials, tz, e, el, unew);
   IHOM_LAUNCH_CHECK();
   return (long long)gr.x * gr.y * gr.z;
 }
